@@ -1,0 +1,366 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched early-exit (EE) decode step on B200.
+
+Metric (BASELINE.json): EE decode tokens/s (whole job, all GPUs) with the
+exit-head / decode-GEMM fraction of HBM roofline.  One "step" = one batched
+decode step: every one of the B rows advances one token through the
+introspective early-exit path (exits 6/12/18/24, compaction of survivors).
+
+Workload (BASELINE configs[1], C2): OPT-1.3B shape (24 layers, d 2048, 32
+heads, ffn 8192, V 50272), exits at 6/12/18/24, random-init weights with
+biased exit heads, batch 64 per GPU, bf16, prompt 128 + up to 100 decode
+positions (KV context 128..227), teacher-forced synthetic tokens.  N GPUs run
+N independent replicas over disjoint request shards (weak scaling); the only
+collective is the profiler-histogram all-reduce after the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl eeb|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[3:7]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------
+# algorithmic bytes
+# ----------------------------------------------------------------------------
+def gemm_bytes_per_step(desc, batch: int, layers: int) -> int:
+    """Weights of every layer GEMM read once + activations in/out."""
+    bw = desc.bytes_per_el
+    hd = desc.head_dim
+    dq, dkv = desc.n_heads * hd, desc.n_kv_heads * hd
+    up = 2 * desc.d_ffn if desc.mlp_kind == 1 else desc.d_ffn
+    D, F = desc.d_model, desc.d_ffn
+    shapes = [(dq + 2 * dkv, D), (D, dq), (up, D), (D, F)]
+    per_layer = sum(n * k * bw + batch * k * bw + batch * n * 4 for n, k in shapes)
+    return per_layer * layers
+
+
+def head_bytes(desc, batch: int) -> int:
+    """K2: V x d head weights + normed activations + 17 B per row."""
+    return desc.vocab * desc.d_model * desc.bytes_per_el + batch * desc.d_model * desc.bytes_per_el + 17 * batch
+
+
+# ----------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port on host cores
+# ----------------------------------------------------------------------------
+def cpu_port_run(desc, steps: int, warmup: int, rows: int = 16, prefill: int = 4, seed: int = 1):
+    from oracle.oracle import OracleModel
+    from paper_2504_10724_b200 import eeb
+
+    cores = os.cpu_count() or 1
+    d = desc.replace(max_slots=rows, max_seq_len=max(16, prefill + steps + warmup + 1))
+    ref = OracleModel(d, threads=cores)
+    ref.load(d.num_layers)
+    rng = np.random.default_rng(seed)
+    slots = np.arange(rows)
+    for p in range(prefill):
+        ref.decode_step(0, eeb.FULL_DEPTH, 0.7, slots, rng.integers(0, d.vocab, rows), np.full(rows, p))
+    times = []
+    for k in range(warmup + steps):
+        toks = rng.integers(0, d.vocab, rows)
+        t0 = time.perf_counter()
+        ref.decode_step(0, eeb.INTROSPECTIVE, 0.7, slots, toks, np.full(rows, prefill + k))
+        if k >= warmup:
+            times.append(time.perf_counter() - t0)
+    total = sum(times)
+    return {"value": rows * len(times) / total, "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"{len(times)} introspective steps x {rows} rows of the same model on the CPU oracle "
+                      f"(f64-accumulating fp32 restatement, {cores} threads), context {prefill}..{prefill + steps + warmup}",
+            "seconds": total}
+
+
+def run_reference(args, desc):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    r = cpu_port_run(desc, args.steps, args.warmup)
+    line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * r["seconds"] / max(1, args.steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, desc),
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "EE decode tokens/s vs batch at 1/2/4/8 B200; exit-head/GEMM % HBM roofline"
+
+
+def workload_config(args, desc):
+    return {"workload": "C2: OPT-1.3B-shape early-exit decode step, exits 6/12/18/24, introspective "
+                        "(earliest confident head, survivors compacted), teacher-forced synthetic tokens",
+            "model_shape": desc.name, "layers": desc.num_layers, "d_model": desc.d_model,
+            "vocab": desc.vocab, "exit_layers": list(desc.exit_layers), "batch_per_gpu": args.batch,
+            "global_batch": args.batch * args.gpus, "prompt_len": args.prompt,
+            "context": f"{args.prompt}..{args.prompt + 99}", "th": args.th, "policy": args.policy,
+            "parallelism": f"replicas x{args.gpus} (requests sharded, no data-path collective)",
+            "l2": "inputs larger than L2 (2.9 GB of weights streamed per step > 126 MB L2)"}
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_eeb(args, desc):
+    import torch
+
+    from paper_2504_10724_b200 import eeb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    B, P = args.batch, args.prompt
+    policy = {"introspective": eeb.INTROSPECTIVE, "flat": eeb.FLAT, "profile": eeb.PROFILE,
+              "full_depth": eeb.FULL_DEPTH}[args.policy]
+    depth = args.depth if policy == eeb.FLAT else 0
+    desc = desc.replace(max_slots=B, max_seq_len=P + 100)
+    ctx = eeb.Context(local)
+    m = ctx.register(desc)
+    ctx.load_layers(m, desc.num_layers)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    rng = np.random.default_rng(1000 + rank)
+    slots = np.arange(B, dtype=np.int32)
+
+    # prefill: the prompt's KV at every layer (full-depth decode steps; untimed)
+    for p in range(P):
+        ctx.decode_step(m, 0, eeb.FULL_DEPTH, args.th, slots, rng.integers(0, desc.vocab, B), np.full(B, p))
+
+    n_tok = args.warmup + args.steps
+    toks_h = rng.integers(0, desc.vocab, (n_tok, B)).astype(np.int32)
+    pos_h = np.stack([np.full(B, P + (k % 100), np.int32) for k in range(n_tok)])
+    dev = torch.device("cuda", local)
+    toks_d = torch.from_numpy(toks_h).to(dev)
+    pos_d = torch.from_numpy(pos_h).to(dev)
+    slots_d = torch.from_numpy(slots).to(dev)
+    ne = len(desc.exit_layers)
+    outs = {"exit_layer": torch.zeros(B, dtype=torch.int32, device=dev),
+            "token_id": torch.zeros(B, dtype=torch.int32, device=dev),
+            "confidence": torch.zeros(B, dtype=torch.float32, device=dev),
+            "hist": torch.zeros(ne, dtype=torch.int64, device=dev)}
+    hist_acc = torch.zeros(ne, dtype=torch.int64, device=dev)
+    out_ptrs = {k: v.data_ptr() for k, v in outs.items()}
+    torch.cuda.synchronize()
+
+    def step(k):
+        ctx.decode_step_device(m, depth, policy, args.th, B, slots_d.data_ptr(), toks_d[k].data_ptr(),
+                               pos_d[k].data_ptr(), out_ptrs)
+
+    for k in range(args.warmup):
+        step(k)
+    ctx.synchronize()
+
+    # ---- timed region (device events on the eeb stream), graphs on ----------
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.warmup, n_tok):
+        step(k)
+        with torch.cuda.stream(stream):
+            hist_acc += outs["hist"]
+    ev1.record(stream)
+    ev1.synchronize()
+    ctx.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local)
+    value = world * B / (ms / 1000.0)
+
+    # ---- instrumented pass: per-kernel-category CUDA-event times -------------
+    ctx.profile_enable(True)
+    for k in range(args.warmup, n_tok):
+        step(k)
+    ctx.synchronize()
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    nsteps = max(1, prof["steps"])
+    launches_per_step = prof["last_step_launches"]
+    gemm_ms = prof["layer_gemm_ms"] / nsteps
+    head_ms = prof["exit_head_ms"] / nsteps
+    attn_ms = prof["attention_ms"] / nsteps
+    pk, pk_kind = peaks()
+    hbm = float(pk["hbm_gbs"])
+    g_bytes = gemm_bytes_per_step(desc, B, desc.num_layers)
+    h_bytes = head_bytes(desc, B) * ne
+    roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1)",
+            "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+            "traffic": None, "peak_source": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy burst)",
+            "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
+            "step_share": gemm_ms / max(1e-9, gemm_ms + head_ms + attn_ms + prof["norm_ms"] / nsteps
+                                        + prof["other_ms"] / nsteps)}
+    roof["frac"] = roof["achieved"] / hbm
+    exit_head = {"achieved": h_bytes / (head_ms / 1000.0) / 1e9 if head_ms > 0 else None, "unit": "GB/s",
+                 "ms_per_step": head_ms, "algorithmic_bytes_per_step": h_bytes}
+    if exit_head["achieved"]:
+        exit_head["frac"] = exit_head["achieved"] / hbm
+
+    # ---- e2e: public host-pointer API, H2D + D2H inside every call ------------
+    barrier()
+    t0 = time.perf_counter()
+    last = None
+    for k in range(args.warmup, n_tok):
+        last = ctx.decode_step(m, depth, policy, args.th, slots, toks_h[k], pos_h[k])
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = world * B * args.steps / e2e_s
+    h2d = 3 * B * 4
+    d2h = B * (4 + 4 + 4 + 4 + 1 + 1) + ne * 8 + 8 + 8
+
+    # ---- profiler histogram all-reduce across replicas (the one collective) ---
+    hist_total = hist_acc.cpu().numpy()
+    if world > 1:
+        uid = [eeb.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], world, rank)
+        hist_total, _ = ctx.profile_allreduce(hist_total, 0.0)
+    exit_frac = {str(l): float(c) / max(1, hist_total.sum()) for l, c in zip(desc.exit_layers, hist_total)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_port_run(desc, steps=2, warmup=0)
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, biased exit heads)",
+                "config": workload_config(args, desc), "roofline": roof, "exit_head_roofline": exit_head,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h},
+                "gpu_launches": int(launches_per_step * args.steps),
+                "launches_per_step": launches_per_step,
+                "clocks": clocks, "exit_fractions": exit_frac,
+                "kernel_ms_per_step": {k.replace("_ms", ""): v / nsteps for k, v in prof.items()
+                                       if k.endswith("_ms")}}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="eeb", choices=["eeb", "reference"])
+    ap.add_argument("--model", default="opt-1.3b-4x")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--prompt", type=int, default=128)
+    ap.add_argument("--policy", default="introspective",
+                    choices=["introspective", "flat", "profile", "full_depth"])
+    ap.add_argument("--depth", type=int, default=6)
+    ap.add_argument("--th", type=float, default=0.7)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    from paper_2504_10724_b200 import eeb
+
+    desc = eeb.PRESETS[args.model]
+    if args.impl == "reference":
+        return run_reference(args, desc)
+    return run_eeb(args, desc)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,187 @@
+/*
+ * eeb.h — C ABI of the B200-native batched early-exit (EE) decode step.
+ *
+ * This is the drop-in seam for the reference's decode step.  In the reference
+ * (HELIOS simulator, /root/reference/proj/include/eeserve/) `Simulator::serve_one`
+ * obtains each token's exit-head verdicts from a pre-computed trace
+ * (`tok.for_model(model)`, engine.hpp:345) and then applies the token policy
+ * (engine.hpp:349-366).  `eeb_decode_step` replaces exactly that pair for a
+ * whole batch: it runs the real decoder layers on the GPU, evaluates the exit
+ * heads, applies the same exit rule and returns, per row, the `ExitObservation`
+ * fields (trace.hpp:17-22) plus the breached / unchanged flags
+ * (engine.hpp:353,358,363,366) and the exit-layer histogram that feeds the
+ * profiler (`ExitHistogram`, pht.hpp:15-38; `record_token`, pht.hpp:92-102).
+ *
+ * Conventions (mirroring the reference):
+ *   - status codes map 1:1 onto the reference's exception types
+ *     (errors.hpp:9-30); no C++ exception crosses this boundary;
+ *   - one context per (host thread, GPU); calls on a context are externally
+ *     serialised; distinct contexts are independent (the reference's
+ *     `sweep -j` model, eeserve.cpp:220-259);
+ *   - the caller owns every buffer passed in; model descriptors are copied.
+ *
+ * Plain C: no torch or CUDA types in any signature (streams are opaque).
+ */
+#ifndef EEB_H_
+#define EEB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EEB_ABI_VERSION 1
+
+/* ↔ errors.hpp:9-30 (ValidationError, CapacityError, DomainError, StalenessError). */
+typedef enum {
+    EEB_OK = 0,
+    EEB_E_VALIDATION = 1,
+    EEB_E_CAPACITY = 2,
+    EEB_E_DOMAIN = 3,
+    EEB_E_STALE = 4,
+    EEB_E_CUDA = 5
+} eeb_status;
+
+/* ↔ Simulator::TokenPolicy (engine.hpp:156) plus the profiling pass of
+ * run_eval_cycle (engine.hpp:261-263, every head observed at full depth). */
+typedef enum {
+    EEB_FLAT = 0,          /* helios serving: every row runs `serving_depth` layers (trace.hpp:86-97) */
+    EEB_INTROSPECTIVE = 1, /* earliest confident head exits (trace.hpp:69-76); survivors compacted   */
+    EEB_FULL_DEPTH = 2,    /* vanilla: final head only, breached = false (engine.hpp:360-364)       */
+    EEB_PROFILE = 3        /* all heads on all rows at full depth: a full ModelTokenRecord per row  */
+} eeb_token_policy;
+
+typedef enum { EEB_F32 = 0, EEB_BF16 = 1 } eeb_dtype;
+typedef enum { EEB_MLP_RELU = 0, EEB_MLP_SWIGLU = 1 } eeb_mlp_kind;
+
+/* Model/layer descriptor ↔ ModelSpec (model_spec.hpp:15-37), extended
+ * additively with the real architecture dimensions the reference lacks. */
+typedef struct {
+    int32_t num_layers;
+    int32_t d_model;
+    int32_t n_heads;
+    int32_t n_kv_heads;
+    int32_t d_ffn;
+    int32_t vocab;
+    int32_t n_exits;
+    const int32_t* exit_layers;   /* strictly increasing, last == num_layers (model_spec.hpp:62-83) */
+    const float* exit_coverage;   /* biased-head calibration: fraction of tokens whose earliest
+                                     confident head (at design_th) is <= each exit; NULL = defaults */
+    float design_th;              /* threshold the exit heads are calibrated for (policy.hpp:51) */
+    int32_t dtype;                /* eeb_dtype of weights / GEMM activations / KV */
+    int32_t mlp_kind;             /* eeb_mlp_kind */
+    int32_t max_slots;            /* KV slot pool (memory_model.hpp:58-72 sizes it) */
+    int32_t max_seq_len;          /* KV positions per slot */
+    uint64_t seed;                /* weights are a pure function of (seed, tensor, index) */
+    float rope_theta;
+    float norm_eps;
+} eeb_model_desc;
+
+/* Per-step outputs, all arrays of length `batch` unless noted.  Any pointer
+ * may be NULL (not returned).  Row order = input row order. */
+typedef struct {
+    int32_t* exit_layer;     /* layer the row's token left the network at           */
+    int32_t* token_id;       /* argmax of the exit head used (trace.hpp:19)         */
+    float* confidence;       /* max softmax probability               */
+    float* logprob;          /* log-prob of the emitted token at that head          */
+    uint8_t* breached;       /* confidence < th (engine.hpp:353,358); 0 for full depth */
+    uint8_t* unchanged;      /* 1/0 = head token ==/!= final token; 2 = unknown (final head not run) */
+    int64_t* hist;           /* [n_exits] step exit histogram (K4)                  */
+    int64_t* n_breached;     /* [1] breached rows in this step                      */
+    double* sum_logprob;     /* [1] sum of logprob over rows, fixed order (fp64)    */
+    /* EEB_PROFILE only: every head's observation, [batch][n_exits] row-major. */
+    int32_t* head_token;
+    float* head_confidence;
+    float* head_logprob;
+} eeb_step_out;
+
+typedef struct eeb_ctx eeb_ctx;
+
+/* Lifecycle. */
+eeb_status eeb_create(int device, eeb_ctx** out);
+void eeb_destroy(eeb_ctx* ctx);
+const char* eeb_last_error(void);   /* thread-local message of the last failure */
+int eeb_abi_version(void);
+
+/* Register a model (descriptor copied) and allocate its KV slot pool.
+ * No weights are resident until eeb_load_layers. */
+eeb_status eeb_model_register(eeb_ctx* ctx, const eeb_model_desc* desc, int* model);
+
+/* Greedy layer loader ↔ do_load (engine.hpp:197-216) / apply_load
+ * (memory_model.hpp:86-105): make layers [1, to_depth] plus the base weights
+ * (embedding, exit heads) resident.  Weights are materialised on device from
+ * the model seed.  Shrinking frees layers deeper than to_depth. */
+eeb_status eeb_load_layers(eeb_ctx* ctx, int model, int to_depth);
+eeb_status eeb_evict(eeb_ctx* ctx, int model);   /* ↔ evict_model (memory_model.hpp:104) */
+eeb_status eeb_loaded_depth(eeb_ctx* ctx, int model, int* depth);
+eeb_status eeb_weight_bytes(eeb_ctx* ctx, int model, int depth, int64_t* bytes);
+
+/* Clear the KV of slots (positions marked as never computed). */
+eeb_status eeb_reset_slots(eeb_ctx* ctx, int model, int32_t n, const int32_t* slot_ids);
+
+/* The decode step ↔ Simulator::serve_one token loop (engine.hpp:344-386),
+ * batched per SPEC.md:465-473.  Row i decodes `input_tokens[i]` at position
+ * `positions[i]` of KV slot `slot_ids[i]`.
+ *   flat:          head at the deepest exit <= serving_depth; exit_layer = serving_depth
+ *   introspective: shallowest head with confidence >= th, final head forced
+ *   full_depth:    final head; exit_layer = num_layers, breached = 0
+ *   profile:       every head on every row (introspective rule picks exit_layer)
+ * Host-pointer variant: inputs/outputs are host memory (pageable or pinned);
+ * the H2D/D2H copies are part of the call, which returns when `out` is filled. */
+eeb_status eeb_decode_step(eeb_ctx* ctx, int model, int serving_depth, int policy, float th,
+                           int32_t batch, const int32_t* slot_ids, const int32_t* input_tokens,
+                           const int32_t* positions, eeb_step_out* out);
+
+/* Device-resident variant: every pointer (inputs and outputs) is device
+ * memory; the call is asynchronous on the context stream (eeb_synchronize). */
+eeb_status eeb_decode_step_device(eeb_ctx* ctx, int model, int serving_depth, int policy, float th,
+                                  int32_t batch, const int32_t* d_slot_ids,
+                                  const int32_t* d_input_tokens, const int32_t* d_positions,
+                                  eeb_step_out* d_out);
+eeb_status eeb_synchronize(eeb_ctx* ctx);
+
+/* Capture the step for (model, depth, policy, batch) into a CUDA graph and
+ * reuse it on later identical calls (0 = off, 1 = on; default on). */
+eeb_status eeb_set_graphs(eeb_ctx* ctx, int enable);
+
+/* Kernel tier override for tests: 0 = auto, 1 = CUDA-core GEMV only,
+ * 2 = tcgen05 tensor-core GEMM where applicable. */
+eeb_status eeb_set_gemm_tier(eeb_ctx* ctx, int tier);
+
+/* Test/diagnostic hooks (not used on the serving path). */
+eeb_status eeb_debug_last_logits(eeb_ctx* ctx, int head, float* host_out, int64_t n);  /* [batch][vocab] of one head, when retained */
+eeb_status eeb_debug_retain_logits(eeb_ctx* ctx, int enable);
+eeb_status eeb_debug_read_weight(eeb_ctx* ctx, int model, int tensor, int layer, int64_t offset,
+                                 int64_t n, float* host_out);
+eeb_status eeb_debug_read_kv(eeb_ctx* ctx, int model, int layer, int slot, int pos, float* host_k,
+                             float* host_v);
+
+/* Run one decode GEMM y[b][n] = sum_k x[b][k] * w[n][k] through a given tier
+ * (1 CUDA cores, 2 tcgen05) with an epilogue mode (0 store f32, 1 residual add
+ * onto zeros, 2 relu, 3 swiglu).  w, x are host arrays in the dtype (f32 or
+ * bf16 bit patterns); y is host f32, [batch][n] (or [batch][n/2] for swiglu). */
+eeb_status eeb_debug_gemm(eeb_ctx* ctx, int tier, int dtype, int n, int k, int batch, int mode,
+                          const void* w_host, const void* x_host, float* y_host);
+
+/* Per-kernel timing of the last step (CUDA events on the context stream).
+ * names: "gemm", "attention", "exit_head", ... ; returns total ms. */
+eeb_status eeb_profile_enable(eeb_ctx* ctx, int enable);
+eeb_status eeb_profile_read(eeb_ctx* ctx, char* json_out, int64_t cap);
+
+/* Stream handle as an opaque pointer (cudaStream_t) for callers that want to
+ * order their own work (e.g. torch) behind the step. */
+void* eeb_stream(eeb_ctx* ctx);
+
+/* NCCL histogram all-reduce across replicas at profiling boundaries
+ * (SURVEY §8e): sums `n` int64 counters and one double in place.  The
+ * communicator is created from a caller-distributed unique id. */
+eeb_status eeb_nccl_unique_id(uint8_t* id128);
+eeb_status eeb_nccl_init(eeb_ctx* ctx, const uint8_t* id128, int nranks, int rank);
+eeb_status eeb_profile_allreduce(eeb_ctx* ctx, int64_t* counters, int n, double* sum_neg_logprob);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EEB_H_ */

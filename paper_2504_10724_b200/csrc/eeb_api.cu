@@ -1,0 +1,1146 @@
+// eeb_api.cu — context, model registry, greedy layer loader and the batched
+// early-exit decode step behind the C ABI in include/eeb/eeb.h.
+//
+// The step is the batched form of Simulator::serve_one's token loop
+// (/root/reference/proj/include/eeserve/engine.hpp:344-386):
+// one call advances every row one token.  The launch sequence for a given
+// (model, depth, policy, batch) is fixed — row counts after compaction live
+// in device memory — so it is captured once into a CUDA graph and replayed.
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/eeb/eeb.h"
+#include "kernels.h"
+#include "synth.cuh"
+
+namespace eeb {
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        release();
+        EEB_CUDA(cudaMalloc(&p, n));
+        bytes = n;
+    }
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct LayerWeights {
+    DevBuf attn_norm, mlp_norm, wqkv, wo, wup, wdown;
+};
+
+struct Model {
+    eeb_model_desc desc{};
+    std::vector<int> exits;
+    std::vector<float> coverage;
+    std::vector<float> alphas;
+    int head_dim = 0, dq = 0, dkv = 0, up_rows = 0;
+    size_t wbytes = 0;  // weight element size
+    // base weights
+    DevBuf emb;
+    std::vector<std::unique_ptr<DevBuf>> head, head_norm;
+    std::vector<std::unique_ptr<LayerWeights>> layers;  // index l-1
+    int loaded = 0;
+    // KV pool
+    DevBuf k_cache, v_cache, kv_depth, rope_cos, rope_sin;
+    size_t kv_layer_elems = 0;
+};
+
+struct GraphKey {
+    int model, depth, policy, batch, tier;
+    uint32_t th_bits;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(model, depth, policy, batch, tier, th_bits) <
+               std::tie(o.model, o.depth, o.policy, o.batch, o.tier, o.th_bits);
+    }
+};
+
+enum Cat { kCatGemm = 0, kCatAttn, kCatHead, kCatNorm, kCatOther, kNumCat };
+const char* kCatNames[kNumCat] = {"layer_gemm", "attention", "exit_head", "norm", "other"};
+
+}  // namespace
+
+}  // namespace eeb
+
+struct eeb_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<std::unique_ptr<eeb::Model>> models;
+    int graphs_enabled = 1;
+    int gemm_tier = 0;
+    int retain_logits = 0;
+    // step workspace (grow-only)
+    int cap_rows = 0;
+    eeb::DevBuf xA, xB, hn, qkv, attn, mlp_h, logits, ws;
+    eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
+    eeb::DevBuf head_tok, head_conf, head_logp;
+    eeb::DevBuf o_exit, o_tok, o_conf, o_logp, o_breach, o_unch, o_bin, o_hist, o_nbr, o_sum;
+    eeb::DevBuf o_htok, o_hconf, o_hlogp;
+    std::vector<std::unique_ptr<eeb::DevBuf>> logits_keep;
+    int64_t ws_elems = 0;
+    // pinned staging for the host-pointer API
+    void* pin = nullptr;
+    size_t pin_bytes = 0;
+    std::map<eeb::GraphKey, cudaGraphExec_t> graphs;
+    // profiling
+    int profiling = 0;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+    double cat_ms[eeb::kNumCat] = {0};
+    int64_t cat_launches[eeb::kNumCat] = {0};
+    int64_t step_launches = 0;
+    int64_t steps_profiled = 0;
+    ncclComm_t nccl = nullptr;
+    eeb::DevBuf nccl_buf;
+};
+
+namespace eeb {
+
+namespace {
+
+
+// NCCL is resolved at run time (dlopen) rather than linked: the process may
+// already hold torch's bundled libnccl.so.2, and two NCCL builds under one
+// soname would clash.  An already-loaded NCCL is preferred.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char* env = std::getenv("EEB_NCCL_LIB");
+            h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!h) return;
+        api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
+        api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
+        api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
+        api.group_start = (decltype(api.group_start))dlsym(h, "ncclGroupStart");
+        api.group_end = (decltype(api.group_end))dlsym(h, "ncclGroupEnd");
+        api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
+        api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+    });
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce)
+        throw Error(EEB_E_CUDA, "NCCL (libnccl.so.2) could not be loaded");
+    return api;
+}
+
+int status_of(const Error& e) { return e.code; }
+
+void set_error(const std::string& m) { g_last_error = m; }
+
+template <typename F>
+eeb_status guarded(F&& f) {
+    try {
+        f();
+        return EEB_OK;
+    } catch (const Error& e) {
+        set_error(e.what());
+        return static_cast<eeb_status>(status_of(e));
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return EEB_E_CAPACITY;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return EEB_E_CUDA;
+    }
+}
+
+Model& model_of(eeb_ctx* c, int m) {
+    if (!c) throw Error(EEB_E_DOMAIN, "null context");
+    if (m < 0 || m >= (int)c->models.size() || !c->models[m])
+        throw Error(EEB_E_DOMAIN, "unknown model handle " + std::to_string(m));
+    return *c->models[m];
+}
+
+std::vector<float> default_coverage(int n) {
+    // Cumulative exit law of the reference's OPT-1.3B calibration: 73.0 / 4.7 /
+    // 22.3 % (fixtures/FIXTURES.md:47-55); intermediate heads spread the 4.7 %.
+    std::vector<float> c(n);
+    for (int i = 0; i < n; ++i) {
+        if (i == n - 1) c[i] = 1.0f;
+        else if (n <= 2 || i == 0) c[i] = 0.73f;
+        else c[i] = 0.73f + 0.047f * (float)i / (float)(n - 2);
+    }
+    return c;
+}
+
+void validate_desc(const eeb_model_desc& d) {
+    auto bad = [](const std::string& m) { throw Error(EEB_E_VALIDATION, "model: " + m); };
+    if (d.num_layers <= 0 || d.num_layers > 255) bad("num_layers must be in [1, 255]");
+    if (d.d_model <= 0 || d.n_heads <= 0 || d.n_kv_heads <= 0 || d.d_ffn <= 0 || d.vocab <= 1)
+        bad("dimensions must be positive");
+    if (d.d_model % d.n_heads != 0) bad("d_model must be a multiple of n_heads");
+    if (d.n_heads % d.n_kv_heads != 0) bad("n_heads must be a multiple of n_kv_heads");
+    if (d.d_model % 256 != 0 || d.d_ffn % 256 != 0) bad("d_model and d_ffn must be multiples of 256");
+    if (d.n_exits <= 0 || d.n_exits > 64 || !d.exit_layers) bad("exit_layers must be non-empty (<= 64)");
+    for (int i = 0; i < d.n_exits; ++i) {
+        if (d.exit_layers[i] <= 0) bad("exit layers must be positive");
+        if (i > 0 && d.exit_layers[i] <= d.exit_layers[i - 1]) bad("exit_layers must be strictly increasing");
+    }
+    if (d.exit_layers[d.n_exits - 1] != d.num_layers) bad("last exit layer must equal num_layers");
+    if (d.dtype != EEB_F32 && d.dtype != EEB_BF16) bad("dtype must be f32 or bf16");
+    if (d.mlp_kind != EEB_MLP_RELU && d.mlp_kind != EEB_MLP_SWIGLU) bad("unknown mlp kind");
+    if (d.max_slots <= 0 || d.max_seq_len <= 0) bad("max_slots and max_seq_len must be positive");
+    if (!(d.design_th >= 0.f && d.design_th <= 1.f)) bad("design_th must be in [0,1]");
+}
+
+// ---------------------------------------------------------------------------
+// Loader ↔ do_load / apply_load: materialise layers [loaded+1, to] (and the
+// base weights on the first load); free layers deeper than `to` on shrink.
+// ---------------------------------------------------------------------------
+void load_to(eeb_ctx* c, Model& m, int to) {
+    const eeb_model_desc& d = m.desc;
+    if (to < 0 || to > d.num_layers)
+        throw Error(EEB_E_DOMAIN, "load: depth " + std::to_string(to) + " outside [0, " +
+                                      std::to_string(d.num_layers) + "]");
+    cudaStream_t s = c->stream;
+    const uint64_t seed = d.seed;
+    const int D = d.d_model, F = d.d_ffn;
+    if (to == 0) {
+        m.layers.clear();
+        m.head.clear();
+        m.head_norm.clear();
+        m.emb.release();
+        m.loaded = 0;
+        return;
+    }
+    if (m.loaded == 0) {
+        m.emb.ensure((size_t)d.vocab * D * m.wbytes);
+        synth_embedding(d.dtype, m.emb.p, seed, d.vocab, D, s);
+        m.head.clear();
+        m.head_norm.clear();
+        for (int e = 0; e < d.n_exits; ++e) {
+            auto h = std::make_unique<DevBuf>();
+            h->ensure((size_t)d.vocab * D * m.wbytes);
+            synth_head(d.dtype, h->p, seed, e, m.alphas[e], d.vocab, D, s);
+            auto g = std::make_unique<DevBuf>();
+            g->ensure((size_t)D * sizeof(float));
+            synth_norm(g->p, seed, synth::base_tid(synth::kHeadNorm, e), D, s);
+            m.head.push_back(std::move(h));
+            m.head_norm.push_back(std::move(g));
+        }
+    }
+    const float rsig = synth::residual_sigma(D, F);
+    while ((int)m.layers.size() < to) {
+        const int l = (int)m.layers.size() + 1;
+        auto L = std::make_unique<LayerWeights>();
+        L->attn_norm.ensure((size_t)D * 4);
+        L->mlp_norm.ensure((size_t)D * 4);
+        synth_norm(L->attn_norm.p, seed, synth::layer_tid(l, synth::kAttnNorm), D, s);
+        synth_norm(L->mlp_norm.p, seed, synth::layer_tid(l, synth::kMlpNorm), D, s);
+        const int qkv_rows = m.dq + 2 * m.dkv;
+        L->wqkv.ensure((size_t)qkv_rows * D * m.wbytes);
+        synth_linear(d.dtype, L->wqkv.p, seed, synth::layer_tid(l, synth::kWqkv), qkv_rows, D,
+                     synth::kSigma, false, D, s);
+        L->wo.ensure((size_t)D * m.dq * m.wbytes);
+        synth_linear(d.dtype, L->wo.p, seed, synth::layer_tid(l, synth::kWo), D, m.dq, rsig, true, D, s);
+        L->wup.ensure((size_t)m.up_rows * D * m.wbytes);
+        synth_linear(d.dtype, L->wup.p, seed, synth::layer_tid(l, synth::kWup), m.up_rows, D,
+                     synth::kSigma, false, D, s);
+        L->wdown.ensure((size_t)D * F * m.wbytes);
+        synth_linear(d.dtype, L->wdown.p, seed, synth::layer_tid(l, synth::kWdown), D, F, rsig, true,
+                     D, s);
+        m.layers.push_back(std::move(L));
+    }
+    while ((int)m.layers.size() > to) m.layers.pop_back();
+    m.loaded = to;
+    EEB_CUDA(cudaStreamSynchronize(s));
+}
+
+int64_t weight_bytes_at(const Model& m, int depth) {
+    const eeb_model_desc& d = m.desc;
+    const int64_t D = d.d_model, F = d.d_ffn;
+    const int64_t base = (int64_t)d.vocab * D * m.wbytes * (1 + d.n_exits) + (int64_t)d.n_exits * D * 4;
+    const int64_t per_layer =
+        ((int64_t)(m.dq + 2 * m.dkv) * D + D * m.dq + (int64_t)m.up_rows * D + D * F) * m.wbytes +
+        2 * D * 4;
+    return depth <= 0 ? 0 : base + per_layer * depth;
+}
+
+// ---------------------------------------------------------------------------
+// Step workspace.
+// ---------------------------------------------------------------------------
+struct Ints {  // offsets into ctx->rows
+    int* nA; int* nB; int* rowA; int* slotA; int* posA; int* rowB; int* slotB; int* posB;
+    int* src; int* tok; int* slot; int* pos;
+};
+
+Ints ints_of(eeb_ctx* c) {
+    int* base = c->rows.as<int>();
+    const int R = c->cap_rows;
+    Ints r;
+    r.nA = base; r.nB = base + 1;
+    int* p = base + 32;
+    r.rowA = p; p += R; r.slotA = p; p += R; r.posA = p; p += R;
+    r.rowB = p; p += R; r.slotB = p; p += R; r.posB = p; p += R;
+    r.src = p; p += R; r.tok = p; p += R; r.slot = p; p += R; r.pos = p; p += R;
+    return r;
+}
+
+void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
+    const eeb_model_desc& d = m.desc;
+    const int R = std::max(batch, c->cap_rows);
+    const size_t act = m.wbytes;
+    const int64_t D = d.d_model, F = d.d_ffn;
+    if (R > c->cap_rows) {
+        for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
+        c->graphs.clear();
+    }
+    c->cap_rows = R;
+    c->xA.ensure((size_t)R * D * 4);
+    c->xB.ensure((size_t)R * D * 4);
+    c->hn.ensure((size_t)R * D * act);
+    c->qkv.ensure((size_t)R * (m.dq + 2 * m.dkv) * 4);
+    c->attn.ensure((size_t)R * m.dq * act);
+    c->mlp_h.ensure((size_t)R * F * act);
+    c->logits.ensure((size_t)R * d.vocab * 4);
+    // split-K partial bound: splits <= K / (32 * vec) for every GEMM of the step.
+    const int64_t kmin = act == 4 ? 128 : 256;
+    int64_t need = 0;
+    auto upd = [&](int64_t N, int64_t K) { need = std::max(need, (K / kmin + 1) * R * N); };
+    upd(m.dq + 2 * m.dkv, D);
+    upd(D, m.dq);
+    upd(m.up_rows, D);
+    upd(D, F);
+    upd(d.vocab, D);
+    c->ws.ensure((size_t)need * 4);
+    c->ws_elems = (int64_t)(c->ws.bytes / 4);
+    c->rows.ensure((size_t)(32 + 12 * R) * 4);
+    c->head_tok.ensure((size_t)R * 4);
+    c->head_conf.ensure((size_t)R * 4);
+    c->head_logp.ensure((size_t)R * 4);
+    c->o_exit.ensure((size_t)R * 4);
+    c->o_tok.ensure((size_t)R * 4);
+    c->o_conf.ensure((size_t)R * 4);
+    c->o_logp.ensure((size_t)R * 4);
+    c->o_breach.ensure((size_t)R);
+    c->o_unch.ensure((size_t)R);
+    c->o_bin.ensure((size_t)R * 4);
+    c->o_hist.ensure(64 * 8);
+    c->o_nbr.ensure(8);
+    c->o_sum.ensure(8);
+    c->o_htok.ensure((size_t)R * d.n_exits * 4);
+    c->o_hconf.ensure((size_t)R * d.n_exits * 4);
+    c->o_hlogp.ensure((size_t)R * d.n_exits * 4);
+    const size_t pin_need = (size_t)R * (3 * 4 + 6 * 4 + 2 + 3 * 64 * 4) + 1024;
+    if (pin_need > c->pin_bytes) {
+        if (c->pin) cudaFreeHost(c->pin);
+        c->pin = nullptr;
+        EEB_CUDA(cudaMallocHost(&c->pin, pin_need));
+        c->pin_bytes = pin_need;
+    }
+}
+
+StepOutDev out_dev(eeb_ctx* c) {
+    StepOutDev o;
+    o.exit_layer = c->o_exit.as<int32_t>();
+    o.token_id = c->o_tok.as<int32_t>();
+    o.confidence = c->o_conf.as<float>();
+    o.logprob = c->o_logp.as<float>();
+    o.breached = c->o_breach.as<uint8_t>();
+    o.unchanged = c->o_unch.as<uint8_t>();
+    o.bin = c->o_bin.as<int32_t>();
+    o.hist = c->o_hist.as<int64_t>();
+    o.n_breached = c->o_nbr.as<int64_t>();
+    o.sum_logprob = c->o_sum.as<double>();
+    o.head_token = c->o_htok.as<int32_t>();
+    o.head_confidence = c->o_hconf.as<float>();
+    o.head_logprob = c->o_hlogp.as<float>();
+    return o;
+}
+
+// ---------------------------------------------------------------------------
+// Launch helpers with optional per-category event timing.
+// ---------------------------------------------------------------------------
+struct Timer {
+    eeb_ctx* c;
+    int cat;
+    cudaEvent_t b = nullptr, e = nullptr;
+    Timer(eeb_ctx* ctx, int category) : c(ctx), cat(category) {
+        c->cat_launches[cat] += 0;
+        if (!c->profiling) return;
+        b = take();
+        e = take();
+        EEB_CUDA(cudaEventRecord(b, c->stream));
+    }
+    ~Timer() {
+        if (!c->profiling) return;
+        cudaEventRecord(e, c->stream);
+        c->ev_used.push_back({cat, {b, e}});
+    }
+    cudaEvent_t take() {
+        if (c->ev_pool.empty()) {
+            cudaEvent_t ev;
+            EEB_CUDA(cudaEventCreate(&ev));
+            return ev;
+        }
+        cudaEvent_t ev = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return ev;
+    }
+};
+
+void count(eeb_ctx* c, int cat, int n) {
+    c->cat_launches[cat] += n;
+    c->step_launches += n;
+}
+
+void gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int N, int K, int mode,
+          float* out_f32, int ldo, void* out_act, const int* n_active, int batch) {
+    GemmArgs a;
+    a.dtype = m.desc.dtype;
+    a.W = W;
+    a.X = X;
+    a.n_active = n_active;
+    a.max_rows = batch;
+    a.N = N;
+    a.K = K;
+    a.mode = mode;
+    a.out_f32 = out_f32;
+    a.out_act = out_act;
+    a.ldo = ldo;
+    a.workspace = c->ws.as<float>();
+    a.workspace_elems = c->ws_elems;
+    a.num_sms = c->num_sms;
+    if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) {
+        const int n = gemm_tc(a, c->stream);
+        if (n > 0) {
+            count(c, cat, n);
+            return;
+        }
+        if (c->gemm_tier == 2 && batch >= 16)
+            throw Error(EEB_E_DOMAIN, "tensor-core tier requested but not applicable");
+    }
+    gemm_cc(a, c->stream);
+    count(c, cat, 2);
+}
+
+// ---------------------------------------------------------------------------
+// The step.
+// ---------------------------------------------------------------------------
+void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
+    Model& m = model_of(c, mi);
+    const eeb_model_desc& d = m.desc;
+    const int L = d.num_layers, D = d.d_model, F = d.d_ffn;
+    cudaStream_t s = c->stream;
+    Ints I = ints_of(c);
+    RowState A{I.nA, I.rowA, I.slotA, I.posA, c->xA.as<float>()};
+    RowState B{I.nB, I.rowB, I.slotB, I.posB, c->xB.as<float>()};
+    const StepOutDev o = out_dev(c);
+
+    // Which heads run, and how deep the stack goes.
+    std::vector<int> heads;
+    int run_layers = L;
+    if (policy == EEB_FLAT) {
+        int e_used = -1;
+        for (int e = 0; e < d.n_exits; ++e)
+            if (m.exits[e] <= depth) e_used = e;
+        if (e_used < 0)  // observation_for_depth throws DomainError (trace.hpp:92-93)
+            throw Error(EEB_E_DOMAIN, "no exit head at or below layer " + std::to_string(depth));
+        heads.push_back(e_used);
+        run_layers = depth;
+    } else if (policy == EEB_FULL_DEPTH) {
+        heads.push_back(d.n_exits - 1);
+    } else {
+        for (int e = 0; e < d.n_exits; ++e) heads.push_back(e);
+    }
+
+    {
+        Timer t(c, kCatOther);
+        launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, batch, D, A, s);
+        count(c, kCatOther, 1);
+    }
+    RowState cur = A, alt = B;
+    size_t hi = 0;
+    const int qkv_n = m.dq + 2 * m.dkv;
+    for (int l = 1; l <= run_layers; ++l) {
+        const LayerWeights& W = *m.layers[l - 1];
+        {
+            Timer t(c, kCatNorm);
+            launch_rmsnorm(d.dtype, cur.x, W.attn_norm.as<float>(), cur.n_active, batch, D,
+                           d.norm_eps, c->hn.p, s);
+            count(c, kCatNorm, 1);
+        }
+        {
+            Timer t(c, kCatGemm);
+            gemm(c, kCatGemm, m, W.wqkv.p, c->hn.p, qkv_n, D, kStoreF32, c->qkv.as<float>(), qkv_n,
+                 nullptr, cur.n_active, batch);
+        }
+        {
+            Timer t(c, kCatAttn);
+            AttnArgs a;
+            a.dtype = d.dtype;
+            a.qkv = c->qkv.as<float>();
+            const size_t esz = m.wbytes;
+            a.k_cache = static_cast<char*>(m.k_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * esz;
+            a.v_cache = static_cast<char*>(m.v_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * esz;
+            a.kv_depth = m.kv_depth.as<uint8_t>();
+            a.rope_cos = m.rope_cos.as<float>();
+            a.rope_sin = m.rope_sin.as<float>();
+            a.n_active = cur.n_active;
+            a.slot = cur.slot;
+            a.pos = cur.pos;
+            a.max_rows = batch;
+            a.layer = l;
+            a.n_heads = d.n_heads;
+            a.n_kv_heads = d.n_kv_heads;
+            a.head_dim = m.head_dim;
+            a.max_seq = d.max_seq_len;
+            a.out = c->attn.p;
+            launch_attention(a, s);
+            count(c, kCatAttn, 1);
+        }
+        {
+            Timer t(c, kCatGemm);
+            gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, kResidAdd, cur.x, D, nullptr, cur.n_active,
+                 batch);
+        }
+        {
+            Timer t(c, kCatNorm);
+            launch_rmsnorm(d.dtype, cur.x, W.mlp_norm.as<float>(), cur.n_active, batch, D, d.norm_eps,
+                           c->hn.p, s);
+            count(c, kCatNorm, 1);
+        }
+        {
+            Timer t(c, kCatGemm);
+            gemm(c, kCatGemm, m, W.wup.p, c->hn.p, m.up_rows, D,
+                 d.mlp_kind == EEB_MLP_SWIGLU ? kSwigluAct : kReluAct, nullptr, 0, c->mlp_h.p,
+                 cur.n_active, batch);
+            gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, kResidAdd, cur.x, D, nullptr,
+                 cur.n_active, batch);
+        }
+        while (hi < heads.size() && m.exits[heads[hi]] == l) {
+            const int e = heads[hi];
+            const bool is_final = hi + 1 == heads.size();
+            Timer t(c, kCatHead);
+            launch_rmsnorm(d.dtype, cur.x, m.head_norm[e]->as<float>(), cur.n_active, batch, D,
+                           d.norm_eps, c->hn.p, s);
+            gemm(c, kCatHead, m, m.head[e]->p, c->hn.p, d.vocab, D, kStoreF32, c->logits.as<float>(),
+                 d.vocab, nullptr, cur.n_active, batch);
+            if (c->retain_logits) {
+                while ((int)c->logits_keep.size() < d.n_exits)
+                    c->logits_keep.push_back(std::make_unique<DevBuf>());
+                c->logits_keep[e]->ensure((size_t)batch * d.vocab * 4);
+                EEB_CUDA(cudaMemcpyAsync(c->logits_keep[e]->p, c->logits.p, (size_t)batch * d.vocab * 4,
+                                         cudaMemcpyDeviceToDevice, s));
+            }
+            HeadOut h{c->head_tok.as<int>(), c->head_conf.as<float>(), c->head_logp.as<float>()};
+            launch_head_reduce(c->logits.as<float>(), d.vocab, cur.n_active, batch, h, s);
+            DecideArgs da;
+            da.policy = policy;
+            da.exit_index = e;
+            da.n_exits = d.n_exits;
+            da.exit_layer = m.exits[e];
+            da.num_layers = L;
+            da.serving_depth = depth;
+            da.is_final = is_final ? 1 : 0;
+            da.th = th;
+            da.max_rows = batch;
+            da.cur = cur;
+            da.nxt = alt;
+            da.gather_src = I.src;
+            da.head = h;
+            da.out = o;
+            for (int k = 0; k < 64; ++k) da.layers[k] = k < d.n_exits ? m.exits[k] : 0;
+            launch_decide(da, s);
+            count(c, kCatHead, 3);
+            if (policy == EEB_INTROSPECTIVE && !is_final) {
+                launch_gather_rows(cur.x, alt.x, I.src, alt.n_active, batch, D, s);
+                count(c, kCatHead, 1);
+                std::swap(cur, alt);
+            }
+            ++hi;
+        }
+    }
+    {
+        Timer t(c, kCatOther);
+        launch_finalize(batch, d.n_exits, o, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len, s);
+        count(c, kCatOther, 1);
+    }
+}
+
+void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int batch) {
+    const eeb_model_desc& d = m.desc;
+    if (batch <= 0 || batch > d.max_slots)
+        throw Error(EEB_E_DOMAIN, "batch must be in [1, max_slots]");
+    if (batch > 1024) throw Error(EEB_E_DOMAIN, "batch above 1024 rows per step");
+    if (!(th >= 0.f && th <= 1.f)) throw Error(EEB_E_VALIDATION, "th must be in [0,1]");
+    if (policy < EEB_FLAT || policy > EEB_PROFILE) throw Error(EEB_E_DOMAIN, "unknown token policy");
+    const int need = policy == EEB_FLAT ? depth : d.num_layers;
+    if (policy == EEB_FLAT && (depth <= 0 || depth > d.num_layers))
+        throw Error(EEB_E_DOMAIN, "serving depth " + std::to_string(depth) + " outside [1, num_layers]");
+    if (m.loaded < need)
+        throw Error(EEB_E_CAPACITY, "layers up to " + std::to_string(need) + " are not resident (loaded " +
+                                        std::to_string(m.loaded) + ")");
+    if (d.dtype == EEB_F32 && batch > 64)
+        throw Error(EEB_E_DOMAIN, "f32 parity model supports at most 64 rows per step");
+    (void)c;
+}
+
+void run_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
+    Model& m = model_of(c, mi);
+    const bool use_graph = c->graphs_enabled && !c->profiling && !c->retain_logits;
+    if (!use_graph) {
+        c->step_launches = 0;
+        enqueue_step(c, mi, depth, policy, th, batch);
+        return;
+    }
+    uint32_t thb;
+    std::memcpy(&thb, &th, 4);
+    GraphKey key{mi, policy == EEB_FLAT ? depth : 0, policy, batch, c->gemm_tier, thb};
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        c->step_launches = 0;
+        cudaGraph_t g;
+        EEB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_step(c, mi, depth, policy, th, batch);
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &g);
+            throw;
+        }
+        EEB_CUDA(cudaStreamEndCapture(c->stream, &g));
+        cudaGraphExec_t ex;
+        EEB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        cudaGraphDestroy(g);
+        it = c->graphs.emplace(key, ex).first;
+    }
+    (void)m;
+    EEB_CUDA(cudaGraphLaunch(it->second, c->stream));
+}
+
+void harvest_profile(eeb_ctx* c) {
+    if (!c->profiling) return;
+    EEB_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& [cat, ev] : c->ev_used) {
+        float ms = 0.f;
+        EEB_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+        c->cat_ms[cat] += ms;
+        c->ev_pool.push_back(ev.first);
+        c->ev_pool.push_back(ev.second);
+    }
+    c->ev_used.clear();
+    c->steps_profiled += 1;
+}
+
+}  // namespace
+}  // namespace eeb
+
+using namespace eeb;
+
+extern "C" {
+
+int eeb_abi_version(void) { return EEB_ABI_VERSION; }
+
+const char* eeb_last_error(void) { return g_last_error.c_str(); }
+
+eeb_status eeb_create(int device, eeb_ctx** out) {
+    return guarded([&] {
+        if (!out) throw Error(EEB_E_DOMAIN, "null output handle");
+        *out = nullptr;
+        int n = 0;
+        EEB_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw Error(EEB_E_DOMAIN, "no CUDA device " + std::to_string(device));
+        EEB_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        EEB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw Error(EEB_E_CUDA, std::string("eeb targets sm_100a (B200); device is ") + prop.name);
+        auto c = std::make_unique<eeb_ctx>();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        EEB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c.release();
+    });
+}
+
+void eeb_destroy(eeb_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
+    for (auto ev : c->ev_pool) cudaEventDestroy(ev);
+    if (c->nccl) nccl().comm_destroy(c->nccl);
+    if (c->pin) cudaFreeHost(c->pin);
+    c->models.clear();
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+eeb_status eeb_model_register(eeb_ctx* c, const eeb_model_desc* desc, int* model) {
+    return guarded([&] {
+        if (!c || !desc || !model) throw Error(EEB_E_DOMAIN, "null argument");
+        validate_desc(*desc);
+        EEB_CUDA(cudaSetDevice(c->device));
+        auto m = std::make_unique<Model>();
+        m->desc = *desc;
+        m->exits.assign(desc->exit_layers, desc->exit_layers + desc->n_exits);
+        m->desc.exit_layers = m->exits.data();
+        if (desc->exit_coverage) m->coverage.assign(desc->exit_coverage, desc->exit_coverage + desc->n_exits);
+        else m->coverage = default_coverage(desc->n_exits);
+        m->desc.exit_coverage = m->coverage.data();
+        if (m->desc.norm_eps <= 0.f) m->desc.norm_eps = 1e-5f;
+        if (m->desc.rope_theta <= 0.f) m->desc.rope_theta = 10000.f;
+        const eeb_model_desc& d = m->desc;
+        m->alphas = synth::head_alphas(d.d_model, d.vocab, d.num_layers, m->exits, m->coverage, d.design_th);
+        m->head_dim = d.d_model / d.n_heads;
+        m->dq = d.n_heads * m->head_dim;
+        m->dkv = d.n_kv_heads * m->head_dim;
+        m->up_rows = d.mlp_kind == EEB_MLP_SWIGLU ? 2 * d.d_ffn : d.d_ffn;
+        m->wbytes = d.dtype == EEB_BF16 ? 2 : 4;
+        if (m->head_dim % 16 != 0 || m->head_dim > 128) throw Error(EEB_E_VALIDATION, "head_dim must be a multiple of 16, <= 128");
+        // KV pool ↔ kv_bytes_per_slot (memory_model.hpp:58-60): every layer, max_seq positions.
+        m->kv_layer_elems = (size_t)d.max_slots * d.n_kv_heads * d.max_seq_len * m->head_dim;
+        m->k_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
+        m->v_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
+        m->kv_depth.ensure((size_t)d.max_slots * d.max_seq_len);
+        EEB_CUDA(cudaMemset(m->kv_depth.p, 0, m->kv_depth.bytes));
+        // RoPE tables in f64 then rounded (restated identically by the oracle).
+        const int half = m->head_dim / 2;
+        std::vector<float> cs((size_t)d.max_seq_len * half), sn((size_t)d.max_seq_len * half);
+        for (int p = 0; p < d.max_seq_len; ++p)
+            for (int j = 0; j < half; ++j) {
+                const double inv = std::pow((double)d.rope_theta, -2.0 * j / (double)m->head_dim);
+                const double ang = (double)p * inv;
+                cs[(size_t)p * half + j] = (float)std::cos(ang);
+                sn[(size_t)p * half + j] = (float)std::sin(ang);
+            }
+        m->rope_cos.ensure(cs.size() * 4);
+        m->rope_sin.ensure(sn.size() * 4);
+        EEB_CUDA(cudaMemcpy(m->rope_cos.p, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+        EEB_CUDA(cudaMemcpy(m->rope_sin.p, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+        c->models.push_back(std::move(m));
+        *model = (int)c->models.size() - 1;
+    });
+}
+
+eeb_status eeb_load_layers(eeb_ctx* c, int model, int to_depth) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        EEB_CUDA(cudaSetDevice(c->device));
+        for (auto it = c->graphs.begin(); it != c->graphs.end();) {
+            if (it->first.model == model) {
+                cudaGraphExecDestroy(it->second);
+                it = c->graphs.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        load_to(c, m, to_depth);
+    });
+}
+
+eeb_status eeb_evict(eeb_ctx* c, int model) { return eeb_load_layers(c, model, 0); }
+
+eeb_status eeb_loaded_depth(eeb_ctx* c, int model, int* depth) {
+    return guarded([&] {
+        if (!depth) throw Error(EEB_E_DOMAIN, "null output");
+        *depth = model_of(c, model).loaded;
+    });
+}
+
+eeb_status eeb_weight_bytes(eeb_ctx* c, int model, int depth, int64_t* bytes) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (!bytes) throw Error(EEB_E_DOMAIN, "null output");
+        if (depth < 0 || depth > m.desc.num_layers) throw Error(EEB_E_DOMAIN, "depth outside [0, num_layers]");
+        *bytes = weight_bytes_at(m, depth);
+    });
+}
+
+eeb_status eeb_reset_slots(eeb_ctx* c, int model, int32_t n, const int32_t* slot_ids) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        for (int i = 0; i < n; ++i) {
+            if (slot_ids[i] < 0 || slot_ids[i] >= m.desc.max_slots) throw Error(EEB_E_DOMAIN, "slot out of range");
+            EEB_CUDA(cudaMemsetAsync(m.kv_depth.as<uint8_t>() + (size_t)slot_ids[i] * m.desc.max_seq_len, 0,
+                                     m.desc.max_seq_len, c->stream));
+        }
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+static void validate_rows_host(const Model& m, int batch, const int32_t* slot, const int32_t* tok,
+                               const int32_t* pos) {
+    for (int i = 0; i < batch; ++i) {
+        if (slot[i] < 0 || slot[i] >= m.desc.max_slots) throw Error(EEB_E_DOMAIN, "slot id out of range");
+        if (tok[i] < 0 || tok[i] >= m.desc.vocab) throw Error(EEB_E_DOMAIN, "token id out of range");
+        if (pos[i] < 0 || pos[i] >= m.desc.max_seq_len) throw Error(EEB_E_DOMAIN, "position out of range");
+        for (int j = 0; j < i; ++j)
+            if (slot[j] == slot[i]) throw Error(EEB_E_VALIDATION, "duplicate slot id in one step");
+    }
+}
+
+eeb_status eeb_decode_step(eeb_ctx* c, int model, int depth, int policy, float th, int32_t batch,
+                           const int32_t* slot_ids, const int32_t* input_tokens, const int32_t* positions,
+                           eeb_step_out* out) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (!slot_ids || !input_tokens || !positions) throw Error(EEB_E_DOMAIN, "null input array");
+        check_step_args(c, m, depth, policy, th, batch);
+        validate_rows_host(m, batch, slot_ids, input_tokens, positions);
+        EEB_CUDA(cudaSetDevice(c->device));
+        ensure_workspace(c, m, batch);
+        Ints I = ints_of(c);
+        cudaStream_t s = c->stream;
+        // inputs: pinned staging → device
+        char* pin = static_cast<char*>(c->pin);
+        int32_t* pin_in = reinterpret_cast<int32_t*>(pin);
+        std::memcpy(pin_in, input_tokens, (size_t)batch * 4);
+        std::memcpy(pin_in + batch, slot_ids, (size_t)batch * 4);
+        std::memcpy(pin_in + 2 * batch, positions, (size_t)batch * 4);
+        EEB_CUDA(cudaMemcpyAsync(I.tok, pin_in, (size_t)batch * 4, cudaMemcpyHostToDevice, s));
+        EEB_CUDA(cudaMemcpyAsync(I.slot, pin_in + batch, (size_t)batch * 4, cudaMemcpyHostToDevice, s));
+        EEB_CUDA(cudaMemcpyAsync(I.pos, pin_in + 2 * batch, (size_t)batch * 4, cudaMemcpyHostToDevice, s));
+        run_step(c, model, depth, policy, th, batch);
+        // outputs: device → pinned staging → caller
+        char* po = pin + (size_t)batch * 12 + 256;
+        po = reinterpret_cast<char*>(((uintptr_t)po + 255) & ~(uintptr_t)255);
+        struct Item { void* dst; const void* src; size_t bytes; };
+        std::vector<Item> items;
+        const int ne = m.desc.n_exits;
+        if (out) {
+            auto add = [&](void* dst, const DevBuf& src, size_t bytes) {
+                if (dst) items.push_back({dst, src.p, bytes});
+            };
+            add(out->exit_layer, c->o_exit, (size_t)batch * 4);
+            add(out->token_id, c->o_tok, (size_t)batch * 4);
+            add(out->confidence, c->o_conf, (size_t)batch * 4);
+            add(out->logprob, c->o_logp, (size_t)batch * 4);
+            add(out->breached, c->o_breach, (size_t)batch);
+            add(out->unchanged, c->o_unch, (size_t)batch);
+            add(out->hist, c->o_hist, (size_t)ne * 8);
+            add(out->n_breached, c->o_nbr, 8);
+            add(out->sum_logprob, c->o_sum, 8);
+            if (policy == EEB_PROFILE) {
+                add(out->head_token, c->o_htok, (size_t)batch * ne * 4);
+                add(out->head_confidence, c->o_hconf, (size_t)batch * ne * 4);
+                add(out->head_logprob, c->o_hlogp, (size_t)batch * ne * 4);
+            }
+        }
+        std::vector<char*> staged;
+        for (auto& it : items) {
+            staged.push_back(po);
+            EEB_CUDA(cudaMemcpyAsync(po, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
+            po += (it.bytes + 255) & ~(size_t)255;
+        }
+        EEB_CUDA(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < items.size(); ++k) std::memcpy(items[k].dst, staged[k], items[k].bytes);
+        harvest_profile(c);
+    });
+}
+
+eeb_status eeb_decode_step_device(eeb_ctx* c, int model, int depth, int policy, float th, int32_t batch,
+                                  const int32_t* d_slot, const int32_t* d_tok, const int32_t* d_pos,
+                                  eeb_step_out* d_out) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (!d_slot || !d_tok || !d_pos) throw Error(EEB_E_DOMAIN, "null input array");
+        check_step_args(c, m, depth, policy, th, batch);
+        EEB_CUDA(cudaSetDevice(c->device));
+        ensure_workspace(c, m, batch);
+        Ints I = ints_of(c);
+        cudaStream_t s = c->stream;
+        EEB_CUDA(cudaMemcpyAsync(I.tok, d_tok, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
+        EEB_CUDA(cudaMemcpyAsync(I.slot, d_slot, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
+        EEB_CUDA(cudaMemcpyAsync(I.pos, d_pos, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
+        run_step(c, model, depth, policy, th, batch);
+        if (d_out) {
+            const int ne = m.desc.n_exits;
+            auto cp = [&](void* dst, const DevBuf& src, size_t bytes) {
+                if (dst) EEB_CUDA(cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDeviceToDevice, s));
+            };
+            cp(d_out->exit_layer, c->o_exit, (size_t)batch * 4);
+            cp(d_out->token_id, c->o_tok, (size_t)batch * 4);
+            cp(d_out->confidence, c->o_conf, (size_t)batch * 4);
+            cp(d_out->logprob, c->o_logp, (size_t)batch * 4);
+            cp(d_out->breached, c->o_breach, (size_t)batch);
+            cp(d_out->unchanged, c->o_unch, (size_t)batch);
+            cp(d_out->hist, c->o_hist, (size_t)ne * 8);
+            cp(d_out->n_breached, c->o_nbr, 8);
+            cp(d_out->sum_logprob, c->o_sum, 8);
+            if (policy == EEB_PROFILE) {
+                cp(d_out->head_token, c->o_htok, (size_t)batch * ne * 4);
+                cp(d_out->head_confidence, c->o_hconf, (size_t)batch * ne * 4);
+                cp(d_out->head_logprob, c->o_hlogp, (size_t)batch * ne * 4);
+            }
+        }
+        if (c->profiling) harvest_profile(c);
+    });
+}
+
+eeb_status eeb_synchronize(eeb_ctx* c) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+eeb_status eeb_set_graphs(eeb_ctx* c, int enable) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        c->graphs_enabled = enable ? 1 : 0;
+    });
+}
+
+eeb_status eeb_set_gemm_tier(eeb_ctx* c, int tier) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        if (tier < 0 || tier > 2) throw Error(EEB_E_DOMAIN, "tier must be 0, 1 or 2");
+        c->gemm_tier = tier;
+    });
+}
+
+eeb_status eeb_debug_retain_logits(eeb_ctx* c, int enable) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        c->retain_logits = enable ? 1 : 0;
+        for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
+        c->graphs.clear();
+    });
+}
+
+eeb_status eeb_debug_last_logits(eeb_ctx* c, int head, float* host_out, int64_t n) {
+    return guarded([&] {
+        if (!c || !host_out) throw Error(EEB_E_DOMAIN, "null argument");
+        if (head < 0 || head >= (int)c->logits_keep.size() || !c->logits_keep[head]->p)
+            throw Error(EEB_E_STALE, "no logits retained for that head");
+        if ((size_t)n * 4 > c->logits_keep[head]->bytes) throw Error(EEB_E_DOMAIN, "n too large");
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        EEB_CUDA(cudaMemcpy(host_out, c->logits_keep[head]->p, (size_t)n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+eeb_status eeb_debug_read_weight(eeb_ctx* c, int model, int tensor, int layer, int64_t offset, int64_t n,
+                                 float* host_out) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const void* src = nullptr;
+        size_t esz = m.wbytes;
+        size_t total = 0;
+        if (tensor >= 100) {  // base: 100 = embedding, 200+e = head e, 300+e = head norm e
+            if (m.loaded == 0) throw Error(EEB_E_STALE, "model not loaded");
+            if (tensor == 100) { src = m.emb.p; total = m.emb.bytes; }
+            else if (tensor >= 300) { src = m.head_norm.at(tensor - 300)->p; esz = 4; total = m.head_norm.at(tensor - 300)->bytes; }
+            else { src = m.head.at(tensor - 200)->p; total = m.head.at(tensor - 200)->bytes; }
+        } else {
+            if (layer < 1 || layer > m.loaded) throw Error(EEB_E_STALE, "layer not resident");
+            const LayerWeights& W = *m.layers[layer - 1];
+            const DevBuf* b = nullptr;
+            switch (tensor) {
+                case synth::kAttnNorm: b = &W.attn_norm; esz = 4; break;
+                case synth::kMlpNorm: b = &W.mlp_norm; esz = 4; break;
+                case synth::kWqkv: b = &W.wqkv; break;
+                case synth::kWo: b = &W.wo; break;
+                case synth::kWup: b = &W.wup; break;
+                case synth::kWdown: b = &W.wdown; break;
+                default: throw Error(EEB_E_DOMAIN, "unknown tensor");
+            }
+            src = b->p;
+            total = b->bytes;
+        }
+        if (offset < 0 || n < 0 || (size_t)(offset + n) * esz > total) throw Error(EEB_E_DOMAIN, "range outside tensor");
+        std::vector<char> tmp((size_t)n * esz);
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        EEB_CUDA(cudaMemcpy(tmp.data(), static_cast<const char*>(src) + (size_t)offset * esz, tmp.size(),
+                            cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) {
+            if (esz == 4) std::memcpy(&host_out[i], &tmp[(size_t)i * 4], 4);
+            else {
+                uint16_t h;
+                std::memcpy(&h, &tmp[(size_t)i * 2], 2);
+                uint32_t u = (uint32_t)h << 16;
+                std::memcpy(&host_out[i], &u, 4);
+            }
+        }
+    });
+}
+
+eeb_status eeb_debug_read_kv(eeb_ctx* c, int model, int layer, int slot, int pos, float* host_k, float* host_v) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const eeb_model_desc& d = m.desc;
+        if (layer < 1 || layer > d.num_layers || slot < 0 || slot >= d.max_slots || pos < 0 || pos >= d.max_seq_len)
+            throw Error(EEB_E_DOMAIN, "kv coordinate out of range");
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        const int hd = m.head_dim;
+        std::vector<char> tmp((size_t)hd * m.wbytes);
+        for (int g = 0; g < d.n_kv_heads; ++g) {
+            const size_t off = (size_t)(layer - 1) * m.kv_layer_elems +
+                               (((size_t)slot * d.n_kv_heads + g) * d.max_seq_len + pos) * hd;
+            for (int which = 0; which < 2; ++which) {
+                const DevBuf& b = which == 0 ? m.k_cache : m.v_cache;
+                float* dst = (which == 0 ? host_k : host_v) + (size_t)g * hd;
+                if (!dst) continue;
+                EEB_CUDA(cudaMemcpy(tmp.data(), static_cast<const char*>(b.p) + off * m.wbytes, tmp.size(),
+                                    cudaMemcpyDeviceToHost));
+                for (int j = 0; j < hd; ++j) {
+                    if (m.wbytes == 4) std::memcpy(&dst[j], &tmp[(size_t)j * 4], 4);
+                    else {
+                        uint16_t h;
+                        std::memcpy(&h, &tmp[(size_t)j * 2], 2);
+                        uint32_t u = (uint32_t)h << 16;
+                        std::memcpy(&dst[j], &u, 4);
+                    }
+                }
+            }
+        }
+    });
+}
+
+eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int batch, int mode, const void* w_host,
+                          const void* x_host, float* y_host) {
+    return guarded([&] {
+        if (!c || !w_host || !x_host || !y_host) throw Error(EEB_E_DOMAIN, "null argument");
+        if (n <= 0 || k <= 0 || batch <= 0 || batch > 1024 || mode < 0 || mode > 3 || (mode == 3 && n % 2))
+            throw Error(EEB_E_DOMAIN, "bad gemm shape");
+        EEB_CUDA(cudaSetDevice(c->device));
+        const size_t es = dtype == EEB_BF16 ? 2 : 4;
+        const int n_out = mode == kSwigluAct ? n / 2 : n;
+        DevBuf w, x, y, act, ws, na;
+        w.ensure((size_t)n * k * es);
+        x.ensure((size_t)batch * k * es);
+        y.ensure((size_t)batch * n * 4);
+        act.ensure((size_t)batch * n_out * es);
+        const int64_t ws_elems = (int64_t)(k / 64 + 2) * batch * n;
+        ws.ensure((size_t)ws_elems * 4);
+        na.ensure(4);
+        EEB_CUDA(cudaMemcpy(w.p, w_host, w.bytes, cudaMemcpyHostToDevice));
+        EEB_CUDA(cudaMemcpy(x.p, x_host, x.bytes, cudaMemcpyHostToDevice));
+        EEB_CUDA(cudaMemset(y.p, 0, y.bytes));
+        EEB_CUDA(cudaMemcpy(na.p, &batch, 4, cudaMemcpyHostToDevice));
+        GemmArgs a;
+        a.dtype = dtype; a.W = w.p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
+        a.mode = mode; a.out_f32 = y.as<float>(); a.out_act = act.p; a.ldo = n; a.workspace = ws.as<float>();
+        a.workspace_elems = ws_elems; a.num_sms = c->num_sms;
+        if (tier == 2) {
+            if (gemm_tc(a, c->stream) == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
+        } else {
+            gemm_cc(a, c->stream);
+        }
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        if (mode <= kResidAdd) {
+            EEB_CUDA(cudaMemcpy(y_host, y.p, (size_t)batch * n * 4, cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<char> tmp((size_t)batch * n_out * es);
+            EEB_CUDA(cudaMemcpy(tmp.data(), act.p, tmp.size(), cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < (size_t)batch * n_out; ++i) {
+                if (es == 4) std::memcpy(&y_host[i], &tmp[i * 4], 4);
+                else {
+                    uint16_t h;
+                    std::memcpy(&h, &tmp[i * 2], 2);
+                    const uint32_t u = (uint32_t)h << 16;
+                    std::memcpy(&y_host[i], &u, 4);
+                }
+            }
+        }
+    });
+}
+
+eeb_status eeb_profile_enable(eeb_ctx* c, int enable) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        c->profiling = enable ? 1 : 0;
+        for (int k = 0; k < kNumCat; ++k) { c->cat_ms[k] = 0; c->cat_launches[k] = 0; }
+        c->steps_profiled = 0;
+    });
+}
+
+eeb_status eeb_profile_read(eeb_ctx* c, char* json_out, int64_t cap) {
+    return guarded([&] {
+        if (!c || !json_out) throw Error(EEB_E_DOMAIN, "null argument");
+        std::string j = "{\"steps\": " + std::to_string(c->steps_profiled) + ", \"last_step_launches\": " +
+                        std::to_string(c->step_launches);
+        for (int k = 0; k < kNumCat; ++k) {
+            char buf[160];
+            std::snprintf(buf, sizeof buf, ", \"%s_ms\": %.6f, \"%s_launches\": %lld", kCatNames[k], c->cat_ms[k],
+                          kCatNames[k], (long long)c->cat_launches[k]);
+            j += buf;
+        }
+        j += "}";
+        if ((int64_t)j.size() + 1 > cap) throw Error(EEB_E_DOMAIN, "buffer too small");
+        std::memcpy(json_out, j.c_str(), j.size() + 1);
+    });
+}
+
+void* eeb_stream(eeb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+eeb_status eeb_nccl_unique_id(uint8_t* id128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        if (nccl().get_unique_id(&id) != ncclSuccess) throw Error(EEB_E_CUDA, "ncclGetUniqueId failed");
+        std::memcpy(id128, id.internal, 128);
+    });
+}
+
+eeb_status eeb_nccl_init(eeb_ctx* c, const uint8_t* id128, int nranks, int rank) {
+    return guarded([&] {
+        if (!c || !id128) throw Error(EEB_E_DOMAIN, "null argument");
+        EEB_CUDA(cudaSetDevice(c->device));
+        ncclUniqueId id;
+        std::memcpy(id.internal, id128, 128);
+        ncclResult_t r = nccl().comm_init_rank(&c->nccl, nranks, id, rank);
+        if (r != ncclSuccess) throw Error(EEB_E_CUDA, std::string("ncclCommInitRank: ") + nccl().error_string(r));
+    });
+}
+
+eeb_status eeb_profile_allreduce(eeb_ctx* c, int64_t* counters, int n, double* sum_neg_logprob) {
+    return guarded([&] {
+        if (!c || !c->nccl) throw Error(EEB_E_STALE, "NCCL communicator not initialised");
+        if (n < 0 || (n > 0 && !counters)) throw Error(EEB_E_DOMAIN, "bad counter array");
+        c->nccl_buf.ensure((size_t)n * 8 + 8);
+        int64_t* dc = c->nccl_buf.as<int64_t>();
+        double* dd = reinterpret_cast<double*>(dc + n);
+        if (n) EEB_CUDA(cudaMemcpyAsync(dc, counters, (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
+        if (sum_neg_logprob) EEB_CUDA(cudaMemcpyAsync(dd, sum_neg_logprob, 8, cudaMemcpyHostToDevice, c->stream));
+        const NcclApi& api = nccl();
+        api.group_start();
+        if (n) api.all_reduce(dc, dc, n, ncclInt64, ncclSum, c->nccl, c->stream);
+        if (sum_neg_logprob) api.all_reduce(dd, dd, 1, ncclFloat64, ncclSum, c->nccl, c->stream);
+        ncclResult_t r = api.group_end();
+        if (r != ncclSuccess) throw Error(EEB_E_CUDA, std::string("ncclAllReduce: ") + api.error_string(r));
+        if (n) EEB_CUDA(cudaMemcpyAsync(counters, dc, (size_t)n * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (sum_neg_logprob) EEB_CUDA(cudaMemcpyAsync(sum_neg_logprob, dd, 8, cudaMemcpyDeviceToHost, c->stream));
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+// gemm_cc.cu — tier-1 decode GEMM on CUDA cores: y[B, N] = x[B, K] · W[N, K]^T.
+//
+// Weight-streaming: every weight element is read exactly once per launch with
+// 16-byte non-allocating loads; the activation slice [B, KS] is staged in
+// shared memory and reused across the CTA's output rows.  Split-K fills the
+// 148 SMs when N is small; partials are summed in a fixed order by the
+// epilogue kernel (deterministic — no atomics feed the logits, SURVEY §7
+// hard part 2).  This tier serves small batches and the f32 parity model; the
+// tcgen05 tier (gemm_tc.cu) takes over for bf16 once B >= 16.
+#include "kernels.h"
+
+namespace eeb {
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kRowsPerWarp = 2;
+constexpr int kRowsPerCta = kWarps * kRowsPerWarp;
+
+template <typename T, int MAXB>
+__global__ void __launch_bounds__(kWarps * 32)
+    gemm_cc_kernel(const T* __restrict__ W, const T* __restrict__ X, const int* __restrict__ n_active,
+                   float* __restrict__ part, int N, int K, int KS, int64_t split_stride) {
+    constexpr int VEC = Vec16<T>::N;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* xs = reinterpret_cast<T*>(smem_raw);  // [MAXB][KS]
+
+    const int nb = min(*n_active, MAXB);
+    if (nb <= 0) return;
+    const int k0 = blockIdx.y * KS;
+    const int kn = min(KS, K - k0);
+
+    // Stage the activation slice.
+    const int vec_per_row = kn / VEC;
+    for (int idx = threadIdx.x; idx < nb * vec_per_row; idx += blockDim.x) {
+        const int b = idx / vec_per_row, v = idx % vec_per_row;
+        reinterpret_cast<uint4*>(xs + b * KS)[v] =
+            *reinterpret_cast<const uint4*>(X + (int64_t)b * K + k0 + v * VEC);
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * kRowsPerCta + warp * kRowsPerWarp;
+    float acc[kRowsPerWarp][MAXB];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) acc[r][b] = 0.f;
+
+    const T* wrow[kRowsPerWarp];
+    bool rvalid[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+        rvalid[r] = (n0 + r) < N;
+        wrow[r] = W + (int64_t)(rvalid[r] ? n0 + r : 0) * K + k0;
+    }
+
+    for (int kk = lane * VEC; kk < kn; kk += 32 * VEC) {
+        float w[kRowsPerWarp][VEC];
+#pragma unroll
+        for (int r = 0; r < kRowsPerWarp; ++r) {
+            const uint4 u = ldg_stream(wrow[r] + kk);
+            unpack16(u, w[r], (const T*)nullptr);
+        }
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+            if (b < nb) {
+                float xv[VEC];
+                unpack16(*reinterpret_cast<const uint4*>(xs + b * KS + kk), xv, (const T*)nullptr);
+#pragma unroll
+                for (int r = 0; r < kRowsPerWarp; ++r) {
+                    float a = acc[r][b];
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) a = fmaf(w[r][j], xv[j], a);
+                    acc[r][b] = a;
+                }
+            }
+        }
+    }
+
+    float* out = part + blockIdx.y * split_stride;
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+            if (b < nb) {
+                const float v = warp_sum(acc[r][b]);
+                if (lane == 0 && rvalid[r]) out[(int64_t)b * N + n0 + r] = v;
+            }
+        }
+    }
+}
+
+template <typename T>
+__global__ void splitk_epilogue_kernel(const float* __restrict__ part, int splits,
+                                       int64_t split_stride, const int* __restrict__ n_active,
+                                       int N, int mode, float* __restrict__ out_f32, int ldo,
+                                       T* __restrict__ out_act) {
+    const int n_out = mode == kSwigluAct ? N / 2 : N;
+    const int rows = *n_active;
+    const int64_t total = (int64_t)rows * n_out;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n_out), n = (int)(idx % n_out);
+        if (mode == kSwigluAct) {
+            float g = 0.f, u = 0.f;
+            for (int s = 0; s < splits; ++s) {
+                g += part[s * split_stride + (int64_t)i * N + 2 * n];
+                u += part[s * split_stride + (int64_t)i * N + 2 * n + 1];
+            }
+            const float silu = g / (1.f + __expf(-g));
+            out_act[(int64_t)i * n_out + n] = from_f32<T>(silu * u);
+        } else {
+            float y = 0.f;
+            for (int s = 0; s < splits; ++s) y += part[s * split_stride + (int64_t)i * N + n];
+            if (mode == kStoreF32) out_f32[(int64_t)i * ldo + n] = y;
+            else if (mode == kResidAdd) out_f32[(int64_t)i * ldo + n] += y;
+            else out_act[(int64_t)i * n_out + n] = from_f32<T>(fmaxf(y, 0.f));
+        }
+    }
+}
+
+template <typename T, int MAXB>
+void run_cc(const GemmArgs& a, cudaStream_t s) {
+    constexpr int VEC = Vec16<T>::N;
+    const int tiles = (a.N + kRowsPerCta - 1) / kRowsPerCta;
+    // Split K until the grid covers ~2 waves, keeping KS a multiple of 32*VEC
+    // and the staged slice within 96 KB of shared memory.
+    int splits = 1;
+    const int kmin = 32 * VEC;
+    auto ks_of = [&](int sp) {
+        int ks = (a.K + sp - 1) / sp;
+        return (ks + kmin - 1) / kmin * kmin;
+    };
+    while (true) {
+        const int ks = ks_of(splits);
+        const bool smem_ok = (int64_t)ks * MAXB * (int)sizeof(T) <= 96 * 1024;
+        const bool occ_ok = (int64_t)tiles * splits >= 2LL * a.num_sms;
+        if (smem_ok && (occ_ok || ks <= kmin)) break;
+        if (ks <= kmin) break;
+        ++splits;
+    }
+    const int KS = ks_of(splits);
+    splits = (a.K + KS - 1) / KS;
+    const int64_t split_stride = (int64_t)a.max_rows * a.N;
+    if ((int64_t)splits * split_stride > a.workspace_elems)
+        throw Error(2, "gemm_cc: split-K workspace too small");
+    const size_t smem = (size_t)KS * MAXB * sizeof(T);
+    auto kern = gemm_cc_kernel<T, MAXB>;
+    EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid(tiles, splits);
+    kern<<<grid, kWarps * 32, smem, s>>>(static_cast<const T*>(a.W), static_cast<const T*>(a.X),
+                                         a.n_active, a.workspace, a.N, a.K, KS, split_stride);
+    EEB_CHECK_LAUNCH();
+    const int n_out = a.mode == kSwigluAct ? a.N / 2 : a.N;
+    int64_t blocks = ((int64_t)a.max_rows * n_out + 255) / 256;
+    if (blocks > a.num_sms * 16) blocks = a.num_sms * 16;
+    splitk_epilogue_kernel<T><<<(int)blocks, 256, 0, s>>>(a.workspace, splits, split_stride,
+                                                          a.n_active, a.N, a.mode, a.out_f32, a.ldo,
+                                                          static_cast<T*>(a.out_act));
+    EEB_CHECK_LAUNCH();
+}
+
+template <typename T>
+void dispatch_cc(const GemmArgs& a, cudaStream_t s) {
+    if (a.K % (32 * Vec16<T>::N) != 0) throw Error(1, "gemm_cc: K must be a multiple of 32 vectors");
+    const int b = a.max_rows;
+    if (b <= 1) run_cc<T, 1>(a, s);
+    else if (b <= 2) run_cc<T, 2>(a, s);
+    else if (b <= 4) run_cc<T, 4>(a, s);
+    else if (b <= 8) run_cc<T, 8>(a, s);
+    else if (b <= 16) run_cc<T, 16>(a, s);
+    else if (b <= 32) run_cc<T, 32>(a, s);
+    else if (b <= 64) run_cc<T, 64>(a, s);
+    else throw Error(1, "gemm_cc: batch > 64 needs the tensor-core tier or row chunking");
+}
+
+}  // namespace
+
+void splitk_epilogue(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
+                     int max_rows, int N, int mode, float* out_f32, int ldo, void* out_act, int num_sms,
+                     cudaStream_t s) {
+    const int n_out = mode == kSwigluAct ? N / 2 : N;
+    int64_t blocks = ((int64_t)max_rows * n_out + 255) / 256;
+    if (blocks > num_sms * 16) blocks = num_sms * 16;
+    if (dtype == 0)
+        splitk_epilogue_kernel<float><<<(int)blocks, 256, 0, s>>>(part, splits, split_stride, n_active, N, mode,
+                                                                  out_f32, ldo, static_cast<float*>(out_act));
+    else
+        splitk_epilogue_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>(
+            part, splits, split_stride, n_active, N, mode, out_f32, ldo, static_cast<__nv_bfloat16*>(out_act));
+    EEB_CHECK_LAUNCH();
+}
+
+void gemm_cc(const GemmArgs& a, cudaStream_t s) {
+    if (a.dtype == 0) dispatch_cc<float>(a, s);
+    else dispatch_cc<__nv_bfloat16>(a, s);
+}
+
+}  // namespace eeb

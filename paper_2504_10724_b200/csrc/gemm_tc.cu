@@ -1,0 +1,339 @@
+// gemm_tc.cu — tier-2 decode GEMM on the 5th-generation tensor cores.
+//
+// y[B, N] = x[B, K] · W[N, K]^T for bf16 weights once the batch makes the
+// weight stream a dense contraction (B >= 16: 2·B flop per weight byte
+// outruns the CUDA cores, SURVEY §7 hard part 6).  Swap-AB: the weight tile is
+// the MMA's M operand (128 output features), the batch is its N operand, so a
+// [128 x B] f32 accumulator lives in TMEM and one tcgen05.mma
+// (M=128, N=B, K=16) consumes a 128 x 16 weight slice.
+//
+// Warp roles (192 threads, one CTA per SM):
+//   warp 0      TMA producer: weight tile [128 x 64] + activation tile [B x 64]
+//               per stage, 128B-swizzled, arriving on the stage's mbarrier;
+//   warp 1      TMEM allocator + single-thread MMA issuer; tcgen05.commit
+//               frees a stage and, after the last k-block, signals the epilogue;
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (thread = output feature), fused
+//               residual-add / ReLU / SwiGLU / f32 store, or split-K partials.
+// Split-K spreads small N over the 148 SMs; partials are reduced in a fixed
+// order by splitk_epilogue (deterministic, no atomics).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "kernels.h"
+
+namespace eeb {
+
+namespace {
+
+constexpr int kBM = 128;           // output features per tile (UMMA M)
+constexpr int kBK = 64;            // K per stage: one 128-byte swizzle atom of bf16
+constexpr int kThreads = 192;
+constexpr int kSmemBudget = 227 * 1024;
+
+// ---- PTX wrappers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128B-swizzled shared-memory matrix descriptor (rows of 128 B,
+// 8-row atoms 1024 B apart).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);  // start address
+    d |= (uint64_t)1 << 16;                    // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+    return d;
+}
+// Instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major.
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcParams {
+    int N, K;
+    int kb_per;        // k-blocks per split
+    int kblocks;       // total k-blocks
+    int bpad;          // UMMA N (batch rows, multiple of 16)
+    int stages;
+    int tmem_cols;
+    int mode;          // EpilogueMode, or -1 = split-K partials
+    const int* n_active;
+    float* out_f32;
+    __nv_bfloat16* out_act;
+    int ldo;
+    float* part;
+    int64_t split_stride;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+                   TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B-swizzle atoms.
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* base_ptr = smem_raw + (base - raw);
+    const int S = p.stages;
+    const uint32_t a_bytes = kBM * kBK * 2;
+    const uint32_t b_bytes = (uint32_t)p.bpad * kBK * 2;
+    const uint32_t stage_bytes = a_bytes + b_bytes;
+    // barriers + tmem slot after the tiles
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base_ptr + (size_t)S * stage_bytes);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S), tfull = smem_u32(bars + 2 * S);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tile = blockIdx.x, split = blockIdx.y;
+    const int kb0 = split * p.kb_per;
+    const int kb1 = min(kb0 + p.kb_per, p.kblocks);
+    const int nkb = kb1 - kb0;
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&tmap_w);
+        prefetch_tmap(&tmap_x);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"((uint32_t)p.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % S;
+                const uint32_t ph = (uint32_t)(i / S) & 1u;
+                mbar_wait(empty0 + 8 * s, ph ^ 1u);
+                const uint32_t sa = base + (uint32_t)s * stage_bytes;
+                mbar_expect_tx(full0 + 8 * s, stage_bytes);
+                const int kc = (kb0 + i) * kBK;
+                tma_load_2d(sa, &tmap_w, full0 + 8 * s, kc, m_tile * kBM, pol_w);
+                tma_load_2d(sa + a_bytes, &tmap_x, full0 + 8 * s, kc, 0, pol_x);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = instr_desc(kBM, p.bpad);
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % S;
+                const uint32_t ph = (uint32_t)(i / S) & 1u;
+                mbar_wait(full0 + 8 * s, ph);
+                tc_fence_after();
+                const uint32_t sa = base + (uint32_t)s * stage_bytes;
+                const uint64_t da = smem_desc(sa), db = smem_desc(sa + a_bytes);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
+                    umma(tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (i | k) != 0);
+                umma_commit(empty0 + 8 * s);
+            }
+            umma_commit(tfull);
+        }
+    } else {
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31  (thread = output feature)
+        const int quarter = warp & 3;
+        const int n = m_tile * kBM + quarter * 32 + lane;
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        const int rows = *p.n_active;
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
+        for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)c0, v);
+            if (c0 >= rows) continue;  // (uniform) tcgen05.ld stays warp-collective
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int b = c0 + j;
+                const bool ok = b < rows && n < p.N;
+                float y = v[j];
+                if (p.mode < 0) {
+                    if (ok) p.part[(int64_t)split * p.split_stride + (int64_t)b * p.N + n] = y;
+                } else if (p.mode == kStoreF32) {
+                    if (ok) p.out_f32[(int64_t)b * p.ldo + n] = y;
+                } else if (p.mode == kResidAdd) {
+                    if (ok) p.out_f32[(int64_t)b * p.ldo + n] += y;
+                } else if (p.mode == kReluAct) {
+                    if (ok) p.out_act[(int64_t)b * p.N + n] = __float2bfloat16_rn(fmaxf(y, 0.f));
+                } else {  // SwiGLU: even lane = gate, odd lane = up
+                    const float u = __shfl_down_sync(0xffffffffu, y, 1);
+                    if (ok && (n & 1) == 0) {
+                        const float silu = y / (1.f + __expf(-y));
+                        p.out_act[(int64_t)b * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu * u);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)p.tmem_cols));
+    }
+}
+
+// ---- host side -----------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+CUtensorMap make_map(const void* ptr, int rows, int cols, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(5, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+}  // namespace
+
+void splitk_epilogue(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
+                     int max_rows, int N, int mode, float* out_f32, int ldo, void* out_act, int num_sms,
+                     cudaStream_t s);
+
+bool gemm_tc_available() { return encode_fn() != nullptr; }
+
+int gemm_tc(const GemmArgs& a, cudaStream_t s) {
+    if (a.dtype != 1 || a.max_rows < 16 || a.max_rows > 256 || a.K % kBK != 0) return 0;
+    if (!gemm_tc_available()) return 0;
+    const int bpad = (a.max_rows + 15) / 16 * 16;
+    const int tiles = (a.N + kBM - 1) / kBM;
+    const int kblocks = a.K / kBK;
+    // split K so the grid covers the SMs once, keeping >= 2 k-blocks per CTA
+    int splits = std::max(1, std::min(kblocks / 2, a.num_sms / tiles));
+    const int kb_per = (kblocks + splits - 1) / splits;
+    splits = (kblocks + kb_per - 1) / kb_per;
+    const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
+    int stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
+    stages = std::min(stages, std::max(2, kb_per));
+    if (stages < 2) return 0;
+    int tmem_cols = 32;
+    while (tmem_cols < bpad) tmem_cols *= 2;
+
+    TcParams p;
+    p.N = a.N;
+    p.K = a.K;
+    p.kb_per = kb_per;
+    p.kblocks = kblocks;
+    p.bpad = bpad;
+    p.stages = stages;
+    p.tmem_cols = tmem_cols;
+    p.n_active = a.n_active;
+    p.out_f32 = a.out_f32;
+    p.out_act = static_cast<__nv_bfloat16*>(a.out_act);
+    p.ldo = a.ldo;
+    p.split_stride = (int64_t)a.max_rows * a.N;
+    if (splits > 1) {
+        if ((int64_t)splits * p.split_stride > a.workspace_elems) return 0;
+        p.mode = -1;
+        p.part = a.workspace;
+    } else {
+        p.mode = a.mode;
+        p.part = nullptr;
+    }
+    const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
+    const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
+    const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
+    EEB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid(tiles, splits);
+    gemm_tc_kernel<<<grid, kThreads, smem, s>>>(mw, mx, p);
+    EEB_CHECK_LAUNCH();
+    if (splits > 1) {
+        splitk_epilogue(a.dtype, a.workspace, splits, p.split_stride, a.n_active, a.max_rows, a.N, a.mode,
+                        a.out_f32, a.ldo, a.out_act, a.num_sms, s);
+        return 2;
+    }
+    return 1;
+}
+
+}  // namespace eeb
