@@ -1,0 +1,232 @@
+// eeserve/backend.hpp — where the decode step gets its exit-head verdicts.
+//
+// In the reference, Simulator::serve_one reads them from the trace
+// (`tok.for_model(model)`, /root/reference/proj/include/eeserve/engine.hpp:345)
+// and applies the token policy (:349-366).  Here that seam is an interface:
+//   * CudaBackend  — the B200 decode step through the C ABI (include/eeb/eeb.h);
+//   * TraceBackend — replays reference-format ModelTokenRecords (exactly the
+//                    reference's semantics; used to cross-check the engine).
+// Both return, per row, the observation the policy picked plus the
+// breached / unchanged flags, and the step's exit histogram.
+#pragma once
+
+#include <chrono>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "eeb/eeb.h"
+#include "eeserve/model_spec.hpp"
+#include "eeserve/trace.hpp"
+
+namespace eeserve {
+
+/// ↔ Simulator::TokenPolicy (engine.hpp:156) + the all-heads profiling pass.
+enum class TokenPolicy { flat = EEB_FLAT, introspective = EEB_INTROSPECTIVE, full_depth = EEB_FULL_DEPTH,
+                         profile = EEB_PROFILE };
+
+struct StepRows {
+    std::vector<int32_t> slots, tokens, positions;
+    std::vector<std::int64_t> request_ids;  // trace backend: which request...
+    std::vector<int32_t> token_index;       // ...and which of its tokens
+    int size() const { return (int)slots.size(); }
+};
+
+struct StepOutcome {
+    std::vector<ExitObservation> obs;      // per row: the observation the policy used
+    std::vector<int> exit_layer;           // per row (flat: the serving depth)
+    std::vector<uint8_t> breached, unchanged;  // unchanged: 1/0, 2 = unknown
+    std::vector<std::int64_t> hist;        // per exit head
+    std::int64_t n_breached = 0;
+    double sum_logprob = 0.0;
+    std::vector<ModelTokenRecord> records;  // profile policy: every head per row
+    double seconds = 0.0;                   // measured step wall time
+};
+
+class DecodeBackend {
+public:
+    virtual ~DecodeBackend() = default;
+    virtual void register_model(const ModelSpec& spec, int max_slots, int max_seq_len) = 0;
+    /// Greedy loader ↔ do_load (engine.hpp:197-216): make layers [1, depth] resident.
+    virtual void load(const std::string& model, int depth) = 0;
+    virtual StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
+                             const StepRows& rows) = 0;
+};
+
+// ---------------------------------------------------------------------------
+// CUDA backend (C ABI).
+// ---------------------------------------------------------------------------
+class CudaBackend final : public DecodeBackend {
+public:
+    explicit CudaBackend(int device = 0) { throw_if_error(eeb_create(device, &ctx_), "eeb_create"); }
+    ~CudaBackend() override { eeb_destroy(ctx_); }
+    CudaBackend(const CudaBackend&) = delete;
+    CudaBackend& operator=(const CudaBackend&) = delete;
+
+    void register_model(const ModelSpec& spec, int max_slots, int max_seq_len) override {
+        const Architecture& a = spec.arch;
+        eeb_model_desc d{};
+        d.num_layers = spec.num_layers;
+        d.d_model = a.d_model;
+        d.n_heads = a.n_heads;
+        d.n_kv_heads = a.n_kv_heads;
+        d.d_ffn = a.d_ffn;
+        d.vocab = a.vocab;
+        d.n_exits = (int32_t)spec.exit_layers.size();
+        std::vector<int32_t> exits(spec.exit_layers.begin(), spec.exit_layers.end());
+        d.exit_layers = exits.data();
+        d.exit_coverage = a.exit_coverage.empty() ? nullptr : a.exit_coverage.data();
+        d.design_th = a.design_th;
+        d.dtype = a.dtype;
+        d.mlp_kind = a.mlp_kind;
+        d.max_slots = max_slots;
+        d.max_seq_len = max_seq_len;
+        d.seed = a.seed;
+        int h = -1;
+        throw_if_error(eeb_model_register(ctx_, &d, &h), "eeb_model_register");
+        handles_[spec.id] = {h, spec};
+    }
+
+    void load(const std::string& model, int depth) override {
+        throw_if_error(eeb_load_layers(ctx_, handle(model).h, depth), "eeb_load_layers");
+    }
+
+    StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
+                     const StepRows& rows) override {
+        const Entry& e = handle(model);
+        const int b = rows.size(), ne = (int)e.spec.exit_layers.size();
+        StepOutcome out;
+        std::vector<int32_t> exit_layer(b), tok(b);
+        std::vector<float> conf(b), logp(b);
+        out.breached.resize(b);
+        out.unchanged.resize(b);
+        out.hist.resize(ne);
+        std::vector<int32_t> htok;
+        std::vector<float> hconf, hlogp;
+        eeb_step_out o{};
+        o.exit_layer = exit_layer.data();
+        o.token_id = tok.data();
+        o.confidence = conf.data();
+        o.logprob = logp.data();
+        o.breached = out.breached.data();
+        o.unchanged = out.unchanged.data();
+        o.hist = out.hist.data();
+        o.n_breached = &out.n_breached;
+        o.sum_logprob = &out.sum_logprob;
+        if (policy == TokenPolicy::profile) {
+            htok.resize((size_t)b * ne);
+            hconf.resize((size_t)b * ne);
+            hlogp.resize((size_t)b * ne);
+            o.head_token = htok.data();
+            o.head_confidence = hconf.data();
+            o.head_logprob = hlogp.data();
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        throw_if_error(eeb_decode_step(ctx_, e.h, depth, (int)policy, (float)th, b, rows.slots.data(),
+                                       rows.tokens.data(), rows.positions.data(), &o),
+                       "eeb_decode_step");
+        out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out.exit_layer.assign(exit_layer.begin(), exit_layer.end());
+        out.obs.resize(b);
+        for (int i = 0; i < b; ++i) {
+            // The head the policy used: its layer is the exit layer except in
+            // flat mode between heads (observation_for_depth's fallback).
+            int layer = exit_layer[i];
+            if (policy == TokenPolicy::flat) layer = observation_layer_for_depth(e.spec, depth);
+            out.obs[i] = ExitObservation{layer, tok[i], (double)conf[i], (double)logp[i]};
+        }
+        if (policy == TokenPolicy::profile) {
+            out.records.resize(b);
+            for (int i = 0; i < b; ++i) {
+                ModelTokenRecord& r = out.records[i];
+                for (int k = 0; k < ne; ++k)
+                    r.observations.push_back({e.spec.exit_layers[k], htok[(size_t)i * ne + k],
+                                              (double)hconf[(size_t)i * ne + k], (double)hlogp[(size_t)i * ne + k]});
+                r.final_token_id = r.observations.back().token_id;
+            }
+        }
+        return out;
+    }
+
+    eeb_ctx* context() const { return ctx_; }
+
+private:
+    struct Entry {
+        int h;
+        ModelSpec spec;
+    };
+    const Entry& handle(const std::string& id) const {
+        const auto it = handles_.find(id);
+        if (it == handles_.end()) throw DomainError("model '" + id + "' is not registered with the backend");
+        return it->second;
+    }
+    static int observation_layer_for_depth(const ModelSpec& spec, int depth) {
+        int best = -1;
+        for (int l : spec.exit_layers)
+            if (l <= depth) best = l;
+        if (best < 0) throw DomainError("no observation at or below layer " + std::to_string(depth));
+        return best;
+    }
+    eeb_ctx* ctx_ = nullptr;
+    std::map<std::string, Entry> handles_;
+};
+
+// ---------------------------------------------------------------------------
+// Trace backend: the reference's token oracle, batched.
+// ---------------------------------------------------------------------------
+class TraceBackend final : public DecodeBackend {
+public:
+    explicit TraceBackend(const Trace& trace) {
+        for (const auto& r : trace.requests) by_id_[r.request_id] = &r;
+    }
+    void register_model(const ModelSpec& spec, int, int) override { specs_[spec.id] = spec; }
+    void load(const std::string&, int) override {}
+
+    StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
+                     const StepRows& rows) override {
+        const ModelSpec& spec = specs_.at(model);
+        const int b = rows.size();
+        StepOutcome out;
+        out.hist.assign(spec.exit_layers.size(), 0);
+        for (int i = 0; i < b; ++i) {
+            const TraceRequest& req = *by_id_.at(rows.request_ids[i]);
+            const ModelTokenRecord& rec = req.tokens.at(rows.token_index[i]).for_model(model);
+            const ExitObservation* obs = nullptr;
+            int exit_layer = 0;
+            bool breached = false;
+            switch (policy) {
+                case TokenPolicy::flat:
+                    obs = &observation_for_depth(rec, depth);
+                    exit_layer = depth;
+                    breached = obs->confidence < th;
+                    break;
+                case TokenPolicy::full_depth:
+                    obs = &rec.observations.back();
+                    exit_layer = spec.num_layers;
+                    break;
+                default:
+                    obs = &earliest_confident_obs(rec, th);
+                    exit_layer = obs->layer;
+                    breached = obs->confidence < th;
+                    break;
+            }
+            out.obs.push_back(*obs);
+            out.exit_layer.push_back(exit_layer);
+            out.breached.push_back(breached ? 1 : 0);
+            out.unchanged.push_back(obs->token_id == rec.final_token_id ? 1 : 0);
+            out.hist[exit_index(spec.exit_layers, obs->layer)] += 1;
+            out.n_breached += breached ? 1 : 0;
+            out.sum_logprob += obs->logprob;
+            if (policy == TokenPolicy::profile) out.records.push_back(rec);
+        }
+        return out;
+    }
+
+private:
+    std::map<std::int64_t, const TraceRequest*> by_id_;
+    std::map<std::string, ModelSpec> specs_;
+};
+
+}  // namespace eeserve

@@ -1,0 +1,324 @@
+// eeserve/engine.hpp — the batched serving loop around the decode step.
+//
+// The reference's Simulator (/root/reference/proj/include/eeserve/engine.hpp:108-399)
+// serves requests one at a time (batch 1, :104-107) and reads every token's
+// exit verdicts from a trace.  BatchedEngine keeps its control flow — mode
+// dispatch (:139-151), evaluation cycles that profile every candidate at full
+// depth with the introspective rule (:243-278), replanning (:280-299), breach
+// actions queued by decide_action and applied at the next request boundary
+// (:301-323, :381-385) — but advances up to `max_batch` requests per decode
+// step through a DecodeBackend (every in-flight request
+// moves one token per step).  Metrics follow metrics.hpp:85-93: the tokens of
+// one step share one timestamp, so a step's wall time is charged once.
+//
+// With max_batch = 1 and the TraceBackend the engine reproduces the
+// reference's exit tables and breach/switch decisions (tests/cpp).
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "eeserve/backend.hpp"
+#include "eeserve/memory_model.hpp"
+#include "eeserve/pht.hpp"
+#include "eeserve/policy.hpp"
+
+namespace eeserve {
+
+enum class Mode { vanilla, ee_single, helios };
+
+struct ModeSpec {
+    Mode kind = Mode::helios;
+    std::string model;  // pinned modes
+};
+
+struct RequestSpec {
+    std::int64_t request_id = 0;
+    int prompt_len = 0;
+    int num_tokens = 0;
+};
+
+struct EngineConfig {
+    MemoryConfig mem;
+    PolicyConfig policy;
+    ModeSpec mode;
+    int max_batch = 64;
+    int max_seq_len = 256;
+    std::uint64_t token_seed = 20260819;
+    bool prefill = true;  // run the prompt through the backend (real KV); off for trace replay
+};
+
+struct EngineReport {
+    std::int64_t tokens = 0;
+    std::int64_t steps = 0;
+    double decode_wall_s = 0.0;
+    double throughput_tok_s = 0.0;
+    double perplexity = 0.0;
+    double unchanged_fraction = 0.0;  // over tokens whose final-head token is known
+    std::map<std::string, std::map<int, std::int64_t>> exit_counts;
+    std::map<std::string, std::map<int, double>> exit_table;  // percent of tokens
+    int achieved_batch_size = 0;
+    std::int64_t ld_count = 0, sw_count = 0, eval_cycles = 0;
+    std::vector<std::pair<std::string, int>> serving_history;  // (model, depth) per served batch
+    Pht pht;
+};
+
+/// Teacher-forced synthetic token for (request, position): a splitmix64 hash,
+/// the same request-keyed substream idea as the reference generator
+/// (rng.hpp:9-38, generator.hpp:319-323).
+inline int32_t synthetic_token(std::uint64_t seed, std::int64_t request_id, int position, int vocab) {
+    std::uint64_t z = seed ^ (0x9e3779b97f4a7c15ULL * (std::uint64_t)(request_id + 1)) ^
+                      (0xd1b54a32d192ed03ULL * (std::uint64_t)(position + 7));
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return (int32_t)(z % (std::uint64_t)vocab);
+}
+
+class BatchedEngine {
+public:
+    BatchedEngine(const ModelRepository& repo, DecodeBackend& backend, EngineConfig cfg)
+        : repo_(repo), be_(backend), cfg_(std::move(cfg)) {}
+
+    EngineReport run(const std::vector<RequestSpec>& reqs) {
+        validate_memory_config(cfg_.mem);
+        validate_policy_config(cfg_.policy);
+        if (cfg_.max_batch < 1) throw ValidationError("engine: max_batch must be at least 1");
+        const PolicyConfig& pol = cfg_.policy;
+        if (cfg_.mode.kind == Mode::helios) {
+            candidates_ = select_candidates(repo_, pol.slo, cfg_.mem, pol.k);
+        } else {
+            if (!repo_.has(cfg_.mode.model))
+                throw ValidationError("mode model '" + cfg_.mode.model + "' is not in the repository");
+            candidates_ = {cfg_.mode.model};
+        }
+        for (const auto& id : candidates_) be_.register_model(repo_.at(id), cfg_.max_batch, cfg_.max_seq_len);
+        if (reqs.empty()) return finish();
+        if (cfg_.mode.kind == Mode::helios) {
+            since_eval_ = pol.ri;  // evaluate before serving anything (engine.hpp:130)
+        } else {
+            serving_ = cfg_.mode.model;
+            depth_ = repo_.at(serving_).num_layers;
+            do_load(serving_, depth_, "startup");
+        }
+        const TokenPolicy tp = cfg_.mode.kind == Mode::vanilla    ? TokenPolicy::full_depth
+                               : cfg_.mode.kind == Mode::ee_single ? TokenPolicy::introspective
+                                                                   : TokenPolicy::flat;
+        while (cursor_ < reqs.size()) {
+            if (cfg_.mode.kind == Mode::helios && should_reassess(since_eval_, pol)) {
+                eval_cycle(reqs);
+                continue;
+            }
+            if (pending_) apply_pending();
+            const size_t n = std::min<size_t>(cfg_.max_batch, reqs.size() - cursor_);
+            std::vector<const RequestSpec*> batch;
+            for (size_t i = 0; i < n; ++i) batch.push_back(&reqs[cursor_ + i]);
+            cursor_ += n;
+            since_eval_ += (std::int64_t)n;
+            serve_batch(batch, serving_, depth_, tp, false);
+        }
+        return finish();
+    }
+
+private:
+    const ModelRepository& repo_;
+    DecodeBackend& be_;
+    EngineConfig cfg_;
+    std::vector<std::string> candidates_;
+    MemoryState mem_;
+    std::string serving_;
+    int depth_ = 0;
+    Pht pht_;
+    BreachTracker breach_;
+    std::optional<ActionPlan> pending_;
+    std::int64_t since_eval_ = 0;
+    size_t cursor_ = 0;
+    EngineReport rep_;
+    double sum_logprob_ = 0.0;
+    std::int64_t unchanged_ = 0, unchanged_known_ = 0;
+
+    void do_load(const std::string& id, int target, const std::string& reason) {
+        if (mem_.depth_of(id) == target) return;
+        apply_load(mem_, repo_, cfg_.mem, id, target);  // CapacityError leaves state untouched
+        be_.load(id, target);
+        if (reason == "breach_load_more") ++rep_.ld_count;
+    }
+
+    void load_for_eval(const std::string& id) {  // engine.hpp:220-234
+        const ModelSpec& spec = repo_.at(id);
+        MemoryState trial = mem_;
+        trial.loaded_depth[id] = spec.num_layers;
+        if (weights_loaded_bytes(trial, repo_) > cfg_.mem.capacity_bytes - cfg_.mem.reserve_bytes) {
+            std::vector<std::string> others;
+            for (const auto& [o, d] : mem_.loaded_depth)
+                if (o != id && d > 0) others.push_back(o);
+            for (const auto& o : others) do_load(o, 0, "evict");
+        }
+        do_load(id, spec.num_layers, "eval");
+    }
+
+    void eval_cycle(const std::vector<RequestSpec>& reqs) {  // engine.hpp:243-278
+        ++rep_.eval_cycles;
+        pending_.reset();
+        breach_.reset();
+        since_eval_ = 0;
+        for (const std::string& id : candidates_) {
+            if (cursor_ >= reqs.size()) break;
+            pht_.reset(id);
+            load_for_eval(id);
+            const ModelSpec& spec = repo_.at(id);
+            int served = 0;
+            while (served < cfg_.policy.n_eval_requests && cursor_ < reqs.size()) {
+                const size_t n = std::min<size_t>({(size_t)cfg_.max_batch, reqs.size() - cursor_,
+                                                   (size_t)(cfg_.policy.n_eval_requests - served)});
+                std::vector<const RequestSpec*> batch;
+                for (size_t i = 0; i < n; ++i) batch.push_back(&reqs[cursor_ + i]);
+                cursor_ += n;
+                served += (int)n;
+                serve_batch(batch, id, spec.num_layers, TokenPolicy::profile, true);
+            }
+        }
+        std::vector<std::string> profiled;
+        for (const auto& id : candidates_)
+            if (pht_.has(id)) profiled.push_back(id);
+        if (profiled.empty()) return;
+        const ReplanResult plan = replan_after_eval(repo_, pht_, profiled, cfg_.policy, cfg_.mem);
+        std::vector<std::string> drop;
+        for (const auto& [id, d] : mem_.loaded_depth) {
+            if (d <= 0) continue;
+            bool keep = false;
+            for (const auto& r : plan.residency) keep |= r.first == id;
+            if (!keep) drop.push_back(id);
+        }
+        for (const auto& id : drop) do_load(id, 0, "reassess");
+        for (const auto& [id, depth] : plan.residency) do_load(id, depth, "reassess");
+        serving_ = plan.serving_model;
+        depth_ = plan.serving_depth;
+    }
+
+    void apply_pending() {  // engine.hpp:301-323
+        const ActionPlan plan = *pending_;
+        pending_.reset();
+        if (plan.kind != ActionKind::stay) {
+            for (const auto& id : plan.evict) do_load(id, 0, "breach_evict");
+            if (plan.kind == ActionKind::load_more) {
+                do_load(plan.model_id, plan.serving_depth, "breach_load_more");
+            } else {
+                if (mem_.depth_of(plan.model_id) < plan.serving_depth)
+                    do_load(plan.model_id, plan.serving_depth, "breach_switch");
+                ++rep_.sw_count;
+                serving_ = plan.model_id;
+            }
+            depth_ = plan.serving_depth;
+        }
+        breach_.reset();
+    }
+
+    std::vector<std::string> profiled_candidates() const {
+        std::vector<std::string> out;
+        for (const auto& id : candidates_)
+            if (id == serving_ || pht_.has(id)) out.push_back(id);
+        return out;
+    }
+
+    void serve_batch(const std::vector<const RequestSpec*>& batch, const std::string& model, int depth,
+                     TokenPolicy tp, bool profile) {
+        const ModelSpec& spec = repo_.at(model);
+        const int vocab = spec.arch.vocab > 0 ? spec.arch.vocab : 1;
+        rep_.serving_history.emplace_back(model, depth);
+        const int b = (int)batch.size();
+        int max_prompt = 0, max_tokens = 0;
+        for (const auto* r : batch) {
+            max_prompt = std::max(max_prompt, r->prompt_len);
+            max_tokens = std::max(max_tokens, r->num_tokens);
+        }
+        // Prefill (engine.hpp:333-341): the prompt's KV through the serving depth.
+        if (cfg_.prefill) {
+            const TokenPolicy pre = tp == TokenPolicy::flat ? TokenPolicy::flat : TokenPolicy::full_depth;
+            for (int p = 0; p < max_prompt; ++p) {
+                StepRows rows;
+                for (int i = 0; i < b; ++i) {
+                    if (p >= batch[i]->prompt_len) continue;
+                    rows.slots.push_back(i);
+                    rows.tokens.push_back(synthetic_token(cfg_.token_seed, batch[i]->request_id, p, vocab));
+                    rows.positions.push_back(p);
+                    rows.request_ids.push_back(batch[i]->request_id);
+                    rows.token_index.push_back(0);
+                }
+                if (rows.size()) be_.step(model, depth, pre, cfg_.policy.th, rows);
+            }
+        }
+        // Decode: one token per in-flight request per step.
+        for (int t = 0; t < max_tokens; ++t) {
+            StepRows rows;
+            for (int i = 0; i < b; ++i) {
+                if (t >= batch[i]->num_tokens) continue;
+                const int pos = batch[i]->prompt_len + t;
+                rows.slots.push_back(i);
+                rows.tokens.push_back(synthetic_token(cfg_.token_seed, batch[i]->request_id, pos, vocab));
+                rows.positions.push_back(pos);
+                rows.request_ids.push_back(batch[i]->request_id);
+                rows.token_index.push_back(t);
+            }
+            const StepOutcome o = be_.step(model, depth, tp, cfg_.policy.th, rows);
+            double dur = o.seconds;
+            if (dur <= 0.0) {  // modelled (trace backend): the step lasts as long as its deepest row
+                int deepest = 0;
+                for (int x : o.exit_layer) deepest = std::max(deepest, x);
+                dur = deepest * spec.t_decode_per_layer_s;
+            }
+            consume(model, spec, tp, profile, rows, o, dur);
+        }
+    }
+
+    void consume(const std::string& model, const ModelSpec& spec, TokenPolicy tp, bool profile,
+                 const StepRows& rows, const StepOutcome& o, double dur) {
+        const int n = rows.size();
+        rep_.tokens += n;
+        rep_.steps += 1;
+        rep_.decode_wall_s += dur;
+        rep_.achieved_batch_size = std::max(rep_.achieved_batch_size, n);
+        for (int i = 0; i < n; ++i) {
+            rep_.exit_counts[model][o.exit_layer[i]] += 1;
+            sum_logprob_ += o.obs[i].logprob;
+            if (o.unchanged[i] != 2) {
+                ++unchanged_known_;
+                unchanged_ += o.unchanged[i];
+            }
+        }
+        if (profile) {  // record_token per row == record_step over the step histogram
+            std::vector<std::int64_t> hist(spec.exit_layers.size(), 0);
+            double sl = 0.0;
+            for (int i = 0; i < n; ++i) {
+                hist[exit_index(spec.exit_layers, o.exit_layer[i])] += 1;
+                sl += o.obs[i].logprob;
+            }
+            record_step(pht_, spec, hist, sl, dur);
+        }
+        if (tp == TokenPolicy::flat && cfg_.mode.kind == Mode::helios) {
+            for (int i = 0; i < n; ++i)  // ascending slot order (SURVEY §7 hard part 4)
+                if (observe_token(breach_, o.breached[i] != 0, cfg_.policy) && !pending_)
+                    pending_ = decide_action(repo_, pht_, profiled_candidates(), serving_, depth_, cfg_.mem, mem_,
+                                             cfg_.policy);
+        }
+    }
+
+    EngineReport finish() {
+        EngineReport r = rep_;
+        if (r.tokens > 0) {
+            r.throughput_tok_s = (double)r.tokens / r.decode_wall_s;
+            r.perplexity = std::exp(-sum_logprob_ / (double)r.tokens);
+            r.unchanged_fraction = unchanged_known_ ? (double)unchanged_ / (double)unchanged_known_ : 0.0;
+            for (const auto& [m, per] : r.exit_counts)
+                for (const auto& [l, c] : per) r.exit_table[m][l] = 100.0 * (double)c / (double)r.tokens;
+        }
+        r.pht = pht_;
+        return r;
+    }
+};
+
+}  // namespace eeserve

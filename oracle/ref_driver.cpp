@@ -11,6 +11,7 @@
 
 #include "eeserve/config.hpp"
 #include "eeserve/engine.hpp"
+#include "eeserve/generator.hpp"
 #include "eeserve/metrics.hpp"
 #include "eeserve/policy.hpp"
 
@@ -147,6 +148,17 @@ int ref_decide_action(const char* in_json, char* out, int cap) {
         Json j{{"kind", to_string(p.kind)}, {"model", p.model_id}, {"depth", p.serving_depth},
                {"evict", p.evict}, {"load_bytes", p.load_bytes}, {"cost_s", p.cost_s}};
         return copy_out(j.dump(), out, cap);
+    });
+}
+
+// Generate a workload with the reference generator (generator.hpp:347) and
+// write it as the reference JSONL trace format (trace.hpp:163-169).
+int ref_generate_trace(const char* gen_json, const char* repo_json, const char* out_jsonl) {
+    return guard([&] {
+        const ModelRepository repo = load_repository(repo_json);
+        const Trace t = generate_workload(load_generator_config(gen_json), repo);
+        write_workload(t, out_jsonl);
+        return (int)t.requests.size();
     });
 }
 

@@ -98,7 +98,7 @@ struct eeb_ctx {
     int retain_logits = 0;
     // step workspace (grow-only)
     int cap_rows = 0;
-    eeb::DevBuf xA, xB, hn, qkv, attn, mlp_h, logits, ws;
+    eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
     eeb::DevBuf head_tok, head_conf, head_logp;
     eeb::DevBuf o_exit, o_tok, o_conf, o_logp, o_breach, o_unch, o_bin, o_hist, o_nbr, o_sum;
@@ -328,14 +328,17 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     c->xA.ensure((size_t)R * D * 4);
     c->xB.ensure((size_t)R * D * 4);
     c->hn.ensure((size_t)R * D * act);
-    c->qkv.ensure((size_t)R * (m.dq + 2 * m.dkv) * 4);
+    c->hnB.ensure((size_t)R * D * act);
+    c->hhead.ensure((size_t)R * D * act);
     c->attn.ensure((size_t)R * m.dq * act);
     c->mlp_h.ensure((size_t)R * F * act);
-    c->logits.ensure((size_t)R * d.vocab * 4);
     // split-K partial bound: splits <= K / (32 * vec) for every GEMM of the step.
     const int64_t kmin = act == 4 ? 128 : 256;
-    int64_t need = 0;
-    auto upd = [&](int64_t N, int64_t K) { need = std::max(need, (K / kmin + 1) * R * N); };
+    int64_t need = 0;  // split-K planes per GEMM: tier 1 <= K/(32 vec)+1, tier 2 <= SMs/tiles+1
+    auto upd = [&](int64_t N, int64_t K) {
+        const int64_t tiles = (N + 127) / 128;
+        need = std::max(need, std::max<int64_t>(K / kmin + 1, c->num_sms / tiles + 1) * R * N);
+    };
     upd(m.dq + 2 * m.dkv, D);
     upd(D, m.dq);
     upd(m.up_rows, D);
@@ -423,8 +426,9 @@ void count(eeb_ctx* c, int cat, int n) {
     c->step_launches += n;
 }
 
-void gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int N, int K, int mode,
-          float* out_f32, int ldo, void* out_act, const int* n_active, int batch) {
+// One decode GEMM into the split-K plane workspace; returns the planes written.
+int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int N, int K, const int* n_active,
+         int batch) {
     GemmArgs a;
     a.dtype = m.desc.dtype;
     a.W = W;
@@ -433,28 +437,26 @@ void gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int
     a.max_rows = batch;
     a.N = N;
     a.K = K;
-    a.mode = mode;
-    a.out_f32 = out_f32;
-    a.out_act = out_act;
-    a.ldo = ldo;
-    a.workspace = c->ws.as<float>();
-    a.workspace_elems = c->ws_elems;
+    a.out = c->ws.as<float>();
+    a.plane_stride = (int64_t)batch * N;
+    a.max_planes = (int)std::min<int64_t>(64, c->ws_elems / a.plane_stride);
     a.num_sms = c->num_sms;
-    if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) {
-        const int n = gemm_tc(a, c->stream);
-        if (n > 0) {
-            count(c, cat, n);
-            return;
-        }
-        if (c->gemm_tier == 2 && batch >= 16)
+    int planes = 0;
+    if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) planes = gemm_tc(a, c->stream);
+    if (planes == 0) {
+        if (c->gemm_tier == 2 && m.desc.dtype == EEB_BF16 && batch >= 16 && gemm_tc_available())
             throw Error(EEB_E_DOMAIN, "tensor-core tier requested but not applicable");
+        planes = gemm_cc(a, c->stream);
     }
-    gemm_cc(a, c->stream);
-    count(c, cat, 2);
+    count(c, cat, 1);
+    return planes;
 }
 
 // ---------------------------------------------------------------------------
-// The step.
+// The step.  Per layer: QKV GEMM -> attention (sums the QKV planes, RoPE, KV
+// append) -> O GEMM -> residual+RMSNorm -> up GEMM -> activation -> down GEMM
+// -> residual+RMSNorm (next layer's norm, plus the exit head's norm after an
+// exit layer).  Heads: head GEMM -> max/argmax/sum-exp -> decide (+ compaction).
 // ---------------------------------------------------------------------------
 void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
     Model& m = model_of(c, mi);
@@ -464,9 +466,11 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
     Ints I = ints_of(c);
     RowState A{I.nA, I.rowA, I.slotA, I.posA, c->xA.as<float>()};
     RowState B{I.nB, I.rowB, I.slotB, I.posB, c->xB.as<float>()};
+    void* hA = c->hn.p;    // normalised activations for the next layer (per state)
+    void* hB = c->hnB.p;
     const StepOutDev o = out_dev(c);
+    const int64_t hrow = (int64_t)D * m.wbytes;
 
-    // Which heads run, and how deep the stack goes.
     std::vector<int> heads;
     int run_layers = L;
     if (policy == EEB_FLAT) {
@@ -482,33 +486,35 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
     } else {
         for (int e = 0; e < d.n_exits; ++e) heads.push_back(e);
     }
+    auto head_at = [&](size_t hi, int l) { return hi < heads.size() && m.exits[heads[hi]] == l; };
 
+    RowState cur = A, alt = B;
+    void* h_cur = hA;
+    void* h_alt = hB;
     {
         Timer t(c, kCatOther);
-        launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, batch, D, A, s);
-        count(c, kCatOther, 1);
+        launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, batch, D, cur, s);
+        launch_residual_norm(d.dtype, nullptr, 0, 0, cur.n_active, batch, cur.x, D, d.norm_eps,
+                             m.layers[0]->attn_norm.as<float>(), h_cur, nullptr, nullptr, s);
+        count(c, kCatOther, 2);
     }
-    RowState cur = A, alt = B;
     size_t hi = 0;
     const int qkv_n = m.dq + 2 * m.dkv;
+    float* ws = c->ws.as<float>();
     for (int l = 1; l <= run_layers; ++l) {
         const LayerWeights& W = *m.layers[l - 1];
-        {
-            Timer t(c, kCatNorm);
-            launch_rmsnorm(d.dtype, cur.x, W.attn_norm.as<float>(), cur.n_active, batch, D,
-                           d.norm_eps, c->hn.p, s);
-            count(c, kCatNorm, 1);
-        }
+        int planes;
         {
             Timer t(c, kCatGemm);
-            gemm(c, kCatGemm, m, W.wqkv.p, c->hn.p, qkv_n, D, kStoreF32, c->qkv.as<float>(), qkv_n,
-                 nullptr, cur.n_active, batch);
+            planes = gemm(c, kCatGemm, m, W.wqkv.p, h_cur, qkv_n, D, cur.n_active, batch);
         }
         {
             Timer t(c, kCatAttn);
             AttnArgs a;
             a.dtype = d.dtype;
-            a.qkv = c->qkv.as<float>();
+            a.qkv = ws;
+            a.splits = planes;
+            a.split_stride = (int64_t)batch * qkv_n;
             const size_t esz = m.wbytes;
             a.k_cache = static_cast<char*>(m.k_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * esz;
             a.v_cache = static_cast<char*>(m.v_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * esz;
@@ -530,40 +536,57 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
         }
         {
             Timer t(c, kCatGemm);
-            gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, kResidAdd, cur.x, D, nullptr, cur.n_active,
-                 batch);
+            planes = gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, cur.n_active, batch);
         }
         {
             Timer t(c, kCatNorm);
-            launch_rmsnorm(d.dtype, cur.x, W.mlp_norm.as<float>(), cur.n_active, batch, D, d.norm_eps,
-                           c->hn.p, s);
+            launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
+                                 W.mlp_norm.as<float>(), h_cur, nullptr, nullptr, s);
             count(c, kCatNorm, 1);
         }
         {
             Timer t(c, kCatGemm);
-            gemm(c, kCatGemm, m, W.wup.p, c->hn.p, m.up_rows, D,
-                 d.mlp_kind == EEB_MLP_SWIGLU ? kSwigluAct : kReluAct, nullptr, 0, c->mlp_h.p,
-                 cur.n_active, batch);
-            gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, kResidAdd, cur.x, D, nullptr,
-                 cur.n_active, batch);
+            planes = gemm(c, kCatGemm, m, W.wup.p, h_cur, m.up_rows, D, cur.n_active, batch);
         }
-        while (hi < heads.size() && m.exits[heads[hi]] == l) {
+        {
+            Timer t(c, kCatNorm);
+            launch_act(d.dtype, ws, planes, (int64_t)batch * m.up_rows, cur.n_active, batch, m.up_rows,
+                       d.mlp_kind == EEB_MLP_SWIGLU, c->mlp_h.p, c->num_sms, s);
+            count(c, kCatNorm, 1);
+        }
+        {
+            Timer t(c, kCatGemm);
+            planes = gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, cur.n_active, batch);
+        }
+        const bool exit_here = head_at(hi, l);
+        const bool more = l < run_layers;
+        {
+            Timer t(c, kCatNorm);
+            // next layer's attention norm -> h_cur; the exit head's norm -> hhead
+            const float* g_next = more ? m.layers[l]->attn_norm.as<float>() : nullptr;
+            const float* g_head = exit_here ? m.head_norm[heads[hi]]->as<float>() : nullptr;
+            const float* g1 = g_next ? g_next : g_head;
+            void* o1 = g_next ? h_cur : c->hhead.p;
+            const float* g2 = g_next ? g_head : nullptr;
+            void* o2 = g_next && g_head ? c->hhead.p : nullptr;
+            if (g1)
+                launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
+                                     d.norm_eps, g1, o1, g2, o2, s);
+            count(c, kCatNorm, 1);
+        }
+        while (head_at(hi, l)) {
             const int e = heads[hi];
             const bool is_final = hi + 1 == heads.size();
             Timer t(c, kCatHead);
-            launch_rmsnorm(d.dtype, cur.x, m.head_norm[e]->as<float>(), cur.n_active, batch, D,
-                           d.norm_eps, c->hn.p, s);
-            gemm(c, kCatHead, m, m.head[e]->p, c->hn.p, d.vocab, D, kStoreF32, c->logits.as<float>(),
-                 d.vocab, nullptr, cur.n_active, batch);
+            const int hp = gemm(c, kCatHead, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
+            float* keep = nullptr;
             if (c->retain_logits) {
-                while ((int)c->logits_keep.size() < d.n_exits)
-                    c->logits_keep.push_back(std::make_unique<DevBuf>());
+                while ((int)c->logits_keep.size() < d.n_exits) c->logits_keep.push_back(std::make_unique<DevBuf>());
                 c->logits_keep[e]->ensure((size_t)batch * d.vocab * 4);
-                EEB_CUDA(cudaMemcpyAsync(c->logits_keep[e]->p, c->logits.p, (size_t)batch * d.vocab * 4,
-                                         cudaMemcpyDeviceToDevice, s));
+                keep = c->logits_keep[e]->as<float>();
             }
             HeadOut h{c->head_tok.as<int>(), c->head_conf.as<float>(), c->head_logp.as<float>()};
-            launch_head_reduce(c->logits.as<float>(), d.vocab, cur.n_active, batch, h, s);
+            launch_head_reduce(ws, hp, (int64_t)batch * d.vocab, d.vocab, cur.n_active, batch, h, keep, s);
             DecideArgs da;
             da.policy = policy;
             da.exit_index = e;
@@ -581,11 +604,13 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             da.out = o;
             for (int k = 0; k < 64; ++k) da.layers[k] = k < d.n_exits ? m.exits[k] : 0;
             launch_decide(da, s);
-            count(c, kCatHead, 3);
+            count(c, kCatHead, 2);
             if (policy == EEB_INTROSPECTIVE && !is_final) {
-                launch_gather_rows(cur.x, alt.x, I.src, alt.n_active, batch, D, s);
+                launch_gather_rows(cur.x, alt.x, more ? h_cur : nullptr, h_alt, (int)hrow, I.src, alt.n_active,
+                                   batch, D, s);
                 count(c, kCatHead, 1);
                 std::swap(cur, alt);
+                std::swap(h_cur, h_alt);
             }
             ++hi;
         }
@@ -1030,46 +1055,51 @@ eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int bat
                           const void* x_host, float* y_host) {
     return guarded([&] {
         if (!c || !w_host || !x_host || !y_host) throw Error(EEB_E_DOMAIN, "null argument");
-        if (n <= 0 || k <= 0 || batch <= 0 || batch > 1024 || mode < 0 || mode > 3 || (mode == 3 && n % 2))
-            throw Error(EEB_E_DOMAIN, "bad gemm shape");
+        if (n <= 0 || k <= 0 || batch <= 0 || batch > 1024 || (mode != 0 && mode != 2 && mode != 3) ||
+            (mode == 3 && n % 2))
+            throw Error(EEB_E_DOMAIN, "bad gemm shape or mode");
         EEB_CUDA(cudaSetDevice(c->device));
         const size_t es = dtype == EEB_BF16 ? 2 : 4;
-        const int n_out = mode == kSwigluAct ? n / 2 : n;
-        DevBuf w, x, y, act, ws, na;
+        const int n_out = mode == 3 ? n / 2 : n;
+        DevBuf w, x, act, ws, na;
         w.ensure((size_t)n * k * es);
         x.ensure((size_t)batch * k * es);
-        y.ensure((size_t)batch * n * 4);
         act.ensure((size_t)batch * n_out * es);
-        const int64_t ws_elems = (int64_t)(k / 64 + 2) * batch * n;
-        ws.ensure((size_t)ws_elems * 4);
+        const int64_t plane = (int64_t)batch * n;
+        const int max_planes = std::max(k / 128 + 2, c->num_sms + 1);
+        ws.ensure((size_t)plane * max_planes * 4);
         na.ensure(4);
         EEB_CUDA(cudaMemcpy(w.p, w_host, w.bytes, cudaMemcpyHostToDevice));
         EEB_CUDA(cudaMemcpy(x.p, x_host, x.bytes, cudaMemcpyHostToDevice));
-        EEB_CUDA(cudaMemset(y.p, 0, y.bytes));
         EEB_CUDA(cudaMemcpy(na.p, &batch, 4, cudaMemcpyHostToDevice));
         GemmArgs a;
         a.dtype = dtype; a.W = w.p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
-        a.mode = mode; a.out_f32 = y.as<float>(); a.out_act = act.p; a.ldo = n; a.workspace = ws.as<float>();
-        a.workspace_elems = ws_elems; a.num_sms = c->num_sms;
-        if (tier == 2) {
-            if (gemm_tc(a, c->stream) == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
-        } else {
-            gemm_cc(a, c->stream);
+        a.out = ws.as<float>(); a.plane_stride = plane; a.max_planes = max_planes; a.num_sms = c->num_sms;
+        const int planes = tier == 2 ? gemm_tc(a, c->stream) : gemm_cc(a, c->stream);
+        if (planes == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
+        if (mode == 0) {  // fixed-order sum of the planes on the host
+            std::vector<float> tmp((size_t)plane * planes);
+            EEB_CUDA(cudaStreamSynchronize(c->stream));
+            EEB_CUDA(cudaMemcpy(tmp.data(), ws.p, tmp.size() * 4, cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < plane; ++i) {
+                float v = 0.f;
+                for (int p2 = 0; p2 < planes; ++p2) v += tmp[(size_t)p2 * plane + i];
+                y_host[i] = v;
+            }
+            return;
         }
+        launch_act(dtype, ws.as<float>(), planes, plane, na.as<int>(), batch, n, mode == 3, act.p, c->num_sms,
+                   c->stream);
         EEB_CUDA(cudaStreamSynchronize(c->stream));
-        if (mode <= kResidAdd) {
-            EEB_CUDA(cudaMemcpy(y_host, y.p, (size_t)batch * n * 4, cudaMemcpyDeviceToHost));
-        } else {
-            std::vector<char> tmp((size_t)batch * n_out * es);
-            EEB_CUDA(cudaMemcpy(tmp.data(), act.p, tmp.size(), cudaMemcpyDeviceToHost));
-            for (size_t i = 0; i < (size_t)batch * n_out; ++i) {
-                if (es == 4) std::memcpy(&y_host[i], &tmp[i * 4], 4);
-                else {
-                    uint16_t h;
-                    std::memcpy(&h, &tmp[i * 2], 2);
-                    const uint32_t u = (uint32_t)h << 16;
-                    std::memcpy(&y_host[i], &u, 4);
-                }
+        std::vector<char> tmp((size_t)batch * n_out * es);
+        EEB_CUDA(cudaMemcpy(tmp.data(), act.p, tmp.size(), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < (size_t)batch * n_out; ++i) {
+            if (es == 4) std::memcpy(&y_host[i], &tmp[i * 4], 4);
+            else {
+                uint16_t h;
+                std::memcpy(&h, &tmp[i * 2], 2);
+                const uint32_t u = (uint32_t)h << 16;
+                std::memcpy(&y_host[i], &u, 4);
             }
         }
     });

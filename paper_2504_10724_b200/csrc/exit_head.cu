@@ -24,15 +24,19 @@ constexpr int kReduceThreads = 1024;
 
 // Per-row max / argmax / sum-exp over the vocabulary.
 __global__ void __launch_bounds__(kReduceThreads)
-    head_reduce_kernel(const float* __restrict__ logits, int vocab, const int* __restrict__ n_active,
-                       HeadOut h) {
+    head_reduce_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int vocab,
+                       const int* __restrict__ n_active, HeadOut h, float* __restrict__ logits_out) {
     const int i = blockIdx.x;
     if (i >= *n_active) return;
-    const float* l = logits + (int64_t)i * vocab;
+    extern __shared__ float lg[];  // [vocab] summed logits of this row
+    const float* l = lg;
     float m = -INFINITY;
     int am = 0x7fffffff;
     for (int v = threadIdx.x; v < vocab; v += kReduceThreads) {
-        const float x = l[v];
+        float x = 0.f;
+        for (int s = 0; s < splits; ++s) x += part[s * split_stride + (int64_t)i * vocab + v];
+        lg[v] = x;
+        if (logits_out) logits_out[(int64_t)i * vocab + v] = x;
         if (x > m) { m = x; am = v; }  // strided scan: first occurrence within the thread
     }
     __shared__ float ms[32];
@@ -199,9 +203,13 @@ __global__ void __launch_bounds__(1024)
 
 }  // namespace
 
-void launch_head_reduce(const float* logits, int vocab, const int* n_active, int max_rows,
-                        HeadOut h, cudaStream_t s) {
-    head_reduce_kernel<<<max_rows, kReduceThreads, 0, s>>>(logits, vocab, n_active, h);
+void launch_head_reduce(const float* part, int splits, int64_t split_stride, int vocab, const int* n_active,
+                        int max_rows, HeadOut h, float* logits_out, cudaStream_t s) {
+    const size_t smem = (size_t)vocab * 4;
+    if (smem > 200 * 1024) throw Error(1, "head_reduce: vocabulary above 51200 entries");
+    EEB_CUDA(cudaFuncSetAttribute(head_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    head_reduce_kernel<<<max_rows, kReduceThreads, smem, s>>>(part, splits, split_stride, vocab, n_active, h,
+                                                              logits_out);
     EEB_CHECK_LAUNCH();
 }
 

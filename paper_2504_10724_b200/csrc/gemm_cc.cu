@@ -91,37 +91,8 @@ __global__ void __launch_bounds__(kWarps * 32)
     }
 }
 
-template <typename T>
-__global__ void splitk_epilogue_kernel(const float* __restrict__ part, int splits,
-                                       int64_t split_stride, const int* __restrict__ n_active,
-                                       int N, int mode, float* __restrict__ out_f32, int ldo,
-                                       T* __restrict__ out_act) {
-    const int n_out = mode == kSwigluAct ? N / 2 : N;
-    const int rows = *n_active;
-    const int64_t total = (int64_t)rows * n_out;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / n_out), n = (int)(idx % n_out);
-        if (mode == kSwigluAct) {
-            float g = 0.f, u = 0.f;
-            for (int s = 0; s < splits; ++s) {
-                g += part[s * split_stride + (int64_t)i * N + 2 * n];
-                u += part[s * split_stride + (int64_t)i * N + 2 * n + 1];
-            }
-            const float silu = g / (1.f + __expf(-g));
-            out_act[(int64_t)i * n_out + n] = from_f32<T>(silu * u);
-        } else {
-            float y = 0.f;
-            for (int s = 0; s < splits; ++s) y += part[s * split_stride + (int64_t)i * N + n];
-            if (mode == kStoreF32) out_f32[(int64_t)i * ldo + n] = y;
-            else if (mode == kResidAdd) out_f32[(int64_t)i * ldo + n] += y;
-            else out_act[(int64_t)i * n_out + n] = from_f32<T>(fmaxf(y, 0.f));
-        }
-    }
-}
-
 template <typename T, int MAXB>
-void run_cc(const GemmArgs& a, cudaStream_t s) {
+int run_cc(const GemmArgs& a, cudaStream_t s) {
     constexpr int VEC = Vec16<T>::N;
     const int tiles = (a.N + kRowsPerCta - 1) / kRowsPerCta;
     // Split K until the grid covers ~2 waves, keeping KS a multiple of 32*VEC
@@ -142,59 +113,36 @@ void run_cc(const GemmArgs& a, cudaStream_t s) {
     }
     const int KS = ks_of(splits);
     splits = (a.K + KS - 1) / KS;
-    const int64_t split_stride = (int64_t)a.max_rows * a.N;
-    if ((int64_t)splits * split_stride > a.workspace_elems)
-        throw Error(2, "gemm_cc: split-K workspace too small");
+    const int64_t split_stride = a.plane_stride;
+    if (splits > a.max_planes) throw Error(2, "gemm_cc: split-K workspace too small");
     const size_t smem = (size_t)KS * MAXB * sizeof(T);
     auto kern = gemm_cc_kernel<T, MAXB>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(tiles, splits);
     kern<<<grid, kWarps * 32, smem, s>>>(static_cast<const T*>(a.W), static_cast<const T*>(a.X),
-                                         a.n_active, a.workspace, a.N, a.K, KS, split_stride);
+                                         a.n_active, a.out, a.N, a.K, KS, split_stride);
     EEB_CHECK_LAUNCH();
-    const int n_out = a.mode == kSwigluAct ? a.N / 2 : a.N;
-    int64_t blocks = ((int64_t)a.max_rows * n_out + 255) / 256;
-    if (blocks > a.num_sms * 16) blocks = a.num_sms * 16;
-    splitk_epilogue_kernel<T><<<(int)blocks, 256, 0, s>>>(a.workspace, splits, split_stride,
-                                                          a.n_active, a.N, a.mode, a.out_f32, a.ldo,
-                                                          static_cast<T*>(a.out_act));
-    EEB_CHECK_LAUNCH();
+    return splits;
 }
 
 template <typename T>
-void dispatch_cc(const GemmArgs& a, cudaStream_t s) {
+int dispatch_cc(const GemmArgs& a, cudaStream_t s) {
     if (a.K % (32 * Vec16<T>::N) != 0) throw Error(1, "gemm_cc: K must be a multiple of 32 vectors");
     const int b = a.max_rows;
-    if (b <= 1) run_cc<T, 1>(a, s);
-    else if (b <= 2) run_cc<T, 2>(a, s);
-    else if (b <= 4) run_cc<T, 4>(a, s);
-    else if (b <= 8) run_cc<T, 8>(a, s);
-    else if (b <= 16) run_cc<T, 16>(a, s);
-    else if (b <= 32) run_cc<T, 32>(a, s);
-    else if (b <= 64) run_cc<T, 64>(a, s);
-    else throw Error(1, "gemm_cc: batch > 64 needs the tensor-core tier or row chunking");
+    if (b <= 1) return run_cc<T, 1>(a, s);
+    if (b <= 2) return run_cc<T, 2>(a, s);
+    if (b <= 4) return run_cc<T, 4>(a, s);
+    if (b <= 8) return run_cc<T, 8>(a, s);
+    if (b <= 16) return run_cc<T, 16>(a, s);
+    if (b <= 32) return run_cc<T, 32>(a, s);
+    if (b <= 64) return run_cc<T, 64>(a, s);
+    throw Error(1, "gemm_cc: batch > 64 needs the tensor-core tier");
 }
 
 }  // namespace
 
-void splitk_epilogue(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
-                     int max_rows, int N, int mode, float* out_f32, int ldo, void* out_act, int num_sms,
-                     cudaStream_t s) {
-    const int n_out = mode == kSwigluAct ? N / 2 : N;
-    int64_t blocks = ((int64_t)max_rows * n_out + 255) / 256;
-    if (blocks > num_sms * 16) blocks = num_sms * 16;
-    if (dtype == 0)
-        splitk_epilogue_kernel<float><<<(int)blocks, 256, 0, s>>>(part, splits, split_stride, n_active, N, mode,
-                                                                  out_f32, ldo, static_cast<float*>(out_act));
-    else
-        splitk_epilogue_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>(
-            part, splits, split_stride, n_active, N, mode, out_f32, ldo, static_cast<__nv_bfloat16*>(out_act));
-    EEB_CHECK_LAUNCH();
-}
-
-void gemm_cc(const GemmArgs& a, cudaStream_t s) {
-    if (a.dtype == 0) dispatch_cc<float>(a, s);
-    else dispatch_cc<__nv_bfloat16>(a, s);
+int gemm_cc(const GemmArgs& a, cudaStream_t s) {
+    return a.dtype == 0 ? dispatch_cc<float>(a, s) : dispatch_cc<__nv_bfloat16>(a, s);
 }
 
 }  // namespace eeb

@@ -122,12 +122,8 @@ struct TcParams {
     int bpad;          // UMMA N (batch rows, multiple of 16)
     int stages;
     int tmem_cols;
-    int mode;          // EpilogueMode, or -1 = split-K partials
     const int* n_active;
-    float* out_f32;
-    __nv_bfloat16* out_act;
-    int ldo;
-    float* part;
+    float* part;       // split-K planes, row stride N
     int64_t split_stride;
 };
 
@@ -213,30 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
+        float* plane = p.part + (int64_t)split * p.split_stride;
         for (int c0 = 0; c0 < p.bpad; c0 += 16) {
             float v[16];
-            tmem_ld16(taddr + (uint32_t)c0, v);
-            if (c0 >= rows) continue;  // (uniform) tcgen05.ld stays warp-collective
+            tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective: every warp runs every chunk
+            if (n < p.N) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int b = c0 + j;
-                const bool ok = b < rows && n < p.N;
-                float y = v[j];
-                if (p.mode < 0) {
-                    if (ok) p.part[(int64_t)split * p.split_stride + (int64_t)b * p.N + n] = y;
-                } else if (p.mode == kStoreF32) {
-                    if (ok) p.out_f32[(int64_t)b * p.ldo + n] = y;
-                } else if (p.mode == kResidAdd) {
-                    if (ok) p.out_f32[(int64_t)b * p.ldo + n] += y;
-                } else if (p.mode == kReluAct) {
-                    if (ok) p.out_act[(int64_t)b * p.N + n] = __float2bfloat16_rn(fmaxf(y, 0.f));
-                } else {  // SwiGLU: even lane = gate, odd lane = up
-                    const float u = __shfl_down_sync(0xffffffffu, y, 1);
-                    if (ok && (n & 1) == 0) {
-                        const float silu = y / (1.f + __expf(-y));
-                        p.out_act[(int64_t)b * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu * u);
-                    }
-                }
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < rows) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
             }
         }
     }
@@ -277,10 +257,6 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int box_rows) {
 
 }  // namespace
 
-void splitk_epilogue(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
-                     int max_rows, int N, int mode, float* out_f32, int ldo, void* out_act, int num_sms,
-                     cudaStream_t s);
-
 bool gemm_tc_available() { return encode_fn() != nullptr; }
 
 int gemm_tc(const GemmArgs& a, cudaStream_t s) {
@@ -290,7 +266,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     const int tiles = (a.N + kBM - 1) / kBM;
     const int kblocks = a.K / kBK;
     // split K so the grid covers the SMs once, keeping >= 2 k-blocks per CTA
-    int splits = std::max(1, std::min(kblocks / 2, a.num_sms / tiles));
+    int splits = std::max(1, std::min(std::min(kblocks / 2, a.max_planes), a.num_sms / tiles));
     const int kb_per = (kblocks + splits - 1) / splits;
     splits = (kblocks + kb_per - 1) / kb_per;
     const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
@@ -309,18 +285,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.stages = stages;
     p.tmem_cols = tmem_cols;
     p.n_active = a.n_active;
-    p.out_f32 = a.out_f32;
-    p.out_act = static_cast<__nv_bfloat16*>(a.out_act);
-    p.ldo = a.ldo;
-    p.split_stride = (int64_t)a.max_rows * a.N;
-    if (splits > 1) {
-        if ((int64_t)splits * p.split_stride > a.workspace_elems) return 0;
-        p.mode = -1;
-        p.part = a.workspace;
-    } else {
-        p.mode = a.mode;
-        p.part = nullptr;
-    }
+    p.part = a.out;
+    p.split_stride = a.plane_stride;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
@@ -328,12 +294,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     dim3 grid(tiles, splits);
     gemm_tc_kernel<<<grid, kThreads, smem, s>>>(mw, mx, p);
     EEB_CHECK_LAUNCH();
-    if (splits > 1) {
-        splitk_epilogue(a.dtype, a.workspace, splits, p.split_stride, a.n_active, a.max_rows, a.N, a.mode,
-                        a.out_f32, a.ldo, a.out_act, a.num_sms, s);
-        return 2;
-    }
-    return 1;
+    return splits;
 }
 
 }  // namespace eeb

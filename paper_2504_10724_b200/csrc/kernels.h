@@ -27,47 +27,46 @@ struct RowState {
     float* x;        // [maxB, d] residual stream (f32)
 };
 
-// ---- elementwise / normalisation (rows.cu) ---------------------------------
+// ---- row kernels (rows.cu) ---------------------------------------------------
 // x[i] = emb[tok[i]]; initialises the compact state to the identity.
 void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in,
                   int batch, int d, RowState st, cudaStream_t s);
-// out[i] = act(x[i] * gain / rms(x[i])) for live rows.
-void launch_rmsnorm(int dtype, const float* x, const float* gain, const int* n_active, int max_rows,
-                    int d, float eps, void* out, cudaStream_t s);
+// x[i] += sum_s part[s][i] (part may be null); out1 = act(x*g1/rms), out2 = act(x*g2/rms) (optional).
+void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
+                          int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
+                          void* out2, cudaStream_t s);
+// out[i][n] = relu(sum_s part) or silu(gate)*up over interleaved (gate, up) columns.
+void launch_act(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active, int max_rows,
+                int N, bool swiglu, void* out, int num_sms, cudaStream_t s);
 
-// ---- GEMM (gemm_cc.cu: CUDA-core split-K; gemm_tc.cu: tcgen05) -------------
-enum EpilogueMode : int {
-    kStoreF32 = 0,   // out_f32[i][n] = y
-    kResidAdd = 1,   // x[i][n] += y
-    kReluAct = 2,    // out_act[i][n] = relu(y)
-    kSwigluAct = 3,  // out_act[i][j] = silu(y[2j]) * y[2j+1]
-};
+// ---- decode GEMM (gemm_cc.cu: CUDA cores; gemm_tc.cu: tcgen05) ---------------
+// y[b][n] = sum_k X[b][k] * W[n][k], written as split-K partial planes:
+// plane s at out + s * plane_stride, row stride N.  Consumers reduce the
+// planes in a fixed order (deterministic, no atomics).
 struct GemmArgs {
     int dtype;          // weight / activation dtype
     const void* W;      // [N, K] row-major (K contiguous)
-    const void* X;      // [maxB, K] activations, row-major
+    const void* X;      // [max_rows, K] activations, row-major
     const int* n_active;
-    int max_rows;       // capacity / launch bound for rows
+    int max_rows;
     int N, K;
-    int mode;
-    float* out_f32;     // kStoreF32 / kResidAdd target, row stride ldo
-    void* out_act;      // kReluAct / kSwigluAct target
-    int ldo;
-    float* workspace;   // split-K partials
-    int64_t workspace_elems;
+    float* out;         // partial planes
+    int64_t plane_stride;
+    int max_planes;
     int num_sms;
 };
-// Tier 1: CUDA cores (any dtype, any batch).
-void gemm_cc(const GemmArgs& a, cudaStream_t s);
-// Tier 2: tcgen05 + TMA (bf16, batch >= 16).  Returns the number of kernels
-// launched, 0 when the shape is not applicable (caller falls back to tier 1).
+// Tier 1: CUDA cores (any dtype, <= 64 rows).  Returns the planes written.
+int gemm_cc(const GemmArgs& a, cudaStream_t s);
+// Tier 2: tcgen05 + TMA (bf16, 16..256 rows).  Returns planes, 0 if not applicable.
 int gemm_tc(const GemmArgs& a, cudaStream_t s);
 bool gemm_tc_available();
 
 // ---- attention (attention.cu) ------------------------------------------------
 struct AttnArgs {
     int dtype;
-    const float* qkv;        // [maxB, dq + 2 dkv] f32
+    const float* qkv;        // partial planes of the QKV GEMM, rows of dq + 2 dkv
+    int splits;
+    int64_t split_stride;
     void* k_cache;           // this layer: [slots][Hkv][S][hd]
     void* v_cache;
     const uint8_t* kv_depth; // [slots][S] layers computed per position
@@ -89,8 +88,9 @@ struct HeadOut {             // result of one head on the live rows (compact-ind
     float* conf;
     float* logp;
 };
-void launch_head_reduce(const float* logits, int vocab, const int* n_active, int max_rows,
-                        HeadOut h, cudaStream_t s);
+// Head logits arrive as split-K planes; logits_out (optional) receives the sum.
+void launch_head_reduce(const float* part, int splits, int64_t split_stride, int vocab, const int* n_active,
+                        int max_rows, HeadOut h, float* logits_out, cudaStream_t s);
 
 struct StepOutDev {          // caller-row-indexed outputs (device)
     int32_t* exit_layer;
@@ -126,9 +126,9 @@ struct DecideArgs {
     int layers[64];          // exit ladder (profile mode maps head index -> layer)
 };
 void launch_decide(const DecideArgs& a, cudaStream_t s);
-// x_nxt[j] = x_cur[src[j]] for live rows of the compacted state.
-void launch_gather_rows(const float* x_cur, float* x_nxt, const int* src, const int* n_active,
-                        int max_rows, int d, cudaStream_t s);
+// x_nxt[j] = x_cur[src[j]] (and the normalised row h) for live rows of the compacted state.
+void launch_gather_rows(const float* x_cur, float* x_nxt, const void* h_cur, void* h_nxt, int h_bytes_per_row,
+                        const int* src, const int* n_active, int max_rows, int d, cudaStream_t s);
 // Histogram (K4), breach count and fixed-order logprob sum over `batch` rows;
 // records each row's computed depth in the KV depth map.
 void launch_finalize(int batch, int n_exits, StepOutDev out, const int* slot_in, const int* pos_in,
