@@ -12,6 +12,8 @@
 // this layer has no K/V here (kv_depth[slot][p] < layer) and is masked; the
 // current position is always valid because this kernel writes it
 // (SURVEY §7 hard part 5).
+#include <cuda.h>
+
 #include "kernels.h"
 
 namespace eeb {
@@ -231,9 +233,300 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// bf16 path: flash-decode on the tensor cores.
+//
+// Q (G <= 8 heads, padded to the 16 rows of an m16n8k16 A operand) times K^T
+// and P times V run as mma.sync tiles; K and V chunks arrive by TMA in
+// 128-byte-swizzled [positions][64 dims] boxes so every ldmatrix is
+// conflict-free.  Warp w owns position tiles w, w+4, ... with its own online
+// softmax; the four warps are combined at the end (split-K style).
+// ---------------------------------------------------------------------------
+constexpr int kBoxRows = 32;    // positions per TMA box
+constexpr int kMmaWarps = 4;
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// byte offset of (row, 16-byte chunk) inside a 128B-swizzled [rows][128 B] block
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+    return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kMmaWarps * 32)
+    attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                         AttnArgs a) {
+    constexpr int CB = HD / 64;                    // 64-dim column blocks
+    constexpr int CP = HD == 64 ? 256 : 128;       // positions per chunk
+    constexpr int NT = HD / 8;                     // 8-dim n-tiles of O
+    constexpr int KS = HD / 16;                    // 16-dim k-steps of Q.K
+    constexpr int TPW = CP / 8 / kMmaWarps;        // position tiles per warp per chunk
+    constexpr uint32_t kBlockBytes = CP * 128;     // one column block of a chunk
+    const int i = blockIdx.x;
+    if (i >= *a.n_active) return;
+    const int g = blockIdx.y;
+    const int H = a.n_heads, Hkv = a.n_kv_heads, G = H / Hkv;
+    const int dq = H * HD, dkv = Hkv * HD, half = HD / 2;
+    const int slot = a.slot[i], pos = a.pos[i];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    uint8_t* base = smem_raw + (sbase - raw);
+    const uint32_t k_s = sbase, v_s = sbase + CB * kBlockBytes;  // [CB][CP][128 B] each
+    float* q_s = reinterpret_cast<float*>(base + 2 * CB * kBlockBytes);  // [8][HD]
+    __shared__ float kn_s[HD], vn_s[HD];
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t bar_a = smem_u32(&bar);
+
+    const int64_t row_off = (int64_t)i * (dq + 2 * dkv);
+    auto qkv = [&](int col) {
+        float v = 0.f;
+        for (int s = 0; s < a.splits; ++s) v += a.qkv[s * a.split_stride + row_off + col];
+        return v;
+    };
+    __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
+    __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
+    const int zc = slot * Hkv + g;
+
+    auto issue = [&](int c0) {  // thread 0: TMA positions [c0, c0+cn) rounded up to whole boxes
+        const int n_load = min(CP, pos + 1 - c0);
+        const int boxes = n_load > 0 ? (n_load + kBoxRows - 1) / kBoxRows : 0;
+        const uint32_t bytes = (uint32_t)boxes * CB * kBoxRows * 128 * 2;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(bytes) : "memory");
+        for (int b = 0; b < boxes; ++b)
+            for (int cb = 0; cb < CB; ++cb) {
+                const uint32_t off = cb * kBlockBytes + b * kBoxRows * 128;
+                tma_3d(k_s + off, &kmap, bar_a, cb * 64, c0 + b * kBoxRows, zc);
+                tma_3d(v_s + off, &vmap, bar_a, cb * 64, c0 + b * kBoxRows, zc);
+            }
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue(0);
+    }
+    // RoPE: queries (scaled) into q_s, the new key/value into the cache and kn_s / vn_s.
+    const float* cs = a.rope_cos + (int64_t)pos * half;
+    const float* sn = a.rope_sin + (int64_t)pos * half;
+    const float qscale = rsqrtf((float)HD);
+    for (int idx = threadIdx.x; idx < 8 * HD; idx += blockDim.x) {
+        const int h = idx / HD, j = idx % HD;
+        float v = 0.f;
+        if (h < G) {
+            const int q0 = (g * G + h) * HD;
+            const int jj = j < half ? j : j - half;
+            const float x0 = qkv(q0 + jj), x1 = qkv(q0 + jj + half);
+            v = (j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj]) * qscale;
+        }
+        q_s[h * HD + j] = v;
+    }
+    for (int j = threadIdx.x; j < HD; j += blockDim.x) {
+        const int k0 = dq + g * HD, v0 = dq + dkv + g * HD;
+        const int jj = j < half ? j : j - half;
+        const float x0 = qkv(k0 + jj), x1 = qkv(k0 + jj + half);
+        const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
+        const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(qkv(v0 + j));
+        kc[(int64_t)pos * HD + j] = kt;
+        vc[(int64_t)pos * HD + j] = vt;
+        kn_s[j] = __bfloat162float(kt);
+        vn_s[j] = __bfloat162float(vt);
+    }
+    __syncthreads();
+    // Q as m16n8k16 A fragments: rows = heads (lane/4), rows 8..15 are zero.
+    const int h = lane >> 2, kq = (lane & 3) * 2;
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+        qa[k][0] = pack_bf16(q_s[h * HD + 16 * k + kq], q_s[h * HD + 16 * k + kq + 1]);
+        qa[k][1] = 0u;
+        qa[k][2] = pack_bf16(q_s[h * HD + 16 * k + 8 + kq], q_s[h * HD + 16 * k + 8 + kq + 1]);
+        qa[k][3] = 0u;
+    }
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;
+    const uint8_t* depth = a.kv_depth + (int64_t)slot * a.max_seq;
+
+    const int n_chunks = pos / CP + 1;
+    for (int ci = 0; ci < n_chunks; ++ci) {
+        const int c0 = ci * CP;
+        const int cn = min(CP, pos + 1 - c0);
+        if (ci > 0) {
+            __syncthreads();  // everyone is done with the previous chunk
+            if (threadIdx.x == 0) issue(c0);
+        }
+        mbar_wait(bar_a, (uint32_t)(ci & 1));
+        if (pos < c0 + CP) {  // the new position lives in this chunk: write it (swizzled)
+            const int r = pos - c0;
+            for (int j = threadIdx.x; j < HD; j += blockDim.x) {
+                const uint32_t off = (j / 64) * kBlockBytes + swz(r, (j % 64) / 8) + (j % 8) * 2;
+                *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(kn_s[j]);
+                *reinterpret_cast<__nv_bfloat16*>(base + CB * kBlockBytes + off) = __float2bfloat16_rn(vn_s[j]);
+            }
+        }
+        __syncthreads();
+        const int n_tiles = (cn + 7) / 8;
+        // scores for this warp's tiles (C fragment: row h, positions kq, kq+1)
+        float sc[TPW][2];
+        int my_tiles = 0;
+        float cmax = -INFINITY;
+#pragma unroll
+        for (int tt = 0; tt < TPW; ++tt) {
+            const int t = warp + tt * kMmaWarps;
+            sc[tt][0] = sc[tt][1] = -INFINITY;
+            if (t >= n_tiles) continue;
+            my_tiles = tt + 1;
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+            const int row = t * 8 + (lane & 7);
+#pragma unroll
+            for (int k2 = 0; k2 < KS; k2 += 2) {
+                // matrices: (k-step k2 lo, hi), (k-step k2+1 lo, hi)
+                const int mi = lane >> 3;
+                const int dim = 16 * (k2 + (mi >> 1)) + 8 * (mi & 1);
+                uint32_t b[4];
+                ldsm_x4(k_s + (dim / 64) * kBlockBytes + swz(row, (dim % 64) / 8), b);
+                mma_bf16(c, qa[k2], b[0], b[1]);
+                mma_bf16(c, qa[k2 + 1], b[2], b[3]);
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int p = c0 + t * 8 + kq + e;
+                const bool valid = h < G && p <= pos && (p == pos || depth[p] >= a.layer);
+                sc[tt][e] = valid ? c[e] : -INFINITY;
+                cmax = fmaxf(cmax, sc[tt][e]);
+            }
+        }
+        // online softmax per (warp, head): reduce over the 4 lanes of a head
+        cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, 1));
+        cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, 2));
+        const float m_new = fmaxf(m_run, cmax);
+        const float scale = m_new == -INFINITY ? 1.f : __expf(m_run - m_new);
+        float psum = 0.f;
+#pragma unroll
+        for (int tt = 0; tt < TPW; ++tt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float p = sc[tt][e] == -INFINITY ? 0.f : __expf(sc[tt][e] - m_new);
+                sc[tt][e] = p;
+                psum += p;
+            }
+        psum += __shfl_xor_sync(0xffffffffu, psum, 1);
+        psum += __shfl_xor_sync(0xffffffffu, psum, 2);
+        l_run = l_run * scale + psum;
+        m_run = m_new;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            o[n][0] *= scale;
+            o[n][1] *= scale;
+        }
+        // P.V over tile pairs (tiles of one pair need not be adjacent positions)
+#pragma unroll
+        for (int tt = 0; tt < TPW; tt += 2) {
+            if (tt >= my_tiles) break;
+            const int ta = warp + tt * kMmaWarps;
+            const bool has_b = tt + 1 < my_tiles;
+            const int tb = has_b ? ta + kMmaWarps : ta;  // pad with a loaded tile, P = 0
+            uint32_t pa[4];
+            pa[0] = pack_bf16(sc[tt][0], sc[tt][1]);
+            pa[1] = 0u;
+            pa[2] = has_b ? pack_bf16(sc[tt + 1][0], sc[tt + 1][1]) : 0u;
+            pa[3] = 0u;
+            const int mi = lane >> 3;
+            const int row = ((mi & 1) ? tb : ta) * 8 + (lane & 7);
+#pragma unroll
+            for (int n = 0; n < NT; n += 2) {
+                const int dim = 8 * (n + (mi >> 1));
+                uint32_t b[4];
+                ldsm_x4_t(v_s + (dim / 64) * kBlockBytes + swz(row, (dim % 64) / 8), b);
+                mma_bf16(o[n], pa, b[0], b[1]);
+                mma_bf16(o[n + 1], pa, b[2], b[3]);
+            }
+        }
+    }
+    // combine the four warps: O = sum_w e^(m_w - M) O_w / sum_w e^(m_w - M) l_w
+    __syncthreads();
+    float* comb = reinterpret_cast<float*>(base);  // reuse the K/V chunk memory
+    float* ml = comb + kMmaWarps * 8 * HD;          // [warp][head][2]
+    if (h < G) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            comb[(warp * 8 + h) * HD + n * 8 + kq] = o[n][0];
+            comb[(warp * 8 + h) * HD + n * 8 + kq + 1] = o[n][1];
+        }
+        if ((lane & 3) == 0) {
+            ml[(warp * 8 + h) * 2] = m_run;
+            ml[(warp * 8 + h) * 2 + 1] = l_run;
+        }
+    }
+    __syncthreads();
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out) + (int64_t)i * dq;
+    for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+        const int hh = idx / HD, j = idx % HD;
+        float M = -INFINITY;
+        for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, ml[(w * 8 + hh) * 2]);
+        float num = 0.f, den = 0.f;
+        for (int w = 0; w < kMmaWarps; ++w) {
+            const float mw = ml[(w * 8 + hh) * 2];
+            const float f = mw == -INFINITY ? 0.f : __expf(mw - M);
+            num += f * comb[(w * 8 + hh) * HD + j];
+            den += f * ml[(w * 8 + hh) * 2 + 1];
+        }
+        out[(g * G + hh) * HD + j] = __float2bfloat16_rn(num / den);
+    }
+}
+
+template <int HD>
+void launch_mma(const AttnArgs& a, cudaStream_t s) {
+    constexpr int CB = HD / 64, CP = HD == 64 ? 256 : 128;
+    const size_t smem = 1024 + 2 * (size_t)CB * CP * 128 + 8 * HD * 4;
+    auto kern = attention_mma_kernel<HD>;
+    EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid(a.max_rows, a.n_kv_heads);
+    kern<<<grid, kMmaWarps * 32, smem, s>>>(*static_cast<const CUtensorMap*>(a.k_map),
+                                            *static_cast<const CUtensorMap*>(a.v_map), a);
+    EEB_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
+    if (a.dtype == 1 && a.k_map && a.v_map && a.n_heads / a.n_kv_heads <= 8 &&
+        (a.head_dim == 64 || a.head_dim == 128)) {
+        if (a.head_dim == 64) launch_mma<64>(a, s);
+        else launch_mma<128>(a, s);
+        return;
+    }
     const int G = a.n_heads / a.n_kv_heads;
     if (G > kMaxG || a.head_dim > kMaxHd || a.head_dim % 16 != 0 || kThreads % (a.head_dim / 2) != 0)
         throw Error(1, "attention: unsupported head geometry");

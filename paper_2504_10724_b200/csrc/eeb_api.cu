@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -70,6 +71,7 @@ struct Model {
     // KV pool
     DevBuf k_cache, v_cache, kv_depth, rope_cos, rope_sin;
     size_t kv_layer_elems = 0;
+    std::vector<std::array<uint8_t, 128>> k_maps, v_maps;  // bf16: per-layer TMA maps of the KV cache
 };
 
 struct GraphKey {
@@ -531,6 +533,8 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             a.head_dim = m.head_dim;
             a.max_seq = d.max_seq_len;
             a.out = c->attn.p;
+            a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[l - 1].data();
+            a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[l - 1].data();
             launch_attention(a, s);
             count(c, kCatAttn, 1);
         }
@@ -756,6 +760,19 @@ eeb_status eeb_model_register(eeb_ctx* c, const eeb_model_desc* desc, int* model
         m->kv_layer_elems = (size_t)d.max_slots * d.n_kv_heads * d.max_seq_len * m->head_dim;
         m->k_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
         m->v_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
+        EEB_CUDA(cudaMemset(m->k_cache.p, 0, m->k_cache.bytes));  // finite values behind masked rows
+        EEB_CUDA(cudaMemset(m->v_cache.p, 0, m->v_cache.bytes));
+        if (d.dtype == EEB_BF16 && (m->head_dim == 64 || m->head_dim == 128) && gemm_tc_available()) {
+            m->k_maps.resize(d.num_layers);
+            m->v_maps.resize(d.num_layers);
+            for (int l = 0; l < d.num_layers; ++l) {
+                const size_t off = (size_t)l * m->kv_layer_elems * 2;
+                make_kv_tensor_map(m->k_maps[l].data(), static_cast<char*>(m->k_cache.p) + off, m->head_dim,
+                                   d.max_seq_len, d.max_slots * d.n_kv_heads, 32);
+                make_kv_tensor_map(m->v_maps[l].data(), static_cast<char*>(m->v_cache.p) + off, m->head_dim,
+                                   d.max_seq_len, d.max_slots * d.n_kv_heads, 32);
+            }
+        }
         m->kv_depth.ensure((size_t)d.max_slots * d.max_seq_len);
         EEB_CUDA(cudaMemset(m->kv_depth.p, 0, m->kv_depth.bytes));
         // RoPE tables in f64 then rounded (restated identically by the oracle).

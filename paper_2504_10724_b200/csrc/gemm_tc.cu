@@ -259,6 +259,20 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int box_rows) {
 
 bool gemm_tc_available() { return encode_fn() != nullptr; }
 
+void make_kv_tensor_map(void* out_map, const void* base, int head_dim, int max_seq, int slots_x_heads,
+                        int box_rows) {
+    if (!encode_fn()) throw Error(5, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {(cuuint64_t)head_dim, (cuuint64_t)max_seq, (cuuint64_t)slots_x_heads};
+    const cuuint64_t strides[2] = {(cuuint64_t)head_dim * 2, (cuuint64_t)head_dim * 2 * max_seq};
+    const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(static_cast<CUtensorMap*>(out_map), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(5, "cuTensorMapEncodeTiled (kv) failed: " + std::to_string((int)r));
+}
+
 int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     if (a.dtype != 1 || a.max_rows < 16 || a.max_rows > 256 || a.K % kBK != 0) return 0;
     if (!gemm_tc_available()) return 0;

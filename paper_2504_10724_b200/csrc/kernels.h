@@ -60,6 +60,10 @@ int gemm_cc(const GemmArgs& a, cudaStream_t s);
 // Tier 2: tcgen05 + TMA (bf16, 16..256 rows).  Returns planes, 0 if not applicable.
 int gemm_tc(const GemmArgs& a, cudaStream_t s);
 bool gemm_tc_available();
+// 3-D TMA map over one layer's bf16 KV cache [slots*Hkv][max_seq][head_dim],
+// box {64 dims, box_rows positions, 1}, 128-byte swizzle.  out_map: 128 B.
+void make_kv_tensor_map(void* out_map, const void* base, int head_dim, int max_seq, int slots_x_heads,
+                        int box_rows);
 
 // ---- attention (attention.cu) ------------------------------------------------
 struct AttnArgs {
@@ -79,6 +83,8 @@ struct AttnArgs {
     int layer;               // 1-indexed
     int n_heads, n_kv_heads, head_dim, max_seq;
     void* out;               // [maxB, dq] act dtype
+    const void* k_map;       // bf16: TMA maps of this layer's K / V (128 B each), else null
+    const void* v_map;
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 

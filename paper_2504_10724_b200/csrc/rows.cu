@@ -5,7 +5,11 @@
 // Fusing the split-K reduction into these consumers removes a launch per
 // GEMM and produces the next GEMM's normalised bf16 input in the same pass
 // over the row (the residual stream stays f32).
+#include <cooperative_groups.h>
+
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace eeb {
 
@@ -31,36 +35,64 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // x[i] (+)= sum_s part[s][i]; out1 = T(x * inv_rms * g1); out2 likewise with g2.
-// When part is null x is taken as is (first layer after the embedding).
+// A cluster of kClusterRow CTAs owns one row: each sums its column slice of the
+// split-K planes (many independent loads in flight), the row's sum of squares
+// is combined through distributed shared memory in rank order (deterministic),
+// and each CTA normalises its slice.  part == null: x is taken as is.
+constexpr int kClusterRow = 8;
+
 template <typename T>
-__global__ void __launch_bounds__(kRowThreads)
+__global__ void __cluster_dims__(kClusterRow, 1, 1) __launch_bounds__(kRowThreads)
     residual_norm_kernel(const float* __restrict__ part, int splits, int64_t split_stride,
                          const int* __restrict__ n_active, float* __restrict__ x, int d, float eps,
                          const float* __restrict__ g1, T* __restrict__ out1, const float* __restrict__ g2,
                          T* __restrict__ out2) {
-    const int i = blockIdx.x;
-    if (i >= *n_active) return;
-    extern __shared__ float xs[];  // [d]
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int i = blockIdx.x / kClusterRow;
+    const bool live = i < *n_active;  // uniform over the cluster
     __shared__ float red[32];
+    __shared__ float ss_slice;
+    const int per = d / kClusterRow;
+    const int c0 = rank * per;
     float* row = x + (int64_t)i * d;
+    constexpr int kMaxCols = 8;  // per thread: d <= 8 * 8 * 256
+    float v[kMaxCols];
     float ss = 0.f;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        float v = row[c];
-        if (part) {
-            float y = 0.f;
-            for (int s = 0; s < splits; ++s) y += part[s * split_stride + (int64_t)i * d + c];
-            v += y;
-            row[c] = v;
+    if (live) {
+#pragma unroll
+        for (int k = 0; k < kMaxCols; ++k) {
+            const int c = c0 + threadIdx.x + k * kRowThreads;
+            v[k] = 0.f;
+            if (threadIdx.x + k * kRowThreads < per) {
+                float xv = row[c];
+                if (part) {
+                    float y = 0.f;
+                    for (int s = 0; s < splits; ++s) y += part[s * split_stride + (int64_t)i * d + c];
+                    xv += y;
+                    row[c] = xv;
+                }
+                v[k] = xv;
+                ss += xv * xv;
+            }
         }
-        xs[c] = v;
-        ss += v * v;
     }
-    const float tot = block_sum(ss, red);
+    ss = block_sum(ss, red);
+    if (threadIdx.x == 0) ss_slice = ss;
+    cluster.sync();
+    float tot = 0.f;
+    for (int r = 0; r < kClusterRow; ++r) tot += *cluster.map_shared_rank(&ss_slice, r);
+    cluster.sync();  // keep every slice alive until all ranks have read it
+    if (!live) return;
     const float inv = rsqrtf(tot / (float)d + eps);
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        const float v = xs[c] * inv;
-        out1[(int64_t)i * d + c] = from_f32<T>(v * g1[c]);
-        if (out2) out2[(int64_t)i * d + c] = from_f32<T>(v * g2[c]);
+#pragma unroll
+    for (int k = 0; k < kMaxCols; ++k) {
+        const int c = c0 + threadIdx.x + k * kRowThreads;
+        if (threadIdx.x + k * kRowThreads < per) {
+            const float nv = v[k] * inv;
+            out1[(int64_t)i * d + c] = from_f32<T>(nv * g1[c]);
+            if (out2) out2[(int64_t)i * d + c] = from_f32<T>(nv * g2[c]);
+        }
     }
 }
 
@@ -137,20 +169,17 @@ void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
                           void* out2, cudaStream_t s) {
-    const size_t smem = (size_t)d * 4;
-    if (dtype == 0) {
-        EEB_CUDA(cudaFuncSetAttribute(residual_norm_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        residual_norm_kernel<float><<<max_rows, kRowThreads, smem, s>>>(
-            part, splits, split_stride, n_active, x, d, eps, g1, static_cast<float*>(out1), g2,
-            static_cast<float*>(out2));
-    } else {
-        EEB_CUDA(cudaFuncSetAttribute(residual_norm_kernel<__nv_bfloat16>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        residual_norm_kernel<__nv_bfloat16><<<max_rows, kRowThreads, smem, s>>>(
+    if (d % kClusterRow != 0 || d / kClusterRow > 8 * kRowThreads)
+        throw Error(1, "residual_norm: d_model must be a multiple of 8 and at most 16384");
+    const dim3 grid(max_rows * kClusterRow);
+    if (dtype == 0)
+        residual_norm_kernel<float><<<grid, kRowThreads, 0, s>>>(part, splits, split_stride, n_active, x, d, eps, g1,
+                                                                 static_cast<float*>(out1), g2,
+                                                                 static_cast<float*>(out2));
+    else
+        residual_norm_kernel<__nv_bfloat16><<<grid, kRowThreads, 0, s>>>(
             part, splits, split_stride, n_active, x, d, eps, g1, static_cast<__nv_bfloat16*>(out1), g2,
             static_cast<__nv_bfloat16*>(out2));
-    }
     EEB_CHECK_LAUNCH();
 }
 
