@@ -165,6 +165,11 @@ eeb_status eeb_debug_read_kv(eeb_ctx* ctx, int model, int layer, int slot, int p
 eeb_status eeb_debug_gemm(eeb_ctx* ctx, int tier, int dtype, int n, int k, int batch, int mode,
                           const void* w_host, const void* x_host, float* y_host);
 
+/* Steady-state timing of one decode GEMM shape: `iters` back-to-back launches
+ * (PDL-chained, like inside a step) on device-resident random data; returns the
+ * mean milliseconds per launch (CUDA events on the context stream). */
+eeb_status eeb_debug_bench_gemm(eeb_ctx* ctx, int tier, int n, int k, int batch, int iters, double* ms_out);
+
 /* Per-kernel timing of the last step (CUDA events on the context stream).
  * names: "gemm", "attention", "exit_head", ... ; returns total ms. */
 eeb_status eeb_profile_enable(eeb_ctx* ctx, int enable);

@@ -48,6 +48,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 template <typename T>
 __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
     constexpr int VEC = Vec16<T>::N;  // elements per 16 B
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x;
     if (i >= *a.n_active) return;
     const int g = blockIdx.y;
@@ -288,6 +290,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     constexpr int KS = HD / 16;                    // 16-dim k-steps of Q.K
     constexpr int TPW = CP / 8 / kMmaWarps;        // position tiles per warp per chunk
     constexpr uint32_t kBlockBytes = CP * 128;     // one column block of a chunk
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x;
     if (i >= *a.n_active) return;
     const int g = blockIdx.y;
@@ -307,11 +311,6 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     const uint32_t bar_a = smem_u32(&bar);
 
     const int64_t row_off = (int64_t)i * (dq + 2 * dkv);
-    auto qkv = [&](int col) {
-        float v = 0.f;
-        for (int s = 0; s < a.splits; ++s) v += a.qkv[s * a.split_stride + row_off + col];
-        return v;
-    };
     __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
     __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
     const int zc = slot * Hkv + g;
@@ -335,6 +334,27 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         issue(0);
     }
+    // Stage this CTA's q (G heads), k and v columns, summed over the QKV GEMM's
+    // split-K planes, with every load in flight at once (float4, planes unrolled).
+    float* raw_s = q_s + 8 * HD;  // [(G + 2) * HD]
+    {
+        const int nq4 = G * HD / 4, n4 = (G + 2) * HD / 4;
+        const float* src = a.qkv + row_off;
+        for (int v4 = threadIdx.x; v4 < n4; v4 += blockDim.x) {
+            const int col = v4 < nq4 ? g * G * HD + 4 * v4
+                          : (v4 < nq4 + HD / 4 ? dq + g * HD + 4 * (v4 - nq4) : dq + dkv + g * HD + 4 * (v4 - nq4 - HD / 4));
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int sp = 0; sp < 16; ++sp) {
+                if (sp < a.splits) {
+                    const float4 t = *reinterpret_cast<const float4*>(src + sp * a.split_stride + col);
+                    acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+                }
+            }
+            *reinterpret_cast<float4*>(raw_s + 4 * v4) = acc;
+        }
+    }
+    __syncthreads();
     // RoPE: queries (scaled) into q_s, the new key/value into the cache and kn_s / vn_s.
     const float* cs = a.rope_cos + (int64_t)pos * half;
     const float* sn = a.rope_sin + (int64_t)pos * half;
@@ -343,19 +363,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
         const int h = idx / HD, j = idx % HD;
         float v = 0.f;
         if (h < G) {
-            const int q0 = (g * G + h) * HD;
+            const float* q = raw_s + h * HD;
             const int jj = j < half ? j : j - half;
-            const float x0 = qkv(q0 + jj), x1 = qkv(q0 + jj + half);
+            const float x0 = q[jj], x1 = q[jj + half];
             v = (j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj]) * qscale;
         }
         q_s[h * HD + j] = v;
     }
     for (int j = threadIdx.x; j < HD; j += blockDim.x) {
-        const int k0 = dq + g * HD, v0 = dq + dkv + g * HD;
+        const float* k = raw_s + G * HD;
+        const float* vv = raw_s + (G + 1) * HD;
         const int jj = j < half ? j : j - half;
-        const float x0 = qkv(k0 + jj), x1 = qkv(k0 + jj + half);
+        const float x0 = k[jj], x1 = k[jj + half];
         const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
-        const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(qkv(v0 + j));
+        const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(vv[j]);
         kc[(int64_t)pos * HD + j] = kt;
         vc[(int64_t)pos * HD + j] = vt;
         kn_s[j] = __bfloat162float(kt);
@@ -509,12 +530,14 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
 template <int HD>
 void launch_mma(const AttnArgs& a, cudaStream_t s) {
     constexpr int CB = HD / 64, CP = HD == 64 ? 256 : 128;
-    const size_t smem = 1024 + 2 * (size_t)CB * CP * 128 + 8 * HD * 4;
+    const int G = a.n_heads / a.n_kv_heads;
+    if (a.splits > 16) throw Error(1, "attention: more than 16 QKV split-K planes");
+    const size_t smem = 1024 + 2 * (size_t)CB * CP * 128 + (8 + G + 2) * HD * 4;
     auto kern = attention_mma_kernel<HD>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(a.max_rows, a.n_kv_heads);
-    kern<<<grid, kMmaWarps * 32, smem, s>>>(*static_cast<const CUtensorMap*>(a.k_map),
-                                            *static_cast<const CUtensorMap*>(a.v_map), a);
+    launch_pdl(kern, grid, dim3(kMmaWarps * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
+               *static_cast<const CUtensorMap*>(a.v_map), a);
     EEB_CHECK_LAUNCH();
 }
 
@@ -538,11 +561,11 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     dim3 grid(a.max_rows, a.n_kv_heads);
     if (a.dtype == 0) {
         EEB_CUDA(cudaFuncSetAttribute(attention_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attention_kernel<float><<<grid, kThreads, smem, s>>>(a);
+        launch_pdl(attention_kernel<float>, grid, dim3(kThreads), smem, s, a);
     } else {
         EEB_CUDA(cudaFuncSetAttribute(attention_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-        attention_kernel<__nv_bfloat16><<<grid, kThreads, smem, s>>>(a);
+        launch_pdl(attention_kernel<__nv_bfloat16>, grid, dim3(kThreads), smem, s, a);
     }
     EEB_CHECK_LAUNCH();
 }

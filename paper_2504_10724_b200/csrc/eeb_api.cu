@@ -460,6 +460,13 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
 // -> residual+RMSNorm (next layer's norm, plus the exit head's norm after an
 // exit layer).  Heads: head GEMM -> max/argmax/sum-exp -> decide (+ compaction).
 // ---------------------------------------------------------------------------
+// Timing experiments only (results are wrong): EEB_SKIP=gemm,attn,norm,head
+// drops a kernel category from the step so its share of the graph can be measured.
+bool skip_cat(const char* what) {
+    static const std::string env = std::getenv("EEB_SKIP") ? std::getenv("EEB_SKIP") : "";
+    return !env.empty() && env.find(what) != std::string::npos;
+}
+
 void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
     Model& m = model_of(c, mi);
     const eeb_model_desc& d = m.desc;
@@ -508,7 +515,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
         int planes;
         {
             Timer t(c, kCatGemm);
-            planes = gemm(c, kCatGemm, m, W.wqkv.p, h_cur, qkv_n, D, cur.n_active, batch);
+            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wqkv.p, h_cur, qkv_n, D, cur.n_active, batch);
         }
         {
             Timer t(c, kCatAttn);
@@ -535,32 +542,34 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             a.out = c->attn.p;
             a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[l - 1].data();
             a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[l - 1].data();
-            launch_attention(a, s);
+            if (!skip_cat("attn")) launch_attention(a, s);
             count(c, kCatAttn, 1);
         }
         {
             Timer t(c, kCatGemm);
-            planes = gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, cur.n_active, batch);
+            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, cur.n_active, batch);
         }
         {
             Timer t(c, kCatNorm);
-            launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
-                                 W.mlp_norm.as<float>(), h_cur, nullptr, nullptr, s);
+            if (!skip_cat("norm"))
+                launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
+                                     d.norm_eps, W.mlp_norm.as<float>(), h_cur, nullptr, nullptr, s);
             count(c, kCatNorm, 1);
         }
         {
             Timer t(c, kCatGemm);
-            planes = gemm(c, kCatGemm, m, W.wup.p, h_cur, m.up_rows, D, cur.n_active, batch);
+            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wup.p, h_cur, m.up_rows, D, cur.n_active, batch);
         }
         {
             Timer t(c, kCatNorm);
-            launch_act(d.dtype, ws, planes, (int64_t)batch * m.up_rows, cur.n_active, batch, m.up_rows,
-                       d.mlp_kind == EEB_MLP_SWIGLU, c->mlp_h.p, c->num_sms, s);
+            if (!skip_cat("norm"))
+                launch_act(d.dtype, ws, planes, (int64_t)batch * m.up_rows, cur.n_active, batch, m.up_rows,
+                           d.mlp_kind == EEB_MLP_SWIGLU, c->mlp_h.p, c->num_sms, s);
             count(c, kCatNorm, 1);
         }
         {
             Timer t(c, kCatGemm);
-            planes = gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, cur.n_active, batch);
+            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, cur.n_active, batch);
         }
         const bool exit_here = head_at(hi, l);
         const bool more = l < run_layers;
@@ -573,7 +582,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             void* o1 = g_next ? h_cur : c->hhead.p;
             const float* g2 = g_next ? g_head : nullptr;
             void* o2 = g_next && g_head ? c->hhead.p : nullptr;
-            if (g1)
+            if (g1 && !skip_cat("norm"))
                 launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
                                      d.norm_eps, g1, o1, g2, o2, s);
             count(c, kCatNorm, 1);
@@ -582,7 +591,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             const int e = heads[hi];
             const bool is_final = hi + 1 == heads.size();
             Timer t(c, kCatHead);
-            const int hp = gemm(c, kCatHead, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
+            const int hp = skip_cat("head") ? 1 : gemm(c, kCatHead, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
             float* keep = nullptr;
             if (c->retain_logits) {
                 while ((int)c->logits_keep.size() < d.n_exits) c->logits_keep.push_back(std::make_unique<DevBuf>());
@@ -1119,6 +1128,46 @@ eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int bat
                 std::memcpy(&y_host[i], &u, 4);
             }
         }
+    });
+}
+
+eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, int iters, double* ms_out) {
+    return guarded([&] {
+        if (!c || !ms_out || n <= 0 || k <= 0 || batch <= 0 || iters <= 0) throw Error(EEB_E_DOMAIN, "bad argument");
+        EEB_CUDA(cudaSetDevice(c->device));
+        DevBuf w, x, ws, na;
+        w.ensure((size_t)n * k * 2);
+        x.ensure((size_t)batch * k * 2);
+        const int64_t plane = (int64_t)batch * n;
+        const int max_planes = std::max(k / 128 + 2, c->num_sms + 1);
+        ws.ensure((size_t)plane * max_planes * 4);
+        na.ensure(4);
+        synth_linear(EEB_BF16, w.p, 1, 1, n, k, 0.02f, false, k, c->stream);
+        synth_linear(EEB_BF16, x.p, 2, 1, batch, k, 1.0f, false, k, c->stream);
+        EEB_CUDA(cudaMemcpy(na.p, &batch, 4, cudaMemcpyHostToDevice));
+        GemmArgs a;
+        a.dtype = EEB_BF16; a.W = w.p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
+        a.out = ws.as<float>(); a.plane_stride = plane; a.max_planes = max_planes; a.num_sms = c->num_sms;
+        auto run = [&] {
+            if (tier == 2) {
+                if (gemm_tc(a, c->stream) == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
+            } else {
+                gemm_cc(a, c->stream);
+            }
+        };
+        for (int i = 0; i < 3; ++i) run();
+        cudaEvent_t e0, e1;
+        EEB_CUDA(cudaEventCreate(&e0));
+        EEB_CUDA(cudaEventCreate(&e1));
+        EEB_CUDA(cudaEventRecord(e0, c->stream));
+        for (int i = 0; i < iters; ++i) run();
+        EEB_CUDA(cudaEventRecord(e1, c->stream));
+        EEB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        EEB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = ms / iters;
     });
 }
 

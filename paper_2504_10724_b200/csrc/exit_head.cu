@@ -26,6 +26,8 @@ constexpr int kReduceThreads = 1024;
 __global__ void __launch_bounds__(kReduceThreads)
     head_reduce_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int vocab,
                        const int* __restrict__ n_active, HeadOut h, float* __restrict__ logits_out) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x;
     if (i >= *n_active) return;
     extern __shared__ float lg[];  // [vocab] summed logits of this row
@@ -94,6 +96,8 @@ __device__ __forceinline__ void write_row(const StepOutDev& o, int r, int exit_l
 // Single CTA: applies the token policy to the rows the head just ran on and,
 // for introspective steps, compacts the survivors (ballot + block scan).
 __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ int warp_counts[32];
     __shared__ int n_live_s;
     const int n_live = *a.cur.n_active;
@@ -178,6 +182,8 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
 __global__ void __launch_bounds__(1024)
     finalize_kernel(int batch, int n_exits, StepOutDev o, const int* __restrict__ slot_in,
                     const int* __restrict__ pos_in, uint8_t* __restrict__ kv_depth, int max_seq) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ unsigned long long hist_s[64];
     __shared__ int breach_s;
     if (threadIdx.x < 64) hist_s[threadIdx.x] = 0;
@@ -208,20 +214,20 @@ void launch_head_reduce(const float* part, int splits, int64_t split_stride, int
     const size_t smem = (size_t)vocab * 4;
     if (smem > 200 * 1024) throw Error(1, "head_reduce: vocabulary above 51200 entries");
     EEB_CUDA(cudaFuncSetAttribute(head_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    head_reduce_kernel<<<max_rows, kReduceThreads, smem, s>>>(part, splits, split_stride, vocab, n_active, h,
-                                                              logits_out);
+    launch_pdl(head_reduce_kernel, dim3(max_rows), dim3(kReduceThreads), smem, s, part, splits, split_stride, vocab,
+               n_active, h, logits_out);
     EEB_CHECK_LAUNCH();
 }
 
 void launch_decide(const DecideArgs& a, cudaStream_t s) {
-    decide_kernel<<<1, 1024, 0, s>>>(a);
+    launch_pdl(decide_kernel, dim3(1), dim3(1024), 0, s, a);
     EEB_CHECK_LAUNCH();
 }
 
 void launch_finalize(int batch, int n_exits, StepOutDev out, const int* slot_in, const int* pos_in,
                      uint8_t* kv_depth, int max_seq, cudaStream_t s) {
     if (n_exits > 64) throw Error(1, "finalize: at most 64 exits");
-    finalize_kernel<<<1, 1024, 0, s>>>(batch, n_exits, out, slot_in, pos_in, kv_depth, max_seq);
+    launch_pdl(finalize_kernel, dim3(1), dim3(1024), 0, s, batch, n_exits, out, slot_in, pos_in, kv_depth, max_seq);
     EEB_CHECK_LAUNCH();
 }
 

@@ -25,6 +25,8 @@ __global__ void __launch_bounds__(kWarps * 32)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* xs = reinterpret_cast<T*>(smem_raw);  // [MAXB][KS]
 
+    pdl_launch_dependents();
+    pdl_wait();
     const int nb = min(*n_active, MAXB);
     if (nb <= 0) return;
     const int k0 = blockIdx.y * KS;
@@ -119,8 +121,8 @@ int run_cc(const GemmArgs& a, cudaStream_t s) {
     auto kern = gemm_cc_kernel<T, MAXB>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(tiles, splits);
-    kern<<<grid, kWarps * 32, smem, s>>>(static_cast<const T*>(a.W), static_cast<const T*>(a.X),
-                                         a.n_active, a.out, a.N, a.K, KS, split_stride);
+    launch_pdl(kern, grid, dim3(kWarps * 32), smem, s, static_cast<const T*>(a.W), static_cast<const T*>(a.X),
+               a.n_active, a.out, a.N, a.K, KS, split_stride);
     EEB_CHECK_LAUNCH();
     return splits;
 }

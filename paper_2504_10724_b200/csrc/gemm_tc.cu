@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -127,7 +128,7 @@ struct TcParams {
     int64_t split_stride;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                    TcParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kb1 = min(kb0 + p.kb_per, p.kblocks);
     const int nkb = kb1 - kb0;
 
+    pdl_launch_dependents();  // let the next kernel of the step get resident and prefetch
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_w);
         prefetch_tmap(&tmap_x);
@@ -173,7 +175,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-            for (int i = 0; i < nkb; ++i) {
+            // Weights do not depend on the previous kernel: fill the first
+            // stages with weight tiles before waiting on it (PDL), then add the
+            // activation tiles once the predecessor's output is visible.
+            const int pre = min(S, nkb);
+            for (int i = 0; i < pre; ++i) {
+                const uint32_t sa = base + (uint32_t)i * stage_bytes;
+                mbar_expect_tx(full0 + 8 * i, stage_bytes);
+                tma_load_2d(sa, &tmap_w, full0 + 8 * i, (kb0 + i) * kBK, m_tile * kBM, pol_w);
+            }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,
+                            pol_x);
+            for (int i = pre; i < nkb; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)(i / S) & 1u;
                 mbar_wait(empty0 + 8 * s, ph ^ 1u);
@@ -205,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31  (thread = output feature)
         const int quarter = warp & 3;
         const int n = m_tile * kBM + quarter * 32 + lane;
+        pdl_wait();  // n_active and the plane workspace belong to the previous kernels
         mbar_wait(tfull, 0);
         tc_fence_after();
         const int rows = *p.n_active;
@@ -280,12 +296,19 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     const int tiles = (a.N + kBM - 1) / kBM;
     const int kblocks = a.K / kBK;
     // split K so the grid covers the SMs once, keeping >= 2 k-blocks per CTA
-    int splits = std::max(1, std::min(std::min(kblocks / 2, a.max_planes), a.num_sms / tiles));
+    static const int env_wave = std::getenv("EEB_TC_WAVE") ? std::atoi(std::getenv("EEB_TC_WAVE")) : 0;
+    static const int env_stages = std::getenv("EEB_TC_STAGES") ? std::atoi(std::getenv("EEB_TC_STAGES")) : 0;
+    const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
+    int splits = std::max(1, std::min(std::min(kblocks / 2, a.max_planes), wave / tiles));
     const int kb_per = (kblocks + splits - 1) / splits;
     splits = (kblocks + kb_per - 1) / kb_per;
     const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
-    int stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
+    // ~half the SM's shared memory so two GEMM CTAs co-reside: the next GEMM of
+    // the step (PDL) streams its weights while this one drains.
+    int stages = std::min(4, (int)((kSmemBudget / 2 - 1024 - 256) / stage_bytes));
     stages = std::min(stages, std::max(2, kb_per));
+    if (stages < 2) stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
+    if (env_stages > 0) stages = std::min(env_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (stages < 2) return 0;
     int tmem_cols = 32;
     while (tmem_cols < bpad) tmem_cols *= 2;
@@ -306,7 +329,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
     EEB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(tiles, splits);
-    gemm_tc_kernel<<<grid, kThreads, smem, s>>>(mw, mx, p);
+    launch_pdl(gemm_tc_kernel, grid, dim3(kThreads), smem, s, mw, mx, p);
     EEB_CHECK_LAUNCH();
     return splits;
 }

@@ -47,6 +47,8 @@ __global__ void __cluster_dims__(kClusterRow, 1, 1) __launch_bounds__(kRowThread
                          const int* __restrict__ n_active, float* __restrict__ x, int d, float eps,
                          const float* __restrict__ g1, T* __restrict__ out1, const float* __restrict__ g2,
                          T* __restrict__ out2) {
+    pdl_launch_dependents();
+    pdl_wait();
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int i = blockIdx.x / kClusterRow;
@@ -99,6 +101,8 @@ __global__ void __cluster_dims__(kClusterRow, 1, 1) __launch_bounds__(kRowThread
 template <typename T>
 __global__ void act_kernel(const float* __restrict__ part, int splits, int64_t split_stride,
                            const int* __restrict__ n_active, int N, int swiglu, T* __restrict__ out) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int n_out = swiglu ? N / 2 : N;
     const int64_t total = (int64_t)(*n_active) * n_out;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -124,6 +128,8 @@ template <typename T>
 __global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ tok,
                              const int* __restrict__ slot_in, const int* __restrict__ pos_in, int batch, int d,
                              RowState st) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int i = blockIdx.x;
     if (i >= batch) return;
     if (threadIdx.x == 0) {
@@ -140,6 +146,8 @@ __global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ 
 __global__ void gather_rows_kernel(const float* __restrict__ x_cur, float* __restrict__ x_nxt,
                                    const uint16_t* __restrict__ h_cur, uint16_t* __restrict__ h_nxt, int h_words,
                                    const int* __restrict__ src, const int* __restrict__ n_active, int d) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int j = blockIdx.x;
     if (j >= *n_active) return;
     const int i = src[j];
@@ -158,11 +166,11 @@ __global__ void gather_rows_kernel(const float* __restrict__ x_cur, float* __res
 void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in,
                   int batch, int d, RowState st, cudaStream_t s) {
     if (dtype == 0)
-        embed_kernel<float><<<batch, 256, 0, s>>>(static_cast<const float*>(emb), tok, slot_in, pos_in, batch, d,
-                                                  st);
+        launch_pdl(embed_kernel<float>, dim3(batch), dim3(256), 0, s, static_cast<const float*>(emb), tok, slot_in,
+                   pos_in, batch, d, st);
     else
-        embed_kernel<__nv_bfloat16><<<batch, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(emb), tok, slot_in,
-                                                          pos_in, batch, d, st);
+        launch_pdl(embed_kernel<__nv_bfloat16>, dim3(batch), dim3(256), 0, s,
+                   static_cast<const __nv_bfloat16*>(emb), tok, slot_in, pos_in, batch, d, st);
     EEB_CHECK_LAUNCH();
 }
 
@@ -173,13 +181,11 @@ void launch_residual_norm(int dtype, const float* part, int splits, int64_t spli
         throw Error(1, "residual_norm: d_model must be a multiple of 8 and at most 16384");
     const dim3 grid(max_rows * kClusterRow);
     if (dtype == 0)
-        residual_norm_kernel<float><<<grid, kRowThreads, 0, s>>>(part, splits, split_stride, n_active, x, d, eps, g1,
-                                                                 static_cast<float*>(out1), g2,
-                                                                 static_cast<float*>(out2));
+        launch_pdl(residual_norm_kernel<float>, grid, dim3(kRowThreads), 0, s, part, splits, split_stride, n_active, x,
+                   d, eps, g1, static_cast<float*>(out1), g2, static_cast<float*>(out2));
     else
-        residual_norm_kernel<__nv_bfloat16><<<grid, kRowThreads, 0, s>>>(
-            part, splits, split_stride, n_active, x, d, eps, g1, static_cast<__nv_bfloat16*>(out1), g2,
-            static_cast<__nv_bfloat16*>(out2));
+        launch_pdl(residual_norm_kernel<__nv_bfloat16>, grid, dim3(kRowThreads), 0, s, part, splits, split_stride,
+                   n_active, x, d, eps, g1, static_cast<__nv_bfloat16*>(out1), g2, static_cast<__nv_bfloat16*>(out2));
     EEB_CHECK_LAUNCH();
 }
 
@@ -189,19 +195,18 @@ void launch_act(int dtype, const float* part, int splits, int64_t split_stride, 
     int64_t blocks = ((int64_t)max_rows * n_out + 255) / 256;
     if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
     if (dtype == 0)
-        act_kernel<float><<<(int)blocks, 256, 0, s>>>(part, splits, split_stride, n_active, N, swiglu ? 1 : 0,
-                                                      static_cast<float*>(out));
+        launch_pdl(act_kernel<float>, dim3((unsigned)blocks), dim3(256), 0, s, part, splits, split_stride, n_active, N,
+                   swiglu ? 1 : 0, static_cast<float*>(out));
     else
-        act_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>(part, splits, split_stride, n_active, N,
-                                                              swiglu ? 1 : 0, static_cast<__nv_bfloat16*>(out));
+        launch_pdl(act_kernel<__nv_bfloat16>, dim3((unsigned)blocks), dim3(256), 0, s, part, splits, split_stride,
+                   n_active, N, swiglu ? 1 : 0, static_cast<__nv_bfloat16*>(out));
     EEB_CHECK_LAUNCH();
 }
 
 void launch_gather_rows(const float* x_cur, float* x_nxt, const void* h_cur, void* h_nxt, int h_bytes_per_row,
                         const int* src, const int* n_active, int max_rows, int d, cudaStream_t s) {
-    gather_rows_kernel<<<max_rows, 256, 0, s>>>(x_cur, x_nxt, static_cast<const uint16_t*>(h_cur),
-                                                static_cast<uint16_t*>(h_nxt), h_bytes_per_row / 2, src, n_active,
-                                                d);
+    launch_pdl(gather_rows_kernel, dim3(max_rows), dim3(256), 0, s, x_cur, x_nxt, static_cast<const uint16_t*>(h_cur),
+               static_cast<uint16_t*>(h_nxt), h_bytes_per_row / 2, src, n_active, d);
     EEB_CHECK_LAUNCH();
 }
 

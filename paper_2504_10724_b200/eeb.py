@@ -64,7 +64,7 @@ EXPORTED = [
     "eeb_decode_step", "eeb_decode_step_device", "eeb_synchronize", "eeb_set_graphs",
     "eeb_set_gemm_tier", "eeb_debug_last_logits", "eeb_debug_retain_logits", "eeb_debug_read_weight",
     "eeb_debug_read_kv", "eeb_profile_enable", "eeb_profile_read", "eeb_stream",
-    "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm",
+    "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm",
 ]
 
 _lib = None
@@ -103,6 +103,8 @@ def load_library() -> C.CDLL:
                                           C.c_void_p, C.c_void_p]
         lib.eeb_debug_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.eeb_debug_bench_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.POINTER(C.c_double)]
         lib.eeb_profile_enable.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_profile_read.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         lib.eeb_nccl_unique_id.argtypes = [C.c_void_p]
@@ -355,6 +357,12 @@ class Context:
         _check(self.lib.eeb_debug_gemm(self.h, tier, dtype, n, k, b, mode, wb.ctypes.data, xb.ctypes.data,
                                        y.ctypes.data))
         return y
+
+    def bench_gemm(self, tier: int, n: int, k: int, batch: int, iters: int = 50) -> float:
+        """Mean ms per launch of one GEMM shape, launched back to back."""
+        ms = C.c_double()
+        _check(self.lib.eeb_debug_bench_gemm(self.h, tier, n, k, batch, iters, C.byref(ms)))
+        return ms.value
 
     def profile_enable(self, on: bool) -> None:
         _check(self.lib.eeb_profile_enable(self.h, 1 if on else 0))
