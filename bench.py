@@ -282,7 +282,7 @@ def run_eeb(args, desc):
     h_bytes = head_bytes(desc, B) * ne
     roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1)",
             "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
-            "traffic": None, "peak_source": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy burst)",
+            "traffic": None, "peak_source": ("measured MEASURED_PEAKS.json hbm_gbs (copy burst)" if pk_kind == "measured" else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"),
             "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
             "step_share": gemm_ms / max(1e-9, gemm_ms + head_ms + attn_ms + prof["norm_ms"] / nsteps
                                         + prof["other_ms"] / nsteps)}
@@ -304,12 +304,16 @@ def run_eeb(args, desc):
     d2h = B * (4 + 4 + 4 + 4 + 1 + 1) + ne * 8 + 8 + 8
 
     # ---- profiler histogram all-reduce across replicas (the one collective) ---
-    hist_total = hist_acc.cpu().numpy()
+    from paper_2504_10724_b200 import replicas
+
+    prof_counters = replicas.ProfileCounters(desc.exit_layers, hist=hist_acc.cpu().numpy())
+    prof_counters.tokens = int(prof_counters.hist.sum())
     if world > 1:
         uid = [eeb.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.nccl_init(uid[0], world, rank)
-        hist_total, _ = ctx.profile_allreduce(hist_total, 0.0)
+        prof_counters.allreduce(replicas.eeb_allreduce(ctx))
+    hist_total = prof_counters.hist
     exit_frac = {str(l): float(c) / max(1, hist_total.sum()) for l, c in zip(desc.exit_layers, hist_total)}
 
     cpu = None

@@ -22,6 +22,44 @@ static int fail(const char* m) {
 }
 
 /* ---------------------------------------------------------------------------
+ * The reference's per-token decision over one complete record (every head
+ * observed, ascending layers, last = final head):
+ *   flat          observation_for_depth  trace.hpp:86-97, exit = depth, breached = conf < th  engine.hpp:350-354
+ *   introspective earliest_confident_obs trace.hpp:69-76 (>=), exit = obs.layer               engine.hpp:355-359
+ *   full depth    observations.back(), exit = num_layers, never breached                      engine.hpp:360-364
+ *   unchanged     obs.token == final token                                                    engine.hpp:366
+ * Returns the index of the observation used, or -1 (DomainError) when flat
+ * finds no head at or below the depth (trace.hpp:92-93).
+ * ------------------------------------------------------------------------- */
+int orc_decide(int policy, int n, const int32_t* layers, const int32_t* toks, const float* confs, float th,
+               int depth, int num_layers, orc_decision* out) {
+    int idx = -1;
+    if (n <= 0) return fail("token record has no observations");
+    if (policy == 0) {
+        for (int k = 0; k < n; ++k) {
+            if (layers[k] == depth) { idx = k; break; }
+            if (layers[k] < depth) idx = k;
+        }
+        if (idx < 0) return fail("no observation at or below the serving depth");
+        out->exit_layer = depth;
+        out->breached = confs[idx] < th;
+    } else if (policy == 2) {
+        idx = n - 1;
+        out->exit_layer = num_layers;
+        out->breached = 0;
+    } else {
+        idx = n - 1;
+        for (int k = 0; k < n; ++k)
+            if (confs[k] >= th) { idx = k; break; }
+        out->exit_layer = layers[idx];
+        out->breached = confs[idx] < th;
+    }
+    out->index = idx;
+    out->unchanged = toks[idx] == toks[n - 1];
+    return idx;
+}
+
+/* ---------------------------------------------------------------------------
  * Synthetic model definition (restated).
  * ------------------------------------------------------------------------- */
 #define U_SCALE 3.46410161513775f /* 2*sqrt(3): unit variance */
@@ -454,15 +492,15 @@ int orc_decode_step(orc_model* m, int depth, int policy, float th, int batch, co
                         out->head_confidence[(size_t)r * NE + e] = o.conf;
                         out->head_logprob[(size_t)r * NE + e] = o.logp;
                         if (!is_final) { done = 0; break; }
-                        int ex = NE - 1;
-                        for (int k = 0; k < NE; ++k)
-                            if (out->head_confidence[(size_t)r * NE + k] >= th) { ex = k; break; }
+                        orc_decision dec;
+                        const int ex = orc_decide(1, NE, d->exit_layers, out->head_token + (size_t)r * NE,
+                                                  out->head_confidence + (size_t)r * NE, th, depth, L, &dec);
                         used.tok = out->head_token[(size_t)r * NE + ex];
                         used.conf = out->head_confidence[(size_t)r * NE + ex];
                         used.logp = out->head_logprob[(size_t)r * NE + ex];
-                        exit_layer = d->exit_layers[ex];
-                        brd = used.conf < th;
-                        unch = used.tok == o.tok;
+                        exit_layer = dec.exit_layer;
+                        brd = dec.breached;
+                        unch = dec.unchanged;
                         bin[r] = ex;
                         break;
                     }
@@ -491,7 +529,7 @@ int orc_decode_step(orc_model* m, int depth, int policy, float th, int batch, co
         out->hist[bin[r]] += 1;
         nb += out->breached[r];
         sl += (double)out->logprob[r];
-        m->kv_depth[(size_t)slots[r] * S + positions[r]] = (uint8_t)out->exit_layer[r];
+        m->kv_depth[(size_t)slots[r] * S + positions[r]] = (uint8_t)(policy == 3 ? L : out->exit_layer[r]);
     }
     *out->n_breached = nb;
     *out->sum_logprob = sl;

@@ -77,6 +77,11 @@ typedef struct {
 int orc_decode_step(orc_model* m, int serving_depth, int policy, float th, int batch,
                     const int32_t* slots, const int32_t* tokens, const int32_t* positions,
                     orc_out* out);
+/* The reference's per-token exit rule over one complete ModelTokenRecord
+ * (policy 0 flat / 1 introspective / 2 full depth / 3 = 1), see eeb_oracle.c. */
+typedef struct { int index, exit_layer, breached, unchanged; } orc_decision;
+int orc_decide(int policy, int n, const int32_t* layers, const int32_t* toks, const float* confs, float th,
+               int depth, int num_layers, orc_decision* out);
 /* K/V of one position, [n_kv_heads][head_dim] each. */
 int orc_read_kv(const orc_model* m, int layer, int slot, int pos, float* k, float* v);
 const char* orc_last_error(void);

@@ -34,6 +34,26 @@ class _Out(C.Structure):
         "n_breached", "sum_logprob", "head_token", "head_confidence", "head_logprob", "logits_out")]
 
 
+class _Decision(C.Structure):
+    _fields_ = [("index", C.c_int), ("exit_layer", C.c_int), ("breached", C.c_int), ("unchanged", C.c_int)]
+
+
+def decide(policy: int, layers, tokens, confidences, th: float, depth: int = 0, num_layers: int | None = None):
+    """The reference's per-token exit rule over one complete record (orc_decide).
+
+    Returns (index of the observation used, exit_layer, breached, unchanged);
+    raises ValueError where the reference throws DomainError."""
+    layers = np.ascontiguousarray(layers, np.int32)
+    tokens = np.ascontiguousarray(tokens, np.int32)
+    confs = np.ascontiguousarray(confidences, np.float32)
+    d = _Decision()
+    rc = lib().orc_decide(policy, len(layers), layers.ctypes.data, tokens.ctypes.data, confs.ctypes.data,
+                          float(th), depth, int(num_layers if num_layers is not None else layers[-1]), C.byref(d))
+    if rc < 0:
+        raise ValueError(lib().orc_last_error().decode())
+    return d.index, d.exit_layer, bool(d.breached), bool(d.unchanged)
+
+
 def build() -> None:
     subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
 
@@ -59,6 +79,8 @@ def lib() -> C.CDLL:
                                       C.c_void_p, C.c_void_p, C.POINTER(_Out)]
         L.orc_read_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_last_error.restype = C.c_char_p
+        L.orc_decide.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_int,
+                                 C.c_int, C.POINTER(_Decision)]
         _lib = L
     return _lib
 

@@ -630,7 +630,8 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
     }
     {
         Timer t(c, kCatOther);
-        launch_finalize(batch, d.n_exits, o, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len, s);
+        launch_finalize(batch, d.n_exits, o, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len,
+                        policy == EEB_PROFILE ? L : 0, s);
         count(c, kCatOther, 1);
     }
 }

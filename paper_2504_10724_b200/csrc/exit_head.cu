@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
 // count, fixed-order f64 logprob sum, KV depth map update.
 __global__ void __launch_bounds__(1024)
     finalize_kernel(int batch, int n_exits, StepOutDev o, const int* __restrict__ slot_in,
-                    const int* __restrict__ pos_in, uint8_t* __restrict__ kv_depth, int max_seq) {
+                    const int* __restrict__ pos_in, uint8_t* __restrict__ kv_depth, int max_seq,
+                    int computed_depth) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ unsigned long long hist_s[64];
@@ -194,7 +195,10 @@ __global__ void __launch_bounds__(1024)
         const int b = o.bin[r];
         if (b >= 0 && b < n_exits) atomicAdd(&hist_s[b], 1ull);
         my_breach += o.breached[r] ? 1 : 0;
-        kv_depth[(int64_t)slot_in[r] * max_seq + pos_in[r]] = (uint8_t)o.exit_layer[r];
+        // layers whose K/V this step wrote for the row: its exit layer, or every
+        // layer in the profiling pass (all heads at full depth)
+        kv_depth[(int64_t)slot_in[r] * max_seq + pos_in[r]] =
+            (uint8_t)(computed_depth > 0 ? computed_depth : o.exit_layer[r]);
     }
     atomicAdd(&breach_s, my_breach);
     __syncthreads();
@@ -225,9 +229,10 @@ void launch_decide(const DecideArgs& a, cudaStream_t s) {
 }
 
 void launch_finalize(int batch, int n_exits, StepOutDev out, const int* slot_in, const int* pos_in,
-                     uint8_t* kv_depth, int max_seq, cudaStream_t s) {
+                     uint8_t* kv_depth, int max_seq, int computed_depth, cudaStream_t s) {
     if (n_exits > 64) throw Error(1, "finalize: at most 64 exits");
-    launch_pdl(finalize_kernel, dim3(1), dim3(1024), 0, s, batch, n_exits, out, slot_in, pos_in, kv_depth, max_seq);
+    launch_pdl(finalize_kernel, dim3(1), dim3(1024), 0, s, batch, n_exits, out, slot_in, pos_in, kv_depth, max_seq,
+               computed_depth);
     EEB_CHECK_LAUNCH();
 }
 

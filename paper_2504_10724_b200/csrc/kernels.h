@@ -136,8 +136,9 @@ void launch_decide(const DecideArgs& a, cudaStream_t s);
 void launch_gather_rows(const float* x_cur, float* x_nxt, const void* h_cur, void* h_nxt, int h_bytes_per_row,
                         const int* src, const int* n_active, int max_rows, int d, cudaStream_t s);
 // Histogram (K4), breach count and fixed-order logprob sum over `batch` rows;
-// records each row's computed depth in the KV depth map.
+// records each row's computed depth in the KV depth map (its exit layer, or
+// computed_depth when > 0: the profiling pass runs every row to full depth).
 void launch_finalize(int batch, int n_exits, StepOutDev out, const int* slot_in, const int* pos_in,
-                     uint8_t* kv_depth, int max_seq, cudaStream_t s);
+                     uint8_t* kv_depth, int max_seq, int computed_depth, cudaStream_t s);
 
 }  // namespace eeb
