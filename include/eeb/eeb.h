@@ -146,8 +146,11 @@ eeb_status eeb_synchronize(eeb_ctx* ctx);
  * reuse it on later identical calls (0 = off, 1 = on; default on). */
 eeb_status eeb_set_graphs(eeb_ctx* ctx, int enable);
 
-/* Kernel tier override for tests: 0 = auto, 1 = CUDA-core GEMV only,
- * 2 = tcgen05 tensor-core GEMM where applicable. */
+/* Kernel tier override for tests: 0 = auto (the persistent step kernel where
+ * applicable — bf16, head_dim 64, batch <= 128, max_seq_len <= 256 — else the
+ * per-op kernel chain), 1 = per-op chain with CUDA-core GEMV only, 2 = per-op
+ * chain with tcgen05 GEMMs where applicable, 3 = persistent step kernel
+ * (EEB_E_DOMAIN if not applicable). */
 eeb_status eeb_set_gemm_tier(eeb_ctx* ctx, int tier);
 
 /* Test/diagnostic hooks (not used on the serving path). */
@@ -169,6 +172,11 @@ eeb_status eeb_debug_gemm(eeb_ctx* ctx, int tier, int dtype, int n, int k, int b
  * (PDL-chained, like inside a step) on device-resident random data; returns the
  * mean milliseconds per launch (CUDA events on the context stream). */
 eeb_status eeb_debug_bench_gemm(eeb_ctx* ctx, int tier, int n, int k, int batch, int iters, double* ms_out);
+
+/* Steady-state timing of the persistent step kernel streaming every loaded
+ * layer's four GEMMs of `model` (zero activations, `batch` rows); returns the
+ * mean milliseconds per launch. */
+eeb_status eeb_debug_bench_layers(eeb_ctx* ctx, int model, int batch, int iters, double* ms_out);
 
 /* Per-kernel timing of the last step (CUDA events on the context stream).
  * names: "gemm", "attention", "exit_head", ... ; returns total ms. */

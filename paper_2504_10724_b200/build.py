@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     f"-I{ROOT / 'include'}",
 ]
 SOURCES = ["synth_kernels.cu", "rows.cu", "gemm_cc.cu", "gemm_tc.cu", "attention.cu",
-           "exit_head.cu", "eeb_api.cu"]
+           "exit_head.cu", "step_mk.cu", "eeb_api.cu"]
 
 
 def _deps(src: Path) -> list[Path]:

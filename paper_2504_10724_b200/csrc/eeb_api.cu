@@ -23,6 +23,7 @@
 
 #include "../../include/eeb/eeb.h"
 #include "kernels.h"
+#include "step_mk.cuh"
 #include "synth.cuh"
 
 namespace eeb {
@@ -84,6 +85,14 @@ struct GraphKey {
 };
 
 enum Cat { kCatGemm = 0, kCatAttn, kCatHead, kCatNorm, kCatOther, kNumCat };
+
+// A compiled persistent-kernel program for one (model, depth, policy, batch, th).
+struct MkProg {
+    DevBuf phases, maps, segtab, gains;
+    mk::Params P{};
+    int n_gemm = 0;
+    int64_t weight_bytes = 0;  // algorithmic weight bytes streamed per launch
+};
 const char* kCatNames[kNumCat] = {"layer_gemm", "attention", "exit_head", "norm", "other"};
 
 }  // namespace
@@ -121,6 +130,14 @@ struct eeb_ctx {
     int64_t steps_profiled = 0;
     ncclComm_t nccl = nullptr;
     eeb::DevBuf nccl_buf;
+    // persistent step kernel
+    int mk_mode = -1;  // -1 unset (env EEB_MK, default on), 0 off, 1 on
+    std::map<eeb::GraphKey, std::unique_ptr<eeb::MkProg>> mk_progs;
+    eeb::DevBuf mk_partials, mk_bar, mk_stats;
+    unsigned long long mk_bar_count = 0;
+    int last_step_mk = 0;
+    int64_t last_step_weight_bytes = 0;
+    double mk_ms = 0;  // profiled persistent-kernel time
 };
 
 namespace eeb {
@@ -230,6 +247,7 @@ void validate_desc(const eeb_model_desc& d) {
 // ---------------------------------------------------------------------------
 void load_to(eeb_ctx* c, Model& m, int to) {
     const eeb_model_desc& d = m.desc;
+    c->mk_progs.clear();  // compiled persistent programs hold weight pointers
     if (to < 0 || to > d.num_layers)
         throw Error(EEB_E_DOMAIN, "load: depth " + std::to_string(to) + " outside [0, " +
                                       std::to_string(d.num_layers) + "]");
@@ -325,6 +343,7 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     if (R > c->cap_rows) {
         for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
         c->graphs.clear();
+        c->mk_progs.clear();  // programs hold workspace pointers
     }
     c->cap_rows = R;
     c->xA.ensure((size_t)R * D * 4);
@@ -654,8 +673,249 @@ void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int 
     (void)c;
 }
 
+// ---------------------------------------------------------------------------
+// Persistent step kernel: applicability, program compilation, launch.
+// ---------------------------------------------------------------------------
+bool mk_applicable(eeb_ctx* c, const Model& m, int batch) {
+    if (c->mk_mode < 0) {
+        const char* env = std::getenv("EEB_MK");
+        c->mk_mode = env && env[0] == '0' ? 0 : 1;
+    }
+    const eeb_model_desc& d = m.desc;
+    const bool ok = !c->retain_logits && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
+                    batch <= mk::kMaxRows && d.max_seq_len <= 256 && gemm_tc_available();
+    if (c->gemm_tier == 3) {
+        if (!ok) throw Error(EEB_E_DOMAIN, "persistent step kernel requested but not applicable to this model/batch");
+        return true;
+    }
+    return ok && c->gemm_tier == 0 && c->mk_mode == 1;
+}
+
+std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, float th, int batch) {
+    const eeb_model_desc& d = m.desc;
+    const int L = d.num_layers, D = d.d_model, F = d.d_ffn, G = c->num_sms;
+    const int bpad = std::max(16, (batch + 15) / 16 * 16);
+    auto P = std::make_unique<MkProg>();
+    std::vector<CUtensorMap> maps;
+    auto add_map = [&](const void* ptr, int rows, int cols, int box) {
+        maps.emplace_back();
+        make_bf16_map(&maps.back(), ptr, rows, cols, box);
+        return (int)maps.size() - 1;
+    };
+    const int m_h = add_map(c->hn.p, batch, D, bpad);
+    const int m_attn = add_map(c->attn.p, batch, m.dq, bpad);
+    const int m_hmid = add_map(c->mlp_h.p, batch, F, bpad);
+    const int m_hh = add_map(c->hhead.p, batch, D, bpad);
+
+    std::vector<int> heads;
+    int run_layers = L;
+    if (policy == EEB_FLAT) {
+        int e_used = -1;
+        for (int e = 0; e < d.n_exits; ++e)
+            if (m.exits[e] <= depth) e_used = e;
+        heads.push_back(e_used);
+        run_layers = depth;
+    } else if (policy == EEB_FULL_DEPTH) {
+        heads.push_back(d.n_exits - 1);
+    } else {
+        for (int e = 0; e < d.n_exits; ++e) heads.push_back(e);
+    }
+
+    std::vector<mk::Phase> ph;
+    std::vector<int4> seg;
+    auto simt = [&](int kind, int layer, int src) {
+        mk::Phase x{};
+        x.kind = kind;
+        x.layer = layer;
+        x.src = src;
+        ph.push_back(x);
+        return (int)ph.size() - 1;
+    };
+    auto gemm = [&](int wmap, int xmap, int N, int K) {
+        mk::Phase x{};
+        x.kind = mk::kPhaseGemm;
+        x.src = -1;
+        x.wmap = wmap;
+        x.xmap = xmap;
+        x.N = N;
+        x.K = K;
+        x.kb = K / mk::kBK;
+        x.tiles = (N + mk::kBM - 1) / mk::kBM;
+        x.total = x.kb * x.tiles;
+        const int Gp = std::min(G, x.total);  // CTAs with work in this phase (mirrors cta_range)
+        auto s_of = [&](int cc) { return cc >= Gp ? x.total : (int)(((long long)x.total * cc) / Gp); };
+        int max_tiles = 0;
+        for (int cc = 0; cc < Gp; ++cc) {
+            const int s0 = s_of(cc), e0 = s_of(cc + 1);
+            if (e0 > s0) max_tiles = std::max(max_tiles, (e0 - 1) / x.kb - s0 / x.kb + 1);
+        }
+        if (max_tiles > mk::kMaxSeg) throw Error(EEB_E_DOMAIN, "persistent kernel: too many segments per CTA");
+        x.pad[0] = (int)seg.size();
+        for (int t = 0; t < x.tiles; ++t) {
+            const int k0 = t * x.kb, k1 = k0 + x.kb;
+            int c0 = 0;
+            while (c0 + 1 < Gp && s_of(c0 + 1) <= k0) ++c0;
+            int n = 0;
+            for (int cc = c0; cc < Gp && s_of(cc) < k1; ++cc) ++n;
+            seg.push_back(make_int4(c0, t - s_of(c0) / x.kb, n, 0));
+        }
+        P->n_gemm++;
+        P->weight_bytes += (int64_t)N * K * 2;
+        ph.push_back(x);
+        return (int)ph.size() - 1;
+    };
+    auto norm = [&](int layer, int src, int gain, int flags) {
+        const int i = simt(mk::kPhaseNorm, layer, src);
+        ph[i].gain = gain;
+        ph[i].flags = flags;
+        return i;
+    };
+    norm(1, -1, 0, mk::kFlagEmbed);
+    size_t hi = 0;
+    int down = -1;
+    bool x_current = true;  // x already holds the residual (embedding or a head's norm reduced it)
+    for (int l = 1; l <= run_layers; ++l) {
+        const LayerWeights& W = *m.layers[l - 1];
+        if (l > 1) norm(l, x_current ? -1 : down, l - 1, 0);
+        const int qkv = gemm(add_map(W.wqkv.p, m.dq + 2 * m.dkv, D, mk::kBM), m_h, m.dq + 2 * m.dkv, D);
+        simt(mk::kPhaseAttn, l, qkv);
+        const int o = gemm(add_map(W.wo.p, D, m.dq, mk::kBM), m_attn, D, m.dq);
+        norm(l, o, L + l - 1, 0);
+        const int up = gemm(add_map(W.wup.p, m.up_rows, D, mk::kBM), m_h, m.up_rows, D);
+        simt(mk::kPhaseAct, l, up);
+        down = gemm(add_map(W.wdown.p, D, F, mk::kBM), m_hmid, D, F);
+        x_current = false;
+        bool normed = false;
+        while (hi < heads.size() && m.exits[heads[hi]] == l) {
+            const int e = heads[hi];
+            if (!normed) norm(l, down, 2 * L + e, mk::kFlagOutHead);
+            normed = true;
+            x_current = true;
+            const int hg = gemm(add_map(m.head[e]->p, d.vocab, D, mk::kBM), m_hh, d.vocab, D);
+            const int hr = simt(mk::kPhaseHeadReduce, l, hg);
+            ph[hr].exit_index = e;
+            const int dc = simt(mk::kPhaseDecide, l, -1);
+            ph[dc].exit_index = e;
+            ph[dc].exit_layer = m.exits[e];
+            ph[dc].flags = hi + 1 == heads.size() ? mk::kFlagFinal : 0;
+            ++hi;
+        }
+    }
+    simt(mk::kPhaseFinalize, run_layers, -1);
+
+    P->maps.ensure(maps.size() * sizeof(CUtensorMap));
+    EEB_CUDA(cudaMemcpy(P->maps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    P->phases.ensure(ph.size() * sizeof(mk::Phase));
+    EEB_CUDA(cudaMemcpy(P->phases.p, ph.data(), ph.size() * sizeof(mk::Phase), cudaMemcpyHostToDevice));
+    P->segtab.ensure(seg.size() * sizeof(int4));
+    EEB_CUDA(cudaMemcpy(P->segtab.p, seg.data(), seg.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    std::vector<const float*> gains;
+    for (int l = 0; l < L; ++l) gains.push_back(l < (int)m.layers.size() ? m.layers[l]->attn_norm.as<float>() : nullptr);
+    for (int l = 0; l < L; ++l) gains.push_back(l < (int)m.layers.size() ? m.layers[l]->mlp_norm.as<float>() : nullptr);
+    for (int e = 0; e < d.n_exits; ++e) gains.push_back(m.head_norm[e]->as<float>());
+    P->gains.ensure(gains.size() * sizeof(float*));
+    EEB_CUDA(cudaMemcpy(P->gains.p, gains.data(), gains.size() * sizeof(float*), cudaMemcpyHostToDevice));
+
+    // shared workspace of the context
+    c->mk_partials.ensure((size_t)G * mk::kMaxSeg * bpad * mk::kBM * 4);
+    c->mk_stats.ensure((size_t)bpad * 16);
+    if (!c->mk_bar.p) {
+        c->mk_bar.ensure(64);
+        EEB_CUDA(cudaMemset(c->mk_bar.p, 0, 64));
+    }
+
+    mk::Params& q = P->P;
+    q.phases = P->phases.as<mk::Phase>();
+    q.n_phases = (int)ph.size();
+    q.maps = P->maps.as<CUtensorMap>();
+    q.partials = c->mk_partials.as<float>();
+    q.bar = c->mk_bar.as<unsigned>();
+    q.batch = batch;
+    q.bpad = bpad;
+    q.x_stages = 4;
+    while ((size_t)q.x_stages * bpad * mk::kBK * 2 < (size_t)mk::kSimtWarps * (8 * 64 + 128) * 4) ++q.x_stages;
+    int ws = 2;
+    while (mk::smem_bytes(bpad, ws + 1, q.x_stages, q.n_phases) <= 227u * 1024u) ++ws;
+    if (ws < 3) throw Error(EEB_E_DOMAIN, "persistent kernel: program too large for shared memory");
+    q.w_stages = ws;
+    q.bar_mode = 0;
+    q.D = D;
+    q.F = F;
+    q.dq = m.dq;
+    q.dkv = m.dkv;
+    q.H = d.n_heads;
+    q.Hkv = d.n_kv_heads;
+    q.hd = m.head_dim;
+    q.V = d.vocab;
+    q.S = d.max_seq_len;
+    q.L = L;
+    q.n_exits = d.n_exits;
+    q.mlp_kind = d.mlp_kind;
+    q.policy = policy;
+    q.serving_depth = depth;
+    q.eps = d.norm_eps;
+    q.th = th;
+    q.emb = static_cast<const __nv_bfloat16*>(m.emb.p);
+    q.gains = P->gains.as<const float*>();
+    q.k_cache = static_cast<__nv_bfloat16*>(m.k_cache.p);
+    q.v_cache = static_cast<__nv_bfloat16*>(m.v_cache.p);
+    q.kv_layer_elems = (long long)m.kv_layer_elems;
+    q.kv_depth = m.kv_depth.as<uint8_t>();
+    q.rope_cos = m.rope_cos.as<float>();
+    q.rope_sin = m.rope_sin.as<float>();
+    Ints I = ints_of(c);
+    q.tok = I.tok;
+    q.slot = I.slot;
+    q.pos = I.pos;
+    q.x = c->xA.as<float>();
+    q.h = static_cast<__nv_bfloat16*>(c->hn.p);
+    q.hh = static_cast<__nv_bfloat16*>(c->hhead.p);
+    q.attn = static_cast<__nv_bfloat16*>(c->attn.p);
+    q.hmid = static_cast<__nv_bfloat16*>(c->mlp_h.p);
+    q.stats = c->mk_stats.as<float4>();
+    q.out = out_dev(c);
+    for (int k = 0; k < 64; ++k) q.exit_layers[k] = k < d.n_exits ? m.exits[k] : 0;
+    return P;
+}
+
+void run_step_mk(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
+    Model& m = model_of(c, mi);
+    uint32_t thb;
+    std::memcpy(&thb, &th, 4);
+    GraphKey key{mi, policy == EEB_FLAT ? depth : 0, policy, batch, 100 + m.loaded, thb};
+    auto it = c->mk_progs.find(key);
+    if (it == c->mk_progs.end()) it = c->mk_progs.emplace(key, mk_build(c, m, depth, policy, th, batch)).first;
+    MkProg& P = *it->second;
+    P.P.bar_base = c->mk_bar_count;
+    c->mk_bar_count += (unsigned long long)(P.P.n_phases - 1) * c->num_sms;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) {
+        EEB_CUDA(cudaEventCreate(&e0));
+        EEB_CUDA(cudaEventCreate(&e1));
+        EEB_CUDA(cudaEventRecord(e0, c->stream));
+    }
+    mk::launch(P.P, P.segtab.as<int4>(), c->num_sms, c->stream);
+    if (c->profiling) {
+        EEB_CUDA(cudaEventRecord(e1, c->stream));
+        EEB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        EEB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        c->mk_ms += ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    c->step_launches = 1;
+    c->last_step_mk = 1;
+    c->last_step_weight_bytes = P.weight_bytes;
+}
+
 void run_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
     Model& m = model_of(c, mi);
+    if (mk_applicable(c, m, batch)) {
+        run_step_mk(c, mi, depth, policy, th, batch);
+        return;
+    }
+    c->last_step_mk = 0;
     const bool use_graph = c->graphs_enabled && !c->profiling && !c->retain_logits;
     if (!use_graph) {
         c->step_launches = 0;
@@ -976,7 +1236,7 @@ eeb_status eeb_set_graphs(eeb_ctx* c, int enable) {
 eeb_status eeb_set_gemm_tier(eeb_ctx* c, int tier) {
     return guarded([&] {
         if (!c) throw Error(EEB_E_DOMAIN, "null context");
-        if (tier < 0 || tier > 2) throw Error(EEB_E_DOMAIN, "tier must be 0, 1 or 2");
+        if (tier < 0 || tier > 3) throw Error(EEB_E_DOMAIN, "tier must be 0, 1, 2 or 3");
         c->gemm_tier = tier;
     });
 }
@@ -1132,24 +1392,95 @@ eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int bat
     });
 }
 
+eeb_status eeb_debug_bench_layers(eeb_ctx* c, int model, int batch, int iters, double* ms_out) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const eeb_model_desc& d = m.desc;
+        if (!ms_out || batch < 1 || batch > mk::kMaxRows || iters <= 0) throw Error(EEB_E_DOMAIN, "bad argument");
+        if (d.dtype != EEB_BF16) throw Error(EEB_E_DOMAIN, "persistent step kernel: bf16 models only");
+        if (m.loaded < 1) throw Error(EEB_E_CAPACITY, "no layers resident");
+        EEB_CUDA(cudaSetDevice(c->device));
+        ensure_workspace(c, m, batch);
+        // The FULL_DEPTH program minus every non-GEMM phase: the weight stream alone.
+        std::unique_ptr<MkProg> P = mk_build(c, m, 0, EEB_FULL_DEPTH, 0.5f, batch);
+        std::vector<mk::Phase> ph(P->P.n_phases);
+        EEB_CUDA(cudaMemcpy(ph.data(), P->phases.p, ph.size() * sizeof(mk::Phase), cudaMemcpyDeviceToHost));
+        std::vector<mk::Phase> g;
+        for (auto& x : ph)
+            if (x.kind == mk::kPhaseGemm && x.N != d.vocab) g.push_back(x);
+        EEB_CUDA(cudaMemcpy(P->phases.p, g.data(), g.size() * sizeof(mk::Phase), cudaMemcpyHostToDevice));
+        mk::Params& q = P->P;
+        q.n_phases = (int)g.size();
+        int ws = 2;
+        while (mk::smem_bytes(q.bpad, ws + 1, q.x_stages, q.n_phases) <= 227u * 1024u) ++ws;
+        q.w_stages = ws;
+        if (const char* v = std::getenv("EEB_MK_WSTAGES")) q.w_stages = std::min(ws, std::max(2, std::atoi(v)));
+        q.bar_mode = std::getenv("EEB_MK_BAR") ? std::atoi(std::getenv("EEB_MK_BAR")) : 0;
+        q.dbg = std::getenv("EEB_MK_DBG") ? std::atoi(std::getenv("EEB_MK_DBG")) : 0;
+        DevBuf trace;
+        const char* trace_path = std::getenv("EEB_MK_TRACE");
+        if (trace_path) {
+            trace.ensure((size_t)c->num_sms * g.size() * 8 * 8);
+            q.trace = trace.as<unsigned long long>();
+        }
+        auto launch_once = [&] {
+            q.bar_base = c->mk_bar_count;
+            c->mk_bar_count += (unsigned long long)(q.n_phases - 1) * c->num_sms;
+            mk::launch(q, P->segtab.as<int4>(), c->num_sms, c->stream);
+        };
+        for (int i = 0; i < 2; ++i) launch_once();
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        cudaEvent_t e0, e1;
+        EEB_CUDA(cudaEventCreate(&e0));
+        EEB_CUDA(cudaEventCreate(&e1));
+        EEB_CUDA(cudaEventRecord(e0, c->stream));
+        for (int i = 0; i < iters; ++i) launch_once();
+        EEB_CUDA(cudaEventRecord(e1, c->stream));
+        EEB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        EEB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *ms_out = ms / iters;
+        if (trace_path) {
+            std::vector<unsigned long long> h(trace.bytes / 8);
+            EEB_CUDA(cudaMemcpy(h.data(), trace.p, trace.bytes, cudaMemcpyDeviceToHost));
+            if (FILE* f = std::fopen(trace_path, "wb")) {
+                std::fwrite(h.data(), 8, h.size(), f);
+                std::fclose(f);
+            }
+        }
+    });
+}
+
 eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, int iters, double* ms_out) {
     return guarded([&] {
         if (!c || !ms_out || n <= 0 || k <= 0 || batch <= 0 || iters <= 0) throw Error(EEB_E_DOMAIN, "bad argument");
         EEB_CUDA(cudaSetDevice(c->device));
-        DevBuf w, x, ws, na;
-        w.ensure((size_t)n * k * 2);
+        // Rotate over enough distinct weight copies (>= 512 MB, 4x L2) that every
+        // launch streams its weights from HBM, as in the step.
+        DevBuf x, ws, na;
+        const size_t wbytes = (size_t)n * k * 2;
+        const int nbuf = (int)std::max<size_t>(1, ((size_t)512 << 20) / wbytes + 1);
+        std::vector<std::unique_ptr<DevBuf>> wv;
+        for (int i = 0; i < nbuf; ++i) {
+            wv.push_back(std::make_unique<DevBuf>());
+            wv.back()->ensure(wbytes);
+            synth_linear(EEB_BF16, wv.back()->p, 1 + i, 1, n, k, 0.02f, false, k, c->stream);
+        }
         x.ensure((size_t)batch * k * 2);
         const int64_t plane = (int64_t)batch * n;
         const int max_planes = std::max(k / 128 + 2, c->num_sms + 1);
         ws.ensure((size_t)plane * max_planes * 4);
         na.ensure(4);
-        synth_linear(EEB_BF16, w.p, 1, 1, n, k, 0.02f, false, k, c->stream);
         synth_linear(EEB_BF16, x.p, 2, 1, batch, k, 1.0f, false, k, c->stream);
         EEB_CUDA(cudaMemcpy(na.p, &batch, 4, cudaMemcpyHostToDevice));
         GemmArgs a;
-        a.dtype = EEB_BF16; a.W = w.p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
+        a.dtype = EEB_BF16; a.W = wv[0]->p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
         a.out = ws.as<float>(); a.plane_stride = plane; a.max_planes = max_planes; a.num_sms = c->num_sms;
+        int it = 0;
         auto run = [&] {
+            a.W = wv[it++ % nbuf]->p;
             if (tier == 2) {
                 if (gemm_tc(a, c->stream) == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
             } else {
@@ -1176,6 +1507,7 @@ eeb_status eeb_profile_enable(eeb_ctx* c, int enable) {
     return guarded([&] {
         if (!c) throw Error(EEB_E_DOMAIN, "null context");
         c->profiling = enable ? 1 : 0;
+        c->mk_ms = 0;
         for (int k = 0; k < kNumCat; ++k) { c->cat_ms[k] = 0; c->cat_launches[k] = 0; }
         c->steps_profiled = 0;
     });
@@ -1185,7 +1517,9 @@ eeb_status eeb_profile_read(eeb_ctx* c, char* json_out, int64_t cap) {
     return guarded([&] {
         if (!c || !json_out) throw Error(EEB_E_DOMAIN, "null argument");
         std::string j = "{\"steps\": " + std::to_string(c->steps_profiled) + ", \"last_step_launches\": " +
-                        std::to_string(c->step_launches);
+                        std::to_string(c->step_launches) + ", \"persistent\": " + std::to_string(c->last_step_mk) +
+                        ", \"persistent_ms\": " + std::to_string(c->mk_ms) + ", \"weight_bytes\": " +
+                        std::to_string(c->last_step_weight_bytes);
         for (int k = 0; k < kNumCat; ++k) {
             char buf[160];
             std::snprintf(buf, sizeof buf, ", \"%s_ms\": %.6f, \"%s_launches\": %lld", kCatNames[k], c->cat_ms[k],

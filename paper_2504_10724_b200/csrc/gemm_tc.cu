@@ -275,6 +275,11 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int box_rows) {
 
 bool gemm_tc_available() { return encode_fn() != nullptr; }
 
+void make_bf16_map(void* out_map, const void* ptr, int rows, int cols, int box_rows) {
+    if (!encode_fn()) throw Error(5, "cuTensorMapEncodeTiled unavailable");
+    *static_cast<CUtensorMap*>(out_map) = make_map(ptr, rows, cols, box_rows);
+}
+
 void make_kv_tensor_map(void* out_map, const void* base, int head_dim, int max_seq, int slots_x_heads,
                         int box_rows) {
     if (!encode_fn()) throw Error(5, "cuTensorMapEncodeTiled unavailable");

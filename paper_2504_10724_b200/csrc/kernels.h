@@ -60,6 +60,9 @@ int gemm_cc(const GemmArgs& a, cudaStream_t s);
 // Tier 2: tcgen05 + TMA (bf16, 16..256 rows).  Returns planes, 0 if not applicable.
 int gemm_tc(const GemmArgs& a, cudaStream_t s);
 bool gemm_tc_available();
+// 2-D TMA map over a row-major bf16 [rows][cols] matrix, box {64 cols, box_rows},
+// 128-byte swizzle (the K-major UMMA operand layout).  out_map: 128 B.
+void make_bf16_map(void* out_map, const void* ptr, int rows, int cols, int box_rows);
 // 3-D TMA map over one layer's bf16 KV cache [slots*Hkv][max_seq][head_dim],
 // box {64 dims, box_rows positions, 1}, 128-byte swizzle.  out_map: 128 B.
 void make_kv_tensor_map(void* out_map, const void* base, int head_dim, int max_seq, int slots_x_heads,

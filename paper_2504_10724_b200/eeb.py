@@ -64,7 +64,7 @@ EXPORTED = [
     "eeb_decode_step", "eeb_decode_step_device", "eeb_synchronize", "eeb_set_graphs",
     "eeb_set_gemm_tier", "eeb_debug_last_logits", "eeb_debug_retain_logits", "eeb_debug_read_weight",
     "eeb_debug_read_kv", "eeb_profile_enable", "eeb_profile_read", "eeb_stream",
-    "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm",
+    "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm", "eeb_debug_bench_layers",
 ]
 
 _lib = None
@@ -105,6 +105,7 @@ def load_library() -> C.CDLL:
                                        C.c_void_p, C.c_void_p, C.c_void_p]
         lib.eeb_debug_bench_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.POINTER(C.c_double)]
+        lib.eeb_debug_bench_layers.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
         lib.eeb_profile_enable.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_profile_read.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         lib.eeb_nccl_unique_id.argtypes = [C.c_void_p]
@@ -362,6 +363,12 @@ class Context:
         """Mean ms per launch of one GEMM shape, launched back to back."""
         ms = C.c_double()
         _check(self.lib.eeb_debug_bench_gemm(self.h, tier, n, k, batch, iters, C.byref(ms)))
+        return ms.value
+
+    def bench_layers(self, model: int, batch: int, iters: int = 20) -> float:
+        """ms per launch of the persistent kernel streaming all loaded layers' GEMMs."""
+        ms = C.c_double()
+        _check(self.lib.eeb_debug_bench_layers(self.h, model, batch, iters, C.byref(ms)))
         return ms.value
 
     def profile_enable(self, on: bool) -> None:

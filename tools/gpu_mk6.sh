@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+export EEB_SKIP_BUILD=1
+EEB_MK_TRACE=gpurun_out/mk_trace.bin timeout 120 python tools/mk_bench.py 2>&1 | tail -1
+python tools/mk_trace.py gpurun_out/mk_trace.bin 148 qkv,o,up,down
+EEB_MK_DBG=3 EEB_MK_TRACE=gpurun_out/mk_trace3.bin timeout 120 python tools/mk_bench.py 2>&1 | tail -1
+python tools/mk_trace.py gpurun_out/mk_trace3.bin 148 qkv,o,up,down

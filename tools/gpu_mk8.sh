@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+export EEB_SKIP_BUILD=1
+export EEB_MK_L2=0
+for dbg in 0 4 8 12 5 6; do EEB_MK_DBG=$dbg TAG="dbg=$dbg" timeout 120 python tools/mk_bench.py 2>&1 | tail -1; done
+EEB_MK_DBG=4 EEB_MK_TRACE=gpurun_out/mk_trace.bin timeout 120 python tools/mk_bench.py 2>&1 | tail -1
+python tools/mk_trace.py gpurun_out/mk_trace.bin 148 qkv,o,up,down
