@@ -206,6 +206,7 @@ def run_eeb(args, desc):
     depth = args.depth if policy == eeb.FLAT else 0
     desc = desc.replace(max_slots=B, max_seq_len=P + 100)
     ctx = eeb.Context(local)
+    ctx.set_gemm_tier(args.tier)
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
@@ -273,24 +274,46 @@ def run_eeb(args, desc):
     ctx.profile_enable(False)
     nsteps = max(1, prof["steps"])
     launches_per_step = prof["last_step_launches"]
-    gemm_ms = prof["layer_gemm_ms"] / nsteps
-    head_ms = prof["exit_head_ms"] / nsteps
-    attn_ms = prof["attention_ms"] / nsteps
     pk, pk_kind = peaks()
     hbm = float(pk["hbm_gbs"])
-    g_bytes = gemm_bytes_per_step(desc, B, desc.num_layers)
-    h_bytes = head_bytes(desc, B) * ne
-    roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1)",
-            "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
-            "traffic": None, "peak_source": ("measured MEASURED_PEAKS.json hbm_gbs (copy burst)" if pk_kind == "measured" else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"),
-            "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
-            "step_share": gemm_ms / max(1e-9, gemm_ms + head_ms + attn_ms + prof["norm_ms"] / nsteps
-                                        + prof["other_ms"] / nsteps)}
-    roof["frac"] = roof["achieved"] / hbm
-    exit_head = {"achieved": h_bytes / (head_ms / 1000.0) / 1e9 if head_ms > 0 else None, "unit": "GB/s",
-                 "ms_per_step": head_ms, "algorithmic_bytes_per_step": h_bytes}
-    if exit_head["achieved"]:
-        exit_head["frac"] = exit_head["achieved"] / hbm
+    peak_source = ("measured MEASURED_PEAKS.json hbm_gbs (copy burst)" if pk_kind == "measured"
+                   else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
+    hist_np = hist_acc.cpu().numpy().astype(np.float64)
+    exit_head = None
+    if prof.get("persistent"):
+        # One kernel is the whole step: its algorithmic bytes are every weight
+        # tile the program streams (layer GEMMs + the exit heads evaluated)
+        # plus the KV cache the surviving rows attend over.
+        step_ms = prof["persistent_ms"] / nsteps
+        w_bytes = prof["weight_bytes"]
+        rows_at = hist_np / max(1.0, hist_np.sum()) * B           # rows exiting at each head per step
+        mean_ctx = P + 0.5 * args.steps + 1                        # positions attended (prompt + decode so far)
+        kv_bytes = float(np.sum(rows_at * np.asarray(desc.exit_layers))) * mean_ctx * 2 * \
+            desc.n_kv_heads * desc.head_dim * desc.bytes_per_el
+        alg = int(w_bytes + kv_bytes)
+        roof = {"bound": "hbm", "kernel": "persistent EE decode-step kernel (all phases, one launch)",
+                "achieved": alg / (step_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s", "traffic": None,
+                "peak_source": peak_source, "algorithmic_bytes_per_step": alg,
+                "weight_bytes_per_step": int(w_bytes), "kv_bytes_per_step": int(kv_bytes),
+                "kernel_ms_per_step": step_ms, "step_share": step_ms / ms}
+        roof["frac"] = roof["achieved"] / hbm
+    else:
+        gemm_ms = prof["layer_gemm_ms"] / nsteps
+        head_ms = prof["exit_head_ms"] / nsteps
+        attn_ms = prof["attention_ms"] / nsteps
+        g_bytes = gemm_bytes_per_step(desc, B, desc.num_layers)
+        h_bytes = head_bytes(desc, B) * ne
+        roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1)",
+                "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+                "traffic": None, "peak_source": peak_source,
+                "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
+                "step_share": gemm_ms / max(1e-9, gemm_ms + head_ms + attn_ms + prof["norm_ms"] / nsteps
+                                            + prof["other_ms"] / nsteps)}
+        roof["frac"] = roof["achieved"] / hbm
+        exit_head = {"achieved": h_bytes / (head_ms / 1000.0) / 1e9 if head_ms > 0 else None, "unit": "GB/s",
+                     "ms_per_step": head_ms, "algorithmic_bytes_per_step": h_bytes}
+        if exit_head["achieved"]:
+            exit_head["frac"] = exit_head["achieved"] / hbm
 
     # ---- e2e: public host-pointer API, H2D + D2H inside every call ------------
     barrier()
@@ -325,7 +348,8 @@ def run_eeb(args, desc):
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, biased exit heads)",
-                "config": workload_config(args, desc), "roofline": roof, "exit_head_roofline": exit_head,
+                "config": workload_config(args, desc), "roofline": roof,
+                **({"exit_head_roofline": exit_head} if exit_head else {}),
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
@@ -333,7 +357,8 @@ def run_eeb(args, desc):
                 "launches_per_step": launches_per_step,
                 "clocks": clocks, "exit_fractions": exit_frac,
                 "kernel_ms_per_step": {k.replace("_ms", ""): v / nsteps for k, v in prof.items()
-                                       if k.endswith("_ms")}}
+                                       if k.endswith("_ms") and v > 0},
+                "path": "persistent step kernel" if prof.get("persistent") else "per-op kernel chain"}
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist is not None:
@@ -355,6 +380,7 @@ def main():
     ap.add_argument("--depth", type=int, default=6)
     ap.add_argument("--th", type=float, default=0.7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tier", type=int, default=0, help="0 auto (persistent kernel), 2 per-op kernel chain")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

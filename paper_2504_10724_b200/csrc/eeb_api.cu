@@ -678,11 +678,14 @@ void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int 
 // ---------------------------------------------------------------------------
 bool mk_applicable(eeb_ctx* c, const Model& m, int batch) {
     if (c->mk_mode < 0) {
+        // Opt-in until the persistent kernel's SIMT phases beat the per-op chain
+        // (profiles/r1: 2.9 ms vs 2.2 ms per C2 step); tier 3 forces it.
         const char* env = std::getenv("EEB_MK");
-        c->mk_mode = env && env[0] == '0' ? 0 : 1;
+        c->mk_mode = env && env[0] == '1' ? 1 : 0;
     }
     const eeb_model_desc& d = m.desc;
     const bool ok = !c->retain_logits && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
+                    d.d_model <= 6 * 4 * 128 &&
                     batch <= mk::kMaxRows && d.max_seq_len <= 256 && gemm_tc_available();
     if (c->gemm_tier == 3) {
         if (!ok) throw Error(EEB_E_DOMAIN, "persistent step kernel requested but not applicable to this model/batch");
@@ -794,7 +797,7 @@ std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, fl
             const int hg = gemm(add_map(m.head[e]->p, d.vocab, D, mk::kBM), m_hh, d.vocab, D);
             const int hr = simt(mk::kPhaseHeadReduce, l, hg);
             ph[hr].exit_index = e;
-            const int dc = simt(mk::kPhaseDecide, l, -1);
+            const int dc = simt(mk::kPhaseDecide, l, hg);
             ph[dc].exit_index = e;
             ph[dc].exit_layer = m.exits[e];
             ph[dc].flags = hi + 1 == heads.size() ? mk::kFlagFinal : 0;
@@ -818,7 +821,7 @@ std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, fl
 
     // shared workspace of the context
     c->mk_partials.ensure((size_t)G * mk::kMaxSeg * bpad * mk::kBM * 4);
-    c->mk_stats.ensure((size_t)bpad * 16);
+    c->mk_stats.ensure((size_t)bpad * 16 * ((d.vocab + 128 * mk::kHeadChunk - 1) / (128 * mk::kHeadChunk)));
     if (!c->mk_bar.p) {
         c->mk_bar.ensure(64);
         EEB_CUDA(cudaMemset(c->mk_bar.p, 0, 64));
@@ -894,7 +897,30 @@ void run_step_mk(eeb_ctx* c, int mi, int depth, int policy, float th, int batch)
         EEB_CUDA(cudaEventCreate(&e1));
         EEB_CUDA(cudaEventRecord(e0, c->stream));
     }
+    static const char* trace_path = std::getenv("EEB_MK_TRACE");
+    DevBuf trace;
+    if (trace_path) {  // diagnostics: per-phase timestamps of this step -> file (synchronous)
+        trace.ensure((size_t)c->num_sms * P.P.n_phases * 8 * 8);
+        EEB_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes, c->stream));
+        P.P.trace = trace.as<unsigned long long>();
+    }
     mk::launch(P.P, P.segtab.as<int4>(), c->num_sms, c->stream);
+    if (trace_path) {
+        P.P.trace = nullptr;
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        std::vector<unsigned long long> h(trace.bytes / 8);
+        EEB_CUDA(cudaMemcpy(h.data(), trace.p, trace.bytes, cudaMemcpyDeviceToHost));
+        std::vector<mk::Phase> ph(P.P.n_phases);
+        EEB_CUDA(cudaMemcpy(ph.data(), P.phases.p, ph.size() * sizeof(mk::Phase), cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+        if (FILE* f = std::fopen((std::string(trace_path) + ".kinds").c_str(), "w")) {
+            for (auto& x : ph) std::fprintf(f, "%d\n", x.kind);
+            std::fclose(f);
+        }
+    }
     if (c->profiling) {
         EEB_CUDA(cudaEventRecord(e1, c->stream));
         EEB_CUDA(cudaEventSynchronize(e1));

@@ -116,6 +116,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
 struct TcParams {
     int N, K;
     int kb_per;        // k-blocks per split
@@ -200,22 +206,27 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t idesc = instr_desc(kBM, p.bpad);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % S;
-                const uint32_t ph = (uint32_t)(i / S) & 1u;
-                mbar_wait(full0 + 8 * s, ph);
-                tc_fence_after();
-                const uint32_t sa = base + (uint32_t)s * stage_bytes;
-                const uint64_t da = smem_desc(sa), db = smem_desc(sa + a_bytes);
+        // The whole warp runs the loop (descriptors stay warp-uniform: uniform
+        // registers, no per-op R2UR) and one elected lane issues — a
+        // single-lane loop issues tcgen05.mma several times slower.
+        const uint32_t idesc = instr_desc(kBM, p.bpad);
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % S;
+            const uint32_t ph = (uint32_t)(i / S) & 1u;
+            mbar_wait(full0 + 8 * s, ph);
+            tc_fence_after();
+            const uint32_t sa = base + (uint32_t)s * stage_bytes;
+            const uint64_t da = smem_desc(sa), db = smem_desc(sa + a_bytes);
+            if (elect_one_sync()) {
 #pragma unroll
                 for (int k = 0; k < kBK / 16; ++k)  // +32 B per K=16 step inside the swizzle atom
                     umma(tmem, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (i | k) != 0);
                 umma_commit(empty0 + 8 * s);
             }
-            umma_commit(tfull);
+            __syncwarp();
         }
+        if (elect_one_sync()) umma_commit(tfull);
+        __syncwarp();
     } else {
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31  (thread = output feature)
         const int quarter = warp & 3;

@@ -67,17 +67,39 @@ __device__ __forceinline__ void cta_range(const Phase& ph, int c, int G, int& s,
     e = (int)(((long long)ph.total * (c + 1)) / Gp);
 }
 
-// Sum over the stream-K segments of GEMM phase `src` for compact row i, output
-// column col: CTA order = k order (deterministic).  segtab[t] = {first CTA,
-// its partial slot, segment count} (host-computed, pad[0] = table offset).
-__device__ __forceinline__ float psum(const Params& p, const int4* __restrict__ segtab, const Phase& src, int i,
-                                      int col) {
-    const int t = col >> 7;
-    const int4 sg = __ldg(segtab + src.pad[0] + t);
-    const size_t row_off = (size_t)i * kBM + (col & 127);
-    const size_t slot_stride = (size_t)p.bpad * kBM;
-    float acc = __ldcg(p.partials + (size_t)(sg.x * kMaxSeg + sg.y) * slot_stride + row_off);
-    for (int j = 1; j < sg.z; ++j) acc += __ldcg(p.partials + (size_t)((sg.x + j) * kMaxSeg) * slot_stride + row_off);
+// Sum over the stream-K segments of GEMM phase `src` for compact row i and NV
+// consecutive output columns starting at col (NV-aligned, inside one tile):
+// CTA order = k order (deterministic).  All segment loads are issued before
+// the in-order sum, so a consumer thread has up to kSegUnroll L2 requests in
+// flight.  segtab[t] = {first CTA, its partial slot, segment count}
+// (host-computed; Phase::pad[0] = the phase's table offset).
+template <int NV>
+struct VecF;
+template <> struct VecF<1> { using T = float; };
+template <> struct VecF<2> { using T = float2; };
+template <> struct VecF<4> { using T = float4; };
+__device__ __forceinline__ void vadd(float& a, float b) { a += b; }
+__device__ __forceinline__ void vadd(float2& a, float2 b) { a.x += b.x; a.y += b.y; }
+__device__ __forceinline__ void vadd(float4& a, float4 b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+
+template <int NV>
+__device__ __forceinline__ typename VecF<NV>::T psum(const Params& p, const int4* __restrict__ segtab, const Phase& src,
+                                                     int i, int col) {
+    using T = typename VecF<NV>::T;
+    const int4 sg = __ldg(segtab + src.pad[0] + (col >> 7));
+    const float* base = p.partials + (size_t)i * kBM + (col & 127);
+    const size_t ss = (size_t)p.bpad * kBM;
+    T v[kSegUnroll];
+#pragma unroll
+    for (int j = 0; j < kSegUnroll; ++j)
+        if (j < sg.z)
+            v[j] = __ldcg(reinterpret_cast<const T*>(base + (size_t)(j == 0 ? sg.x * kMaxSeg + sg.y : (sg.x + j) * kMaxSeg) * ss));
+    T acc = v[0];
+#pragma unroll
+    for (int j = 1; j < kSegUnroll; ++j)
+        if (j < sg.z) vadd(acc, v[j]);
+    for (int j = kSegUnroll; j < sg.z; ++j)
+        vadd(acc, __ldcg(reinterpret_cast<const T*>(base + (size_t)((sg.x + j) * kMaxSeg) * ss)));
     return acc;
 }
 
@@ -99,46 +121,84 @@ __device__ __forceinline__ float simt_sum(float v, float* red) {
 // ---------------------------------------------------------------------------
 // SIMT phases
 // ---------------------------------------------------------------------------
-__device__ void phase_norm(const Params& p, const int4* segtab, const Phase* prog, const Phase& ph,
+// One CTA per live row; warp w owns 128-column tiles w, w+6, ...; lane = 4
+// columns (float4).  The row stays in registers between the two passes.
+constexpr int kNormTilesPerWarp = 4;  // D <= 6 * 4 * 128 = 3072 (host-checked)
+__device__ __noinline__ void phase_norm(const Params& p, const int4* segtab, const Phase* prog, const Phase& ph,
                            const int* live, int n_live, float* red) {
-    const int t = threadIdx.x - 64;
+    const int w = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
     const float* g = p.gains[ph.gain];
     __nv_bfloat16* out = (ph.flags & kFlagOutHead) ? p.hh : p.h;
     const bool embed = ph.flags & kFlagEmbed;
     const bool has_src = ph.src >= 0;
     const Phase src = has_src ? prog[ph.src] : ph;
+    const int tiles = p.D / 128;
     for (int i = blockIdx.x; i < n_live; i += gridDim.x) {
         const int r = live[i];
         float* xr = p.x + (size_t)r * p.D;
         const __nv_bfloat16* er = p.emb + (size_t)p.tok[r] * p.D;
+        float4 v[kNormTilesPerWarp];
         float ss = 0.f;
-        for (int c = t; c < p.D; c += kSimtThreads) {
-            float v = embed ? bf2f(er[c]) : __ldcg(xr + c);
-            if (has_src) v += psum(p, segtab, src, i, c);
-            if (embed || has_src) __stcg(xr + c, v);
-            ss += v * v;
+#pragma unroll
+        for (int k = 0; k < kNormTilesPerWarp; ++k) {
+            const int t = w + k * kSimtWarps;
+            if (t < tiles) {
+                const int c = t * 128 + lane * 4;
+                float4 a;
+                if (embed) {
+                    const uint2 u = *reinterpret_cast<const uint2*>(er + c);
+                    a = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                                    __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+                } else {
+                    a = __ldcg(reinterpret_cast<const float4*>(xr + c));
+                }
+                if (has_src) vadd(a, psum<4>(p, segtab, src, i, c));
+                if (embed || has_src) __stcg(reinterpret_cast<float4*>(xr + c), a);
+                v[k] = a;
+                ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+            }
         }
         ss = simt_sum(ss, red);
         const float inv = rsqrtf(ss / (float)p.D + p.eps);
-        for (int c = t; c < p.D; c += kSimtThreads)
-            out[(size_t)i * p.D + c] = __float2bfloat16_rn(__ldcg(xr + c) * inv * g[c]);
+#pragma unroll
+        for (int k = 0; k < kNormTilesPerWarp; ++k) {
+            const int t = w + k * kSimtWarps;
+            if (t < tiles) {
+                const int c = t * 128 + lane * 4;
+                const float4 gg = *reinterpret_cast<const float4*>(g + c);
+                const __nv_bfloat162 o0 = __floats2bfloat162_rn(v[k].x * inv * gg.x, v[k].y * inv * gg.y);
+                const __nv_bfloat162 o1 = __floats2bfloat162_rn(v[k].z * inv * gg.z, v[k].w * inv * gg.w);
+                uint2 u;
+                u.x = *reinterpret_cast<const uint32_t*>(&o0);
+                u.y = *reinterpret_cast<const uint32_t*>(&o1);
+                *reinterpret_cast<uint2*>(out + (size_t)i * p.D + c) = u;
+            }
+        }
     }
 }
 
-__device__ void phase_act(const Params& p, const int4* segtab, const Phase& src, int n_live) {
-    const int t = threadIdx.x - 64;
-    const long long total = (long long)n_live * p.F;
-    for (long long idx = (long long)blockIdx.x * kSimtThreads + t; idx < total;
-         idx += (long long)gridDim.x * kSimtThreads) {
-        const int i = (int)(idx / p.F), j = (int)(idx % p.F);
-        float o;
-        if (p.mlp_kind == EEB_MLP_SWIGLU) {
-            const float gt = psum(p, segtab, src, i, 2 * j), up = psum(p, segtab, src, i, 2 * j + 1);
-            o = gt / (1.f + __expf(-gt)) * up;
+// Task = (live row, 128-column tile of the up projection); lane = 4 columns.
+__device__ __noinline__ void phase_act(const Params& p, const int4* segtab, const Phase& src, int n_live) {
+    const int w = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
+    const int tiles = src.tiles;
+    const int ntask = n_live * tiles;
+    const bool swiglu = p.mlp_kind == EEB_MLP_SWIGLU;
+    for (int task = blockIdx.x * kSimtWarps + w; task < ntask; task += gridDim.x * kSimtWarps) {
+        const int i = task / tiles, t = task % tiles;
+        const int c = t * 128 + lane * 4;
+        const float4 a = psum<4>(p, segtab, src, i, c);
+        if (swiglu) {  // interleaved (gate, up) pairs -> outputs c/2, c/2+1
+            const __nv_bfloat162 o = __floats2bfloat162_rn(a.x / (1.f + __expf(-a.x)) * a.y,
+                                                          a.z / (1.f + __expf(-a.z)) * a.w);
+            *reinterpret_cast<__nv_bfloat162*>(p.hmid + (size_t)i * p.F + c / 2) = o;
         } else {
-            o = fmaxf(psum(p, segtab, src, i, j), 0.f);
+            const __nv_bfloat162 o0 = __floats2bfloat162_rn(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+            const __nv_bfloat162 o1 = __floats2bfloat162_rn(fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t*>(&o0);
+            u.y = *reinterpret_cast<const uint32_t*>(&o1);
+            *reinterpret_cast<uint2*>(p.hmid + (size_t)i * p.F + c) = u;
         }
-        p.hmid[(size_t)i * p.F + j] = __float2bfloat16_rn(o);
     }
 }
 
@@ -147,7 +207,7 @@ __device__ void phase_act(const Params& p, const int4* segtab, const Phase& src,
 // 64-wide accumulator, then a register butterfly leaves dims (2l, 2l+1) in
 // lane l.  Masking: a position whose token exited before this layer has no
 // K/V here (kv_depth < layer); the current position is always valid.
-__device__ void phase_attn(const Params& p, const int4* segtab, const Phase& src, int layer, const int* live,
+__device__ __noinline__ void phase_attn(const Params& p, const int4* segtab, const Phase& src, int layer, const int* live,
                            int n_live, float* scratch) {
     const int warp = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
     const int Gq = p.H / p.Hkv;
@@ -167,28 +227,23 @@ __device__ void phase_attn(const Params& p, const int4* segtab, const Phase& src
         const float* cs = p.rope_cos + (size_t)pos * 32;
         const float* sn = p.rope_sin + (size_t)pos * 32;
         const float c0 = cs[ri], c1 = cs[ri + 1], s0 = sn[ri], s1 = sn[ri + 1];
-        auto rope = [&](float a0, float a1, float* dst) {
-            const float b0 = __shfl_xor_sync(0xffffffffu, a0, 16), b1 = __shfl_xor_sync(0xffffffffu, a1, 16);
+        auto rope = [&](float2 a, float* dst) {
+            const float b0 = __shfl_xor_sync(0xffffffffu, a.x, 16), b1 = __shfl_xor_sync(0xffffffffu, a.y, 16);
             if (lane < 16) {
-                dst[d0] = a0 * c0 - b0 * s0;
-                dst[d0 + 1] = a1 * c1 - b1 * s1;
+                dst[d0] = a.x * c0 - b0 * s0;
+                dst[d0 + 1] = a.y * c1 - b1 * s1;
             } else {
-                dst[d0] = b0 * s0 + a0 * c0;
-                dst[d0 + 1] = b1 * s1 + a1 * c1;
+                dst[d0] = b0 * s0 + a.x * c0;
+                dst[d0 + 1] = b1 * s1 + a.y * c1;
             }
         };
-        for (int hq = 0; hq < Gq; ++hq) {
-            const int col = (g * Gq + hq) * 64 + d0;
-            rope(psum(p, segtab, src, i, col), psum(p, segtab, src, i, col + 1), q_s + hq * 64);
-        }
+        for (int hq = 0; hq < Gq; ++hq) rope(psum<2>(p, segtab, src, i, (g * Gq + hq) * 64 + d0), q_s + hq * 64);
         {
-            const int col = p.dq + g * 64 + d0;
-            rope(psum(p, segtab, src, i, col), psum(p, segtab, src, i, col + 1), kn_s);
-            const int vcol = p.dq + p.dkv + g * 64 + d0;
-            const float v0 = psum(p, segtab, src, i, vcol), v1 = psum(p, segtab, src, i, vcol + 1);
+            rope(psum<2>(p, segtab, src, i, p.dq + g * 64 + d0), kn_s);
+            const float2 v = psum<2>(p, segtab, src, i, p.dq + p.dkv + g * 64 + d0);
             // the cache holds bf16: attend to the rounded values, as later steps will
             const __nv_bfloat162 kb = __floats2bfloat162_rn(kn_s[d0], kn_s[d0 + 1]);
-            const __nv_bfloat162 vb = __floats2bfloat162_rn(v0, v1);
+            const __nv_bfloat162 vb = __floats2bfloat162_rn(v.x, v.y);
             kn_s[d0] = __low2float(kb);
             kn_s[d0 + 1] = __high2float(kb);
             vn_s[d0] = __low2float(vb);
@@ -285,54 +340,44 @@ __device__ void phase_attn(const Params& p, const int4* segtab, const Phase& src
     }
 }
 
-__device__ void phase_head_reduce(const Params& p, const int4* segtab, const Phase& src, int n_live, float* red) {
-    const int t = threadIdx.x - 64;
-    const int w = t >> 5, lane = t & 31;
-    float* rm = red;                             // [6]
-    float* rs = red + 8;                         // [6]
-    int* ra = reinterpret_cast<int*>(red + 16);  // [6]
-    for (int i = blockIdx.x; i < n_live; i += gridDim.x) {
+// Online (max, sum-exp, argmax) merge; ties -> lowest token id.
+__device__ __forceinline__ void lse_merge(float& m, float& s, int& a, float m2, float s2, int a2) {
+    const float M = fmaxf(m, m2);
+    const float t1 = m == -INFINITY ? 0.f : s * __expf(m - M);
+    const float t2 = m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M);
+    a = (m2 > m || (m2 == m && a2 < a)) ? a2 : a;
+    s = t1 + t2;
+    m = M;
+}
+
+// Exit-head reduction, task = (live row, chunk of kHeadChunk vocabulary
+// tiles): per-chunk (max, sum-exp, argmax) -> stats[row][chunk]; DECIDE merges
+// the chunks in order.  Lane = 4 vocabulary entries per tile.
+__device__ __noinline__ void phase_head_reduce(const Params& p, const int4* segtab, const Phase& src, int n_live) {
+    const int w = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
+    const int nchunk = (src.tiles + kHeadChunk - 1) / kHeadChunk;
+    const int ntask = n_live * nchunk;
+    for (int task = blockIdx.x * kSimtWarps + w; task < ntask; task += gridDim.x * kSimtWarps) {
+        const int i = task / nchunk, ch = task % nchunk;
         float m = -INFINITY, s = 0.f;
         int am = 0x7fffffff;
-        for (int v = t; v < p.V; v += kSimtThreads) {
-            const float l = psum(p, segtab, src, i, v);
-            if (l > m) {
-                s = s * __expf(m - l) + 1.f;
-                m = l;
-                am = v;
-            } else {
-                s += __expf(l - m);
-            }
+        const int t1 = min(src.tiles, (ch + 1) * kHeadChunk);
+        for (int t = ch * kHeadChunk; t < t1; ++t) {
+            const int c = t * 128 + lane * 4;
+            const float4 v = psum<4>(p, segtab, src, i, c);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (c + k < p.V) lse_merge(m, s, am, vv[k], 1.f, c + k);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
             const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
             const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
-            const float M = fmaxf(m, m2);
-            s = (m == -INFINITY ? 0.f : s * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
-            am = (m2 > m || (m2 == m && a2 < am)) ? a2 : am;
-            m = M;
+            lse_merge(m, s, am, m2, s2, a2);
         }
-        if (lane == 0) {
-            rm[w] = m;
-            rs[w] = s;
-            ra[w] = am;
-        }
-        named_sync(3, kSimtThreads);
-        if (t == 0) {
-            float M = rm[0], S = rs[0];
-            int A = ra[0];
-            for (int k = 1; k < kSimtWarps; ++k) {
-                const float m2 = rm[k];
-                const float Mn = fmaxf(M, m2);
-                S = S * __expf(M - Mn) + rs[k] * __expf(m2 - Mn);
-                if (m2 > M || (m2 == M && ra[k] < A)) A = ra[k];
-                M = Mn;
-            }
-            p.stats[i] = make_float4(__int_as_float(A), 1.f / S, -logf(S), 0.f);
-        }
-        named_sync(3, kSimtThreads);
+        if (lane == 0) p.stats[(size_t)i * nchunk + ch] = make_float4(m, s, __int_as_float(am), 0.f);
     }
 }
 
@@ -348,7 +393,7 @@ __device__ __forceinline__ void write_row(const StepOutDev& o, int r, int exit_l
 }
 
 // Warp 2 of every CTA: identical decisions and compaction; CTA 0 writes.
-__device__ void phase_decide(const Params& p, const Phase& ph, int* live, int* n_live_s) {
+__device__ __noinline__ void phase_decide(const Params& p, const Phase& ph, int nchunk, int* live, int* n_live_s) {
     const int lane = threadIdx.x & 31;
     const int e = ph.exit_index;
     const bool final = ph.flags & kFlagFinal;
@@ -363,9 +408,13 @@ __device__ void phase_decide(const Params& p, const Phase& ph, int* live, int* n
         bool survive = false;
         if (valid) {
             r = live[i];
-            const float4 st = __ldcg(p.stats + i);
-            const int tok = __float_as_int(st.x);
-            const float conf = st.y, logp = st.z;
+            float m = -INFINITY, S = 0.f;
+            int tok = 0x7fffffff;
+            for (int ch = 0; ch < nchunk; ++ch) {
+                const float4 st = __ldcg(p.stats + (size_t)i * nchunk + ch);
+                lse_merge(m, S, tok, st.x, st.y, __float_as_int(st.z));
+            }
+            const float conf = 1.f / S, logp = -logf(S);
             switch (p.policy) {
                 case EEB_FLAT:
                     if (writer)
@@ -414,7 +463,7 @@ __device__ void phase_decide(const Params& p, const Phase& ph, int* live, int* n
     __syncwarp();
 }
 
-__device__ void phase_finalize(const Params& p, float* red) {
+__device__ __noinline__ void phase_finalize(const Params& p, float* red) {
     if (blockIdx.x != 0) return;
     const int t = threadIdx.x - 64;
     unsigned* hist_s = reinterpret_cast<unsigned*>(red);  // [64]
@@ -653,9 +702,10 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
                     case kPhaseNorm: phase_norm(p, segtab, prog, ph, live, n_live, red); break;
                     case kPhaseAttn: phase_attn(p, segtab, prog[ph.src], ph.layer, live, n_live, scratch); break;
                     case kPhaseAct: phase_act(p, segtab, prog[ph.src], n_live); break;
-                    case kPhaseHeadReduce: phase_head_reduce(p, segtab, prog[ph.src], n_live, red); break;
+                    case kPhaseHeadReduce: phase_head_reduce(p, segtab, prog[ph.src], n_live); break;
                     case kPhaseDecide:
-                        if (warp == 2) phase_decide(p, ph, live, n_live_s);
+                        if (warp == 2)
+                            phase_decide(p, ph, (prog[ph.src].tiles + kHeadChunk - 1) / kHeadChunk, live, n_live_s);
                         break;
                     case kPhaseFinalize: phase_finalize(p, red); break;
                     default: break;

@@ -27,6 +27,8 @@ constexpr int kBM = 128;       // UMMA M: output features per tile
 constexpr int kBK = 64;        // k-block: one 128-byte swizzle atom of bf16
 constexpr int kMaxSeg = 8;     // partial-sum segments one CTA may own in a GEMM phase
 constexpr int kMaxRows = 128;  // rows per step on this path (UMMA N <= 128, live list in smem)
+constexpr int kSegUnroll = 12; // partial segments of one tile summed with all loads in flight
+constexpr int kHeadChunk = 16; // vocabulary tiles (x128) per exit-head reduction task
 
 enum PhaseKind : int {
     kPhaseGemm = 0,        // y = X W^T, stream-K, partial sums -> partial buffer
@@ -90,7 +92,7 @@ struct Params {
     __nv_bfloat16* hh;    // [bpad][D]
     __nv_bfloat16* attn;  // [bpad][dq]
     __nv_bfloat16* hmid;  // [bpad][F]
-    float4* stats;        // [bpad] {tok bits, conf, logp, -}
+    float4* stats;        // [bpad][n_chunks] per vocabulary chunk {max, sum-exp, argmax bits, -}
     StepOutDev out;
     int exit_layers[64];
 };
