@@ -685,7 +685,7 @@ bool mk_applicable(eeb_ctx* c, const Model& m, int batch) {
     }
     const eeb_model_desc& d = m.desc;
     const bool ok = !c->retain_logits && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
-                    d.d_model <= 6 * 4 * 128 &&
+                    d.d_model <= 6 * 3 * 128 &&
                     batch <= mk::kMaxRows && d.max_seq_len <= 256 && gemm_tc_available();
     if (c->gemm_tier == 3) {
         if (!ok) throw Error(EEB_E_DOMAIN, "persistent step kernel requested but not applicable to this model/batch");
@@ -726,6 +726,7 @@ std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, fl
 
     std::vector<mk::Phase> ph;
     std::vector<int4> seg;
+    std::map<std::pair<int, int>, int> seg_of_shape;  // the table depends only on (N, K) and the grid
     auto simt = [&](int kind, int layer, int src) {
         mk::Phase x{};
         x.kind = kind;
@@ -753,7 +754,17 @@ std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, fl
             if (e0 > s0) max_tiles = std::max(max_tiles, (e0 - 1) / x.kb - s0 / x.kb + 1);
         }
         if (max_tiles > mk::kMaxSeg) throw Error(EEB_E_DOMAIN, "persistent kernel: too many segments per CTA");
+        const auto shape = std::make_pair(N, K);
+        auto known = seg_of_shape.find(shape);
+        if (known != seg_of_shape.end()) {
+            x.pad[0] = known->second;
+            P->n_gemm++;
+            P->weight_bytes += (int64_t)N * K * 2;
+            ph.push_back(x);
+            return (int)ph.size() - 1;
+        }
         x.pad[0] = (int)seg.size();
+        seg_of_shape[shape] = x.pad[0];
         for (int t = 0; t < x.tiles; ++t) {
             const int k0 = t * x.kb, k1 = k0 + x.kb;
             int c0 = 0;
@@ -836,12 +847,17 @@ std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, fl
     q.batch = batch;
     q.bpad = bpad;
     q.x_stages = 4;
-    while ((size_t)q.x_stages * bpad * mk::kBK * 2 < (size_t)mk::kSimtWarps * (8 * 64 + 128) * 4) ++q.x_stages;
+    // the X ring doubles as the SIMT phases' scratch (attention K/V rings: 6 warps x ~19 KB)
+    while ((size_t)q.x_stages * bpad * mk::kBK * 2 < (size_t)mk::kSimtWarps * mk::kAttnScratchBytes) ++q.x_stages;
+    if (const char* v = std::getenv("EEB_MK_XSTAGES")) q.x_stages = std::max(q.x_stages, std::atoi(v));
     int ws = 2;
-    while (mk::smem_bytes(bpad, ws + 1, q.x_stages, q.n_phases) <= 227u * 1024u) ++ws;
+    q.n_segtab = (int)seg.size();
+    while (mk::smem_bytes(bpad, ws + 1, q.x_stages, q.n_phases, q.n_segtab) <= 227u * 1024u) ++ws;
     if (ws < 3) throw Error(EEB_E_DOMAIN, "persistent kernel: program too large for shared memory");
     q.w_stages = ws;
+    if (const char* v = std::getenv("EEB_MK_WSTAGES")) q.w_stages = std::min(q.w_stages, std::max(2, std::atoi(v)));
     q.bar_mode = 0;
+    q.dbg = std::getenv("EEB_MK_DBG") ? std::atoi(std::getenv("EEB_MK_DBG")) : 0;  // timing experiments only
     q.D = D;
     q.F = F;
     q.dq = m.dq;
@@ -1438,7 +1454,7 @@ eeb_status eeb_debug_bench_layers(eeb_ctx* c, int model, int batch, int iters, d
         mk::Params& q = P->P;
         q.n_phases = (int)g.size();
         int ws = 2;
-        while (mk::smem_bytes(q.bpad, ws + 1, q.x_stages, q.n_phases) <= 227u * 1024u) ++ws;
+        while (mk::smem_bytes(q.bpad, ws + 1, q.x_stages, q.n_phases, q.n_segtab) <= 227u * 1024u) ++ws;
         q.w_stages = ws;
         if (const char* v = std::getenv("EEB_MK_WSTAGES")) q.w_stages = std::min(ws, std::max(2, std::atoi(v)));
         q.bar_mode = std::getenv("EEB_MK_BAR") ? std::atoi(std::getenv("EEB_MK_BAR")) : 0;
@@ -1487,7 +1503,7 @@ eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, i
         // launch streams its weights from HBM, as in the step.
         DevBuf x, ws, na;
         const size_t wbytes = (size_t)n * k * 2;
-        const int nbuf = (int)std::max<size_t>(1, ((size_t)512 << 20) / wbytes + 1);
+        const int nbuf = std::getenv("EEB_BENCH_L2") ? 1 : (int)std::max<size_t>(1, ((size_t)512 << 20) / wbytes + 1);
         std::vector<std::unique_ptr<DevBuf>> wv;
         for (int i = 0; i < nbuf; ++i) {
             wv.push_back(std::make_unique<DevBuf>());

@@ -187,10 +187,17 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Relaxed polling (no L1 invalidation per poll), one acquire fence on success.
 __device__ __forceinline__ void counter_barrier(unsigned long long* ctr, unsigned long long target) {
     red_release_add_u64(ctr, 1ull);
-    while (ld_acquire_gpu_u64(ctr) < target) {
+    while (ld_relaxed_gpu_u64(ctr) < target) {
     }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 }  // namespace ptx

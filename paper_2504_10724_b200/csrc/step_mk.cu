@@ -86,7 +86,7 @@ template <int NV>
 __device__ __forceinline__ typename VecF<NV>::T psum(const Params& p, const int4* __restrict__ segtab, const Phase& src,
                                                      int i, int col) {
     using T = typename VecF<NV>::T;
-    const int4 sg = __ldg(segtab + src.pad[0] + (col >> 7));
+    const int4 sg = segtab[src.pad[0] + (col >> 7)];  // shared memory
     const float* base = p.partials + (size_t)i * kBM + (col & 127);
     const size_t ss = (size_t)p.bpad * kBM;
     T v[kSegUnroll];
@@ -123,39 +123,53 @@ __device__ __forceinline__ float simt_sum(float v, float* red) {
 // ---------------------------------------------------------------------------
 // One CTA per live row; warp w owns 128-column tiles w, w+6, ...; lane = 4
 // columns (float4).  The row stays in registers between the two passes.
-constexpr int kNormTilesPerWarp = 4;  // D <= 6 * 4 * 128 = 3072 (host-checked)
+constexpr int kNormTilesPerWarp = 3;  // D <= 6 * 3 * 128 = 2304 (host-checked)
 __device__ __noinline__ void phase_norm(const Params& p, const int4* segtab, const Phase* prog, const Phase& ph,
-                           const int* live, int n_live, float* red) {
+                                        const int* live, int n_live, float* red) {
     const int w = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
     const float* g = p.gains[ph.gain];
     __nv_bfloat16* out = (ph.flags & kFlagOutHead) ? p.hh : p.h;
     const bool embed = ph.flags & kFlagEmbed;
-    const bool has_src = ph.src >= 0;
-    const Phase src = has_src ? prog[ph.src] : ph;
+    if (p.dbg & 64) return;  // timing experiment: empty norm phases
+    const bool has_src = ph.src >= 0 && !(p.dbg & 128);  // timing experiment: no partial reads
+    const Phase src = ph.src >= 0 ? prog[ph.src] : ph;
     const int tiles = p.D / 128;
     for (int i = blockIdx.x; i < n_live; i += gridDim.x) {
         const int r = live[i];
         float* xr = p.x + (size_t)r * p.D;
         const __nv_bfloat16* er = p.emb + (size_t)p.tok[r] * p.D;
-        float4 v[kNormTilesPerWarp];
-        float ss = 0.f;
+        float4 v[kNormTilesPerWarp], gg[kNormTilesPerWarp];
+        // 1) every load of the row slice (and the gains) in flight before any use
 #pragma unroll
         for (int k = 0; k < kNormTilesPerWarp; ++k) {
             const int t = w + k * kSimtWarps;
             if (t < tiles) {
                 const int c = t * 128 + lane * 4;
-                float4 a;
+                gg[k] = __ldg(reinterpret_cast<const float4*>(g + c));
                 if (embed) {
                     const uint2 u = *reinterpret_cast<const uint2*>(er + c);
-                    a = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
-                                    __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+                    v[k] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
                 } else {
-                    a = __ldcg(reinterpret_cast<const float4*>(xr + c));
+                    v[k] = __ldcg(reinterpret_cast<const float4*>(xr + c));
                 }
-                if (has_src) vadd(a, psum<4>(p, segtab, src, i, c));
-                if (embed || has_src) __stcg(reinterpret_cast<float4*>(xr + c), a);
-                v[k] = a;
-                ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+            }
+        }
+        if (has_src) {
+#pragma unroll
+            for (int k = 0; k < kNormTilesPerWarp; ++k) {
+                const int t = w + k * kSimtWarps;
+                if (t < tiles) vadd(v[k], psum<4>(p, segtab, src, i, t * 128 + lane * 4));
+            }
+        }
+        // 2) residual write-back and the row's sum of squares
+        float ss = 0.f;
+#pragma unroll
+        for (int k = 0; k < kNormTilesPerWarp; ++k) {
+            const int t = w + k * kSimtWarps;
+            if (t < tiles) {
+                if (embed || has_src) __stcg(reinterpret_cast<float4*>(xr + t * 128 + lane * 4), v[k]);
+                ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
             }
         }
         ss = simt_sum(ss, red);
@@ -165,9 +179,8 @@ __device__ __noinline__ void phase_norm(const Params& p, const int4* segtab, con
             const int t = w + k * kSimtWarps;
             if (t < tiles) {
                 const int c = t * 128 + lane * 4;
-                const float4 gg = *reinterpret_cast<const float4*>(g + c);
-                const __nv_bfloat162 o0 = __floats2bfloat162_rn(v[k].x * inv * gg.x, v[k].y * inv * gg.y);
-                const __nv_bfloat162 o1 = __floats2bfloat162_rn(v[k].z * inv * gg.z, v[k].w * inv * gg.w);
+                const __nv_bfloat162 o0 = __floats2bfloat162_rn(v[k].x * inv * gg[k].x, v[k].y * inv * gg[k].y);
+                const __nv_bfloat162 o1 = __floats2bfloat162_rn(v[k].z * inv * gg[k].z, v[k].w * inv * gg[k].w);
                 uint2 u;
                 u.x = *reinterpret_cast<const uint32_t*>(&o0);
                 u.y = *reinterpret_cast<const uint32_t*>(&o1);
@@ -178,37 +191,53 @@ __device__ __noinline__ void phase_norm(const Params& p, const int4* segtab, con
 }
 
 // Task = (live row, 128-column tile of the up projection); lane = 4 columns.
+__device__ __forceinline__ void act_store(const Params& p, bool swiglu, int i, int c, float4 a) {
+    if (swiglu) {  // interleaved (gate, up) pairs -> outputs c/2, c/2+1
+        const __nv_bfloat162 o = __floats2bfloat162_rn(a.x / (1.f + __expf(-a.x)) * a.y,
+                                                      a.z / (1.f + __expf(-a.z)) * a.w);
+        *reinterpret_cast<__nv_bfloat162*>(p.hmid + (size_t)i * p.F + c / 2) = o;
+    } else {
+        const __nv_bfloat162 o0 = __floats2bfloat162_rn(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+        const __nv_bfloat162 o1 = __floats2bfloat162_rn(fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
+        uint2 u;
+        u.x = *reinterpret_cast<const uint32_t*>(&o0);
+        u.y = *reinterpret_cast<const uint32_t*>(&o1);
+        *reinterpret_cast<uint2*>(p.hmid + (size_t)i * p.F + c) = u;
+    }
+}
+
+// Task = (live row, 128-column tile of the up projection); lane = 4 columns;
+// two tasks per iteration so both tiles' partial loads are in flight together.
 __device__ __noinline__ void phase_act(const Params& p, const int4* segtab, const Phase& src, int n_live) {
     const int w = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
     const int tiles = src.tiles;
     const int ntask = n_live * tiles;
     const bool swiglu = p.mlp_kind == EEB_MLP_SWIGLU;
-    for (int task = blockIdx.x * kSimtWarps + w; task < ntask; task += gridDim.x * kSimtWarps) {
+    const int stride = gridDim.x * kSimtWarps;
+    for (int task = blockIdx.x * kSimtWarps + w; task < ntask; task += 2 * stride) {
+        const int task2 = task + stride;
         const int i = task / tiles, t = task % tiles;
-        const int c = t * 128 + lane * 4;
-        const float4 a = psum<4>(p, segtab, src, i, c);
-        if (swiglu) {  // interleaved (gate, up) pairs -> outputs c/2, c/2+1
-            const __nv_bfloat162 o = __floats2bfloat162_rn(a.x / (1.f + __expf(-a.x)) * a.y,
-                                                          a.z / (1.f + __expf(-a.z)) * a.w);
-            *reinterpret_cast<__nv_bfloat162*>(p.hmid + (size_t)i * p.F + c / 2) = o;
-        } else {
-            const __nv_bfloat162 o0 = __floats2bfloat162_rn(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
-            const __nv_bfloat162 o1 = __floats2bfloat162_rn(fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
-            uint2 u;
-            u.x = *reinterpret_cast<const uint32_t*>(&o0);
-            u.y = *reinterpret_cast<const uint32_t*>(&o1);
-            *reinterpret_cast<uint2*>(p.hmid + (size_t)i * p.F + c) = u;
-        }
+        const int i2 = task2 / tiles, t2 = task2 % tiles;
+        const float4 a = psum<4>(p, segtab, src, i, t * 128 + lane * 4);
+        float4 a2 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (task2 < ntask) a2 = psum<4>(p, segtab, src, i2, t2 * 128 + lane * 4);
+        act_store(p, swiglu, i, t * 128 + lane * 4, a);
+        if (task2 < ntask) act_store(p, swiglu, i2, t2 * 128 + lane * 4, a2);
     }
 }
+
+constexpr int kAttnSlots = 4;                                    // (bulk-copy attention variant: see git history)
+constexpr int kAttnWarpBytes = 2048 + 512 + kAttnSlots * 4096;
+constexpr int kAttnCtlBytes = kAttnSlots * 8 + 8;
 
 // Attention, one warp per (compact row, KV head) task; head_dim 64 (2 dims per
 // lane).  Scores: lanes over positions; P.V: lanes over positions with a
 // 64-wide accumulator, then a register butterfly leaves dims (2l, 2l+1) in
 // lane l.  Masking: a position whose token exited before this layer has no
 // K/V here (kv_depth < layer); the current position is always valid.
-__device__ __noinline__ void phase_attn(const Params& p, const int4* segtab, const Phase& src, int layer, const int* live,
-                           int n_live, float* scratch) {
+__device__ __noinline__ void phase_attn(const Params& p, const int4* segtab, const Phase& src, int layer,
+                                        const int* live, int n_live, float* scratch, uint8_t* attn_ctl) {
+    (void)attn_ctl;
     const int warp = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
     const int Gq = p.H / p.Hkv;
     float* q_s = scratch + warp * (8 * 64 + 128);  // [Gq][64]
@@ -362,13 +391,21 @@ __device__ __noinline__ void phase_head_reduce(const Params& p, const int4* segt
         float m = -INFINITY, s = 0.f;
         int am = 0x7fffffff;
         const int t1 = min(src.tiles, (ch + 1) * kHeadChunk);
-        for (int t = ch * kHeadChunk; t < t1; ++t) {
-            const int c = t * 128 + lane * 4;
-            const float4 v = psum<4>(p, segtab, src, i, c);
-            const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int t = ch * kHeadChunk; t < t1; t += 4) {
+            float4 v[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (c + k < p.V) lse_merge(m, s, am, vv[k], 1.f, c + k);
+            for (int u = 0; u < 4; ++u)
+                if (t + u < t1) v[u] = psum<4>(p, segtab, src, i, (t + u) * 128 + lane * 4);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (t + u < t1) {
+                    const int c = (t + u) * 128 + lane * 4;
+                    const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (c + k < p.V) lse_merge(m, s, am, vv[k], 1.f, c + k);
+                }
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -393,7 +430,28 @@ __device__ __forceinline__ void write_row(const StepOutDev& o, int r, int exit_l
 }
 
 // Warp 2 of every CTA: identical decisions and compaction; CTA 0 writes.
-__device__ __noinline__ void phase_decide(const Params& p, const Phase& ph, int nchunk, int* live, int* n_live_s) {
+// All SIMT threads: thread i merges row i's vocabulary chunks (in order) into
+// {token, confidence, logprob} in shared memory.
+__device__ __noinline__ void decide_merge(const Params& p, int nchunk, int n_live, float4* merged) {
+    const int t = threadIdx.x - 64;
+    for (int i = t; i < n_live; i += kSimtThreads) {
+        float m = -INFINITY, S = 0.f;
+        int tok = 0x7fffffff;
+        for (int c0 = 0; c0 < nchunk; c0 += 16) {
+            float4 st[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (c0 + u < nchunk) st[u] = __ldcg(p.stats + (size_t)i * nchunk + c0 + u);
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (c0 + u < nchunk) lse_merge(m, S, tok, st[u].x, st[u].y, __float_as_int(st[u].z));
+        }
+        merged[i] = make_float4(__int_as_float(tok), 1.f / S, -logf(S), 0.f);
+    }
+}
+
+__device__ __noinline__ void phase_decide(const Params& p, const Phase& ph, const float4* merged, int* live,
+                                          int* n_live_s) {
     const int lane = threadIdx.x & 31;
     const int e = ph.exit_index;
     const bool final = ph.flags & kFlagFinal;
@@ -408,13 +466,9 @@ __device__ __noinline__ void phase_decide(const Params& p, const Phase& ph, int 
         bool survive = false;
         if (valid) {
             r = live[i];
-            float m = -INFINITY, S = 0.f;
-            int tok = 0x7fffffff;
-            for (int ch = 0; ch < nchunk; ++ch) {
-                const float4 st = __ldcg(p.stats + (size_t)i * nchunk + ch);
-                lse_merge(m, S, tok, st.x, st.y, __float_as_int(st.z));
-            }
-            const float conf = 1.f / S, logp = -logf(S);
+            const float4 mr = merged[i];
+            const int tok = __float_as_int(mr.x);
+            const float conf = mr.y, logp = mr.z;
             switch (p.policy) {
                 case EEB_FLAT:
                     if (writer)
@@ -496,7 +550,7 @@ struct Smem {
     uint32_t wfull, wempty, xfull, xempty, accfull, accempty;  // barrier arrays (8 B apart)
 };
 
-__global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant__ Params p, const int4* segtab) {
+__global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant__ Params p, const int4* segtab_g) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -522,6 +576,8 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
     float* red = reinterpret_cast<float*>(ptr_of(misc + 64));                // [64 + 1]
     Phase* prog = reinterpret_cast<Phase*>(ptr_of(misc + 64 + 64 * 4 + 64));  // [n_phases]
     int* live = reinterpret_cast<int*>(prog + p.n_phases);                   // [kMaxRows]
+    int4* seg_s = reinterpret_cast<int4*>(                                   // [n_segtab], 16 B aligned
+        (reinterpret_cast<uintptr_t>(live + kMaxRows) + 15) & ~(uintptr_t)15);
     float* scratch = reinterpret_cast<float*>(ptr_of(sm.x));                 // X ring, idle in SIMT phases
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -529,6 +585,9 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
     for (int i = threadIdx.x; i < p.n_phases * (int)(sizeof(Phase) / 4); i += blockDim.x)
         reinterpret_cast<int*>(prog)[i] = reinterpret_cast<const int*>(p.phases)[i];
     for (int i = threadIdx.x; i < p.batch; i += blockDim.x) live[i] = i;
+    for (int i = threadIdx.x; i < p.n_segtab; i += blockDim.x) seg_s[i] = segtab_g[i];
+    const int4* segtab = seg_s;
+    uint8_t* attn_ctl = reinterpret_cast<uint8_t*>(seg_s + p.n_segtab);  // [kSimtWarps][kAttnCtlBytes], 8 B aligned
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < Sw; ++i) {
@@ -542,6 +601,10 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
         for (int i = 0; i < 2; ++i) {
             mbar_init(sm.accfull + 8 * i, 1);
             mbar_init(sm.accempty + 8 * i, 128);
+        }
+        for (int w = 0; w < kSimtWarps; ++w) {  // attention ring barriers (the rings live in the X ring)
+            for (int k = 0; k < kAttnSlots; ++k) mbar_init(smem_u32(attn_ctl + w * kAttnCtlBytes + 8 * k), 1);
+            *reinterpret_cast<uint32_t*>(attn_ctl + w * kAttnCtlBytes + kAttnSlots * 8) = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         *w_progress = 0;
@@ -638,11 +701,8 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
             if (pi > 0) {
                 const bool prev_gemm = prog[pi - 1].kind == kPhaseGemm;
                 if (!prev_gemm) named_sync(1, kSimtThreads);  // this CTA's SIMT work of phase pi-1 is done
+                else if (warp == 2 || is_epi) named_sync(2, 160);  // this CTA's epilogue of phase pi-1 is done
                 if (warp == 2 && lane == 0) {
-                    if (prev_gemm)
-                        while (*epi_count < 128u * gemm_done) {
-                        }
-                    __threadfence();
                     stamp(p, pi - 1, 3);
                     if (p.bar_mode == 0) counter_barrier(ctr, bar_base + (unsigned long long)pi * G);
                     else if (p.bar_mode == 1) grid_barrier(p.bar, p.bar + 1, (unsigned)G);
@@ -693,26 +753,30 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
                         kbi = kend;
                     }
                     if (warp == 4 && lane == 0) stamp(p, pi, 2);
-                    __threadfence();
-                    atomicAdd((unsigned*)epi_count, 1u);
                 }
                 ++gemm_done;
             } else {
                 switch (ph.kind) {
                     case kPhaseNorm: phase_norm(p, segtab, prog, ph, live, n_live, red); break;
-                    case kPhaseAttn: phase_attn(p, segtab, prog[ph.src], ph.layer, live, n_live, scratch); break;
+                    case kPhaseAttn:
+                        phase_attn(p, segtab, prog[ph.src], ph.layer, live, n_live, scratch, attn_ctl);
+                        break;
                     case kPhaseAct: phase_act(p, segtab, prog[ph.src], n_live); break;
                     case kPhaseHeadReduce: phase_head_reduce(p, segtab, prog[ph.src], n_live); break;
-                    case kPhaseDecide:
-                        if (warp == 2)
-                            phase_decide(p, ph, (prog[ph.src].tiles + kHeadChunk - 1) / kHeadChunk, live, n_live_s);
+                    case kPhaseDecide: {
+                        float4* merged = reinterpret_cast<float4*>(scratch);  // X ring is idle
+                        decide_merge(p, (prog[ph.src].tiles + kHeadChunk - 1) / kHeadChunk, n_live, merged);
+                        named_sync(3, kSimtThreads);
+                        if (warp == 2) phase_decide(p, ph, merged, live, n_live_s);
                         break;
+                    }
                     case kPhaseFinalize: phase_finalize(p, red); break;
                     default: break;
                 }
             }
         }
         if (prog[p.n_phases - 1].kind != kPhaseGemm) named_sync(1, kSimtThreads);
+        else if (warp == 2 || is_epi) named_sync(2, 160);
     }
     tc_fence_before();
     __syncthreads();
@@ -725,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
 }  // namespace
 
 void launch(const Params& p, const int4* segtab, int grid, cudaStream_t s) {
-    const unsigned smem = smem_bytes(p.bpad, p.w_stages, p.x_stages, p.n_phases);
+    const unsigned smem = smem_bytes(p.bpad, p.w_stages, p.x_stages, p.n_phases, p.n_segtab);
     EEB_CUDA(cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);

@@ -27,8 +27,9 @@ constexpr int kBM = 128;       // UMMA M: output features per tile
 constexpr int kBK = 64;        // k-block: one 128-byte swizzle atom of bf16
 constexpr int kMaxSeg = 8;     // partial-sum segments one CTA may own in a GEMM phase
 constexpr int kMaxRows = 128;  // rows per step on this path (UMMA N <= 128, live list in smem)
-constexpr int kSegUnroll = 12; // partial segments of one tile summed with all loads in flight
+constexpr int kSegUnroll = 10; // partial segments of one tile summed with all loads in flight
 constexpr int kHeadChunk = 16; // vocabulary tiles (x128) per exit-head reduction task
+constexpr int kAttnScratchBytes = 2048 + 512 + 4 * 4096;  // per SIMT warp, in the X ring (== kAttnWarpBytes)
 
 enum PhaseKind : int {
     kPhaseGemm = 0,        // y = X W^T, stream-K, partial sums -> partial buffer
@@ -72,6 +73,7 @@ struct Params {
     int bar_mode, dbg, l2_ahead;  // bar_mode 0: counter barrier; dbg / l2_ahead: timing experiments
     unsigned long long* trace;    // optional [G][n_phases][8] globaltimer stamps
     const void* const* wbase;     // timing experiments only
+    int n_segtab;                 // entries of the segment table (copied to shared memory)
     // model
     int D, F, dq, dkv, H, Hkv, hd, V, S, L, n_exits, mlp_kind, policy, serving_depth;
     float eps, th;
@@ -98,10 +100,10 @@ struct Params {
 };
 
 // Shared-memory bytes for a configuration (host and device agree).
-__host__ __device__ inline unsigned smem_bytes(int bpad, int w_stages, int x_stages, int n_phases) {
+__host__ __device__ inline unsigned smem_bytes(int bpad, int w_stages, int x_stages, int n_phases, int n_segtab) {
     return 1024u + (unsigned)w_stages * (kBM * kBK * 2) + (unsigned)x_stages * (unsigned)(bpad * kBK * 2) +
            (unsigned)(2 * w_stages + 2 * x_stages + 8) * 8u + 64u + (unsigned)n_phases * (unsigned)sizeof(Phase) +
-           (unsigned)(kMaxRows + 64) * 4u + 256u;
+           (unsigned)(kMaxRows + 64) * 4u + 256u + (unsigned)n_segtab * 16u + 16u + 6u * 40u;
 }
 
 // Launch the program (cooperative, grid = SM count).  segtab: per GEMM phase
