@@ -858,6 +858,7 @@ std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, fl
     if (const char* v = std::getenv("EEB_MK_WSTAGES")) q.w_stages = std::min(q.w_stages, std::max(2, std::atoi(v)));
     q.bar_mode = 0;
     q.dbg = std::getenv("EEB_MK_DBG") ? std::atoi(std::getenv("EEB_MK_DBG")) : 0;  // timing experiments only
+    q.l2_ahead = std::getenv("EEB_MK_L2") ? std::atoi(std::getenv("EEB_MK_L2")) : 0;
     q.D = D;
     q.F = F;
     q.dq = m.dq;

@@ -19,6 +19,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 #include <mutex>
 
@@ -122,7 +124,10 @@ __device__ __forceinline__ bool elect_one_sync() {
     return pred != 0;
 }
 
+namespace cg = cooperative_groups;
+
 struct TcParams {
+    int cs;            // CTAs per cluster along the split dimension (1 = no on-chip reduction)
     int N, K;
     int kb_per;        // k-blocks per split
     int kblocks;       // total k-blocks
@@ -236,16 +241,51 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
-        float* plane = p.part + (int64_t)split * p.split_stride;
-        for (int c0 = 0; c0 < p.bpad; c0 += 16) {
-            float v[16];
-            tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective: every warp runs every chunk
-            if (n < p.N) {
+        if (p.cs == 1) {
+            float* plane = p.part + (int64_t)split * p.split_stride;
+            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective: every warp runs every chunk
+                if (n < p.N) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (c0 + j < rows) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
+                    for (int j = 0; j < 16; ++j)
+                        if (c0 + j < rows) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
+                }
+            }
+        } else {
+            // stage this CTA's [128 features][bpad rows] partial in its (now idle) pipeline smem
+            float* red = reinterpret_cast<float*>(base_ptr);
+            const int f = quarter * 32 + lane;
+            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) red[(c0 + j) * (kBM + 1) + f] = v[j];
             }
         }
+    }
+    if (p.cs > 1) {
+        // Split-K reduction on chip: the cs CTAs of a cluster hold consecutive
+        // k-ranges of one tile; CTA rank r sums rows r, r+cs, ... of the tile
+        // over the cluster's smem partials in rank (= k) order and writes one
+        // plane per cluster — cs x fewer partial planes in HBM/L2 and for the
+        // consumers to read.  Deterministic (fixed order).
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();
+        if (warp >= 2) {
+            const int rank = (int)cluster.block_rank();
+            const int rows = *p.n_active;
+            const int t = threadIdx.x - 64;  // 0..127: feature of the tile
+            const int n = m_tile * kBM + t;
+            float* plane = p.part + (int64_t)(split / p.cs) * p.split_stride;
+            const float* red = reinterpret_cast<const float*>(base_ptr);
+            for (int row = rank; row < min(rows, p.bpad); row += p.cs) {
+                float acc = 0.f;
+                for (int q = 0; q < p.cs; ++q) acc += cluster.map_shared_rank(red, q)[row * (kBM + 1) + t];
+                if (n < p.N) plane[(int64_t)row * p.N + n] = acc;
+            }
+        }
+        cluster.sync();  // keep every CTA's partial alive until the whole cluster has read it
     }
     tc_fence_before();
     __syncthreads();
@@ -315,9 +355,19 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const int env_wave = std::getenv("EEB_TC_WAVE") ? std::atoi(std::getenv("EEB_TC_WAVE")) : 0;
     static const int env_stages = std::getenv("EEB_TC_STAGES") ? std::atoi(std::getenv("EEB_TC_STAGES")) : 0;
     const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
-    int splits = std::max(1, std::min(std::min(kblocks / 2, a.max_planes), wave / tiles));
-    const int kb_per = (kblocks + splits - 1) / splits;
+    int splits = std::max(1, std::min(kblocks / 2, wave / tiles));
+    int kb_per = (kblocks + splits - 1) / splits;
     splits = (kblocks + kb_per - 1) / kb_per;
+    // Clusters of cs CTAs along K reduce their partials on chip (DSMEM): pick
+    // the largest cs <= 8 dividing the split count.
+    static const int env_cs = std::getenv("EEB_TC_CLUSTER") ? std::atoi(std::getenv("EEB_TC_CLUSTER")) : 1;
+    int cs = 1;
+    for (int c = std::min(env_cs, 8); c > 1; --c)
+        if (splits % c == 0) {
+            cs = c;
+            break;
+        }
+    if (splits > a.max_planes) return 0;  // (cs may still fall back to 1 below)
     const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
     // ~half the SM's shared memory so two GEMM CTAs co-reside: the next GEMM of
     // the step (PDL) streams its weights while this one drains.
@@ -330,6 +380,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     while (tmem_cols < bpad) tmem_cols *= 2;
 
     TcParams p;
+    p.cs = cs;
     p.N = a.N;
     p.K = a.K;
     p.kb_per = kb_per;
@@ -343,11 +394,27 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
+    // the reduction buffer [bpad][129] f32 reuses the (drained) pipeline stages
+    if (cs > 1 && (size_t)bpad * (kBM + 1) * 4 > (size_t)stages * stage_bytes) cs = 1;
+    p.cs = cs;
     EEB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(tiles, splits);
-    launch_pdl(gemm_tc_kernel, grid, dim3(kThreads), smem, s, mw, mx, p);
-    EEB_CHECK_LAUNCH();
-    return splits;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = cs;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p));
+    return splits / cs;
 }
 
 }  // namespace eeb

@@ -624,6 +624,22 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
         // ------------------------------------------------------------------ W producer
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
+            // L2 prefetch cursor, l2_ahead tiles ahead of the ring: HBM keeps
+            // streaming future phases' weights into the 126 MB L2 while the ring
+            // (a few tiles of shared memory) waits for barriers and activations.
+            int ppi = -1, pk = 0, pe = 0;
+            auto pf_next = [&]() {
+                while (pk >= pe) {
+                    if (++ppi >= p.n_phases) return;
+                    if (prog[ppi].kind != kPhaseGemm) continue;
+                    cta_range(prog[ppi], blk, G, pk, pe);
+                }
+                const Phase& q = prog[ppi];
+                const int tile = pk / q.kb, k = pk - tile * q.kb;
+                tma_prefetch_2d(p.maps + q.wmap, k * kBK, tile * kBM);
+                ++pk;
+            };
+            for (int j = 0; j < p.l2_ahead; ++j) pf_next();
             uint32_t it = 0;
             for (int pi = 0; pi < p.n_phases; ++pi) {
                 const Phase ph = prog[pi];
@@ -633,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const __grid_constant
                 cta_range(ph, blk, G, s, e);
                 for (int kbi = s; kbi < e; ++kbi, ++it) {
                     const uint32_t slot = it % Sw, ph_bit = (it / Sw) & 1u;
+                    if (p.l2_ahead > 0 && ppi < p.n_phases) pf_next();
                     mbar_wait(sm.wempty + 8 * slot, ph_bit ^ 1u);
                     if (kbi == s) stamp(p, pi, 4);
                     if (kbi == e - 1) stamp(p, pi, 5);

@@ -29,7 +29,7 @@ constexpr int kMaxSeg = 8;     // partial-sum segments one CTA may own in a GEMM
 constexpr int kMaxRows = 128;  // rows per step on this path (UMMA N <= 128, live list in smem)
 constexpr int kSegUnroll = 10; // partial segments of one tile summed with all loads in flight
 constexpr int kHeadChunk = 16; // vocabulary tiles (x128) per exit-head reduction task
-constexpr int kAttnScratchBytes = 2048 + 512 + 4 * 4096;  // per SIMT warp, in the X ring (== kAttnWarpBytes)
+constexpr int kAttnScratchBytes = (8 * 64 + 128) * 4;  // per SIMT warp attention scratch (q, k, v), in the X ring
 
 enum PhaseKind : int {
     kPhaseGemm = 0,        // y = X W^T, stream-K, partial sums -> partial buffer
