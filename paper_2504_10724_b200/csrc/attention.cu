@@ -14,6 +14,9 @@
 // (SURVEY §7 hard part 5).
 #include <cuda.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "kernels.h"
 
 namespace eeb {
@@ -527,6 +530,405 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant: a CTA walks work items (row, kv-head) with a grid
+// stride, and the K/V chunks of consecutive items stream through NBUF
+// shared-memory buffers, so the TMA for the next item is in flight while the
+// current one computes (the one-item-per-CTA kernel above exposes a full
+// HBM latency per item; C2 has 2048 items of only ~45 KB each).  Chunks are
+// smaller (32 KB of K+V) so three CTAs share an SM and one CTA's prologue
+// (split-K plane sum, RoPE, KV append) overlaps the others' loads.
+// ---------------------------------------------------------------------------
+template <int HD>
+struct PipeCfg {
+    static constexpr int CB = HD / 64;
+    static constexpr int CP = HD == 64 ? 128 : 64;           // positions per chunk
+    static constexpr uint32_t kBlockBytes = CP * 128;        // one 64-dim column block
+    static constexpr uint32_t kBufBytes = 2 * CB * kBlockBytes;  // K + V of one chunk
+    static constexpr int NBUF = 2;
+    static constexpr int NW = HD == 64 ? 8 : 4;  // warps: positions of a chunk split NW ways
+};
+
+// Shared-memory plan of the pipelined kernel (host and device agree).
+template <int HD>
+struct PipeSmem {
+    int n4, pf_floats, pf_bytes;
+    bool use_pf;
+    size_t q_off, raw_off, pf_off, pos_off, total;
+    __host__ __device__ PipeSmem(int G, int splits, int max_rows) {
+        n4 = (G + 2) * HD / 4;
+        pf_floats = splits * n4 * 4 + HD;  // split-K planes of q/k/v + the RoPE cos/sin halves
+        pf_bytes = pf_floats * 4;
+        use_pf = pf_bytes <= 16 * 1024;
+        q_off = (size_t)PipeCfg<HD>::NBUF * PipeCfg<HD>::kBufBytes;
+        raw_off = q_off + 8 * HD * 4;
+        pf_off = raw_off + (size_t)(G + 2) * HD * 4;
+        pos_off = pf_off + (use_pf ? 2 * (size_t)pf_bytes : 0);
+        total = pos_off + 2 * (size_t)max_rows * 4;
+    }
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(PipeCfg<HD>::NW * 32, 2)
+    attention_pipe_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                          AttnArgs a) {
+    using C = PipeCfg<HD>;
+    constexpr int CB = C::CB, CP = C::CP, NBUF = C::NBUF, NW = C::NW;
+    constexpr uint32_t kBlockBytes = C::kBlockBytes, kBufBytes = C::kBufBytes;
+    constexpr int NT = HD / 8, KS = HD / 16, TPW = CP / 8 / NW;
+    static_assert(CP <= C::NW * 32, "one depth byte per thread per chunk");
+    pdl_launch_dependents();
+    pdl_wait();
+    const int H = a.n_heads, Hkv = a.n_kv_heads, G = H / Hkv;
+    const int dq = H * HD, dkv = Hkv * HD, half = HD / 2;
+    const int n_rows = *a.n_active;
+    const int n_items = n_rows * Hkv;
+    if ((int)blockIdx.x >= n_items) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const PipeSmem<HD> L(G, a.splits, a.max_rows);
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    uint8_t* base = smem_raw + (sbase - raw);
+    float* q_s = reinterpret_cast<float*>(base + L.q_off);      // [8][HD]
+    float* raw_s = reinterpret_cast<float*>(base + L.raw_off);  // [(G + 2)][HD]
+    float* pf = reinterpret_cast<float*>(base + L.pf_off);      // [2][pf_floats]
+    int* pos_s = reinterpret_cast<int*>(base + L.pos_off);      // [rows]
+    int* slot_s = pos_s + a.max_rows;
+    __shared__ float kn_s[HD], vn_s[HD], cos_s[HD / 2], sin_s[HD / 2];
+    __shared__ uint8_t dep_s[CP];
+    __shared__ __align__(8) uint64_t bars[NBUF];
+
+    for (int r = threadIdx.x; r < n_rows; r += blockDim.x) {
+        pos_s[r] = a.pos[r];
+        slot_s[r] = a.slot[r];
+    }
+    __syncthreads();
+
+    auto n_chunks_of = [&](int item) { return pos_s[item / Hkv] / CP + 1; };
+    auto issue = [&](int item, int chunk, int buf) {  // thread 0
+        const int i = item / Hkv, g = item % Hkv;
+        const int pos = pos_s[i], zc = slot_s[i] * Hkv + g;
+        const int c0 = chunk * CP;
+        const int n_load = min(CP, pos + 1 - c0);
+        const int boxes = (n_load + kBoxRows - 1) / kBoxRows;
+        const uint32_t bar = smem_u32(&bars[buf]);
+        const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)boxes * CB * kBoxRows * 128 * 2)
+                     : "memory");
+        for (int b = 0; b < boxes; ++b)
+            for (int cb = 0; cb < CB; ++cb) {
+                const uint32_t off = cb * kBlockBytes + b * kBoxRows * 128;
+                tma_3d(k_s + off, &kmap, bar, cb * 64, c0 + b * kBoxRows, zc);
+                tma_3d(v_s + off, &vmap, bar, cb * 64, c0 + b * kBoxRows, zc);
+            }
+    };
+    int is_item = blockIdx.x, is_chunk = 0;  // TMA issue cursor (thread 0)
+    auto issue_next = [&](int buf) {
+        if (is_item >= n_items) return;
+        issue(is_item, is_chunk, buf);
+        if (++is_chunk == n_chunks_of(is_item)) {
+            is_chunk = 0;
+            is_item += gridDim.x;
+        }
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+        for (int b = 0; b < NBUF; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[b])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b < NBUF; ++b) issue_next(b);
+    }
+    // column of the fused QKV row for float4 v4 of item (g): q heads, then k, then v
+    auto col_of = [&](int v4, int g) {
+        const int nq4 = G * HD / 4;
+        return v4 < nq4 ? g * G * HD + 4 * v4
+             : (v4 < nq4 + HD / 4 ? dq + g * HD + 4 * (v4 - nq4) : dq + dkv + g * HD + 4 * (v4 - nq4 - HD / 4));
+    };
+    // async prefetch of an item's q/k/v planes and RoPE row into pf[buf]
+    auto prefetch = [&](int item, int buf) {
+        if (item < n_items) {
+            const int i = item / Hkv, g = item % Hkv;
+            const float* src = a.qkv + (int64_t)i * (dq + 2 * dkv);
+            float* dst = pf + (size_t)buf * L.pf_floats;
+            for (int v4 = threadIdx.x; v4 < L.n4; v4 += blockDim.x) {
+                const int col = col_of(v4, g);
+                for (int sp = 0; sp < a.splits; ++sp)
+                    cp_async16(dst + ((size_t)sp * L.n4 + v4) * 4, src + sp * a.split_stride + col);
+            }
+            const int pos = pos_s[i];
+            for (int t = threadIdx.x; t < HD / 4; t += blockDim.x) {  // cos then sin, half floats each
+                const float* r = t < HD / 8 ? a.rope_cos + (int64_t)pos * half + 4 * t
+                                            : a.rope_sin + (int64_t)pos * half + 4 * (t - HD / 8);
+                cp_async16(dst + (size_t)a.splits * L.n4 * 4 + 4 * t, r);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // depth byte of the next chunk in this CTA's walk, held in a register
+    int dp_item = blockIdx.x, dp_chunk = 0;
+    uint8_t dep_reg = 0;
+    auto load_dep = [&]() {
+        if (dp_item < n_items) {
+            const int i = dp_item / Hkv;
+            const int pos = pos_s[i], c0 = dp_chunk * CP;
+            if ((int)threadIdx.x < min(CP, pos + 1 - c0))
+                dep_reg = a.kv_depth[(int64_t)slot_s[i] * a.max_seq + c0 + threadIdx.x];
+            if (++dp_chunk == pos / CP + 1) {
+                dp_chunk = 0;
+                dp_item += gridDim.x;
+            }
+        }
+    };
+    load_dep();
+    if (L.use_pf) prefetch(blockIdx.x, 0);
+
+    const int h = lane >> 2, kq = (lane & 3) * 2;
+    const float qscale = rsqrtf((float)HD);
+    uint32_t seq = 0;  // consumer's position in the TMA load sequence
+    int it = 0;        // items processed by this CTA
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int i = item / Hkv, g = item % Hkv;
+        const int slot = slot_s[i], pos = pos_s[i];
+        __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
+        __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
+        // q (G heads), k, v of this item: fixed-order sum of the split-K planes
+        if (L.use_pf) {
+            prefetch(item + gridDim.x, (it + 1) & 1);  // next item's planes fly while this one computes
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+            __syncthreads();  // every thread's copies (the RoPE rows are read across threads)
+            const float* src = pf + (size_t)(it & 1) * L.pf_floats;
+            for (int v4 = threadIdx.x; v4 < L.n4; v4 += blockDim.x) {
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int sp = 0; sp < a.splits; ++sp) {
+                    const float4 t = *reinterpret_cast<const float4*>(src + ((size_t)sp * L.n4 + v4) * 4);
+                    acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+                }
+                *reinterpret_cast<float4*>(raw_s + 4 * v4) = acc;
+            }
+            for (int t = threadIdx.x; t < HD; t += blockDim.x) {
+                const float v = src[(size_t)a.splits * L.n4 * 4 + t];
+                if (t < half) cos_s[t] = v;
+                else sin_s[t - half] = v;
+            }
+        } else {
+            const float* src = a.qkv + (int64_t)i * (dq + 2 * dkv);
+            for (int v4 = threadIdx.x; v4 < L.n4; v4 += blockDim.x) {
+                const int col = col_of(v4, g);
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int sp = 0; sp < 16; ++sp) {
+                    if (sp < a.splits) {
+                        const float4 t = *reinterpret_cast<const float4*>(src + sp * a.split_stride + col);
+                        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+                    }
+                }
+                *reinterpret_cast<float4*>(raw_s + 4 * v4) = acc;
+            }
+            for (int t = threadIdx.x; t < half; t += blockDim.x) {
+                cos_s[t] = a.rope_cos[(int64_t)pos * half + t];
+                sin_s[t] = a.rope_sin[(int64_t)pos * half + t];
+            }
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < 8 * HD; idx += blockDim.x) {
+            const int hh = idx / HD, j = idx % HD;
+            float v = 0.f;
+            if (hh < G) {
+                const float* q = raw_s + hh * HD;
+                const int jj = j < half ? j : j - half;
+                const float x0 = q[jj], x1 = q[jj + half];
+                v = (j < half ? x0 * cos_s[jj] - x1 * sin_s[jj] : x0 * sin_s[jj] + x1 * cos_s[jj]) * qscale;
+            }
+            q_s[hh * HD + j] = v;
+        }
+        for (int j = threadIdx.x; j < HD; j += blockDim.x) {
+            const float* k = raw_s + G * HD;
+            const float* vv = raw_s + (G + 1) * HD;
+            const int jj = j < half ? j : j - half;
+            const float x0 = k[jj], x1 = k[jj + half];
+            const float kr = j < half ? x0 * cos_s[jj] - x1 * sin_s[jj] : x0 * sin_s[jj] + x1 * cos_s[jj];
+            const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(vv[j]);
+            kc[(int64_t)pos * HD + j] = kt;
+            vc[(int64_t)pos * HD + j] = vt;
+            kn_s[j] = __bfloat162float(kt);
+            vn_s[j] = __bfloat162float(vt);
+        }
+        __syncthreads();
+        uint32_t qa[KS][4];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            qa[k][0] = pack_bf16(q_s[h * HD + 16 * k + kq], q_s[h * HD + 16 * k + kq + 1]);
+            qa[k][1] = 0u;
+            qa[k][2] = pack_bf16(q_s[h * HD + 16 * k + 8 + kq], q_s[h * HD + 16 * k + 8 + kq + 1]);
+            qa[k][3] = 0u;
+        }
+        float o[NT][4];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+        float m_run = -INFINITY, l_run = 0.f;
+        const int n_chunks = pos / CP + 1;
+        for (int ci = 0; ci < n_chunks; ++ci, ++seq) {
+            const int buf = (int)(seq % NBUF);
+            const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
+            uint8_t* kb = base + buf * kBufBytes;
+            const int c0 = ci * CP;
+            const int cn = min(CP, pos + 1 - c0);
+            if ((int)threadIdx.x < CP) dep_s[threadIdx.x] = dep_reg;
+            load_dep();  // the following chunk's depth bytes
+            mbar_wait(smem_u32(&bars[buf]), (seq / NBUF) & 1u);
+            if (pos < c0 + CP) {  // the new position lives in this chunk: patch it (swizzled)
+                const int r = pos - c0;
+                for (int j = threadIdx.x; j < HD; j += blockDim.x) {
+                    const uint32_t off = (j / 64) * kBlockBytes + swz(r, (j % 64) / 8) + (j % 8) * 2;
+                    *reinterpret_cast<__nv_bfloat16*>(kb + off) = __float2bfloat16_rn(kn_s[j]);
+                    *reinterpret_cast<__nv_bfloat16*>(kb + CB * kBlockBytes + off) = __float2bfloat16_rn(vn_s[j]);
+                }
+            }
+            __syncthreads();
+            const int n_tiles = (cn + 7) / 8;
+            float sc[TPW][2];
+            int my_tiles = 0;
+            float cmax = -INFINITY;
+#pragma unroll
+            for (int tt = 0; tt < TPW; ++tt) {
+                const int t = warp + tt * NW;
+                sc[tt][0] = sc[tt][1] = -INFINITY;
+                if (t >= n_tiles) continue;
+                my_tiles = tt + 1;
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                const int row = t * 8 + (lane & 7);
+#pragma unroll
+                for (int k2 = 0; k2 < KS; k2 += 2) {
+                    const int mi = lane >> 3;
+                    const int dim = 16 * (k2 + (mi >> 1)) + 8 * (mi & 1);
+                    uint32_t b[4];
+                    ldsm_x4(k_s + (dim / 64) * kBlockBytes + swz(row, (dim % 64) / 8), b);
+                    mma_bf16(c, qa[k2], b[0], b[1]);
+                    mma_bf16(c, qa[k2 + 1], b[2], b[3]);
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int pl = t * 8 + kq + e;
+                    const int p = c0 + pl;
+                    const bool valid = h < G && p <= pos && (p == pos || dep_s[pl] >= a.layer);
+                    sc[tt][e] = valid ? c[e] : -INFINITY;
+                    cmax = fmaxf(cmax, sc[tt][e]);
+                }
+            }
+            cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, 1));
+            cmax = fmaxf(cmax, __shfl_xor_sync(0xffffffffu, cmax, 2));
+            const float m_new = fmaxf(m_run, cmax);
+            const float scale = m_new == -INFINITY ? 1.f : __expf(m_run - m_new);
+            float psum = 0.f;
+#pragma unroll
+            for (int tt = 0; tt < TPW; ++tt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float p = sc[tt][e] == -INFINITY ? 0.f : __expf(sc[tt][e] - m_new);
+                    sc[tt][e] = p;
+                    psum += p;
+                }
+            psum += __shfl_xor_sync(0xffffffffu, psum, 1);
+            psum += __shfl_xor_sync(0xffffffffu, psum, 2);
+            l_run = l_run * scale + psum;
+            m_run = m_new;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                o[n][0] *= scale;
+                o[n][1] *= scale;
+            }
+#pragma unroll
+            for (int tt = 0; tt < TPW; tt += 2) {
+                if (tt >= my_tiles) break;
+                const int ta = warp + tt * NW;
+                const bool has_b = tt + 1 < my_tiles;
+                const int tb = has_b ? ta + NW : ta;
+                uint32_t pa[4];
+                pa[0] = pack_bf16(sc[tt][0], sc[tt][1]);
+                pa[1] = 0u;
+                pa[2] = has_b ? pack_bf16(sc[tt + 1][0], sc[tt + 1][1]) : 0u;
+                pa[3] = 0u;
+                const int mi = lane >> 3;
+                const int row = ((mi & 1) ? tb : ta) * 8 + (lane & 7);
+#pragma unroll
+                for (int n = 0; n < NT; n += 2) {
+                    const int dim = 8 * (n + (mi >> 1));
+                    uint32_t b[4];
+                    ldsm_x4_t(v_s + (dim / 64) * kBlockBytes + swz(row, (dim % 64) / 8), b);
+                    mma_bf16(o[n], pa, b[0], b[1]);
+                    mma_bf16(o[n + 1], pa, b[2], b[3]);
+                }
+            }
+            __syncthreads();  // every warp is done reading this buffer
+            if (ci + 1 < n_chunks && threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patch writes
+                issue_next(buf);
+            }
+            if (ci + 1 == n_chunks) {
+                // combine the four warps through this (drained) buffer, then refill it
+                float* comb = reinterpret_cast<float*>(kb);
+                float* ml = comb + NW * 8 * HD;
+                if (h < G) {
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) {
+                        comb[(warp * 8 + h) * HD + n * 8 + kq] = o[n][0];
+                        comb[(warp * 8 + h) * HD + n * 8 + kq + 1] = o[n][1];
+                    }
+                    if ((lane & 3) == 0) {
+                        ml[(warp * 8 + h) * 2] = m_run;
+                        ml[(warp * 8 + h) * 2 + 1] = l_run;
+                    }
+                }
+                __syncthreads();
+                __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out) + (int64_t)i * dq;
+                for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+                    const int hh = idx / HD, j = idx % HD;
+                    float M = -INFINITY;
+                    for (int w = 0; w < NW; ++w) M = fmaxf(M, ml[(w * 8 + hh) * 2]);
+                    float num = 0.f, den = 0.f;
+                    for (int w = 0; w < NW; ++w) {
+                        const float mw = ml[(w * 8 + hh) * 2];
+                        const float f = mw == -INFINITY ? 0.f : __expf(mw - M);
+                        num += f * comb[(w * 8 + hh) * HD + j];
+                        den += f * ml[(w * 8 + hh) * 2 + 1];
+                    }
+                    out[(g * G + hh) * HD + j] = __float2bfloat16_rn(num / den);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    // generic-proxy writes to this buffer precede the async-proxy refill
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue_next(buf);
+                }
+            }
+        }
+    }
+}
+
+template <int HD>
+void launch_pipe(const AttnArgs& a, int num_sms, cudaStream_t s) {
+    using C = PipeCfg<HD>;
+    const int G = a.n_heads / a.n_kv_heads;
+    if (a.splits > 16) throw Error(1, "attention: more than 16 QKV split-K planes");
+    const size_t smem = 1024 + PipeSmem<HD>(G, a.splits, a.max_rows).total;
+    auto kern = attention_pipe_kernel<HD>;
+    EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    EEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::NW * 32, smem));
+    const int items = a.max_rows * a.n_kv_heads;
+    const int grid = std::max(1, std::min(items, std::max(1, per_sm) * num_sms));
+    launch_pdl(kern, dim3(grid), dim3(C::NW * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
+               *static_cast<const CUtensorMap*>(a.v_map), a);
+    EEB_CHECK_LAUNCH();
+}
+
 template <int HD>
 void launch_mma(const AttnArgs& a, cudaStream_t s) {
     constexpr int CB = HD / 64, CP = HD == 64 ? 256 : 128;
@@ -546,8 +948,18 @@ void launch_mma(const AttnArgs& a, cudaStream_t s) {
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
     if (a.dtype == 1 && a.k_map && a.v_map && a.n_heads / a.n_kv_heads <= 8 &&
         (a.head_dim == 64 || a.head_dim == 128)) {
-        if (a.head_dim == 64) launch_mma<64>(a, s);
-        else launch_mma<128>(a, s);
+        // One (row, kv-head) item per CTA for head_dim 64 (MHA, C2: measured
+        // faster than the pipelined walk); the pipelined walk for head_dim 128
+        // (GQA, C4).  EEB_ATTN=one|pipe overrides (A/B).
+        static const char* env = std::getenv("EEB_ATTN");
+        const bool one_item = env ? std::string(env) == "one" : a.head_dim == 64;
+        if (one_item) {
+            if (a.head_dim == 64) launch_mma<64>(a, s);
+            else launch_mma<128>(a, s);
+        } else {
+            if (a.head_dim == 64) launch_pipe<64>(a, a.num_sms, s);
+            else launch_pipe<128>(a, a.num_sms, s);
+        }
         return;
     }
     const int G = a.n_heads / a.n_kv_heads;

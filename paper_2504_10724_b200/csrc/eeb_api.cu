@@ -111,7 +111,7 @@ struct eeb_ctx {
     int cap_rows = 0;
     eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
-    eeb::DevBuf head_tok, head_conf, head_logp;
+    eeb::DevBuf head_tok, head_conf, head_logp, head_tri;
     eeb::DevBuf o_exit, o_tok, o_conf, o_logp, o_breach, o_unch, o_bin, o_hist, o_nbr, o_sum;
     eeb::DevBuf o_htok, o_hconf, o_hlogp;
     std::vector<std::unique_ptr<eeb::DevBuf>> logits_keep;
@@ -369,6 +369,7 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     c->ws_elems = (int64_t)(c->ws.bytes / 4);
     c->rows.ensure((size_t)(32 + 12 * R) * 4);
     c->head_tok.ensure((size_t)R * 4);
+    c->head_tri.ensure((size_t)R * ((d.vocab + 127) / 128) * 16);
     c->head_conf.ensure((size_t)R * 4);
     c->head_logp.ensure((size_t)R * 4);
     c->o_exit.ensure((size_t)R * 4);
@@ -473,6 +474,28 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     return planes;
 }
 
+// Exit-head GEMM with the fused softmax tail; returns the vocab tiles written
+// to ctx->head_tri, 0 when the tensor-core path does not apply.
+int gemm_head_fused(eeb_ctx* c, const Model& m, const void* W, const void* X, int N, int K, const int* n_active,
+                    int batch) {
+    GemmArgs a;
+    a.dtype = m.desc.dtype;
+    a.W = W;
+    a.X = X;
+    a.n_active = n_active;
+    a.max_rows = batch;
+    a.N = N;
+    a.K = K;
+    a.out = nullptr;
+    a.plane_stride = 0;
+    a.max_planes = 1;
+    a.num_sms = c->num_sms;
+    a.head_tri = c->head_tri.as<float>();
+    if (gemm_tc(a, c->stream) == 0) return 0;
+    count(c, kCatHead, 1);
+    return (N + 127) / 128;
+}
+
 // ---------------------------------------------------------------------------
 // The step.  Per layer: QKV GEMM -> attention (sums the QKV planes, RoPE, KV
 // append) -> O GEMM -> residual+RMSNorm -> up GEMM -> activation -> down GEMM
@@ -561,6 +584,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             a.out = c->attn.p;
             a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[l - 1].data();
             a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[l - 1].data();
+            a.num_sms = c->num_sms;
             if (!skip_cat("attn")) launch_attention(a, s);
             count(c, kCatAttn, 1);
         }
@@ -610,16 +634,28 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             const int e = heads[hi];
             const bool is_final = hi + 1 == heads.size();
             Timer t(c, kCatHead);
-            const int hp = skip_cat("head") ? 1 : gemm(c, kCatHead, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
-            float* keep = nullptr;
-            if (c->retain_logits) {
-                while ((int)c->logits_keep.size() < d.n_exits) c->logits_keep.push_back(std::make_unique<DevBuf>());
-                c->logits_keep[e]->ensure((size_t)batch * d.vocab * 4);
-                keep = c->logits_keep[e]->as<float>();
-            }
             HeadOut h{c->head_tok.as<int>(), c->head_conf.as<float>(), c->head_logp.as<float>()};
-            launch_head_reduce(ws, hp, (int64_t)batch * d.vocab, d.vocab, cur.n_active, batch, h, keep, s);
+            // Fused head (tcgen05 GEMM epilogue emits per-tile softmax partials,
+            // decide merges them) unless the logits themselves are retained.
+            int head_tiles = 0;
+            if (!c->retain_logits && !skip_cat("head") && c->gemm_tier != 1 && d.dtype == EEB_BF16 &&
+                !std::getenv("EEB_HEAD_UNFUSED"))
+                head_tiles = gemm_head_fused(c, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
+            if (head_tiles == 0) {
+                const int hp =
+                    skip_cat("head") ? 1 : gemm(c, kCatHead, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
+                float* keep = nullptr;
+                if (c->retain_logits) {
+                    while ((int)c->logits_keep.size() < d.n_exits) c->logits_keep.push_back(std::make_unique<DevBuf>());
+                    c->logits_keep[e]->ensure((size_t)batch * d.vocab * 4);
+                    keep = c->logits_keep[e]->as<float>();
+                }
+                launch_head_reduce(ws, hp, (int64_t)batch * d.vocab, d.vocab, cur.n_active, batch, h, keep, s);
+                count(c, kCatHead, 1);
+            }
             DecideArgs da;
+            da.head_tri = head_tiles ? c->head_tri.as<float>() : nullptr;
+            da.head_tiles = head_tiles;
             da.policy = policy;
             da.exit_index = e;
             da.n_exits = d.n_exits;
@@ -636,7 +672,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             da.out = o;
             for (int k = 0; k < 64; ++k) da.layers[k] = k < d.n_exits ? m.exits[k] : 0;
             launch_decide(da, s);
-            count(c, kCatHead, 2);
+            count(c, kCatHead, 1);
             if (policy == EEB_INTROSPECTIVE && !is_final) {
                 launch_gather_rows(cur.x, alt.x, more ? h_cur : nullptr, h_alt, (int)hrow, I.src, alt.n_active,
                                    batch, D, s);

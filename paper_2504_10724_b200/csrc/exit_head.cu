@@ -102,6 +102,40 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
     __shared__ int n_live_s;
     const int n_live = *a.cur.n_active;
     const int e = a.exit_index;
+    if (a.head_tri) {
+        // K2 tail of the fused head GEMM: merge the per-(row, vocab tile)
+        // {max, sum exp, argmax} partials — warp per row, tiles in a fixed
+        // order (deterministic); argmax ties resolve to the lowest token id.
+        const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int i = threadIdx.x >> 5; i < n_live; i += nw) {
+            const float4* tri = reinterpret_cast<const float4*>(a.head_tri) + (int64_t)i * a.head_tiles;
+            float m = -INFINITY;
+            int am = 0x7fffffff;
+            for (int t = lane; t < a.head_tiles; t += 32) {
+                const float4 v = tri[t];
+                const int ai = __float_as_int(v.z);
+                if (v.x > m || (v.x == m && ai < am)) { m = v.x; am = ai; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+                const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+                if (m2 > m || (m2 == m && a2 < am)) { m = m2; am = a2; }
+            }
+            float sum = 0.f;
+            for (int t = lane; t < a.head_tiles; t += 32) {
+                const float4 v = tri[t];
+                sum += v.y * __expf(v.x - m);
+            }
+            sum = warp_sum(sum);
+            if (lane == 0) {
+                a.head.tok[i] = am;
+                a.head.conf[i] = 1.0f / sum;
+                a.head.logp[i] = -logf(sum);
+            }
+        }
+        __syncthreads();
+    }
     const StepOutDev& o = a.out;
     int survivors_total = 0;
     for (int base = 0; base < n_live; base += blockDim.x) {

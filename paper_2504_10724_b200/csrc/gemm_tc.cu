@@ -137,6 +137,8 @@ struct TcParams {
     const int* n_active;
     float* part;       // split-K planes, row stride N
     int64_t split_stride;
+    float4* head_tri;  // exit-head epilogue (splits == 1): per (row, tile) {max, sumexp, argmax}
+    int tiles;
 };
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -241,7 +243,42 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
-        if (p.cs == 1) {
+        if (p.head_tri) {
+            // Fused exit-head tail: stage the [rows x 128 vocab] logits tile
+            // transposed in the drained pipeline smem, then two threads per row
+            // scan 64 entries each for max / first argmax / sum exp(l - max).
+            float* red = reinterpret_cast<float*>(base_ptr);
+            const int f = quarter * 32 + lane;
+            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) red[(c0 + j) * (kBM + 1) + f] = v[j];
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int t = threadIdx.x - 64, hf = t & 1;
+            const int n0 = m_tile * kBM + hf * 64;
+            const int nv = max(0, min(64, p.N - n0));
+            const int lim = min(rows, p.bpad);
+            for (int r0 = 0; r0 < lim; r0 += 64) {  // warp-uniform trip count (shuffles below)
+                const int r = r0 + (t >> 1);
+                const int nvr = r < lim ? nv : 0;
+                const float* src = red + min(r, p.bpad - 1) * (kBM + 1) + hf * 64;
+                float m = -INFINITY;
+                int am = 0x7fffffff;
+                for (int j = 0; j < nvr; ++j)
+                    if (src[j] > m) { m = src[j]; am = n0 + j; }
+                float sum = 0.f;
+                for (int j = 0; j < nvr; ++j) sum += __expf(src[j] - m);
+                const float m2 = __shfl_xor_sync(0xffffffffu, m, 1);
+                const int a2 = __shfl_xor_sync(0xffffffffu, am, 1);
+                const float s2 = __shfl_xor_sync(0xffffffffu, sum, 1);
+                const float M = fmaxf(m, m2);
+                const int A = (m2 > m || (m2 == m && a2 < am)) ? a2 : am;
+                const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
+                if (hf == 0 && r < lim) p.head_tri[(int64_t)r * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A), 0.f);
+            }
+        } else if (p.cs == 1) {
             float* plane = p.part + (int64_t)split * p.split_stride;
             for (int c0 = 0; c0 < p.bpad; c0 += 16) {
                 float v[16];
@@ -367,6 +404,10 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
             cs = c;
             break;
         }
+    if (a.head_tri) {  // the fused head tail needs whole-K tiles
+        splits = 1;
+        kb_per = kblocks;
+    }
     if (splits > a.max_planes) return 0;  // (cs may still fall back to 1 below)
     const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
     // ~half the SM's shared memory so two GEMM CTAs co-reside: the next GEMM of
@@ -376,6 +417,14 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     if (stages < 2) stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (env_stages > 0) stages = std::min(env_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (stages < 2) return 0;
+    if (a.head_tri) {
+        cs = 1;
+        // the transposed logits tile reuses the pipeline stages
+        while ((size_t)bpad * (kBM + 1) * 4 > (size_t)stages * stage_bytes && stages < 8) ++stages;
+        if ((size_t)bpad * (kBM + 1) * 4 > (size_t)stages * stage_bytes ||
+            1024 + (size_t)stages * stage_bytes + 256 > (size_t)kSmemBudget)
+            return 0;
+    }
     int tmem_cols = 32;
     while (tmem_cols < bpad) tmem_cols *= 2;
 
@@ -391,6 +440,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.n_active = a.n_active;
     p.part = a.out;
     p.split_stride = a.plane_stride;
+    p.head_tri = reinterpret_cast<float4*>(a.head_tri);
+    p.tiles = tiles;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;

@@ -54,6 +54,10 @@ struct GemmArgs {
     int64_t plane_stride;
     int max_planes;
     int num_sms;
+    // Exit-head epilogue (tier 2 only): instead of logits, write per (row, 128-
+    // vocab tile) partials {max, sum exp(l - max), argmax} to head_tri[row *
+    // tiles + tile] (float4, argmax as int bits); decide merges them.
+    float* head_tri = nullptr;
 };
 // Tier 1: CUDA cores (any dtype, <= 64 rows).  Returns the planes written.
 int gemm_cc(const GemmArgs& a, cudaStream_t s);
@@ -88,6 +92,7 @@ struct AttnArgs {
     void* out;               // [maxB, dq] act dtype
     const void* k_map;       // bf16: TMA maps of this layer's K / V (128 B each), else null
     const void* v_map;
+    int num_sms;
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 
@@ -131,6 +136,8 @@ struct DecideArgs {
     RowState nxt;            // compaction target (introspective, non-final)
     int* gather_src;         // [maxB] nxt index -> cur index
     HeadOut head;
+    const float* head_tri = nullptr;  // optional: per-(row, tile) partials from the fused head GEMM (merged here)
+    int head_tiles = 0;
     StepOutDev out;
     int layers[64];          // exit ladder (profile mode maps head index -> layer)
 };
