@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
     constexpr int VEC = Vec16<T>::N;  // elements per 16 B
     pdl_launch_dependents();
     pdl_wait();
-    const int i = blockIdx.x;
+    const int i = blockIdx.y;
     if (i >= *a.n_active) return;
-    const int g = blockIdx.y;
+    const int g = blockIdx.x;
     const int H = a.n_heads, Hkv = a.n_kv_heads, hd = a.head_dim, G = H / Hkv;
     const int dq = H * hd, dkv = Hkv * hd, half = hd / 2;
     const int slot = a.slot[i], pos = a.pos[i];
@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     constexpr uint32_t kBlockBytes = CP * 128;     // one column block of a chunk
     pdl_launch_dependents();
     pdl_wait();
-    const int i = blockIdx.x;
+    const int i = blockIdx.y;
     if (i >= *a.n_active) return;
-    const int g = blockIdx.y;
+    const int g = blockIdx.x;
     const int H = a.n_heads, Hkv = a.n_kv_heads, G = H / Hkv;
     const int dq = H * HD, dkv = Hkv * HD, half = HD / 2;
     const int slot = a.slot[i], pos = a.pos[i];
@@ -357,10 +357,20 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
             *reinterpret_cast<float4*>(raw_s + 4 * v4) = acc;
         }
     }
+    // RoPE row and the KV-depth bytes of the positions, fetched in the same
+    // latency window as the planes (not as dependent global loads later).
+    __shared__ float cs[HD / 2], sn[HD / 2];
+    __shared__ uint8_t dep_s[CP];
+    for (int t = threadIdx.x; t < half; t += blockDim.x) {
+        cs[t] = a.rope_cos[(int64_t)pos * half + t];
+        sn[t] = a.rope_sin[(int64_t)pos * half + t];
+    }
+    {
+        const uint8_t* dsrc = a.kv_depth + (int64_t)slot * a.max_seq;
+        for (int t = threadIdx.x; t < CP && t <= pos; t += blockDim.x) dep_s[t] = dsrc[t];
+    }
     __syncthreads();
     // RoPE: queries (scaled) into q_s, the new key/value into the cache and kn_s / vn_s.
-    const float* cs = a.rope_cos + (int64_t)pos * half;
-    const float* sn = a.rope_sin + (int64_t)pos * half;
     const float qscale = rsqrtf((float)HD);
     for (int idx = threadIdx.x; idx < 8 * HD; idx += blockDim.x) {
         const int h = idx / HD, j = idx % HD;
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int p = c0 + t * 8 + kq + e;
-                const bool valid = h < G && p <= pos && (p == pos || depth[p] >= a.layer);
+                const bool valid = h < G && p <= pos && (p == pos || (c0 == 0 ? dep_s[p] : depth[p]) >= a.layer);
                 sc[tt][e] = valid ? c[e] : -INFINITY;
                 cmax = fmaxf(cmax, sc[tt][e]);
             }
@@ -937,7 +947,8 @@ void launch_mma(const AttnArgs& a, cudaStream_t s) {
     const size_t smem = 1024 + 2 * (size_t)CB * CP * 128 + (8 + G + 2) * HD * 4;
     auto kern = attention_mma_kernel<HD>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid(a.max_rows, a.n_kv_heads);
+    // x = kv head, y = row: the live rows' CTAs come first in launch order
+    dim3 grid(a.n_kv_heads, a.max_rows);
     launch_pdl(kern, grid, dim3(kMmaWarps * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a);
     EEB_CHECK_LAUNCH();
@@ -970,7 +981,8 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     const int npg = kThreads / (a.head_dim / 2);
     const size_t sc_floats = std::max((size_t)G * C, (size_t)npg * G * a.head_dim);
     const size_t smem = 2 * kChunkBytes + (size_t)G * a.head_dim * 4 + sc_floats * 4;
-    dim3 grid(a.max_rows, a.n_kv_heads);
+    // x = kv head, y = row: the live rows' CTAs come first in launch order
+    dim3 grid(a.n_kv_heads, a.max_rows);
     if (a.dtype == 0) {
         EEB_CUDA(cudaFuncSetAttribute(attention_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         launch_pdl(attention_kernel<float>, grid, dim3(kThreads), smem, s, a);
