@@ -116,6 +116,26 @@ eeb_status eeb_model_register(eeb_ctx* ctx, const eeb_model_desc* desc, int* mod
 eeb_status eeb_load_layers(eeb_ctx* ctx, int model, int to_depth);
 eeb_status eeb_evict(eeb_ctx* ctx, int model);   /* ↔ evict_model (memory_model.hpp:104) */
 eeb_status eeb_loaded_depth(eeb_ctx* ctx, int model, int* depth);
+
+/* Host tier ↔ the model held in CPU memory that HELIOS's greedy loader pulls
+ * layers from (engine.hpp:197-216; memory_model.hpp:76-105): layers [1, depth]
+ * plus the base weights (embedding, exit heads) packed into pinned host
+ * memory, one blob per layer.  Blocking. */
+eeb_status eeb_host_stage(eeb_ctx* ctx, int model, int depth);
+/* Asynchronous greedy load ↔ do_load (engine.hpp:197-216) with a real
+ * transfer instead of the modelled bytes / 8.4 GB/s: layers (loaded, to_depth]
+ * (and the base weights on the first load) are copied from the host tier by
+ * pinned cudaMemcpyAsync on the context's load stream, one event per layer.
+ * Returns immediately; decode steps that need only already-resident layers
+ * (flat at the old depth) run concurrently, a step that needs an in-flight
+ * layer waits on its event on the device (no host block).  to_depth <= loaded
+ * shrinks synchronously like eeb_load_layers.  EEB_E_CAPACITY if the host tier
+ * does not hold the layers. */
+eeb_status eeb_load_layers_async(eeb_ctx* ctx, int model, int to_depth);
+/* Block until the model's async load has landed; seconds = its measured
+ * duration on the load stream (CUDA events), bytes = bytes copied — the
+ * stall do_load charges to the next TTFT (engine.hpp:205-216). */
+eeb_status eeb_load_wait(eeb_ctx* ctx, int model, double* seconds, int64_t* bytes);
 eeb_status eeb_weight_bytes(eeb_ctx* ctx, int model, int depth, int64_t* bytes);
 
 /* Clear the KV of slots (positions marked as never computed). */
@@ -141,6 +161,22 @@ eeb_status eeb_decode_step_device(eeb_ctx* ctx, int model, int serving_depth, in
                                   const int32_t* d_input_tokens, const int32_t* d_positions,
                                   eeb_step_out* d_out);
 eeb_status eeb_synchronize(eeb_ctx* ctx);
+
+/* Prefill ↔ the prefill phase of Simulator::serve_one (engine.hpp:333-341:
+ * prompt_len x depth layer-token passes, charged to TTFT), batched.  The
+ * prompts of n_seq sequences — tokens concatenated in sequence order, lens[k]
+ * tokens for sequence k starting at position start_pos[k] of KV slot
+ * slot_ids[k] — run through layers 1..depth, writing their K/V at every
+ * layer <= depth and marking those positions computed to `depth` (deeper
+ * layers mask them, as for a token that exited at `depth`).  Chunked into
+ * passes of <= 256 tokens (one pass over the loaded layers per chunk; a later
+ * chunk attends to the KV of earlier ones).  No token is emitted: the first
+ * output token comes from the decode step, as in serve_one's token loop.
+ * start_pos > 0 re-prefills a suffix (after load-more / switch, SPEC re-prefill).
+ * Host pointers; the call returns when the KV is written.  SURVEY §8(b) sketch:
+ * eeb_prefill(ctx, model, depth, slot, prompt, len). */
+eeb_status eeb_prefill(eeb_ctx* ctx, int model, int depth, int32_t n_seq, const int32_t* slot_ids,
+                       const int32_t* start_pos, const int32_t* lens, const int32_t* tokens);
 
 /* Capture the step for (model, depth, policy, batch) into a CUDA graph and
  * reuse it on later identical calls (0 = off, 1 = on; default on). */

@@ -53,7 +53,7 @@ def _run(cmd: list[str]) -> None:
 
 def build_eeb(verbose: bool = False, extra_flags: list[str] | None = None) -> Path:
     OBJ.mkdir(exist_ok=True)
-    flags = NVCC_FLAGS + (extra_flags or [])
+    flags = NVCC_FLAGS + (extra_flags or []) + os.environ.get("EEB_NVCC_EXTRA", "").split()
     jobs = []
     objs = []
     for name in SOURCES:

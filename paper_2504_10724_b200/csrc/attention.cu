@@ -118,8 +118,10 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
         const float x0 = qkv(k0 + jj), x1 = qkv(k0 + jj + half);
         const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
         const T kt = from_f32<T>(kr), vt = from_f32<T>(qkv(v0 + j));
-        kc[(int64_t)pos * hd + j] = kt;
-        vc[(int64_t)pos * hd + j] = vt;
+        if (!a.kv_ready) {
+            kc[(int64_t)pos * hd + j] = kt;
+            vc[(int64_t)pos * hd + j] = vt;
+        }
         kn_s[j] = to_f32(kt);
         vn_s[j] = to_f32(vt);
     }
@@ -390,8 +392,10 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
         const float x0 = k[jj], x1 = k[jj + half];
         const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
         const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(vv[j]);
-        kc[(int64_t)pos * HD + j] = kt;
-        vc[(int64_t)pos * HD + j] = vt;
+        if (!a.kv_ready) {
+            kc[(int64_t)pos * HD + j] = kt;
+            vc[(int64_t)pos * HD + j] = vt;
+        }
         kn_s[j] = __bfloat162float(kt);
         vn_s[j] = __bfloat162float(vt);
     }
@@ -421,7 +425,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
             if (threadIdx.x == 0) issue(c0);
         }
         mbar_wait(bar_a, (uint32_t)(ci & 1));
-        if (pos < c0 + CP) {  // the new position lives in this chunk: write it (swizzled)
+        if (!a.kv_ready && pos < c0 + CP) {  // the new position lives in this chunk: write it (swizzled)
             const int r = pos - c0;
             for (int j = threadIdx.x; j < HD; j += blockDim.x) {
                 const uint32_t off = (j / 64) * kBlockBytes + swz(r, (j % 64) / 8) + (j % 8) * 2;
@@ -765,8 +769,10 @@ __global__ void __launch_bounds__(PipeCfg<HD>::NW * 32, 2)
             const float x0 = k[jj], x1 = k[jj + half];
             const float kr = j < half ? x0 * cos_s[jj] - x1 * sin_s[jj] : x0 * sin_s[jj] + x1 * cos_s[jj];
             const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(vv[j]);
-            kc[(int64_t)pos * HD + j] = kt;
-            vc[(int64_t)pos * HD + j] = vt;
+            if (!a.kv_ready) {
+                kc[(int64_t)pos * HD + j] = kt;
+                vc[(int64_t)pos * HD + j] = vt;
+            }
             kn_s[j] = __bfloat162float(kt);
             vn_s[j] = __bfloat162float(vt);
         }
@@ -793,7 +799,7 @@ __global__ void __launch_bounds__(PipeCfg<HD>::NW * 32, 2)
             if ((int)threadIdx.x < CP) dep_s[threadIdx.x] = dep_reg;
             load_dep();  // the following chunk's depth bytes
             mbar_wait(smem_u32(&bars[buf]), (seq / NBUF) & 1u);
-            if (pos < c0 + CP) {  // the new position lives in this chunk: patch it (swizzled)
+            if (!a.kv_ready && pos < c0 + CP) {  // the new position lives in this chunk: patch it (swizzled)
                 const int r = pos - c0;
                 for (int j = threadIdx.x; j < HD; j += blockDim.x) {
                     const uint32_t off = (j / 64) * kBlockBytes + swz(r, (j % 64) / 8) + (j % 8) * 2;
@@ -939,6 +945,42 @@ void launch_pipe(const AttnArgs& a, int num_sms, cudaStream_t s) {
     EEB_CHECK_LAUNCH();
 }
 
+template <typename T>
+__global__ void kv_append_kernel(AttnArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int i = blockIdx.x;
+    if (i >= *a.n_active) return;
+    const int Hkv = a.n_kv_heads, hd = a.head_dim, half = hd / 2;
+    const int dq = a.n_heads * hd, dkv = Hkv * hd;
+    const int slot = a.slot[i], pos = a.pos[i];
+    const int64_t row_off = (int64_t)i * (dq + 2 * dkv);
+    auto qkv = [&](int col) {  // same fixed-order plane sum as the attention kernels
+        float v = 0.f;
+        for (int sp = 0; sp < a.splits; ++sp) v += a.qkv[sp * a.split_stride + row_off + col];
+        return v;
+    };
+    const float* cs = a.rope_cos + (int64_t)pos * half;
+    const float* sn = a.rope_sin + (int64_t)pos * half;
+    for (int idx = threadIdx.x; idx < dkv; idx += blockDim.x) {
+        const int g = idx / hd, j = idx % hd;
+        const int jj = j < half ? j : j - half;
+        const float x0 = qkv(dq + g * hd + jj), x1 = qkv(dq + g * hd + jj + half);
+        const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
+        const int64_t off = (((int64_t)slot * Hkv + g) * a.max_seq + pos) * hd + j;
+        static_cast<T*>(a.k_cache)[off] = from_f32<T>(kr);
+        static_cast<T*>(a.v_cache)[off] = from_f32<T>(qkv(dq + dkv + g * hd + j));
+    }
+}
+
+__global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
+                                  uint8_t* kv_depth, int max_seq, int depth) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows) kv_depth[(int64_t)slot[i] * max_seq + pos[i]] = (uint8_t)depth;
+}
+
 template <int HD>
 void launch_mma(const AttnArgs& a, cudaStream_t s) {
     constexpr int CB = HD / 64, CP = HD == 64 ? 256 : 128;
@@ -955,6 +997,20 @@ void launch_mma(const AttnArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+void launch_kv_append(const AttnArgs& a, cudaStream_t s) {
+    if (a.dtype == 0)
+        launch_pdl(kv_append_kernel<float>, dim3(a.max_rows), dim3(256), 0, s, a);
+    else
+        launch_pdl(kv_append_kernel<__nv_bfloat16>, dim3(a.max_rows), dim3(256), 0, s, a);
+    EEB_CHECK_LAUNCH();
+}
+
+void launch_mark_depth(int rows, const int* slot, const int* pos, uint8_t* kv_depth, int max_seq, int depth,
+                       cudaStream_t s) {
+    launch_pdl(mark_depth_kernel, dim3((rows + 255) / 256), dim3(256), 0, s, rows, slot, pos, kv_depth, max_seq, depth);
+    EEB_CHECK_LAUNCH();
+}
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
     if (a.dtype == 1 && a.k_map && a.v_map && a.n_heads / a.n_kv_heads <= 8 &&

@@ -1,6 +1,8 @@
 // common.cuh — shared device/host helpers for the eeb kernels (sm_100a).
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -107,7 +109,23 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool no_pdl = std::getenv("EEB_NO_PDL") != nullptr;  // debugging: plain stream order
+    static const char* no_pdl_k = std::getenv("EEB_NO_PDL_K");          // ... for kernels named like these
+    bool off = no_pdl;
+    if (!off && no_pdl_k) {
+        const char* name = nullptr;
+        if (cudaFuncGetName(&name, reinterpret_cast<const void*>(kern)) == cudaSuccess && name) {
+            std::string list(no_pdl_k), nm(name);
+            size_t a = 0;
+            while (a <= list.size()) {
+                size_t b = list.find(',', a);
+                if (b == std::string::npos) b = list.size();
+                if (b > a && nm.find(list.substr(a, b - a)) != std::string::npos) off = true;
+                a = b + 1;
+            }
+        }
+    }
+    cfg.numAttrs = off ? 0 : 1;
     EEB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 

@@ -49,12 +49,53 @@ struct DevBuf {
         release();
         EEB_CUDA(cudaMalloc(&p, n));
         bytes = n;
+        // debugging aid: fill fresh allocations with NaN-ish bytes so reads of
+        // never-written memory show up deterministically
+        static const bool poison = std::getenv("EEB_DEBUG_POISON") != nullptr;
+        if (poison) EEB_CUDA(cudaMemset(p, 0xFF, n));
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
 struct LayerWeights {
     DevBuf attn_norm, mlp_norm, wqkv, wo, wup, wdown;
+    DevBuf* parts[6] = {&attn_norm, &mlp_norm, &wqkv, &wo, &wup, &wdown};
+};
+
+// Pinned host memory (the host tier the greedy loader copies from).
+struct HostBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void alloc(size_t n) {
+        EEB_CUDA(cudaMallocHost(&p, n));
+        bytes = n;
+    }
+};
+
+// One layer (or the base weights) as a packed pinned blob: part k at off[k].
+struct HostBlob {
+    HostBuf buf;
+    std::vector<size_t> off, sz;
+};
+
+// A model's weights in host memory ↔ the "model in CPU memory" that HELIOS's
+// greedy loader pulls layers from (engine.hpp:197-216, memory_model.hpp:76-105).
+struct HostTier {
+    std::unique_ptr<HostBlob> base;                  // embedding, exit heads, head norms
+    std::vector<std::unique_ptr<HostBlob>> layers;   // index l-1
+};
+
+// An asynchronous load in flight on the context's load stream.
+struct PendingLoad {
+    cudaEvent_t t0 = nullptr, t1 = nullptr;          // timing (load stream)
+    std::vector<std::pair<int, cudaEvent_t>> ready;  // (layer, event); layer 0 = base weights
+    int64_t bytes = 0;
 };
 
 struct Model {
@@ -73,6 +114,11 @@ struct Model {
     DevBuf k_cache, v_cache, kv_depth, rope_cos, rope_sin;
     size_t kv_layer_elems = 0;
     std::vector<std::array<uint8_t, 128>> k_maps, v_maps;  // bf16: per-layer TMA maps of the KV cache
+    // host tier + asynchronous loader state
+    HostTier host;
+    std::unique_ptr<PendingLoad> pending;
+    double last_load_s = 0.0;
+    int64_t last_load_bytes = 0;
 };
 
 struct GraphKey {
@@ -103,6 +149,7 @@ struct eeb_ctx {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t load_stream = nullptr;  // greedy loader: pinned H2D copies, overlapped with decode
     std::vector<std::unique_ptr<eeb::Model>> models;
     int graphs_enabled = 1;
     int gemm_tier = 0;
@@ -112,6 +159,9 @@ struct eeb_ctx {
     eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
     eeb::DevBuf head_tok, head_conf, head_logp, head_tri;
+    eeb::DevBuf pf_meta;            // prefill (tok, slot, pos) of every prompt token
+    void* pf_pin = nullptr;
+    size_t pf_pin_bytes = 0;
     eeb::DevBuf o_exit, o_tok, o_conf, o_logp, o_breach, o_unch, o_bin, o_hist, o_nbr, o_sum;
     eeb::DevBuf o_htok, o_hconf, o_hlogp;
     std::vector<std::unique_ptr<eeb::DevBuf>> logits_keep;
@@ -245,15 +295,81 @@ void validate_desc(const eeb_model_desc& d) {
 // Loader ↔ do_load / apply_load: materialise layers [loaded+1, to] (and the
 // base weights on the first load); free layers deeper than `to` on shrink.
 // ---------------------------------------------------------------------------
+// Base weights (embedding, exit heads + their norms) materialised on device.
+void synth_base(Model& m, cudaStream_t s) {
+    const eeb_model_desc& d = m.desc;
+    const int D = d.d_model;
+    m.emb.ensure((size_t)d.vocab * D * m.wbytes);
+    synth_embedding(d.dtype, m.emb.p, d.seed, d.vocab, D, s);
+    m.head.clear();
+    m.head_norm.clear();
+    for (int e = 0; e < d.n_exits; ++e) {
+        auto h = std::make_unique<DevBuf>();
+        h->ensure((size_t)d.vocab * D * m.wbytes);
+        synth_head(d.dtype, h->p, d.seed, e, m.alphas[e], d.vocab, D, s);
+        auto g = std::make_unique<DevBuf>();
+        g->ensure((size_t)D * sizeof(float));
+        synth_norm(g->p, d.seed, synth::base_tid(synth::kHeadNorm, e), D, s);
+        m.head.push_back(std::move(h));
+        m.head_norm.push_back(std::move(g));
+    }
+}
+
+// Device buffers of layer l, sized but not filled.
+std::unique_ptr<LayerWeights> alloc_layer(const Model& m) {
+    const int D = m.desc.d_model, F = m.desc.d_ffn;
+    auto L = std::make_unique<LayerWeights>();
+    L->attn_norm.ensure((size_t)D * 4);
+    L->mlp_norm.ensure((size_t)D * 4);
+    L->wqkv.ensure((size_t)(m.dq + 2 * m.dkv) * D * m.wbytes);
+    L->wo.ensure((size_t)D * m.dq * m.wbytes);
+    L->wup.ensure((size_t)m.up_rows * D * m.wbytes);
+    L->wdown.ensure((size_t)D * F * m.wbytes);
+    return L;
+}
+
+// Layer l (1-based) materialised on device from the model seed.
+std::unique_ptr<LayerWeights> synth_layer(const Model& m, int l, cudaStream_t s) {
+    const eeb_model_desc& d = m.desc;
+    const uint64_t seed = d.seed;
+    const int D = d.d_model, F = d.d_ffn;
+    const float rsig = synth::residual_sigma(D, F);
+    auto L = alloc_layer(m);
+    synth_norm(L->attn_norm.p, seed, synth::layer_tid(l, synth::kAttnNorm), D, s);
+    synth_norm(L->mlp_norm.p, seed, synth::layer_tid(l, synth::kMlpNorm), D, s);
+    const int qkv_rows = m.dq + 2 * m.dkv;
+    synth_linear(d.dtype, L->wqkv.p, seed, synth::layer_tid(l, synth::kWqkv), qkv_rows, D, synth::kSigma, false, D,
+                 s);
+    synth_linear(d.dtype, L->wo.p, seed, synth::layer_tid(l, synth::kWo), D, m.dq, rsig, true, D, s);
+    synth_linear(d.dtype, L->wup.p, seed, synth::layer_tid(l, synth::kWup), m.up_rows, D, synth::kSigma, false, D,
+                 s);
+    synth_linear(d.dtype, L->wdown.p, seed, synth::layer_tid(l, synth::kWdown), D, F, rsig, true, D, s);
+    return L;
+}
+
+// Host side of every pending asynchronous load has to be settled before the
+// synchronous loader frees or replaces buffers the copies target.
+void settle_pending(Model& m) {
+    if (!m.pending) return;
+    EEB_CUDA(cudaEventSynchronize(m.pending->t1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, m.pending->t0, m.pending->t1);
+    m.last_load_s = ms / 1000.0;
+    m.last_load_bytes = m.pending->bytes;
+    cudaEventDestroy(m.pending->t0);
+    cudaEventDestroy(m.pending->t1);
+    for (auto& [l, ev] : m.pending->ready) cudaEventDestroy(ev);
+    m.pending.reset();
+}
+
 void load_to(eeb_ctx* c, Model& m, int to) {
     const eeb_model_desc& d = m.desc;
     c->mk_progs.clear();  // compiled persistent programs hold weight pointers
     if (to < 0 || to > d.num_layers)
         throw Error(EEB_E_DOMAIN, "load: depth " + std::to_string(to) + " outside [0, " +
                                       std::to_string(d.num_layers) + "]");
+    settle_pending(m);
     cudaStream_t s = c->stream;
-    const uint64_t seed = d.seed;
-    const int D = d.d_model, F = d.d_ffn;
     if (to == 0) {
         m.layers.clear();
         m.head.clear();
@@ -262,47 +378,143 @@ void load_to(eeb_ctx* c, Model& m, int to) {
         m.loaded = 0;
         return;
     }
-    if (m.loaded == 0) {
-        m.emb.ensure((size_t)d.vocab * D * m.wbytes);
-        synth_embedding(d.dtype, m.emb.p, seed, d.vocab, D, s);
-        m.head.clear();
-        m.head_norm.clear();
-        for (int e = 0; e < d.n_exits; ++e) {
-            auto h = std::make_unique<DevBuf>();
-            h->ensure((size_t)d.vocab * D * m.wbytes);
-            synth_head(d.dtype, h->p, seed, e, m.alphas[e], d.vocab, D, s);
-            auto g = std::make_unique<DevBuf>();
-            g->ensure((size_t)D * sizeof(float));
-            synth_norm(g->p, seed, synth::base_tid(synth::kHeadNorm, e), D, s);
-            m.head.push_back(std::move(h));
-            m.head_norm.push_back(std::move(g));
-        }
-    }
-    const float rsig = synth::residual_sigma(D, F);
-    while ((int)m.layers.size() < to) {
-        const int l = (int)m.layers.size() + 1;
-        auto L = std::make_unique<LayerWeights>();
-        L->attn_norm.ensure((size_t)D * 4);
-        L->mlp_norm.ensure((size_t)D * 4);
-        synth_norm(L->attn_norm.p, seed, synth::layer_tid(l, synth::kAttnNorm), D, s);
-        synth_norm(L->mlp_norm.p, seed, synth::layer_tid(l, synth::kMlpNorm), D, s);
-        const int qkv_rows = m.dq + 2 * m.dkv;
-        L->wqkv.ensure((size_t)qkv_rows * D * m.wbytes);
-        synth_linear(d.dtype, L->wqkv.p, seed, synth::layer_tid(l, synth::kWqkv), qkv_rows, D,
-                     synth::kSigma, false, D, s);
-        L->wo.ensure((size_t)D * m.dq * m.wbytes);
-        synth_linear(d.dtype, L->wo.p, seed, synth::layer_tid(l, synth::kWo), D, m.dq, rsig, true, D, s);
-        L->wup.ensure((size_t)m.up_rows * D * m.wbytes);
-        synth_linear(d.dtype, L->wup.p, seed, synth::layer_tid(l, synth::kWup), m.up_rows, D,
-                     synth::kSigma, false, D, s);
-        L->wdown.ensure((size_t)D * F * m.wbytes);
-        synth_linear(d.dtype, L->wdown.p, seed, synth::layer_tid(l, synth::kWdown), D, F, rsig, true,
-                     D, s);
-        m.layers.push_back(std::move(L));
-    }
+    if (m.loaded == 0) synth_base(m, s);
+    while ((int)m.layers.size() < to) m.layers.push_back(synth_layer(m, (int)m.layers.size() + 1, s));
     while ((int)m.layers.size() > to) m.layers.pop_back();
     m.loaded = to;
     EEB_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---- host tier + asynchronous greedy loader --------------------------------
+// Copy device buffers into a packed pinned blob (stream-ordered on s).
+std::unique_ptr<HostBlob> stage_blob(const std::vector<const DevBuf*>& parts, cudaStream_t s) {
+    auto b = std::make_unique<HostBlob>();
+    size_t total = 0;
+    for (auto* p : parts) {
+        b->off.push_back(total);
+        b->sz.push_back(p->bytes);
+        total += (p->bytes + 255) & ~(size_t)255;
+    }
+    b->buf.alloc(std::max<size_t>(total, 256));
+    for (size_t k = 0; k < parts.size(); ++k)
+        EEB_CUDA(cudaMemcpyAsync(static_cast<char*>(b->buf.p) + b->off[k], parts[k]->p, b->sz[k],
+                                 cudaMemcpyDeviceToHost, s));
+    return b;
+}
+
+std::vector<const DevBuf*> base_parts(const Model& m) {
+    std::vector<const DevBuf*> v{&m.emb};
+    for (auto& h : m.head) v.push_back(h.get());
+    for (auto& g : m.head_norm) v.push_back(g.get());
+    return v;
+}
+
+void host_stage(eeb_ctx* c, Model& m, int depth) {
+    const eeb_model_desc& d = m.desc;
+    if (depth < 0 || depth > d.num_layers) throw Error(EEB_E_DOMAIN, "host stage: depth outside [0, num_layers]");
+    settle_pending(m);
+    cudaStream_t s = c->stream;
+    if (!m.host.base) {
+        if (m.loaded > 0) {
+            m.host.base = stage_blob(base_parts(m), s);
+        } else {
+            Model tmp;  // materialise on device only long enough to copy out
+            tmp.desc = d;
+            tmp.alphas = m.alphas;
+            tmp.wbytes = m.wbytes;
+            synth_base(tmp, s);
+            m.host.base = stage_blob(base_parts(tmp), s);
+            EEB_CUDA(cudaStreamSynchronize(s));
+        }
+    }
+    while ((int)m.host.layers.size() < depth) {
+        const int l = (int)m.host.layers.size() + 1;
+        if (l <= (int)m.layers.size()) {
+            const LayerWeights& L = *m.layers[l - 1];
+            m.host.layers.push_back(stage_blob({L.parts, L.parts + 6}, s));
+        } else {
+            auto L = synth_layer(m, l, s);
+            m.host.layers.push_back(stage_blob({L->parts, L->parts + 6}, s));
+            EEB_CUDA(cudaStreamSynchronize(s));  // before the temporary layer is freed
+        }
+    }
+    EEB_CUDA(cudaStreamSynchronize(s));
+}
+
+// Grow the resident prefix to `to` by pinned H2D copies on the load stream;
+// returns immediately.  Steps that need a layer wait on its event.
+void load_async(eeb_ctx* c, Model& m, int to) {
+    const eeb_model_desc& d = m.desc;
+    if (to < 0 || to > d.num_layers) throw Error(EEB_E_DOMAIN, "load: depth outside [0, num_layers]");
+    if (to <= m.loaded) {
+        load_to(c, m, to);  // shrink / no-op: synchronous free
+        return;
+    }
+    if ((int)m.host.layers.size() < to || !m.host.base)
+        throw Error(EEB_E_CAPACITY, "host tier holds " + std::to_string(m.host.layers.size()) +
+                                        " layers; stage them first (eeb_host_stage)");
+    settle_pending(m);
+    c->mk_progs.clear();
+    cudaStream_t ls = c->load_stream;
+    auto P = std::make_unique<PendingLoad>();
+    EEB_CUDA(cudaEventCreate(&P->t0));
+    EEB_CUDA(cudaEventCreate(&P->t1));
+    // the copies must not overtake work already queued on the decode stream
+    // that still reads buffers being replaced (none are: growth only adds)
+    EEB_CUDA(cudaEventRecord(P->t0, ls));
+    auto copy_in = [&](DevBuf& dst, const HostBlob& b, size_t k) {
+        EEB_CUDA(cudaMemcpyAsync(dst.p, static_cast<const char*>(b.buf.p) + b.off[k], b.sz[k], cudaMemcpyHostToDevice,
+                                 ls));
+        P->bytes += (int64_t)b.sz[k];
+    };
+    auto mark = [&](int layer) {
+        cudaEvent_t ev;
+        EEB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        EEB_CUDA(cudaEventRecord(ev, ls));
+        P->ready.push_back({layer, ev});
+    };
+    if (m.loaded == 0) {
+        const HostBlob& b = *m.host.base;
+        m.emb.ensure(b.sz[0]);
+        m.head.clear();
+        m.head_norm.clear();
+        for (int e = 0; e < d.n_exits; ++e) {
+            m.head.push_back(std::make_unique<DevBuf>());
+            m.head.back()->ensure(b.sz[1 + e]);
+            m.head_norm.push_back(std::make_unique<DevBuf>());
+            m.head_norm.back()->ensure(b.sz[1 + d.n_exits + e]);
+        }
+        copy_in(m.emb, b, 0);
+        for (int e = 0; e < d.n_exits; ++e) {
+            copy_in(*m.head[e], b, 1 + e);
+            copy_in(*m.head_norm[e], b, 1 + d.n_exits + e);
+        }
+        mark(0);
+    }
+    while ((int)m.layers.size() < to) {
+        const int l = (int)m.layers.size() + 1;
+        auto L = alloc_layer(m);
+        const HostBlob& b = *m.host.layers[l - 1];
+        for (int k = 0; k < 6; ++k) copy_in(*L->parts[k], b, k);
+        mark(l);
+        m.layers.push_back(std::move(L));
+    }
+    EEB_CUDA(cudaEventRecord(P->t1, ls));
+    m.loaded = to;
+    m.pending = std::move(P);
+}
+
+// Make the decode stream wait for the layers a step needs (1..need, and the
+// base weights) if they are still in flight.  Issued outside graph capture.
+void wait_layers(eeb_ctx* c, Model& m, int need) {
+    if (!m.pending) return;
+    bool all_done = cudaEventQuery(m.pending->t1) == cudaSuccess;
+    if (all_done) {
+        settle_pending(m);
+        return;
+    }
+    for (auto& [l, ev] : m.pending->ready)
+        if (l <= need) EEB_CUDA(cudaStreamWaitEvent(c->stream, ev, 0));
 }
 
 int64_t weight_bytes_at(const Model& m, int depth) {
@@ -691,6 +903,100 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
     }
 }
 
+// ---------------------------------------------------------------------------
+// Prefill chunk: `rows` prompt tokens (I.tok / I.slot / I.pos) through layers
+// 1..depth, no exit heads.  Same layer body as the decode step, except that
+// every row's K/V is appended before the attention (rows of one sequence in
+// the chunk attend to each other) and the positions are marked computed to
+// `depth` up front.
+// ---------------------------------------------------------------------------
+constexpr int kPolicyPrefill = 100;  // graph-cache key
+
+void enqueue_prefill(eeb_ctx* c, int mi, int depth, int rows) {
+    Model& m = model_of(c, mi);
+    const eeb_model_desc& d = m.desc;
+    const int D = d.d_model, F = d.d_ffn;
+    cudaStream_t s = c->stream;
+    Ints I = ints_of(c);
+    RowState cur{I.nA, I.rowA, I.slotA, I.posA, c->xA.as<float>()};
+    void* h = c->hn.p;
+    float* ws = c->ws.as<float>();
+    launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, rows, D, cur, s);
+    launch_mark_depth(rows, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len, depth, s);
+    launch_residual_norm(d.dtype, nullptr, 0, 0, cur.n_active, rows, cur.x, D, d.norm_eps,
+                         m.layers[0]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+    count(c, kCatOther, 3);
+    const int qkv_n = m.dq + 2 * m.dkv;
+    for (int l = 1; l <= depth; ++l) {
+        const LayerWeights& W = *m.layers[l - 1];
+        int planes = gemm(c, kCatGemm, m, W.wqkv.p, h, qkv_n, D, cur.n_active, rows);
+        AttnArgs a;
+        a.dtype = d.dtype;
+        a.qkv = ws;
+        a.splits = planes;
+        a.split_stride = (int64_t)rows * qkv_n;
+        a.k_cache = static_cast<char*>(m.k_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * m.wbytes;
+        a.v_cache = static_cast<char*>(m.v_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * m.wbytes;
+        a.kv_depth = m.kv_depth.as<uint8_t>();
+        a.rope_cos = m.rope_cos.as<float>();
+        a.rope_sin = m.rope_sin.as<float>();
+        a.n_active = cur.n_active;
+        a.slot = cur.slot;
+        a.pos = cur.pos;
+        a.max_rows = rows;
+        a.layer = l;
+        a.n_heads = d.n_heads;
+        a.n_kv_heads = d.n_kv_heads;
+        a.head_dim = m.head_dim;
+        a.max_seq = d.max_seq_len;
+        a.out = c->attn.p;
+        a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[l - 1].data();
+        a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[l - 1].data();
+        a.num_sms = c->num_sms;
+        a.kv_ready = 1;
+        launch_kv_append(a, s);
+        launch_attention(a, s);
+        count(c, kCatAttn, 2);
+        planes = gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, cur.n_active, rows);
+        launch_residual_norm(d.dtype, ws, planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D, d.norm_eps,
+                             W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
+        planes = gemm(c, kCatGemm, m, W.wup.p, h, m.up_rows, D, cur.n_active, rows);
+        launch_act(d.dtype, ws, planes, (int64_t)rows * m.up_rows, cur.n_active, rows, m.up_rows,
+                   d.mlp_kind == EEB_MLP_SWIGLU, c->mlp_h.p, c->num_sms, s);
+        planes = gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, cur.n_active, rows);
+        if (l < depth)  // the next layer's attention norm (the last layer's residual is not needed)
+            launch_residual_norm(d.dtype, ws, planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D, d.norm_eps,
+                                 m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+        count(c, kCatNorm, l < depth ? 3 : 2);
+    }
+}
+
+void run_prefill_chunk(eeb_ctx* c, int mi, int depth, int rows) {
+    const bool use_graph = c->graphs_enabled && !c->profiling;
+    if (!use_graph) {
+        enqueue_prefill(c, mi, depth, rows);
+        return;
+    }
+    GraphKey key{mi, depth, kPolicyPrefill, rows, c->gemm_tier, 0u};
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        cudaGraph_t g;
+        EEB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_prefill(c, mi, depth, rows);
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &g);
+            throw;
+        }
+        EEB_CUDA(cudaStreamEndCapture(c->stream, &g));
+        cudaGraphExec_t ex;
+        EEB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        cudaGraphDestroy(g);
+        it = c->graphs.emplace(key, ex).first;
+    }
+    EEB_CUDA(cudaGraphLaunch(it->second, c->stream));
+}
+
 void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int batch) {
     const eeb_model_desc& d = m.desc;
     if (batch <= 0 || batch > d.max_slots)
@@ -1066,6 +1372,7 @@ eeb_status eeb_create(int device, eeb_ctx** out) {
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
         EEB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        EEB_CUDA(cudaStreamCreateWithFlags(&c->load_stream, cudaStreamNonBlocking));
         *out = c.release();
     });
 }
@@ -1078,8 +1385,16 @@ void eeb_destroy(eeb_ctx* c) {
     for (auto ev : c->ev_pool) cudaEventDestroy(ev);
     if (c->nccl) nccl().comm_destroy(c->nccl);
     if (c->pin) cudaFreeHost(c->pin);
+    if (c->pf_pin) cudaFreeHost(c->pf_pin);
+    for (auto& m : c->models) {
+        if (m && m->pending) {
+            cudaEventSynchronize(m->pending->t1);
+            eeb::settle_pending(*m);
+        }
+    }
     c->models.clear();
     cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->load_stream);
     delete c;
 }
 
@@ -1161,6 +1476,40 @@ eeb_status eeb_load_layers(eeb_ctx* c, int model, int to_depth) {
 
 eeb_status eeb_evict(eeb_ctx* c, int model) { return eeb_load_layers(c, model, 0); }
 
+eeb_status eeb_host_stage(eeb_ctx* c, int model, int depth) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        EEB_CUDA(cudaSetDevice(c->device));
+        host_stage(c, m, depth);
+    });
+}
+
+eeb_status eeb_load_layers_async(eeb_ctx* c, int model, int to_depth) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        EEB_CUDA(cudaSetDevice(c->device));
+        for (auto it = c->graphs.begin(); it != c->graphs.end();) {
+            if (it->first.model == model) {
+                cudaGraphExecDestroy(it->second);
+                it = c->graphs.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        load_async(c, m, to_depth);
+    });
+}
+
+eeb_status eeb_load_wait(eeb_ctx* c, int model, double* seconds, int64_t* bytes) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        EEB_CUDA(cudaSetDevice(c->device));
+        settle_pending(m);
+        if (seconds) *seconds = m.last_load_s;
+        if (bytes) *bytes = m.last_load_bytes;
+    });
+}
+
 eeb_status eeb_loaded_depth(eeb_ctx* c, int model, int* depth) {
     return guarded([&] {
         if (!depth) throw Error(EEB_E_DOMAIN, "null output");
@@ -1210,6 +1559,7 @@ eeb_status eeb_decode_step(eeb_ctx* c, int model, int depth, int policy, float t
         validate_rows_host(m, batch, slot_ids, input_tokens, positions);
         EEB_CUDA(cudaSetDevice(c->device));
         ensure_workspace(c, m, batch);
+        wait_layers(c, m, policy == EEB_FLAT ? depth : m.desc.num_layers);
         Ints I = ints_of(c);
         cudaStream_t s = c->stream;
         // inputs: pinned staging → device
@@ -1268,6 +1618,7 @@ eeb_status eeb_decode_step_device(eeb_ctx* c, int model, int depth, int policy, 
         check_step_args(c, m, depth, policy, th, batch);
         EEB_CUDA(cudaSetDevice(c->device));
         ensure_workspace(c, m, batch);
+        wait_layers(c, m, policy == EEB_FLAT ? depth : m.desc.num_layers);
         Ints I = ints_of(c);
         cudaStream_t s = c->stream;
         EEB_CUDA(cudaMemcpyAsync(I.tok, d_tok, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
@@ -1295,6 +1646,69 @@ eeb_status eeb_decode_step_device(eeb_ctx* c, int model, int depth, int policy, 
             }
         }
         if (c->profiling) harvest_profile(c);
+    });
+}
+
+eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const int32_t* slot_ids,
+                       const int32_t* start_pos, const int32_t* lens, const int32_t* tokens) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const eeb_model_desc& d = m.desc;
+        if (n_seq <= 0) throw Error(EEB_E_DOMAIN, "n_seq must be positive");
+        if (!slot_ids || !start_pos || !lens || !tokens) throw Error(EEB_E_DOMAIN, "null input array");
+        if (depth <= 0 || depth > d.num_layers)
+            throw Error(EEB_E_DOMAIN, "prefill depth " + std::to_string(depth) + " outside [1, num_layers]");
+        if (m.loaded < depth)
+            throw Error(EEB_E_CAPACITY, "layers up to " + std::to_string(depth) + " are not resident (loaded " +
+                                            std::to_string(m.loaded) + ")");
+        int64_t total = 0;
+        for (int k = 0; k < n_seq; ++k) {
+            if (slot_ids[k] < 0 || slot_ids[k] >= d.max_slots) throw Error(EEB_E_DOMAIN, "slot id out of range");
+            if (lens[k] < 0 || start_pos[k] < 0 || (int64_t)start_pos[k] + lens[k] > d.max_seq_len)
+                throw Error(EEB_E_DOMAIN, "prompt exceeds max_seq_len");
+            for (int j = 0; j < k; ++j)
+                if (slot_ids[j] == slot_ids[k]) throw Error(EEB_E_VALIDATION, "duplicate slot id in one prefill");
+            total += lens[k];
+        }
+        for (int64_t t = 0; t < total; ++t)
+            if (tokens[t] < 0 || tokens[t] >= d.vocab) throw Error(EEB_E_DOMAIN, "token id out of range");
+        if (total == 0) return;
+        EEB_CUDA(cudaSetDevice(c->device));
+        wait_layers(c, m, depth);
+        const int chunk = d.dtype == EEB_BF16 ? 256 : 64;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
+        ensure_workspace(c, m, (int)std::min<int64_t>(chunk, total));
+        // (tok, slot, pos) of every prompt token: one pinned staging + one H2D,
+        // then a device-to-device slice per chunk.
+        const size_t meta = (size_t)total * 3 * 4;
+        if (meta > c->pf_pin_bytes) {
+            if (c->pf_pin) cudaFreeHost(c->pf_pin);
+            c->pf_pin = nullptr;
+            EEB_CUDA(cudaMallocHost(&c->pf_pin, meta));
+            c->pf_pin_bytes = meta;
+        }
+        int32_t* ht = static_cast<int32_t*>(c->pf_pin);
+        int32_t* hs = ht + total;
+        int32_t* hp = hs + total;
+        int64_t t = 0;
+        for (int k = 0; k < n_seq; ++k)
+            for (int j = 0; j < lens[k]; ++j, ++t) {
+                ht[t] = tokens[t];
+                hs[t] = slot_ids[k];
+                hp[t] = start_pos[k] + j;
+            }
+        c->pf_meta.ensure(meta);
+        int32_t* dm = c->pf_meta.as<int32_t>();
+        cudaStream_t s = c->stream;
+        EEB_CUDA(cudaMemcpyAsync(dm, ht, meta, cudaMemcpyHostToDevice, s));
+        Ints I = ints_of(c);
+        for (int64_t c0 = 0; c0 < total; c0 += chunk) {
+            const int rows = (int)std::min<int64_t>(chunk, total - c0);
+            EEB_CUDA(cudaMemcpyAsync(I.tok, dm + c0, (size_t)rows * 4, cudaMemcpyDeviceToDevice, s));
+            EEB_CUDA(cudaMemcpyAsync(I.slot, dm + total + c0, (size_t)rows * 4, cudaMemcpyDeviceToDevice, s));
+            EEB_CUDA(cudaMemcpyAsync(I.pos, dm + 2 * total + c0, (size_t)rows * 4, cudaMemcpyDeviceToDevice, s));
+            run_prefill_chunk(c, model, depth, rows);
+        }
+        EEB_CUDA(cudaStreamSynchronize(s));
     });
 }
 

@@ -24,8 +24,8 @@ constexpr int kReduceThreads = 1024;
 
 // Per-row max / argmax / sum-exp over the vocabulary.
 __global__ void __launch_bounds__(kReduceThreads)
-    head_reduce_kernel(const float* __restrict__ part, int splits, int64_t split_stride, int vocab,
-                       const int* __restrict__ n_active, HeadOut h, float* __restrict__ logits_out) {
+    head_reduce_kernel(const float* part, int splits, int64_t split_stride, int vocab,
+                       const int* n_active, HeadOut h, float* logits_out) {
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x;
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
 // K4 + bookkeeping: shared-memory atomic histogram of exit-head bins, breach
 // count, fixed-order f64 logprob sum, KV depth map update.
 __global__ void __launch_bounds__(1024)
-    finalize_kernel(int batch, int n_exits, StepOutDev o, const int* __restrict__ slot_in,
-                    const int* __restrict__ pos_in, uint8_t* __restrict__ kv_depth, int max_seq,
+    finalize_kernel(int batch, int n_exits, StepOutDev o, const int* slot_in,
+                    const int* pos_in, uint8_t* kv_depth, int max_seq,
                     int computed_depth) {
     pdl_launch_dependents();
     pdl_wait();

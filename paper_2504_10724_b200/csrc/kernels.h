@@ -93,8 +93,15 @@ struct AttnArgs {
     const void* k_map;       // bf16: TMA maps of this layer's K / V (128 B each), else null
     const void* v_map;
     int num_sms;
+    int kv_ready = 0;        // prefill: every row's K/V is already in the cache (launch_kv_append)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+// Prefill: RoPE the keys and write K/V of every live row into the cache
+// (a chunk's rows attend to each other, so the append precedes the attention).
+void launch_kv_append(const AttnArgs& a, cudaStream_t s);
+// Prefill: kv_depth[slot[i]][pos[i]] = depth for the rows of the chunk.
+void launch_mark_depth(int rows, const int* slot, const int* pos, uint8_t* kv_depth, int max_seq, int depth,
+                       cudaStream_t s);
 
 // ---- exit head, decisions, compaction, histogram (exit_head.cu) ------------
 struct HeadOut {             // result of one head on the live rows (compact-indexed)

@@ -43,10 +43,10 @@ constexpr int kClusterRow = 8;
 
 template <typename T>
 __global__ void __cluster_dims__(kClusterRow, 1, 1) __launch_bounds__(kRowThreads)
-    residual_norm_kernel(const float* __restrict__ part, int splits, int64_t split_stride,
-                         const int* __restrict__ n_active, float* __restrict__ x, int d, float eps,
-                         const float* __restrict__ g1, T* __restrict__ out1, const float* __restrict__ g2,
-                         T* __restrict__ out2) {
+    residual_norm_kernel(const float* part, int splits, int64_t split_stride,
+                         const int* n_active, float* x, int d, float eps,
+                         const float* g1, T* out1, const float* g2,
+                         T* out2) {
     pdl_launch_dependents();
     pdl_wait();
     cg::cluster_group cluster = cg::this_cluster();
@@ -99,8 +99,8 @@ __global__ void __cluster_dims__(kClusterRow, 1, 1) __launch_bounds__(kRowThread
 }
 
 template <typename T>
-__global__ void act_kernel(const float* __restrict__ part, int splits, int64_t split_stride,
-                           const int* __restrict__ n_active, int N, int swiglu, T* __restrict__ out) {
+__global__ void act_kernel(const float* part, int splits, int64_t split_stride,
+                           const int* n_active, int N, int swiglu, T* out) {
     pdl_launch_dependents();
     pdl_wait();
     const int n_out = swiglu ? N / 2 : N;
@@ -125,8 +125,8 @@ __global__ void act_kernel(const float* __restrict__ part, int splits, int64_t s
 }
 
 template <typename T>
-__global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ tok,
-                             const int* __restrict__ slot_in, const int* __restrict__ pos_in, int batch, int d,
+__global__ void embed_kernel(const T* __restrict__ emb, const int* tok,
+                             const int* slot_in, const int* pos_in, int batch, int d,
                              RowState st) {
     pdl_launch_dependents();
     pdl_wait();
@@ -143,9 +143,9 @@ __global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ 
     for (int c = threadIdx.x; c < d; c += blockDim.x) dst[c] = to_f32(src[c]);
 }
 
-__global__ void gather_rows_kernel(const float* __restrict__ x_cur, float* __restrict__ x_nxt,
-                                   const uint16_t* __restrict__ h_cur, uint16_t* __restrict__ h_nxt, int h_words,
-                                   const int* __restrict__ src, const int* __restrict__ n_active, int d) {
+__global__ void gather_rows_kernel(const float* x_cur, float* x_nxt,
+                                   const uint16_t* h_cur, uint16_t* h_nxt, int h_words,
+                                   const int* src, const int* n_active, int d) {
     pdl_launch_dependents();
     pdl_wait();
     const int j = blockIdx.x;

@@ -23,7 +23,7 @@ struct FillArgs {
 };
 
 template <typename T>
-__global__ void fill_kernel(T* __restrict__ dst, FillArgs a) {
+__global__ void fill_kernel(T* dst, FillArgs a) {
     const int64_t n = (int64_t)a.rows * a.cols;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
          idx += (int64_t)gridDim.x * blockDim.x) {

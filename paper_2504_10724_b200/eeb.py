@@ -12,12 +12,13 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import os
 from pathlib import Path
 
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libeeb.so"
+LIB_PATH = _PKG / os.environ.get("EEB_LIB", "libeeb.so")
 
 FLAT, INTROSPECTIVE, FULL_DEPTH, PROFILE = 0, 1, 2, 3
 F32, BF16 = 0, 1
@@ -65,6 +66,7 @@ EXPORTED = [
     "eeb_set_gemm_tier", "eeb_debug_last_logits", "eeb_debug_retain_logits", "eeb_debug_read_weight",
     "eeb_debug_read_kv", "eeb_profile_enable", "eeb_profile_read", "eeb_stream",
     "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm", "eeb_debug_bench_layers",
+    "eeb_prefill", "eeb_host_stage", "eeb_load_layers_async", "eeb_load_wait",
 ]
 
 _lib = None
@@ -93,6 +95,11 @@ def load_library() -> C.CDLL:
         lib.eeb_decode_step.argtypes = step_args
         lib.eeb_decode_step_device.argtypes = step_args
         lib.eeb_synchronize.argtypes = [C.c_void_p]
+        lib.eeb_host_stage.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        lib.eeb_load_layers_async.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        lib.eeb_load_wait.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        lib.eeb_prefill.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]
         lib.eeb_set_graphs.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_set_gemm_tier.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_debug_last_logits.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
@@ -279,6 +286,30 @@ class Context:
     def reset_slots(self, model: int, slots) -> None:
         s = np.ascontiguousarray(slots, dtype=np.int32)
         _check(self.lib.eeb_reset_slots(self.h, model, len(s), s.ctypes.data))
+
+    def host_stage(self, model: int, depth: int) -> None:
+        _check(self.lib.eeb_host_stage(self.h, model, depth))
+
+    def load_layers_async(self, model: int, depth: int) -> None:
+        _check(self.lib.eeb_load_layers_async(self.h, model, depth))
+
+    def load_wait(self, model: int) -> tuple[float, int]:
+        sec, nb = C.c_double(), C.c_int64()
+        _check(self.lib.eeb_load_wait(self.h, model, C.byref(sec), C.byref(nb)))
+        return sec.value, nb.value
+
+    def prefill(self, model: int, depth: int, slots, prompts, start_pos=None) -> None:
+        """Run each prompt (list of token arrays) through layers 1..depth into its
+        KV slot (eeb_prefill); start_pos defaults to 0 per sequence."""
+        sl = np.ascontiguousarray(slots, dtype=np.int32)
+        lens = np.ascontiguousarray([len(p) for p in prompts], dtype=np.int32)
+        sp = np.zeros(len(sl), np.int32) if start_pos is None else np.ascontiguousarray(start_pos, dtype=np.int32)
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts])
+                                    if len(prompts) else np.zeros(0, np.int32), dtype=np.int32)
+        if len(toks) == 0:
+            toks = np.zeros(1, np.int32)
+        _check(self.lib.eeb_prefill(self.h, model, depth, len(sl), sl.ctypes.data, sp.ctypes.data, lens.ctypes.data,
+                                    toks.ctypes.data))
 
     def set_graphs(self, on: bool) -> None:
         _check(self.lib.eeb_set_graphs(self.h, 1 if on else 0))

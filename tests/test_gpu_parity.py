@@ -114,8 +114,9 @@ def test_f32_step_parity_all_policies(ctx, desc):
                     continue
                 gk, gv = ctx.read_kv(m, layer, int(slots[b]), pos)
                 rk, rv = ref.read_kv(layer, int(slots[b]), pos)
-                np.testing.assert_allclose(gk, rk, atol=1e-4, rtol=1e-3)
-                np.testing.assert_allclose(gv, rv, atol=1e-4, rtol=1e-3)
+                where = f"pos {pos} policy {policy} layer {layer} row {b}"
+                np.testing.assert_allclose(gk, rk, atol=1e-4, rtol=1e-3, err_msg="K " + where)
+                np.testing.assert_allclose(gv, rv, atol=1e-4, rtol=1e-3, err_msg="V " + where)
     ctx.retain_logits(False)
 
 

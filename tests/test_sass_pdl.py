@@ -1,0 +1,57 @@
+"""Static check of the built kernels (CPU, cuobjdump): no kernel of the PDL
+chain may load global memory before `griddepcontrol.wait` (SASS ACQBULK).
+
+A `const T* __restrict__` kernel parameter lets the compiler treat its loads
+as invariant and hoist them above the wait, so a kernel reads its
+predecessor's output (e.g. the compacted row count) before the predecessor
+has written it — a race that only shows under particular timings.  Weight
+streams (TMA, UTMALDG) are allowed before the wait: weights never change
+inside a step.
+"""
+import re
+import subprocess
+
+import pytest
+
+from paper_2504_10724_b200 import eeb
+
+ALLOWED_PRE_WAIT = ("UTMALDG",)        # TMA weight prefetch
+NO_PDL_KERNELS = ("step_kernel", "synth")  # standalone launches (persistent step, weight synthesis)
+
+
+def _functions(sass: str):
+    cur, body = None, []
+    for line in sass.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            if cur:
+                yield cur, body
+            cur, body = m.group(1), []
+        elif cur:
+            ins = re.search(r"/\*[0-9a-f]{4,}\*/\s+(.*?);", line)
+            if ins:
+                body.append(ins.group(1))
+    if cur:
+        yield cur, body
+
+
+def test_no_global_load_before_griddepcontrol_wait():
+    try:
+        sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(eeb.LIB_PATH)], capture_output=True,
+                              text=True, check=True).stdout
+    except (FileNotFoundError, subprocess.CalledProcessError) as e:
+        pytest.skip(f"cuobjdump unavailable: {e}")
+    checked, bad = 0, []
+    for name, body in _functions(sass):
+        if any(k in name for k in NO_PDL_KERNELS) or not any("ACQBULK" in i for i in body):
+            continue
+        checked += 1
+        for ins in body:
+            if "ACQBULK" in ins:
+                break
+            op = ins.split()[0] if not ins.startswith("@") else ins.split()[1]
+            if op.startswith(("LDG", "LD.", "ATOMG", "REDG", "STG", "ST.")) and not op.startswith(ALLOWED_PRE_WAIT):
+                bad.append((name, ins))
+                break
+    assert checked >= 10, checked
+    assert not bad, bad
