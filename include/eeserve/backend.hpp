@@ -45,12 +45,29 @@ struct StepOutcome {
     double seconds = 0.0;                   // measured step wall time
 };
 
+/// Prompts of a batch: sequence k = `prompts[k]` into KV slot `slots[k]`.
+struct PrefillRows {
+    std::vector<int32_t> slots;
+    std::vector<std::vector<int32_t>> prompts;
+    int size() const { return (int)slots.size(); }
+};
+
+/// A finished load: measured seconds and bytes moved (0 = not measured; the
+/// engine then charges the reference's modelled bytes / bandwidth).
+struct LoadResult {
+    double seconds = 0.0;
+    std::int64_t bytes = 0;
+};
+
 class DecodeBackend {
 public:
     virtual ~DecodeBackend() = default;
     virtual void register_model(const ModelSpec& spec, int max_slots, int max_seq_len) = 0;
     /// Greedy loader ↔ do_load (engine.hpp:197-216): make layers [1, depth] resident.
-    virtual void load(const std::string& model, int depth) = 0;
+    virtual LoadResult load(const std::string& model, int depth) = 0;
+    /// Prefill ↔ serve_one's prefill phase (engine.hpp:333-341): the prompts'
+    /// KV through layers 1..depth.  Returns the measured seconds (0 = modelled).
+    virtual double prefill(const std::string& model, int depth, const PrefillRows& rows) = 0;
     virtual StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
                              const StepRows& rows) = 0;
 };
@@ -60,7 +77,12 @@ public:
 // ---------------------------------------------------------------------------
 class CudaBackend final : public DecodeBackend {
 public:
-    explicit CudaBackend(int device = 0) { throw_if_error(eeb_create(device, &ctx_), "eeb_create"); }
+    /// host_tier: keep every registered model's layers in pinned host memory
+    /// and load by asynchronous H2D copies from it (the HELIOS loader);
+    /// otherwise layers are materialised on device from the seed.
+    explicit CudaBackend(int device = 0, bool host_tier = false) : host_tier_(host_tier) {
+        throw_if_error(eeb_create(device, &ctx_), "eeb_create");
+    }
     ~CudaBackend() override { eeb_destroy(ctx_); }
     CudaBackend(const CudaBackend&) = delete;
     CudaBackend& operator=(const CudaBackend&) = delete;
@@ -87,10 +109,37 @@ public:
         int h = -1;
         throw_if_error(eeb_model_register(ctx_, &d, &h), "eeb_model_register");
         handles_[spec.id] = {h, spec};
+        if (host_tier_) throw_if_error(eeb_host_stage(ctx_, h, spec.num_layers), "eeb_host_stage");
     }
 
-    void load(const std::string& model, int depth) override {
-        throw_if_error(eeb_load_layers(ctx_, handle(model).h, depth), "eeb_load_layers");
+    LoadResult load(const std::string& model, int depth) override {
+        const int h = handle(model).h;
+        LoadResult r;
+        if (!host_tier_) {
+            const auto t0 = std::chrono::steady_clock::now();
+            throw_if_error(eeb_load_layers(ctx_, h, depth), "eeb_load_layers");
+            r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            return r;
+        }
+        int before = 0;
+        throw_if_error(eeb_loaded_depth(ctx_, h, &before), "eeb_loaded_depth");
+        throw_if_error(eeb_load_layers_async(ctx_, h, depth), "eeb_load_layers_async");
+        if (depth > before) throw_if_error(eeb_load_wait(ctx_, h, &r.seconds, &r.bytes), "eeb_load_wait");
+        return r;
+    }
+
+    double prefill(const std::string& model, int depth, const PrefillRows& rows) override {
+        std::vector<int32_t> start(rows.size(), 0), lens, toks;
+        for (const auto& p : rows.prompts) {
+            lens.push_back((int32_t)p.size());
+            toks.insert(toks.end(), p.begin(), p.end());
+        }
+        if (toks.empty()) return 0.0;
+        const auto t0 = std::chrono::steady_clock::now();
+        throw_if_error(eeb_prefill(ctx_, handle(model).h, depth, rows.size(), rows.slots.data(), start.data(),
+                                   lens.data(), toks.data()),
+                       "eeb_prefill");
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
 
     StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
@@ -170,6 +219,7 @@ private:
         return best;
     }
     eeb_ctx* ctx_ = nullptr;
+    bool host_tier_ = false;
     std::map<std::string, Entry> handles_;
 };
 
@@ -182,7 +232,8 @@ public:
         for (const auto& r : trace.requests) by_id_[r.request_id] = &r;
     }
     void register_model(const ModelSpec& spec, int, int) override { specs_[spec.id] = spec; }
-    void load(const std::string&, int) override {}
+    LoadResult load(const std::string&, int) override { return {}; }
+    double prefill(const std::string&, int, const PrefillRows&) override { return 0.0; }
 
     StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
                      const StepRows& rows) override {

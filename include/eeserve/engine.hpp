@@ -52,6 +52,13 @@ struct EngineConfig {
     bool prefill = true;  // run the prompt through the backend (real KV); off for trace replay
 };
 
+struct RequestTiming {  // ↔ the request's TTFT (engine.hpp:333-337) and its tokens' TPOT
+    std::int64_t request_id = 0;
+    double ttft_s = 0.0;
+    double tpot_sum_s = 0.0;
+    int tokens = 0;
+};
+
 struct EngineReport {
     std::int64_t tokens = 0;
     std::int64_t steps = 0;
@@ -64,6 +71,10 @@ struct EngineReport {
     int achieved_batch_size = 0;
     std::int64_t ld_count = 0, sw_count = 0, eval_cycles = 0;
     std::vector<std::pair<std::string, int>> serving_history;  // (model, depth) per served batch
+    double load_s = 0.0;              // loader stalls (measured, or bytes / bandwidth when not measured)
+    std::int64_t load_bytes = 0;
+    double prefill_s = 0.0;
+    std::vector<RequestTiming> requests;
     Pht pht;
 };
 
@@ -140,11 +151,20 @@ private:
     EngineReport rep_;
     double sum_logprob_ = 0.0;
     std::int64_t unchanged_ = 0, unchanged_known_ = 0;
+    double pending_stall_s_ = 0.0;  // loads charged to the next batch's TTFT (engine.hpp:205-207, :336)
 
     void do_load(const std::string& id, int target, const std::string& reason) {
-        if (mem_.depth_of(id) == target) return;
+        const int from = mem_.depth_of(id);
+        if (from == target) return;
+        const std::int64_t modelled = load_delta_bytes(repo_.at(id), from, target);
         apply_load(mem_, repo_, cfg_.mem, id, target);  // CapacityError leaves state untouched
-        be_.load(id, target);
+        const LoadResult lr = be_.load(id, target);
+        // growth pays the transfer (measured when the backend moved real bytes);
+        // shrink and eviction are free (engine.hpp:197-199)
+        const double dur = target < from ? 0.0 : lr.seconds > 0.0 ? lr.seconds : load_seconds(modelled, cfg_.mem);
+        rep_.load_s += dur;
+        rep_.load_bytes += lr.bytes > 0 ? lr.bytes : std::max<std::int64_t>(0, modelled);
+        pending_stall_s_ += dur;
         if (reason == "breach_load_more") ++rep_.ld_count;
     }
 
@@ -236,22 +256,28 @@ private:
             max_prompt = std::max(max_prompt, r->prompt_len);
             max_tokens = std::max(max_tokens, r->num_tokens);
         }
-        // Prefill (engine.hpp:333-341): the prompt's KV through the serving depth.
+        // Prefill (engine.hpp:333-341): the prompts' KV through the layers the
+        // step will run (the serving depth in flat mode, all layers otherwise).
+        // TTFT = the pending loader stall + the prefill (engine.hpp:336).
+        double prefill_s = 0.0;
         if (cfg_.prefill) {
-            const TokenPolicy pre = tp == TokenPolicy::flat ? TokenPolicy::flat : TokenPolicy::full_depth;
-            for (int p = 0; p < max_prompt; ++p) {
-                StepRows rows;
-                for (int i = 0; i < b; ++i) {
-                    if (p >= batch[i]->prompt_len) continue;
-                    rows.slots.push_back(i);
-                    rows.tokens.push_back(synthetic_token(cfg_.token_seed, batch[i]->request_id, p, vocab));
-                    rows.positions.push_back(p);
-                    rows.request_ids.push_back(batch[i]->request_id);
-                    rows.token_index.push_back(0);
-                }
-                if (rows.size()) be_.step(model, depth, pre, cfg_.policy.th, rows);
+            PrefillRows pr;
+            for (int i = 0; i < b; ++i) {
+                pr.slots.push_back(i);
+                std::vector<int32_t> p(batch[i]->prompt_len);
+                for (int k = 0; k < batch[i]->prompt_len; ++k)
+                    p[k] = synthetic_token(cfg_.token_seed, batch[i]->request_id, k, vocab);
+                pr.prompts.push_back(std::move(p));
             }
+            prefill_s = be_.prefill(model, tp == TokenPolicy::flat ? depth : spec.num_layers, pr);
         }
+        if (prefill_s <= 0.0)  // modelled (engine.hpp:333-334): prompt_len x depth x t_prefill
+            prefill_s = (double)max_prompt * depth * spec.t_prefill_per_layer_per_token_s;
+        rep_.prefill_s += prefill_s;
+        const double ttft = pending_stall_s_ + prefill_s;
+        pending_stall_s_ = 0.0;
+        const size_t first_timing = rep_.requests.size();
+        for (int i = 0; i < b; ++i) rep_.requests.push_back({batch[i]->request_id, ttft, 0.0, 0});
         // Decode: one token per in-flight request per step.
         for (int t = 0; t < max_tokens; ++t) {
             StepRows rows;
@@ -272,6 +298,11 @@ private:
                 dur = deepest * spec.t_decode_per_layer_s;
             }
             consume(model, spec, tp, profile, rows, o, dur);
+            for (int i = 0; i < b; ++i)
+                if (t < batch[i]->num_tokens) {
+                    rep_.requests[first_timing + i].tpot_sum_s += dur;
+                    rep_.requests[first_timing + i].tokens += 1;
+                }
         }
     }
 

@@ -459,8 +459,23 @@ void load_async(eeb_ctx* c, Model& m, int to) {
     auto P = std::make_unique<PendingLoad>();
     EEB_CUDA(cudaEventCreate(&P->t0));
     EEB_CUDA(cudaEventCreate(&P->t1));
-    // the copies must not overtake work already queued on the decode stream
-    // that still reads buffers being replaced (none are: growth only adds)
+    // Device buffers first (cudaMalloc is host-side work), then the copies
+    // back to back on the load stream: the timed region is the transfer.
+    std::vector<std::unique_ptr<LayerWeights>> fresh;
+    for (int l = (int)m.layers.size() + 1; l <= to; ++l) fresh.push_back(alloc_layer(m));
+    if (m.loaded == 0) {
+        const HostBlob& b = *m.host.base;
+        m.emb.ensure(b.sz[0]);
+        m.head.clear();
+        m.head_norm.clear();
+        for (int e = 0; e < d.n_exits; ++e) {
+            m.head.push_back(std::make_unique<DevBuf>());
+            m.head.back()->ensure(b.sz[1 + e]);
+            m.head_norm.push_back(std::make_unique<DevBuf>());
+            m.head_norm.back()->ensure(b.sz[1 + d.n_exits + e]);
+        }
+    }
+    // growth only adds buffers: nothing queued on the decode stream reads them
     EEB_CUDA(cudaEventRecord(P->t0, ls));
     auto copy_in = [&](DevBuf& dst, const HostBlob& b, size_t k) {
         EEB_CUDA(cudaMemcpyAsync(dst.p, static_cast<const char*>(b.buf.p) + b.off[k], b.sz[k], cudaMemcpyHostToDevice,
@@ -475,15 +490,6 @@ void load_async(eeb_ctx* c, Model& m, int to) {
     };
     if (m.loaded == 0) {
         const HostBlob& b = *m.host.base;
-        m.emb.ensure(b.sz[0]);
-        m.head.clear();
-        m.head_norm.clear();
-        for (int e = 0; e < d.n_exits; ++e) {
-            m.head.push_back(std::make_unique<DevBuf>());
-            m.head.back()->ensure(b.sz[1 + e]);
-            m.head_norm.push_back(std::make_unique<DevBuf>());
-            m.head_norm.back()->ensure(b.sz[1 + d.n_exits + e]);
-        }
         copy_in(m.emb, b, 0);
         for (int e = 0; e < d.n_exits; ++e) {
             copy_in(*m.head[e], b, 1 + e);
@@ -491,9 +497,8 @@ void load_async(eeb_ctx* c, Model& m, int to) {
         }
         mark(0);
     }
-    while ((int)m.layers.size() < to) {
+    for (auto& L : fresh) {
         const int l = (int)m.layers.size() + 1;
-        auto L = alloc_layer(m);
         const HostBlob& b = *m.host.layers[l - 1];
         for (int k = 0; k < 6; ++k) copy_in(*L->parts[k], b, k);
         mark(l);

@@ -13,6 +13,25 @@ ROOT = Path(__file__).resolve().parent.parent
 JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 
 
+def build_engine_gpu(verbose: bool = False) -> Path:
+    """tests/_bin/test_engine_gpu: BatchedEngine + CudaBackend end to end (needs a GPU to run)."""
+    src = ROOT / "tests" / "cpp" / "test_engine_gpu.cpp"
+    out = ROOT / "tests" / "_bin" / "test_engine_gpu"
+    lib = ROOT / "paper_2504_10724_b200"
+    deps = [src, lib / "libeeb.so", ROOT / "include" / "eeb" / "eeb.h", *(ROOT / "include" / "eeserve").glob("*.hpp")]
+    if out.exists() and all(d.stat().st_mtime <= out.stat().st_mtime for d in deps):
+        return out
+    out.parent.mkdir(exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-I/usr/local/cuda/include", str(src), "-o", str(out),
+           f"-L{lib}", "-leeb", f"-Wl,-rpath,{lib}", "-L/usr/local/cuda/lib64", "-lcudart"]
+    if verbose:
+        print(" ".join(cmd))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"engine GPU test build failed:\n{r.stderr}")
+    return out
+
+
 def build_host(verbose: bool = False) -> Path | None:
     ref = ROOT / "oracle" / "_ref" / "libeeref.so"
     src = ROOT / "tests" / "cpp" / "test_host.cpp"
