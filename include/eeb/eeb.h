@@ -77,6 +77,13 @@ typedef struct {
     uint64_t seed;                /* weights are a pure function of (seed, tensor, index) */
     float rope_theta;
     float norm_eps;
+    /* Tensor parallelism (C5: 70B over 8 GPUs): 0/1 = none.  tp_rank >= 0: this
+     * context holds shard tp_rank (its q/kv heads, d_ffn/tp MLP columns,
+     * vocab/tp head rows) and sums row-parallel partials / gathers head
+     * partials over the context's NCCL communicator (eeb_nccl_init).
+     * tp_rank = -1: all tp shards in this context, combined locally. */
+    int32_t tp_size;
+    int32_t tp_rank;
 } eeb_model_desc;
 
 /* Per-step outputs, all arrays of length `batch` unless noted.  Any pointer

@@ -105,6 +105,15 @@ struct Model {
     std::vector<float> alphas;
     int head_dim = 0, dq = 0, dkv = 0, up_rows = 0;
     size_t wbytes = 0;  // weight element size
+    // Tensor parallelism (Megatron layout): column-parallel QKV / up, row-parallel
+    // O / down (partials summed across ranks), vocab-parallel exit heads.  A rank
+    // context holds one shard (tp_rank >= 0, NCCL between ranks); tp_rank = -1
+    // holds all tp shards in one context and sums them locally (single-GPU
+    // emulation of the group: same kernels, same shard weights).
+    int tp = 1, rank = 0, shards = 1;
+    int hq_l = 0, hkv_l = 0, dq_l = 0, dkv_l = 0, f_l = 0, up_l = 0, v_l = 0;  // per-shard dims
+    int shard_rank(int s) const { return rank >= 0 ? rank : s; }
+    size_t kv_shard_elems = 0;  // one (layer, shard) block of the KV cache
     // base weights
     DevBuf emb;
     std::vector<std::unique_ptr<DevBuf>> head, head_norm;
@@ -159,6 +168,7 @@ struct eeb_ctx {
     eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
     eeb::DevBuf head_tok, head_conf, head_logp, head_tri;
+    eeb::DevBuf tp_partial;         // row-parallel partial sums all-reduced across TP ranks
     eeb::DevBuf pf_meta;            // prefill (tok, slot, pos) of every prompt token
     void* pf_pin = nullptr;
     size_t pf_pin_bytes = 0;
@@ -202,6 +212,7 @@ struct NcclApi {
     decltype(&ncclGetUniqueId) get_unique_id = nullptr;
     decltype(&ncclCommInitRank) comm_init_rank = nullptr;
     decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
     decltype(&ncclGroupStart) group_start = nullptr;
     decltype(&ncclGroupEnd) group_end = nullptr;
     decltype(&ncclCommDestroy) comm_destroy = nullptr;
@@ -221,6 +232,7 @@ const NcclApi& nccl() {
         api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
         api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
         api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
+        api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
         api.group_start = (decltype(api.group_start))dlsym(h, "ncclGroupStart");
         api.group_end = (decltype(api.group_end))dlsym(h, "ncclGroupEnd");
         api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
@@ -289,6 +301,15 @@ void validate_desc(const eeb_model_desc& d) {
     if (d.mlp_kind != EEB_MLP_RELU && d.mlp_kind != EEB_MLP_SWIGLU) bad("unknown mlp kind");
     if (d.max_slots <= 0 || d.max_seq_len <= 0) bad("max_slots and max_seq_len must be positive");
     if (!(d.design_th >= 0.f && d.design_th <= 1.f)) bad("design_th must be in [0,1]");
+    if (d.tp_size < 0 || d.tp_size > 64) bad("tp_size must be in [0, 64]");
+    if (d.tp_size > 1) {
+        const int t = d.tp_size;
+        if (d.tp_rank < -1 || d.tp_rank >= t) bad("tp_rank must be -1 (all shards local) or in [0, tp_size)");
+        if (d.n_heads % t || d.n_kv_heads % t || d.d_ffn % t || d.vocab % t)
+            bad("n_heads, n_kv_heads, d_ffn and vocab must be multiples of tp_size");
+        if ((d.d_ffn / t) % 256 != 0) bad("d_ffn / tp_size must be a multiple of 256");
+        if (d.dtype != EEB_BF16) bad("tensor parallelism needs bf16 weights");
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -305,8 +326,10 @@ void synth_base(Model& m, cudaStream_t s) {
     m.head_norm.clear();
     for (int e = 0; e < d.n_exits; ++e) {
         auto h = std::make_unique<DevBuf>();
-        h->ensure((size_t)d.vocab * D * m.wbytes);
-        synth_head(d.dtype, h->p, d.seed, e, m.alphas[e], d.vocab, D, s);
+        h->ensure((size_t)m.shards * m.v_l * D * m.wbytes);  // vocab shards, shard-major
+        for (int sh = 0; sh < m.shards; ++sh)
+            synth_head(d.dtype, static_cast<char*>(h->p) + (size_t)sh * m.v_l * D * m.wbytes, d.seed, e, m.alphas[e],
+                       d.vocab, D, s, m.shard_rank(sh) * m.v_l, m.v_l);
         auto g = std::make_unique<DevBuf>();
         g->ensure((size_t)D * sizeof(float));
         synth_norm(g->p, d.seed, synth::base_tid(synth::kHeadNorm, e), D, s);
@@ -321,10 +344,12 @@ std::unique_ptr<LayerWeights> alloc_layer(const Model& m) {
     auto L = std::make_unique<LayerWeights>();
     L->attn_norm.ensure((size_t)D * 4);
     L->mlp_norm.ensure((size_t)D * 4);
-    L->wqkv.ensure((size_t)(m.dq + 2 * m.dkv) * D * m.wbytes);
-    L->wo.ensure((size_t)D * m.dq * m.wbytes);
-    L->wup.ensure((size_t)m.up_rows * D * m.wbytes);
-    L->wdown.ensure((size_t)D * F * m.wbytes);
+    const size_t S = (size_t)m.shards;
+    L->wqkv.ensure(S * (m.dq_l + 2 * m.dkv_l) * D * m.wbytes);
+    L->wo.ensure(S * D * m.dq_l * m.wbytes);
+    L->wup.ensure(S * m.up_l * D * m.wbytes);
+    L->wdown.ensure(S * D * m.f_l * m.wbytes);
+    (void)F;
     return L;
 }
 
@@ -337,13 +362,27 @@ std::unique_ptr<LayerWeights> synth_layer(const Model& m, int l, cudaStream_t s)
     auto L = alloc_layer(m);
     synth_norm(L->attn_norm.p, seed, synth::layer_tid(l, synth::kAttnNorm), D, s);
     synth_norm(L->mlp_norm.p, seed, synth::layer_tid(l, synth::kMlpNorm), D, s);
-    const int qkv_rows = m.dq + 2 * m.dkv;
-    synth_linear(d.dtype, L->wqkv.p, seed, synth::layer_tid(l, synth::kWqkv), qkv_rows, D, synth::kSigma, false, D,
-                 s);
-    synth_linear(d.dtype, L->wo.p, seed, synth::layer_tid(l, synth::kWo), D, m.dq, rsig, true, D, s);
-    synth_linear(d.dtype, L->wup.p, seed, synth::layer_tid(l, synth::kWup), m.up_rows, D, synth::kSigma, false, D,
-                 s);
-    synth_linear(d.dtype, L->wdown.p, seed, synth::layer_tid(l, synth::kWdown), D, F, rsig, true, D, s);
+    // Shard sh of rank g: its q heads, k heads, v heads (rows of the full
+    // [dq + 2 dkv][D] QKV), its columns of O and down, its rows of up — every
+    // element the same (seed, tensor, index) value as in the unsharded model.
+    const size_t wb = m.wbytes;
+    const int qkv_l = m.dq_l + 2 * m.dkv_l;
+    for (int sh = 0; sh < m.shards; ++sh) {
+        const int g = m.shard_rank(sh);
+        char* q = static_cast<char*>(L->wqkv.p) + (size_t)sh * qkv_l * D * wb;
+        const int tq = synth::layer_tid(l, synth::kWqkv);
+        synth_linear_slice(d.dtype, q, seed, tq, m.dq_l, D, g * m.dq_l, 0, D, synth::kSigma, false, D, s);
+        synth_linear_slice(d.dtype, q + (size_t)m.dq_l * D * wb, seed, tq, m.dkv_l, D, m.dq + g * m.dkv_l, 0, D,
+                           synth::kSigma, false, D, s);
+        synth_linear_slice(d.dtype, q + (size_t)(m.dq_l + m.dkv_l) * D * wb, seed, tq, m.dkv_l, D,
+                           m.dq + m.dkv + g * m.dkv_l, 0, D, synth::kSigma, false, D, s);
+        synth_linear_slice(d.dtype, static_cast<char*>(L->wo.p) + (size_t)sh * D * m.dq_l * wb, seed,
+                           synth::layer_tid(l, synth::kWo), D, m.dq_l, 0, g * m.dq_l, m.dq, rsig, true, D, s);
+        synth_linear_slice(d.dtype, static_cast<char*>(L->wup.p) + (size_t)sh * m.up_l * D * wb, seed,
+                           synth::layer_tid(l, synth::kWup), m.up_l, D, g * m.up_l, 0, D, synth::kSigma, false, D, s);
+        synth_linear_slice(d.dtype, static_cast<char*>(L->wdown.p) + (size_t)sh * D * m.f_l * wb, seed,
+                           synth::layer_tid(l, synth::kWdown), D, m.f_l, 0, g * m.f_l, F, rsig, true, D, s);
+    }
     return L;
 }
 
@@ -422,6 +461,10 @@ void host_stage(eeb_ctx* c, Model& m, int depth) {
             tmp.desc = d;
             tmp.alphas = m.alphas;
             tmp.wbytes = m.wbytes;
+            tmp.tp = m.tp;
+            tmp.rank = m.rank;
+            tmp.shards = m.shards;
+            tmp.v_l = m.v_l;
             synth_base(tmp, s);
             m.host.base = stage_blob(base_parts(tmp), s);
             EEB_CUDA(cudaStreamSynchronize(s));
@@ -525,10 +568,12 @@ void wait_layers(eeb_ctx* c, Model& m, int need) {
 int64_t weight_bytes_at(const Model& m, int depth) {
     const eeb_model_desc& d = m.desc;
     const int64_t D = d.d_model, F = d.d_ffn;
-    const int64_t base = (int64_t)d.vocab * D * m.wbytes * (1 + d.n_exits) + (int64_t)d.n_exits * D * 4;
+    const int64_t S = m.shards;
+    const int64_t base = (int64_t)d.vocab * D * m.wbytes + (int64_t)d.n_exits * (S * m.v_l * D * m.wbytes + D * 4);
     const int64_t per_layer =
-        ((int64_t)(m.dq + 2 * m.dkv) * D + D * m.dq + (int64_t)m.up_rows * D + D * F) * m.wbytes +
+        S * ((int64_t)(m.dq_l + 2 * m.dkv_l) * D + D * m.dq_l + (int64_t)m.up_l * D + D * m.f_l) * m.wbytes +
         2 * D * 4;
+    (void)F;
     return depth <= 0 ? 0 : base + per_layer * depth;
 }
 
@@ -577,16 +622,18 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
         const int64_t tiles = (N + 127) / 128;
         need = std::max(need, std::max<int64_t>(K / kmin + 1, c->num_sms / tiles + 1) * R * N);
     };
-    upd(m.dq + 2 * m.dkv, D);
-    upd(D, m.dq);
-    upd(m.up_rows, D);
-    upd(D, F);
-    upd(d.vocab, D);
+    upd(m.dq_l + 2 * m.dkv_l, D);
+    upd(D, m.dq_l);
+    upd(m.up_l, D);
+    upd(D, m.f_l);
+    upd(m.v_l, D);
+    need *= m.shards;  // row-parallel shards write their partial planes side by side
     c->ws.ensure((size_t)need * 4);
     c->ws_elems = (int64_t)(c->ws.bytes / 4);
     c->rows.ensure((size_t)(32 + 12 * R) * 4);
     c->head_tok.ensure((size_t)R * 4);
-    c->head_tri.ensure((size_t)R * ((d.vocab + 127) / 128) * 16);
+    c->head_tri.ensure((size_t)R * ((m.v_l + 127) / 128) * m.tp * 16);
+    if (m.tp > 1) c->tp_partial.ensure((size_t)R * D * 4);
     c->head_conf.ensure((size_t)R * 4);
     c->head_logp.ensure((size_t)R * 4);
     c->o_exit.ensure((size_t)R * 4);
@@ -667,7 +714,7 @@ void count(eeb_ctx* c, int cat, int n) {
 
 // One decode GEMM into the split-K plane workspace; returns the planes written.
 int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int N, int K, const int* n_active,
-         int batch) {
+         int batch, int plane0 = 0) {
     GemmArgs a;
     a.dtype = m.desc.dtype;
     a.W = W;
@@ -676,9 +723,9 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     a.max_rows = batch;
     a.N = N;
     a.K = K;
-    a.out = c->ws.as<float>();
     a.plane_stride = (int64_t)batch * N;
-    a.max_planes = (int)std::min<int64_t>(64, c->ws_elems / a.plane_stride);
+    a.out = c->ws.as<float>() + (int64_t)plane0 * a.plane_stride;
+    a.max_planes = (int)std::min<int64_t>(64, c->ws_elems / a.plane_stride - plane0);
     a.num_sms = c->num_sms;
     int planes = 0;
     if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) planes = gemm_tc(a, c->stream);
@@ -694,7 +741,7 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
 // Exit-head GEMM with the fused softmax tail; returns the vocab tiles written
 // to ctx->head_tri, 0 when the tensor-core path does not apply.
 int gemm_head_fused(eeb_ctx* c, const Model& m, const void* W, const void* X, int N, int K, const int* n_active,
-                    int batch) {
+                    int batch, float* tri, int vocab_off) {
     GemmArgs a;
     a.dtype = m.desc.dtype;
     a.W = W;
@@ -707,7 +754,8 @@ int gemm_head_fused(eeb_ctx* c, const Model& m, const void* W, const void* X, in
     a.plane_stride = 0;
     a.max_planes = 1;
     a.num_sms = c->num_sms;
-    a.head_tri = c->head_tri.as<float>();
+    a.head_tri = tri;
+    a.vocab_off = vocab_off;
     if (gemm_tc(a, c->stream) == 0) return 0;
     count(c, kCatHead, 1);
     return (N + 127) / 128;
@@ -724,6 +772,128 @@ int gemm_head_fused(eeb_ctx* c, const Model& m, const void* W, const void* X, in
 bool skip_cat(const char* what) {
     static const std::string env = std::getenv("EEB_SKIP") ? std::getenv("EEB_SKIP") : "";
     return !env.empty() && env.find(what) != std::string::npos;
+}
+
+// Sum the `planes` split-K partial planes into the context's partial buffer
+// and all-reduce it over the tensor-parallel group (NCCL, on the step stream;
+// capturable into the step's graph).  Returns the single plane to consume.
+const float* tp_allreduce(eeb_ctx* c, const Model& m, const float* planes_base, int planes, const int* n_active,
+                          int batch) {
+    const int D = m.desc.d_model;
+    float* part = c->tp_partial.as<float>();
+    launch_plane_sum(planes_base, planes, (int64_t)batch * D, n_active, batch, D, part, c->num_sms, c->stream);
+    if (!c->nccl) throw Error(EEB_E_DOMAIN, "tensor-parallel rank without a communicator (eeb_nccl_init)");
+    const ncclResult_t r = nccl().all_reduce(part, part, (size_t)batch * D, ncclFloat32, ncclSum, c->nccl, c->stream);
+    if (r != ncclSuccess) throw Error(EEB_E_CUDA, "ncclAllReduce failed");
+    count(c, kCatNorm, 1);
+    return part;
+}
+
+struct PlaneSet {
+    const float* base;
+    int planes;
+};
+
+// One decoder layer up to (not including) the final residual + RMSNorm:
+// per shard QKV GEMM -> [KV append] -> attention; per shard O GEMM (row-parallel
+// partials side by side in the plane workspace) -> residual + mlp norm; per
+// shard up GEMM -> activation; per shard down GEMM.  Returns the down partial
+// planes (all-reduced over the TP group for a rank context).
+PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, int batch, bool kv_ready) {
+    const eeb_model_desc& d = m.desc;
+    const int D = d.d_model;
+    cudaStream_t s = c->stream;
+    const LayerWeights& W = *m.layers[l - 1];
+    float* ws = c->ws.as<float>();
+    const size_t wb = m.wbytes;
+    const int qkv_l = m.dq_l + 2 * m.dkv_l;
+    for (int sh = 0; sh < m.shards; ++sh) {
+        int planes;
+        {
+            Timer t(c, kCatGemm);
+            planes = skip_cat("gemm") ? 1
+                                      : gemm(c, kCatGemm, m, static_cast<const char*>(W.wqkv.p) + (size_t)sh * qkv_l * D * wb,
+                                             h, qkv_l, D, cur.n_active, batch);
+        }
+        Timer t(c, kCatAttn);
+        AttnArgs a;
+        a.dtype = d.dtype;
+        a.qkv = ws;
+        a.splits = planes;
+        a.split_stride = (int64_t)batch * qkv_l;
+        const size_t kv_off = ((size_t)(l - 1) * m.kv_layer_elems + (size_t)sh * m.kv_shard_elems) * wb;
+        a.k_cache = static_cast<char*>(m.k_cache.p) + kv_off;
+        a.v_cache = static_cast<char*>(m.v_cache.p) + kv_off;
+        a.kv_depth = m.kv_depth.as<uint8_t>();
+        a.rope_cos = m.rope_cos.as<float>();
+        a.rope_sin = m.rope_sin.as<float>();
+        a.n_active = cur.n_active;
+        a.slot = cur.slot;
+        a.pos = cur.pos;
+        a.max_rows = batch;
+        a.layer = l;
+        a.n_heads = m.hq_l;
+        a.n_kv_heads = m.hkv_l;
+        a.head_dim = m.head_dim;
+        a.max_seq = d.max_seq_len;
+        a.out = static_cast<char*>(c->attn.p) + (size_t)sh * batch * m.dq_l * wb;
+        const size_t mk = (size_t)(l - 1) * m.shards + sh;
+        a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[mk].data();
+        a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[mk].data();
+        a.num_sms = c->num_sms;
+        a.kv_ready = kv_ready ? 1 : 0;
+        if (kv_ready) {
+            launch_kv_append(a, s);
+            count(c, kCatAttn, 1);
+        }
+        if (!skip_cat("attn")) launch_attention(a, s);
+        count(c, kCatAttn, 1);
+    }
+    int planes = 0;
+    {
+        Timer t(c, kCatGemm);
+        for (int sh = 0; sh < m.shards; ++sh)
+            planes += skip_cat("gemm") ? 1
+                                       : gemm(c, kCatGemm, m, static_cast<const char*>(W.wo.p) + (size_t)sh * D * m.dq_l * wb,
+                                              static_cast<const char*>(c->attn.p) + (size_t)sh * batch * m.dq_l * wb, D,
+                                              m.dq_l, cur.n_active, batch, planes);
+    }
+    PlaneSet o{ws, planes};
+    if (m.tp > 1 && m.shards == 1) o = {tp_allreduce(c, m, ws, planes, cur.n_active, batch), 1};
+    {
+        Timer t(c, kCatNorm);
+        if (!skip_cat("norm"))
+            launch_residual_norm(d.dtype, o.base, o.planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
+                                 W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
+        count(c, kCatNorm, 1);
+    }
+    for (int sh = 0; sh < m.shards; ++sh) {
+        int up_planes;
+        {
+            Timer t(c, kCatGemm);
+            up_planes = skip_cat("gemm") ? 1
+                                         : gemm(c, kCatGemm, m, static_cast<const char*>(W.wup.p) + (size_t)sh * m.up_l * D * wb,
+                                                h, m.up_l, D, cur.n_active, batch);
+        }
+        Timer t(c, kCatNorm);
+        if (!skip_cat("norm"))
+            launch_act(d.dtype, ws, up_planes, (int64_t)batch * m.up_l, cur.n_active, batch, m.up_l,
+                       d.mlp_kind == EEB_MLP_SWIGLU, static_cast<char*>(c->mlp_h.p) + (size_t)sh * batch * m.f_l * wb,
+                       c->num_sms, s);
+        count(c, kCatNorm, 1);
+    }
+    planes = 0;
+    {
+        Timer t(c, kCatGemm);
+        for (int sh = 0; sh < m.shards; ++sh)
+            planes += skip_cat("gemm") ? 1
+                                       : gemm(c, kCatGemm, m, static_cast<const char*>(W.wdown.p) + (size_t)sh * D * m.f_l * wb,
+                                              static_cast<const char*>(c->mlp_h.p) + (size_t)sh * batch * m.f_l * wb, D,
+                                              m.f_l, cur.n_active, batch, planes);
+    }
+    PlaneSet dn{ws, planes};
+    if (m.tp > 1 && m.shards == 1) dn = {tp_allreduce(c, m, ws, planes, cur.n_active, batch), 1};
+    return dn;
 }
 
 void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
@@ -767,70 +937,11 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
         count(c, kCatOther, 2);
     }
     size_t hi = 0;
-    const int qkv_n = m.dq + 2 * m.dkv;
     float* ws = c->ws.as<float>();
     for (int l = 1; l <= run_layers; ++l) {
-        const LayerWeights& W = *m.layers[l - 1];
-        int planes;
-        {
-            Timer t(c, kCatGemm);
-            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wqkv.p, h_cur, qkv_n, D, cur.n_active, batch);
-        }
-        {
-            Timer t(c, kCatAttn);
-            AttnArgs a;
-            a.dtype = d.dtype;
-            a.qkv = ws;
-            a.splits = planes;
-            a.split_stride = (int64_t)batch * qkv_n;
-            const size_t esz = m.wbytes;
-            a.k_cache = static_cast<char*>(m.k_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * esz;
-            a.v_cache = static_cast<char*>(m.v_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * esz;
-            a.kv_depth = m.kv_depth.as<uint8_t>();
-            a.rope_cos = m.rope_cos.as<float>();
-            a.rope_sin = m.rope_sin.as<float>();
-            a.n_active = cur.n_active;
-            a.slot = cur.slot;
-            a.pos = cur.pos;
-            a.max_rows = batch;
-            a.layer = l;
-            a.n_heads = d.n_heads;
-            a.n_kv_heads = d.n_kv_heads;
-            a.head_dim = m.head_dim;
-            a.max_seq = d.max_seq_len;
-            a.out = c->attn.p;
-            a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[l - 1].data();
-            a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[l - 1].data();
-            a.num_sms = c->num_sms;
-            if (!skip_cat("attn")) launch_attention(a, s);
-            count(c, kCatAttn, 1);
-        }
-        {
-            Timer t(c, kCatGemm);
-            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, cur.n_active, batch);
-        }
-        {
-            Timer t(c, kCatNorm);
-            if (!skip_cat("norm"))
-                launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
-                                     d.norm_eps, W.mlp_norm.as<float>(), h_cur, nullptr, nullptr, s);
-            count(c, kCatNorm, 1);
-        }
-        {
-            Timer t(c, kCatGemm);
-            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wup.p, h_cur, m.up_rows, D, cur.n_active, batch);
-        }
-        {
-            Timer t(c, kCatNorm);
-            if (!skip_cat("norm"))
-                launch_act(d.dtype, ws, planes, (int64_t)batch * m.up_rows, cur.n_active, batch, m.up_rows,
-                           d.mlp_kind == EEB_MLP_SWIGLU, c->mlp_h.p, c->num_sms, s);
-            count(c, kCatNorm, 1);
-        }
-        {
-            Timer t(c, kCatGemm);
-            planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, cur.n_active, batch);
-        }
+        const PlaneSet dn = layer_core(c, m, l, cur, h_cur, batch, false);
+        const float* planes_base = dn.base;
+        const int planes = dn.planes;
         const bool exit_here = head_at(hi, l);
         const bool more = l < run_layers;
         {
@@ -843,7 +954,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             const float* g2 = g_next ? g_head : nullptr;
             void* o2 = g_next && g_head ? c->hhead.p : nullptr;
             if (g1 && !skip_cat("norm"))
-                launch_residual_norm(d.dtype, ws, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
+                launch_residual_norm(d.dtype, planes_base, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
                                      d.norm_eps, g1, o1, g2, o2, s);
             count(c, kCatNorm, 1);
         }
@@ -854,10 +965,31 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             HeadOut h{c->head_tok.as<int>(), c->head_conf.as<float>(), c->head_logp.as<float>()};
             // Fused head (tcgen05 GEMM epilogue emits per-tile softmax partials,
             // decide merges them) unless the logits themselves are retained.
+            // vocab-parallel: shard sh covers rows [g v_l, (g+1) v_l) of the head;
+            // its tile partials land in region g of head_tri (all-gathered over
+            // the TP group for a rank context) and decide merges all regions.
             int head_tiles = 0;
+            const int tiles_l = (m.v_l + 127) / 128;
+            const int64_t region = (int64_t)batch * tiles_l * 4;  // floats per rank region
             if (!c->retain_logits && !skip_cat("head") && c->gemm_tier != 1 && d.dtype == EEB_BF16 &&
-                !std::getenv("EEB_HEAD_UNFUSED"))
-                head_tiles = gemm_head_fused(c, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
+                !std::getenv("EEB_HEAD_UNFUSED")) {
+                for (int sh = 0; sh < m.shards; ++sh) {
+                    const int g = m.shard_rank(sh);
+                    head_tiles = gemm_head_fused(c, m, static_cast<const char*>(m.head[e]->p) + (size_t)sh * m.v_l * D * m.wbytes,
+                                                 c->hhead.p, m.v_l, D, cur.n_active, batch,
+                                                 c->head_tri.as<float>() + g * region, g * m.v_l);
+                    if (head_tiles == 0) break;
+                }
+                if (head_tiles && m.tp > 1 && m.shards == 1) {
+                    if (!c->nccl) throw Error(EEB_E_DOMAIN, "tensor-parallel rank without a communicator (eeb_nccl_init)");
+                    float* all = c->head_tri.as<float>();
+                    const ncclResult_t r = nccl().all_gather(all + m.rank * region, all, (size_t)region, ncclFloat32,
+                                                             c->nccl, s);
+                    if (r != ncclSuccess) throw Error(EEB_E_CUDA, "ncclAllGather failed");
+                }
+            }
+            if (head_tiles == 0 && m.tp > 1)
+                throw Error(EEB_E_DOMAIN, "tensor-parallel exit heads need the fused tensor-core head (bf16, batch >= 16)");
             if (head_tiles == 0) {
                 const int hp =
                     skip_cat("head") ? 1 : gemm(c, kCatHead, m, m.head[e]->p, c->hhead.p, d.vocab, D, cur.n_active, batch);
@@ -873,6 +1005,8 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             DecideArgs da;
             da.head_tri = head_tiles ? c->head_tri.as<float>() : nullptr;
             da.head_tiles = head_tiles;
+            da.head_shards = m.tp;
+            da.head_shard_stride = region / 4;  // float4 entries per rank region
             da.policy = policy;
             da.exit_index = e;
             da.n_exits = d.n_exits;
@@ -920,59 +1054,22 @@ constexpr int kPolicyPrefill = 100;  // graph-cache key
 void enqueue_prefill(eeb_ctx* c, int mi, int depth, int rows) {
     Model& m = model_of(c, mi);
     const eeb_model_desc& d = m.desc;
-    const int D = d.d_model, F = d.d_ffn;
+    const int D = d.d_model;
     cudaStream_t s = c->stream;
     Ints I = ints_of(c);
     RowState cur{I.nA, I.rowA, I.slotA, I.posA, c->xA.as<float>()};
     void* h = c->hn.p;
-    float* ws = c->ws.as<float>();
     launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, rows, D, cur, s);
     launch_mark_depth(rows, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len, depth, s);
     launch_residual_norm(d.dtype, nullptr, 0, 0, cur.n_active, rows, cur.x, D, d.norm_eps,
                          m.layers[0]->attn_norm.as<float>(), h, nullptr, nullptr, s);
     count(c, kCatOther, 3);
-    const int qkv_n = m.dq + 2 * m.dkv;
     for (int l = 1; l <= depth; ++l) {
-        const LayerWeights& W = *m.layers[l - 1];
-        int planes = gemm(c, kCatGemm, m, W.wqkv.p, h, qkv_n, D, cur.n_active, rows);
-        AttnArgs a;
-        a.dtype = d.dtype;
-        a.qkv = ws;
-        a.splits = planes;
-        a.split_stride = (int64_t)rows * qkv_n;
-        a.k_cache = static_cast<char*>(m.k_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * m.wbytes;
-        a.v_cache = static_cast<char*>(m.v_cache.p) + (size_t)(l - 1) * m.kv_layer_elems * m.wbytes;
-        a.kv_depth = m.kv_depth.as<uint8_t>();
-        a.rope_cos = m.rope_cos.as<float>();
-        a.rope_sin = m.rope_sin.as<float>();
-        a.n_active = cur.n_active;
-        a.slot = cur.slot;
-        a.pos = cur.pos;
-        a.max_rows = rows;
-        a.layer = l;
-        a.n_heads = d.n_heads;
-        a.n_kv_heads = d.n_kv_heads;
-        a.head_dim = m.head_dim;
-        a.max_seq = d.max_seq_len;
-        a.out = c->attn.p;
-        a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[l - 1].data();
-        a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[l - 1].data();
-        a.num_sms = c->num_sms;
-        a.kv_ready = 1;
-        launch_kv_append(a, s);
-        launch_attention(a, s);
-        count(c, kCatAttn, 2);
-        planes = gemm(c, kCatGemm, m, W.wo.p, c->attn.p, D, m.dq, cur.n_active, rows);
-        launch_residual_norm(d.dtype, ws, planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D, d.norm_eps,
-                             W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
-        planes = gemm(c, kCatGemm, m, W.wup.p, h, m.up_rows, D, cur.n_active, rows);
-        launch_act(d.dtype, ws, planes, (int64_t)rows * m.up_rows, cur.n_active, rows, m.up_rows,
-                   d.mlp_kind == EEB_MLP_SWIGLU, c->mlp_h.p, c->num_sms, s);
-        planes = gemm(c, kCatGemm, m, W.wdown.p, c->mlp_h.p, D, F, cur.n_active, rows);
+        const PlaneSet dn = layer_core(c, m, l, cur, h, rows, true);
         if (l < depth)  // the next layer's attention norm (the last layer's residual is not needed)
-            launch_residual_norm(d.dtype, ws, planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D, d.norm_eps,
-                                 m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
-        count(c, kCatNorm, l < depth ? 3 : 2);
+            launch_residual_norm(d.dtype, dn.base, dn.planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D,
+                                 d.norm_eps, m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+        count(c, kCatNorm, l < depth ? 1 : 0);
     }
 }
 
@@ -1017,6 +1114,8 @@ void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int 
                                         std::to_string(m.loaded) + ")");
     if (d.dtype == EEB_F32 && batch > 64)
         throw Error(EEB_E_DOMAIN, "f32 parity model supports at most 64 rows per step");
+    if (m.tp > 1 && (batch < 16 || c->gemm_tier == 1 || c->retain_logits))
+        throw Error(EEB_E_DOMAIN, "tensor-parallel steps need the tensor-core tier (batch >= 16, no logit retention)");
     (void)c;
 }
 
@@ -1031,7 +1130,7 @@ bool mk_applicable(eeb_ctx* c, const Model& m, int batch) {
         c->mk_mode = env && env[0] == '1' ? 1 : 0;
     }
     const eeb_model_desc& d = m.desc;
-    const bool ok = !c->retain_logits && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
+    const bool ok = !c->retain_logits && m.tp == 1 && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
                     d.d_model <= 6 * 3 * 128 &&
                     batch <= mk::kMaxRows && d.max_seq_len <= 256 && gemm_tc_available();
     if (c->gemm_tier == 3) {
@@ -1424,26 +1523,43 @@ eeb_status eeb_model_register(eeb_ctx* c, const eeb_model_desc* desc, int* model
         m->dkv = d.n_kv_heads * m->head_dim;
         m->up_rows = d.mlp_kind == EEB_MLP_SWIGLU ? 2 * d.d_ffn : d.d_ffn;
         m->wbytes = d.dtype == EEB_BF16 ? 2 : 4;
+        m->tp = std::max(1, d.tp_size);
+        m->rank = m->tp > 1 ? d.tp_rank : 0;
+        m->shards = m->tp > 1 && m->rank < 0 ? m->tp : 1;
+        m->hq_l = d.n_heads / m->tp;
+        m->hkv_l = d.n_kv_heads / m->tp;
+        m->dq_l = m->hq_l * m->head_dim;
+        m->dkv_l = m->hkv_l * m->head_dim;
+        m->f_l = d.d_ffn / m->tp;
+        m->up_l = m->up_rows / m->tp;
+        m->v_l = d.vocab / m->tp;
         if (m->head_dim % 16 != 0 || m->head_dim > 128) throw Error(EEB_E_VALIDATION, "head_dim must be a multiple of 16, <= 128");
         // KV pool ↔ kv_bytes_per_slot (memory_model.hpp:58-60): every layer, max_seq positions.
-        m->kv_layer_elems = (size_t)d.max_slots * d.n_kv_heads * d.max_seq_len * m->head_dim;
+        // (KV heads of a layer: shard-major, each shard [slots][hkv_l][S][hd])
+        m->kv_shard_elems = (size_t)d.max_slots * m->hkv_l * d.max_seq_len * m->head_dim;
+        m->kv_layer_elems = m->kv_shard_elems * m->shards;
         m->k_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
         m->v_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
-        EEB_CUDA(cudaMemset(m->k_cache.p, 0, m->k_cache.bytes));  // finite values behind masked rows
-        EEB_CUDA(cudaMemset(m->v_cache.p, 0, m->v_cache.bytes));
+        // stream-ordered (the context stream is non-blocking: a legacy-stream
+        // memset would not be ordered before the first step)
+        EEB_CUDA(cudaMemsetAsync(m->k_cache.p, 0, m->k_cache.bytes, c->stream));  // finite values behind masked rows
+        EEB_CUDA(cudaMemsetAsync(m->v_cache.p, 0, m->v_cache.bytes, c->stream));
         if (d.dtype == EEB_BF16 && (m->head_dim == 64 || m->head_dim == 128) && gemm_tc_available()) {
-            m->k_maps.resize(d.num_layers);
-            m->v_maps.resize(d.num_layers);
-            for (int l = 0; l < d.num_layers; ++l) {
-                const size_t off = (size_t)l * m->kv_layer_elems * 2;
-                make_kv_tensor_map(m->k_maps[l].data(), static_cast<char*>(m->k_cache.p) + off, m->head_dim,
-                                   d.max_seq_len, d.max_slots * d.n_kv_heads, 32);
-                make_kv_tensor_map(m->v_maps[l].data(), static_cast<char*>(m->v_cache.p) + off, m->head_dim,
-                                   d.max_seq_len, d.max_slots * d.n_kv_heads, 32);
-            }
+            m->k_maps.resize((size_t)d.num_layers * m->shards);
+            m->v_maps.resize((size_t)d.num_layers * m->shards);
+            for (int l = 0; l < d.num_layers; ++l)
+                for (int sh = 0; sh < m->shards; ++sh) {
+                    const size_t off = ((size_t)l * m->kv_layer_elems + sh * m->kv_shard_elems) * 2;
+                    const size_t k = (size_t)l * m->shards + sh;
+                    make_kv_tensor_map(m->k_maps[k].data(), static_cast<char*>(m->k_cache.p) + off, m->head_dim,
+                                       d.max_seq_len, d.max_slots * m->hkv_l, 32);
+                    make_kv_tensor_map(m->v_maps[k].data(), static_cast<char*>(m->v_cache.p) + off, m->head_dim,
+                                       d.max_seq_len, d.max_slots * m->hkv_l, 32);
+                }
         }
         m->kv_depth.ensure((size_t)d.max_slots * d.max_seq_len);
-        EEB_CUDA(cudaMemset(m->kv_depth.p, 0, m->kv_depth.bytes));
+        EEB_CUDA(cudaMemsetAsync(m->kv_depth.p, 0, m->kv_depth.bytes, c->stream));
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
         // RoPE tables in f64 then rounded (restated identically by the oracle).
         const int half = m->head_dim / 2;
         std::vector<float> cs((size_t)d.max_seq_len * half), sn((size_t)d.max_seq_len * half);
@@ -1813,9 +1929,13 @@ eeb_status eeb_debug_read_kv(eeb_ctx* c, int model, int layer, int slot, int pos
         EEB_CUDA(cudaStreamSynchronize(c->stream));
         const int hd = m.head_dim;
         std::vector<char> tmp((size_t)hd * m.wbytes);
-        for (int g = 0; g < d.n_kv_heads; ++g) {
-            const size_t off = (size_t)(layer - 1) * m.kv_layer_elems +
-                               (((size_t)slot * d.n_kv_heads + g) * d.max_seq_len + pos) * hd;
+        // heads held here: all of them (one shard or all shards), or the
+        // rank's hkv_l heads in a tensor-parallel rank context
+        const int heads = m.shards * m.hkv_l;
+        for (int g = 0; g < heads; ++g) {
+            const int sh = g / m.hkv_l, lg = g % m.hkv_l;
+            const size_t off = (size_t)(layer - 1) * m.kv_layer_elems + (size_t)sh * m.kv_shard_elems +
+                               (((size_t)slot * m.hkv_l + lg) * d.max_seq_len + pos) * hd;
             for (int which = 0; which < 2; ++which) {
                 const DevBuf& b = which == 0 ? m.k_cache : m.v_cache;
                 float* dst = (which == 0 ? host_k : host_v) + (size_t)g * hd;

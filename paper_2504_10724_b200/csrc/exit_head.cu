@@ -107,12 +107,18 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
         // {max, sum exp, argmax} partials — warp per row, tiles in a fixed
         // order (deterministic); argmax ties resolve to the lowest token id.
         const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int tiles = a.head_tiles * a.head_shards;
         for (int i = threadIdx.x >> 5; i < n_live; i += nw) {
             const float4* tri = reinterpret_cast<const float4*>(a.head_tri) + (int64_t)i * a.head_tiles;
+            // tile t of the whole vocabulary: region t / head_tiles (a TP shard), local tile t % head_tiles
+            auto at = [&](int t) {
+                const int r = t / a.head_tiles;
+                return tri[r * a.head_shard_stride + (t - r * a.head_tiles)];
+            };
             float m = -INFINITY;
             int am = 0x7fffffff;
-            for (int t = lane; t < a.head_tiles; t += 32) {
-                const float4 v = tri[t];
+            for (int t = lane; t < tiles; t += 32) {
+                const float4 v = at(t);
                 const int ai = __float_as_int(v.z);
                 if (v.x > m || (v.x == m && ai < am)) { m = v.x; am = ai; }
             }
@@ -123,8 +129,8 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
                 if (m2 > m || (m2 == m && a2 < am)) { m = m2; am = a2; }
             }
             float sum = 0.f;
-            for (int t = lane; t < a.head_tiles; t += 32) {
-                const float4 v = tri[t];
+            for (int t = lane; t < tiles; t += 32) {
+                const float4 v = at(t);
                 sum += v.y * __expf(v.x - m);
             }
             sum = warp_sum(sum);

@@ -139,6 +139,7 @@ struct TcParams {
     int64_t split_stride;
     float4* head_tri;  // exit-head epilogue (splits == 1): per (row, tile) {max, sumexp, argmax}
     int tiles;
+    int vocab_off;     // added to the argmax (vocab-parallel shard)
 };
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float M = fmaxf(m, m2);
                 const int A = (m2 > m || (m2 == m && a2 < am)) ? a2 : am;
                 const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
-                if (hf == 0 && r < lim) p.head_tri[(int64_t)r * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A), 0.f);
+                if (hf == 0 && r < lim) p.head_tri[(int64_t)r * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
             }
         } else if (p.cs == 1) {
             float* plane = p.part + (int64_t)split * p.split_stride;
@@ -442,6 +443,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.split_stride = a.plane_stride;
     p.head_tri = reinterpret_cast<float4*>(a.head_tri);
     p.tiles = tiles;
+    p.vocab_off = a.vocab_off;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;

@@ -11,10 +11,14 @@ namespace eeb {
 // ---- synthetic weights (synth_kernels.cu) ---------------------------------
 void synth_linear(int dtype, void* dst, uint64_t seed, int tid, int rows, int cols, float scale,
                   bool zero_signal_rows, int d, cudaStream_t s);
+// rows x cols block at (row0, col0) of a [*][full_cols] tensor (a tensor-parallel shard)
+void synth_linear_slice(int dtype, void* dst, uint64_t seed, int tid, int rows, int cols, int row0, int col0,
+                        int full_cols, float scale, bool zero_signal_rows, int d, cudaStream_t s);
 void synth_norm(void* dst_f32, uint64_t seed, int tid, int d, cudaStream_t s);
 void synth_embedding(int dtype, void* dst, uint64_t seed, int vocab, int d, cudaStream_t s);
+// rows (0 = vocab) vocabulary rows starting at row0 (vocab-parallel shard)
 void synth_head(int dtype, void* dst, uint64_t seed, int e, float alpha, int vocab, int d,
-                cudaStream_t s);
+                cudaStream_t s, int row0 = 0, int rows = 0);
 
 // ---- per-step row state ----------------------------------------------------
 // Rows are kept compact: entries [0, *n_active) are live.  row_of maps a
@@ -35,6 +39,9 @@ void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
                           void* out2, cudaStream_t s);
+// out[i][:] = sum_s part[s][i][:] for the live rows (tensor-parallel partial before all-reduce).
+void launch_plane_sum(const float* part, int splits, int64_t split_stride, const int* n_active, int max_rows, int d,
+                      float* out, int num_sms, cudaStream_t s);
 // out[i][n] = relu(sum_s part) or silu(gate)*up over interleaved (gate, up) columns.
 void launch_act(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active, int max_rows,
                 int N, bool swiglu, void* out, int num_sms, cudaStream_t s);
@@ -58,6 +65,7 @@ struct GemmArgs {
     // vocab tile) partials {max, sum exp(l - max), argmax} to head_tri[row *
     // tiles + tile] (float4, argmax as int bits); decide merges them.
     float* head_tri = nullptr;
+    int vocab_off = 0;  // global id of this shard's first vocabulary row (vocab-parallel heads)
 };
 // Tier 1: CUDA cores (any dtype, <= 64 rows).  Returns the planes written.
 int gemm_cc(const GemmArgs& a, cudaStream_t s);
@@ -144,7 +152,9 @@ struct DecideArgs {
     int* gather_src;         // [maxB] nxt index -> cur index
     HeadOut head;
     const float* head_tri = nullptr;  // optional: per-(row, tile) partials from the fused head GEMM (merged here)
-    int head_tiles = 0;
+    int head_tiles = 0;               // tiles per shard region
+    int head_shards = 1;              // regions (tensor-parallel ranks)
+    int64_t head_shard_stride = 0;    // float4 entries between regions
     StepOutDev out;
     int layers[64];          // exit ladder (profile mode maps head index -> layer)
 };

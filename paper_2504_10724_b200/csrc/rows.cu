@@ -124,6 +124,19 @@ __global__ void act_kernel(const float* part, int splits, int64_t split_stride,
     }
 }
 
+__global__ void plane_sum_kernel(const float* part, int splits, int64_t split_stride, const int* n_active, int d,
+                                 float* out) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int64_t total = (int64_t)(*n_active) * d;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        float y = 0.f;
+        for (int s = 0; s < splits; ++s) y += part[s * split_stride + idx];
+        out[idx] = y;
+    }
+}
+
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ emb, const int* tok,
                              const int* slot_in, const int* pos_in, int batch, int d,
@@ -186,6 +199,14 @@ void launch_residual_norm(int dtype, const float* part, int splits, int64_t spli
     else
         launch_pdl(residual_norm_kernel<__nv_bfloat16>, grid, dim3(kRowThreads), 0, s, part, splits, split_stride,
                    n_active, x, d, eps, g1, static_cast<__nv_bfloat16*>(out1), g2, static_cast<__nv_bfloat16*>(out2));
+    EEB_CHECK_LAUNCH();
+}
+
+void launch_plane_sum(const float* part, int splits, int64_t split_stride, const int* n_active, int max_rows, int d,
+                      float* out, int num_sms, cudaStream_t s) {
+    int64_t blocks = ((int64_t)max_rows * d + 255) / 256;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    launch_pdl(plane_sum_kernel, dim3((unsigned)blocks), dim3(256), 0, s, part, splits, split_stride, n_active, d, out);
     EEB_CHECK_LAUNCH();
 }
 

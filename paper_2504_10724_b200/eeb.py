@@ -46,7 +46,7 @@ class _Desc(C.Structure):
         ("exit_coverage", C.POINTER(C.c_float)), ("design_th", C.c_float),
         ("dtype", C.c_int32), ("mlp_kind", C.c_int32), ("max_slots", C.c_int32),
         ("max_seq_len", C.c_int32), ("seed", C.c_uint64), ("rope_theta", C.c_float),
-        ("norm_eps", C.c_float),
+        ("norm_eps", C.c_float), ("tp_size", C.c_int32), ("tp_rank", C.c_int32),
     ]
 
 
@@ -148,6 +148,8 @@ class ModelDesc:
     seed: int = 20260819           # fixtures/gen_calibration.json:2
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
+    tp_size: int = 1               # tensor parallelism (C5); 1 = none
+    tp_rank: int = 0               # this context's shard; -1 = all shards in one context
 
     def replace(self, **kw) -> "ModelDesc":
         return dataclasses.replace(self, **kw)
@@ -176,7 +178,8 @@ class ModelDesc:
         d = _Desc(self.num_layers, self.d_model, self.n_heads, self.n_kv_heads, self.d_ffn, self.vocab,
                   len(self.exit_layers), C.cast(layers, C.POINTER(C.c_int32)),
                   C.cast(cov, C.POINTER(C.c_float)), self.design_th, self.dtype, self.mlp_kind,
-                  self.max_slots, self.max_seq_len, self.seed, self.rope_theta, self.norm_eps)
+                  self.max_slots, self.max_seq_len, self.seed, self.rope_theta, self.norm_eps,
+                  self.tp_size, self.tp_rank)
         return d, (layers, cov)
 
     def layer_weight_elems(self) -> int:
