@@ -183,6 +183,42 @@ def workload_config(args, desc):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
+def batch_sweep(ctx, eeb, desc, args, stream, batches=(1, 4, 16, 32, 64, 128, 256), n_steps=10):
+    """The metric is 'EE decode tokens/s vs batch': the same workload at each
+    batch (own model instance with a 256-slot KV pool, prompts prefilled)."""
+    import torch
+
+    P = args.prompt
+    d = desc.replace(max_slots=max(batches), max_seq_len=P + 100, name=desc.name + "-sweep")
+    m = ctx.register(d)
+    ctx.load_layers(m, d.num_layers)
+    policy = {"introspective": eeb.INTROSPECTIVE, "flat": eeb.FLAT}.get(args.policy, eeb.INTROSPECTIVE)
+    depth = args.depth if policy == eeb.FLAT else 0
+    rng = np.random.default_rng(77)
+    dev = torch.device("cuda")
+    out = []
+    for B in batches:
+        slots = np.arange(B, dtype=np.int32)
+        ctx.prefill(m, d.num_layers, slots, list(rng.integers(0, d.vocab, (B, P)).astype(np.int32)))
+        toks = torch.from_numpy(rng.integers(0, d.vocab, (n_steps + 3, B)).astype(np.int32)).to(dev)
+        pos = torch.from_numpy(np.stack([np.full(B, P + k, np.int32) for k in range(n_steps + 3)])).to(dev)
+        sl = torch.from_numpy(slots).to(dev)
+        torch.cuda.synchronize()
+        for k in range(3):
+            ctx.decode_step_device(m, depth, policy, args.th, B, sl.data_ptr(), toks[k].data_ptr(), pos[k].data_ptr())
+        ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(3, n_steps + 3):
+            ctx.decode_step_device(m, depth, policy, args.th, B, sl.data_ptr(), toks[k].data_ptr(), pos[k].data_ptr())
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / n_steps
+        out.append({"batch": B, "ms_per_step": ms, "tokens_per_s": B / (ms / 1000.0)})
+    ctx.evict(m)
+    return out
+
+
 def measure_loader(ctx, m, eeb, step, args, stream, depth=16, n_steps=20):
     """C3's switching partner: stage OPT-2.7B to pinned host memory, then load its
     first `depth` layers (+ base weights) asynchronously while the serving model
@@ -420,8 +456,12 @@ def run_eeb(args, desc):
 
     # ---- greedy loader: real pinned H2D of a second model's
     # first layers on the load stream, overlapped with this model's decode steps
-    loader = None
+    loader = sweep = None
     if rank == 0 and world == 1 and not args.no_secondary:
+        try:
+            sweep = batch_sweep(ctx, eeb, desc, args, stream)
+        except Exception as e:  # reported, never fatal for the headline line
+            sweep = {"error": repr(e)[:200]}
         try:
             loader = measure_loader(ctx, m, eeb, step, args, stream)
         except Exception as e:  # reported, never fatal for the headline line
@@ -468,6 +508,8 @@ def run_eeb(args, desc):
             line["secondary_c4"] = secondary
         if loader is not None:
             line["loader"] = loader
+        if sweep is not None:
+            line["batch_sweep"] = sweep
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

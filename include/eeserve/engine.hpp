@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "eeserve/backend.hpp"
+#include "eeserve/events.hpp"
 #include "eeserve/memory_model.hpp"
 #include "eeserve/pht.hpp"
 #include "eeserve/policy.hpp"
@@ -50,6 +51,7 @@ struct EngineConfig {
     int max_seq_len = 256;
     std::uint64_t token_seed = 20260819;
     bool prefill = true;  // run the prompt through the backend (real KV); off for trace replay
+    bool record_events = false;  // keep the reference-format event log (events.hpp) in the report
 };
 
 struct RequestTiming {  // ↔ the request's TTFT (engine.hpp:333-337) and its tokens' TPOT
@@ -75,6 +77,8 @@ struct EngineReport {
     std::int64_t load_bytes = 0;
     double prefill_s = 0.0;
     std::vector<RequestTiming> requests;
+    double mean_ttft_s = 0.0, mean_tpot_s = 0.0;
+    std::vector<EngineEvent> events;  // EngineConfig::record_events
     Pht pht;
 };
 
@@ -152,6 +156,11 @@ private:
     double sum_logprob_ = 0.0;
     std::int64_t unchanged_ = 0, unchanged_known_ = 0;
     double pending_stall_s_ = 0.0;  // loads charged to the next batch's TTFT (engine.hpp:205-207, :336)
+    double clock_ = 0.0;            // serving clock of the event log (s)
+
+    void emit(const char* kind, const JsonFields& f) {
+        if (cfg_.record_events) rep_.events.push_back({clock_, kind, f.body()});
+    }
 
     void do_load(const std::string& id, int target, const std::string& reason) {
         const int from = mem_.depth_of(id);
@@ -163,8 +172,19 @@ private:
         // shrink and eviction are free (engine.hpp:197-199)
         const double dur = target < from ? 0.0 : lr.seconds > 0.0 ? lr.seconds : load_seconds(modelled, cfg_.mem);
         rep_.load_s += dur;
-        rep_.load_bytes += lr.bytes > 0 ? lr.bytes : std::max<std::int64_t>(0, modelled);
+        const std::int64_t moved = lr.bytes > 0 ? lr.bytes : std::max<std::int64_t>(0, modelled);
+        rep_.load_bytes += moved;
         pending_stall_s_ += dur;
+        clock_ += dur;
+        emit("weights_load", JsonFields()
+                                 .str("model", id)
+                                 .i64("from_depth", from)
+                                 .i64("to_depth", target)
+                                 .i64("bytes", moved)
+                                 .num("duration_s", dur)
+                                 .str("reason", reason)
+                                 .i64("loaded_bytes_after", weights_loaded_bytes(mem_, repo_))
+                                 .num("energy_mwh", 0.0));
         if (reason == "breach_load_more") ++rep_.ld_count;
     }
 
@@ -186,8 +206,10 @@ private:
         pending_.reset();
         breach_.reset();
         since_eval_ = 0;
+        emit("reassess_start", JsonFields().i64("cycle", rep_.eval_cycles));
         for (const std::string& id : candidates_) {
             if (cursor_ >= reqs.size()) break;
+            emit("eval_phase_start", JsonFields().str("model", id));
             pht_.reset(id);
             load_for_eval(id);
             const ModelSpec& spec = repo_.at(id);
@@ -201,11 +223,15 @@ private:
                 served += (int)n;
                 serve_batch(batch, id, spec.num_layers, TokenPolicy::profile, true);
             }
+            emit("eval_phase_end", JsonFields().str("model", id));
         }
         std::vector<std::string> profiled;
         for (const auto& id : candidates_)
             if (pht_.has(id)) profiled.push_back(id);
-        if (profiled.empty()) return;
+        if (profiled.empty()) {
+            emit("reassess_end", JsonFields().i64("cycle", rep_.eval_cycles));
+            return;
+        }
         const ReplanResult plan = replan_after_eval(repo_, pht_, profiled, cfg_.policy, cfg_.mem);
         std::vector<std::string> drop;
         for (const auto& [id, d] : mem_.loaded_depth) {
@@ -216,8 +242,11 @@ private:
         }
         for (const auto& id : drop) do_load(id, 0, "reassess");
         for (const auto& [id, depth] : plan.residency) do_load(id, depth, "reassess");
+        if (!serving_.empty() && serving_ != plan.serving_model)
+            emit("model_switch", JsonFields().str("from", serving_).str("to", plan.serving_model).str("reason", "reassess"));
         serving_ = plan.serving_model;
         depth_ = plan.serving_depth;
+        emit("reassess_end", JsonFields().i64("cycle", rep_.eval_cycles));
     }
 
     void apply_pending() {  // engine.hpp:301-323
@@ -231,6 +260,8 @@ private:
                 if (mem_.depth_of(plan.model_id) < plan.serving_depth)
                     do_load(plan.model_id, plan.serving_depth, "breach_switch");
                 ++rep_.sw_count;
+                emit("model_switch",
+                     JsonFields().str("from", serving_).str("to", plan.model_id).str("reason", "breach_action"));
                 serving_ = plan.model_id;
             }
             depth_ = plan.serving_depth;
@@ -259,6 +290,7 @@ private:
         // Prefill (engine.hpp:333-341): the prompts' KV through the layers the
         // step will run (the serving depth in flat mode, all layers otherwise).
         // TTFT = the pending loader stall + the prefill (engine.hpp:336).
+        for (int i = 0; i < b; ++i) emit("request_start", JsonFields().i64("request_id", batch[i]->request_id));
         double prefill_s = 0.0;
         if (cfg_.prefill) {
             PrefillRows pr;
@@ -274,6 +306,13 @@ private:
         if (prefill_s <= 0.0)  // modelled (engine.hpp:333-334): prompt_len x depth x t_prefill
             prefill_s = (double)max_prompt * depth * spec.t_prefill_per_layer_per_token_s;
         rep_.prefill_s += prefill_s;
+        clock_ += prefill_s;
+        for (int i = 0; i < b; ++i)
+            emit("prefill", JsonFields()
+                                .i64("request_id", batch[i]->request_id)
+                                .str("model", model)
+                                .i64("depth", depth)
+                                .num("duration_s", prefill_s));
         const double ttft = pending_stall_s_ + prefill_s;
         pending_stall_s_ = 0.0;
         const size_t first_timing = rep_.requests.size();
@@ -297,12 +336,33 @@ private:
                 for (int x : o.exit_layer) deepest = std::max(deepest, x);
                 dur = deepest * spec.t_decode_per_layer_s;
             }
+            clock_ += dur;  // every row of the step is emitted at the step's end (one t_s)
+            for (int i = 0; i < rows.size(); ++i)
+                emit("token_emitted", JsonFields()
+                                          .i64("request_id", rows.request_ids[i])
+                                          .str("model", model)
+                                          .i64("exit_layer", o.exit_layer[i])
+                                          .boolean("breached", o.breached[i] != 0)
+                                          .boolean("unchanged", o.unchanged[i] == 1)
+                                          .num("duration_s", dur)
+                                          .num("logprob", o.obs[i].logprob)
+                                          .num("energy_mwh", o.exit_layer[i] * spec.energy_per_layer_per_token_mwh));
             consume(model, spec, tp, profile, rows, o, dur);
             for (int i = 0; i < b; ++i)
                 if (t < batch[i]->num_tokens) {
                     rep_.requests[first_timing + i].tpot_sum_s += dur;
                     rep_.requests[first_timing + i].tokens += 1;
                 }
+        }
+        for (int i = 0; i < b; ++i) {  // engine.hpp:387-395
+            const RequestTiming& rt = rep_.requests[first_timing + i];
+            const double tpot_mean = rt.tokens ? rt.tpot_sum_s / rt.tokens : 0.0;
+            emit("request_complete", JsonFields()
+                                         .i64("request_id", rt.request_id)
+                                         .num("ttft_s", rt.ttft_s)
+                                         .num("tpot_mean_s", tpot_mean)
+                                         .num("latency_s", rt.ttft_s + tpot_mean * (double)rt.tokens)
+                                         .i64("tokens", rt.tokens));
         }
     }
 
@@ -346,6 +406,14 @@ private:
             r.unchanged_fraction = unchanged_known_ ? (double)unchanged_ / (double)unchanged_known_ : 0.0;
             for (const auto& [m, per] : r.exit_counts)
                 for (const auto& [l, c] : per) r.exit_table[m][l] = 100.0 * (double)c / (double)r.tokens;
+        }
+        if (!r.requests.empty()) {
+            for (const auto& t : r.requests) {
+                r.mean_ttft_s += t.ttft_s;
+                r.mean_tpot_s += t.tokens ? t.tpot_sum_s / t.tokens : 0.0;
+            }
+            r.mean_ttft_s /= (double)r.requests.size();
+            r.mean_tpot_s /= (double)r.requests.size();
         }
         r.pht = pht_;
         return r;

@@ -126,6 +126,15 @@ int ref_simulate(const char* repo_json, const char* trace_jsonl, const char* mod
     });
 }
 
+// The reference's aggregate() (metrics.hpp:51-145) over an event log written
+// by our engine (events.jsonl): the report it rebuilds, as JSON.
+int ref_aggregate(const char* events_jsonl, char* out, int cap) {
+    return guard([&] {
+        const MetricsReport r = aggregate(read_event_log(events_jsonl));
+        return copy_out(metrics_report_to_json(r).dump(), out, cap);
+    });
+}
+
 // decide_action (policy.hpp:243-286) driven by a JSON description:
 // {"repo": path, "pht": {id: {layer: count}}, "candidates": [...], "current": id,
 //  "depth": d, "memory": {...}, "state": {id: depth}, "policy": {...}}

@@ -97,13 +97,24 @@ static void check_report(const EngineReport& rep, const std::vector<RequestSpec>
     CHECK(rep.prefill_s > 0.0);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const std::string events_path = argc > 1 ? argv[1] : "";
     const ModelRepository repo = make_repo();
     const auto reqs = make_requests(96);
     {  // HELIOS: eval cycles profile both candidates, replan, serve flat at the chosen depth
         CudaBackend be(0, /*host_tier=*/true);
-        BatchedEngine eng(repo, be, make_cfg(Mode::helios, ""));
+        EngineConfig cfg = make_cfg(Mode::helios, "");
+        cfg.record_events = !events_path.empty();
+        BatchedEngine eng(repo, be, cfg);
         const EngineReport rep = eng.run(reqs);
+        if (!events_path.empty()) {  // reference-format event log of a real GPU run (events.hpp)
+            write_event_log(rep.events, events_path);
+            std::printf("REPORT {\"throughput_tok_s\": %.17g, \"perplexity\": %.17g, \"mean_ttft_s\": %.17g, "
+                        "\"mean_tpot_s\": %.17g, \"achieved_batch_size\": %d, \"ld\": %lld, \"sw\": %lld, "
+                        "\"tokens\": %lld}\n",
+                        rep.throughput_tok_s, rep.perplexity, rep.mean_ttft_s, rep.mean_tpot_s, rep.achieved_batch_size,
+                        (long long)rep.ld_count, (long long)rep.sw_count, (long long)rep.tokens);
+        }
         check_report(rep, reqs);
         CHECK(rep.eval_cycles >= 2);
         CHECK(rep.load_bytes > 0 && rep.load_s > 0.0);

@@ -59,6 +59,7 @@ int ref_choose_depth(int, const int*, const int64_t*, int, double);
 int ref_simulate(const char*, const char*, const char*, const char*, const char*, char*, int);
 int ref_decide_action(const char*, char*, int);
 int ref_generate_trace(const char*, const char*, const char*);
+int ref_aggregate(const char*, char*, int);
 const char* ref_last_error();
 }
 
@@ -480,10 +481,36 @@ static void engine_matches_reference(const std::string& trace_path, const std::s
     cfg.mode = ModeSpec{mode, model};
     cfg.max_batch = 1;
     cfg.prefill = false;
+    cfg.record_events = true;
     BatchedEngine eng(repo, be, cfg);
     std::vector<RequestSpec> reqs;
     for (const auto& r : trace.requests) reqs.push_back({r.request_id, r.prompt_len, r.num_tokens()});
     const EngineReport rep = eng.run(reqs);
+    // Event-log parity: the reference's aggregate() over OUR event log must
+    // rebuild the reference simulate()'s own report (metrics.hpp:51-145).
+    {
+        const std::string log = "/tmp/eeserve_engine_events.jsonl";
+        write_event_log(rep.events, log);
+        std::vector<char> ab(1 << 24);
+        const int arc = ref_aggregate(log.c_str(), ab.data(), (int)ab.size());
+        CHECK(arc > 0);
+        if (arc > 0) {
+            const Json agg = Json::parse(ab.data());
+            const Json& a1 = agg.at("aggregates");
+            const Json& a0 = ref.at("report").at("aggregates");
+            for (const char* k : {"throughput_tok_s", "mean_ttft_s", "mean_tpot_s", "perplexity",
+                                  "energy_mwh_per_prompt", "unchanged_fraction"})
+                CHECK(approx(a1.at(k).get<double>(), a0.at(k).get<double>(), 1e-9));
+            CHECK(a1.at("achieved_batch_size") == a0.at("achieved_batch_size"));
+            CHECK(agg.at("action_counts") == ref.at("report").at("action_counts"));
+            CHECK(agg.at("exit_table").size() == ref.at("report").at("exit_table").size());
+            for (auto& [m, per] : ref.at("report").at("exit_table").items())
+                for (auto& [layer, pct] : per.items())
+                    CHECK(approx(agg.at("exit_table").at(m).at(layer).get<double>(), pct.get<double>(), 1e-12));
+            CHECK(agg.at("per_request").size() == ref.at("report").at("per_request").size());
+            CHECK(approx(a1.at("mean_ttft_s").get<double>(), rep.mean_ttft_s, 1e-9));
+        }
+    }
     const Json& et = ref.at("report").at("exit_table");
     int rows = 0;
     for (auto& [m, per] : et.items())
@@ -506,6 +533,46 @@ static void engine_matches_reference(const std::string& trace_path, const std::s
         CHECK(rep.pht.entry_of(m).token_count == e.at("token_count").get<int64_t>());
         CHECK(approx(*rep.pht.entry_of(m).perplexity(), e.at("perplexity").get<double>(), 1e-12));
     }
+}
+
+// Batched (width 4) run through the trace backend: the reference's aggregate()
+// over the engine's event log rebuilds the engine's own report, with a
+// decode step of 4 rows counted once (same t_s, metrics.hpp:85-93).
+TEST_CASE(event_log_aggregates_to_engine_report_at_batch_4) {
+    const std::string gen = "/tmp/eeserve_gen_small_b4.jsonl";
+    CHECK(ref_generate_trace(fx("gen_small.json").c_str(), fx("repo_opt.json").c_str(), gen.c_str()) == 10);
+    const ModelRepository repo = load_repo(fx("repo_opt.json"));
+    const Trace trace = load_trace(gen);
+    TraceBackend be(trace);
+    EngineConfig cfg;
+    cfg.mem = MemoryConfig{40'000'000'000, 1'000'000'000, 256, 8.4e9};
+    cfg.policy.k = 2;
+    cfg.mode = ModeSpec{Mode::helios, ""};
+    cfg.max_batch = 4;
+    cfg.prefill = false;
+    cfg.record_events = true;
+    BatchedEngine eng(repo, be, cfg);
+    std::vector<RequestSpec> reqs;
+    for (const auto& r : trace.requests) reqs.push_back({r.request_id, r.prompt_len, r.num_tokens()});
+    const EngineReport rep = eng.run(reqs);
+    const std::string log = "/tmp/eeserve_engine_events_b4.jsonl";
+    write_event_log(rep.events, log);
+    std::vector<char> ab(1 << 24);
+    CHECK(ref_aggregate(log.c_str(), ab.data(), (int)ab.size()) > 0);
+    const Json agg = Json::parse(ab.data());
+    const Json& a = agg.at("aggregates");
+    CHECK(approx(a.at("throughput_tok_s").get<double>(), rep.throughput_tok_s, 1e-9));
+    CHECK(approx(a.at("perplexity").get<double>(), rep.perplexity, 1e-12));
+    CHECK(approx(a.at("mean_ttft_s").get<double>(), rep.mean_ttft_s, 1e-9));
+    CHECK(approx(a.at("mean_tpot_s").get<double>(), rep.mean_tpot_s, 1e-9));
+    CHECK(a.at("achieved_batch_size").get<int>() == rep.achieved_batch_size);
+    CHECK(rep.achieved_batch_size == 4);
+    CHECK(agg.at("action_counts").at("ld").get<int64_t>() == rep.ld_count);
+    CHECK(agg.at("action_counts").at("sw").get<int64_t>() == rep.sw_count);
+    for (const auto& [m, per] : rep.exit_table)
+        for (const auto& [l, pct] : per)
+            CHECK(approx(agg.at("exit_table").at(m).at(std::to_string(l)).get<double>(), pct, 1e-12));
+    CHECK(agg.at("per_request").size() == reqs.size());
 }
 
 TEST_CASE(engine_replays_reference_traces_at_batch_1) {
