@@ -730,7 +730,7 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     int planes = 0;
     if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) planes = gemm_tc(a, c->stream);
     if (planes == 0) {
-        if (c->gemm_tier == 2 && m.desc.dtype == EEB_BF16 && batch >= 16 && gemm_tc_available())
+        if (c->gemm_tier == 2 && m.desc.dtype == EEB_BF16 && batch >= tc_min_rows() && gemm_tc_available())
             throw Error(EEB_E_DOMAIN, "tensor-core tier requested but not applicable");
         planes = gemm_cc(a, c->stream);
     }
@@ -1114,8 +1114,9 @@ void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int 
                                         std::to_string(m.loaded) + ")");
     if (d.dtype == EEB_F32 && batch > 64)
         throw Error(EEB_E_DOMAIN, "f32 parity model supports at most 64 rows per step");
-    if (m.tp > 1 && (batch < 16 || c->gemm_tier == 1 || c->retain_logits))
-        throw Error(EEB_E_DOMAIN, "tensor-parallel steps need the tensor-core tier (batch >= 16, no logit retention)");
+    if (m.tp > 1 && (batch < tc_min_rows() || c->gemm_tier == 1 || c->retain_logits))
+        throw Error(EEB_E_DOMAIN, "tensor-parallel steps need the tensor-core tier (batch >= " +
+                                      std::to_string(tc_min_rows()) + ", no logit retention)");
     (void)c;
 }
 

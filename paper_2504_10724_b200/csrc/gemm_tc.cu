@@ -364,6 +364,15 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int box_rows) {
 
 bool gemm_tc_available() { return encode_fn() != nullptr; }
 
+// Smallest batch the tensor-core tier takes (measured: the CUDA-core GEMV wins
+// at 1-2 rows, tcgen05 from 4 rows: 1.16 vs 1.52 ms per C2 step; rows are padded to UMMA N = 16;
+// the padding costs MMA issue slots only, the weight stream is the same).
+// EEB_TC_MIN_ROWS overrides (A/B against the CUDA-core GEMV).
+int tc_min_rows() {
+    static const int v = std::getenv("EEB_TC_MIN_ROWS") ? std::max(1, std::atoi(std::getenv("EEB_TC_MIN_ROWS"))) : 3;
+    return v;
+}
+
 void make_bf16_map(void* out_map, const void* ptr, int rows, int cols, int box_rows) {
     if (!encode_fn()) throw Error(5, "cuTensorMapEncodeTiled unavailable");
     *static_cast<CUtensorMap*>(out_map) = make_map(ptr, rows, cols, box_rows);
@@ -384,7 +393,7 @@ void make_kv_tensor_map(void* out_map, const void* base, int head_dim, int max_s
 }
 
 int gemm_tc(const GemmArgs& a, cudaStream_t s) {
-    if (a.dtype != 1 || a.max_rows < 16 || a.max_rows > 256 || a.K % kBK != 0) return 0;
+    if (a.dtype != 1 || a.max_rows < tc_min_rows() || a.max_rows > 256 || a.K % kBK != 0) return 0;
     if (!gemm_tc_available()) return 0;
     const int bpad = (a.max_rows + 15) / 16 * 16;
     const int tiles = (a.N + kBM - 1) / kBM;

@@ -72,6 +72,7 @@ int gemm_cc(const GemmArgs& a, cudaStream_t s);
 // Tier 2: tcgen05 + TMA (bf16, 16..256 rows).  Returns planes, 0 if not applicable.
 int gemm_tc(const GemmArgs& a, cudaStream_t s);
 bool gemm_tc_available();
+int tc_min_rows();
 // 2-D TMA map over a row-major bf16 [rows][cols] matrix, box {64 cols, box_rows},
 // 128-byte swizzle (the K-major UMMA operand layout).  out_map: 128 B.
 void make_bf16_map(void* out_map, const void* ptr, int rows, int cols, int box_rows);
