@@ -867,13 +867,36 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
                                  W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
         count(c, kCatNorm, 1);
     }
+    static const bool act_unfused = std::getenv("EEB_ACT_UNFUSED") != nullptr;  // A/B
     for (int sh = 0; sh < m.shards; ++sh) {
+        void* act_dst = static_cast<char*>(c->mlp_h.p) + (size_t)sh * batch * m.f_l * wb;
+        const void* wup = static_cast<const char*>(W.wup.p) + (size_t)sh * m.up_l * D * wb;
+        if (!act_unfused && !skip_cat("gemm") && d.dtype == EEB_BF16 && c->gemm_tier != 1) {
+            // up projection with the activation in its epilogue (one split)
+            Timer t(c, kCatGemm);
+            GemmArgs ga;
+            ga.dtype = d.dtype;
+            ga.W = wup;
+            ga.X = h;
+            ga.n_active = cur.n_active;
+            ga.max_rows = batch;
+            ga.N = m.up_l;
+            ga.K = D;
+            ga.out = nullptr;
+            ga.plane_stride = 0;
+            ga.max_planes = 1;
+            ga.num_sms = c->num_sms;
+            ga.act_out = act_dst;
+            ga.act_kind = d.mlp_kind == EEB_MLP_SWIGLU ? 2 : 1;
+            if (gemm_tc(ga, s) > 0) {
+                count(c, kCatGemm, 1);
+                continue;
+            }
+        }
         int up_planes;
         {
             Timer t(c, kCatGemm);
-            up_planes = skip_cat("gemm") ? 1
-                                         : gemm(c, kCatGemm, m, static_cast<const char*>(W.wup.p) + (size_t)sh * m.up_l * D * wb,
-                                                h, m.up_l, D, cur.n_active, batch);
+            up_planes = skip_cat("gemm") ? 1 : gemm(c, kCatGemm, m, wup, h, m.up_l, D, cur.n_active, batch);
         }
         Timer t(c, kCatNorm);
         if (!skip_cat("norm"))
@@ -1981,6 +2004,12 @@ eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int bat
         GemmArgs a;
         a.dtype = dtype; a.W = w.p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
         a.out = ws.as<float>(); a.plane_stride = plane; a.max_planes = max_planes; a.num_sms = c->num_sms;
+        if (tier == 2 && mode != 0 && dtype == EEB_BF16) {  // the step's path: activation fused in the epilogue
+            a.act_out = act.p;
+            a.act_kind = mode == 3 ? 2 : 1;
+            a.out = nullptr;
+            a.max_planes = 1;
+        }
         const int planes = tier == 2 ? gemm_tc(a, c->stream) : gemm_cc(a, c->stream);
         if (planes == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
         if (mode == 0) {  // fixed-order sum of the planes on the host
@@ -1994,8 +2023,9 @@ eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int bat
             }
             return;
         }
-        launch_act(dtype, ws.as<float>(), planes, plane, na.as<int>(), batch, n, mode == 3, act.p, c->num_sms,
-                   c->stream);
+        if (!a.act_out)
+            launch_act(dtype, ws.as<float>(), planes, plane, na.as<int>(), batch, n, mode == 3, act.p, c->num_sms,
+                       c->stream);
         EEB_CUDA(cudaStreamSynchronize(c->stream));
         std::vector<char> tmp((size_t)batch * n_out * es);
         EEB_CUDA(cudaMemcpy(tmp.data(), act.p, tmp.size(), cudaMemcpyDeviceToHost));

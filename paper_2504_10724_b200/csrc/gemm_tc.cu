@@ -137,6 +137,8 @@ struct TcParams {
     const int* n_active;
     float* part;       // split-K planes, row stride N
     int64_t split_stride;
+    __nv_bfloat16* act_out;  // fused MLP activation (splits == 1): bf16 [rows][N or N/2]
+    int act_kind;            // 1 ReLU, 2 SwiGLU over interleaved (gate, up) features
     float4* head_tri;  // exit-head epilogue (splits == 1): per (row, tile) {max, sumexp, argmax}
     int tiles;
     int vocab_off;     // added to the argmax (vocab-parallel shard)
@@ -279,6 +281,30 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
                 if (hf == 0 && r < lim) p.head_tri[(int64_t)r * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
             }
+        } else if (p.act_out) {
+            // Fused MLP activation: the up projection's tile goes straight to the
+            // down GEMM's bf16 input — no split-K planes, no activation kernel.
+            const int lim = min(rows, p.bpad);
+            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective
+                if (p.act_kind == 2) {
+                    const int half_n = p.N / 2;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const float u = __shfl_xor_sync(0xffffffffu, v[j], 1);  // odd lane: up, even: gate
+                        if ((lane & 1) == 0 && n < p.N && c0 + j < lim) {
+                            const float g = v[j];
+                            p.act_out[(int64_t)(c0 + j) * half_n + n / 2] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (n < p.N && c0 + j < lim)
+                            p.act_out[(int64_t)(c0 + j) * p.N + n] = __float2bfloat16_rn(fmaxf(v[j], 0.f));
+                }
+            }
         } else if (p.cs == 1) {
             float* plane = p.part + (int64_t)split * p.split_stride;
             for (int c0 = 0; c0 < p.bpad; c0 += 16) {
@@ -414,7 +440,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
             cs = c;
             break;
         }
-    if (a.head_tri) {  // the fused head tail needs whole-K tiles
+    if (a.head_tri || a.act_out) {  // the fused epilogues need whole-K tiles
         splits = 1;
         kb_per = kblocks;
     }
@@ -427,6 +453,11 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     if (stages < 2) stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (env_stages > 0) stages = std::min(env_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (stages < 2) return 0;
+    if (a.act_out) {
+        cs = 1;
+        static const int env_act_stages = std::getenv("EEB_ACT_STAGES") ? std::atoi(std::getenv("EEB_ACT_STAGES")) : 0;
+        if (env_act_stages > 0) stages = std::min(env_act_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
+    }
     if (a.head_tri) {
         cs = 1;
         // the transposed logits tile reuses the pipeline stages
@@ -451,6 +482,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.part = a.out;
     p.split_stride = a.plane_stride;
     p.head_tri = reinterpret_cast<float4*>(a.head_tri);
+    p.act_out = static_cast<__nv_bfloat16*>(a.act_out);
+    p.act_kind = a.act_kind;
     p.tiles = tiles;
     p.vocab_off = a.vocab_off;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);

@@ -65,7 +65,11 @@ struct GemmArgs {
     // vocab tile) partials {max, sum exp(l - max), argmax} to head_tri[row *
     // tiles + tile] (float4, argmax as int bits); decide merges them.
     float* head_tri = nullptr;
-    int vocab_off = 0;  // global id of this shard's first vocabulary row (vocab-parallel heads)
+    int vocab_off = 0;
+    // Fused MLP activation (tier 2 only): write act(y) as bf16 [rows][N] (ReLU,
+    // act_kind 1) or [rows][N/2] (SwiGLU over interleaved gate/up, act_kind 2).
+    void* act_out = nullptr;
+    int act_kind = 0;  // global id of this shard's first vocabulary row (vocab-parallel heads)
 };
 // Tier 1: CUDA cores (any dtype, <= 64 rows).  Returns the planes written.
 int gemm_cc(const GemmArgs& a, cudaStream_t s);
