@@ -163,6 +163,9 @@ struct eeb_ctx {
     int graphs_enabled = 1;
     int gemm_tier = 0;
     int retain_logits = 0;
+    // the next tensor-core GEMM's weights, prefetched into L2 by the current one
+    const void* pf_ptr = nullptr;
+    size_t pf_bytes = 0;
     // step workspace (grow-only)
     int cap_rows = 0;
     eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
@@ -727,6 +730,10 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     a.out = c->ws.as<float>() + (int64_t)plane0 * a.plane_stride;
     a.max_planes = (int)std::min<int64_t>(64, c->ws_elems / a.plane_stride - plane0);
     a.num_sms = c->num_sms;
+    a.pf = c->pf_ptr;
+    a.pf_bytes = c->pf_bytes;
+    c->pf_ptr = nullptr;
+    c->pf_bytes = 0;
     int planes = 0;
     if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) planes = gemm_tc(a, c->stream);
     if (planes == 0) {
@@ -807,8 +814,16 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
     float* ws = c->ws.as<float>();
     const size_t wb = m.wbytes;
     const int qkv_l = m.dq_l + 2 * m.dkv_l;
+    // L2 prefetch chain (one context shard only): each GEMM pulls the next
+    // GEMM's weights into L2 — QKV -> O -> up -> down -> next layer's QKV.
+    const bool pf_on = m.shards == 1;
+    auto next_pf = [&](const void* p, size_t bytes) {
+        c->pf_ptr = pf_on && p ? p : nullptr;
+        c->pf_bytes = pf_on && p ? bytes : 0;
+    };
     for (int sh = 0; sh < m.shards; ++sh) {
         int planes;
+        next_pf(W.wo.p, (size_t)D * m.dq_l * wb);
         {
             Timer t(c, kCatGemm);
             planes = skip_cat("gemm") ? 1
@@ -850,6 +865,7 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         count(c, kCatAttn, 1);
     }
     int planes = 0;
+    next_pf(W.wup.p, (size_t)m.up_l * D * wb);
     {
         Timer t(c, kCatGemm);
         for (int sh = 0; sh < m.shards; ++sh)
@@ -888,6 +904,10 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
             ga.num_sms = c->num_sms;
             ga.act_out = act_dst;
             ga.act_kind = d.mlp_kind == EEB_MLP_SWIGLU ? 2 : 1;
+            if (pf_on && W.wdown.p) {
+                ga.pf = W.wdown.p;
+                ga.pf_bytes = (size_t)D * m.f_l * wb;
+            }
             if (gemm_tc(ga, s) > 0) {
                 count(c, kCatGemm, 1);
                 continue;
@@ -906,6 +926,8 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         count(c, kCatNorm, 1);
     }
     planes = 0;
+    if (l < (int)m.layers.size() && m.layers[l])
+        next_pf(m.layers[l]->wqkv.p, (size_t)qkv_l * D * wb);
     {
         Timer t(c, kCatGemm);
         for (int sh = 0; sh < m.shards; ++sh)
@@ -2128,8 +2150,13 @@ eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, i
         a.dtype = EEB_BF16; a.W = wv[0]->p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
         a.out = ws.as<float>(); a.plane_stride = plane; a.max_planes = max_planes; a.num_sms = c->num_sms;
         int it = 0;
+        static const bool bench_pf = std::getenv("EEB_BENCH_PF") != nullptr;  // + L2 prefetch of the next copy
         auto run = [&] {
             a.W = wv[it++ % nbuf]->p;
+            if (bench_pf) {
+                a.pf = wv[it % nbuf]->p;
+                a.pf_bytes = wbytes;
+            }
             if (tier == 2) {
                 if (gemm_tc(a, c->stream) == 0) throw Error(EEB_E_DOMAIN, "tensor-core tier not applicable");
             } else {

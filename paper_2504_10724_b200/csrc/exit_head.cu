@@ -115,12 +115,22 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
                 const int r = t / a.head_tiles;
                 return tri[r * a.head_shard_stride + (t - r * a.head_tiles)];
             };
+            // kPre partials per lane are loaded at once (one L2 latency per
+            // chunk, not one per tile); same per-lane order as a strided scan
+            constexpr int kPre = 8;
             float m = -INFINITY;
             int am = 0x7fffffff;
-            for (int t = lane; t < tiles; t += 32) {
-                const float4 v = at(t);
-                const int ai = __float_as_int(v.z);
-                if (v.x > m || (v.x == m && ai < am)) { m = v.x; am = ai; }
+            for (int t0 = lane; t0 < tiles; t0 += 32 * kPre) {
+                float4 pre[kPre];
+#pragma unroll
+                for (int k = 0; k < kPre; ++k)
+                    pre[k] = t0 + 32 * k < tiles ? at(t0 + 32 * k)
+                                                 : make_float4(-INFINITY, 0.f, __int_as_float(0x7fffffff), 0.f);
+#pragma unroll
+                for (int k = 0; k < kPre; ++k) {
+                    const int ai = __float_as_int(pre[k].z);
+                    if (pre[k].x > m || (pre[k].x == m && ai < am)) { m = pre[k].x; am = ai; }
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -129,9 +139,14 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
                 if (m2 > m || (m2 == m && a2 < am)) { m = m2; am = a2; }
             }
             float sum = 0.f;
-            for (int t = lane; t < tiles; t += 32) {
-                const float4 v = at(t);
-                sum += v.y * __expf(v.x - m);
+            for (int t0 = lane; t0 < tiles; t0 += 32 * kPre) {
+                float4 pre[kPre];
+#pragma unroll
+                for (int k = 0; k < kPre; ++k)
+                    pre[k] = t0 + 32 * k < tiles ? at(t0 + 32 * k) : make_float4(-INFINITY, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < kPre; ++k)
+                    if (t0 + 32 * k < tiles) sum += pre[k].y * __expf(pre[k].x - m);
             }
             sum = warp_sum(sum);
             if (lane == 0) {

@@ -142,6 +142,8 @@ struct TcParams {
     float4* head_tri;  // exit-head epilogue (splits == 1): per (row, tile) {max, sumexp, argmax}
     int tiles;
     int vocab_off;     // added to the argmax (vocab-parallel shard)
+    const char* pf;    // next GEMM's weights: L2 prefetch, this CTA's share
+    size_t pf_bytes;
 };
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -189,17 +191,34 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
+        const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+        const int pre = min(S, nkb);
         if (lane == 0) {
-            const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
             // Weights do not depend on the previous kernel: fill the first
             // stages with weight tiles before waiting on it (PDL), then add the
             // activation tiles once the predecessor's output is visible.
-            const int pre = min(S, nkb);
             for (int i = 0; i < pre; ++i) {
                 const uint32_t sa = base + (uint32_t)i * stage_bytes;
                 mbar_expect_tx(full0 + 8 * i, stage_bytes);
                 tma_load_2d(sa, &tmap_w, full0 + 8 * i, (kb0 + i) * kBK, m_tile * kBM, pol_w);
             }
+        }
+        __syncwarp();
+        if (lane != 0 && p.pf_bytes) {
+            // lanes 1..31, behind this CTA's own first tiles: its share of the
+            // next GEMM's weights -> L2
+            const size_t nct = (size_t)gridDim.x * gridDim.y;
+            const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+            const size_t share = ((p.pf_bytes + nct - 1) / nct + 15) & ~(size_t)15;
+            const size_t b0 = cta * share, b1 = min(p.pf_bytes, b0 + share);
+            constexpr size_t kPiece = 16384;
+            for (size_t o = b0 + (size_t)(lane - 1) * kPiece; o < b1; o += 31 * kPiece) {
+                const uint32_t n = (uint32_t)min(kPiece, b1 - o) & ~15u;
+                if (n)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf + o), "r"(n) : "memory");
+            }
+        }
+        if (lane == 0) {
             pdl_wait();
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,
@@ -246,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
-        if (p.head_tri) {
+        if (p.head_tri && p.cs == 1) {
             // Fused exit-head tail: stage the [rows x 128 vocab] logits tile
             // transposed in the drained pipeline smem, then two threads per row
             // scan 64 entries each for max / first argmax / sum exp(l - max).
@@ -281,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
                 if (hf == 0 && r < lim) p.head_tri[(int64_t)r * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
             }
-        } else if (p.act_out) {
+        } else if (p.act_out && p.cs == 1) {
             // Fused MLP activation: the up projection's tile goes straight to the
             // down GEMM's bf16 input — no split-K planes, no activation kernel.
             const int lim = min(rows, p.bpad);
@@ -331,25 +350,93 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (p.cs > 1) {
         // Split-K reduction on chip: the cs CTAs of a cluster hold consecutive
         // k-ranges of one tile; CTA rank r sums rows r, r+cs, ... of the tile
-        // over the cluster's smem partials in rank (= k) order and writes one
-        // plane per cluster — cs x fewer partial planes in HBM/L2 and for the
-        // consumers to read.  Deterministic (fixed order).
+        // over the cluster's smem partials in rank (= k) order (deterministic)
+        // and finishes them: one plane per cluster (cs x fewer partial planes
+        // for the consumers to read), or the fused MLP activation, or the
+        // exit-head softmax partials — the fused epilogues get the SM coverage
+        // of split-K without a round trip through HBM/L2.
         cg::cluster_group cluster = cg::this_cluster();
         cluster.sync();
+        const int rank = (int)cluster.block_rank();
+        const int rows = *p.n_active;
+        const int lim = min(rows, p.bpad);
+        const float* red = reinterpret_cast<const float*>(base_ptr);
+        // this rank's finished rows (head mode), after the staged partials
+        float* fin = reinterpret_cast<float*>(base_ptr) + (size_t)p.bpad * (kBM + 1);
         if (warp >= 2) {
-            const int rank = (int)cluster.block_rank();
-            const int rows = *p.n_active;
             const int t = threadIdx.x - 64;  // 0..127: feature of the tile
             const int n = m_tile * kBM + t;
             float* plane = p.part + (int64_t)(split / p.cs) * p.split_stride;
-            const float* red = reinterpret_cast<const float*>(base_ptr);
-            for (int row = rank; row < min(rows, p.bpad); row += p.cs) {
-                float acc = 0.f;
-                for (int q = 0; q < p.cs; ++q) acc += cluster.map_shared_rank(red, q)[row * (kBM + 1) + t];
-                if (n < p.N) plane[(int64_t)row * p.N + n] = acc;
+            const float* peer[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) peer[q] = cluster.map_shared_rank(red, q < p.cs ? q : 0);
+            // kR rows x cs peers of DSMEM loads in flight at once (a
+            // row-at-a-time loop pays one DSMEM round trip per load);
+            // warp-uniform trip counts (the SwiGLU pairing shuffles)
+            constexpr int kR = 4;
+            for (int j0 = 0; rank + j0 * p.cs < lim; j0 += kR) {
+                float v[kR][8];
+#pragma unroll
+                for (int r = 0; r < kR; ++r) {
+                    const int row = rank + (j0 + r) * p.cs;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        v[r][q] = (q < p.cs && row < lim) ? peer[q][row * (kBM + 1) + t] : 0.f;
+                }
+#pragma unroll
+                for (int r = 0; r < kR; ++r) {
+                    const int j = j0 + r;
+                    const int row = rank + j * p.cs;
+                    if (row >= lim) break;
+                    float acc = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (q < p.cs) acc += v[r][q];
+                    if (p.head_tri) {
+                        fin[j * (kBM + 1) + t] = acc;
+                    } else if (p.act_out) {
+                        if (p.act_kind == 2) {
+                            const float u = __shfl_xor_sync(0xffffffffu, acc, 1);  // odd lane: up, even: gate
+                            if ((t & 1) == 0 && n < p.N)
+                                p.act_out[(int64_t)row * (p.N / 2) + n / 2] =
+                                    __float2bfloat16_rn(acc / (1.f + __expf(-acc)) * u);
+                        } else if (n < p.N) {
+                            p.act_out[(int64_t)row * p.N + n] = __float2bfloat16_rn(fmaxf(acc, 0.f));
+                        }
+                    } else if (n < p.N) {
+                        plane[(int64_t)row * p.N + n] = acc;
+                    }
+                }
             }
         }
         cluster.sync();  // keep every CTA's partial alive until the whole cluster has read it
+        if (p.head_tri && warp >= 2) {
+            // two threads per finished row scan 64 vocab entries each
+            const int t = threadIdx.x - 64, hf = t & 1;
+            const int n0 = m_tile * kBM + hf * 64;
+            const int nv = max(0, min(64, p.N - n0));
+            const int nmine = lim > rank ? (lim - rank + p.cs - 1) / p.cs : 0;
+            for (int j0 = 0; j0 < nmine; j0 += 64) {
+                const int j = j0 + (t >> 1);
+                const int nvr = j < nmine ? nv : 0;
+                const float* src = fin + min(j, max(nmine - 1, 0)) * (kBM + 1) + hf * 64;
+                float m = -INFINITY;
+                int am = 0x7fffffff;
+                for (int q = 0; q < nvr; ++q)
+                    if (src[q] > m) { m = src[q]; am = n0 + q; }
+                float sum = 0.f;
+                for (int q = 0; q < nvr; ++q) sum += __expf(src[q] - m);
+                const float m2 = __shfl_xor_sync(0xffffffffu, m, 1);
+                const int a2 = __shfl_xor_sync(0xffffffffu, am, 1);
+                const float s2 = __shfl_xor_sync(0xffffffffu, sum, 1);
+                const float M = fmaxf(m, m2);
+                const int A = (m2 > m || (m2 == m && a2 < am)) ? a2 : am;
+                const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
+                const int row = rank + j * p.cs;
+                if (hf == 0 && j < nmine)
+                    p.head_tri[(int64_t)row * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -440,11 +527,33 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
             cs = c;
             break;
         }
-    if (a.head_tri || a.act_out) {  // the fused epilogues need whole-K tiles
-        splits = 1;
-        kb_per = kblocks;
+    if (a.head_tri || a.act_out) {
+        // The fused epilogues need whole-K tiles: one CTA per tile, or a
+        // cluster of cs CTAs splitting K whose partials are reduced on chip
+        // (DSMEM) so that the grid still covers the SMs.
+        // measured (C2): the up projection gains from clustering (64 tiles ->
+        // 4-CTA clusters), the exit head does not; EEB_ACT_CS / EEB_HEAD_CS override.
+        static const int env_act_cs = std::getenv("EEB_ACT_CS") ? std::atoi(std::getenv("EEB_ACT_CS")) : -1;
+        static const int env_head_cs = std::getenv("EEB_HEAD_CS") ? std::atoi(std::getenv("EEB_HEAD_CS")) : 1;
+        const int env_fcs = a.head_tri ? env_head_cs : env_act_cs;
+        // cs: the best wave efficiency tiles*cs / (waves * wave), ties to the
+        // smaller cluster (e.g. C2 up-proj 64 tiles -> 4, C2 head 393 -> 2).
+        cs = 1;
+        double best = 0.0;
+        for (int c = 1; c <= 8; ++c) {
+            if (kblocks % c != 0 || (c > 1 && kblocks / c < 2)) continue;
+            if (env_fcs >= 1 && c != env_fcs) continue;
+            const int units = tiles * c;
+            const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
+            if (eff > best + 0.02) {
+                best = eff;
+                cs = c;
+            }
+        }
+        splits = cs;
+        kb_per = kblocks / cs;
     }
-    if (splits > a.max_planes) return 0;  // (cs may still fall back to 1 below)
+    if (splits / cs > a.max_planes) return 0;
     const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
     // ~half the SM's shared memory so two GEMM CTAs co-reside: the next GEMM of
     // the step (PDL) streams its weights while this one drains.
@@ -453,18 +562,25 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     if (stages < 2) stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (env_stages > 0) stages = std::min(env_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (stages < 2) return 0;
+    if (a.head_tri) {
+        // measured (gemm_sweep, C2 head 50272 x 2048): 3 stages -> 3 CTAs per SM
+        // stream the head at 88% of HBM peak vs 77% with 4 stages / 2 per SM
+        static const int env_head_stages = std::getenv("EEB_HEAD_STAGES") ? std::atoi(std::getenv("EEB_HEAD_STAGES")) : 3;
+        if (env_head_stages > 0) stages = std::min(env_head_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
+    }
     if (a.act_out) {
-        cs = 1;
         static const int env_act_stages = std::getenv("EEB_ACT_STAGES") ? std::atoi(std::getenv("EEB_ACT_STAGES")) : 0;
         if (env_act_stages > 0) stages = std::min(env_act_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     }
-    if (a.head_tri) {
+    // smem the epilogue reuses from the drained pipeline stages: the staged
+    // [bpad][129] f32 partial (cs > 1) or logits tile (head), plus the head's
+    // finished rows when the head is split
+    const size_t red_bytes = (size_t)bpad * (kBM + 1) * 4;
+    const size_t need = (cs > 1 || a.head_tri) ? red_bytes * (a.head_tri && cs > 1 ? 2 : 1) : 0;
+    while (need > (size_t)stages * stage_bytes && stages < 8) ++stages;
+    if (need > (size_t)stages * stage_bytes || 1024 + (size_t)stages * stage_bytes + 256 > (size_t)kSmemBudget) {
+        if (a.head_tri || a.act_out) return 0;
         cs = 1;
-        // the transposed logits tile reuses the pipeline stages
-        while ((size_t)bpad * (kBM + 1) * 4 > (size_t)stages * stage_bytes && stages < 8) ++stages;
-        if ((size_t)bpad * (kBM + 1) * 4 > (size_t)stages * stage_bytes ||
-            1024 + (size_t)stages * stage_bytes + 256 > (size_t)kSmemBudget)
-            return 0;
     }
     int tmem_cols = 32;
     while (tmem_cols < bpad) tmem_cols *= 2;
@@ -486,11 +602,12 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.act_kind = a.act_kind;
     p.tiles = tiles;
     p.vocab_off = a.vocab_off;
+    static const bool no_pf = std::getenv("EEB_L2PF") && std::atoi(std::getenv("EEB_L2PF")) == 0;
+    p.pf = no_pf ? nullptr : static_cast<const char*>(a.pf);
+    p.pf_bytes = no_pf || !a.pf ? 0 : a.pf_bytes;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
-    // the reduction buffer [bpad][129] f32 reuses the (drained) pipeline stages
-    if (cs > 1 && (size_t)bpad * (kBM + 1) * 4 > (size_t)stages * stage_bytes) cs = 1;
     p.cs = cs;
     EEB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(tiles, splits);
@@ -507,7 +624,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     attr[1].val.clusterDim.y = cs;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = cs > 1 ? 2 : 1;  // no cluster attribute unless clustering (launch cost)
     EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p));
     return splits / cs;
 }

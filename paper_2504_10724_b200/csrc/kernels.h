@@ -70,6 +70,11 @@ struct GemmArgs {
     // act_kind 1) or [rows][N/2] (SwiGLU over interleaved gate/up, act_kind 2).
     void* act_out = nullptr;
     int act_kind = 0;  // global id of this shard's first vocabulary row (vocab-parallel heads)
+    // L2 prefetch of the NEXT GEMM's weights (tier 2): issued by this GEMM's
+    // CTAs right after their own first weight tiles, so the HBM stream stays
+    // busy through this GEMM's tail and the non-GEMM kernels in between.
+    const void* pf = nullptr;
+    size_t pf_bytes = 0;
 };
 // Tier 1: CUDA cores (any dtype, <= 64 rows).  Returns the planes written.
 int gemm_cc(const GemmArgs& a, cudaStream_t s);

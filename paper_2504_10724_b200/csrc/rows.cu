@@ -5,11 +5,9 @@
 // Fusing the split-K reduction into these consumers removes a launch per
 // GEMM and produces the next GEMM's normalised bf16 input in the same pass
 // over the row (the residual stream stays f32).
-#include <cooperative_groups.h>
+#include <algorithm>
 
 #include "kernels.h"
-
-namespace cg = cooperative_groups;
 
 namespace eeb {
 
@@ -35,65 +33,86 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // x[i] (+)= sum_s part[s][i]; out1 = T(x * inv_rms * g1); out2 likewise with g2.
-// A cluster of kClusterRow CTAs owns one row: each sums its column slice of the
-// split-K planes (many independent loads in flight), the row's sum of squares
-// is combined through distributed shared memory in rank order (deterministic),
-// and each CTA normalises its slice.  part == null: x is taken as is.
-constexpr int kClusterRow = 8;
+// One CTA per row (no cluster: a cluster launch costs ~1.5 us more per kernel
+// in the step's graph than the whole row's work, tools/micro/rows_bench.cu).
+// A thread owns kV float4 column groups; the planes are read kBatch at a time
+// into registers before they are added (in plane order, so the sum equals a
+// sequential one): one L2 round trip per kBatch planes, not one per plane.
+// The row's sum of squares is a fixed-tree block reduction (deterministic).
+// part == null: x is taken as is.
+constexpr int kBatch = 8;
+constexpr int kNormThreads = 512;
 
 template <typename T>
-__global__ void __cluster_dims__(kClusterRow, 1, 1) __launch_bounds__(kRowThreads)
+__device__ __forceinline__ void store4(T* dst, float4 v);
+template <>
+__device__ __forceinline__ void store4<float>(float* dst, float4 v) {
+    *reinterpret_cast<float4*>(dst) = v;
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float4 v) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(dst) = u;
+}
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+
+template <typename T, int kV>
+__global__ void __launch_bounds__(kNormThreads)
     residual_norm_kernel(const float* part, int splits, int64_t split_stride,
                          const int* n_active, float* x, int d, float eps,
                          const float* g1, T* out1, const float* g2,
                          T* out2) {
     pdl_launch_dependents();
     pdl_wait();
-    cg::cluster_group cluster = cg::this_cluster();
-    const int rank = (int)cluster.block_rank();
-    const int i = blockIdx.x / kClusterRow;
-    const bool live = i < *n_active;  // uniform over the cluster
+    const int i = blockIdx.x;
+    if (i >= *n_active) return;
     __shared__ float red[32];
-    __shared__ float ss_slice;
-    const int per = d / kClusterRow;
-    const int c0 = rank * per;
     float* row = x + (int64_t)i * d;
-    constexpr int kMaxCols = 8;  // per thread: d <= 8 * 8 * 256
-    float v[kMaxCols];
+    float4 v[kV];
     float ss = 0.f;
-    if (live) {
 #pragma unroll
-        for (int k = 0; k < kMaxCols; ++k) {
-            const int c = c0 + threadIdx.x + k * kRowThreads;
-            v[k] = 0.f;
-            if (threadIdx.x + k * kRowThreads < per) {
-                float xv = row[c];
-                if (part) {
-                    float y = 0.f;
-                    for (int s = 0; s < splits; ++s) y += part[s * split_stride + (int64_t)i * d + c];
-                    xv += y;
-                    row[c] = xv;
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < d) {
+            float4 xv = *reinterpret_cast<const float4*>(row + c);
+            if (part) {
+                const float* src = part + (int64_t)i * d + c;
+                float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int s0 = 0; s0 < splits; s0 += kBatch) {
+                    float4 t[kBatch];
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j)
+                        if (s0 + j < splits) t[j] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + j) * split_stride));
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j)
+                        if (s0 + j < splits) add4(y, t[j]);
                 }
-                v[k] = xv;
-                ss += xv * xv;
+                add4(xv, y);
+                *reinterpret_cast<float4*>(row + c) = xv;
             }
+            v[k] = xv;
+            ss += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
         }
     }
     ss = block_sum(ss, red);
-    if (threadIdx.x == 0) ss_slice = ss;
-    cluster.sync();
-    float tot = 0.f;
-    for (int r = 0; r < kClusterRow; ++r) tot += *cluster.map_shared_rank(&ss_slice, r);
-    cluster.sync();  // keep every slice alive until all ranks have read it
-    if (!live) return;
-    const float inv = rsqrtf(tot / (float)d + eps);
+    const float inv = rsqrtf(ss / (float)d + eps);
 #pragma unroll
-    for (int k = 0; k < kMaxCols; ++k) {
-        const int c = c0 + threadIdx.x + k * kRowThreads;
-        if (threadIdx.x + k * kRowThreads < per) {
-            const float nv = v[k] * inv;
-            out1[(int64_t)i * d + c] = from_f32<T>(nv * g1[c]);
-            if (out2) out2[(int64_t)i * d + c] = from_f32<T>(nv * g2[c]);
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        if (c < d) {
+            const float4 gg = *reinterpret_cast<const float4*>(g1 + c);
+            const float4 nv = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
+            store4<T>(out1 + (int64_t)i * d + c, make_float4(nv.x * gg.x, nv.y * gg.y, nv.z * gg.z, nv.w * gg.w));
+            if (out2) {
+                const float4 g = *reinterpret_cast<const float4*>(g2 + c);
+                store4<T>(out2 + (int64_t)i * d + c, make_float4(nv.x * g.x, nv.y * g.y, nv.z * g.z, nv.w * g.w));
+            }
         }
     }
 }
@@ -190,15 +209,27 @@ void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
                           void* out2, cudaStream_t s) {
-    if (d % kClusterRow != 0 || d / kClusterRow > 8 * kRowThreads)
-        throw Error(1, "residual_norm: d_model must be a multiple of 8 and at most 16384");
-    const dim3 grid(max_rows * kClusterRow);
-    if (dtype == 0)
-        launch_pdl(residual_norm_kernel<float>, grid, dim3(kRowThreads), 0, s, part, splits, split_stride, n_active, x,
-                   d, eps, g1, static_cast<float*>(out1), g2, static_cast<float*>(out2));
-    else
-        launch_pdl(residual_norm_kernel<__nv_bfloat16>, grid, dim3(kRowThreads), 0, s, part, splits, split_stride,
-                   n_active, x, d, eps, g1, static_cast<__nv_bfloat16*>(out1), g2, static_cast<__nv_bfloat16*>(out2));
+    const int q = d / 4;  // float4 groups per row
+    if (d % 4 != 0 || q > 4 * kNormThreads)
+        throw Error(1, "residual_norm: d_model must be a multiple of 4 and at most 8192");
+    const int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
+    const dim3 grid(max_rows), block(std::max(32, std::min(kNormThreads, (q / kv + 31) / 32 * 32)));
+    auto go = [&](auto kern, auto* o1, auto* o2) {
+        launch_pdl(kern, grid, block, 0, s, part, splits, split_stride, n_active, x, d, eps, g1, o1, g2, o2);
+    };
+    if (dtype == 0) {
+        float* o1 = static_cast<float*>(out1);
+        float* o2 = static_cast<float*>(out2);
+        if (kv == 1) go(residual_norm_kernel<float, 1>, o1, o2);
+        else if (kv == 2) go(residual_norm_kernel<float, 2>, o1, o2);
+        else go(residual_norm_kernel<float, 4>, o1, o2);
+    } else {
+        __nv_bfloat16* o1 = static_cast<__nv_bfloat16*>(out1);
+        __nv_bfloat16* o2 = static_cast<__nv_bfloat16*>(out2);
+        if (kv == 1) go(residual_norm_kernel<__nv_bfloat16, 1>, o1, o2);
+        else if (kv == 2) go(residual_norm_kernel<__nv_bfloat16, 2>, o1, o2);
+        else go(residual_norm_kernel<__nv_bfloat16, 4>, o1, o2);
+    }
     EEB_CHECK_LAUNCH();
 }
 
