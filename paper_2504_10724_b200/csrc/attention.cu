@@ -285,12 +285,11 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
     return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-template <int HD>
+template <int HD, int CP>  // CP: positions per chunk (one chunk in smem at a time)
 __global__ void __launch_bounds__(kMmaWarps * 32)
     attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          AttnArgs a) {
     constexpr int CB = HD / 64;                    // 64-dim column blocks
-    constexpr int CP = HD == 64 ? 256 : 128;       // positions per chunk
     constexpr int NT = HD / 8;                     // 8-dim n-tiles of O
     constexpr int KS = HD / 16;                    // 16-dim k-steps of Q.K
     constexpr int TPW = CP / 8 / kMmaWarps;        // position tiles per warp per chunk
@@ -981,19 +980,33 @@ __global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
     if (i < rows) kv_depth[(int64_t)slot[i] * max_seq + pos[i]] = (uint8_t)depth;
 }
 
-template <int HD>
-void launch_mma(const AttnArgs& a, cudaStream_t s) {
-    constexpr int CB = HD / 64, CP = HD == 64 ? 256 : 128;
+template <int HD, int CP>
+void launch_mma_cp(const AttnArgs& a, cudaStream_t s) {
+    constexpr int CB = HD / 64;
     const int G = a.n_heads / a.n_kv_heads;
     if (a.splits > 16) throw Error(1, "attention: more than 16 QKV split-K planes");
     const size_t smem = 1024 + 2 * (size_t)CB * CP * 128 + (8 + G + 2) * HD * 4;
-    auto kern = attention_mma_kernel<HD>;
+    auto kern = attention_mma_kernel<HD, CP>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // x = kv head, y = row: the live rows' CTAs come first in launch order
     dim3 grid(a.n_kv_heads, a.max_rows);
     launch_pdl(kern, grid, dim3(kMmaWarps * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a);
     EEB_CHECK_LAUNCH();
+}
+
+// Chunk size: the whole context of a (row, kv head) in one chunk keeps one
+// TMA round trip per CTA; a smaller chunk fits more CTAs per SM (more loads
+// in flight, prologues overlapping other CTAs' loads).  EEB_ATTN_CP overrides.
+template <int HD>
+void launch_mma(const AttnArgs& a, cudaStream_t s) {
+    static const int env_cp = std::getenv("EEB_ATTN_CP") ? std::atoi(std::getenv("EEB_ATTN_CP")) : 0;
+    // measured C2 (hd 64, context 128..227): 64 positions 1.56 ms/step, 128 1.61, 256 1.64
+    const int cp = env_cp > 0 ? env_cp : (HD == 64 ? 64 : 128);
+    if (cp <= 32) launch_mma_cp<HD, 32>(a, s);
+    else if (cp <= 64) launch_mma_cp<HD, 64>(a, s);
+    else if (cp <= 128) launch_mma_cp<HD, 128>(a, s);
+    else launch_mma_cp<HD, 256>(a, s);
 }
 
 }  // namespace

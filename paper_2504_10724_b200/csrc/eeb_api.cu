@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -2168,7 +2169,21 @@ eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, i
         EEB_CUDA(cudaEventCreate(&e0));
         EEB_CUDA(cudaEventCreate(&e1));
         EEB_CUDA(cudaEventRecord(e0, c->stream));
-        for (int i = 0; i < iters; ++i) run();
+        // EEB_GEMM_TRACE=path: globaltimer stamps of every CTA of two consecutive
+        // mid-chain launches (u64 [2][ctas][8]) written to path
+        static const char* trace_path = std::getenv("EEB_GEMM_TRACE");
+        DevBuf trace;
+        const size_t tr_per = (size_t)8 * 2048;
+        if (trace_path) {
+            trace.ensure(2 * tr_per * 8);
+            EEB_CUDA(cudaMemset(trace.p, 0, 2 * tr_per * 8));
+        }
+        for (int i = 0; i < iters; ++i) {
+            a.trace = trace_path && (i == iters / 2 || i == iters / 2 + 1)
+                          ? trace.as<unsigned long long>() + (i - iters / 2) * tr_per : nullptr;
+            run();
+        }
+        a.trace = nullptr;
         EEB_CUDA(cudaEventRecord(e1, c->stream));
         EEB_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;
@@ -2176,6 +2191,14 @@ eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, i
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         *ms_out = ms / iters;
+        if (trace_path) {
+            std::vector<unsigned long long> h(2 * tr_per);
+            EEB_CUDA(cudaMemcpy(h.data(), trace.p, h.size() * 8, cudaMemcpyDeviceToHost));
+            if (FILE* f = std::fopen(trace_path, "wb")) {
+                std::fwrite(h.data(), 8, h.size(), f);
+                std::fclose(f);
+            }
+        }
     });
 }
 

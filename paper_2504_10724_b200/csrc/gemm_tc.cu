@@ -144,7 +144,15 @@ struct TcParams {
     int vocab_off;     // added to the argmax (vocab-parallel shard)
     const char* pf;    // next GEMM's weights: L2 prefetch, this CTA's share
     size_t pf_bytes;
+    unsigned long long* trace;  // timing experiments: 8 globaltimer stamps per CTA (null = off)
+    int dbg;                    // timing experiments: bit 0 = no plane stores (results wrong)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
+    return t;
+}
 
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
@@ -169,6 +177,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int kb1 = min(kb0 + p.kb_per, p.kblocks);
     const int nkb = kb1 - kb0;
 
+    unsigned long long* tr = p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtime();  // CTA start
     pdl_launch_dependents();  // let the next kernel of the step get resident and prefetch
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_w);
@@ -189,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (tr && threadIdx.x == 0) tr[1] = gtime();  // barriers + TMEM ready
 
     if (warp == 0) {
         const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
@@ -220,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         if (lane == 0) {
             pdl_wait();
+            if (tr) tr[2] = gtime();  // predecessor complete
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,
                             pol_x);
@@ -234,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tma_load_2d(sa + a_bytes, &tmap_x, full0 + 8 * s, kc, 0, pol_x);
             }
         }
+        __syncwarp();  // reconverge before the CTA barrier (bar.sync is warp-aligned)
     } else if (warp == 1) {
         // The whole warp runs the loop (descriptors stay warp-uniform: uniform
         // registers, no per-op R2UR) and one elected lane issues — a
@@ -244,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t ph = (uint32_t)(i / S) & 1u;
             mbar_wait(full0 + 8 * s, ph);
             tc_fence_after();
+            if (tr && i == 0 && lane == 0) tr[3] = gtime();  // first stage (W + X) landed
             const uint32_t sa = base + (uint32_t)s * stage_bytes;
             const uint64_t da = smem_desc(sa), db = smem_desc(sa + a_bytes);
             if (elect_one_sync()) {
@@ -263,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         pdl_wait();  // n_active and the plane workspace belong to the previous kernels
         mbar_wait(tfull, 0);
         tc_fence_after();
+        if (tr && threadIdx.x == 64) tr[4] = gtime();  // accumulator complete
         const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
         if (p.head_tri && p.cs == 1) {
@@ -329,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int c0 = 0; c0 < p.bpad; c0 += 16) {
                 float v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective: every warp runs every chunk
-                if (n < p.N) {
+                if (n < p.N && !(p.dbg & 1)) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (c0 + j < rows) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
@@ -440,9 +455,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     tc_fence_before();
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[5] = gtime();  // epilogue stores issued
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)p.tmem_cols));
+        if (tr && lane == 0) tr[6] = gtime();  // TMEM released
     }
 }
 
@@ -516,6 +533,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const int env_stages = std::getenv("EEB_TC_STAGES") ? std::atoi(std::getenv("EEB_TC_STAGES")) : 0;
     const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
     int splits = std::max(1, std::min(kblocks / 2, wave / tiles));
+    static const int env_maxsplit = std::getenv("EEB_TC_MAXSPLIT") ? std::atoi(std::getenv("EEB_TC_MAXSPLIT")) : 0;
+    if (env_maxsplit > 0) splits = std::min(splits, env_maxsplit);
     int kb_per = (kblocks + splits - 1) / splits;
     splits = (kblocks + kb_per - 1) / kb_per;
     // Clusters of cs CTAs along K reduce their partials on chip (DSMEM): pick
@@ -602,9 +621,14 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.act_kind = a.act_kind;
     p.tiles = tiles;
     p.vocab_off = a.vocab_off;
-    static const bool no_pf = std::getenv("EEB_L2PF") && std::atoi(std::getenv("EEB_L2PF")) == 0;
+    // measured slower on C2 (1.654 vs 1.621 ms/step) and far slower where the next
+    // GEMM's weights exceed L2 (C4): opt-in with EEB_L2PF=1
+    static const bool no_pf = !(std::getenv("EEB_L2PF") && std::atoi(std::getenv("EEB_L2PF")) == 1);
     p.pf = no_pf ? nullptr : static_cast<const char*>(a.pf);
     p.pf_bytes = no_pf || !a.pf ? 0 : a.pf_bytes;
+    p.trace = a.trace;
+    static const int env_dbg = std::getenv("EEB_GEMM_DBG") ? std::atoi(std::getenv("EEB_GEMM_DBG")) : 0;
+    p.dbg = env_dbg;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;

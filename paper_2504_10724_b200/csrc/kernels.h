@@ -75,6 +75,7 @@ struct GemmArgs {
     // busy through this GEMM's tail and the non-GEMM kernels in between.
     const void* pf = nullptr;
     size_t pf_bytes = 0;
+    unsigned long long* trace = nullptr;  // timing experiments (tier 2): 8 stamps per CTA
 };
 // Tier 1: CUDA cores (any dtype, <= 64 rows).  Returns the planes written.
 int gemm_cc(const GemmArgs& a, cudaStream_t s);
