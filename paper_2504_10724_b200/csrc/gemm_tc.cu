@@ -371,7 +371,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         // exit-head softmax partials — the fused epilogues get the SM coverage
         // of split-K without a round trip through HBM/L2.
         cg::cluster_group cluster = cg::this_cluster();
-        cluster.sync();
+        // partials staged (st.shared) -> visible to the cluster: release/acquire
+        // barrier (no cg::sync, whose GPU-scope fence would also drain this
+        // CTA's global stores)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int rank = (int)cluster.block_rank();
         const int rows = *p.n_active;
         const int lim = min(rows, p.bpad);
@@ -424,7 +427,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
             }
         }
-        cluster.sync();  // keep every CTA's partial alive until the whole cluster has read it
+        // keep every CTA's partial alive until the whole cluster has read it: the
+        // DSMEM loads have returned (their values were used), so a relaxed
+        // arrive suffices and the act/plane stores above need not drain
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
         if (p.head_tri && warp >= 2) {
             // two threads per finished row scan 64 vocab entries each
             const int t = threadIdx.x - 64, hf = t & 1;
