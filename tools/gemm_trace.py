@@ -1,5 +1,7 @@
 """Per-CTA timeline of two consecutive mid-chain tcgen05 GEMM launches
 (EEB_GEMM_TRACE stamps, see gemm_tc.cu): where a launch's time goes.
+Needs libeeb built with -DEEB_GEMM_TRACE:
+  EEB_NVCC_EXTRA=-DEEB_GEMM_TRACE python -c "from paper_2504_10724_b200 import build as b; b.build_eeb()"
 Run on the GPU box:  python tools/gemm_trace.py N K [B]"""
 import os
 import sys

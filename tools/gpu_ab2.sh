@@ -10,6 +10,6 @@ run() {  # label, env...
 }
 for v in ${AB_VARIANTS:-new:X=1}; do run ${v%%:*} ${v#*:}; done
 if [ -n "$LAUNCHES" ]; then
-  timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_step.py --steps 1 > gpurun_out/prof_launch.log 2>&1
+  timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/profile_step.py --steps 1 --graphs 0 > gpurun_out/prof_launch.log 2>&1
   python tools/launch_summary.py gpurun_out/launches.csv
 fi
