@@ -285,7 +285,9 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
     return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-template <int HD, int CP>  // CP: positions per chunk (one chunk in smem at a time)
+// CP: positions per chunk; NB: chunk buffers (2 = the next chunk's TMA is in
+// flight while this one computes)
+template <int HD, int CP, int NB>
 __global__ void __launch_bounds__(kMmaWarps * 32)
     attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          AttnArgs a) {
@@ -308,18 +310,23 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (sbase - raw);
-    const uint32_t k_s = sbase, v_s = sbase + CB * kBlockBytes;  // [CB][CP][128 B] each
-    float* q_s = reinterpret_cast<float*>(base + 2 * CB * kBlockBytes);  // [8][HD]
+    // buffer b: K at sbase + b * 2 * CB * kBlockBytes, V right after ([CB][CP][128 B] each)
+    constexpr uint32_t kBufBytes = 2 * CB * kBlockBytes;
+    float* q_s = reinterpret_cast<float*>(base + NB * kBufBytes);  // [8][HD]
     __shared__ float kn_s[HD], vn_s[HD];
-    __shared__ __align__(8) uint64_t bar;
-    const uint32_t bar_a = smem_u32(&bar);
+    __shared__ __align__(8) uint64_t bars[NB];
 
     const int64_t row_off = (int64_t)i * (dq + 2 * dkv);
     __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
     __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
     const int zc = slot * Hkv + g;
 
-    auto issue = [&](int c0) {  // thread 0: TMA positions [c0, c0+cn) rounded up to whole boxes
+    const int n_chunks = pos / CP + 1;
+    // thread 0: TMA positions [c0, c0+cn) of chunk ci (rounded up to whole boxes) into buffer ci % NB
+    auto issue = [&](int ci) {
+        const int c0 = ci * CP, buf = ci % NB;
+        const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
+        const uint32_t bar_a = smem_u32(&bars[buf]);
         const int n_load = min(CP, pos + 1 - c0);
         const int boxes = n_load > 0 ? (n_load + kBoxRows - 1) / kBoxRows : 0;
         const uint32_t bytes = (uint32_t)boxes * CB * kBoxRows * 128 * 2;
@@ -334,9 +341,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+        for (int b = 0; b < NB; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[b])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        issue(0);
+        for (int c = 0; c < NB && c < n_chunks; ++c) issue(c);
     }
     // Stage this CTA's q (G heads), k and v columns, summed over the QKV GEMM's
     // split-K planes, with every load in flight at once (float4, planes unrolled).
@@ -415,24 +422,29 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     float m_run = -INFINITY, l_run = 0.f;
     const uint8_t* depth = a.kv_depth + (int64_t)slot * a.max_seq;
 
-    const int n_chunks = pos / CP + 1;
     for (int ci = 0; ci < n_chunks; ++ci) {
         const int c0 = ci * CP;
         const int cn = min(CP, pos + 1 - c0);
-        if (ci > 0) {
+        const int buf = ci % NB;
+        const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
+        if (NB == 1 && ci > 0) {
             __syncthreads();  // everyone is done with the previous chunk
-            if (threadIdx.x == 0) issue(c0);
+            if (threadIdx.x == 0) issue(ci);
         }
-        mbar_wait(bar_a, (uint32_t)(ci & 1));
+        mbar_wait(smem_u32(&bars[buf]), (uint32_t)((ci / NB) & 1));
         if (!a.kv_ready && pos < c0 + CP) {  // the new position lives in this chunk: write it (swizzled)
             const int r = pos - c0;
+            uint8_t* bb = base + buf * kBufBytes;
             for (int j = threadIdx.x; j < HD; j += blockDim.x) {
                 const uint32_t off = (j / 64) * kBlockBytes + swz(r, (j % 64) / 8) + (j % 8) * 2;
-                *reinterpret_cast<__nv_bfloat16*>(base + off) = __float2bfloat16_rn(kn_s[j]);
-                *reinterpret_cast<__nv_bfloat16*>(base + CB * kBlockBytes + off) = __float2bfloat16_rn(vn_s[j]);
+                *reinterpret_cast<__nv_bfloat16*>(bb + off) = __float2bfloat16_rn(kn_s[j]);
+                *reinterpret_cast<__nv_bfloat16*>(bb + CB * kBlockBytes + off) = __float2bfloat16_rn(vn_s[j]);
             }
         }
         __syncthreads();
+        // NB >= 2: everyone is past chunk ci-1, so its buffer takes chunk ci-1+NB
+        // while this chunk computes
+        if (NB >= 2 && threadIdx.x == 0 && ci >= 1 && ci - 1 + NB < n_chunks) issue(ci - 1 + NB);
         const int n_tiles = (cn + 7) / 8;
         // scores for this warp's tiles (C fragment: row h, positions kq, kq+1)
         float sc[TPW][2];
@@ -980,13 +992,13 @@ __global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
     if (i < rows) kv_depth[(int64_t)slot[i] * max_seq + pos[i]] = (uint8_t)depth;
 }
 
-template <int HD, int CP>
+template <int HD, int CP, int NB>
 void launch_mma_cp(const AttnArgs& a, cudaStream_t s) {
     constexpr int CB = HD / 64;
     const int G = a.n_heads / a.n_kv_heads;
     if (a.splits > 16) throw Error(1, "attention: more than 16 QKV split-K planes");
-    const size_t smem = 1024 + 2 * (size_t)CB * CP * 128 + (8 + G + 2) * HD * 4;
-    auto kern = attention_mma_kernel<HD, CP>;
+    const size_t smem = 1024 + (size_t)NB * 2 * CB * CP * 128 + (8 + G + 2) * HD * 4;
+    auto kern = attention_mma_kernel<HD, CP, NB>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // x = kv head, y = row: the live rows' CTAs come first in launch order
     dim3 grid(a.n_kv_heads, a.max_rows);
@@ -1003,10 +1015,19 @@ void launch_mma(const AttnArgs& a, cudaStream_t s) {
     static const int env_cp = std::getenv("EEB_ATTN_CP") ? std::atoi(std::getenv("EEB_ATTN_CP")) : 0;
     // measured C2 (hd 64, context 128..227): 64 positions 1.56 ms/step, 128 1.61, 256 1.64
     const int cp = env_cp > 0 ? env_cp : (HD == 64 ? 64 : 128);
-    if (cp <= 32) launch_mma_cp<HD, 32>(a, s);
-    else if (cp <= 64) launch_mma_cp<HD, 64>(a, s);
-    else if (cp <= 128) launch_mma_cp<HD, 128>(a, s);
-    else launch_mma_cp<HD, 256>(a, s);
+    static const int env_nb = std::getenv("EEB_ATTN_NB") ? std::atoi(std::getenv("EEB_ATTN_NB")) : 0;
+    // double-buffered chunks measured slower on C2 (1.548 vs 1.515 ms/step): opt-in
+    const int nb = env_nb > 0 ? env_nb : 1;
+    if (nb >= 2) {
+        if (cp <= 32) launch_mma_cp<HD, 32, 2>(a, s);
+        else if (cp <= 64) launch_mma_cp<HD, 64, 2>(a, s);
+        else launch_mma_cp<HD, 128, 2>(a, s);
+    } else {
+        if (cp <= 32) launch_mma_cp<HD, 32, 1>(a, s);
+        else if (cp <= 64) launch_mma_cp<HD, 64, 1>(a, s);
+        else if (cp <= 128) launch_mma_cp<HD, 128, 1>(a, s);
+        else launch_mma_cp<HD, 256, 1>(a, s);
+    }
 }
 
 }  // namespace

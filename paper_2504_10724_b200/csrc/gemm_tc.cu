@@ -148,6 +148,18 @@ struct TcParams {
     int dbg;                    // timing experiments: bit 0 = no plane stores (results wrong)
 };
 
+// Timeline stamps are compiled in only for the timing experiments
+// (-DEEB_GEMM_TRACE, tools/gemm_trace.py); the product kernel has none.
+#ifdef EEB_GEMM_TRACE
+#define EEB_STAMP(cond, slot) \
+    do {                      \
+        if (tr && (cond)) tr[slot] = gtime(); \
+    } while (0)
+#else
+#define EEB_STAMP(cond, slot) \
+    do {                      \
+    } while (0)
+#endif
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
@@ -177,8 +189,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int kb1 = min(kb0 + p.kb_per, p.kblocks);
     const int nkb = kb1 - kb0;
 
+#ifdef EEB_GEMM_TRACE
     unsigned long long* tr = p.trace ? p.trace + 8 * ((size_t)blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
-    if (tr && threadIdx.x == 0) tr[0] = gtime();  // CTA start
+#endif
+    EEB_STAMP(threadIdx.x == 0, 0);  // CTA start
     pdl_launch_dependents();  // let the next kernel of the step get resident and prefetch
     if (threadIdx.x == 0) {
         prefetch_tmap(&tmap_w);
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (tr && threadIdx.x == 0) tr[1] = gtime();  // barriers + TMEM ready
+    EEB_STAMP(threadIdx.x == 0, 1);  // barriers + TMEM ready
 
     if (warp == 0) {
         const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
@@ -215,6 +229,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
         __syncwarp();
+#ifdef EEB_L2_PREFETCH
+        // (compiled in only for the experiment: measured slower, see gemm_tc host)
         if (lane != 0 && p.pf_bytes) {
             // lanes 1..31, behind this CTA's own first tiles: its share of the
             // next GEMM's weights -> L2
@@ -229,9 +245,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.pf + o), "r"(n) : "memory");
             }
         }
+#endif
         if (lane == 0) {
             pdl_wait();
-            if (tr) tr[2] = gtime();  // predecessor complete
+            EEB_STAMP(true, 2);  // predecessor complete
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,
                             pol_x);
@@ -257,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t ph = (uint32_t)(i / S) & 1u;
             mbar_wait(full0 + 8 * s, ph);
             tc_fence_after();
-            if (tr && i == 0 && lane == 0) tr[3] = gtime();  // first stage (W + X) landed
+            EEB_STAMP(i == 0 && lane == 0, 3);  // first stage (W + X) landed
             const uint32_t sa = base + (uint32_t)s * stage_bytes;
             const uint64_t da = smem_desc(sa), db = smem_desc(sa + a_bytes);
             if (elect_one_sync()) {
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         pdl_wait();  // n_active and the plane workspace belong to the previous kernels
         mbar_wait(tfull, 0);
         tc_fence_after();
-        if (tr && threadIdx.x == 64) tr[4] = gtime();  // accumulator complete
+        EEB_STAMP(threadIdx.x == 64, 4);  // accumulator complete
         const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
         if (p.head_tri && p.cs == 1) {
@@ -461,11 +478,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     tc_fence_before();
     __syncthreads();
-    if (tr && threadIdx.x == 0) tr[5] = gtime();  // epilogue stores issued
+    EEB_STAMP(threadIdx.x == 0, 5);  // epilogue stores issued
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)p.tmem_cols));
-        if (tr && lane == 0) tr[6] = gtime();  // TMEM released
+        EEB_STAMP(lane == 0, 6);  // TMEM released
     }
 }
 
@@ -654,7 +671,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     attr[1].val.clusterDim.y = cs;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = cs > 1 ? 2 : 1;  // no cluster attribute unless clustering (launch cost)
+    static const bool force_cl = std::getenv("EEB_TC_CLUSTER_ATTR") != nullptr;
+    cfg.numAttrs = cs > 1 || force_cl ? 2 : 1;  // no cluster attribute unless clustering (launch cost)
     EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p));
     return splits / cs;
 }
