@@ -148,6 +148,21 @@ eeb_status eeb_weight_bytes(eeb_ctx* ctx, int model, int depth, int64_t* bytes);
 /* Clear the KV of slots (positions marked as never computed). */
 eeb_status eeb_reset_slots(eeb_ctx* ctx, int model, int32_t n, const int32_t* slot_ids);
 
+/* Paged KV pool (replaces the slot-contiguous pool sized by
+ * kv_bytes_per_slot x max_batch, memory_model.hpp:53-72).  configure_pages
+ * re-creates the model's pool as n_pages pages of page_size positions
+ * (multiple of 64, at most 64 pages per sequence) — call it before the first
+ * step; it drops every slot's KV.  A slot takes pages from a free list as its
+ * positions grow: eeb_decode_step / eeb_prefill (host arrays) reserve them
+ * themselves, eeb_decode_step_device needs eeb_kv_reserve first (its positions
+ * are device-side).  Out of pages -> EEB_E_CAPACITY (CapacityError).
+ * eeb_kv_release returns a finished request's pages (continuous batching:
+ * the slot is free for the next request).  bf16 models with head_dim 64/128. */
+eeb_status eeb_kv_configure_pages(eeb_ctx* ctx, int model, int32_t page_size, int32_t n_pages);
+eeb_status eeb_kv_reserve(eeb_ctx* ctx, int model, int32_t slot, int32_t n_positions);
+eeb_status eeb_kv_release(eeb_ctx* ctx, int model, int32_t slot);
+eeb_status eeb_kv_pages(eeb_ctx* ctx, int model, int32_t* page_size, int32_t* n_pages, int32_t* n_free);
+
 /* The decode step ↔ Simulator::serve_one token loop (engine.hpp:344-386),
  * batched per SPEC.md:465-473.  Row i decodes `input_tokens[i]` at position
  * `positions[i]` of KV slot `slot_ids[i]`.

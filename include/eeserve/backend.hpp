@@ -70,6 +70,9 @@ public:
     virtual double prefill(const std::string& model, int depth, const PrefillRows& rows) = 0;
     virtual StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
                              const StepRows& rows) = 0;
+    /// Continuous batching: the request in `slot` finished; its KV (pages) may
+    /// be reused by the next request admitted into the slot.
+    virtual void release(const std::string& model, int slot) { (void)model, (void)slot; }
 };
 
 // ---------------------------------------------------------------------------
@@ -82,6 +85,12 @@ public:
     /// otherwise layers are materialised on device from the seed.
     explicit CudaBackend(int device = 0, bool host_tier = false) : host_tier_(host_tier) {
         throw_if_error(eeb_create(device, &ctx_), "eeb_create");
+    }
+    /// Paged KV pool for models registered after this call (eeb_kv_configure_pages):
+    /// n_pages pages of page_size positions instead of max_slots x max_seq_len.
+    void set_kv_pages(int page_size, int n_pages) {
+        kv_page_ = page_size;
+        kv_pages_ = n_pages;
     }
     ~CudaBackend() override { eeb_destroy(ctx_); }
     CudaBackend(const CudaBackend&) = delete;
@@ -109,7 +118,12 @@ public:
         int h = -1;
         throw_if_error(eeb_model_register(ctx_, &d, &h), "eeb_model_register");
         handles_[spec.id] = {h, spec};
+        if (kv_page_ > 0) throw_if_error(eeb_kv_configure_pages(ctx_, h, kv_page_, kv_pages_), "eeb_kv_configure_pages");
         if (host_tier_) throw_if_error(eeb_host_stage(ctx_, h, spec.num_layers), "eeb_host_stage");
+    }
+
+    void release(const std::string& model, int slot) override {
+        throw_if_error(eeb_kv_release(ctx_, handle(model).h, slot), "eeb_kv_release");
     }
 
     LoadResult load(const std::string& model, int depth) override {
@@ -202,6 +216,7 @@ public:
     eeb_ctx* context() const { return ctx_; }
 
 private:
+    int kv_page_ = 0, kv_pages_ = 0;
     struct Entry {
         int h;
         ModelSpec spec;

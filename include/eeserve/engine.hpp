@@ -52,6 +52,13 @@ struct EngineConfig {
     std::uint64_t token_seed = 20260819;
     bool prefill = true;  // run the prompt through the backend (real KV); off for trace replay
     bool record_events = false;  // keep the reference-format event log (events.hpp) in the report
+    // Continuous batching: a finished request's slot is
+    // released (DecodeBackend::release) and the next queued request is
+    // prefilled into it while the others keep decoding; admission stops at a
+    // policy boundary (reassessment due or a pending breach action) and the
+    // in-flight requests drain first, so actions still apply at request
+    // boundaries (engine.hpp:143).  max_batch = 1 is the reference's loop.
+    bool continuous = false;
 };
 
 struct RequestTiming {  // ↔ the request's TTFT (engine.hpp:333-337) and its tokens' TPOT
@@ -129,6 +136,10 @@ public:
                 continue;
             }
             if (pending_) apply_pending();
+            if (cfg_.continuous) {
+                serve_continuous(reqs, serving_, depth_, tp);
+                continue;
+            }
             const size_t n = std::min<size_t>(cfg_.max_batch, reqs.size() - cursor_);
             std::vector<const RequestSpec*> batch;
             for (size_t i = 0; i < n; ++i) batch.push_back(&reqs[cursor_ + i]);
@@ -363,6 +374,123 @@ private:
                                          .num("tpot_mean_s", tpot_mean)
                                          .num("latency_s", rt.ttft_s + tpot_mean * (double)rt.tokens)
                                          .i64("tokens", rt.tokens));
+        }
+    }
+
+    // Continuous batching over the request queue from cursor_ (see EngineConfig::continuous).
+    void serve_continuous(const std::vector<RequestSpec>& reqs, const std::string& model, int depth, TokenPolicy tp) {
+        const ModelSpec& spec = repo_.at(model);
+        const int vocab = spec.arch.vocab > 0 ? spec.arch.vocab : 1;
+        rep_.serving_history.emplace_back(model, depth);
+        struct Active {
+            const RequestSpec* r;
+            int slot;
+            int t;          // tokens emitted so far
+            size_t timing;  // index in rep_.requests
+        };
+        std::vector<Active> act;
+        std::vector<int> free_slots;
+        for (int s = cfg_.max_batch - 1; s >= 0; --s) free_slots.push_back(s);  // lowest slot first
+        auto admissible = [&] {
+            return cursor_ < reqs.size() && !pending_ &&
+                   !(cfg_.mode.kind == Mode::helios && should_reassess(since_eval_, cfg_.policy));
+        };
+        auto complete = [&](const Active& a) {  // engine.hpp:387-395
+            const RequestTiming& rt = rep_.requests[a.timing];
+            const double tpot_mean = rt.tokens ? rt.tpot_sum_s / rt.tokens : 0.0;
+            emit("request_complete", JsonFields()
+                                         .i64("request_id", rt.request_id)
+                                         .num("ttft_s", rt.ttft_s)
+                                         .num("tpot_mean_s", tpot_mean)
+                                         .num("latency_s", rt.ttft_s + tpot_mean * (double)rt.tokens)
+                                         .i64("tokens", rt.tokens));
+            be_.release(model, a.slot);
+            free_slots.push_back(a.slot);
+        };
+        auto admit = [&] {
+            std::vector<Active> fresh;
+            while (!free_slots.empty() && admissible()) {
+                fresh.push_back({&reqs[cursor_], free_slots.back(), 0, 0});
+                free_slots.pop_back();
+                ++cursor_;
+                ++since_eval_;
+            }
+            if (fresh.empty()) return;
+            for (const auto& a : fresh) emit("request_start", JsonFields().i64("request_id", a.r->request_id));
+            double prefill_s = 0.0;
+            int max_prompt = 0;
+            for (const auto& a : fresh) max_prompt = std::max(max_prompt, a.r->prompt_len);
+            if (cfg_.prefill) {
+                PrefillRows pr;
+                for (const auto& a : fresh) {
+                    pr.slots.push_back(a.slot);
+                    std::vector<int32_t> p(a.r->prompt_len);
+                    for (int k = 0; k < a.r->prompt_len; ++k)
+                        p[k] = synthetic_token(cfg_.token_seed, a.r->request_id, k, vocab);
+                    pr.prompts.push_back(std::move(p));
+                }
+                prefill_s = be_.prefill(model, tp == TokenPolicy::flat ? depth : spec.num_layers, pr);
+            }
+            if (prefill_s <= 0.0) prefill_s = (double)max_prompt * depth * spec.t_prefill_per_layer_per_token_s;
+            rep_.prefill_s += prefill_s;
+            clock_ += prefill_s;
+            for (const auto& a : fresh)
+                emit("prefill", JsonFields()
+                                    .i64("request_id", a.r->request_id)
+                                    .str("model", model)
+                                    .i64("depth", depth)
+                                    .num("duration_s", prefill_s));
+            const double ttft = pending_stall_s_ + prefill_s;
+            pending_stall_s_ = 0.0;
+            for (auto& a : fresh) {
+                a.timing = rep_.requests.size();
+                rep_.requests.push_back({a.r->request_id, ttft, 0.0, 0});
+                if (a.r->num_tokens <= 0) complete(a);
+                else act.push_back(a);
+            }
+        };
+        admit();
+        while (!act.empty()) {
+            // rows in ascending slot order (breach observation order, SURVEY §7 hard part 4)
+            std::sort(act.begin(), act.end(), [](const Active& x, const Active& y) { return x.slot < y.slot; });
+            StepRows rows;
+            for (const auto& a : act) {
+                const int pos = a.r->prompt_len + a.t;
+                rows.slots.push_back(a.slot);
+                rows.tokens.push_back(synthetic_token(cfg_.token_seed, a.r->request_id, pos, vocab));
+                rows.positions.push_back(pos);
+                rows.request_ids.push_back(a.r->request_id);
+                rows.token_index.push_back(a.t);
+            }
+            const StepOutcome o = be_.step(model, depth, tp, cfg_.policy.th, rows);
+            double dur = o.seconds;
+            if (dur <= 0.0) {
+                int deepest = 0;
+                for (int x : o.exit_layer) deepest = std::max(deepest, x);
+                dur = deepest * spec.t_decode_per_layer_s;
+            }
+            clock_ += dur;
+            for (int i = 0; i < rows.size(); ++i)
+                emit("token_emitted", JsonFields()
+                                          .i64("request_id", rows.request_ids[i])
+                                          .str("model", model)
+                                          .i64("exit_layer", o.exit_layer[i])
+                                          .boolean("breached", o.breached[i] != 0)
+                                          .boolean("unchanged", o.unchanged[i] == 1)
+                                          .num("duration_s", dur)
+                                          .num("logprob", o.obs[i].logprob)
+                                          .num("energy_mwh", o.exit_layer[i] * spec.energy_per_layer_per_token_mwh));
+            consume(model, spec, tp, false, rows, o, dur);
+            std::vector<Active> still;
+            for (auto& a : act) {
+                RequestTiming& rt = rep_.requests[a.timing];
+                rt.tpot_sum_s += dur;
+                rt.tokens += 1;
+                if (++a.t >= a.r->num_tokens) complete(a);
+                else still.push_back(a);
+            }
+            act.swap(still);
+            admit();
         }
     }
 

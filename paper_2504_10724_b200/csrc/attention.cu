@@ -287,7 +287,7 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 
 // CP: positions per chunk; NB: chunk buffers (2 = the next chunk's TMA is in
 // flight while this one computes)
-template <int HD, int CP, int NB>
+template <int HD, int CP, int NB, bool PAGED>
 __global__ void __launch_bounds__(kMmaWarps * 32)
     attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          AttnArgs a) {
@@ -317,9 +317,24 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     __shared__ __align__(8) uint64_t bars[NB];
 
     const int64_t row_off = (int64_t)i * (dq + 2 * dkv);
-    __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
-    __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + (((int64_t)slot * Hkv + g) * a.max_seq) * HD;
-    const int zc = slot * Hkv + g;
+    // Page of each position: the unpaged pool's table is the identity (page ==
+    // slot, no load on the TMA's critical path); a paged pool's row for this
+    // slot is read into smem once.
+    // (a separate instantiation: the unpaged kernel keeps its registers)
+    constexpr int kMaxPt = PAGED ? 64 : 1;
+    __shared__ int pt_s[kMaxPt];
+    const int PS = PAGED ? a.page_size : a.max_seq;
+    if constexpr (PAGED) {
+        for (int t = threadIdx.x; t < a.pages_per_seq && t < kMaxPt; t += blockDim.x)
+            pt_s[t] = a.page_table[(int64_t)slot * a.pages_per_seq + t];
+        __syncthreads();
+    }
+    auto page_of = [&](int p) { return PAGED ? pt_s[p / PS] : slot; };
+    auto row_of = [&](int p) { return PAGED ? p % PS : p; };
+    // the new position's K/V row
+    const int64_t new_off = (((int64_t)page_of(pos) * Hkv + g) * PS + row_of(pos)) * HD;
+    __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + new_off;
+    __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + new_off;
 
     const int n_chunks = pos / CP + 1;
     // thread 0: TMA positions [c0, c0+cn) of chunk ci (rounded up to whole boxes) into buffer ci % NB
@@ -331,12 +346,15 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
         const int boxes = n_load > 0 ? (n_load + kBoxRows - 1) / kBoxRows : 0;
         const uint32_t bytes = (uint32_t)boxes * CB * kBoxRows * 128 * 2;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(bytes) : "memory");
-        for (int b = 0; b < boxes; ++b)
+        for (int b = 0; b < boxes; ++b) {
+            const int p = c0 + b * kBoxRows;  // page_size is a multiple of the box
+            const int zc = page_of(p) * Hkv + g;
             for (int cb = 0; cb < CB; ++cb) {
                 const uint32_t off = cb * kBlockBytes + b * kBoxRows * 128;
-                tma_3d(k_s + off, &kmap, bar_a, cb * 64, c0 + b * kBoxRows, zc);
-                tma_3d(v_s + off, &vmap, bar_a, cb * 64, c0 + b * kBoxRows, zc);
+                tma_3d(k_s + off, &kmap, bar_a, cb * 64, row_of(p), zc);
+                tma_3d(v_s + off, &vmap, bar_a, cb * 64, row_of(p), zc);
             }
+        }
     };
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
@@ -399,8 +417,8 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
         const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
         const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(vv[j]);
         if (!a.kv_ready) {
-            kc[(int64_t)pos * HD + j] = kt;
-            vc[(int64_t)pos * HD + j] = vt;
+            kc[j] = kt;
+            vc[j] = vt;
         }
         kn_s[j] = __bfloat162float(kt);
         vn_s[j] = __bfloat162float(vt);
@@ -978,7 +996,7 @@ __global__ void kv_append_kernel(AttnArgs a) {
         const int jj = j < half ? j : j - half;
         const float x0 = qkv(dq + g * hd + jj), x1 = qkv(dq + g * hd + jj + half);
         const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
-        const int64_t off = (((int64_t)slot * Hkv + g) * a.max_seq + pos) * hd + j;
+        const int64_t off = kv_elem_offset(a, slot, pos, g) + j;
         static_cast<T*>(a.k_cache)[off] = from_f32<T>(kr);
         static_cast<T*>(a.v_cache)[off] = from_f32<T>(qkv(dq + dkv + g * hd + j));
     }
@@ -992,19 +1010,28 @@ __global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
     if (i < rows) kv_depth[(int64_t)slot[i] * max_seq + pos[i]] = (uint8_t)depth;
 }
 
-template <int HD, int CP, int NB>
-void launch_mma_cp(const AttnArgs& a, cudaStream_t s) {
+template <int HD, int CP, int NB, bool PAGED>
+void launch_mma_cp_t(const AttnArgs& a, cudaStream_t s) {
     constexpr int CB = HD / 64;
     const int G = a.n_heads / a.n_kv_heads;
     if (a.splits > 16) throw Error(1, "attention: more than 16 QKV split-K planes");
     const size_t smem = 1024 + (size_t)NB * 2 * CB * CP * 128 + (8 + G + 2) * HD * 4;
-    auto kern = attention_mma_kernel<HD, CP, NB>;
+    auto kern = attention_mma_kernel<HD, CP, NB, PAGED>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // x = kv head, y = row: the live rows' CTAs come first in launch order
     dim3 grid(a.n_kv_heads, a.max_rows);
     launch_pdl(kern, grid, dim3(kMmaWarps * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a);
     EEB_CHECK_LAUNCH();
+}
+
+template <int HD, int CP, int NB>
+void launch_mma_cp(const AttnArgs& a, cudaStream_t s) {
+    if (a.page_size != a.max_seq) {
+        launch_mma_cp_t<HD, CP, NB, true>(a, s);
+    } else {
+        launch_mma_cp_t<HD, CP, NB, false>(a, s);
+    }
 }
 
 // Chunk size: the whole context of a (row, kv head) in one chunk keeps one
@@ -1047,8 +1074,14 @@ void launch_mark_depth(int rows, const int* slot, const int* pos, uint8_t* kv_de
 }
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
+    const bool paged = a.page_size != a.max_seq;
     if (a.dtype == 1 && a.k_map && a.v_map && a.n_heads / a.n_kv_heads <= 8 &&
         (a.head_dim == 64 || a.head_dim == 128)) {
+        if (paged) {  // only the one-item kernel walks page tables
+            if (a.head_dim == 64) launch_mma<64>(a, s);
+            else launch_mma<128>(a, s);
+            return;
+        }
         // One (row, kv-head) item per CTA for head_dim 64 (MHA, C2: measured
         // faster than the pipelined walk); the pipelined walk for head_dim 128
         // (GQA, C4).  EEB_ATTN=one|pipe overrides (A/B).
@@ -1064,6 +1097,7 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
         return;
     }
     const int G = a.n_heads / a.n_kv_heads;
+    if (paged) throw Error(3, "attention: the paged KV pool needs a bf16 model with head_dim 64 or 128");
     if (G > kMaxG || a.head_dim > kMaxHd || a.head_dim % 16 != 0 || kThreads % (a.head_dim / 2) != 0)
         throw Error(1, "attention: unsupported head geometry");
     const int esz = a.dtype == 0 ? 4 : 2;

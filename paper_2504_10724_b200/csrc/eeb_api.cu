@@ -123,6 +123,17 @@ struct Model {
     // KV pool
     DevBuf k_cache, v_cache, kv_depth, rope_cos, rope_sin;
     size_t kv_layer_elems = 0;
+    // KV pages.  Unpaged (default): one page per slot of
+    // max_seq_len positions, identity table.  Paged (eeb_kv_configure_pages):
+    // n_pages pages of page_size positions on a free list; a slot's table row
+    // grows as its positions do and is released with the slot.
+    int kv_page = 0, kv_pages = 0, pages_per_seq = 1;
+    bool paged = false;
+    DevBuf page_table;                 // int32 [max_slots][pages_per_seq]
+    std::vector<int32_t> h_table;      // host mirror
+    std::vector<int32_t> slot_npages;  // pages held per slot
+    std::vector<int32_t> free_pages;   // LIFO free list
+    bool table_dirty = false;
     std::vector<std::array<uint8_t, 128>> k_maps, v_maps;  // bf16: per-layer TMA maps of the KV cache
     // host tier + asynchronous loader state
     HostTier host;
@@ -852,6 +863,9 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         a.n_kv_heads = m.hkv_l;
         a.head_dim = m.head_dim;
         a.max_seq = d.max_seq_len;
+        a.page_table = m.page_table.as<int>();
+        a.page_size = m.kv_page;
+        a.pages_per_seq = m.pages_per_seq;
         a.out = static_cast<char*>(c->attn.p) + (size_t)sh * batch * m.dq_l * wb;
         const size_t mk = (size_t)(l - 1) * m.shards + sh;
         a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[mk].data();
@@ -1177,7 +1191,7 @@ bool mk_applicable(eeb_ctx* c, const Model& m, int batch) {
         c->mk_mode = env && env[0] == '1' ? 1 : 0;
     }
     const eeb_model_desc& d = m.desc;
-    const bool ok = !c->retain_logits && m.tp == 1 && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
+    const bool ok = !c->retain_logits && !m.paged && m.tp == 1 && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
                     d.d_model <= 6 * 3 * 128 &&
                     batch <= mk::kMaxRows && d.max_seq_len <= 256 && gemm_tc_available();
     if (c->gemm_tier == 3) {
@@ -1496,6 +1510,90 @@ void harvest_profile(eeb_ctx* c) {
     c->steps_profiled += 1;
 }
 
+// KV pool ↔ kv_bytes_per_slot (memory_model.hpp:58-60).  Per layer and
+// shard: [pages][hkv_l][page][hd]; unpaged = one page of max_seq_len
+// positions per slot (slot == page), paged = n_pages pages on a free list.
+void alloc_kv(eeb_ctx* c, Model& m, int page, int n_pages, bool paged) {
+    const eeb_model_desc& d = m.desc;
+    m.kv_page = page;
+    m.kv_pages = n_pages;
+    m.pages_per_seq = (d.max_seq_len + page - 1) / page;
+    m.paged = paged;
+    m.kv_shard_elems = (size_t)n_pages * m.hkv_l * page * m.head_dim;
+    m.kv_layer_elems = m.kv_shard_elems * m.shards;
+    m.k_cache.release();
+    m.v_cache.release();
+    m.k_cache.ensure(m.kv_layer_elems * d.num_layers * m.wbytes);
+    m.v_cache.ensure(m.kv_layer_elems * d.num_layers * m.wbytes);
+    // stream-ordered (the context stream is non-blocking: a legacy-stream
+    // memset would not be ordered before the first step)
+    EEB_CUDA(cudaMemsetAsync(m.k_cache.p, 0, m.k_cache.bytes, c->stream));  // finite values behind masked rows
+    EEB_CUDA(cudaMemsetAsync(m.v_cache.p, 0, m.v_cache.bytes, c->stream));
+    m.k_maps.clear();
+    m.v_maps.clear();
+    if (d.dtype == EEB_BF16 && (m.head_dim == 64 || m.head_dim == 128) && gemm_tc_available()) {
+        m.k_maps.resize((size_t)d.num_layers * m.shards);
+        m.v_maps.resize((size_t)d.num_layers * m.shards);
+        for (int l = 0; l < d.num_layers; ++l)
+            for (int sh = 0; sh < m.shards; ++sh) {
+                const size_t off = ((size_t)l * m.kv_layer_elems + sh * m.kv_shard_elems) * 2;
+                const size_t k = (size_t)l * m.shards + sh;
+                make_kv_tensor_map(m.k_maps[k].data(), static_cast<char*>(m.k_cache.p) + off, m.head_dim, page,
+                                   n_pages * m.hkv_l, 32);
+                make_kv_tensor_map(m.v_maps[k].data(), static_cast<char*>(m.v_cache.p) + off, m.head_dim, page,
+                                   n_pages * m.hkv_l, 32);
+            }
+    }
+    m.h_table.assign((size_t)d.max_slots * m.pages_per_seq, paged ? -1 : 0);
+    m.slot_npages.assign(d.max_slots, 0);
+    m.free_pages.clear();
+    if (!paged) {
+        for (int sl = 0; sl < d.max_slots; ++sl) m.h_table[sl] = sl;
+    } else {
+        for (int pg = n_pages - 1; pg >= 0; --pg) m.free_pages.push_back(pg);
+    }
+    m.page_table.ensure(m.h_table.size() * 4);
+    m.table_dirty = true;
+}
+
+// Paged pool: give `slot` pages for positions [0, n_positions) (EEB_E_CAPACITY
+// when the free list runs dry, like CapacityError in apply_load,
+// memory_model.hpp:86-105).
+void kv_reserve(Model& m, int slot, int n_positions) {
+    if (!m.paged) return;
+    const int need = (n_positions + m.kv_page - 1) / m.kv_page;
+    int& have = m.slot_npages[slot];
+    while (have < need) {
+        if (m.free_pages.empty())
+            throw Error(EEB_E_CAPACITY, "KV page pool exhausted (" + std::to_string(m.kv_pages) + " pages of " +
+                                            std::to_string(m.kv_page) + " positions)");
+        m.h_table[(size_t)slot * m.pages_per_seq + have] = m.free_pages.back();
+        m.free_pages.pop_back();
+        ++have;
+        m.table_dirty = true;
+    }
+}
+
+void kv_release(Model& m, int slot) {
+    if (!m.paged) return;
+    int& have = m.slot_npages[slot];
+    for (int k = have - 1; k >= 0; --k) {
+        int32_t& e = m.h_table[(size_t)slot * m.pages_per_seq + k];
+        m.free_pages.push_back(e);
+        e = -1;
+    }
+    have = 0;
+    m.table_dirty = true;
+}
+
+// Stream-ordered upload of the page table before work that reads it.
+void kv_sync_table(eeb_ctx* c, Model& m) {
+    if (!m.table_dirty) return;
+    EEB_CUDA(cudaMemcpyAsync(m.page_table.p, m.h_table.data(), m.h_table.size() * 4, cudaMemcpyHostToDevice,
+                             c->stream));
+    m.table_dirty = false;
+}
+
 }  // namespace
 }  // namespace eeb
 
@@ -1581,29 +1679,7 @@ eeb_status eeb_model_register(eeb_ctx* c, const eeb_model_desc* desc, int* model
         m->up_l = m->up_rows / m->tp;
         m->v_l = d.vocab / m->tp;
         if (m->head_dim % 16 != 0 || m->head_dim > 128) throw Error(EEB_E_VALIDATION, "head_dim must be a multiple of 16, <= 128");
-        // KV pool ↔ kv_bytes_per_slot (memory_model.hpp:58-60): every layer, max_seq positions.
-        // (KV heads of a layer: shard-major, each shard [slots][hkv_l][S][hd])
-        m->kv_shard_elems = (size_t)d.max_slots * m->hkv_l * d.max_seq_len * m->head_dim;
-        m->kv_layer_elems = m->kv_shard_elems * m->shards;
-        m->k_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
-        m->v_cache.ensure(m->kv_layer_elems * d.num_layers * m->wbytes);
-        // stream-ordered (the context stream is non-blocking: a legacy-stream
-        // memset would not be ordered before the first step)
-        EEB_CUDA(cudaMemsetAsync(m->k_cache.p, 0, m->k_cache.bytes, c->stream));  // finite values behind masked rows
-        EEB_CUDA(cudaMemsetAsync(m->v_cache.p, 0, m->v_cache.bytes, c->stream));
-        if (d.dtype == EEB_BF16 && (m->head_dim == 64 || m->head_dim == 128) && gemm_tc_available()) {
-            m->k_maps.resize((size_t)d.num_layers * m->shards);
-            m->v_maps.resize((size_t)d.num_layers * m->shards);
-            for (int l = 0; l < d.num_layers; ++l)
-                for (int sh = 0; sh < m->shards; ++sh) {
-                    const size_t off = ((size_t)l * m->kv_layer_elems + sh * m->kv_shard_elems) * 2;
-                    const size_t k = (size_t)l * m->shards + sh;
-                    make_kv_tensor_map(m->k_maps[k].data(), static_cast<char*>(m->k_cache.p) + off, m->head_dim,
-                                       d.max_seq_len, d.max_slots * m->hkv_l, 32);
-                    make_kv_tensor_map(m->v_maps[k].data(), static_cast<char*>(m->v_cache.p) + off, m->head_dim,
-                                       d.max_seq_len, d.max_slots * m->hkv_l, 32);
-                }
-        }
+        alloc_kv(c, *m, d.max_seq_len, d.max_slots, false);
         m->kv_depth.ensure((size_t)d.max_slots * d.max_seq_len);
         EEB_CUDA(cudaMemsetAsync(m->kv_depth.p, 0, m->kv_depth.bytes, c->stream));
         EEB_CUDA(cudaStreamSynchronize(c->stream));
@@ -1725,6 +1801,8 @@ eeb_status eeb_decode_step(eeb_ctx* c, int model, int depth, int policy, float t
         if (!slot_ids || !input_tokens || !positions) throw Error(EEB_E_DOMAIN, "null input array");
         check_step_args(c, m, depth, policy, th, batch);
         validate_rows_host(m, batch, slot_ids, input_tokens, positions);
+        for (int i = 0; i < batch; ++i) kv_reserve(m, slot_ids[i], positions[i] + 1);
+        kv_sync_table(c, m);
         EEB_CUDA(cudaSetDevice(c->device));
         ensure_workspace(c, m, batch);
         wait_layers(c, m, policy == EEB_FLAT ? depth : m.desc.num_layers);
@@ -1787,6 +1865,7 @@ eeb_status eeb_decode_step_device(eeb_ctx* c, int model, int depth, int policy, 
         EEB_CUDA(cudaSetDevice(c->device));
         ensure_workspace(c, m, batch);
         wait_layers(c, m, policy == EEB_FLAT ? depth : m.desc.num_layers);
+        kv_sync_table(c, m);  // pages reserved with eeb_kv_reserve (positions are device-side here)
         Ints I = ints_of(c);
         cudaStream_t s = c->stream;
         EEB_CUDA(cudaMemcpyAsync(I.tok, d_tok, (size_t)batch * 4, cudaMemcpyDeviceToDevice, s));
@@ -1841,6 +1920,8 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
         for (int64_t t = 0; t < total; ++t)
             if (tokens[t] < 0 || tokens[t] >= d.vocab) throw Error(EEB_E_DOMAIN, "token id out of range");
         if (total == 0) return;
+        for (int k = 0; k < n_seq; ++k) kv_reserve(m, slot_ids[k], start_pos[k] + lens[k]);
+        kv_sync_table(c, m);
         EEB_CUDA(cudaSetDevice(c->device));
         wait_layers(c, m, depth);
         const int chunk = d.dtype == EEB_BF16 ? 256 : 64;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
@@ -1967,6 +2048,57 @@ eeb_status eeb_debug_read_weight(eeb_ctx* c, int model, int tensor, int layer, i
     });
 }
 
+/* Paged KV pool. */
+eeb_status eeb_kv_configure_pages(eeb_ctx* c, int model, int32_t page_size, int32_t n_pages) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const eeb_model_desc& d = m.desc;
+        if (page_size <= 0 || page_size % 64 != 0)
+            throw Error(EEB_E_VALIDATION, "page_size must be a positive multiple of 64 positions");
+        if (n_pages <= 0) throw Error(EEB_E_VALIDATION, "n_pages must be positive");
+        if ((d.max_seq_len + page_size - 1) / page_size > 64)
+            throw Error(EEB_E_VALIDATION, "at most 64 pages per sequence (max_seq_len / page_size)");
+        if (d.dtype != EEB_BF16 || (m.head_dim != 64 && m.head_dim != 128) || !gemm_tc_available())
+            throw Error(EEB_E_DOMAIN, "the paged KV pool needs a bf16 model with head_dim 64 or 128");
+        EEB_CUDA(cudaSetDevice(c->device));
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        alloc_kv(c, m, page_size, n_pages, true);
+        EEB_CUDA(cudaMemsetAsync(m.kv_depth.p, 0, m.kv_depth.bytes, c->stream));
+        kv_sync_table(c, m);
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+eeb_status eeb_kv_reserve(eeb_ctx* c, int model, int32_t slot, int32_t n_positions) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (slot < 0 || slot >= m.desc.max_slots) throw Error(EEB_E_DOMAIN, "slot out of range");
+        if (n_positions < 0 || n_positions > m.desc.max_seq_len) throw Error(EEB_E_DOMAIN, "positions out of range");
+        kv_reserve(m, slot, n_positions);
+    });
+}
+
+eeb_status eeb_kv_release(eeb_ctx* c, int model, int32_t slot) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (slot < 0 || slot >= m.desc.max_slots) throw Error(EEB_E_DOMAIN, "slot out of range");
+        // the released pages may be handed out by the next reservation: work
+        // already queued on the context stream reads them first (stream order)
+        kv_release(m, slot);
+        EEB_CUDA(cudaMemsetAsync(m.kv_depth.as<uint8_t>() + (size_t)slot * m.desc.max_seq_len, 0,
+                                 m.desc.max_seq_len, c->stream));
+    });
+}
+
+eeb_status eeb_kv_pages(eeb_ctx* c, int model, int32_t* page_size, int32_t* n_pages, int32_t* n_free) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (page_size) *page_size = m.kv_page;
+        if (n_pages) *n_pages = m.kv_pages;
+        if (n_free) *n_free = m.paged ? (int32_t)m.free_pages.size() : 0;
+    });
+}
+
 eeb_status eeb_debug_read_kv(eeb_ctx* c, int model, int layer, int slot, int pos, float* host_k, float* host_v) {
     return guarded([&] {
         Model& m = model_of(c, model);
@@ -1981,8 +2113,10 @@ eeb_status eeb_debug_read_kv(eeb_ctx* c, int model, int layer, int slot, int pos
         const int heads = m.shards * m.hkv_l;
         for (int g = 0; g < heads; ++g) {
             const int sh = g / m.hkv_l, lg = g % m.hkv_l;
+            const int32_t pg = m.h_table[(size_t)slot * m.pages_per_seq + pos / m.kv_page];
+            if (pg < 0) throw Error(EEB_E_DOMAIN, "kv position has no page (paged pool)");
             const size_t off = (size_t)(layer - 1) * m.kv_layer_elems + (size_t)sh * m.kv_shard_elems +
-                               (((size_t)slot * m.hkv_l + lg) * d.max_seq_len + pos) * hd;
+                               (((size_t)pg * m.hkv_l + lg) * m.kv_page + pos % m.kv_page) * hd;
             for (int which = 0; which < 2; ++which) {
                 const DevBuf& b = which == 0 ? m.k_cache : m.v_cache;
                 float* dst = (which == 0 ? host_k : host_v) + (size_t)g * hd;

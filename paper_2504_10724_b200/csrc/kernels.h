@@ -97,7 +97,7 @@ struct AttnArgs {
     const float* qkv;        // partial planes of the QKV GEMM, rows of dq + 2 dkv
     int splits;
     int64_t split_stride;
-    void* k_cache;           // this layer: [slots][Hkv][S][hd]
+    void* k_cache;           // this layer: [pages][Hkv][page_size][hd] (unpaged: page = slot, page_size = S)
     void* v_cache;
     const uint8_t* kv_depth; // [slots][S] layers computed per position
     const float* rope_cos;   // [S][hd/2]
@@ -113,7 +113,17 @@ struct AttnArgs {
     const void* v_map;
     int num_sms;
     int kv_ready = 0;        // prefill: every row's K/V is already in the cache (launch_kv_append)
+    // Paged KV pool: position p of slot s lives in page page_table[s * pages_per_seq + p / page_size]
+    // at row p % page_size.  Unpaged: page_size = max_seq, pages_per_seq = 1, table = identity.
+    const int* page_table = nullptr;
+    int page_size = 0;
+    int pages_per_seq = 1;
 };
+// Device address of (page-table row of slot, position, kv head, dim 0) in a layer's K or V cache.
+__host__ __device__ inline int64_t kv_elem_offset(const AttnArgs& a, int slot, int pos, int g) {
+    const int pg = a.page_table[(int64_t)slot * a.pages_per_seq + pos / a.page_size];
+    return (((int64_t)pg * a.n_kv_heads + g) * a.page_size + pos % a.page_size) * a.head_dim;
+}
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 // Prefill: RoPE the keys and write K/V of every live row into the cache
 // (a chunk's rows attend to each other, so the append precedes the attention).

@@ -67,6 +67,7 @@ EXPORTED = [
     "eeb_debug_read_kv", "eeb_profile_enable", "eeb_profile_read", "eeb_stream",
     "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm", "eeb_debug_bench_layers",
     "eeb_prefill", "eeb_host_stage", "eeb_load_layers_async", "eeb_load_wait",
+    "eeb_kv_configure_pages", "eeb_kv_reserve", "eeb_kv_release", "eeb_kv_pages",
 ]
 
 _lib = None
@@ -289,6 +290,22 @@ class Context:
     def reset_slots(self, model: int, slots) -> None:
         s = np.ascontiguousarray(slots, dtype=np.int32)
         _check(self.lib.eeb_reset_slots(self.h, model, len(s), s.ctypes.data))
+
+    # ---- paged KV pool (eeb_kv_configure_pages & co.) -------------------------
+    def kv_configure_pages(self, model: int, page_size: int, n_pages: int) -> None:
+        _check(self.lib.eeb_kv_configure_pages(self.h, model, page_size, n_pages))
+
+    def kv_reserve(self, model: int, slot: int, n_positions: int) -> None:
+        _check(self.lib.eeb_kv_reserve(self.h, model, slot, n_positions))
+
+    def kv_release(self, model: int, slot: int) -> None:
+        _check(self.lib.eeb_kv_release(self.h, model, slot))
+
+    def kv_pages(self, model: int) -> tuple[int, int, int]:
+        """(page_size, n_pages, n_free)."""
+        ps, n, f = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(self.lib.eeb_kv_pages(self.h, model, C.byref(ps), C.byref(n), C.byref(f)))
+        return ps.value, n.value, f.value
 
     def host_stage(self, model: int, depth: int) -> None:
         _check(self.lib.eeb_host_stage(self.h, model, depth))

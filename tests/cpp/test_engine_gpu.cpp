@@ -137,6 +137,24 @@ int main(int argc, char** argv) {
         CHECK(first > 50.0 && first < 95.0);
         std::printf("ee_single: exit@6 %.1f%%, %.0f tok/s\n", first, rep.throughput_tok_s);
     }
+    {  // continuous batching over a paged KV pool with exactly one page per slot:
+       // every finished request must hand its page back before the next one is
+       // admitted (else CapacityError); per-token decisions match static batching
+        CudaBackend be_st(0);
+        const EngineReport st = BatchedEngine(repo, be_st, make_cfg(Mode::ee_single, "small")).run(reqs);
+        CudaBackend be(0);
+        be.set_kv_pages(64, 16);
+        EngineConfig cc = make_cfg(Mode::ee_single, "small");
+        cc.continuous = true;
+        const EngineReport rep = BatchedEngine(repo, be, cc).run(reqs);
+        check_report(rep, reqs);
+        CHECK(rep.steps < st.steps);
+        for (const auto& [l, p] : st.exit_table.at("small"))  // rows < 3 take the CUDA-core GEMV (other rounding)
+            CHECK(std::fabs((rep.exit_table.at("small").count(l) ? rep.exit_table.at("small").at(l) : 0.0) - p) < 1.0);
+        std::printf("continuous+paged: %lld steps (static %lld), exit@6 %.1f%% (static %.1f%%)\n", (long long)rep.steps,
+                    (long long)st.steps, rep.exit_table.at("small").count(6) ? rep.exit_table.at("small").at(6) : 0.0,
+                    st.exit_table.at("small").count(6) ? st.exit_table.at("small").at(6) : 0.0);
+    }
     {  // vanilla: every token at full depth
         CudaBackend be(0);
         BatchedEngine eng(repo, be, make_cfg(Mode::vanilla, "large"));

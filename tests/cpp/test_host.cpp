@@ -454,7 +454,7 @@ TEST_CASE(decide_action_matches_reference_randomized) {
 
 // ---- the batched engine replaying reference traces at batch 1 ---------------------------
 static void engine_matches_reference(const std::string& trace_path, const std::string& mode_str, Mode mode,
-                                     const std::string& model, int k) {
+                                     const std::string& model, int k, bool continuous = false) {
     const ModelRepository repo = load_repo(fx("repo_opt.json"));
     const Trace trace = load_trace(trace_path);
     const MemoryConfig mem{40'000'000'000, 1'000'000'000, 256, 8.4e9};
@@ -482,6 +482,7 @@ static void engine_matches_reference(const std::string& trace_path, const std::s
     cfg.max_batch = 1;
     cfg.prefill = false;
     cfg.record_events = true;
+    cfg.continuous = continuous;
     BatchedEngine eng(repo, be, cfg);
     std::vector<RequestSpec> reqs;
     for (const auto& r : trace.requests) reqs.push_back({r.request_id, r.prompt_len, r.num_tokens()});
@@ -583,6 +584,55 @@ TEST_CASE(engine_replays_reference_traces_at_batch_1) {
     engine_matches_reference(gen, "ee_single:opt-6.7b", Mode::ee_single, "opt-6.7b", 2);
     engine_matches_reference(gen, "helios", Mode::helios, "", 2);
     engine_matches_reference(fx("eval_quality.jsonl"), "helios", Mode::helios, "", 2);  // PHT 1.47 / 1.49
+}
+
+// Continuous batching (EngineConfig::continuous): at width 1 it is the
+// reference loop (same report, same event log through the reference
+// aggregate()); at width 4 the teacher-forced traces give every token the same
+// observation however requests interleave, so the exit table, perplexity and
+// token count equal the reference's, with decode steps 4 rows wide and the
+// event log still aggregating to the engine's own report.
+TEST_CASE(continuous_batching_matches_reference) {
+    const std::string gen = "/tmp/eeserve_gen_small_cb.jsonl";
+    CHECK(ref_generate_trace(fx("gen_small.json").c_str(), fx("repo_opt.json").c_str(), gen.c_str()) == 10);
+    engine_matches_reference(gen, "ee_single:opt-1.3b", Mode::ee_single, "opt-1.3b", 2, true);
+    engine_matches_reference(gen, "helios", Mode::helios, "", 2, true);
+    const ModelRepository repo = load_repo(fx("repo_opt.json"));
+    const Trace trace = load_trace(gen);
+    std::vector<RequestSpec> reqs;
+    for (const auto& r : trace.requests) reqs.push_back({r.request_id, r.prompt_len, r.num_tokens()});
+    auto run = [&](int width, bool continuous) {
+        TraceBackend be(trace);
+        EngineConfig cfg;
+        cfg.mem = MemoryConfig{40'000'000'000, 1'000'000'000, 256, 8.4e9};
+        cfg.mode = ModeSpec{Mode::ee_single, "opt-1.3b"};
+        cfg.max_batch = width;
+        cfg.prefill = false;
+        cfg.record_events = true;
+        cfg.continuous = continuous;
+        BatchedEngine eng(repo, be, cfg);
+        return eng.run(reqs);
+    };
+    const EngineReport one = run(1, false), cb = run(4, true), st = run(4, false);
+    CHECK(cb.tokens == one.tokens);
+    CHECK(approx(cb.perplexity, one.perplexity, 1e-12));
+    for (const auto& [m, per] : one.exit_table)
+        for (const auto& [l, pct] : per) CHECK(approx(cb.exit_table.at(m).at(l), pct, 1e-12));
+    CHECK(cb.achieved_batch_size == 4);
+    CHECK(cb.steps < one.steps);
+    CHECK(cb.steps <= st.steps);  // a freed slot is refilled at once: never more steps than static batches
+    CHECK(cb.requests.size() == reqs.size());
+    const std::string log = "/tmp/eeserve_engine_events_cb.jsonl";
+    write_event_log(cb.events, log);
+    std::vector<char> ab(1 << 24);
+    CHECK(ref_aggregate(log.c_str(), ab.data(), (int)ab.size()) > 0);
+    const Json agg = Json::parse(ab.data());
+    const Json& a = agg.at("aggregates");
+    CHECK(approx(a.at("throughput_tok_s").get<double>(), cb.throughput_tok_s, 1e-9));
+    CHECK(approx(a.at("perplexity").get<double>(), cb.perplexity, 1e-12));
+    CHECK(approx(a.at("mean_ttft_s").get<double>(), cb.mean_ttft_s, 1e-9));
+    CHECK(a.at("achieved_batch_size").get<int>() == 4);
+    CHECK(agg.at("per_request").size() == reqs.size());
 }
 
 int main(int argc, char** argv) {
