@@ -386,14 +386,17 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
     // RoPE row and the KV-depth bytes of the positions, fetched in the same
     // latency window as the planes (not as dependent global loads later).
     __shared__ float cs[HD / 2], sn[HD / 2];
-    __shared__ uint8_t dep_s[CP];
+    // KV depth bytes of every position (all chunks, not only the first: a
+    // global read inside the score loop stalls on long scoreboard)
+    constexpr int kDep = CP > 1024 ? CP : 1024;
+    __shared__ uint8_t dep_s[kDep];
     for (int t = threadIdx.x; t < half; t += blockDim.x) {
         cs[t] = a.rope_cos[(int64_t)pos * half + t];
         sn[t] = a.rope_sin[(int64_t)pos * half + t];
     }
     {
         const uint8_t* dsrc = a.kv_depth + (int64_t)slot * a.max_seq;
-        for (int t = threadIdx.x; t < CP && t <= pos; t += blockDim.x) dep_s[t] = dsrc[t];
+        for (int t = threadIdx.x; t < kDep && t <= pos; t += blockDim.x) dep_s[t] = dsrc[t];
     }
     __syncthreads();
     // RoPE: queries (scaled) into q_s, the new key/value into the cache and kn_s / vn_s.
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int p = c0 + t * 8 + kq + e;
-                const bool valid = h < G && p <= pos && (p == pos || (c0 == 0 ? dep_s[p] : depth[p]) >= a.layer);
+                const bool valid = h < G && p <= pos && (p == pos || (p < kDep ? dep_s[p] : depth[p]) >= a.layer);
                 sc[tt][e] = valid ? c[e] : -INFINITY;
                 cmax = fmaxf(cmax, sc[tt][e]);
             }
