@@ -288,7 +288,7 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 // CP: positions per chunk; NB: chunk buffers (2 = the next chunk's TMA is in
 // flight while this one computes)
 template <int HD, int CP, int NB, bool PAGED>
-__global__ void __launch_bounds__(kMmaWarps * 32)
+__global__ void __launch_bounds__(kMmaWarps * 32, HD == 64 ? 5 : 1)  // hd 64: 5 CTAs/SM (register-limited)
     attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          AttnArgs a) {
     constexpr int CB = HD / 64;                    // 64-dim column blocks
@@ -1046,8 +1046,9 @@ void launch_mma(const AttnArgs& a, cudaStream_t s) {
     // measured C2 (hd 64, context 128..227): 64 positions 1.56 ms/step, 128 1.61, 256 1.64
     const int cp = env_cp > 0 ? env_cp : (HD == 64 ? 64 : 128);
     static const int env_nb = std::getenv("EEB_ATTN_NB") ? std::atoi(std::getenv("EEB_ATTN_NB")) : 0;
-    // double-buffered chunks measured slower on C2 (1.548 vs 1.515 ms/step): opt-in
-    const int nb = env_nb > 0 ? env_nb : 1;
+    // double-buffered 64-position chunks at 5 CTAs/SM: C2 1.497 vs 1.565 ms/step
+    // single-buffered (same box, two orders)
+    const int nb = env_nb > 0 ? env_nb : (cp <= 64 ? 2 : 1);
     if (nb >= 2) {
         if (cp <= 32) launch_mma_cp<HD, 32, 2>(a, s);
         else if (cp <= 64) launch_mma_cp<HD, 64, 2>(a, s);
