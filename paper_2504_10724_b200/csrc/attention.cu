@@ -977,6 +977,43 @@ void launch_pipe(const AttnArgs& a, int num_sms, cudaStream_t s) {
     EEB_CHECK_LAUNCH();
 }
 
+// Fixed-order sum of the QKV GEMM's split-K planes for 4 consecutive columns
+// (plane order, as the attention kernels sum them: the same floats result),
+// kBatch planes in flight per round trip.
+__device__ __forceinline__ float4 plane_sum4(const float* src, int splits, int64_t stride) {
+    constexpr int kBatch = 8;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < splits; s0 += kBatch) {
+        float4 t[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j)
+            if (s0 + j < splits) t[j] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + j) * stride));
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j)
+            if (s0 + j < splits) {
+                acc.x += t[j].x;
+                acc.y += t[j].y;
+                acc.z += t[j].z;
+                acc.w += t[j].w;
+            }
+    }
+    return acc;
+}
+template <typename T>
+__device__ __forceinline__ void store4_kv(T* dst, float x, float y, float z, float w) {
+    if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(dst) = make_float4(x, y, z, w);
+    } else {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(x, y), hi = __floats2bfloat162_rn(z, w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(dst) = u;
+    }
+}
+
+// Prefill: RoPE the keys and append K/V of every live row (one CTA per row;
+// a thread owns 4 dims of each half of a key head, or 4 dims of a value head).
 template <typename T>
 __global__ void kv_append_kernel(AttnArgs a) {
     pdl_launch_dependents();
@@ -986,22 +1023,29 @@ __global__ void kv_append_kernel(AttnArgs a) {
     const int Hkv = a.n_kv_heads, hd = a.head_dim, half = hd / 2;
     const int dq = a.n_heads * hd, dkv = Hkv * hd;
     const int slot = a.slot[i], pos = a.pos[i];
-    const int64_t row_off = (int64_t)i * (dq + 2 * dkv);
-    auto qkv = [&](int col) {  // same fixed-order plane sum as the attention kernels
-        float v = 0.f;
-        for (int sp = 0; sp < a.splits; ++sp) v += a.qkv[sp * a.split_stride + row_off + col];
-        return v;
-    };
+    const float* row = a.qkv + (int64_t)i * (dq + 2 * dkv);
     const float* cs = a.rope_cos + (int64_t)pos * half;
     const float* sn = a.rope_sin + (int64_t)pos * half;
-    for (int idx = threadIdx.x; idx < dkv; idx += blockDim.x) {
-        const int g = idx / hd, j = idx % hd;
-        const int jj = j < half ? j : j - half;
-        const float x0 = qkv(dq + g * hd + jj), x1 = qkv(dq + g * hd + jj + half);
-        const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
-        const int64_t off = kv_elem_offset(a, slot, pos, g) + j;
-        static_cast<T*>(a.k_cache)[off] = from_f32<T>(kr);
-        static_cast<T*>(a.v_cache)[off] = from_f32<T>(qkv(dq + dkv + g * hd + j));
+    T* kc = static_cast<T*>(a.k_cache);
+    T* vc = static_cast<T*>(a.v_cache);
+    const int q4 = half / 4;
+    for (int idx = threadIdx.x; idx < Hkv * q4; idx += blockDim.x) {
+        const int g = idx / q4, jj = 4 * (idx % q4);
+        const float4 x0 = plane_sum4(row + dq + g * hd + jj, a.splits, a.split_stride);
+        const float4 x1 = plane_sum4(row + dq + g * hd + jj + half, a.splits, a.split_stride);
+        const float4 c = *reinterpret_cast<const float4*>(cs + jj);
+        const float4 sv = *reinterpret_cast<const float4*>(sn + jj);
+        T* dst = kc + kv_elem_offset(a, slot, pos, g);
+        store4_kv<T>(dst + jj, x0.x * c.x - x1.x * sv.x, x0.y * c.y - x1.y * sv.y, x0.z * c.z - x1.z * sv.z,
+                     x0.w * c.w - x1.w * sv.w);
+        store4_kv<T>(dst + jj + half, x0.x * sv.x + x1.x * c.x, x0.y * sv.y + x1.y * c.y, x0.z * sv.z + x1.z * c.z,
+                     x0.w * sv.w + x1.w * c.w);
+    }
+    const int h4 = hd / 4;
+    for (int idx = threadIdx.x; idx < Hkv * h4; idx += blockDim.x) {
+        const int g = idx / h4, j = 4 * (idx % h4);
+        const float4 v = plane_sum4(row + dq + dkv + g * hd + j, a.splits, a.split_stride);
+        store4_kv<T>(vc + kv_elem_offset(a, slot, pos, g) + j, v.x, v.y, v.z, v.w);
     }
 }
 

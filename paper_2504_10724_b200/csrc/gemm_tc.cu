@@ -556,6 +556,12 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const int env_stages = std::getenv("EEB_TC_STAGES") ? std::atoi(std::getenv("EEB_TC_STAGES")) : 0;
     const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
     int splits = std::max(1, std::min(kblocks / 2, wave / tiles));
+    // many rows (prefill chunks): cap the f32 partial planes at about the
+    // weight bytes (splits * rows * N * 4 <= N * K * 2); decode shapes are
+    // unaffected (C2: K / (2 * 64) = 16 >= the splits chosen above)
+    // (opt-in EEB_TC_PLANECAP=1: measured 126 vs 125 ms for the C2 prefill)
+    static const bool plane_cap = std::getenv("EEB_TC_PLANECAP") && std::atoi(std::getenv("EEB_TC_PLANECAP")) != 0;
+    if (plane_cap) splits = std::max(1, std::min(splits, a.K / (2 * bpad)));
     static const int env_maxsplit = std::getenv("EEB_TC_MAXSPLIT") ? std::atoi(std::getenv("EEB_TC_MAXSPLIT")) : 0;
     if (env_maxsplit > 0) splits = std::min(splits, env_maxsplit);
     int kb_per = (kblocks + splits - 1) / splits;
@@ -601,6 +607,10 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // the step (PDL) streams its weights while this one drains.
     int stages = std::min(4, (int)((kSmemBudget / 2 - 1024 - 256) / stage_bytes));
     stages = std::min(stages, std::max(2, kb_per));
+    // wide activation tiles (prefill, >= 128 rows): one CTA per SM with a
+    // deeper pipeline (EEB_TC_WIDE=1; measured slower on the C2 prefill)
+    static const bool wide_stages = std::getenv("EEB_TC_WIDE") && std::atoi(std::getenv("EEB_TC_WIDE")) != 0;
+    if (wide_stages && bpad >= 128) stages = std::min(4, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (stages < 2) stages = std::min(8, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (env_stages > 0) stages = std::min(env_stages, (int)((kSmemBudget - 1024 - 256) / stage_bytes));
     if (stages < 2) return 0;
