@@ -1049,6 +1049,246 @@ __global__ void kv_append_kernel(AttnArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Prefill attention on the tensor cores (flash-attention forward, mma.sync
+// m16n8k16 bf16): one CTA per (query block, query head).  A block is <= 64
+// consecutive prompt rows of one sequence; each of the 4 warps owns 16 of
+// them.  The block's K/V (its sequence's positions [0, last row's position])
+// stream once through double-buffered 64-position TMA chunks shared by all
+// 64 query rows — the per-row decode kernel would re-read them per row.
+// Masking is the decode rule per row: position p is visible to the row at
+// position r iff p <= r and (p == r or kv_depth[p] >= layer).
+// ---------------------------------------------------------------------------
+template <int HD, bool PAGED>
+__global__ void __launch_bounds__(128)
+    attention_prefill_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                             AttnArgs a) {
+    constexpr int CB = HD / 64, CP = 64, NT = HD / 8, KS = HD / 16, NB = 2;
+    constexpr uint32_t kBlockBytes = CP * 128, kBufBytes = 2 * CB * kBlockBytes;
+    constexpr int kDep = 1024, kMaxPt = PAGED ? 64 : 1;
+    pdl_launch_dependents();
+    pdl_wait();
+    const int item = blockIdx.y;
+    if (item >= *a.pf_n_items) return;
+    const int4 it = a.pf_items[item];  // {first row, rows, slot, first position}
+    const int hq = blockIdx.x;
+    const int H = a.n_heads, Hkv = a.n_kv_heads, G = H / Hkv, g = hq / G;
+    const int dq = H * HD, dkv = Hkv * HD, half = HD / 2;
+    const int r0 = it.x, nrows = it.y, slot = it.z, p0 = it.w;
+    const int last = p0 + nrows - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    uint8_t* base = smem_raw + (sbase - raw);
+    __nv_bfloat16* q_s = reinterpret_cast<__nv_bfloat16*>(base + NB * kBufBytes);  // [64][HD]
+    __shared__ uint8_t dep_s[kDep];
+    __shared__ int pt_s[kMaxPt];
+    __shared__ __align__(8) uint64_t bars[NB];
+    const int PS = PAGED ? a.page_size : a.max_seq;
+    if constexpr (PAGED) {
+        for (int t = threadIdx.x; t < a.pages_per_seq && t < kMaxPt; t += blockDim.x)
+            pt_s[t] = a.page_table[(int64_t)slot * a.pages_per_seq + t];
+        __syncthreads();
+    }
+    auto page_of = [&](int p) { return PAGED ? pt_s[p / PS] : slot; };
+    auto row_of = [&](int p) { return PAGED ? p % PS : p; };
+    const int n_chunks = last / CP + 1;
+    auto issue = [&](int ci) {  // thread 0
+        const int c0 = ci * CP, buf = ci % NB;
+        const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
+        const uint32_t bar = smem_u32(&bars[buf]);
+        const int n_load = min(CP, last + 1 - c0);
+        const int boxes = (n_load + kBoxRows - 1) / kBoxRows;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)boxes * CB * kBoxRows * 128 * 2)
+                     : "memory");
+        for (int b = 0; b < boxes; ++b) {
+            const int p = c0 + b * kBoxRows;
+            const int zc = page_of(p) * Hkv + g;
+            for (int cb = 0; cb < CB; ++cb) {
+                const uint32_t off = cb * kBlockBytes + b * kBoxRows * 128;
+                tma_3d(k_s + off, &kmap, bar, cb * 64, row_of(p), zc);
+                tma_3d(v_s + off, &vmap, bar, cb * 64, row_of(p), zc);
+            }
+        }
+    };
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&vmap)) : "memory");
+        for (int b = 0; b < NB; ++b) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[b])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int c = 0; c < NB && c < n_chunks; ++c) issue(c);
+    }
+    // queries: fixed-order plane sums, RoPE at each row's position, 1/sqrt(hd), bf16
+    const float qscale = rsqrtf((float)HD);
+    for (int idx = threadIdx.x; idx < 64 * (half / 4); idx += blockDim.x) {
+        const int r = idx / (half / 4), jj = 4 * (idx % (half / 4));
+        float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
+        if (r < nrows) {
+            const float* src = a.qkv + (int64_t)(r0 + r) * (dq + 2 * dkv) + hq * HD + jj;
+            lo = plane_sum4(src, a.splits, a.split_stride);
+            hi = plane_sum4(src + half, a.splits, a.split_stride);
+            const int pos = p0 + r;
+            const float4 c = *reinterpret_cast<const float4*>(a.rope_cos + (int64_t)pos * half + jj);
+            const float4 sv = *reinterpret_cast<const float4*>(a.rope_sin + (int64_t)pos * half + jj);
+            const float4 l2 = make_float4((lo.x * c.x - hi.x * sv.x) * qscale, (lo.y * c.y - hi.y * sv.y) * qscale,
+                                          (lo.z * c.z - hi.z * sv.z) * qscale, (lo.w * c.w - hi.w * sv.w) * qscale);
+            const float4 h2 = make_float4((lo.x * sv.x + hi.x * c.x) * qscale, (lo.y * sv.y + hi.y * c.y) * qscale,
+                                          (lo.z * sv.z + hi.z * c.z) * qscale, (lo.w * sv.w + hi.w * c.w) * qscale);
+            lo = l2;
+            hi = h2;
+        }
+        store4_kv<__nv_bfloat16>(q_s + r * HD + jj, lo.x, lo.y, lo.z, lo.w);
+        store4_kv<__nv_bfloat16>(q_s + r * HD + jj + half, hi.x, hi.y, hi.z, hi.w);
+    }
+    {
+        const uint8_t* dsrc = a.kv_depth + (int64_t)slot * a.max_seq;
+        for (int t = threadIdx.x; t < kDep && t <= last; t += blockDim.x) dep_s[t] = dsrc[t];
+    }
+    __syncthreads();
+    // A fragments of this warp's 16 query rows: rows gq and gq + 8
+    const int gq = lane >> 2, kq = (lane & 3) * 2;
+    const int ra = 16 * warp + gq, rb = ra + 8;
+    auto q2 = [&](int r, int d) { return *reinterpret_cast<const uint32_t*>(q_s + r * HD + d); };
+    uint32_t qa[KS][4];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+        qa[k][0] = q2(ra, 16 * k + kq);
+        qa[k][1] = q2(rb, 16 * k + kq);
+        qa[k][2] = q2(ra, 16 * k + 8 + kq);
+        qa[k][3] = q2(rb, 16 * k + 8 + kq);
+    }
+    const int pos_a = p0 + ra, pos_b = p0 + rb;  // rows >= nrows: masked everywhere, never stored
+    const bool live_a = ra < nrows, live_b = rb < nrows;
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+    const uint8_t* depth = a.kv_depth + (int64_t)slot * a.max_seq;
+    auto visible = [&](int p, int pos, bool live) {
+        return live && p <= pos && (p == pos || (p < kDep ? dep_s[p] : depth[p]) >= a.layer);
+    };
+    // this warp's rows see no position past its last row
+    const int warp_last = min(last, p0 + 16 * warp + 15);
+    for (int ci = 0; ci < n_chunks; ++ci) {
+        const int c0 = ci * CP, buf = ci % NB;
+        const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
+        mbar_wait(smem_u32(&bars[buf]), (uint32_t)((ci / NB) & 1));
+        // tiles the TMA wrote (whole 32-row boxes: an even count); rows past
+        // them hold stale shared memory, which may not even be finite
+        const int loaded = 4 * ((min(CP, last + 1 - c0) + kBoxRows - 1) / kBoxRows);
+        if (c0 <= warp_last) {
+            float sc[CP / 8][4];
+#pragma unroll
+            for (int t = 0; t < CP / 8; ++t) {
+                sc[t][0] = sc[t][1] = sc[t][2] = sc[t][3] = -INFINITY;
+                if (t >= loaded) continue;
+                float c[4] = {0.f, 0.f, 0.f, 0.f};
+                const int row = t * 8 + (lane & 7);
+#pragma unroll
+                for (int k2 = 0; k2 < KS; k2 += 2) {
+                    const int mi = lane >> 3;
+                    const int dim = 16 * (k2 + (mi >> 1)) + 8 * (mi & 1);
+                    uint32_t b[4];
+                    ldsm_x4(k_s + (dim / 64) * kBlockBytes + swz(row, (dim % 64) / 8), b);
+                    mma_bf16(c, qa[k2], b[0], b[1]);
+                    mma_bf16(c, qa[k2 + 1], b[2], b[3]);
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int p = c0 + t * 8 + kq + e;
+                    sc[t][e] = visible(p, pos_a, live_a) ? c[e] : -INFINITY;
+                    sc[t][2 + e] = visible(p, pos_b, live_b) ? c[2 + e] : -INFINITY;
+                }
+            }
+            float mxa = -INFINITY, mxb = -INFINITY;
+#pragma unroll
+            for (int t = 0; t < CP / 8; ++t) {
+                mxa = fmaxf(mxa, fmaxf(sc[t][0], sc[t][1]));
+                mxb = fmaxf(mxb, fmaxf(sc[t][2], sc[t][3]));
+            }
+            mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 1));
+            mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 2));
+            mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 1));
+            mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 2));
+            const float na = fmaxf(m_a, mxa), nb = fmaxf(m_b, mxb);
+            const float sa = na == -INFINITY ? 1.f : __expf(m_a - na), sb = nb == -INFINITY ? 1.f : __expf(m_b - nb);
+            float psa = 0.f, psb = 0.f;
+#pragma unroll
+            for (int t = 0; t < CP / 8; ++t) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    sc[t][e] = sc[t][e] == -INFINITY ? 0.f : __expf(sc[t][e] - na);
+                    sc[t][2 + e] = sc[t][2 + e] == -INFINITY ? 0.f : __expf(sc[t][2 + e] - nb);
+                    psa += sc[t][e];
+                    psb += sc[t][2 + e];
+                }
+            }
+            psa += __shfl_xor_sync(0xffffffffu, psa, 1);
+            psa += __shfl_xor_sync(0xffffffffu, psa, 2);
+            psb += __shfl_xor_sync(0xffffffffu, psb, 1);
+            psb += __shfl_xor_sync(0xffffffffu, psb, 2);
+            l_a = l_a * sa + psa;
+            l_b = l_b * sb + psb;
+            m_a = na;
+            m_b = nb;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                o[n][0] *= sa;
+                o[n][1] *= sa;
+                o[n][2] *= sb;
+                o[n][3] *= sb;
+            }
+            // P.V: k = 16 positions = tiles (2j, 2j+1)
+#pragma unroll
+            for (int tp = 0; tp < CP / 8; tp += 2) {
+                if (tp >= loaded) break;
+                uint32_t pa[4];
+                pa[0] = pack_bf16(sc[tp][0], sc[tp][1]);
+                pa[1] = pack_bf16(sc[tp][2], sc[tp][3]);
+                pa[2] = pack_bf16(sc[tp + 1][0], sc[tp + 1][1]);
+                pa[3] = pack_bf16(sc[tp + 1][2], sc[tp + 1][3]);
+                const int mi = lane >> 3;
+                const int row = (tp + (mi & 1)) * 8 + (lane & 7);
+#pragma unroll
+                for (int n = 0; n < NT; n += 2) {
+                    const int dim = 8 * (n + (mi >> 1));
+                    uint32_t b[4];
+                    ldsm_x4_t(v_s + (dim / 64) * kBlockBytes + swz(row, (dim % 64) / 8), b);
+                    mma_bf16(o[n], pa, b[0], b[1]);
+                    mma_bf16(o[n + 1], pa, b[2], b[3]);
+                }
+            }
+        }
+        __syncthreads();  // every warp is past this chunk: its buffer takes chunk ci + NB
+        if (threadIdx.x == 0 && ci + NB < n_chunks) issue(ci + NB);
+    }
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
+    const float ia = l_a > 0.f ? 1.f / l_a : 0.f, ib = l_b > 0.f ? 1.f / l_b : 0.f;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        const int d = 8 * n + kq;
+        if (live_a)
+            *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + ra) * dq + hq * HD + d) = pack_bf16(o[n][0] * ia, o[n][1] * ia);
+        if (live_b)
+            *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + rb) * dq + hq * HD + d) = pack_bf16(o[n][2] * ib, o[n][3] * ib);
+    }
+}
+
+template <int HD>
+void launch_prefill_attn(const AttnArgs& a, cudaStream_t s) {
+    const size_t smem = 1024 + 2 * 2 * (size_t)(HD / 64) * 64 * 128 + 64 * HD * 2;
+    const bool paged = a.page_size != a.max_seq;
+    auto kern = paged ? attention_prefill_kernel<HD, true> : attention_prefill_kernel<HD, false>;
+    EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    launch_pdl(kern, dim3(a.n_heads, a.pf_max_items), dim3(128), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
+               *static_cast<const CUtensorMap*>(a.v_map), a);
+    EEB_CHECK_LAUNCH();
+}
+
 __global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
                                   uint8_t* kv_depth, int max_seq, int depth) {
     pdl_launch_dependents();
@@ -1123,6 +1363,13 @@ void launch_mark_depth(int rows, const int* slot, const int* pos, uint8_t* kv_de
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {
     const bool paged = a.page_size != a.max_seq;
+    static const bool no_pf_attn = std::getenv("EEB_PREFILL_ATTN") && std::atoi(std::getenv("EEB_PREFILL_ATTN")) == 0;
+    if (a.kv_ready && a.pf_items && !no_pf_attn && a.dtype == 1 && a.k_map && a.v_map &&
+        (a.head_dim == 64 || a.head_dim == 128) && a.max_seq <= 1024) {
+        if (a.head_dim == 64) launch_prefill_attn<64>(a, s);
+        else launch_prefill_attn<128>(a, s);
+        return;
+    }
     if (a.dtype == 1 && a.k_map && a.v_map && a.n_heads / a.n_kv_heads <= 8 &&
         (a.head_dim == 64 || a.head_dim == 128)) {
         if (paged) {  // only the one-item kernel walks page tables

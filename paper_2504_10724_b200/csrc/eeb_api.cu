@@ -184,7 +184,9 @@ struct eeb_ctx {
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
     eeb::DevBuf head_tok, head_conf, head_logp, head_tri;
     eeb::DevBuf tp_partial;         // row-parallel partial sums all-reduced across TP ranks
-    eeb::DevBuf pf_meta;            // prefill (tok, slot, pos) of every prompt token
+    eeb::DevBuf pf_meta;            // prefill (tok, slot, pos) of every prompt token, then the query blocks
+    eeb::DevBuf pf_items;           // the current chunk's query blocks (int4) + their count
+    int pf_cur_items = 0;           // query blocks of the chunk being enqueued (graph key)
     void* pf_pin = nullptr;
     size_t pf_pin_bytes = 0;
     eeb::DevBuf o_exit, o_tok, o_conf, o_logp, o_breach, o_unch, o_bin, o_hist, o_nbr, o_sum;
@@ -866,6 +868,11 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         a.page_table = m.page_table.as<int>();
         a.page_size = m.kv_page;
         a.pages_per_seq = m.pages_per_seq;
+        if (kv_ready && c->pf_cur_items > 0) {
+            a.pf_items = c->pf_items.as<int4>();
+            a.pf_n_items = reinterpret_cast<const int*>(c->pf_items.as<int4>() + c->pf_cur_items);
+            a.pf_max_items = c->pf_cur_items;
+        }
         a.out = static_cast<char*>(c->attn.p) + (size_t)sh * batch * m.dq_l * wb;
         const size_t mk = (size_t)(l - 1) * m.shards + sh;
         a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[mk].data();
@@ -1139,7 +1146,7 @@ void run_prefill_chunk(eeb_ctx* c, int mi, int depth, int rows) {
         enqueue_prefill(c, mi, depth, rows);
         return;
     }
-    GraphKey key{mi, depth, kPolicyPrefill, rows, c->gemm_tier, 0u};
+    GraphKey key{mi, depth, kPolicyPrefill, rows, c->gemm_tier, (uint32_t)c->pf_cur_items};
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         cudaGraph_t g;
@@ -1928,12 +1935,33 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
         ensure_workspace(c, m, (int)std::min<int64_t>(chunk, total));
         // (tok, slot, pos) of every prompt token: one pinned staging + one H2D,
         // then a device-to-device slice per chunk.
+        // query blocks of every chunk for the tensor-core prefill attention:
+        // runs of consecutive rows of one sequence (consecutive positions),
+        // at most 64 rows, never across a chunk boundary
+        std::vector<std::vector<int4>> chunk_items;
+        {
+            int64_t t0 = 0;
+            for (int k = 0; k < n_seq; t0 += lens[k], ++k)
+                for (int j = 0; j < lens[k];) {
+                    const int64_t row = t0 + j;
+                    const int64_t ci = row / chunk;
+                    while ((int64_t)chunk_items.size() <= ci) chunk_items.emplace_back();
+                    const int in_chunk = (int)(row - ci * chunk);
+                    const int n = (int)std::min<int64_t>({64, lens[k] - j, (ci + 1) * chunk - row});
+                    chunk_items[ci].push_back(make_int4(in_chunk, n, slot_ids[k], start_pos[k] + j));
+                    j += n;
+                }
+        }
+        size_t max_items = 0;
+        for (const auto& v : chunk_items) max_items = std::max(max_items, v.size());
+        const size_t item_bytes = chunk_items.size() * (max_items + 1) * sizeof(int4);
         const size_t meta = (size_t)total * 3 * 4;
-        if (meta > c->pf_pin_bytes) {
+        const size_t meta_al = ((meta + 15) / 16) * 16;
+        if (meta_al + item_bytes > c->pf_pin_bytes) {
             if (c->pf_pin) cudaFreeHost(c->pf_pin);
             c->pf_pin = nullptr;
-            EEB_CUDA(cudaMallocHost(&c->pf_pin, meta));
-            c->pf_pin_bytes = meta;
+            EEB_CUDA(cudaMallocHost(&c->pf_pin, meta_al + item_bytes));
+            c->pf_pin_bytes = meta_al + item_bytes;
         }
         int32_t* ht = static_cast<int32_t*>(c->pf_pin);
         int32_t* hs = ht + total;
@@ -1945,18 +1973,36 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
                 hs[t] = slot_ids[k];
                 hp[t] = start_pos[k] + j;
             }
-        c->pf_meta.ensure(meta);
+        // per chunk: max_items + 1 int4 (the blocks, then their count in .x)
+        int4* hi = reinterpret_cast<int4*>(static_cast<char*>(c->pf_pin) + meta_al);
+        for (size_t ci = 0; ci < chunk_items.size(); ++ci) {
+            int4* dst = hi + ci * (max_items + 1);
+            for (size_t q = 0; q < chunk_items[ci].size(); ++q) dst[q] = chunk_items[ci][q];
+            dst[chunk_items[ci].size()] = make_int4((int)chunk_items[ci].size(), 0, 0, 0);
+        }
+        c->pf_meta.ensure(meta_al + item_bytes);
         int32_t* dm = c->pf_meta.as<int32_t>();
         cudaStream_t s = c->stream;
-        EEB_CUDA(cudaMemcpyAsync(dm, ht, meta, cudaMemcpyHostToDevice, s));
+        EEB_CUDA(cudaMemcpyAsync(dm, ht, meta_al + item_bytes, cudaMemcpyHostToDevice, s));
+        const int4* di = reinterpret_cast<const int4*>(reinterpret_cast<const char*>(dm) + meta_al);
+        c->pf_items.ensure((max_items + 1) * sizeof(int4));
         Ints I = ints_of(c);
         for (int64_t c0 = 0; c0 < total; c0 += chunk) {
             const int rows = (int)std::min<int64_t>(chunk, total - c0);
+            const size_t ci = (size_t)(c0 / chunk);
             EEB_CUDA(cudaMemcpyAsync(I.tok, dm + c0, (size_t)rows * 4, cudaMemcpyDeviceToDevice, s));
             EEB_CUDA(cudaMemcpyAsync(I.slot, dm + total + c0, (size_t)rows * 4, cudaMemcpyDeviceToDevice, s));
             EEB_CUDA(cudaMemcpyAsync(I.pos, dm + 2 * total + c0, (size_t)rows * 4, cudaMemcpyDeviceToDevice, s));
+            // this chunk's blocks, then the count right after them (the kernel's pf_n_items)
+            const int n_items = (int)chunk_items[ci].size();
+            EEB_CUDA(cudaMemcpyAsync(c->pf_items.p, di + ci * (max_items + 1), (size_t)n_items * sizeof(int4),
+                                     cudaMemcpyDeviceToDevice, s));
+            EEB_CUDA(cudaMemcpyAsync(c->pf_items.as<int4>() + n_items, di + ci * (max_items + 1) + n_items,
+                                     sizeof(int4), cudaMemcpyDeviceToDevice, s));
+            c->pf_cur_items = n_items;
             run_prefill_chunk(c, model, depth, rows);
         }
+        c->pf_cur_items = 0;
         EEB_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -118,6 +118,12 @@ struct AttnArgs {
     const int* page_table = nullptr;
     int page_size = 0;
     int pages_per_seq = 1;
+    // Prefill (kv_ready): query blocks of <= 64 consecutive rows of one
+    // sequence, {first row, rows, slot, position of the first row}; the
+    // tensor-core prefill kernel runs one CTA per (block, query head).
+    const int4* pf_items = nullptr;
+    const int* pf_n_items = nullptr;
+    int pf_max_items = 0;
 };
 // Device address of (page-table row of slot, position, kv head, dim 0) in a layer's K or V cache.
 __host__ __device__ inline int64_t kv_elem_offset(const AttnArgs& a, int slot, int pos, int g) {

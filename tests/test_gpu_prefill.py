@@ -74,17 +74,38 @@ def test_prefill_matches_oracle_tokenwise(ctx, depth_policy):
     ref.close() if hasattr(ref, "close") else None
 
 
-def test_prefill_bf16_chunk_boundary(ctx):
-    """bf16, > 256 prompt tokens: two chunks, one sequence split across them."""
-    desc = eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, name="tiny-bf16-pf", max_slots=8, max_seq_len=160)
+HD128 = eeb.ModelDesc("pf-gqa-hd128", 4, 1024, 8, 2, 1024, 1000, (2, 4), dtype=eeb.BF16, max_slots=8,
+                      max_seq_len=160)
+
+
+@pytest.mark.parametrize("which", ["tiny", "gqa-hd128", "paged", "history"])
+def test_prefill_bf16_chunk_boundary(ctx, which):
+    """bf16, > 256 prompt tokens: two chunks, one sequence split across them;
+    the tensor-core prefill attention (64-row query blocks, causal within the
+    chunk) on MHA head_dim 64, GQA head_dim 128, a paged pool, and prompts
+    that continue a sequence with decoded history (start position > 0)."""
+    if which == "gqa-hd128":
+        desc = HD128
+    else:
+        desc = eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, name="tiny-bf16-pf-" + which, max_slots=8,
+                                           max_seq_len=192)
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
+    if which == "paged":
+        ctx.kv_configure_pages(m, 64, 20)
+        ctx.kv_reserve(m, 7, 64)  # page 0 taken: the sequences' pages differ from their slots
     ref = OracleModel(desc)
     ref.load(desc.num_layers)
     rng = np.random.default_rng(5)
     slots = np.array([0, 1, 2])
     lens = [150, 90, 40]  # 280 tokens: chunk 0 = seq 0 + 106 tokens of seq 1
     start = np.zeros(3, np.int32)
+    if which == "history":  # 7 decoded tokens before slot 1's prompt (its blocks start at position 7)
+        hist = rng.integers(0, desc.vocab, 7)
+        for p in range(7):
+            ctx.decode_step(m, 0, eeb.FULL_DEPTH, TH, [1], [hist[p]], [p])
+            ref.decode_step(0, eeb.FULL_DEPTH, TH, [1], [hist[p]], [p])
+        start[1] = 7
     prompts = [rng.integers(0, desc.vocab, n) for n in lens]
     ctx.prefill(m, desc.num_layers, slots, prompts, start)
     _tokenwise(lambda s, t, p: ref.decode_step(0, eeb.FULL_DEPTH, TH, s, t, p), slots, prompts, start)
@@ -92,15 +113,15 @@ def test_prefill_bf16_chunk_boundary(ctx):
     for i, s in enumerate(slots):
         for k in (0, lens[i] // 2, lens[i] - 1):
             for layer in (1, desc.num_layers):
-                gk, gv = ctx.read_kv(m, layer, int(s), k)
-                rk, rv = ref.read_kv(layer, int(s), k)
+                gk, gv = ctx.read_kv(m, layer, int(s), int(start[i] + k))
+                rk, rv = ref.read_kv(layer, int(s), int(start[i] + k))
                 for g_, r_ in ((gk, rk), (gv, rv)):
                     worst = max(worst, float(np.abs(g_ - r_).max() / max(1e-6, np.abs(r_).max())))
     assert worst < 0.05, worst  # bf16 activations through 12 layers
     agree = []
     for step in range(4):
         nxt = rng.integers(0, desc.vocab, 3)
-        pos = np.array(lens) + step
+        pos = start + np.array(lens) + step
         g = ctx.decode_step(m, 0, eeb.INTROSPECTIVE, TH, slots, nxt, pos)
         r = ref.decode_step(0, eeb.INTROSPECTIVE, TH, slots, nxt, pos)
         agree.extend(g["token_id"] == r["token_id"])
