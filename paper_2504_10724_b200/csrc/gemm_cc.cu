@@ -26,11 +26,30 @@ __global__ void __launch_bounds__(kWarps * 32)
     T* xs = reinterpret_cast<T*>(smem_raw);  // [MAXB][KS]
 
     pdl_launch_dependents();
+    const int k0 = blockIdx.y * KS;
+    const int kn = min(KS, K - k0);
+    // The weights do not depend on the predecessor: pull this CTA's slice
+    // (one K-span per weight row) into L2 while the predecessor drains, so
+    // the stream after the wait runs out of L2 — at 1-2 rows the GEMV's
+    // weight stream is otherwise fully exposed after every kernel boundary.
+    // Skipped when no row is live (every row exited early): the count is read
+    // before the wait, so it may be stale — that costs only a useless or a
+    // missed prefetch; the count after the wait decides what is computed.
+    static constexpr bool kL2Prefetch = false;  // measured: B=1 C2 0.78 -> 0.85 ms/step with it
+    if (kL2Prefetch && threadIdx.x < kRowsPerCta && *reinterpret_cast<const volatile int*>(n_active) > 0) {
+        const int n = blockIdx.x * kRowsPerCta + threadIdx.x;
+        if (n < N) {
+            const char* src = reinterpret_cast<const char*>(W + (int64_t)n * K + k0);
+            const uint32_t bytes = (uint32_t)(kn * (int)sizeof(T)) & ~15u;
+            for (uint32_t o = 0; o < bytes; o += 16384u) {
+                const uint32_t len = min(16384u, bytes - o);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + o), "r"(len) : "memory");
+            }
+        }
+    }
     pdl_wait();
     const int nb = min(*n_active, MAXB);
     if (nb <= 0) return;
-    const int k0 = blockIdx.y * KS;
-    const int kn = min(KS, K - k0);
 
     // Stage the activation slice.
     const int vec_per_row = kn / VEC;

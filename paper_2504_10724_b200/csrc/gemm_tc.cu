@@ -146,6 +146,7 @@ struct TcParams {
     size_t pf_bytes;
     unsigned long long* trace;  // timing experiments: 8 globaltimer stamps per CTA (null = off)
     int dbg;                    // timing experiments: bit 0 = no plane stores (results wrong)
+    int skip_dead;              // read n_active before the weight prefetch (skip it when 0)
 };
 
 // Timeline stamps are compiled in only for the timing experiments
@@ -217,7 +218,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == 0) {
         const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-        const int pre = min(S, nkb);
+        // No weight prefetch when no row is live (all exited): the count read
+        // before the wait may be stale, which costs only a useless or missed
+        // prefetch — the count after the wait decides what is computed.
+        static constexpr bool kSkipDead = true;
+        const int pre = (kSkipDead && p.skip_dead && *reinterpret_cast<const volatile int*>(p.n_active) <= 0)
+                            ? 0 : min(S, nkb);
         if (lane == 0) {
             // Weights do not depend on the previous kernel: fill the first
             // stages with weight tiles before waiting on it (PDL), then add the
@@ -252,7 +258,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,
                             pol_x);
-            for (int i = pre; i < nkb; ++i) {
+            // every row exited before this layer: complete the stages already
+            // in flight (their barriers expect the X bytes too) and stream no
+            // more (read after the X loads are issued: off the critical path)
+            const int last = *p.n_active > 0 ? nkb : pre;
+            if (last == pre)
+                for (int i = 0; i < pre; ++i) mbar_wait(full0 + 8 * i, 0);
+            for (int i = pre; i < last; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)(i / S) & 1u;
                 mbar_wait(empty0 + 8 * s, ph ^ 1u);
@@ -269,7 +281,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         // registers, no per-op R2UR) and one elected lane issues — a
         // single-lane loop issues tcgen05.mma several times slower.
         const uint32_t idesc = instr_desc(kBM, p.bpad);
-        for (int i = 0; i < nkb; ++i) {
+        pdl_wait();
+        const int live = *p.n_active;  // 0: every row exited, nothing to multiply
+        for (int i = 0; i < (live > 0 ? nkb : 0); ++i) {
             const int s = i % S;
             const uint32_t ph = (uint32_t)(i / S) & 1u;
             mbar_wait(full0 + 8 * s, ph);
@@ -285,17 +299,18 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             __syncwarp();
         }
-        if (elect_one_sync()) umma_commit(tfull);
+        if (live > 0 && elect_one_sync()) umma_commit(tfull);
         __syncwarp();
     } else {
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31  (thread = output feature)
         const int quarter = warp & 3;
         const int n = m_tile * kBM + quarter * 32 + lane;
         pdl_wait();  // n_active and the plane workspace belong to the previous kernels
+        const int rows = *p.n_active;
+        if (rows > 0) {
         mbar_wait(tfull, 0);
         tc_fence_after();
         EEB_STAMP(threadIdx.x == 64, 4);  // accumulator complete
-        const int rows = *p.n_active;
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
         if (p.head_tri && p.cs == 1) {
             // Fused exit-head tail: stage the [rows x 128 vocab] logits tile
@@ -378,8 +393,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int j = 0; j < 16; ++j) red[(c0 + j) * (kBM + 1) + f] = v[j];
             }
         }
+        }  // rows > 0
     }
-    if (p.cs > 1) {
+    // every thread: the live-row count (uniform over a cluster) gates the on-chip reduction
+    pdl_wait();
+    const int rows_all = *p.n_active;
+    if (p.cs > 1 && rows_all > 0) {
         // Split-K reduction on chip: the cs CTAs of a cluster hold consecutive
         // k-ranges of one tile; CTA rank r sums rows r, r+cs, ... of the tile
         // over the cluster's smem partials in rank (= k) order (deterministic)
@@ -662,6 +681,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.trace = a.trace;
     static const int env_dbg = std::getenv("EEB_GEMM_DBG") ? std::atoi(std::getenv("EEB_GEMM_DBG")) : 0;
     p.dbg = env_dbg;
+    static const bool skip_dead = !std::getenv("EEB_SKIP_DEAD") || std::atoi(std::getenv("EEB_SKIP_DEAD")) != 0;
+    p.skip_dead = skip_dead ? 1 : 0;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;

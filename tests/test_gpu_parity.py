@@ -234,3 +234,28 @@ def test_opt13b_shape_bf16_agreement(ctx):
         near = np.abs(r["confidence"] - TH) <= 1e-2
         assert ((g["exit_layer"] == r["exit_layer"]) | near).all()
     assert agree / total >= BF16_AGREE
+
+
+def test_all_rows_exit_early_bf16(ctx):
+    """Every row exits at the first head (th = 0): the deeper layers' tcgen05
+    GEMMs see no live row and stream no weights; the steps that follow (th
+    0.7, rows reaching deeper layers whose older positions have no KV there)
+    must still agree with the oracle at the bf16 bar."""
+    desc = MINI.replace(dtype=eeb.BF16, name="mini-bf16-allexit")
+    m, ref = _pair(ctx, desc)
+    rng = np.random.default_rng(9)
+    B = 8  # >= 3 rows: the tensor-core GEMM tier
+    slots = np.arange(B)
+    agree = total = 0
+    for pos in range(12):
+        th = 0.0 if pos % 3 != 2 else TH
+        toks = rng.integers(0, desc.vocab, B)
+        g = ctx.decode_step(m, 0, eeb.INTROSPECTIVE, th, slots, toks, np.full(B, pos))
+        r = ref.decode_step(0, eeb.INTROSPECTIVE, th, slots, toks, np.full(B, pos))
+        if th == 0.0:
+            assert (g["exit_layer"] == desc.exit_layers[0]).all()
+        near = np.abs(r["confidence"] - th) <= 1e-3
+        assert ((g["exit_layer"] == r["exit_layer"]) | near).all(), (g["exit_layer"], r["exit_layer"])
+        agree += int((g["token_id"] == r["token_id"]).sum())
+        total += B
+    assert agree / total >= BF16_AGREE, agree / total
