@@ -6,7 +6,11 @@ as invariant and hoist them above the wait, so a kernel reads its
 predecessor's output (e.g. the compacted row count) before the predecessor
 has written it — a race that only shows under particular timings.  Weight
 streams (TMA, UTMALDG) are allowed before the wait: weights never change
-inside a step.
+inside a step.  A volatile load (LDG.E.STRONG.SYS) is the one deliberate
+exception: the tcgen05 GEMM reads the live-row count before the wait only as
+a hint whether to prefetch weights (a stale value costs a useless or a missed
+prefetch; the count read after the wait decides what is computed) — plain
+(hoistable) loads stay forbidden.
 """
 import re
 import subprocess
@@ -15,7 +19,7 @@ import pytest
 
 from paper_2504_10724_b200 import eeb
 
-ALLOWED_PRE_WAIT = ("UTMALDG",)        # TMA weight prefetch
+ALLOWED_PRE_WAIT = ("UTMALDG", "LDG.E.STRONG.SYS")  # TMA weight prefetch; the volatile live-count hint
 NO_PDL_KERNELS = ("step_kernel", "synth")  # standalone launches (persistent step, weight synthesis)
 
 
