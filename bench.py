@@ -183,7 +183,7 @@ def workload_config(args, desc):
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
-def batch_sweep(ctx, eeb, desc, args, stream, batches=(1, 4, 16, 32, 64, 128, 256), n_steps=10):
+def batch_sweep(ctx, eeb, desc, args, stream, batches=(1, 2, 4, 16, 32, 64, 128, 256), n_steps=10):
     """The metric is 'EE decode tokens/s vs batch': the same workload at each
     batch (own model instance with a 256-slot KV pool, prompts prefilled)."""
     import torch

@@ -536,12 +536,14 @@ CUtensorMap make_map(const void* ptr, int rows, int cols, int box_rows) {
 
 bool gemm_tc_available() { return encode_fn() != nullptr; }
 
-// Smallest batch the tensor-core tier takes (measured: the CUDA-core GEMV wins
-// at 1-2 rows, tcgen05 from 4 rows: 1.16 vs 1.52 ms per C2 step; rows are padded to UMMA N = 16;
-// the padding costs MMA issue slots only, the weight stream is the same).
-// EEB_TC_MIN_ROWS overrides (A/B against the CUDA-core GEMV).
+// Smallest batch the tensor-core tier takes.  Rows are padded to UMMA N = 16
+// (the padding costs MMA issue slots only; the weight stream is the same) and
+// the tcgen05 path prefetches its weights before the PDL wait, which the
+// CUDA-core GEMV does not: measured at batch 1 (C2, tools/b1check.py) a full
+// 24-layer step takes 1.09 ms on tcgen05 vs 1.39 ms on the GEMV, an exit-6
+// step 0.45 vs 0.48 ms.  EEB_TC_MIN_ROWS overrides (A/B against the GEMV).
 int tc_min_rows() {
-    static const int v = std::getenv("EEB_TC_MIN_ROWS") ? std::max(1, std::atoi(std::getenv("EEB_TC_MIN_ROWS"))) : 3;
+    static const int v = std::getenv("EEB_TC_MIN_ROWS") ? std::max(1, std::atoi(std::getenv("EEB_TC_MIN_ROWS"))) : 1;
     return v;
 }
 

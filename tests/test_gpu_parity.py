@@ -244,7 +244,7 @@ def test_all_rows_exit_early_bf16(ctx):
     desc = MINI.replace(dtype=eeb.BF16, name="mini-bf16-allexit")
     m, ref = _pair(ctx, desc)
     rng = np.random.default_rng(9)
-    B = 8  # >= 3 rows: the tensor-core GEMM tier
+    B = 8
     slots = np.arange(B)
     agree = total = 0
     for pos in range(12):
