@@ -171,6 +171,10 @@ struct eeb_ctx {
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t load_stream = nullptr;  // greedy loader: pinned H2D copies, overlapped with decode
+    cudaStream_t main_stream = nullptr;  // `stream` while a conditional body is being captured
+    std::vector<cudaStream_t> cond_streams;  // capture streams of nested conditional bodies (step graphs)
+    bool capturing = false;               // enqueue_step runs under stream capture
+    size_t cond_open = 0;                 // conditional bodies open in the capture
     std::vector<std::unique_ptr<eeb::Model>> models;
     int graphs_enabled = 1;
     int gemm_tier = 0;
@@ -963,6 +967,59 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
     return dn;
 }
 
+// A conditional node costs ~12 us of the step (it ends the PDL overlap into
+// the next layer) and pays off only when all rows tend to exit together:
+// measured on C2, batch 1 0.65 -> 0.56 ms/step, batch 2 0.61 -> 0.51, but
+// batch 4 1.03 -> 1.04 and batch 64 1.51 -> 1.55.  So: batches of <= 2 rows
+// (EEB_COND_MAX_ROWS overrides; 0 disables).
+bool cond_enabled(int batch) {
+    static const int max_rows =
+        std::getenv("EEB_COND_MAX_ROWS") ? std::atoi(std::getenv("EEB_COND_MAX_ROWS")) : 2;
+    return batch <= max_rows;
+}
+
+// Open an IF body after the current capture position of c->stream: later
+// launches are captured into the body (on a nested capture stream) until
+// close_cond_bodies.  Returns the stream to launch on.
+cudaStream_t open_cond_body(eeb_ctx* c, cudaGraphConditionalHandle h) {
+    cudaStream_t outer = c->stream;
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    EEB_CUDA(cudaStreamGetCaptureInfo(outer, &st, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    EEB_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+    EEB_CUDA(cudaStreamUpdateCaptureDependencies(outer, &node, 1, cudaStreamSetCaptureDependencies));
+    const size_t level = c->cond_open;
+    while (c->cond_streams.size() <= level) {
+        cudaStream_t cs;
+        EEB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        c->cond_streams.push_back(cs);
+    }
+    cudaStream_t body = c->cond_streams[level];
+    EEB_CUDA(cudaStreamBeginCaptureToGraph(body, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+    ++c->cond_open;
+    c->stream = body;
+    return body;
+}
+
+cudaStream_t close_cond_bodies(eeb_ctx* c) {
+    while (c->cond_open > 0) {
+        --c->cond_open;
+        cudaGraph_t ignored;
+        EEB_CUDA(cudaStreamEndCapture(c->cond_streams[c->cond_open], &ignored));
+    }
+    c->stream = c->main_stream;
+    return c->stream;
+}
+
 void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
     Model& m = model_of(c, mi);
     const eeb_model_desc& d = m.desc;
@@ -1089,6 +1146,19 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             da.head = h;
             da.out = o;
             for (int k = 0; k < 64; ++k) da.layers[k] = k < d.n_exits ? m.exits[k] : 0;
+            // Captured introspective step: everything after this head runs in a
+            // conditional body that decide switches off when no row survives —
+            // an all-exited step (batch 1: 71% of C2 steps) skips the deeper
+            // layers' launches instead of running them on zero rows.
+            const bool cond = c->capturing && policy == EEB_INTROSPECTIVE && !is_final && m.tp == 1 &&
+                              m.shards == 1 && cond_enabled(batch);
+            if (cond) {
+                cudaStreamCaptureStatus st;
+                cudaGraph_t g;
+                EEB_CUDA(cudaStreamGetCaptureInfo(s, &st, nullptr, &g, nullptr, nullptr));
+                EEB_CUDA(cudaGraphConditionalHandleCreate(&da.cond, g, 1, cudaGraphCondAssignDefault));
+                da.has_cond = 1;
+            }
             launch_decide(da, s);
             count(c, kCatHead, 1);
             if (policy == EEB_INTROSPECTIVE && !is_final) {
@@ -1098,9 +1168,11 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
                 std::swap(cur, alt);
                 std::swap(h_cur, h_alt);
             }
+            if (cond) s = open_cond_body(c, da.cond);
             ++hi;
         }
     }
+    s = close_cond_bodies(c);  // finalize runs whatever the conditionals decided
     {
         Timer t(c, kCatOther);
         launch_finalize(batch, d.n_exits, o, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len,
@@ -1487,12 +1559,21 @@ void run_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
         c->step_launches = 0;
         cudaGraph_t g;
         EEB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        c->capturing = true;
         try {
             enqueue_step(c, mi, depth, policy, th, batch);
         } catch (...) {
+            c->capturing = false;
+            while (c->cond_open > 0) {
+                --c->cond_open;
+                cudaGraph_t ig;
+                cudaStreamEndCapture(c->cond_streams[c->cond_open], &ig);
+            }
+            c->stream = c->main_stream;
             cudaStreamEndCapture(c->stream, &g);
             throw;
         }
+        c->capturing = false;
         EEB_CUDA(cudaStreamEndCapture(c->stream, &g));
         cudaGraphExec_t ex;
         EEB_CUDA(cudaGraphInstantiate(&ex, g, 0));
@@ -1629,6 +1710,7 @@ eeb_status eeb_create(int device, eeb_ctx** out) {
         c->num_sms = prop.multiProcessorCount;
         EEB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         EEB_CUDA(cudaStreamCreateWithFlags(&c->load_stream, cudaStreamNonBlocking));
+        c->main_stream = c->stream;
         *out = c.release();
     });
 }
@@ -1651,6 +1733,7 @@ void eeb_destroy(eeb_ctx* c) {
     c->models.clear();
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->load_stream);
+    for (cudaStream_t cs : c->cond_streams) cudaStreamDestroy(cs);
     delete c;
 }
 

@@ -228,8 +228,11 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
         survivors_total += n_live_s;
         __syncthreads();
     }
-    if (a.policy == EEB_INTROSPECTIVE && !a.is_final && threadIdx.x == 0)
+    if (a.policy == EEB_INTROSPECTIVE && !a.is_final && threadIdx.x == 0) {
         *a.nxt.n_active = survivors_total;
+        // no survivor: the deeper layers' conditional body is skipped
+        if (a.has_cond) cudaGraphSetConditional(a.cond, survivors_total > 0 ? 1u : 0u);
+    }
 }
 
 // K4 + bookkeeping: shared-memory atomic histogram of exit-head bins, breach

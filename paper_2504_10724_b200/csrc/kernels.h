@@ -184,6 +184,11 @@ struct DecideArgs {
     int64_t head_shard_stride = 0;    // float4 entries between regions
     StepOutDev out;
     int layers[64];          // exit ladder (profile mode maps head index -> layer)
+    // Captured introspective step: the rest of the step (deeper layers and
+    // heads) is a conditional graph body run only if a row survives this head
+    // (decide sets the condition from the survivor count).
+    int has_cond = 0;
+    cudaGraphConditionalHandle cond = 0;
 };
 void launch_decide(const DecideArgs& a, cudaStream_t s);
 // x_nxt[j] = x_cur[src[j]] (and the normalised row h) for live rows of the compacted state.

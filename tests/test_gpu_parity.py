@@ -259,3 +259,36 @@ def test_all_rows_exit_early_bf16(ctx):
         agree += int((g["token_id"] == r["token_id"]).sum())
         total += B
     assert agree / total >= BF16_AGREE, agree / total
+
+
+@pytest.mark.parametrize("B", [1, 2])
+def test_conditional_skip_small_batch(ctx, B):
+    """Batches of <= 2 rows capture the layers after each non-final head as a
+    conditional graph body that decide switches off when no row survives.
+    Graph replay must equal eager launches (same kernels, all rows exited or
+    not) and the oracle at the bf16 bar, over steps of both kinds."""
+    desc = MINI.replace(dtype=eeb.BF16, name=f"mini-bf16-cond{B}")
+    mg, ref = _pair(ctx, desc)
+    me = ctx.register(desc.replace(name=f"mini-bf16-cond{B}-eager"))
+    ctx.load_layers(me, desc.num_layers)
+    rng = np.random.default_rng(21 + B)
+    slots = np.arange(B)
+    exits = set()
+    agree = total = 0
+    for pos in range(24):
+        toks = rng.integers(0, desc.vocab, B)
+        ctx.set_graphs(True)
+        g = ctx.decode_step(mg, 0, eeb.INTROSPECTIVE, TH, slots, toks, np.full(B, pos))
+        ctx.set_graphs(False)
+        e = ctx.decode_step(me, 0, eeb.INTROSPECTIVE, TH, slots, toks, np.full(B, pos))
+        ctx.set_graphs(True)
+        r = ref.decode_step(0, eeb.INTROSPECTIVE, TH, slots, toks, np.full(B, pos))
+        for k in ("token_id", "exit_layer", "confidence", "hist"):
+            np.testing.assert_array_equal(np.asarray(g[k]), np.asarray(e[k]), err_msg=k)
+        near = np.abs(r["confidence"] - TH) <= 1e-3
+        assert ((g["exit_layer"] == r["exit_layer"]) | near).all()
+        agree += int((g["token_id"] == r["token_id"]).sum())
+        total += B
+        exits.add(int(max(g["exit_layer"])))
+    assert agree / total >= BF16_AGREE, agree / total
+    assert len(exits) >= 2, exits  # both skipped and full steps were exercised
