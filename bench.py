@@ -484,6 +484,19 @@ def run_eeb(args, desc):
         except Exception as e:  # reported, never fatal for the headline line
             secondary = {"error": repr(e)[:200]}
 
+    c3 = None
+    serve_c3 = ROOT / "paper_2504_10724_b200" / "_build" / "serve_c3"
+    if rank == 0 and world == 1 and not args.no_secondary and serve_c3.exists():
+        # C3 (BASELINE configs[2]): OPT-1.3B + OPT-2.7B shapes behind the host C++
+        # engine in HELIOS mode at batch 256 (eval cycles, greedy loads from a
+        # pinned host tier, continuous batching), its own process.
+        try:
+            out = subprocess.run([str(serve_c3), "1024", "128", "64"], capture_output=True, text=True,
+                                 timeout=600).stdout.strip().splitlines()
+            c3 = json.loads(out[-1])
+        except Exception as e:  # reported, never fatal for the headline line
+            c3 = {"error": repr(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_port_run(desc, steps=2, warmup=0)
@@ -506,6 +519,8 @@ def run_eeb(args, desc):
                 "path": "persistent step kernel" if prof.get("persistent") else "per-op kernel chain"}
         if secondary is not None:
             line["secondary_c4"] = secondary
+        if c3 is not None:
+            line["secondary_c3"] = c3
         if loader is not None:
             line["loader"] = loader
         if sweep is not None:

@@ -87,7 +87,8 @@ public:
         throw_if_error(eeb_create(device, &ctx_), "eeb_create");
     }
     /// Paged KV pool for models registered after this call (eeb_kv_configure_pages):
-    /// n_pages pages of page_size positions instead of max_slots x max_seq_len.
+    /// n_pages pages of page_size positions instead of max_slots x max_seq_len
+    /// (bf16 models with head_dim 64 or 128; other models keep the slot pool).
     void set_kv_pages(int page_size, int n_pages) {
         kv_page_ = page_size;
         kv_pages_ = n_pages;
@@ -118,7 +119,11 @@ public:
         int h = -1;
         throw_if_error(eeb_model_register(ctx_, &d, &h), "eeb_model_register");
         handles_[spec.id] = {h, spec};
-        if (kv_page_ > 0) throw_if_error(eeb_kv_configure_pages(ctx_, h, kv_page_, kv_pages_), "eeb_kv_configure_pages");
+        // the paged pool serves bf16 models with head_dim 64 / 128 (the tensor-core
+        // attention kernels walk page tables); others keep the slot pool
+        const int hd = a.n_heads > 0 ? a.d_model / a.n_heads : 0;
+        if (kv_page_ > 0 && a.dtype == EEB_BF16 && (hd == 64 || hd == 128))
+            throw_if_error(eeb_kv_configure_pages(ctx_, h, kv_page_, kv_pages_), "eeb_kv_configure_pages");
         if (host_tier_) throw_if_error(eeb_host_stage(ctx_, h, spec.num_layers), "eeb_host_stage");
     }
 

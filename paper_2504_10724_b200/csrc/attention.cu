@@ -127,9 +127,10 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
     }
 
     const uint8_t* depth = a.kv_depth + (int64_t)slot * a.max_seq;
-    const int npg = kThreads / (hd / 2);        // P·V position groups
+    const int npg = kThreads / (hd / 2);        // P·V position groups (head_dim 80: 3, threads 120+ idle)
     const int dp = threadIdx.x % (hd / 2);       // dim pair
     const int pg = threadIdx.x / (hd / 2);
+    const bool pv = pg < npg;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int vpr = hd / VEC;                    // 16-byte vectors per row
     float acc[kMaxG][2];
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
             acc[h][0] *= scale_s[h];
             acc[h][1] *= scale_s[h];
         }
-        for (int t = pg; t < cn; t += npg) {
+        for (int t = pg; pv && t < cn; t += npg) {
             const int p = c0 + t;
             float v0, v1;
             if (p == pos) {
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
     }
     // reduce the position groups through (now free) score memory
     float* red = sc;  // [npg][G][hd]
-    for (int h = 0; h < G; ++h) {
+    for (int h = 0; pv && h < G; ++h) {
         red[(pg * G + h) * hd + 2 * dp] = acc[h][0];
         red[(pg * G + h) * hd + 2 * dp + 1] = acc[h][1];
     }
@@ -1393,7 +1394,7 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     }
     const int G = a.n_heads / a.n_kv_heads;
     if (paged) throw Error(3, "attention: the paged KV pool needs a bf16 model with head_dim 64 or 128");
-    if (G > kMaxG || a.head_dim > kMaxHd || a.head_dim % 16 != 0 || kThreads % (a.head_dim / 2) != 0)
+    if (G > kMaxG || a.head_dim > kMaxHd || a.head_dim % 16 != 0 || a.head_dim / 2 > kThreads)
         throw Error(1, "attention: unsupported head geometry");
     const int esz = a.dtype == 0 ? 4 : 2;
     const int C = kChunkBytes / (a.head_dim * esz);

@@ -32,6 +32,25 @@ def build_engine_gpu(verbose: bool = False) -> Path:
     return out
 
 
+def build_serve_c3(verbose: bool = False) -> Path:
+    """paper_2504_10724_b200/_build/serve_c3: the C3 serving run (engine + CudaBackend), used by bench.py."""
+    src = ROOT / "tools" / "serve_c3.cpp"
+    lib = ROOT / "paper_2504_10724_b200"
+    out = lib / "_build" / "serve_c3"
+    deps = [src, lib / "libeeb.so", ROOT / "include" / "eeb" / "eeb.h", *(ROOT / "include" / "eeserve").glob("*.hpp")]
+    if out.exists() and all(d.stat().st_mtime <= out.stat().st_mtime for d in deps):
+        return out
+    out.parent.mkdir(exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-I/usr/local/cuda/include", str(src), "-o", str(out),
+           f"-L{lib}", "-leeb", f"-Wl,-rpath,{lib}", "-L/usr/local/cuda/lib64", "-lcudart"]
+    if verbose:
+        print(" ".join(cmd))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"serve_c3 build failed:\n{r.stderr}")
+    return out
+
+
 def build_host(verbose: bool = False) -> Path | None:
     ref = ROOT / "oracle" / "_ref" / "libeeref.so"
     src = ROOT / "tests" / "cpp" / "test_host.cpp"

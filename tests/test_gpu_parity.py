@@ -292,3 +292,31 @@ def test_conditional_skip_small_batch(ctx, B):
         exits.add(int(max(g["exit_layer"])))
     assert agree / total >= BF16_AGREE, agree / total
     assert len(exits) >= 2, exits  # both skipped and full steps were exercised
+
+
+@pytest.mark.parametrize("dtype", [eeb.F32, eeb.BF16], ids=["f32", "bf16"])
+def test_head_dim_80(ctx, dtype):
+    """OPT-2.7B's head geometry (2560 = 32 heads x 80): the generic attention
+    kernel (P.V thread groups that do not divide the CTA) against the oracle,
+    prefill then decode."""
+    desc = eeb.ModelDesc("mini-hd80", 4, 1280, 16, 16, 1024, 1000, (2, 4), dtype=dtype, max_slots=4,
+                         max_seq_len=96)
+    m, ref = _pair(ctx, desc)
+    rng = np.random.default_rng(80)
+    slots = np.arange(4)
+    prompts = [rng.integers(0, desc.vocab, n) for n in (20, 7, 33, 1)]
+    ctx.prefill(m, desc.num_layers, slots, prompts)
+    for i, p in enumerate(prompts):
+        for k, t in enumerate(p):
+            ref.decode_step(0, eeb.FULL_DEPTH, TH, [slots[i]], [t], [k])
+    pos = np.array([len(p) for p in prompts])
+    agree = total = 0
+    for step in range(6):
+        toks = rng.integers(0, desc.vocab, 4)
+        g = ctx.decode_step(m, 0, eeb.INTROSPECTIVE, TH, slots, toks, pos + step)
+        r = ref.decode_step(0, eeb.INTROSPECTIVE, TH, slots, toks, pos + step)
+        if dtype == eeb.F32:
+            _compare_rows(g, r, TH)
+        agree += int((g["token_id"] == r["token_id"]).sum())
+        total += 4
+    assert agree / total >= BF16_AGREE, agree / total

@@ -1,0 +1,110 @@
+// C3 serving run (BASELINE.json configs[2]): OPT-1.3B + OPT-2.7B shapes behind
+// the host C++ engine (include/eeserve BatchedEngine, the drop-in for
+// Simulator::run, engine.hpp:114-153) over CudaBackend and the C ABI: HELIOS
+// mode with real-time profiling (evaluation cycles on both candidates, PHT,
+// choose_depth), greedy layer loading from a pinned host tier, breach-driven
+// switching, batch 256 with continuous batching over a paged KV pool.
+// Prints one JSON line (bench.py attaches it as "secondary_c3").
+//
+//   serve_c3 [n_requests] [prompt_len] [tokens]
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "eeserve/engine.hpp"
+
+using namespace eeserve;
+
+static ModelSpec opt_shape(const std::string& id, int layers, std::vector<int> exits, int d, int heads, int ffn,
+                           std::uint64_t seed, double thr, double t_layer) {
+    ModelSpec s;
+    s.id = id;
+    s.num_layers = layers;
+    s.exit_layers = std::move(exits);
+    const std::int64_t bw = 2, vocab = 50272;
+    s.per_layer_weight_bytes = (4LL * d * d + 2LL * d * ffn) * bw + 2LL * d * 4;
+    s.base_weight_bytes = vocab * d * bw * (1 + (std::int64_t)s.exit_layers.size()) +
+                          (std::int64_t)s.exit_layers.size() * d * 4;
+    s.kv_bytes_per_token_per_layer = 2LL * d * bw;
+    s.t_decode_per_layer_s = t_layer;
+    s.t_prefill_per_layer_per_token_s = t_layer / 64.0;
+    s.repo_metrics["throughput"] = thr;
+    s.arch.d_model = d;
+    s.arch.n_heads = heads;
+    s.arch.n_kv_heads = heads;
+    s.arch.d_ffn = ffn;
+    s.arch.vocab = (int)vocab;
+    s.arch.dtype = EEB_BF16;
+    s.arch.seed = seed;
+    validate_model_spec(s);
+    return s;
+}
+
+int main(int argc, char** argv) {
+    const int n_req = argc > 1 ? std::atoi(argv[1]) : 1024;
+    const int prompt = argc > 2 ? std::atoi(argv[2]) : 128;
+    const int tokens = argc > 3 ? std::atoi(argv[3]) : 64;
+    ModelRepository repo;
+    // public OPT dims: 1.3B L24 d2048 ffn 8192; 2.7B L32 d2560 ffn 10240; V 50272
+    repo.models["opt-1.3b"] = opt_shape("opt-1.3b", 24, {6, 12, 24}, 2048, 32, 8192, 20260819, 2.0, 6e-5);
+    repo.models["opt-2.7b"] = opt_shape("opt-2.7b", 32, {8, 16, 32}, 2560, 32, 10240, 20260820, 1.0, 8e-5);
+    repo.metric_directions["throughput"] = MetricDirection::higher_better;
+
+    EngineConfig cfg;
+    cfg.mem.capacity_bytes = 40LL << 30;
+    cfg.mem.reserve_bytes = 2LL << 30;
+    cfg.mem.max_seq_len = prompt + tokens;
+    cfg.mem.bandwidth_bytes_per_s = 8.4e9;  // modelled only where nothing is measured
+    cfg.policy.k = 2;
+    cfg.policy.n_eval_requests = 64;
+    cfg.policy.ri = 512;
+    cfg.policy.window = 100;
+    cfg.policy.cbc_max = 50;
+    cfg.mode = ModeSpec{Mode::helios, ""};
+    cfg.max_batch = 256;
+    cfg.max_seq_len = prompt + tokens;
+    cfg.continuous = true;
+
+    const auto t0 = std::chrono::steady_clock::now();
+    CudaBackend be(0, /*host_tier=*/true);
+    be.set_kv_pages(64, 256 * ((prompt + tokens + 63) / 64));
+    std::vector<RequestSpec> reqs;
+    for (int i = 0; i < n_req; ++i) reqs.push_back({i, prompt, tokens});
+    BatchedEngine eng(repo, be, cfg);
+    const auto t1 = std::chrono::steady_clock::now();
+    const EngineReport rep = eng.run(reqs);
+    const auto t2 = std::chrono::steady_clock::now();
+    const double setup_s = std::chrono::duration<double>(t1 - t0).count();
+    const double run_s = std::chrono::duration<double>(t2 - t1).count();
+    std::string exits = "{";
+    for (const auto& [m, per] : rep.exit_table) {
+        exits += (exits.size() > 1 ? ", \"" : "\"") + m + "\": {";
+        bool first = true;
+        for (const auto& [l, p] : per) {
+            exits += (first ? "\"" : ", \"") + std::to_string(l) + "\": " + std::to_string(p);
+            first = false;
+        }
+        exits += "}";
+    }
+    exits += "}";
+    std::string hist = "[";
+    for (size_t i = 0; i < rep.serving_history.size() && i < 12; ++i)
+        hist += (i ? ", [\"" : "[\"") + rep.serving_history[i].first + "\", " +
+                std::to_string(rep.serving_history[i].second) + "]";
+    hist += "]";
+    std::printf(
+        "{\"workload\": \"C3: OPT-1.3B + OPT-2.7B shapes, HELIOS mode (eval cycles, PHT, choose_depth, greedy "
+        "loads from a pinned host tier, breach switching), batch 256, continuous batching over a paged KV pool\", "
+        "\"requests\": %d, \"prompt_len\": %d, \"tokens_per_request\": %d, \"tokens\": %lld, \"steps\": %lld, "
+        "\"decode_tokens_per_s\": %.1f, \"serving_tokens_per_s\": %.1f, \"wall_s\": %.3f, \"host_stage_s\": %.3f, "
+        "\"mean_ttft_ms\": %.3f, \"mean_tpot_ms\": %.4f, \"achieved_batch\": %d, \"eval_cycles\": %lld, "
+        "\"ld\": %lld, \"sw\": %lld, \"load_bytes\": %lld, \"load_s\": %.4f, \"load_gbs\": %.2f, \"prefill_s\": %.3f, "
+        "\"perplexity\": %.6f, \"exit_table_pct\": %s, \"serving_history\": %s}\n",
+        n_req, prompt, tokens, (long long)rep.tokens, (long long)rep.steps, rep.throughput_tok_s,
+        rep.tokens / run_s, run_s, setup_s, rep.mean_ttft_s * 1e3, rep.mean_tpot_s * 1e3, rep.achieved_batch_size,
+        (long long)rep.eval_cycles, (long long)rep.ld_count, (long long)rep.sw_count, (long long)rep.load_bytes,
+        rep.load_s, rep.load_bytes / std::max(1e-9, rep.load_s) / 1e9, rep.prefill_s, rep.perplexity,
+        exits.c_str(), hist.c_str());
+    return 0;
+}
