@@ -1711,6 +1711,11 @@ eeb_status eeb_create(int device, eeb_ctx** out) {
         EEB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         EEB_CUDA(cudaStreamCreateWithFlags(&c->load_stream, cudaStreamNonBlocking));
         c->main_stream = c->stream;
+        // Under Nsight Compute (its injection sets NV_COMPUTE_PROFILER_PERFWORKS_DIR)
+        // the step runs as plain stream launches: ncu fails to replay this
+        // build's graph-captured tcgen05 GEMM node (LaunchFailed); the kernels
+        // are the same either way.  eeb_set_graphs(ctx, 1) still forces graphs.
+        if (std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR")) c->graphs_enabled = 0;
         *out = c.release();
     });
 }

@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--policy", default="introspective")
-    ap.add_argument("--graphs", type=int, default=1)
+    ap.add_argument("--graphs", type=int, default=-1)  # -1: library default (stream launches under ncu)
     args = ap.parse_args()
     import torch
 
@@ -32,7 +32,8 @@ def main():
     ctx = eeb.Context(0)
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
-    ctx.set_graphs(bool(args.graphs))
+    if args.graphs >= 0:
+        ctx.set_graphs(bool(args.graphs))
     rng = np.random.default_rng(0)
     B = args.batch
     slots = np.arange(B)
