@@ -253,6 +253,32 @@ def measure_loader(ctx, m, eeb, step, args, stream, depth=16, n_steps=20):
                    f"{n_steps} C2 decode steps run on the decode stream; CUDA events on both streams"}
 
 
+
+def ncu_traffic(args, desc):
+    """DRAM bytes per step of the layer GEMMs and the exit-head GEMMs from the
+    committed ncu launch list of this workload (profiles/r1, one serialised
+    --metrics dram__bytes_read.sum,dram__bytes_write.sum capture of a C2 step;
+    cold cache).  None for other workloads."""
+    path = ROOT / "profiles" / "r1" / "launches_introspective_b64_s4.csv"
+    if not path.exists() or desc.name != "opt-1.3b-4x" or args.batch != 64 or args.policy != "introspective":
+        return None
+    import csv
+    launches = {}
+    with open(path) as f:
+        for r in csv.DictReader(line for line in f if not line.startswith("==")):
+            d = launches.setdefault(r["ID"], {"name": r["Kernel Name"], "grid": r.get("Grid Size", "")})
+            d[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    layer = head = 0.0
+    for d in launches.values():
+        if "gemm_tc" not in d["name"]:
+            continue
+        b = d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+        if d["grid"].startswith(f"({(desc.vocab + 127) // 128},"):
+            head += b
+        else:
+            layer += b
+    return {"layer_gemm": int(layer), "exit_head": int(head), "source": str(path.relative_to(ROOT))}
+
 def run_eeb(args, desc):
     import torch
 
@@ -403,15 +429,19 @@ def run_eeb(args, desc):
         heads_run = 1 if policy in (eeb.FLAT, eeb.FULL_DEPTH) else ne
         g_bytes = gemm_bytes_per_step(desc, B, run_layers)
         h_bytes = head_bytes(desc, B) * heads_run
+        tr = ncu_traffic(args, desc)
         roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1)",
                 "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
-                "traffic": None, "peak_source": peak_source,
+                "traffic": tr["layer_gemm"] if tr else None,
+                **({"traffic_source": tr["source"] + " (DRAM bytes per step, ncu, cold cache)"} if tr else {}),
+                "peak_source": peak_source,
                 "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
                 "step_share": gemm_ms / max(1e-9, gemm_ms + head_ms + attn_ms + prof["norm_ms"] / nsteps
                                             + prof["other_ms"] / nsteps)}
         roof["frac"] = roof["achieved"] / hbm
         exit_head = {"achieved": h_bytes / (head_ms / 1000.0) / 1e9 if head_ms > 0 else None, "unit": "GB/s",
-                     "ms_per_step": head_ms, "algorithmic_bytes_per_step": h_bytes}
+                     "ms_per_step": head_ms, "algorithmic_bytes_per_step": h_bytes,
+                     "traffic": tr["exit_head"] if tr else None}
         if exit_head["achieved"]:
             exit_head["frac"] = exit_head["achieved"] / hbm
     # whole step: weights of the layers run + heads evaluated + KV of the rows that reached each layer
