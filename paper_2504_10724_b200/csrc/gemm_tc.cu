@@ -118,6 +118,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Two 16-column TMEM loads in flight before one wait (epilogue latency).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr + 16u));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ bool elect_one_sync() {
     uint32_t pred = 0;
     asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
@@ -373,13 +391,25 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         } else if (p.cs == 1) {
             float* plane = p.part + (int64_t)split * p.split_stride;
-            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+            // only the live rows' columns (warp-uniform bound), 32 per wait
+            const int lim = min(rows, p.bpad);
+            int c0 = 0;
+            for (; c0 + 32 <= p.bpad && c0 < lim; c0 += 32) {
+                float v[32];
+                tmem_ld32(taddr + (uint32_t)c0, v);  // warp-collective
+                if (n < p.N && !(p.dbg & 1)) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (c0 + j < lim) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
+                }
+            }
+            for (; c0 < lim; c0 += 16) {
                 float v[16];
-                tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective: every warp runs every chunk
+                tmem_ld16(taddr + (uint32_t)c0, v);
                 if (n < p.N && !(p.dbg & 1)) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (c0 + j < rows) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
+                        if (c0 + j < lim) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
                 }
             }
         } else {
