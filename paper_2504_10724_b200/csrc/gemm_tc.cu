@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             // scan 64 entries each for max / first argmax / sum exp(l - max).
             float* red = reinterpret_cast<float*>(base_ptr);
             const int f = quarter * 32 + lane;
-            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+            for (int c0 = 0; c0 < min(rows, p.bpad); c0 += 16) {  // live rows only
                 float v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);
 #pragma unroll
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             // Fused MLP activation: the up projection's tile goes straight to the
             // down GEMM's bf16 input — no split-K planes, no activation kernel.
             const int lim = min(rows, p.bpad);
-            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+            for (int c0 = 0; c0 < min(rows, p.bpad); c0 += 16) {  // live rows only
                 float v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);  // warp-collective
                 if (p.act_kind == 2) {
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             // stage this CTA's [128 features][bpad rows] partial in its (now idle) pipeline smem
             float* red = reinterpret_cast<float*>(base_ptr);
             const int f = quarter * 32 + lane;
-            for (int c0 = 0; c0 < p.bpad; c0 += 16) {
+            for (int c0 = 0; c0 < min(rows, p.bpad); c0 += 16) {  // live rows only
                 float v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);
 #pragma unroll
