@@ -187,6 +187,7 @@ struct eeb_ctx {
     eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
     eeb::DevBuf head_tok, head_conf, head_logp, head_tri;
+    eeb::DevBuf decide_ticket;  // int, zero between decide launches
     eeb::DevBuf tp_partial;         // row-parallel partial sums all-reduced across TP ranks
     eeb::DevBuf pf_meta;            // prefill (tok, slot, pos) of every prompt token, then the query blocks
     eeb::DevBuf pf_items;           // the current chunk's query blocks (int4) + their count
@@ -619,6 +620,10 @@ Ints ints_of(eeb_ctx* c) {
 }
 
 void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
+    if (!c->decide_ticket.p) {  // outside any capture
+        c->decide_ticket.ensure(4);
+        EEB_CUDA(cudaMemsetAsync(c->decide_ticket.p, 0, 4, c->stream));
+    }
     const eeb_model_desc& d = m.desc;
     const int R = std::max(batch, c->cap_rows);
     const size_t act = m.wbytes;
@@ -1128,6 +1133,7 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             }
             DecideArgs da;
             da.head_tri = head_tiles ? c->head_tri.as<float>() : nullptr;
+            da.ticket = c->decide_ticket.as<int>();  // allocated (zeroed) by ensure_workspace
             da.head_tiles = head_tiles;
             da.head_shards = m.tp;
             da.head_shard_stride = region / 4;  // float4 entries per rank region

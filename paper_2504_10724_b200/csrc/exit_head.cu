@@ -14,6 +14,8 @@
 //   unchanged  = head token == final token — engine.hpp:366;
 //   histogram  = ExitHistogram::add per exit layer — pht.hpp:19-22, engine.hpp:49.
 #include "../../include/eeb/eeb.h"
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace eeb {
@@ -93,13 +95,18 @@ __device__ __forceinline__ void write_row(const StepOutDev& o, int r, int exit_l
     o.bin[r] = bin;
 }
 
-// Single CTA: applies the token policy to the rows the head just ran on and,
-// for introspective steps, compacts the survivors (ballot + block scan).
-__global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
+// Applies the token policy to the rows the head just ran on and, for
+// introspective steps, compacts the survivors (ballot + block scan).  With the
+// fused head the per-tile partials are merged first, a warp per row spread
+// over the grid (one SM's L2 bandwidth would bound a single-CTA merge); the
+// last CTA to finish (ticket) then decides for every row.
+constexpr int kDecideThreads = 256;
+__global__ void __launch_bounds__(kDecideThreads) decide_kernel(DecideArgs a) {
     pdl_launch_dependents();
     pdl_wait();
     __shared__ int warp_counts[32];
     __shared__ int n_live_s;
+    __shared__ int last_s;
     const int n_live = *a.cur.n_active;
     const int e = a.exit_index;
     if (a.head_tri) {
@@ -108,7 +115,7 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
         // order (deterministic); argmax ties resolve to the lowest token id.
         const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
         const int tiles = a.head_tiles * a.head_shards;
-        for (int i = threadIdx.x >> 5; i < n_live; i += nw) {
+        for (int i = blockIdx.x * nw + (threadIdx.x >> 5); i < n_live; i += gridDim.x * nw) {
             const float4* tri = reinterpret_cast<const float4*>(a.head_tri) + (int64_t)i * a.head_tiles;
             // tile t of the whole vocabulary: region t / head_tiles (a TP shard), local tile t % head_tiles
             auto at = [&](int t) {
@@ -154,6 +161,15 @@ __global__ void __launch_bounds__(1024) decide_kernel(DecideArgs a) {
                 a.head.conf[i] = 1.0f / sum;
                 a.head.logp[i] = -logf(sum);
             }
+        }
+        if (gridDim.x > 1) {
+            __threadfence();  // this CTA's merged rows, visible before its ticket
+            __syncthreads();
+            if (threadIdx.x == 0) last_s = atomicAdd(a.ticket, 1) == (int)gridDim.x - 1;
+            __syncthreads();
+            if (!last_s) return;
+            __threadfence();
+            if (threadIdx.x == 0) *a.ticket = 0;  // every CTA has arrived: ready for the next launch
         }
         __syncthreads();
     }
@@ -282,7 +298,9 @@ void launch_head_reduce(const float* part, int splits, int64_t split_stride, int
 }
 
 void launch_decide(const DecideArgs& a, cudaStream_t s) {
-    launch_pdl(decide_kernel, dim3(1), dim3(1024), 0, s, a);
+    const int warps = kDecideThreads / 32;
+    const int grid = a.head_tri && a.ticket ? std::max(1, (a.max_rows + warps - 1) / warps) : 1;
+    launch_pdl(decide_kernel, dim3(grid), dim3(kDecideThreads), 0, s, a);
     EEB_CHECK_LAUNCH();
 }
 

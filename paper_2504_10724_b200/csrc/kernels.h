@@ -189,6 +189,9 @@ struct DecideArgs {
     // (decide sets the condition from the survivor count).
     int has_cond = 0;
     cudaGraphConditionalHandle cond = 0;
+    // fused-head merge spread over CTAs (a warp per row); the last CTA to
+    // finish, counted here (zero between launches), decides and compacts
+    int* ticket = nullptr;
 };
 void launch_decide(const DecideArgs& a, cudaStream_t s);
 // x_nxt[j] = x_cur[src[j]] (and the normalised row h) for live rows of the compacted state.
