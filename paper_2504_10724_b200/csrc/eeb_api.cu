@@ -2025,7 +2025,9 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
         kv_sync_table(c, m);
         EEB_CUDA(cudaSetDevice(c->device));
         wait_layers(c, m, depth);
-        const int chunk = d.dtype == EEB_BF16 ? 256 : 64;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
+        static const int env_chunk = std::getenv("EEB_PREFILL_CHUNK") ? std::atoi(std::getenv("EEB_PREFILL_CHUNK")) : 0;
+        const int chunk = d.dtype == EEB_BF16 ? (env_chunk >= 16 && env_chunk <= 256 ? env_chunk : 256)
+                                              : 64;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
         ensure_workspace(c, m, (int)std::min<int64_t>(chunk, total));
         // (tok, slot, pos) of every prompt token: one pinned staging + one H2D,
         // then a device-to-device slice per chunk.
