@@ -606,7 +606,9 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const int env_wave = std::getenv("EEB_TC_WAVE") ? std::atoi(std::getenv("EEB_TC_WAVE")) : 0;
     static const int env_stages = std::getenv("EEB_TC_STAGES") ? std::atoi(std::getenv("EEB_TC_STAGES")) : 0;
     const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
-    int splits = std::max(1, std::min(kblocks / 2, wave / tiles));
+    // (at most 16 planes: the attention kernels sum up to 16 QKV planes in registers;
+    //  only narrow GEMMs such as a 70B tensor-parallel QKV shard would want more)
+    int splits = std::max(1, std::min(std::min(kblocks / 2, wave / tiles), 16));
     // many rows (prefill chunks): cap the f32 partial planes at about the
     // weight bytes (splits * rows * N * 4 <= N * K * 2); decode shapes are
     // unaffected (C2: K / (2 * 64) = 16 >= the splits chosen above)
