@@ -288,14 +288,14 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 
 // CP: positions per chunk; NB: chunk buffers (2 = the next chunk's TMA is in
 // flight while this one computes)
-template <int HD, int CP, int NB, bool PAGED>
-__global__ void __launch_bounds__(kMmaWarps * 32, HD == 64 ? 5 : 1)  // hd 64: 5 CTAs/SM (register-limited)
+template <int HD, int CP, int NB, bool PAGED, int W = kMmaWarps>
+__global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 4-warp CTAs/SM (register-limited)
     attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          AttnArgs a) {
     constexpr int CB = HD / 64;                    // 64-dim column blocks
     constexpr int NT = HD / 8;                     // 8-dim n-tiles of O
     constexpr int KS = HD / 16;                    // 16-dim k-steps of Q.K
-    constexpr int TPW = CP / 8 / kMmaWarps;        // position tiles per warp per chunk
+    constexpr int TPW = CP / 8 / W;        // position tiles per warp per chunk
     constexpr uint32_t kBlockBytes = CP * 128;     // one column block of a chunk
     pdl_launch_dependents();
     pdl_wait();
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HD == 64 ? 5 : 1)  // hd 64: 5
         float cmax = -INFINITY;
 #pragma unroll
         for (int tt = 0; tt < TPW; ++tt) {
-            const int t = warp + tt * kMmaWarps;
+            const int t = warp + tt * W;
             sc[tt][0] = sc[tt][1] = -INFINITY;
             if (t >= n_tiles) continue;
             my_tiles = tt + 1;
@@ -525,9 +525,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HD == 64 ? 5 : 1)  // hd 64: 5
 #pragma unroll
         for (int tt = 0; tt < TPW; tt += 2) {
             if (tt >= my_tiles) break;
-            const int ta = warp + tt * kMmaWarps;
+            const int ta = warp + tt * W;
             const bool has_b = tt + 1 < my_tiles;
-            const int tb = has_b ? ta + kMmaWarps : ta;  // pad with a loaded tile, P = 0
+            const int tb = has_b ? ta + W : ta;  // pad with a loaded tile, P = 0
             uint32_t pa[4];
             pa[0] = pack_bf16(sc[tt][0], sc[tt][1]);
             pa[1] = 0u;
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HD == 64 ? 5 : 1)  // hd 64: 5
     // combine the four warps: O = sum_w e^(m_w - M) O_w / sum_w e^(m_w - M) l_w
     __syncthreads();
     float* comb = reinterpret_cast<float*>(base);  // reuse the K/V chunk memory
-    float* ml = comb + kMmaWarps * 8 * HD;          // [warp][head][2]
+    float* ml = comb + W * 8 * HD;          // [warp][head][2]
     if (h < G) {
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
@@ -565,9 +565,9 @@ __global__ void __launch_bounds__(kMmaWarps * 32, HD == 64 ? 5 : 1)  // hd 64: 5
     for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
         const int hh = idx / HD, j = idx % HD;
         float M = -INFINITY;
-        for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, ml[(w * 8 + hh) * 2]);
+        for (int w = 0; w < W; ++w) M = fmaxf(M, ml[(w * 8 + hh) * 2]);
         float num = 0.f, den = 0.f;
-        for (int w = 0; w < kMmaWarps; ++w) {
+        for (int w = 0; w < W; ++w) {
             const float mw = ml[(w * 8 + hh) * 2];
             const float f = mw == -INFINITY ? 0.f : __expf(mw - M);
             num += f * comb[(w * 8 + hh) * HD + j];
@@ -1298,19 +1298,27 @@ __global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
     if (i < rows) kv_depth[(int64_t)slot[i] * max_seq + pos[i]] = (uint8_t)depth;
 }
 
-template <int HD, int CP, int NB, bool PAGED>
-void launch_mma_cp_t(const AttnArgs& a, cudaStream_t s) {
+template <int HD, int CP, int NB, bool PAGED, int W>
+void launch_mma_cp_w(const AttnArgs& a, cudaStream_t s) {
     constexpr int CB = HD / 64;
     const int G = a.n_heads / a.n_kv_heads;
     if (a.splits > 16) throw Error(1, "attention: more than 16 QKV split-K planes");
     const size_t smem = 1024 + (size_t)NB * 2 * CB * CP * 128 + (8 + G + 2) * HD * 4;
-    auto kern = attention_mma_kernel<HD, CP, NB, PAGED>;
+    auto kern = attention_mma_kernel<HD, CP, NB, PAGED, W>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // x = kv head, y = row: the live rows' CTAs come first in launch order
     dim3 grid(a.n_kv_heads, a.max_rows);
-    launch_pdl(kern, grid, dim3(kMmaWarps * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
+    launch_pdl(kern, grid, dim3(W * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a);
     EEB_CHECK_LAUNCH();
+}
+
+template <int HD, int CP, int NB, bool PAGED>
+void launch_mma_cp_t(const AttnArgs& a, cudaStream_t s) {
+    // EEB_ATTN_WARPS=2: 2-warp CTAs (twice the CTAs per SM, half the cross-warp combine)
+    static const int env_w = std::getenv("EEB_ATTN_WARPS") ? std::atoi(std::getenv("EEB_ATTN_WARPS")) : 4;
+    if (env_w == 2 && CP / 8 / 2 >= 1) launch_mma_cp_w<HD, CP, NB, PAGED, 2>(a, s);
+    else launch_mma_cp_w<HD, CP, NB, PAGED, kMmaWarps>(a, s);
 }
 
 template <int HD, int CP, int NB>
