@@ -337,10 +337,17 @@ __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 
     __nv_bfloat16* kc = static_cast<__nv_bfloat16*>(a.k_cache) + new_off;
     __nv_bfloat16* vc = static_cast<__nv_bfloat16*>(a.v_cache) + new_off;
 
-    const int n_chunks = pos / CP + 1;
-    // thread 0: TMA positions [c0, c0+cn) of chunk ci (rounded up to whole boxes) into buffer ci % NB
-    auto issue = [&](int ci) {
-        const int c0 = ci * CP, buf = ci % NB;
+    const int n_all = pos / CP + 1;  // chunks of this row
+    // KV split z owns chunks [cb, ce) (possibly none); the one holding pos writes the new K/V
+    const int S = a.kv_splits, z = blockIdx.z;
+    const int per = (n_all + S - 1) / S;
+    const int cb = min(n_all, z * per), ce = min(n_all, cb + per);
+    const int n_chunks = ce - cb;
+    const bool owns_pos = ce == n_all && n_chunks > 0;
+    // thread 0: TMA positions [c0, c0+cn) of local chunk li (rounded up to whole boxes) into buffer li % NB
+    auto issue = [&](int li) {
+        const int ci = cb + li;
+        const int c0 = ci * CP, buf = li % NB;
         const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
         const uint32_t bar_a = smem_u32(&bars[buf]);
         const int n_load = min(CP, pos + 1 - c0);
@@ -420,7 +427,7 @@ __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 
         const float x0 = k[jj], x1 = k[jj + half];
         const float kr = j < half ? x0 * cs[jj] - x1 * sn[jj] : x0 * sn[jj] + x1 * cs[jj];
         const __nv_bfloat16 kt = __float2bfloat16_rn(kr), vt = __float2bfloat16_rn(vv[j]);
-        if (!a.kv_ready) {
+        if (!a.kv_ready && owns_pos) {
             kc[j] = kt;
             vc[j] = vt;
         }
@@ -444,16 +451,17 @@ __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 
     float m_run = -INFINITY, l_run = 0.f;
     const uint8_t* depth = a.kv_depth + (int64_t)slot * a.max_seq;
 
-    for (int ci = 0; ci < n_chunks; ++ci) {
+    for (int li = 0; li < n_chunks; ++li) {
+        const int ci = cb + li;
         const int c0 = ci * CP;
         const int cn = min(CP, pos + 1 - c0);
-        const int buf = ci % NB;
+        const int buf = li % NB;
         const uint32_t k_s = sbase + buf * kBufBytes, v_s = k_s + CB * kBlockBytes;
-        if (NB == 1 && ci > 0) {
+        if (NB == 1 && li > 0) {
             __syncthreads();  // everyone is done with the previous chunk
-            if (threadIdx.x == 0) issue(ci);
+            if (threadIdx.x == 0) issue(li);
         }
-        mbar_wait(smem_u32(&bars[buf]), (uint32_t)((ci / NB) & 1));
+        mbar_wait(smem_u32(&bars[buf]), (uint32_t)((li / NB) & 1));
         if (!a.kv_ready && pos < c0 + CP) {  // the new position lives in this chunk: write it (swizzled)
             const int r = pos - c0;
             uint8_t* bb = base + buf * kBufBytes;
@@ -464,9 +472,9 @@ __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 
             }
         }
         __syncthreads();
-        // NB >= 2: everyone is past chunk ci-1, so its buffer takes chunk ci-1+NB
+        // NB >= 2: everyone is past chunk li-1, so its buffer takes chunk li-1+NB
         // while this chunk computes
-        if (NB >= 2 && threadIdx.x == 0 && ci >= 1 && ci - 1 + NB < n_chunks) issue(ci - 1 + NB);
+        if (NB >= 2 && threadIdx.x == 0 && li >= 1 && li - 1 + NB < n_chunks) issue(li - 1 + NB);
         const int n_tiles = (cn + 7) / 8;
         // scores for this warp's tiles (C fragment: row h, positions kq, kq+1)
         float sc[TPW][2];
@@ -562,6 +570,8 @@ __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 
     }
     __syncthreads();
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out) + (int64_t)i * dq;
+    // this CTA's partial per head: (O unnormalised w.r.t. its max M, M, l)
+    float* part = S > 1 ? a.kv_part + ((int64_t)(i * Hkv + g) * S) * (8 * (HD + 2)) : nullptr;
     for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
         const int hh = idx / HD, j = idx % HD;
         float M = -INFINITY;
@@ -573,8 +583,41 @@ __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 
             num += f * comb[(w * 8 + hh) * HD + j];
             den += f * ml[(w * 8 + hh) * 2 + 1];
         }
+        if (S == 1) {
+            out[(g * G + hh) * HD + j] = __float2bfloat16_rn(num / den);
+        } else {
+            float* pz = part + (int64_t)z * (8 * (HD + 2)) + hh * (HD + 2);
+            pz[j] = num;
+            if (j == 0) {
+                pz[HD] = M;
+                pz[HD + 1] = den;
+            }
+        }
+    }
+    if (S == 1) return;
+    __threadfence();
+    __syncthreads();
+    __shared__ int last_s;
+    if (threadIdx.x == 0) last_s = atomicAdd(a.kv_ticket + i * Hkv + g, 1) == S - 1;
+    __syncthreads();
+    if (!last_s) return;
+    __threadfence();
+    // last split: combine the S partials in split order (deterministic)
+    for (int idx = threadIdx.x; idx < G * HD; idx += blockDim.x) {
+        const int hh = idx / HD, j = idx % HD;
+        float M = -INFINITY;
+        for (int q = 0; q < S; ++q) M = fmaxf(M, __ldcg(part + (int64_t)q * (8 * (HD + 2)) + hh * (HD + 2) + HD));
+        float num = 0.f, den = 0.f;
+        for (int q = 0; q < S; ++q) {
+            const float* pq = part + (int64_t)q * (8 * (HD + 2)) + hh * (HD + 2);
+            const float mq = __ldcg(pq + HD);
+            const float f = mq == -INFINITY ? 0.f : __expf(mq - M);
+            num += f * __ldcg(pq + j);
+            den += f * __ldcg(pq + HD + 1);
+        }
         out[(g * G + hh) * HD + j] = __float2bfloat16_rn(num / den);
     }
+    if (threadIdx.x == 0) a.kv_ticket[i * Hkv + g] = 0;  // all splits arrived: ready for the next launch
 }
 
 // ---------------------------------------------------------------------------
@@ -1307,7 +1350,7 @@ void launch_mma_cp_w(const AttnArgs& a, cudaStream_t s) {
     auto kern = attention_mma_kernel<HD, CP, NB, PAGED, W>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     // x = kv head, y = row: the live rows' CTAs come first in launch order
-    dim3 grid(a.n_kv_heads, a.max_rows);
+    dim3 grid(a.n_kv_heads, a.max_rows, a.kv_part && a.kv_ticket ? a.kv_splits : 1);
     launch_pdl(kern, grid, dim3(W * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a);
     EEB_CHECK_LAUNCH();

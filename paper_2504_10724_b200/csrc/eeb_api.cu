@@ -188,6 +188,7 @@ struct eeb_ctx {
     eeb::DevBuf rows;  // ints: nA, nB, rowA, slotA, posA, rowB, slotB, posB, src, in_tok, in_slot, in_pos
     eeb::DevBuf head_tok, head_conf, head_logp, head_tri;
     eeb::DevBuf decide_ticket;  // int, zero between decide launches
+    eeb::DevBuf kv_part, kv_ticket;  // decode KV-split partials and per-(row, kv head) tickets
     eeb::DevBuf tp_partial;         // row-parallel partial sums all-reduced across TP ranks
     eeb::DevBuf pf_meta;            // prefill (tok, slot, pos) of every prompt token, then the query blocks
     eeb::DevBuf pf_items;           // the current chunk's query blocks (int4) + their count
@@ -619,10 +620,29 @@ Ints ints_of(eeb_ctx* c) {
     return r;
 }
 
+// Decode attention KV splits (flash-decoding; EEB_ATTN_KVSPLIT, default 1: on
+// C2 2 splits measured 1.73 vs 1.47 ms/step — the per-CTA prologue and the
+// combine cost more than the parallelism gains at <= 227 positions).
+int kv_splits() {
+    static const int v = std::getenv("EEB_ATTN_KVSPLIT") ? std::max(1, std::min(8, std::atoi(std::getenv("EEB_ATTN_KVSPLIT"))))
+                                                         : 1;
+    return v;
+}
+
 void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     if (!c->decide_ticket.p) {  // outside any capture
         c->decide_ticket.ensure(4);
         EEB_CUDA(cudaMemsetAsync(c->decide_ticket.p, 0, 4, c->stream));
+    }
+    if (const int S = kv_splits(); S > 1) {  // decode KV split: partials + tickets (zeroed when grown)
+        const size_t rows = (size_t)std::max(batch, c->cap_rows);
+        const size_t part = rows * m.hkv_l * m.shards * S * 8 * (m.head_dim + 2) * 4;
+        const size_t tick = rows * m.hkv_l * m.shards * 4;
+        if (part > c->kv_part.bytes) c->kv_part.ensure(part);
+        if (tick > c->kv_ticket.bytes) {
+            c->kv_ticket.ensure(tick);
+            EEB_CUDA(cudaMemsetAsync(c->kv_ticket.p, 0, c->kv_ticket.bytes, c->stream));
+        }
     }
     const eeb_model_desc& d = m.desc;
     const int R = std::max(batch, c->cap_rows);
@@ -877,6 +897,11 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         a.page_table = m.page_table.as<int>();
         a.page_size = m.kv_page;
         a.pages_per_seq = m.pages_per_seq;
+        if (!kv_ready && kv_splits() > 1 && c->kv_part.p && c->kv_ticket.p) {
+            a.kv_splits = kv_splits();
+            a.kv_part = c->kv_part.as<float>();
+            a.kv_ticket = c->kv_ticket.as<int>();
+        }
         if (kv_ready && c->pf_cur_items > 0) {
             a.pf_items = c->pf_items.as<int4>();
             a.pf_n_items = reinterpret_cast<const int*>(c->pf_items.as<int4>() + c->pf_cur_items);

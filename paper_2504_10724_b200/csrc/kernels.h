@@ -124,6 +124,13 @@ struct AttnArgs {
     const int4* pf_items = nullptr;
     const int* pf_n_items = nullptr;
     int pf_max_items = 0;
+    // Decode KV split (flash-decoding): kv_splits CTAs share a (row, kv head),
+    // each over a contiguous range of 64-position chunks; partials
+    // {O (unnormalised), max, sum} go to kv_part and the last split to finish
+    // (kv_ticket, zero between launches) combines them in split order.
+    int kv_splits = 1;
+    float* kv_part = nullptr;   // [max_rows][Hkv][kv_splits][8][hd + 2]
+    int* kv_ticket = nullptr;   // [max_rows][Hkv]
 };
 // Device address of (page-table row of slot, position, kv head, dim 0) in a layer's K or V cache.
 __host__ __device__ inline int64_t kv_elem_offset(const AttnArgs& a, int slot, int pos, int g) {
