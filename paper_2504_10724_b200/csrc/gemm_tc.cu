@@ -213,7 +213,13 @@ __global__ void __launch_bounds__(kThreads, 2)
 #endif
     EEB_STAMP(threadIdx.x == 0, 0);  // CTA start
     pdl_launch_dependents();  // let the next kernel of the step get resident and prefetch
+    __shared__ int pre_s;
     if (threadIdx.x == 0) {
+        // The live-row hint is loaded first (its latency overlaps the barrier
+        // inits).  No weight prefetch when no row is live (all exited): read
+        // before the PDL wait it may be stale, which costs only a useless or a
+        // missed prefetch — the count after the wait decides what is computed.
+        const int hint = p.skip_dead ? *reinterpret_cast<const volatile int*>(p.n_active) : 1;
         prefetch_tmap(&tmap_w);
         prefetch_tmap(&tmap_x);
         for (int s = 0; s < S; ++s) {
@@ -222,6 +228,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         mbar_init(tfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // Weights do not depend on the previous kernel: the first stages' weight
+        // tiles stream before the TMEM allocation and the PDL wait; the
+        // activation tiles follow once the predecessor's output is visible.
+        const int pre = hint <= 0 ? 0 : min(S, nkb);
+        const uint64_t pol_w0 = policy_evict_first();
+        for (int i = 0; i < pre; ++i) {
+            const uint32_t sa = base + (uint32_t)i * stage_bytes;
+            mbar_expect_tx(full0 + 8 * i, stage_bytes);
+            tma_load_2d(sa, &tmap_w, full0 + 8 * i, (kb0 + i) * kBK, m_tile * kBM, pol_w0);
+        }
+        pre_s = pre;
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -236,23 +253,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == 0) {
         const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-        // No weight prefetch when no row is live (all exited): the count read
-        // before the wait may be stale, which costs only a useless or missed
-        // prefetch — the count after the wait decides what is computed.
-        static constexpr bool kSkipDead = true;
-        const int pre = (kSkipDead && p.skip_dead && *reinterpret_cast<const volatile int*>(p.n_active) <= 0)
-                            ? 0 : min(S, nkb);
-        if (lane == 0) {
-            // Weights do not depend on the previous kernel: fill the first
-            // stages with weight tiles before waiting on it (PDL), then add the
-            // activation tiles once the predecessor's output is visible.
-            for (int i = 0; i < pre; ++i) {
-                const uint32_t sa = base + (uint32_t)i * stage_bytes;
-                mbar_expect_tx(full0 + 8 * i, stage_bytes);
-                tma_load_2d(sa, &tmap_w, full0 + 8 * i, (kb0 + i) * kBK, m_tile * kBM, pol_w);
-            }
-        }
-        __syncwarp();
+        const int pre = pre_s;  // weight stages already in flight (issued by thread 0 above)
 #ifdef EEB_L2_PREFETCH
         // (compiled in only for the experiment: measured slower, see gemm_tc host)
         if (lane != 0 && p.pf_bytes) {
