@@ -1379,13 +1379,16 @@ void launch_mma_cp(const AttnArgs& a, cudaStream_t s) {
 template <int HD>
 void launch_mma(const AttnArgs& a, cudaStream_t s) {
     static const int env_cp = std::getenv("EEB_ATTN_CP") ? std::atoi(std::getenv("EEB_ATTN_CP")) : 0;
-    // measured C2 (hd 64, context 128..227): 64 positions 1.56 ms/step, 128 1.61, 256 1.64
-    const int cp = env_cp > 0 ? env_cp : (HD == 64 ? 64 : 128);
+    // measured C2 (hd 64, context 128..227), single-buffered: 64 positions 1.56 ms/step, 128 1.61, 256 1.64
+    // C2 (same box): 32-position double-buffered chunks 1.458 ms/step, 64 1.468
+    const int cp = env_cp > 0 ? env_cp : (HD == 64 ? 32 : 128);
     static const int env_nb = std::getenv("EEB_ATTN_NB") ? std::atoi(std::getenv("EEB_ATTN_NB")) : 0;
     // double-buffered 64-position chunks at 5 CTAs/SM: C2 1.497 vs 1.565 ms/step
     // single-buffered (same box, two orders)
     const int nb = env_nb > 0 ? env_nb : (cp <= 64 ? 2 : 1);
-    if (nb >= 2) {
+    if (nb >= 4 && cp <= 32) {
+        launch_mma_cp<HD, 32, 4>(a, s);
+    } else if (nb >= 2) {
         if (cp <= 32) launch_mma_cp<HD, 32, 2>(a, s);
         else if (cp <= 64) launch_mma_cp<HD, 64, 2>(a, s);
         else launch_mma_cp<HD, 128, 2>(a, s);
