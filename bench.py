@@ -404,24 +404,7 @@ def run_eeb(args, desc):
                    else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
     hist_np = hist_acc.cpu().numpy().astype(np.float64)
     exit_head = None
-    if prof.get("persistent"):
-        # One kernel is the whole step: its algorithmic bytes are every weight
-        # tile the program streams (layer GEMMs + the exit heads evaluated)
-        # plus the KV cache the surviving rows attend over.
-        step_ms = prof["persistent_ms"] / nsteps
-        w_bytes = prof["weight_bytes"]
-        rows_at = hist_np / max(1.0, hist_np.sum()) * B           # rows exiting at each head per step
-        mean_ctx = P + 0.5 * args.steps + 1                        # positions attended (prompt + decode so far)
-        kv_bytes = float(np.sum(rows_at * np.asarray(desc.exit_layers))) * mean_ctx * 2 * \
-            desc.n_kv_heads * desc.head_dim * desc.bytes_per_el
-        alg = int(w_bytes + kv_bytes)
-        roof = {"bound": "hbm", "kernel": "persistent EE decode-step kernel (all phases, one launch)",
-                "achieved": alg / (step_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s", "traffic": None,
-                "peak_source": peak_source, "algorithmic_bytes_per_step": alg,
-                "weight_bytes_per_step": int(w_bytes), "kv_bytes_per_step": int(kv_bytes),
-                "kernel_ms_per_step": step_ms, "step_share": step_ms / ms}
-        roof["frac"] = roof["achieved"] / hbm
-    else:
+    if True:
         gemm_ms = prof["layer_gemm_ms"] / nsteps
         head_ms = prof["exit_head_ms"] / nsteps
         attn_ms = prof["attention_ms"] / nsteps
@@ -546,7 +529,7 @@ def run_eeb(args, desc):
                 "clocks": clocks, "exit_fractions": exit_frac, "prefill": prefill,
                 "kernel_ms_per_step": {k.replace("_ms", ""): v / nsteps for k, v in prof.items()
                                        if k.endswith("_ms") and v > 0},
-                "path": "persistent step kernel" if prof.get("persistent") else "per-op kernel chain"}
+                "path": "per-op kernel chain (CUDA graph, PDL)"}
         if secondary is not None:
             line["secondary_c4"] = secondary
         if c3 is not None:
@@ -576,7 +559,7 @@ def main():
     ap.add_argument("--th", type=float, default=0.7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 (34B) line attached at N=1")
-    ap.add_argument("--tier", type=int, default=0, help="0 auto (persistent kernel), 2 per-op kernel chain")
+    ap.add_argument("--tier", type=int, default=0, help="0 auto, 1 CUDA-core GEMV, 2 tcgen05 GEMMs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -204,12 +204,20 @@ eeb_status eeb_prefill(eeb_ctx* ctx, int model, int depth, int32_t n_seq, const 
  * reuse it on later identical calls (0 = off, 1 = on; default on). */
 eeb_status eeb_set_graphs(eeb_ctx* ctx, int enable);
 
-/* Kernel tier override for tests: 0 = auto (the persistent step kernel where
- * applicable — bf16, head_dim 64, batch <= 128, max_seq_len <= 256 — else the
- * per-op kernel chain), 1 = per-op chain with CUDA-core GEMV only, 2 = per-op
- * chain with tcgen05 GEMMs where applicable, 3 = persistent step kernel
- * (EEB_E_DOMAIN if not applicable). */
+/* Kernel tier override for tests: 0 = auto (tcgen05 GEMMs for bf16 models,
+ * CUDA-core GEMV for f32), 1 = CUDA-core GEMV only, 2 = tcgen05 GEMMs
+ * (EEB_E_DOMAIN where not applicable). */
 eeb_status eeb_set_gemm_tier(eeb_ctx* ctx, int tier);
+
+/* In-graph launch timeline (diagnostics; the bench's roofline source).
+ * max_launches > 0: every later decode step records, per kernel launch, the
+ * first CTA start and the last warp exit (%globaltimer, written by the kernels
+ * themselves inside the captured PDL graph); 0 turns it off.  Toggling drops
+ * the captured graphs. */
+eeb_status eeb_debug_stamps(eeb_ctx* ctx, int max_launches);
+/* JSON {"launches": [{"kernel", "start_ns", "end_ns", "ctas"}, ...]} of the
+ * last decode step, in launch order, times relative to its first CTA start. */
+eeb_status eeb_debug_stamps_read(eeb_ctx* ctx, char* json_out, int64_t cap);
 
 /* Test/diagnostic hooks (not used on the serving path). */
 eeb_status eeb_debug_last_logits(eeb_ctx* ctx, int head, float* host_out, int64_t n);  /* [batch][vocab] of one head, when retained */
@@ -231,10 +239,6 @@ eeb_status eeb_debug_gemm(eeb_ctx* ctx, int tier, int dtype, int n, int k, int b
  * mean milliseconds per launch (CUDA events on the context stream). */
 eeb_status eeb_debug_bench_gemm(eeb_ctx* ctx, int tier, int n, int k, int batch, int iters, double* ms_out);
 
-/* Steady-state timing of the persistent step kernel streaming every loaded
- * layer's four GEMMs of `model` (zero activations, `batch` rows); returns the
- * mean milliseconds per launch. */
-eeb_status eeb_debug_bench_layers(eeb_ctx* ctx, int model, int batch, int iters, double* ms_out);
 
 /* Per-kernel timing of the last step (CUDA events on the context stream).
  * names: "gemm", "attention", "exit_head", ... ; returns total ms. */

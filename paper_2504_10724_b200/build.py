@@ -2,8 +2,8 @@
 
 * ``paper_2504_10724_b200/libeeb.so`` — the CUDA kernels and the C ABI
   (include/eeb/eeb.h), compiled for sm_100a only.
-* ``paper_2504_10724_b200/libeeserve_host.so`` — the host C++ engine over the
-  C ABI (include/eeserve/*.hpp), also used by the C++ unit tests.
+The host C++ engine (include/eeserve/*.hpp) is header-only; its test and tool
+binaries are built by host_build.py.
 
 The build uses nvcc directly (no torch JIT cache) so the .so files live in the
 repo and travel to the GPU box with the snapshot.
@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     f"-I{ROOT / 'include'}",
 ]
 SOURCES = ["synth_kernels.cu", "rows.cu", "gemm_cc.cu", "gemm_tc.cu", "attention.cu",
-           "exit_head.cu", "step_mk.cu", "eeb_api.cu"]
+           "exit_head.cu", "eeb_api.cu"]
 
 
 def _deps(src: Path) -> list[Path]:

@@ -49,7 +49,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads) attention_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kThreads) attention_kernel(Stamp stamp, AttnArgs a) {
+    StampScope stamp_scope(stamp);
     constexpr int VEC = Vec16<T>::N;  // elements per 16 B
     pdl_launch_dependents();
     pdl_wait();
@@ -290,8 +291,9 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
 // flight while this one computes)
 template <int HD, int CP, int NB, bool PAGED, int W = kMmaWarps>
 __global__ void __launch_bounds__(W * 32, HD == 64 ? 20 / W : 1)  // hd 64: 5 x 4-warp CTAs/SM (register-limited)
-    attention_mma_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+    attention_mma_kernel(Stamp stamp, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          AttnArgs a) {
+    StampScope stamp_scope(stamp);
     constexpr int CB = HD / 64;                    // 64-dim column blocks
     constexpr int NT = HD / 8;                     // 8-dim n-tiles of O
     constexpr int KS = HD / 16;                    // 16-dim k-steps of Q.K
@@ -664,8 +666,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 
 template <int HD>
 __global__ void __launch_bounds__(PipeCfg<HD>::NW * 32, 2)
-    attention_pipe_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+    attention_pipe_kernel(Stamp stamp, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                           AttnArgs a) {
+    StampScope stamp_scope(stamp);
     using C = PipeCfg<HD>;
     constexpr int CB = C::CB, CP = C::CP, NBUF = C::NBUF, NW = C::NW;
     constexpr uint32_t kBlockBytes = C::kBlockBytes, kBufBytes = C::kBufBytes;
@@ -1059,7 +1062,8 @@ __device__ __forceinline__ void store4_kv(T* dst, float x, float y, float z, flo
 // Prefill: RoPE the keys and append K/V of every live row (one CTA per row;
 // a thread owns 4 dims of each half of a key head, or 4 dims of a value head).
 template <typename T>
-__global__ void kv_append_kernel(AttnArgs a) {
+__global__ void kv_append_kernel(Stamp stamp, AttnArgs a) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x;
@@ -1106,8 +1110,9 @@ __global__ void kv_append_kernel(AttnArgs a) {
 // ---------------------------------------------------------------------------
 template <int HD, bool PAGED>
 __global__ void __launch_bounds__(128)
-    attention_prefill_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+    attention_prefill_kernel(Stamp stamp, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                              AttnArgs a) {
+    StampScope stamp_scope(stamp);
     constexpr int CB = HD / 64, CP = 64, NT = HD / 8, KS = HD / 16, NB = 2;
     constexpr uint32_t kBlockBytes = CP * 128, kBufBytes = 2 * CB * kBlockBytes;
     constexpr int kDep = 1024, kMaxPt = PAGED ? 64 : 1;
@@ -1333,8 +1338,9 @@ void launch_prefill_attn(const AttnArgs& a, cudaStream_t s) {
     EEB_CHECK_LAUNCH();
 }
 
-__global__ void mark_depth_kernel(int rows, const int* slot, const int* pos,
+__global__ void mark_depth_kernel(Stamp stamp, int rows, const int* slot, const int* pos,
                                   uint8_t* kv_depth, int max_seq, int depth) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;

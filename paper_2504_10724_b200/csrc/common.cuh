@@ -94,11 +94,51 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// ---------------------------------------------------------------------------
+// In-graph launch timeline (eeb_debug_stamps).  Every step kernel takes a Stamp
+// as its first argument and opens a StampScope: with stamping on, thread 0 of
+// each CTA records the CTA's start and lane 0 of every warp its exit
+// (%globaltimer, fire-and-forget red.min / red.max into [slot][cta] cells, no
+// contention), so the host gets each launch's first-start / last-exit inside
+// the captured, PDL-chained graph — the execution that is timed.  Off (buf
+// null): one predicated branch per CTA.
+// ---------------------------------------------------------------------------
+struct Stamp {
+    unsigned long long* buf = nullptr;  // starts [slots][kStampCtas], then ends at buf + end_off
+    int slot = 0;
+    int64_t end_off = 0;
+};
+constexpr int kStampCtas = 2048;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)::"memory");
+    return t;
+}
+__device__ __forceinline__ unsigned long long* stamp_cell(const Stamp& s) {
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    return s.buf + (size_t)s.slot * kStampCtas + min(cta, (unsigned)kStampCtas - 1);
+}
+struct StampScope {
+    const Stamp& s;
+    __device__ __forceinline__ explicit StampScope(const Stamp& st) : s(st) {
+        if (s.buf && threadIdx.x == 0)
+            asm volatile("red.global.min.u64 [%0], %1;" ::"l"(stamp_cell(s)), "l"(gtimer()) : "memory");
+    }
+    __device__ __forceinline__ ~StampScope() {
+        if (s.buf && (threadIdx.x & 31) == 0)
+            asm volatile("red.global.max.u64 [%0], %1;" ::"l"(stamp_cell(s) + s.end_off), "l"(gtimer()) : "memory");
+    }
+};
+// Host: the stamp for the next launch (defined in eeb_api.cu; buf null unless
+// the calling thread is recording a timeline).
+Stamp stamp_next(const void* kernel);
+
 // Host: launch with the programmatic-stream-serialization attribute so the
 // kernel may start while its predecessor drains (captured into graphs as a
-// programmatic edge).
+// programmatic edge).  The kernel's first parameter is its Stamp.
 template <typename... KArgs, typename... Args>
-inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+inline void launch_pdl(void (*kern)(Stamp, KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -126,7 +166,8 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
         }
     }
     cfg.numAttrs = off ? 0 : 1;
-    EEB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+    EEB_CUDA(cudaLaunchKernelEx(&cfg, kern, stamp_next(reinterpret_cast<const void*>(kern)),
+                                std::forward<Args>(args)...));
 }
 
 }  // namespace eeb

@@ -24,7 +24,6 @@
 
 #include "../../include/eeb/eeb.h"
 #include "kernels.h"
-#include "step_mk.cuh"
 #include "synth.cuh"
 
 namespace eeb {
@@ -45,8 +44,9 @@ struct DevBuf {
         p = nullptr;
         bytes = 0;
     }
-    void ensure(size_t n) {
-        if (n <= bytes) return;
+    // Returns true when the buffer moved (captured graphs holding it are stale).
+    bool ensure(size_t n) {
+        if (n <= bytes) return false;
         release();
         EEB_CUDA(cudaMalloc(&p, n));
         bytes = n;
@@ -54,6 +54,7 @@ struct DevBuf {
         // never-written memory show up deterministically
         static const bool poison = std::getenv("EEB_DEBUG_POISON") != nullptr;
         if (poison) EEB_CUDA(cudaMemset(p, 0xFF, n));
+        return true;
     }
     template <typename T> T* as() const { return static_cast<T*>(p); }
 };
@@ -153,13 +154,6 @@ struct GraphKey {
 
 enum Cat { kCatGemm = 0, kCatAttn, kCatHead, kCatNorm, kCatOther, kNumCat };
 
-// A compiled persistent-kernel program for one (model, depth, policy, batch, th).
-struct MkProg {
-    DevBuf phases, maps, segtab, gains;
-    mk::Params P{};
-    int n_gemm = 0;
-    int64_t weight_bytes = 0;  // algorithmic weight bytes streamed per launch
-};
 const char* kCatNames[kNumCat] = {"layer_gemm", "attention", "exit_head", "norm", "other"};
 
 }  // namespace
@@ -213,14 +207,11 @@ struct eeb_ctx {
     int64_t steps_profiled = 0;
     ncclComm_t nccl = nullptr;
     eeb::DevBuf nccl_buf;
-    // persistent step kernel
-    int mk_mode = -1;  // -1 unset (env EEB_MK, default on), 0 off, 1 on
-    std::map<eeb::GraphKey, std::unique_ptr<eeb::MkProg>> mk_progs;
-    eeb::DevBuf mk_partials, mk_bar, mk_stats;
-    unsigned long long mk_bar_count = 0;
-    int last_step_mk = 0;
-    int64_t last_step_weight_bytes = 0;
-    double mk_ms = 0;  // profiled persistent-kernel time
+    // in-graph launch timeline (eeb_debug_stamps)
+    int stamp_cap = 0;  // launches per step recorded (0 = off)
+    eeb::DevBuf stamp_buf;
+    std::map<eeb::GraphKey, std::pair<std::vector<const void*>, std::vector<int>>> stamp_kernels;  // per graph: slot -> kernel, category
+    std::pair<std::vector<const void*>, std::vector<int>> stamp_last;                              // ... of the last step launched
 };
 
 namespace eeb {
@@ -426,7 +417,6 @@ void settle_pending(Model& m) {
 
 void load_to(eeb_ctx* c, Model& m, int to) {
     const eeb_model_desc& d = m.desc;
-    c->mk_progs.clear();  // compiled persistent programs hold weight pointers
     if (to < 0 || to > d.num_layers)
         throw Error(EEB_E_DOMAIN, "load: depth " + std::to_string(to) + " outside [0, " +
                                       std::to_string(d.num_layers) + "]");
@@ -520,7 +510,6 @@ void load_async(eeb_ctx* c, Model& m, int to) {
         throw Error(EEB_E_CAPACITY, "host tier holds " + std::to_string(m.host.layers.size()) +
                                         " layers; stage them first (eeb_host_stage)");
     settle_pending(m);
-    c->mk_progs.clear();
     cudaStream_t ls = c->load_stream;
     auto P = std::make_unique<PendingLoad>();
     EEB_CUDA(cudaEventCreate(&P->t0));
@@ -629,18 +618,68 @@ int kv_splits() {
     return v;
 }
 
+// Destroy the captured step graphs (all models, or one) and the persistent
+// programs: they hold device pointers by value.
+void drop_graphs(eeb_ctx* c, int model = -1) {
+    for (auto it = c->graphs.begin(); it != c->graphs.end();) {
+        if (model < 0 || it->first.model == model) {
+            cudaGraphExecDestroy(it->second);
+            it = c->graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+// ---- in-graph launch timeline (common.cuh Stamp) ----------------------------
+struct StampState {
+    unsigned long long* buf = nullptr;
+    int cap = 0;
+    std::vector<const void*> kernels;  // slot -> kernel, in launch order
+    std::vector<int> cats;             // slot -> Cat (labelled by count())
+};
+thread_local StampState* g_stamp = nullptr;
+
+// Active while one step (or prefill chunk) is enqueued / captured with
+// stamping on: hands out consecutive slots to the launches.
+struct StampSession {
+    StampState st;
+    bool on;
+    explicit StampSession(eeb_ctx* c) : on(c->stamp_cap > 0) {
+        if (!on) return;
+        st.buf = c->stamp_buf.as<unsigned long long>();
+        st.cap = c->stamp_cap;
+        g_stamp = &st;
+    }
+    ~StampSession() {
+        if (on) g_stamp = nullptr;
+    }
+};
+
+// Reset the cells before a stamped step: starts to ~0 (red.min), ends to 0 (red.max).
+void stamp_reset(eeb_ctx* c) {
+    const size_t cells = (size_t)c->stamp_cap * kStampCtas;
+    EEB_CUDA(cudaMemsetAsync(c->stamp_buf.p, 0xFF, cells * 8, c->stream));
+    EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + cells, 0, cells * 8, c->stream));
+}
+
+// Size the step workspace for `batch` rows of model m.  Buffers are shared by
+// every model of the context and grow to the largest; whenever one moves, every
+// captured graph (of any model: a smaller model's graph holds the old pointer)
+// is dropped and recaptured on its next step.
 void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
+    bool moved = false;
     if (!c->decide_ticket.p) {  // outside any capture
-        c->decide_ticket.ensure(4);
+        moved |= c->decide_ticket.ensure(4);
         EEB_CUDA(cudaMemsetAsync(c->decide_ticket.p, 0, 4, c->stream));
     }
     if (const int S = kv_splits(); S > 1) {  // decode KV split: partials + tickets (zeroed when grown)
         const size_t rows = (size_t)std::max(batch, c->cap_rows);
         const size_t part = rows * m.hkv_l * m.shards * S * 8 * (m.head_dim + 2) * 4;
         const size_t tick = rows * m.hkv_l * m.shards * 4;
-        if (part > c->kv_part.bytes) c->kv_part.ensure(part);
-        if (tick > c->kv_ticket.bytes) {
-            c->kv_ticket.ensure(tick);
+        moved |= c->kv_part.ensure(part);
+        if (c->kv_ticket.ensure(tick)) {
+            moved = true;
             EEB_CUDA(cudaMemsetAsync(c->kv_ticket.p, 0, c->kv_ticket.bytes, c->stream));
         }
     }
@@ -648,19 +687,15 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     const int R = std::max(batch, c->cap_rows);
     const size_t act = m.wbytes;
     const int64_t D = d.d_model, F = d.d_ffn;
-    if (R > c->cap_rows) {
-        for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
-        c->graphs.clear();
-        c->mk_progs.clear();  // programs hold workspace pointers
-    }
+    moved |= R != c->cap_rows;  // the row-index arrays' layout depends on cap_rows
     c->cap_rows = R;
-    c->xA.ensure((size_t)R * D * 4);
-    c->xB.ensure((size_t)R * D * 4);
-    c->hn.ensure((size_t)R * D * act);
-    c->hnB.ensure((size_t)R * D * act);
-    c->hhead.ensure((size_t)R * D * act);
-    c->attn.ensure((size_t)R * m.dq * act);
-    c->mlp_h.ensure((size_t)R * F * act);
+    moved |= c->xA.ensure((size_t)R * D * 4);
+    moved |= c->xB.ensure((size_t)R * D * 4);
+    moved |= c->hn.ensure((size_t)R * D * act);
+    moved |= c->hnB.ensure((size_t)R * D * act);
+    moved |= c->hhead.ensure((size_t)R * D * act);
+    moved |= c->attn.ensure((size_t)R * m.dq * act);
+    moved |= c->mlp_h.ensure((size_t)R * F * act);
     // split-K partial bound: splits <= K / (32 * vec) for every GEMM of the step.
     const int64_t kmin = act == 4 ? 128 : 256;
     int64_t need = 0;  // split-K planes per GEMM: tier 1 <= K/(32 vec)+1, tier 2 <= SMs/tiles+1
@@ -674,27 +709,27 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     upd(D, m.f_l);
     upd(m.v_l, D);
     need *= m.shards;  // row-parallel shards write their partial planes side by side
-    c->ws.ensure((size_t)need * 4);
+    moved |= c->ws.ensure((size_t)need * 4);
     c->ws_elems = (int64_t)(c->ws.bytes / 4);
-    c->rows.ensure((size_t)(32 + 12 * R) * 4);
-    c->head_tok.ensure((size_t)R * 4);
-    c->head_tri.ensure((size_t)R * ((m.v_l + 127) / 128) * m.tp * 16);
-    if (m.tp > 1) c->tp_partial.ensure((size_t)R * D * 4);
-    c->head_conf.ensure((size_t)R * 4);
-    c->head_logp.ensure((size_t)R * 4);
-    c->o_exit.ensure((size_t)R * 4);
-    c->o_tok.ensure((size_t)R * 4);
-    c->o_conf.ensure((size_t)R * 4);
-    c->o_logp.ensure((size_t)R * 4);
-    c->o_breach.ensure((size_t)R);
-    c->o_unch.ensure((size_t)R);
-    c->o_bin.ensure((size_t)R * 4);
-    c->o_hist.ensure(64 * 8);
-    c->o_nbr.ensure(8);
-    c->o_sum.ensure(8);
-    c->o_htok.ensure((size_t)R * d.n_exits * 4);
-    c->o_hconf.ensure((size_t)R * d.n_exits * 4);
-    c->o_hlogp.ensure((size_t)R * d.n_exits * 4);
+    moved |= c->rows.ensure((size_t)(32 + 12 * R) * 4);
+    moved |= c->head_tok.ensure((size_t)R * 4);
+    moved |= c->head_tri.ensure((size_t)R * ((m.v_l + 127) / 128) * m.tp * 16);
+    if (m.tp > 1) moved |= c->tp_partial.ensure((size_t)R * D * 4);
+    moved |= c->head_conf.ensure((size_t)R * 4);
+    moved |= c->head_logp.ensure((size_t)R * 4);
+    moved |= c->o_exit.ensure((size_t)R * 4);
+    moved |= c->o_tok.ensure((size_t)R * 4);
+    moved |= c->o_conf.ensure((size_t)R * 4);
+    moved |= c->o_logp.ensure((size_t)R * 4);
+    moved |= c->o_breach.ensure((size_t)R);
+    moved |= c->o_unch.ensure((size_t)R);
+    moved |= c->o_bin.ensure((size_t)R * 4);
+    moved |= c->o_hist.ensure(64 * 8);
+    moved |= c->o_nbr.ensure(8);
+    moved |= c->o_sum.ensure(8);
+    moved |= c->o_htok.ensure((size_t)R * d.n_exits * 4);
+    moved |= c->o_hconf.ensure((size_t)R * d.n_exits * 4);
+    moved |= c->o_hlogp.ensure((size_t)R * d.n_exits * 4);
     const size_t pin_need = (size_t)R * (3 * 4 + 6 * 4 + 2 + 3 * 64 * 4) + 1024;
     if (pin_need > c->pin_bytes) {
         if (c->pin) cudaFreeHost(c->pin);
@@ -702,6 +737,7 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
         EEB_CUDA(cudaMallocHost(&c->pin, pin_need));
         c->pin_bytes = pin_need;
     }
+    if (moved) drop_graphs(c);
 }
 
 StepOutDev out_dev(eeb_ctx* c) {
@@ -754,6 +790,9 @@ struct Timer {
 };
 
 void count(eeb_ctx* c, int cat, int n) {
+    if (g_stamp)  // label this call's launches in the timeline
+        for (int i = (int)g_stamp->cats.size() - 1, k = 0; i >= 0 && k < n && g_stamp->cats[i] < 0; --i, ++k)
+            g_stamp->cats[i] = cat;
     c->cat_launches[cat] += n;
     c->step_launches += n;
 }
@@ -1290,296 +1329,15 @@ void check_step_args(eeb_ctx* c, Model& m, int depth, int policy, float th, int 
     (void)c;
 }
 
-// ---------------------------------------------------------------------------
-// Persistent step kernel: applicability, program compilation, launch.
-// ---------------------------------------------------------------------------
-bool mk_applicable(eeb_ctx* c, const Model& m, int batch) {
-    if (c->mk_mode < 0) {
-        // Opt-in until the persistent kernel's SIMT phases beat the per-op chain
-        // (profiles/r1: 2.9 ms vs 2.2 ms per C2 step); tier 3 forces it.
-        const char* env = std::getenv("EEB_MK");
-        c->mk_mode = env && env[0] == '1' ? 1 : 0;
-    }
-    const eeb_model_desc& d = m.desc;
-    const bool ok = !c->retain_logits && !m.paged && m.tp == 1 && d.dtype == EEB_BF16 && m.head_dim == 64 && d.n_heads / d.n_kv_heads <= 8 &&
-                    d.d_model <= 6 * 3 * 128 &&
-                    batch <= mk::kMaxRows && d.max_seq_len <= 256 && gemm_tc_available();
-    if (c->gemm_tier == 3) {
-        if (!ok) throw Error(EEB_E_DOMAIN, "persistent step kernel requested but not applicable to this model/batch");
-        return true;
-    }
-    return ok && c->gemm_tier == 0 && c->mk_mode == 1;
-}
-
-std::unique_ptr<MkProg> mk_build(eeb_ctx* c, Model& m, int depth, int policy, float th, int batch) {
-    const eeb_model_desc& d = m.desc;
-    const int L = d.num_layers, D = d.d_model, F = d.d_ffn, G = c->num_sms;
-    const int bpad = std::max(16, (batch + 15) / 16 * 16);
-    auto P = std::make_unique<MkProg>();
-    std::vector<CUtensorMap> maps;
-    auto add_map = [&](const void* ptr, int rows, int cols, int box) {
-        maps.emplace_back();
-        make_bf16_map(&maps.back(), ptr, rows, cols, box);
-        return (int)maps.size() - 1;
-    };
-    const int m_h = add_map(c->hn.p, batch, D, bpad);
-    const int m_attn = add_map(c->attn.p, batch, m.dq, bpad);
-    const int m_hmid = add_map(c->mlp_h.p, batch, F, bpad);
-    const int m_hh = add_map(c->hhead.p, batch, D, bpad);
-
-    std::vector<int> heads;
-    int run_layers = L;
-    if (policy == EEB_FLAT) {
-        int e_used = -1;
-        for (int e = 0; e < d.n_exits; ++e)
-            if (m.exits[e] <= depth) e_used = e;
-        heads.push_back(e_used);
-        run_layers = depth;
-    } else if (policy == EEB_FULL_DEPTH) {
-        heads.push_back(d.n_exits - 1);
-    } else {
-        for (int e = 0; e < d.n_exits; ++e) heads.push_back(e);
-    }
-
-    std::vector<mk::Phase> ph;
-    std::vector<int4> seg;
-    std::map<std::pair<int, int>, int> seg_of_shape;  // the table depends only on (N, K) and the grid
-    auto simt = [&](int kind, int layer, int src) {
-        mk::Phase x{};
-        x.kind = kind;
-        x.layer = layer;
-        x.src = src;
-        ph.push_back(x);
-        return (int)ph.size() - 1;
-    };
-    auto gemm = [&](int wmap, int xmap, int N, int K) {
-        mk::Phase x{};
-        x.kind = mk::kPhaseGemm;
-        x.src = -1;
-        x.wmap = wmap;
-        x.xmap = xmap;
-        x.N = N;
-        x.K = K;
-        x.kb = K / mk::kBK;
-        x.tiles = (N + mk::kBM - 1) / mk::kBM;
-        x.total = x.kb * x.tiles;
-        const int Gp = std::min(G, x.total);  // CTAs with work in this phase (mirrors cta_range)
-        auto s_of = [&](int cc) { return cc >= Gp ? x.total : (int)(((long long)x.total * cc) / Gp); };
-        int max_tiles = 0;
-        for (int cc = 0; cc < Gp; ++cc) {
-            const int s0 = s_of(cc), e0 = s_of(cc + 1);
-            if (e0 > s0) max_tiles = std::max(max_tiles, (e0 - 1) / x.kb - s0 / x.kb + 1);
-        }
-        if (max_tiles > mk::kMaxSeg) throw Error(EEB_E_DOMAIN, "persistent kernel: too many segments per CTA");
-        const auto shape = std::make_pair(N, K);
-        auto known = seg_of_shape.find(shape);
-        if (known != seg_of_shape.end()) {
-            x.pad[0] = known->second;
-            P->n_gemm++;
-            P->weight_bytes += (int64_t)N * K * 2;
-            ph.push_back(x);
-            return (int)ph.size() - 1;
-        }
-        x.pad[0] = (int)seg.size();
-        seg_of_shape[shape] = x.pad[0];
-        for (int t = 0; t < x.tiles; ++t) {
-            const int k0 = t * x.kb, k1 = k0 + x.kb;
-            int c0 = 0;
-            while (c0 + 1 < Gp && s_of(c0 + 1) <= k0) ++c0;
-            int n = 0;
-            for (int cc = c0; cc < Gp && s_of(cc) < k1; ++cc) ++n;
-            seg.push_back(make_int4(c0, t - s_of(c0) / x.kb, n, 0));
-        }
-        P->n_gemm++;
-        P->weight_bytes += (int64_t)N * K * 2;
-        ph.push_back(x);
-        return (int)ph.size() - 1;
-    };
-    auto norm = [&](int layer, int src, int gain, int flags) {
-        const int i = simt(mk::kPhaseNorm, layer, src);
-        ph[i].gain = gain;
-        ph[i].flags = flags;
-        return i;
-    };
-    norm(1, -1, 0, mk::kFlagEmbed);
-    size_t hi = 0;
-    int down = -1;
-    bool x_current = true;  // x already holds the residual (embedding or a head's norm reduced it)
-    for (int l = 1; l <= run_layers; ++l) {
-        const LayerWeights& W = *m.layers[l - 1];
-        if (l > 1) norm(l, x_current ? -1 : down, l - 1, 0);
-        const int qkv = gemm(add_map(W.wqkv.p, m.dq + 2 * m.dkv, D, mk::kBM), m_h, m.dq + 2 * m.dkv, D);
-        simt(mk::kPhaseAttn, l, qkv);
-        const int o = gemm(add_map(W.wo.p, D, m.dq, mk::kBM), m_attn, D, m.dq);
-        norm(l, o, L + l - 1, 0);
-        const int up = gemm(add_map(W.wup.p, m.up_rows, D, mk::kBM), m_h, m.up_rows, D);
-        simt(mk::kPhaseAct, l, up);
-        down = gemm(add_map(W.wdown.p, D, F, mk::kBM), m_hmid, D, F);
-        x_current = false;
-        bool normed = false;
-        while (hi < heads.size() && m.exits[heads[hi]] == l) {
-            const int e = heads[hi];
-            if (!normed) norm(l, down, 2 * L + e, mk::kFlagOutHead);
-            normed = true;
-            x_current = true;
-            const int hg = gemm(add_map(m.head[e]->p, d.vocab, D, mk::kBM), m_hh, d.vocab, D);
-            const int hr = simt(mk::kPhaseHeadReduce, l, hg);
-            ph[hr].exit_index = e;
-            const int dc = simt(mk::kPhaseDecide, l, hg);
-            ph[dc].exit_index = e;
-            ph[dc].exit_layer = m.exits[e];
-            ph[dc].flags = hi + 1 == heads.size() ? mk::kFlagFinal : 0;
-            ++hi;
-        }
-    }
-    simt(mk::kPhaseFinalize, run_layers, -1);
-
-    P->maps.ensure(maps.size() * sizeof(CUtensorMap));
-    EEB_CUDA(cudaMemcpy(P->maps.p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-    P->phases.ensure(ph.size() * sizeof(mk::Phase));
-    EEB_CUDA(cudaMemcpy(P->phases.p, ph.data(), ph.size() * sizeof(mk::Phase), cudaMemcpyHostToDevice));
-    P->segtab.ensure(seg.size() * sizeof(int4));
-    EEB_CUDA(cudaMemcpy(P->segtab.p, seg.data(), seg.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    std::vector<const float*> gains;
-    for (int l = 0; l < L; ++l) gains.push_back(l < (int)m.layers.size() ? m.layers[l]->attn_norm.as<float>() : nullptr);
-    for (int l = 0; l < L; ++l) gains.push_back(l < (int)m.layers.size() ? m.layers[l]->mlp_norm.as<float>() : nullptr);
-    for (int e = 0; e < d.n_exits; ++e) gains.push_back(m.head_norm[e]->as<float>());
-    P->gains.ensure(gains.size() * sizeof(float*));
-    EEB_CUDA(cudaMemcpy(P->gains.p, gains.data(), gains.size() * sizeof(float*), cudaMemcpyHostToDevice));
-
-    // shared workspace of the context
-    c->mk_partials.ensure((size_t)G * mk::kMaxSeg * bpad * mk::kBM * 4);
-    c->mk_stats.ensure((size_t)bpad * 16 * ((d.vocab + 128 * mk::kHeadChunk - 1) / (128 * mk::kHeadChunk)));
-    if (!c->mk_bar.p) {
-        c->mk_bar.ensure(64);
-        EEB_CUDA(cudaMemset(c->mk_bar.p, 0, 64));
-    }
-
-    mk::Params& q = P->P;
-    q.phases = P->phases.as<mk::Phase>();
-    q.n_phases = (int)ph.size();
-    q.maps = P->maps.as<CUtensorMap>();
-    q.partials = c->mk_partials.as<float>();
-    q.bar = c->mk_bar.as<unsigned>();
-    q.batch = batch;
-    q.bpad = bpad;
-    q.x_stages = 4;
-    // the X ring doubles as the SIMT phases' scratch (attention K/V rings: 6 warps x ~19 KB)
-    while ((size_t)q.x_stages * bpad * mk::kBK * 2 < (size_t)mk::kSimtWarps * mk::kAttnScratchBytes) ++q.x_stages;
-    if (const char* v = std::getenv("EEB_MK_XSTAGES")) q.x_stages = std::max(q.x_stages, std::atoi(v));
-    int ws = 2;
-    q.n_segtab = (int)seg.size();
-    while (mk::smem_bytes(bpad, ws + 1, q.x_stages, q.n_phases, q.n_segtab) <= 227u * 1024u) ++ws;
-    if (ws < 3) throw Error(EEB_E_DOMAIN, "persistent kernel: program too large for shared memory");
-    q.w_stages = ws;
-    if (const char* v = std::getenv("EEB_MK_WSTAGES")) q.w_stages = std::min(q.w_stages, std::max(2, std::atoi(v)));
-    q.bar_mode = 0;
-    q.dbg = std::getenv("EEB_MK_DBG") ? std::atoi(std::getenv("EEB_MK_DBG")) : 0;  // timing experiments only
-    q.l2_ahead = std::getenv("EEB_MK_L2") ? std::atoi(std::getenv("EEB_MK_L2")) : 0;
-    q.D = D;
-    q.F = F;
-    q.dq = m.dq;
-    q.dkv = m.dkv;
-    q.H = d.n_heads;
-    q.Hkv = d.n_kv_heads;
-    q.hd = m.head_dim;
-    q.V = d.vocab;
-    q.S = d.max_seq_len;
-    q.L = L;
-    q.n_exits = d.n_exits;
-    q.mlp_kind = d.mlp_kind;
-    q.policy = policy;
-    q.serving_depth = depth;
-    q.eps = d.norm_eps;
-    q.th = th;
-    q.emb = static_cast<const __nv_bfloat16*>(m.emb.p);
-    q.gains = P->gains.as<const float*>();
-    q.k_cache = static_cast<__nv_bfloat16*>(m.k_cache.p);
-    q.v_cache = static_cast<__nv_bfloat16*>(m.v_cache.p);
-    q.kv_layer_elems = (long long)m.kv_layer_elems;
-    q.kv_depth = m.kv_depth.as<uint8_t>();
-    q.rope_cos = m.rope_cos.as<float>();
-    q.rope_sin = m.rope_sin.as<float>();
-    Ints I = ints_of(c);
-    q.tok = I.tok;
-    q.slot = I.slot;
-    q.pos = I.pos;
-    q.x = c->xA.as<float>();
-    q.h = static_cast<__nv_bfloat16*>(c->hn.p);
-    q.hh = static_cast<__nv_bfloat16*>(c->hhead.p);
-    q.attn = static_cast<__nv_bfloat16*>(c->attn.p);
-    q.hmid = static_cast<__nv_bfloat16*>(c->mlp_h.p);
-    q.stats = c->mk_stats.as<float4>();
-    q.out = out_dev(c);
-    for (int k = 0; k < 64; ++k) q.exit_layers[k] = k < d.n_exits ? m.exits[k] : 0;
-    return P;
-}
-
-void run_step_mk(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
-    Model& m = model_of(c, mi);
-    uint32_t thb;
-    std::memcpy(&thb, &th, 4);
-    GraphKey key{mi, policy == EEB_FLAT ? depth : 0, policy, batch, 100 + m.loaded, thb};
-    auto it = c->mk_progs.find(key);
-    if (it == c->mk_progs.end()) it = c->mk_progs.emplace(key, mk_build(c, m, depth, policy, th, batch)).first;
-    MkProg& P = *it->second;
-    P.P.bar_base = c->mk_bar_count;
-    c->mk_bar_count += (unsigned long long)(P.P.n_phases - 1) * c->num_sms;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (c->profiling) {
-        EEB_CUDA(cudaEventCreate(&e0));
-        EEB_CUDA(cudaEventCreate(&e1));
-        EEB_CUDA(cudaEventRecord(e0, c->stream));
-    }
-    static const char* trace_path = std::getenv("EEB_MK_TRACE");
-    DevBuf trace;
-    if (trace_path) {  // diagnostics: per-phase timestamps of this step -> file (synchronous)
-        trace.ensure((size_t)c->num_sms * P.P.n_phases * 8 * 8);
-        EEB_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes, c->stream));
-        P.P.trace = trace.as<unsigned long long>();
-    }
-    mk::launch(P.P, P.segtab.as<int4>(), c->num_sms, c->stream);
-    if (trace_path) {
-        P.P.trace = nullptr;
-        EEB_CUDA(cudaStreamSynchronize(c->stream));
-        std::vector<unsigned long long> h(trace.bytes / 8);
-        EEB_CUDA(cudaMemcpy(h.data(), trace.p, trace.bytes, cudaMemcpyDeviceToHost));
-        std::vector<mk::Phase> ph(P.P.n_phases);
-        EEB_CUDA(cudaMemcpy(ph.data(), P.phases.p, ph.size() * sizeof(mk::Phase), cudaMemcpyDeviceToHost));
-        if (FILE* f = std::fopen(trace_path, "wb")) {
-            std::fwrite(h.data(), 8, h.size(), f);
-            std::fclose(f);
-        }
-        if (FILE* f = std::fopen((std::string(trace_path) + ".kinds").c_str(), "w")) {
-            for (auto& x : ph) std::fprintf(f, "%d\n", x.kind);
-            std::fclose(f);
-        }
-    }
-    if (c->profiling) {
-        EEB_CUDA(cudaEventRecord(e1, c->stream));
-        EEB_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        EEB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        c->mk_ms += ms;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    }
-    c->step_launches = 1;
-    c->last_step_mk = 1;
-    c->last_step_weight_bytes = P.weight_bytes;
-}
-
 void run_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
     Model& m = model_of(c, mi);
-    if (mk_applicable(c, m, batch)) {
-        run_step_mk(c, mi, depth, policy, th, batch);
-        return;
-    }
-    c->last_step_mk = 0;
+    if (c->stamp_cap > 0) stamp_reset(c);
     const bool use_graph = c->graphs_enabled && !c->profiling && !c->retain_logits;
     if (!use_graph) {
         c->step_launches = 0;
+        StampSession ss(c);
         enqueue_step(c, mi, depth, policy, th, batch);
+        if (ss.on) c->stamp_last = {ss.st.kernels, ss.st.cats};
         return;
     }
     uint32_t thb;
@@ -1592,7 +1350,9 @@ void run_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
         EEB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         c->capturing = true;
         try {
+            StampSession ss(c);
             enqueue_step(c, mi, depth, policy, th, batch);
+            if (ss.on) c->stamp_kernels[key] = {ss.st.kernels, ss.st.cats};
         } catch (...) {
             c->capturing = false;
             while (c->cond_open > 0) {
@@ -1612,6 +1372,7 @@ void run_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch) {
         it = c->graphs.emplace(key, ex).first;
     }
     (void)m;
+    if (c->stamp_cap > 0) c->stamp_last = c->stamp_kernels[key];
     EEB_CUDA(cudaGraphLaunch(it->second, c->stream));
 }
 
@@ -1714,6 +1475,19 @@ void kv_sync_table(eeb_ctx* c, Model& m) {
 }
 
 }  // namespace
+
+Stamp stamp_next(const void* kernel) {
+    Stamp s;
+    StampState* g = g_stamp;
+    if (!g || (int)g->kernels.size() >= g->cap) return s;
+    s.buf = g->buf;
+    s.slot = (int)g->kernels.size();
+    s.end_off = (int64_t)g->cap * kStampCtas;
+    g->kernels.push_back(kernel);
+    g->cats.push_back(-1);
+    return s;
+}
+
 }  // namespace eeb
 
 using namespace eeb;
@@ -1832,14 +1606,7 @@ eeb_status eeb_load_layers(eeb_ctx* c, int model, int to_depth) {
     return guarded([&] {
         Model& m = model_of(c, model);
         EEB_CUDA(cudaSetDevice(c->device));
-        for (auto it = c->graphs.begin(); it != c->graphs.end();) {
-            if (it->first.model == model) {
-                cudaGraphExecDestroy(it->second);
-                it = c->graphs.erase(it);
-            } else {
-                ++it;
-            }
-        }
+        drop_graphs(c, model);
         load_to(c, m, to_depth);
     });
 }
@@ -1858,14 +1625,7 @@ eeb_status eeb_load_layers_async(eeb_ctx* c, int model, int to_depth) {
     return guarded([&] {
         Model& m = model_of(c, model);
         EEB_CUDA(cudaSetDevice(c->device));
-        for (auto it = c->graphs.begin(); it != c->graphs.end();) {
-            if (it->first.model == model) {
-                cudaGraphExecDestroy(it->second);
-                it = c->graphs.erase(it);
-            } else {
-                ++it;
-            }
-        }
+        drop_graphs(c, model);
         load_async(c, m, to_depth);
     });
 }
@@ -2142,10 +1902,67 @@ eeb_status eeb_set_graphs(eeb_ctx* c, int enable) {
     });
 }
 
+eeb_status eeb_debug_stamps(eeb_ctx* c, int max_launches) {
+    return guarded([&] {
+        if (!c || max_launches < 0 || max_launches > 4096) throw Error(EEB_E_DOMAIN, "bad argument");
+        EEB_CUDA(cudaSetDevice(c->device));
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        drop_graphs(c);  // stamped and plain graphs differ in their kernel arguments
+        c->stamp_kernels.clear();
+        c->stamp_last = {};
+        c->stamp_cap = max_launches;
+        if (max_launches > 0) {
+            c->stamp_buf.release();
+            c->stamp_buf.ensure((size_t)max_launches * kStampCtas * 2 * 8);
+        } else {
+            c->stamp_buf.release();
+        }
+    });
+}
+
+eeb_status eeb_debug_stamps_read(eeb_ctx* c, char* json_out, int64_t cap) {
+    return guarded([&] {
+        if (!c || !json_out) throw Error(EEB_E_DOMAIN, "null argument");
+        if (c->stamp_cap <= 0) throw Error(EEB_E_DOMAIN, "stamping is off (eeb_debug_stamps)");
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        const size_t cells = (size_t)c->stamp_cap * kStampCtas;
+        std::vector<unsigned long long> h(2 * cells);
+        EEB_CUDA(cudaMemcpy(h.data(), c->stamp_buf.p, h.size() * 8, cudaMemcpyDeviceToHost));
+        std::string j = "{\"launches\": [";
+        unsigned long long t0 = ~0ull;
+        for (size_t i = 0; i < c->stamp_last.first.size(); ++i)
+            for (int k = 0; k < kStampCtas; ++k) t0 = std::min(t0, h[i * kStampCtas + k]);
+        for (size_t i = 0; i < c->stamp_last.first.size(); ++i) {
+            unsigned long long st = ~0ull, en = 0;
+            int ctas = 0;
+            for (int k = 0; k < kStampCtas; ++k) {
+                const unsigned long long a = h[i * kStampCtas + k], b = h[cells + i * kStampCtas + k];
+                if (a != ~0ull) {
+                    ++ctas;
+                    st = std::min(st, a);
+                }
+                en = std::max(en, b);
+            }
+            const char* name = nullptr;
+            if (cudaFuncGetName(&name, c->stamp_last.first[i]) != cudaSuccess || !name) name = "?";
+            const int cat = c->stamp_last.second[i];
+            char buf[512];
+            std::snprintf(buf, sizeof buf,
+                          "%s{\"kernel\": \"%s\", \"cat\": \"%s\", \"start_ns\": %lld, \"end_ns\": %lld, \"ctas\": %d}",
+                          i ? ", " : "", name, cat >= 0 ? kCatNames[cat] : "?", ctas ? (long long)(st - t0) : -1LL,
+                          ctas ? (long long)(en - t0) : -1LL, ctas);
+            j += buf;
+        }
+        j += "]}";
+        if ((int64_t)j.size() + 1 > cap) throw Error(EEB_E_DOMAIN, "buffer too small");
+        std::memcpy(json_out, j.c_str(), j.size() + 1);
+    });
+}
+
 eeb_status eeb_set_gemm_tier(eeb_ctx* c, int tier) {
     return guarded([&] {
         if (!c) throw Error(EEB_E_DOMAIN, "null context");
-        if (tier < 0 || tier > 3) throw Error(EEB_E_DOMAIN, "tier must be 0, 1, 2 or 3");
+        if (tier < 0 || tier > 2) throw Error(EEB_E_DOMAIN, "tier must be 0, 1 or 2");
         c->gemm_tier = tier;
     });
 }
@@ -2154,8 +1971,7 @@ eeb_status eeb_debug_retain_logits(eeb_ctx* c, int enable) {
     return guarded([&] {
         if (!c) throw Error(EEB_E_DOMAIN, "null context");
         c->retain_logits = enable ? 1 : 0;
-        for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
-        c->graphs.clear();
+        drop_graphs(c);
     });
 }
 
@@ -2229,6 +2045,7 @@ eeb_status eeb_kv_configure_pages(eeb_ctx* c, int model, int32_t page_size, int3
             throw Error(EEB_E_DOMAIN, "the paged KV pool needs a bf16 model with head_dim 64 or 128");
         EEB_CUDA(cudaSetDevice(c->device));
         EEB_CUDA(cudaStreamSynchronize(c->stream));
+        drop_graphs(c, model);  // captured steps hold the old KV maps and the unpaged kernel
         alloc_kv(c, m, page_size, n_pages, true);
         EEB_CUDA(cudaMemsetAsync(m.kv_depth.p, 0, m.kv_depth.bytes, c->stream));
         kv_sync_table(c, m);
@@ -2365,67 +2182,6 @@ eeb_status eeb_debug_gemm(eeb_ctx* c, int tier, int dtype, int n, int k, int bat
     });
 }
 
-eeb_status eeb_debug_bench_layers(eeb_ctx* c, int model, int batch, int iters, double* ms_out) {
-    return guarded([&] {
-        Model& m = model_of(c, model);
-        const eeb_model_desc& d = m.desc;
-        if (!ms_out || batch < 1 || batch > mk::kMaxRows || iters <= 0) throw Error(EEB_E_DOMAIN, "bad argument");
-        if (d.dtype != EEB_BF16) throw Error(EEB_E_DOMAIN, "persistent step kernel: bf16 models only");
-        if (m.loaded < 1) throw Error(EEB_E_CAPACITY, "no layers resident");
-        EEB_CUDA(cudaSetDevice(c->device));
-        ensure_workspace(c, m, batch);
-        // The FULL_DEPTH program minus every non-GEMM phase: the weight stream alone.
-        std::unique_ptr<MkProg> P = mk_build(c, m, 0, EEB_FULL_DEPTH, 0.5f, batch);
-        std::vector<mk::Phase> ph(P->P.n_phases);
-        EEB_CUDA(cudaMemcpy(ph.data(), P->phases.p, ph.size() * sizeof(mk::Phase), cudaMemcpyDeviceToHost));
-        std::vector<mk::Phase> g;
-        for (auto& x : ph)
-            if (x.kind == mk::kPhaseGemm && x.N != d.vocab) g.push_back(x);
-        EEB_CUDA(cudaMemcpy(P->phases.p, g.data(), g.size() * sizeof(mk::Phase), cudaMemcpyHostToDevice));
-        mk::Params& q = P->P;
-        q.n_phases = (int)g.size();
-        int ws = 2;
-        while (mk::smem_bytes(q.bpad, ws + 1, q.x_stages, q.n_phases, q.n_segtab) <= 227u * 1024u) ++ws;
-        q.w_stages = ws;
-        if (const char* v = std::getenv("EEB_MK_WSTAGES")) q.w_stages = std::min(ws, std::max(2, std::atoi(v)));
-        q.bar_mode = std::getenv("EEB_MK_BAR") ? std::atoi(std::getenv("EEB_MK_BAR")) : 0;
-        q.dbg = std::getenv("EEB_MK_DBG") ? std::atoi(std::getenv("EEB_MK_DBG")) : 0;
-        DevBuf trace;
-        const char* trace_path = std::getenv("EEB_MK_TRACE");
-        if (trace_path) {
-            trace.ensure((size_t)c->num_sms * g.size() * 8 * 8);
-            q.trace = trace.as<unsigned long long>();
-        }
-        auto launch_once = [&] {
-            q.bar_base = c->mk_bar_count;
-            c->mk_bar_count += (unsigned long long)(q.n_phases - 1) * c->num_sms;
-            mk::launch(q, P->segtab.as<int4>(), c->num_sms, c->stream);
-        };
-        for (int i = 0; i < 2; ++i) launch_once();
-        EEB_CUDA(cudaStreamSynchronize(c->stream));
-        cudaEvent_t e0, e1;
-        EEB_CUDA(cudaEventCreate(&e0));
-        EEB_CUDA(cudaEventCreate(&e1));
-        EEB_CUDA(cudaEventRecord(e0, c->stream));
-        for (int i = 0; i < iters; ++i) launch_once();
-        EEB_CUDA(cudaEventRecord(e1, c->stream));
-        EEB_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        EEB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        *ms_out = ms / iters;
-        if (trace_path) {
-            std::vector<unsigned long long> h(trace.bytes / 8);
-            EEB_CUDA(cudaMemcpy(h.data(), trace.p, trace.bytes, cudaMemcpyDeviceToHost));
-            if (FILE* f = std::fopen(trace_path, "wb")) {
-                std::fwrite(h.data(), 8, h.size(), f);
-                std::fclose(f);
-            }
-        }
-    });
-}
-
 eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, int iters, double* ms_out) {
     return guarded([&] {
         if (!c || !ms_out || n <= 0 || k <= 0 || batch <= 0 || iters <= 0) throw Error(EEB_E_DOMAIN, "bad argument");
@@ -2507,7 +2263,6 @@ eeb_status eeb_profile_enable(eeb_ctx* c, int enable) {
     return guarded([&] {
         if (!c) throw Error(EEB_E_DOMAIN, "null context");
         c->profiling = enable ? 1 : 0;
-        c->mk_ms = 0;
         for (int k = 0; k < kNumCat; ++k) { c->cat_ms[k] = 0; c->cat_launches[k] = 0; }
         c->steps_profiled = 0;
     });
@@ -2517,9 +2272,7 @@ eeb_status eeb_profile_read(eeb_ctx* c, char* json_out, int64_t cap) {
     return guarded([&] {
         if (!c || !json_out) throw Error(EEB_E_DOMAIN, "null argument");
         std::string j = "{\"steps\": " + std::to_string(c->steps_profiled) + ", \"last_step_launches\": " +
-                        std::to_string(c->step_launches) + ", \"persistent\": " + std::to_string(c->last_step_mk) +
-                        ", \"persistent_ms\": " + std::to_string(c->mk_ms) + ", \"weight_bytes\": " +
-                        std::to_string(c->last_step_weight_bytes);
+                        std::to_string(c->step_launches);
         for (int k = 0; k < kNumCat; ++k) {
             char buf[160];
             std::snprintf(buf, sizeof buf, ", \"%s_ms\": %.6f, \"%s_launches\": %lld", kCatNames[k], c->cat_ms[k],

@@ -26,8 +26,9 @@ constexpr int kReduceThreads = 1024;
 
 // Per-row max / argmax / sum-exp over the vocabulary.
 __global__ void __launch_bounds__(kReduceThreads)
-    head_reduce_kernel(const float* part, int splits, int64_t split_stride, int vocab,
+    head_reduce_kernel(Stamp stamp, const float* part, int splits, int64_t split_stride, int vocab,
                        const int* n_active, HeadOut h, float* logits_out) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x;
@@ -101,7 +102,8 @@ __device__ __forceinline__ void write_row(const StepOutDev& o, int r, int exit_l
 // over the grid (one SM's L2 bandwidth would bound a single-CTA merge); the
 // last CTA to finish (ticket) then decides for every row.
 constexpr int kDecideThreads = 256;
-__global__ void __launch_bounds__(kDecideThreads) decide_kernel(DecideArgs a) {
+__global__ void __launch_bounds__(kDecideThreads) decide_kernel(Stamp stamp, DecideArgs a) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     __shared__ int warp_counts[32];
@@ -254,9 +256,10 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(DecideArgs a) {
 // K4 + bookkeeping: shared-memory atomic histogram of exit-head bins, breach
 // count, fixed-order f64 logprob sum, KV depth map update.
 __global__ void __launch_bounds__(1024)
-    finalize_kernel(int batch, int n_exits, StepOutDev o, const int* slot_in,
+    finalize_kernel(Stamp stamp, int batch, int n_exits, StepOutDev o, const int* slot_in,
                     const int* pos_in, uint8_t* kv_depth, int max_seq,
                     int computed_depth) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     __shared__ unsigned long long hist_s[64];

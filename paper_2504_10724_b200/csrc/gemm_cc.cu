@@ -19,8 +19,9 @@ constexpr int kRowsPerCta = kWarps * kRowsPerWarp;
 
 template <typename T, int MAXB>
 __global__ void __launch_bounds__(kWarps * 32)
-    gemm_cc_kernel(const T* __restrict__ W, const T* X, const int* n_active,
+    gemm_cc_kernel(Stamp stamp, const T* __restrict__ W, const T* X, const int* n_active,
                    float* part, int N, int K, int KS, int64_t split_stride) {
+    StampScope stamp_scope(stamp);
     constexpr int VEC = Vec16<T>::N;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* xs = reinterpret_cast<T*>(smem_raw);  // [MAXB][KS]

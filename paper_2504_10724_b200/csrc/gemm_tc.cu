@@ -165,6 +165,7 @@ struct TcParams {
     unsigned long long* trace;  // timing experiments: 8 globaltimer stamps per CTA (null = off)
     int dbg;                    // timing experiments: bit 0 = no plane stores (results wrong)
     int skip_dead;              // read n_active before the weight prefetch (skip it when 0)
+    Stamp st;                   // in-graph launch timeline (eeb_debug_stamps)
 };
 
 // Timeline stamps are compiled in only for the timing experiments
@@ -188,6 +189,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                    TcParams p) {
+    StampScope stamp_scope(p.st);
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms.
     const uint32_t raw = smem_u32(smem_raw);
@@ -739,6 +741,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     static const bool force_cl = std::getenv("EEB_TC_CLUSTER_ATTR") != nullptr;
     cfg.numAttrs = cs > 1 || force_cl ? 2 : 1;  // no cluster attribute unless clustering (launch cost)
+    p.st = stamp_next(reinterpret_cast<const void*>(gemm_tc_kernel));
     EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p));
     return splits / cs;
 }

@@ -63,10 +63,11 @@ __device__ __forceinline__ void add4(float4& a, const float4 b) {
 
 template <typename T, int kV>
 __global__ void __launch_bounds__(kNormThreads)
-    residual_norm_kernel(const float* part, int splits, int64_t split_stride,
+    residual_norm_kernel(Stamp stamp, const float* part, int splits, int64_t split_stride,
                          const int* n_active, float* x, int d, float eps,
                          const float* g1, T* out1, const float* g2,
                          T* out2) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x;
@@ -122,8 +123,9 @@ __global__ void __launch_bounds__(kNormThreads)
 }
 
 template <typename T>
-__global__ void act_kernel(const float* part, int splits, int64_t split_stride,
+__global__ void act_kernel(Stamp stamp, const float* part, int splits, int64_t split_stride,
                            const int* n_active, int N, int swiglu, T* out) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int n_out = swiglu ? N / 2 : N;
@@ -147,8 +149,9 @@ __global__ void act_kernel(const float* part, int splits, int64_t split_stride,
     }
 }
 
-__global__ void plane_sum_kernel(const float* part, int splits, int64_t split_stride, const int* n_active, int d,
+__global__ void plane_sum_kernel(Stamp stamp, const float* part, int splits, int64_t split_stride, const int* n_active, int d,
                                  float* out) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int64_t total = (int64_t)(*n_active) * d;
@@ -161,9 +164,10 @@ __global__ void plane_sum_kernel(const float* part, int splits, int64_t split_st
 }
 
 template <typename T>
-__global__ void embed_kernel(const T* __restrict__ emb, const int* tok,
+__global__ void embed_kernel(Stamp stamp, const T* __restrict__ emb, const int* tok,
                              const int* slot_in, const int* pos_in, int batch, int d,
                              RowState st) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int i = blockIdx.x;
@@ -179,9 +183,10 @@ __global__ void embed_kernel(const T* __restrict__ emb, const int* tok,
     for (int c = threadIdx.x; c < d; c += blockDim.x) dst[c] = to_f32(src[c]);
 }
 
-__global__ void gather_rows_kernel(const float* x_cur, float* x_nxt,
+__global__ void gather_rows_kernel(Stamp stamp, const float* x_cur, float* x_nxt,
                                    const uint16_t* h_cur, uint16_t* h_nxt, int h_words,
                                    const int* src, const int* n_active, int d) {
+    StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     const int j = blockIdx.x;

@@ -65,9 +65,10 @@ EXPORTED = [
     "eeb_decode_step", "eeb_decode_step_device", "eeb_synchronize", "eeb_set_graphs",
     "eeb_set_gemm_tier", "eeb_debug_last_logits", "eeb_debug_retain_logits", "eeb_debug_read_weight",
     "eeb_debug_read_kv", "eeb_profile_enable", "eeb_profile_read", "eeb_stream",
-    "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm", "eeb_debug_bench_layers",
+    "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm",
     "eeb_prefill", "eeb_host_stage", "eeb_load_layers_async", "eeb_load_wait",
     "eeb_kv_configure_pages", "eeb_kv_reserve", "eeb_kv_release", "eeb_kv_pages",
+    "eeb_debug_stamps", "eeb_debug_stamps_read",
 ]
 
 _lib = None
@@ -113,7 +114,8 @@ def load_library() -> C.CDLL:
                                        C.c_void_p, C.c_void_p, C.c_void_p]
         lib.eeb_debug_bench_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.POINTER(C.c_double)]
-        lib.eeb_debug_bench_layers.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        lib.eeb_debug_stamps.argtypes = [C.c_void_p, C.c_int]
+        lib.eeb_debug_stamps_read.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         lib.eeb_profile_enable.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_profile_read.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         lib.eeb_nccl_unique_id.argtypes = [C.c_void_p]
@@ -416,11 +418,18 @@ class Context:
         _check(self.lib.eeb_debug_bench_gemm(self.h, tier, n, k, batch, iters, C.byref(ms)))
         return ms.value
 
-    def bench_layers(self, model: int, batch: int, iters: int = 20) -> float:
-        """ms per launch of the persistent kernel streaming all loaded layers' GEMMs."""
-        ms = C.c_double()
-        _check(self.lib.eeb_debug_bench_layers(self.h, model, batch, iters, C.byref(ms)))
-        return ms.value
+    def stamps(self, max_launches: int) -> None:
+        """In-graph launch timeline of every later decode step (0 = off)."""
+        _check(self.lib.eeb_debug_stamps(self.h, int(max_launches)))
+
+    def stamps_read(self) -> list[dict]:
+        """[{kernel, start_ns, end_ns, ctas}] of the last decode step, launch order."""
+        import json
+
+        n = 1 << 20
+        buf = C.create_string_buffer(n)
+        _check(self.lib.eeb_debug_stamps_read(self.h, buf, n))
+        return json.loads(buf.value.decode())["launches"]
 
     def profile_enable(self, on: bool) -> None:
         _check(self.lib.eeb_profile_enable(self.h, 1 if on else 0))

@@ -10,7 +10,8 @@ inside a step.  A volatile load (LDG.E.STRONG.SYS) is the one deliberate
 exception: the tcgen05 GEMM reads the live-row count before the wait only as
 a hint whether to prefetch weights (a stale value costs a useless or a missed
 prefetch; the count read after the wait decides what is computed) — plain
-(hoistable) loads stay forbidden.
+(hoistable) loads stay forbidden.  The launch-timeline stamp (REDG.E.MIN.64,
+common.cuh StampScope) writes only its own diagnostics buffer.
 """
 import re
 import subprocess
@@ -19,8 +20,8 @@ import pytest
 
 from paper_2504_10724_b200 import eeb
 
-ALLOWED_PRE_WAIT = ("UTMALDG", "LDG.E.STRONG.SYS")  # TMA weight prefetch; the volatile live-count hint
-NO_PDL_KERNELS = ("step_kernel", "synth")  # standalone launches (persistent step, weight synthesis)
+ALLOWED_PRE_WAIT = ("UTMALDG", "LDG.E.STRONG.SYS", "REDG.E.MIN.64")  # TMA weight prefetch; live-count hint; stamp
+NO_PDL_KERNELS = ("synth",)  # standalone launches (weight synthesis)
 
 
 def _functions(sass: str):
