@@ -226,6 +226,10 @@ eeb_status eeb_debug_read_weight(eeb_ctx* ctx, int model, int tensor, int layer,
                                  int64_t n, float* host_out);
 eeb_status eeb_debug_read_kv(eeb_ctx* ctx, int model, int layer, int slot, int pos, float* host_k,
                              float* host_v);
+/* K/V of positions [pos0, pos0 + n_pos) of one slot at one layer, as f32
+ * [n_pos][n_kv_heads * head_dim] (either output may be null). */
+eeb_status eeb_debug_read_kv_span(eeb_ctx* ctx, int model, int layer, int slot, int pos0, int n_pos,
+                                  float* host_k, float* host_v);
 
 /* Run one decode GEMM y[b][n] = sum_k x[b][k] * w[n][k] through a given tier
  * (1 CUDA cores, 2 tcgen05) with an epilogue mode (0 store f32, 1 residual add

@@ -549,3 +549,49 @@ int orc_read_kv(const orc_model* m, int layer, int slot, int pos, float* k, floa
         }
     return 0;
 }
+
+/* Test hook: import K/V for positions [pos0, pos0 + n) of one slot at one
+ * layer ([n][Hkv*hd] each, rounded to the model dtype) and raise those
+ * positions' KV depth to `layer`.  Used to start the oracle from the GPU's
+ * prefilled KV (tests/test_gpu_bench_parity.py) — the prefill itself is
+ * checked independently on its first positions. */
+int orc_write_kv(orc_model* m, int layer, int slot, int pos0, int n, const float* k, const float* v) {
+    const orc_desc* d = &m->d;
+    const int hd = m->hd, Hkv = d->n_kv_heads, S = d->max_seq_len;
+    if (layer < 1 || layer > d->num_layers || slot < 0 || slot >= d->max_slots || pos0 < 0 || pos0 + n > S)
+        return fail("kv coordinate out of range");
+    const size_t layer_off = (size_t)(layer - 1) * d->max_slots * Hkv * S * hd;
+    for (int q = 0; q < n; ++q) {
+        for (int g = 0; g < Hkv; ++g)
+            for (int j = 0; j < hd; ++j) {
+                const size_t o = layer_off + (((size_t)slot * Hkv + g) * S + pos0 + q) * hd + j;
+                const size_t i = (size_t)q * Hkv * hd + (size_t)g * hd + j;
+                m->kc[o] = rnd(m, k[i]);
+                m->vc[o] = rnd(m, v[i]);
+            }
+        uint8_t* dep = &m->kv_depth[(size_t)slot * S + pos0 + q];
+        if (*dep < layer) *dep = (uint8_t)layer;
+    }
+    return 0;
+}
+
+/* CPU-baseline hook: fill positions [0, n) of one slot at every layer with
+ * deterministic pseudo-random K/V in [-1, 1) (rounded to the dtype) computed
+ * to full depth — a prompt's KV without running the prompt, so a timed decode
+ * step attends over the same context length as the GPU workload. */
+int orc_fill_kv_synthetic(orc_model* m, int slot, int n, uint64_t seed) {
+    const orc_desc* d = &m->d;
+    const int hd = m->hd, Hkv = d->n_kv_heads, S = d->max_seq_len, L = d->num_layers;
+    if (slot < 0 || slot >= d->max_slots || n < 0 || n > S) return fail("kv coordinate out of range");
+    for (int l = 0; l < L; ++l)
+        for (int g = 0; g < Hkv; ++g)
+            for (int p = 0; p < n; ++p)
+                for (int j = 0; j < hd; ++j) {
+                    const size_t o = (((size_t)l * d->max_slots + slot) * Hkv + g) * S * hd + (size_t)p * hd + j;
+                    const uint64_t h = fin64(seed ^ (o * 0x9E3779B97F4A7C15ull));
+                    m->kc[o] = rnd(m, (float)((h >> 40) * (1.0 / 8388608.0) - 1.0));
+                    m->vc[o] = rnd(m, (float)(((h >> 16) & 0xFFFFFF) * (1.0 / 8388608.0) - 1.0));
+                }
+    for (int p = 0; p < n; ++p) m->kv_depth[(size_t)slot * S + p] = (uint8_t)L;
+    return 0;
+}

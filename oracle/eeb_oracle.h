@@ -84,6 +84,10 @@ int orc_decide(int policy, int n, const int32_t* layers, const int32_t* toks, co
                int depth, int num_layers, orc_decision* out);
 /* K/V of one position, [n_kv_heads][head_dim] each. */
 int orc_read_kv(const orc_model* m, int layer, int slot, int pos, float* k, float* v);
+/* Import K/V of positions [pos0, pos0+n) ([n][n_kv_heads*head_dim] each) at one layer. */
+int orc_write_kv(orc_model* m, int layer, int slot, int pos0, int n, const float* k, const float* v);
+/* Synthetic full-depth KV for positions [0, n) of a slot (CPU-baseline context). */
+int orc_fill_kv_synthetic(orc_model* m, int slot, int n, uint64_t seed);
 const char* orc_last_error(void);
 
 #ifdef __cplusplus

@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
         L.orc_decode_step.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_int, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.POINTER(_Out)]
         L.orc_read_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_write_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_fill_kv_synthetic.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64]
         L.orc_last_error.restype = C.c_char_p
         L.orc_decide.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_int,
                                  C.c_int, C.POINTER(_Decision)]
@@ -156,3 +158,15 @@ class OracleModel:
         v = np.zeros(n, np.float32)
         lib().orc_read_kv(self.h, layer, slot, pos, k.ctypes.data, v.ctypes.data)
         return k, v
+
+    def write_kv(self, layer: int, slot: int, pos0: int, k, v) -> None:
+        """Import K/V rows [n, Hkv*hd] at positions pos0.. of a slot (test hook)."""
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        if lib().orc_write_kv(self.h, layer, slot, pos0, len(k), k.ctypes.data, v.ctypes.data) != 0:
+            raise RuntimeError(lib().orc_last_error().decode())
+
+    def fill_kv_synthetic(self, slot: int, n: int, seed: int = 1) -> None:
+        """Synthetic full-depth KV for positions [0, n) of a slot (CPU-baseline context)."""
+        if lib().orc_fill_kv_synthetic(self.h, slot, n, seed) != 0:
+            raise RuntimeError(lib().orc_last_error().decode())

@@ -29,7 +29,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
     f"-I{ROOT / 'include'}",
 ]
-SOURCES = ["synth_kernels.cu", "rows.cu", "gemm_cc.cu", "gemm_tc.cu", "attention.cu",
+SOURCES = ["synth_kernels.cu", "rows.cu", "gemm_cc.cu", "gemm_tc.cu", "attention.cu", "attention_dec.cu",
            "exit_head.cu", "eeb_api.cu"]
 
 

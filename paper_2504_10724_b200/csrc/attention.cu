@@ -1431,6 +1431,7 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
         else launch_prefill_attn<128>(a, s);
         return;
     }
+    if (launch_attention_dec(a, s)) return;  // streaming decode kernel (attention_dec.cu)
     if (a.dtype == 1 && a.k_map && a.v_map && a.n_heads / a.n_kv_heads <= 8 &&
         (a.head_dim == 64 || a.head_dim == 128)) {
         if (paged) {  // only the one-item kernel walks page tables

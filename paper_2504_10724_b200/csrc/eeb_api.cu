@@ -2083,6 +2083,51 @@ eeb_status eeb_kv_pages(eeb_ctx* c, int model, int32_t* page_size, int32_t* n_pa
     });
 }
 
+eeb_status eeb_debug_read_kv_span(eeb_ctx* c, int model, int layer, int slot, int pos0, int n_pos, float* host_k,
+                                  float* host_v) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const eeb_model_desc& d = m.desc;
+        if (layer < 1 || layer > d.num_layers || slot < 0 || slot >= d.max_slots || pos0 < 0 || n_pos < 0 ||
+            pos0 + n_pos > d.max_seq_len)
+            throw Error(EEB_E_DOMAIN, "kv coordinate out of range");
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        const int hd = m.head_dim, heads = m.shards * m.hkv_l, row = heads * hd;
+        std::vector<char> tmp((size_t)m.kv_page * hd * m.wbytes);
+        for (int g = 0; g < heads; ++g) {
+            const int sh = g / m.hkv_l, lg = g % m.hkv_l;
+            for (int p = pos0; p < pos0 + n_pos;) {  // one copy per run of positions inside a page
+                const int in_page = p % m.kv_page, run = std::min(m.kv_page - in_page, pos0 + n_pos - p);
+                const int32_t pg = m.h_table[(size_t)slot * m.pages_per_seq + p / m.kv_page];
+                if (pg < 0) throw Error(EEB_E_DOMAIN, "kv position has no page (paged pool)");
+                const size_t off = (size_t)(layer - 1) * m.kv_layer_elems + (size_t)sh * m.kv_shard_elems +
+                                   (((size_t)pg * m.hkv_l + lg) * m.kv_page + in_page) * hd;
+                for (int which = 0; which < 2; ++which) {
+                    float* dst = which == 0 ? host_k : host_v;
+                    if (!dst) continue;
+                    const DevBuf& b = which == 0 ? m.k_cache : m.v_cache;
+                    EEB_CUDA(cudaMemcpy(tmp.data(), static_cast<const char*>(b.p) + off * m.wbytes,
+                                        (size_t)run * hd * m.wbytes, cudaMemcpyDeviceToHost));
+                    for (int q = 0; q < run; ++q)
+                        for (int j = 0; j < hd; ++j) {
+                            float* o = &dst[(size_t)(p - pos0 + q) * row + (size_t)g * hd + j];
+                            const size_t e = (size_t)q * hd + j;
+                            if (m.wbytes == 4) {
+                                std::memcpy(o, &tmp[e * 4], 4);
+                            } else {
+                                uint16_t h;
+                                std::memcpy(&h, &tmp[e * 2], 2);
+                                const uint32_t u = (uint32_t)h << 16;
+                                std::memcpy(o, &u, 4);
+                            }
+                        }
+                }
+                p += run;
+            }
+        }
+    });
+}
+
 eeb_status eeb_debug_read_kv(eeb_ctx* c, int model, int layer, int slot, int pos, float* host_k, float* host_v) {
     return guarded([&] {
         Model& m = model_of(c, model);

@@ -138,6 +138,9 @@ __host__ __device__ inline int64_t kv_elem_offset(const AttnArgs& a, int slot, i
     return (((int64_t)pg * a.n_kv_heads + g) * a.page_size + pos % a.page_size) * a.head_dim;
 }
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+// Streaming decode attention (attention_dec.cu): bf16, head_dim 64, decode
+// (not kv_ready), no KV split.  Returns false where it does not apply.
+bool launch_attention_dec(const AttnArgs& a, cudaStream_t s);
 // Prefill: RoPE the keys and write K/V of every live row into the cache
 // (a chunk's rows attend to each other, so the append precedes the attention).
 void launch_kv_append(const AttnArgs& a, cudaStream_t s);

@@ -68,7 +68,7 @@ EXPORTED = [
     "eeb_nccl_unique_id", "eeb_nccl_init", "eeb_profile_allreduce", "eeb_debug_gemm", "eeb_debug_bench_gemm",
     "eeb_prefill", "eeb_host_stage", "eeb_load_layers_async", "eeb_load_wait",
     "eeb_kv_configure_pages", "eeb_kv_reserve", "eeb_kv_release", "eeb_kv_pages",
-    "eeb_debug_stamps", "eeb_debug_stamps_read",
+    "eeb_debug_stamps", "eeb_debug_stamps_read", "eeb_debug_read_kv_span",
 ]
 
 _lib = None
@@ -110,6 +110,8 @@ def load_library() -> C.CDLL:
                                               C.c_int64, C.c_void_p]
         lib.eeb_debug_read_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                           C.c_void_p, C.c_void_p]
+        lib.eeb_debug_read_kv_span.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                               C.c_void_p, C.c_void_p]
         lib.eeb_debug_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_void_p, C.c_void_p, C.c_void_p]
         lib.eeb_debug_bench_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -395,6 +397,15 @@ class Context:
         k = np.zeros(desc.n_kv_heads * desc.head_dim, np.float32)
         v = np.zeros_like(k)
         _check(self.lib.eeb_debug_read_kv(self.h, model, layer, slot, pos, k.ctypes.data, v.ctypes.data))
+        return k, v
+
+    def read_kv_span(self, model: int, layer: int, slot: int, pos0: int, n_pos: int):
+        """K, V of positions [pos0, pos0 + n_pos) of a slot at a layer: f32 [n_pos, Hkv * hd]."""
+        desc = self.models[model]
+        k = np.zeros((n_pos, desc.n_kv_heads * desc.head_dim), np.float32)
+        v = np.zeros_like(k)
+        _check(self.lib.eeb_debug_read_kv_span(self.h, model, layer, slot, pos0, n_pos, k.ctypes.data,
+                                               v.ctypes.data))
         return k, v
 
     def debug_gemm(self, tier: int, w: np.ndarray, x: np.ndarray, mode: int = 0, dtype: int = BF16) -> np.ndarray:
