@@ -115,29 +115,37 @@ def head_bytes(desc, batch: int) -> int:
 # ----------------------------------------------------------------------------
 # reference arm / CPU baseline: the oracle port on host cores
 # ----------------------------------------------------------------------------
-def cpu_port_run(desc, steps: int, warmup: int, rows: int = 16, prefill: int = 4, seed: int = 1):
+def cpu_port_run(desc, steps: int, warmup: int, rows: int = 64, prompt: int = 128, seed: int = 1):
+    """The reference path timed on the host cores: the CPU oracle port (the
+    reference itself only looks verdicts up in a trace) running the
+    same workload as the GPU arm — `rows` rows of the same model, KV context
+    `prompt` (the prompt's KV filled synthetically to full depth: running the
+    prompt through the CPU model would dominate the sample), introspective
+    steps at positions prompt, prompt+1, ..."""
     from oracle.oracle import OracleModel
     from paper_2504_10724_b200 import eeb
 
     cores = os.cpu_count() or 1
-    d = desc.replace(max_slots=rows, max_seq_len=max(16, prefill + steps + warmup + 1))
+    d = desc.replace(max_slots=rows, max_seq_len=prompt + steps + warmup + 1)
     ref = OracleModel(d, threads=cores)
     ref.load(d.num_layers)
+    for r in range(rows):
+        ref.fill_kv_synthetic(r, prompt, seed + r)
     rng = np.random.default_rng(seed)
     slots = np.arange(rows)
-    for p in range(prefill):
-        ref.decode_step(0, eeb.FULL_DEPTH, 0.7, slots, rng.integers(0, d.vocab, rows), np.full(rows, p))
     times = []
     for k in range(warmup + steps):
         toks = rng.integers(0, d.vocab, rows)
         t0 = time.perf_counter()
-        ref.decode_step(0, eeb.INTROSPECTIVE, 0.7, slots, toks, np.full(rows, prefill + k))
+        ref.decode_step(0, eeb.INTROSPECTIVE, 0.7, slots, toks, np.full(rows, prompt + k))
         if k >= warmup:
             times.append(time.perf_counter() - t0)
+    ref.close()
     total = sum(times)
     return {"value": rows * len(times) / total, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"{len(times)} introspective steps x {rows} rows of the same model on the CPU oracle "
-                      f"(f64-accumulating fp32 restatement, {cores} threads), context {prefill}..{prefill + steps + warmup}",
+            "sample": f"{len(times)} introspective steps x {rows} rows (the GPU arm's batch) of the same model, "
+                      f"context {prompt}..{prompt + warmup + steps - 1} (prompt KV synthetic, full depth), on the "
+                      f"CPU oracle (f64-accumulating restatement with the device's rounding points, {cores} threads)",
             "seconds": total}
 
 
@@ -145,7 +153,9 @@ def run_reference(args, desc):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    r = cpu_port_run(desc, args.steps, args.warmup)
+    # one warm-up step (first touch of the KV pool); every timed step is the
+    # whole 64-row batch
+    r = cpu_port_run(desc, args.steps, min(args.warmup, 1), rows=args.batch, prompt=args.prompt)
     line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * r["seconds"] / max(1, args.steps), "higher_is_better": True,
@@ -175,7 +185,9 @@ def workload_config(args, desc):
             "model_shape": desc.name, "layers": desc.num_layers, "d_model": desc.d_model,
             "vocab": desc.vocab, "exit_layers": list(desc.exit_layers), "batch_per_gpu": args.batch,
             "global_batch": args.batch * args.gpus, "prompt_len": args.prompt,
-            "context": f"{args.prompt}..{args.prompt + 99}", "th": args.th, "policy": args.policy,
+            "context": f"{args.prompt}..{args.prompt + args.warmup + args.steps - 1} (timed steps: "
+                       f"{args.prompt + args.warmup}..{args.prompt + args.warmup + args.steps - 1})",
+            "th": args.th, "policy": args.policy,
             "parallelism": f"replicas x{args.gpus} (requests sharded, no data-path collective)",
             "l2": "inputs larger than L2 (GBs of weights streamed per step > 126 MB L2)"}
 
@@ -278,6 +290,49 @@ def ncu_traffic(args, desc):
         else:
             layer += b
     return {"layer_gemm": int(layer), "exit_head": int(head), "source": str(path.relative_to(ROOT))}
+
+def parity_sample(ctx, m, desc, eeb, args, policy, depth, toks_h, pos_h, e2e_outs, n_rows: int = 8):
+    """bf16 token / exit agreement of the e2e steps (the headline e2e calls)
+    with the CPU oracle on a sample of rows: the oracle is seeded with those
+    rows' prompt KV read back from the GPU (prefill parity is its own test),
+    then replays every decode step of the run (warm-up positions included, so
+    its KV of the decode positions is its own) and each e2e step's outputs for
+    the sampled rows are compared."""
+    from oracle.oracle import OracleModel
+
+    t0 = time.perf_counter()
+    B, P = args.batch, args.prompt
+    rows = np.linspace(0, B - 1, n_rows).astype(np.int32)
+    ref = OracleModel(desc.replace(max_slots=n_rows))
+    ref.load(depth or desc.num_layers)
+    for i, r in enumerate(rows):
+        for layer in range(1, desc.num_layers + 1):
+            k, v = ctx.read_kv_span(m, layer, int(r), 0, P)
+            ref.write_kv(layer, i, 0, k, v)
+    tok_same = exit_same = n = 0
+    conf_err = 0.0
+    near_th = 0
+    for k in range(len(toks_h)):
+        r = ref.decode_step(depth, policy, args.th, np.arange(n_rows), toks_h[k][rows], pos_h[k][rows])
+        if k < args.warmup:
+            continue
+        g = e2e_outs[k - args.warmup]
+        tok_same += int((g["token_id"][rows] == r["token_id"]).sum())
+        same = g["exit_layer"][rows] == r["exit_layer"]
+        exit_same += int(same.sum())
+        near_th += int((~same & ((np.abs(r["confidence"] - args.th) <= 2e-2) |
+                                 (np.abs(g["confidence"][rows] - args.th) <= 2e-2))).sum())
+        if same.any():
+            conf_err = max(conf_err, float(np.max(np.abs(g["confidence"][rows][same] - r["confidence"][same]))))
+        n += n_rows
+    ref.close()
+    return {"token_agreement": tok_same / max(1, n), "exit_agreement": exit_same / max(1, n),
+            "exit_mismatches_within_2e-2_of_th": near_th, "exit_mismatches": n - exit_same,
+            "max_abs_conf_diff_where_exits_agree": conf_err, "row_steps": n, "rows": rows.tolist(),
+            "seconds": time.perf_counter() - t0,
+            "how": "the e2e steps' outputs (host API) for the sampled rows vs the CPU oracle replaying every decode "
+                   "step from the GPU's prompt KV; bf16 bar: token agreement >= 0.99"}
+
 
 def run_eeb(args, desc):
     import torch
@@ -389,67 +444,81 @@ def run_eeb(args, desc):
     ms = max_over_ranks(ms_local)
     value = world * B / (ms / 1000.0)
 
-    # ---- instrumented pass: per-kernel-category CUDA-event times -------------
-    ctx.profile_enable(True)
-    for k in range(args.warmup, n_tok):
-        step(k)
-    ctx.synchronize()
-    prof = ctx.profile_read()
-    ctx.profile_enable(False)
-    nsteps = max(1, prof["steps"])
-    launches_per_step = prof["last_step_launches"]
+    # ---- in-graph launch timeline of the same steps (eeb_debug_stamps) ---------
+    # Every kernel of the captured PDL graph stamps its first-CTA start and
+    # last-warp exit; per-launch critical-path times sum to the step span.
+    from paper_2504_10724_b200 import timeline
+
+    n_tl = min(args.steps, 8)
+    tl = timeline.run(ctx, lambda k: step(args.warmup + (k % args.steps)), n_tl)
+    launches_per_step = len(tl["launches"])
     pk, pk_kind = peaks()
     hbm = float(pk["hbm_gbs"])
     peak_source = ("measured MEASURED_PEAKS.json hbm_gbs (copy burst)" if pk_kind == "measured"
                    else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
     hist_np = hist_acc.cpu().numpy().astype(np.float64)
-    exit_head = None
-    if True:
-        gemm_ms = prof["layer_gemm_ms"] / nsteps
-        head_ms = prof["exit_head_ms"] / nsteps
-        attn_ms = prof["attention_ms"] / nsteps
-        run_layers = args.depth if policy == eeb.FLAT else desc.num_layers
-        heads_run = 1 if policy in (eeb.FLAT, eeb.FULL_DEPTH) else ne
-        g_bytes = gemm_bytes_per_step(desc, B, run_layers)
-        h_bytes = head_bytes(desc, B) * heads_run
-        tr = ncu_traffic(args, desc)
-        roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1)",
-                "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
-                "traffic": tr["layer_gemm"] if tr else None,
-                **({"traffic_source": tr["source"] + " (DRAM bytes per step, ncu, cold cache)"} if tr else {}),
-                "peak_source": peak_source,
-                "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
-                "step_share": gemm_ms / max(1e-9, gemm_ms + head_ms + attn_ms + prof["norm_ms"] / nsteps
-                                            + prof["other_ms"] / nsteps)}
-        roof["frac"] = roof["achieved"] / hbm
-        exit_head = {"achieved": h_bytes / (head_ms / 1000.0) / 1e9 if head_ms > 0 else None, "unit": "GB/s",
-                     "ms_per_step": head_ms, "algorithmic_bytes_per_step": h_bytes,
-                     "traffic": tr["exit_head"] if tr else None}
-        if exit_head["achieved"]:
-            exit_head["frac"] = exit_head["achieved"] / hbm
-    # whole step: weights of the layers run + heads evaluated + KV of the rows that reached each layer
     run_layers = args.depth if policy == eeb.FLAT else desc.num_layers
     heads_run = 1 if policy in (eeb.FLAT, eeb.FULL_DEPTH) else ne
     hist_frac = hist_np / max(1.0, hist_np.sum())
+
+    def crit_ms(pred):
+        return sum(l["crit_us"] for l in tl["launches"] if pred(l)) / 1e3
+
+    gemm_ms = crit_ms(lambda l: l["cat"] == "layer_gemm")
+    head_gemm_ms = crit_ms(lambda l: l["cat"] == "exit_head" and l["kernel"] in ("gemm_tc", "gemm_cc", "head_reduce"))
+    head_ms = crit_ms(lambda l: l["cat"] == "exit_head")
+    attn_ms = crit_ms(lambda l: l["cat"] == "attention")
+    g_bytes = gemm_bytes_per_step(desc, B, run_layers)
+    h_bytes = head_bytes(desc, B) * heads_run
+    tr = ncu_traffic(args, desc)
+    roof = {"bound": "hbm", "kernel": "layer decode GEMMs (K1, tcgen05)",
+            "achieved": g_bytes / (gemm_ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s",
+            "traffic": tr["layer_gemm"] if tr else None,
+            **({"traffic_source": tr["source"] + " (DRAM bytes per step, ncu, cold cache)"} if tr else {}),
+            "peak_source": peak_source, "algorithmic_bytes_per_step": g_bytes, "kernel_ms_per_step": gemm_ms,
+            "time_source": "in-graph %globaltimer stamps (critical-path time per launch, captured PDL graph)",
+            "step_share": gemm_ms / max(1e-9, tl["span_ms"])}
+    roof["frac"] = roof["achieved"] / hbm
+    exit_head = {"kernel": "fused exit-head GEMM (K2: LM head + max/argmax/sum-exp epilogue)",
+                 "achieved": h_bytes / (head_gemm_ms / 1000.0) / 1e9 if head_gemm_ms > 0 else None,
+                 "unit": "GB/s", "ms_per_step": head_gemm_ms, "head_path_ms_per_step": head_ms,
+                 "algorithmic_bytes_per_step": h_bytes, "traffic": tr["exit_head"] if tr else None}
+    if exit_head["achieved"]:
+        exit_head["frac"] = exit_head["achieved"] / hbm
+        exit_head["frac_incl_decide"] = h_bytes / (head_ms / 1000.0) / 1e9 / hbm
+    # KV of the rows that reached each layer (introspective: survivors only)
     if policy == eeb.INTROSPECTIVE:
         row_layers = float(np.sum(hist_frac * np.asarray(desc.exit_layers))) * B
     else:
         row_layers = float(run_layers * B)
-    kv_step = row_layers * (P + 0.5 * args.steps + 1) * 2 * desc.n_kv_heads * desc.head_dim * desc.bytes_per_el
+    mean_ctx = P + args.warmup + 0.5 * args.steps + 1
+    kv_step = row_layers * mean_ctx * 2 * desc.n_kv_heads * desc.head_dim * desc.bytes_per_el
+    attention = {"kernel": "decode attention (K1b)", "ms_per_step": attn_ms, "algorithmic_bytes_per_step": int(kv_step),
+                 "achieved": kv_step / (attn_ms / 1000.0) / 1e9 if attn_ms > 0 else None, "unit": "GB/s"}
+    if attention["achieved"]:
+        attention["frac"] = attention["achieved"] / hbm
     w_step = desc.layer_weight_elems() * desc.bytes_per_el * run_layers + \
         desc.vocab * desc.d_model * desc.bytes_per_el * heads_run
     step_roof = {"bound": "hbm", "algorithmic_bytes_per_step": int(w_step + kv_step),
                  "weight_bytes": int(w_step), "kv_bytes": int(kv_step),
                  "achieved": (w_step + kv_step) / (ms / 1000.0) / 1e9, "peak": hbm, "unit": "GB/s"}
     step_roof["frac"] = step_roof["achieved"] / hbm
+    kernel_ms = {c: v["crit_ms"] for c, v in tl["cats"].items()}
+    kernel_ms["span"] = tl["span_ms"]
 
     # ---- e2e: public host-pointer API, H2D + D2H inside every call ------------
     barrier()
     t0 = time.perf_counter()
-    last = None
+    e2e_outs = []
     for k in range(args.warmup, n_tok):
-        last = ctx.decode_step(m, depth, policy, args.th, slots, toks_h[k], pos_h[k])
+        e2e_outs.append(ctx.decode_step(m, depth, policy, args.th, slots, toks_h[k], pos_h[k]))
     e2e_s = max_over_ranks(time.perf_counter() - t0)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        try:
+            parity = parity_sample(ctx, m, desc, eeb, args, policy, depth, toks_h, pos_h, e2e_outs)
+        except Exception as e:  # reported, never fatal for the headline line
+            parity = {"error": repr(e)[:200]}
     e2e_value = world * B * args.steps / e2e_s
     h2d = 3 * B * 4
     d2h = B * (4 + 4 + 4 + 4 + 1 + 1) + ne * 8 + 8 + 8
@@ -512,7 +581,7 @@ def run_eeb(args, desc):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_port_run(desc, steps=2, warmup=0)
+        r = cpu_port_run(desc, steps=2, warmup=0, rows=B, prompt=P + args.warmup)
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -520,15 +589,17 @@ def run_eeb(args, desc):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, biased exit heads)",
                 "config": workload_config(args, desc), "roofline": roof, "step_roofline": step_roof,
-                **({"exit_head_roofline": exit_head} if exit_head else {}),
-                "cpu_baseline": cpu,
+                "exit_head_roofline": exit_head, "attention_roofline": attention,
+                "cpu_baseline": cpu, "parity": parity,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
                 "gpu_launches": int(launches_per_step * args.steps),
                 "launches_per_step": launches_per_step,
+                "timeline": {"span_ms": tl["span_ms"], "steps_stamped": n_tl,
+                             "how": "separate stamped replay of the timed steps' inputs; per-launch critical-path "
+                                    "times (end - previous end) from in-kernel %globaltimer stamps"},
                 "clocks": clocks, "exit_fractions": exit_frac, "prefill": prefill,
-                "kernel_ms_per_step": {k.replace("_ms", ""): v / nsteps for k, v in prof.items()
-                                       if k.endswith("_ms") and v > 0},
+                "kernel_ms_per_step": kernel_ms,
                 "path": "per-op kernel chain (CUDA graph, PDL)"}
         if secondary is not None:
             line["secondary_c4"] = secondary
@@ -558,6 +629,7 @@ def main():
     ap.add_argument("--depth", type=int, default=6)
     ap.add_argument("--th", type=float, default=0.7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of sampled e2e rows")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 (34B) line attached at N=1")
     ap.add_argument("--tier", type=int, default=0, help="0 auto, 1 CUDA-core GEMV, 2 tcgen05 GEMMs")
     args = ap.parse_args()

@@ -124,6 +124,33 @@ eeb_status eeb_load_layers(eeb_ctx* ctx, int model, int to_depth);
 eeb_status eeb_evict(eeb_ctx* ctx, int model);   /* ↔ evict_model (memory_model.hpp:104) */
 eeb_status eeb_loaded_depth(eeb_ctx* ctx, int model, int* depth);
 
+/* Caller-supplied weights (real checkpoints; tp_size == 1 models).  The packed
+ * host layout, all tensors row-major with K contiguous, in the model dtype
+ * except the norm gains (f32), each part at a 256-byte aligned offset:
+ *   layer l:  0 attn_norm [D] f32 | 1 mlp_norm [D] f32 | 2 Wqkv [dq + 2 dkv][D]
+ *             (q rows, k rows, v rows) | 3 Wo [D][dq] | 4 Wup [F][D] (ReLU) or
+ *             [2F][D] (SwiGLU: gate and up rows interleaved) | 5 Wdown [D][F]
+ *   base:     embedding [V][D] | exit heads e = 0..n_exits-1 [V][D] | head
+ *             norm gains e = 0..n_exits-1 [D] f32
+ * Replaces the reference's `do_load` source (engine.hpp:197-216: a model's
+ * layers in CPU memory moved to the GPU); SURVEY §8(b) eeb_load_layers(ctx,
+ * model, from, to, pinned_host, bytes). */
+typedef struct {
+    int64_t layer_bytes, base_bytes;  /* bytes of one packed layer / of the base weights */
+    int64_t layer_off[6];             /* part offsets inside a layer */
+    int64_t base_off[1 + 2 * 64];     /* embedding, heads, head norms (-1 past n_exits) */
+} eeb_weight_layout_t;
+eeb_status eeb_weight_layout(eeb_ctx* ctx, int model, eeb_weight_layout_t* out);
+/* Copy one packed layer (1-based) / the base weights into the host tier (pinned;
+ * the source of eeb_load_layers and eeb_load_layers_async from then on).  The
+ * tier is a prefix: layer l needs layers < l staged.  A resident layer's device
+ * copy is refreshed. */
+eeb_status eeb_host_stage_layer(eeb_ctx* ctx, int model, int layer, const void* host, int64_t bytes);
+eeb_status eeb_host_stage_base(eeb_ctx* ctx, int model, const void* host, int64_t bytes);
+/* Layers [from, to] from one buffer of (to - from + 1) packed layers: staged to
+ * the host tier and made resident (from <= loaded_depth + 1); returns when done. */
+eeb_status eeb_load_layers_from(eeb_ctx* ctx, int model, int from, int to, const void* host, int64_t bytes);
+
 /* Host tier ↔ the model held in CPU memory that HELIOS's greedy loader pulls
  * layers from (engine.hpp:197-216; memory_model.hpp:76-105): layers [1, depth]
  * plus the base weights (embedding, exit heads) packed into pinned host
@@ -218,6 +245,10 @@ eeb_status eeb_debug_stamps(eeb_ctx* ctx, int max_launches);
 /* JSON {"launches": [{"kernel", "start_ns", "end_ns", "ctas"}, ...]} of the
  * last decode step, in launch order, times relative to its first CTA start. */
 eeb_status eeb_debug_stamps_read(eeb_ctx* ctx, char* json_out, int64_t cap);
+/* Per-CTA stamps (ns from the step's first start; -1 = none) of launch
+ * `launch` of the last stamped step, CTAs [0, n) in linear block order. */
+eeb_status eeb_debug_stamps_cta(eeb_ctx* ctx, int launch, int64_t* start_ns, int64_t* end_ns, int64_t* wait_ns,
+                                int n);
 
 /* Test/diagnostic hooks (not used on the serving path). */
 eeb_status eeb_debug_last_logits(eeb_ctx* ctx, int head, float* host_out, int64_t n);  /* [batch][vocab] of one head, when retained */

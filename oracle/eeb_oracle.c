@@ -314,6 +314,47 @@ float orc_weight(const orc_model* m, int tensor, int layer, int64_t index) {
     return p ? p[index] : NAN;
 }
 
+/* Whole-tensor access (test hooks: caller-supplied weights).  Element counts
+ * per kind: 0/3 norms [D]; 1 Wqkv [dq+2dkv][D]; 2 Wo [D][dq]; 4 Wup [up_rows][D];
+ * 5 Wdown [D][F]; 100 embedding [V][D]; 200+e head [V][D]; 300+e head norm [D]. */
+static float* tensor_ptr(orc_model* m, int tensor, int layer, int64_t* n) {
+    const orc_desc* d = &m->d;
+    const int64_t D = d->d_model;
+    if (tensor == 100) { *n = (int64_t)d->vocab * D; return m->emb; }
+    if (tensor >= 300 && tensor - 300 < d->n_exits) { *n = D; return m->head_norm[tensor - 300]; }
+    if (tensor >= 200 && tensor - 200 < d->n_exits) { *n = (int64_t)d->vocab * D; return m->head[tensor - 200]; }
+    if (layer < 1 || layer > m->loaded) return NULL;
+    const int i = layer - 1;
+    switch (tensor) {
+        case 0: *n = D; return m->attn_norm[i];
+        case 1: *n = (int64_t)(m->dq + 2 * m->dkv) * D; return m->wqkv[i];
+        case 2: *n = D * m->dq; return m->wo[i];
+        case 3: *n = D; return m->mlp_norm[i];
+        case 4: *n = (int64_t)m->up_rows * D; return m->wup[i];
+        case 5: *n = D * d->d_ffn; return m->wdown[i];
+        default: return NULL;
+    }
+}
+
+int64_t orc_tensor_get(orc_model* m, int tensor, int layer, float* out, int64_t n) {
+    int64_t have = 0;
+    const float* p = tensor_ptr(m, tensor, layer, &have);
+    if (!p) return fail("no such tensor (or layer not loaded)");
+    if (out) memcpy(out, p, sizeof(float) * (size_t)(n < have ? n : have));
+    return have;
+}
+
+/* Replace a tensor (values rounded to the model dtype, as the device stores them). */
+int orc_tensor_set(orc_model* m, int tensor, int layer, const float* src, int64_t n) {
+    int64_t have = 0;
+    float* p = tensor_ptr(m, tensor, layer, &have);
+    if (!p) return fail("no such tensor (or layer not loaded)");
+    if (n != have) return fail("tensor size mismatch");
+    const int norm = tensor == 0 || tensor == 3 || tensor >= 300;
+    for (int64_t i = 0; i < n; ++i) p[i] = norm ? src[i] : rnd(m, src[i]);
+    return 0;
+}
+
 /* ---------------------------------------------------------------------------
  * The step.
  * ------------------------------------------------------------------------- */

@@ -84,6 +84,10 @@ int orc_decide(int policy, int n, const int32_t* layers, const int32_t* toks, co
                int depth, int num_layers, orc_decision* out);
 /* K/V of one position, [n_kv_heads][head_dim] each. */
 int orc_read_kv(const orc_model* m, int layer, int slot, int pos, float* k, float* v);
+/* Whole tensors (kinds as orc_weight): get returns the element count (copies
+ * min(n, count) when out is set); set replaces all of it (rounded to the dtype). */
+int64_t orc_tensor_get(orc_model* m, int tensor, int layer, float* out, int64_t n);
+int orc_tensor_set(orc_model* m, int tensor, int layer, const float* src, int64_t n);
 /* Import K/V of positions [pos0, pos0+n) ([n][n_kv_heads*head_dim] each) at one layer. */
 int orc_write_kv(orc_model* m, int layer, int slot, int pos0, int n, const float* k, const float* v);
 /* Synthetic full-depth KV for positions [0, n) of a slot (CPU-baseline context). */

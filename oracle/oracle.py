@@ -78,6 +78,9 @@ def lib() -> C.CDLL:
         L.orc_decode_step.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_float, C.c_int, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.POINTER(_Out)]
         L.orc_read_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.orc_tensor_get.restype = C.c_int64
+        L.orc_tensor_get.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
+        L.orc_tensor_set.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
         L.orc_write_kv.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         L.orc_fill_kv_synthetic.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64]
         L.orc_last_error.restype = C.c_char_p
@@ -169,4 +172,18 @@ class OracleModel:
     def fill_kv_synthetic(self, slot: int, n: int, seed: int = 1) -> None:
         """Synthetic full-depth KV for positions [0, n) of a slot (CPU-baseline context)."""
         if lib().orc_fill_kv_synthetic(self.h, slot, n, seed) != 0:
+            raise RuntimeError(lib().orc_last_error().decode())
+
+    def tensor(self, tensor: int, layer: int = 0) -> np.ndarray:
+        """A whole weight tensor (f32 values, already on the dtype's grid)."""
+        n = lib().orc_tensor_get(self.h, tensor, layer, None, 0)
+        if n < 0:
+            raise RuntimeError(lib().orc_last_error().decode())
+        out = np.empty(n, np.float32)
+        lib().orc_tensor_get(self.h, tensor, layer, out.ctypes.data, n)
+        return out
+
+    def set_tensor(self, tensor: int, layer: int, values) -> None:
+        v = np.ascontiguousarray(values, np.float32).ravel()
+        if lib().orc_tensor_set(self.h, tensor, layer, v.ctypes.data, v.size) != 0:
             raise RuntimeError(lib().orc_last_error().decode())

@@ -104,7 +104,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // null): one predicated branch per CTA.
 // ---------------------------------------------------------------------------
 struct Stamp {
-    unsigned long long* buf = nullptr;  // starts [slots][kStampCtas], then ends at buf + end_off
+    unsigned long long* buf = nullptr;  // starts [slots][kStampCtas], ends at + end_off, waits at + 2 end_off
     int slot = 0;
     int64_t end_off = 0;
 };
@@ -130,6 +130,12 @@ struct StampScope {
             asm volatile("red.global.max.u64 [%0], %1;" ::"l"(stamp_cell(s) + s.end_off), "l"(gtimer()) : "memory");
     }
 };
+// After the kernel's griddepcontrol.wait returned (first CTA): the predecessor
+// finished; wait - previous end = launch/flush latency, end - wait = work.
+__device__ __forceinline__ void stamp_waited(const Stamp& s) {
+    if (s.buf && threadIdx.x == 0)
+        asm volatile("red.global.min.u64 [%0], %1;" ::"l"(stamp_cell(s) + 2 * s.end_off), "l"(gtimer()) : "memory");
+}
 // Host: the stamp for the next launch (defined in eeb_api.cu; buf null unless
 // the calling thread is recording a timeline).
 Stamp stamp_next(const void* kernel);

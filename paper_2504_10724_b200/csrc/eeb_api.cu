@@ -415,6 +415,9 @@ void settle_pending(Model& m) {
     m.pending.reset();
 }
 
+std::unique_ptr<LayerWeights> layer_from_host(const Model& m, int l, cudaStream_t s);
+void base_from_host(Model& m, cudaStream_t s);
+
 void load_to(eeb_ctx* c, Model& m, int to) {
     const eeb_model_desc& d = m.desc;
     if (to < 0 || to > d.num_layers)
@@ -430,8 +433,16 @@ void load_to(eeb_ctx* c, Model& m, int to) {
         m.loaded = 0;
         return;
     }
-    if (m.loaded == 0) synth_base(m, s);
-    while ((int)m.layers.size() < to) m.layers.push_back(synth_layer(m, (int)m.layers.size() + 1, s));
+    // The host tier (caller-supplied weights, or a staged copy of the synthetic
+    // ones) is the source when it holds the tensor; otherwise synthesise.
+    if (m.loaded == 0) {
+        if (m.host.base) base_from_host(m, s);
+        else synth_base(m, s);
+    }
+    while ((int)m.layers.size() < to) {
+        const int l = (int)m.layers.size() + 1;
+        m.layers.push_back(l <= (int)m.host.layers.size() ? layer_from_host(m, l, s) : synth_layer(m, l, s));
+    }
     while ((int)m.layers.size() > to) m.layers.pop_back();
     m.loaded = to;
     EEB_CUDA(cudaStreamSynchronize(s));
@@ -459,6 +470,75 @@ std::vector<const DevBuf*> base_parts(const Model& m) {
     for (auto& h : m.head) v.push_back(h.get());
     for (auto& g : m.head_norm) v.push_back(g.get());
     return v;
+}
+
+// ---- caller-supplied weights (eeb_host_stage_layer / _base, eeb_load_layers_from) --
+// Packed host layout = the host tier's blob layout: parts back to back, each
+// at a 256-byte aligned offset (include/eeb/eeb.h, eeb_weight_layout).
+constexpr size_t kPartAlign = 256;
+std::vector<size_t> layer_part_bytes(const Model& m) {
+    const size_t D = m.desc.d_model, wb = m.wbytes;
+    return {D * 4, D * 4, (size_t)(m.dq_l + 2 * m.dkv_l) * D * wb, D * m.dq_l * wb, (size_t)m.up_l * D * wb,
+            D * (size_t)m.f_l * wb};
+}
+std::vector<size_t> base_part_bytes(const Model& m) {
+    const size_t D = m.desc.d_model, V = m.desc.vocab, wb = m.wbytes;
+    std::vector<size_t> v{V * D * wb};
+    for (int e = 0; e < m.desc.n_exits; ++e) v.push_back(V * D * wb);
+    for (int e = 0; e < m.desc.n_exits; ++e) v.push_back(D * 4);
+    return v;
+}
+size_t packed_offsets(const std::vector<size_t>& sz, std::vector<size_t>* off) {
+    size_t total = 0;
+    for (size_t k : sz) {
+        if (off) off->push_back(total);
+        total += (k + kPartAlign - 1) & ~(kPartAlign - 1);
+    }
+    return total;
+}
+// A host-tier blob holding a copy of the caller's packed buffer.
+std::unique_ptr<HostBlob> blob_from_host(const std::vector<size_t>& sz, const void* src, int64_t bytes) {
+    auto b = std::make_unique<HostBlob>();
+    const size_t total = packed_offsets(sz, &b->off);
+    if (!src || bytes != (int64_t)total)
+        throw Error(EEB_E_VALIDATION, "weights buffer must be " + std::to_string(total) + " bytes (eeb_weight_layout)");
+    b->sz = sz;
+    b->buf.alloc(total);
+    std::memcpy(b->buf.p, src, total);
+    return b;
+}
+void require_single_shard(const Model& m) {
+    if (m.shards != 1 || m.tp != 1)
+        throw Error(EEB_E_DOMAIN, "caller-supplied weights: tensor-parallel models are not supported (tp_size must be 1)");
+}
+// Device layer l (1-based) filled from the host tier's blob (synchronous on s).
+std::unique_ptr<LayerWeights> layer_from_host(const Model& m, int l, cudaStream_t s) {
+    auto L = alloc_layer(m);
+    const HostBlob& b = *m.host.layers[l - 1];
+    for (int k = 0; k < 6; ++k)
+        EEB_CUDA(cudaMemcpyAsync(L->parts[k]->p, static_cast<const char*>(b.buf.p) + b.off[k], b.sz[k],
+                                 cudaMemcpyHostToDevice, s));
+    return L;
+}
+void base_from_host(Model& m, cudaStream_t s) {
+    const eeb_model_desc& d = m.desc;
+    const HostBlob& b = *m.host.base;
+    m.emb.ensure(b.sz[0]);
+    EEB_CUDA(cudaMemcpyAsync(m.emb.p, b.buf.p, b.sz[0], cudaMemcpyHostToDevice, s));
+    m.head.clear();
+    m.head_norm.clear();
+    for (int e = 0; e < d.n_exits; ++e) {
+        auto h = std::make_unique<DevBuf>();
+        h->ensure(b.sz[1 + e]);
+        EEB_CUDA(cudaMemcpyAsync(h->p, static_cast<const char*>(b.buf.p) + b.off[1 + e], b.sz[1 + e],
+                                 cudaMemcpyHostToDevice, s));
+        auto g = std::make_unique<DevBuf>();
+        g->ensure(b.sz[1 + d.n_exits + e]);
+        EEB_CUDA(cudaMemcpyAsync(g->p, static_cast<const char*>(b.buf.p) + b.off[1 + d.n_exits + e],
+                                 b.sz[1 + d.n_exits + e], cudaMemcpyHostToDevice, s));
+        m.head.push_back(std::move(h));
+        m.head_norm.push_back(std::move(g));
+    }
 }
 
 void host_stage(eeb_ctx* c, Model& m, int depth) {
@@ -661,6 +741,7 @@ void stamp_reset(eeb_ctx* c) {
     const size_t cells = (size_t)c->stamp_cap * kStampCtas;
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.p, 0xFF, cells * 8, c->stream));
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + cells, 0, cells * 8, c->stream));
+    EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + 2 * cells, 0xFF, cells * 8, c->stream));
 }
 
 // Size the step workspace for `batch` rows of model m.  Buffers are shared by
@@ -1621,6 +1702,81 @@ eeb_status eeb_host_stage(eeb_ctx* c, int model, int depth) {
     });
 }
 
+eeb_status eeb_weight_layout(eeb_ctx* c, int model, eeb_weight_layout_t* out) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        if (!out) throw Error(EEB_E_DOMAIN, "null argument");
+        std::vector<size_t> lo, bo;
+        out->layer_bytes = (int64_t)packed_offsets(layer_part_bytes(m), &lo);
+        out->base_bytes = (int64_t)packed_offsets(base_part_bytes(m), &bo);
+        for (int k = 0; k < 6; ++k) out->layer_off[k] = (int64_t)lo[k];
+        for (int k = 0; k < 1 + 2 * 64; ++k) out->base_off[k] = k < (int)bo.size() ? (int64_t)bo[k] : -1;
+    });
+}
+
+eeb_status eeb_host_stage_layer(eeb_ctx* c, int model, int layer, const void* host, int64_t bytes) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        require_single_shard(m);
+        if (layer < 1 || layer > m.desc.num_layers) throw Error(EEB_E_DOMAIN, "layer outside [1, num_layers]");
+        if (layer > (int)m.host.layers.size() + 1)
+            throw Error(EEB_E_DOMAIN, "host tier is a prefix: stage layer " + std::to_string(m.host.layers.size() + 1) +
+                                          " first");
+        EEB_CUDA(cudaSetDevice(c->device));
+        settle_pending(m);
+        auto b = blob_from_host(layer_part_bytes(m), host, bytes);
+        if (layer == (int)m.host.layers.size() + 1) m.host.layers.push_back(std::move(b));
+        else m.host.layers[layer - 1] = std::move(b);
+        if (layer <= (int)m.layers.size()) {  // resident: refresh the device copy
+            EEB_CUDA(cudaStreamSynchronize(c->stream));
+            m.layers[layer - 1] = layer_from_host(m, layer, c->stream);
+            EEB_CUDA(cudaStreamSynchronize(c->stream));
+            drop_graphs(c, model);
+        }
+    });
+}
+
+eeb_status eeb_host_stage_base(eeb_ctx* c, int model, const void* host, int64_t bytes) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        require_single_shard(m);
+        EEB_CUDA(cudaSetDevice(c->device));
+        settle_pending(m);
+        m.host.base = blob_from_host(base_part_bytes(m), host, bytes);
+        if (m.loaded > 0) {  // resident: refresh the device copy
+            EEB_CUDA(cudaStreamSynchronize(c->stream));
+            base_from_host(m, c->stream);
+            EEB_CUDA(cudaStreamSynchronize(c->stream));
+            drop_graphs(c, model);
+        }
+    });
+}
+
+eeb_status eeb_load_layers_from(eeb_ctx* c, int model, int from, int to, const void* host, int64_t bytes) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        require_single_shard(m);
+        if (from < 1 || to < from || to > m.desc.num_layers) throw Error(EEB_E_DOMAIN, "need 1 <= from <= to <= num_layers");
+        if (from > (int)m.host.layers.size() + 1 || from > m.loaded + 1)
+            throw Error(EEB_E_DOMAIN, "layers are loaded as a prefix: from must be <= loaded_depth + 1");
+        const int64_t per = (int64_t)packed_offsets(layer_part_bytes(m), nullptr);
+        if (!host || bytes != per * (to - from + 1))
+            throw Error(EEB_E_VALIDATION, "buffer must hold " + std::to_string(to - from + 1) + " packed layers of " +
+                                              std::to_string(per) + " bytes");
+        EEB_CUDA(cudaSetDevice(c->device));
+        settle_pending(m);
+        for (int l = from; l <= to; ++l) {
+            auto b = blob_from_host(layer_part_bytes(m), static_cast<const char*>(host) + (l - from) * per, per);
+            if (l == (int)m.host.layers.size() + 1) m.host.layers.push_back(std::move(b));
+            else m.host.layers[l - 1] = std::move(b);
+        }
+        drop_graphs(c, model);
+        while ((int)m.layers.size() >= from) m.layers.pop_back();  // reloaded from the new host copies
+        m.loaded = (int)m.layers.size();
+        load_to(c, m, std::max(to, m.loaded));
+    });
+}
+
 eeb_status eeb_load_layers_async(eeb_ctx* c, int model, int to_depth) {
     return guarded([&] {
         Model& m = model_of(c, model);
@@ -1913,7 +2069,7 @@ eeb_status eeb_debug_stamps(eeb_ctx* c, int max_launches) {
         c->stamp_cap = max_launches;
         if (max_launches > 0) {
             c->stamp_buf.release();
-            c->stamp_buf.ensure((size_t)max_launches * kStampCtas * 2 * 8);
+            c->stamp_buf.ensure((size_t)max_launches * kStampCtas * 3 * 8);
         } else {
             c->stamp_buf.release();
         }
@@ -1926,17 +2082,18 @@ eeb_status eeb_debug_stamps_read(eeb_ctx* c, char* json_out, int64_t cap) {
         if (c->stamp_cap <= 0) throw Error(EEB_E_DOMAIN, "stamping is off (eeb_debug_stamps)");
         EEB_CUDA(cudaStreamSynchronize(c->stream));
         const size_t cells = (size_t)c->stamp_cap * kStampCtas;
-        std::vector<unsigned long long> h(2 * cells);
+        std::vector<unsigned long long> h(3 * cells);
         EEB_CUDA(cudaMemcpy(h.data(), c->stamp_buf.p, h.size() * 8, cudaMemcpyDeviceToHost));
         std::string j = "{\"launches\": [";
         unsigned long long t0 = ~0ull;
         for (size_t i = 0; i < c->stamp_last.first.size(); ++i)
             for (int k = 0; k < kStampCtas; ++k) t0 = std::min(t0, h[i * kStampCtas + k]);
         for (size_t i = 0; i < c->stamp_last.first.size(); ++i) {
-            unsigned long long st = ~0ull, en = 0;
+            unsigned long long st = ~0ull, en = 0, wt = ~0ull;
             int ctas = 0;
             for (int k = 0; k < kStampCtas; ++k) {
                 const unsigned long long a = h[i * kStampCtas + k], b = h[cells + i * kStampCtas + k];
+                wt = std::min(wt, h[2 * cells + i * kStampCtas + k]);
                 if (a != ~0ull) {
                     ++ctas;
                     st = std::min(st, a);
@@ -1948,14 +2105,43 @@ eeb_status eeb_debug_stamps_read(eeb_ctx* c, char* json_out, int64_t cap) {
             const int cat = c->stamp_last.second[i];
             char buf[512];
             std::snprintf(buf, sizeof buf,
-                          "%s{\"kernel\": \"%s\", \"cat\": \"%s\", \"start_ns\": %lld, \"end_ns\": %lld, \"ctas\": %d}",
+                          "%s{\"kernel\": \"%s\", \"cat\": \"%s\", \"start_ns\": %lld, \"end_ns\": %lld, "
+                          "\"wait_ns\": %lld, \"ctas\": %d}",
                           i ? ", " : "", name, cat >= 0 ? kCatNames[cat] : "?", ctas ? (long long)(st - t0) : -1LL,
-                          ctas ? (long long)(en - t0) : -1LL, ctas);
+                          ctas ? (long long)(en - t0) : -1LL, wt != ~0ull ? (long long)(wt - t0) : -1LL, ctas);
             j += buf;
         }
         j += "]}";
         if ((int64_t)j.size() + 1 > cap) throw Error(EEB_E_DOMAIN, "buffer too small");
         std::memcpy(json_out, j.c_str(), j.size() + 1);
+    });
+}
+
+eeb_status eeb_debug_stamps_cta(eeb_ctx* c, int launch, int64_t* start_ns, int64_t* end_ns, int64_t* wait_ns,
+                                int n) {
+    return guarded([&] {
+        if (!c || c->stamp_cap <= 0) throw Error(EEB_E_DOMAIN, "stamping is off (eeb_debug_stamps)");
+        if (launch < 0 || launch >= (int)c->stamp_last.first.size() || n < 0 || n > kStampCtas)
+            throw Error(EEB_E_DOMAIN, "bad argument");
+        EEB_CUDA(cudaStreamSynchronize(c->stream));
+        const size_t cells = (size_t)c->stamp_cap * kStampCtas;
+        std::vector<unsigned long long> all(cells);
+        EEB_CUDA(cudaMemcpy(all.data(), c->stamp_buf.p, cells * 8, cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull;
+        for (size_t i = 0; i < c->stamp_last.first.size() * kStampCtas; ++i) t0 = std::min(t0, all[i]);
+        std::vector<unsigned long long> h(3 * (size_t)n);
+        for (int w = 0; w < 3; ++w)
+            EEB_CUDA(cudaMemcpy(h.data() + (size_t)w * n, c->stamp_buf.as<unsigned long long>() + w * cells +
+                                (size_t)launch * kStampCtas, (size_t)n * 8, cudaMemcpyDeviceToHost));
+        auto rel = [&](unsigned long long v, bool is_end) -> int64_t {
+            if ((!is_end && v == ~0ull) || (is_end && v == 0)) return -1;
+            return (int64_t)(v - t0);
+        };
+        for (int k = 0; k < n; ++k) {
+            if (start_ns) start_ns[k] = rel(h[k], false);
+            if (end_ns) end_ns[k] = rel(h[(size_t)n + k], true);
+            if (wait_ns) wait_ns[k] = rel(h[2 * (size_t)n + k], false);
+        }
     });
 }
 

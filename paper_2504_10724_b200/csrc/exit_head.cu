@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(Stamp stamp, Dec
     StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
+    stamp_waited(stamp);
     __shared__ int warp_counts[32];
     __shared__ int n_live_s;
     __shared__ int last_s;

@@ -275,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #endif
         if (lane == 0) {
             pdl_wait();
+            stamp_waited(p.st);
             EEB_STAMP(true, 2);  // predecessor complete
             for (int i = 0; i < pre; ++i)
                 tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,

@@ -131,6 +131,7 @@ struct AttnArgs {
     int kv_splits = 1;
     float* kv_part = nullptr;   // [max_rows][Hkv][kv_splits][8][hd + 2]
     int* kv_ticket = nullptr;   // [max_rows][Hkv]
+    int dbg = 0;                // timing experiments (attention_dec, EEB_ATTN_DBG): 1 no compute, 2 no K/V loads
 };
 // Device address of (page-table row of slot, position, kv head, dim 0) in a layer's K or V cache.
 __host__ __device__ inline int64_t kv_elem_offset(const AttnArgs& a, int slot, int pos, int g) {

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kNormThreads)
     StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
+    stamp_waited(stamp);
     const int i = blockIdx.x;
     if (i >= *n_active) return;
     __shared__ float red[32];

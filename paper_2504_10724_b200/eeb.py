@@ -69,7 +69,14 @@ EXPORTED = [
     "eeb_prefill", "eeb_host_stage", "eeb_load_layers_async", "eeb_load_wait",
     "eeb_kv_configure_pages", "eeb_kv_reserve", "eeb_kv_release", "eeb_kv_pages",
     "eeb_debug_stamps", "eeb_debug_stamps_read", "eeb_debug_read_kv_span",
+    "eeb_weight_layout", "eeb_host_stage_layer", "eeb_host_stage_base", "eeb_load_layers_from",
+    "eeb_debug_stamps_cta",
 ]
+
+
+class _Layout(C.Structure):
+    _fields_ = [("layer_bytes", C.c_int64), ("base_bytes", C.c_int64), ("layer_off", C.c_int64 * 6),
+                ("base_off", C.c_int64 * 129)]
 
 _lib = None
 
@@ -116,6 +123,11 @@ def load_library() -> C.CDLL:
                                        C.c_void_p, C.c_void_p, C.c_void_p]
         lib.eeb_debug_bench_gemm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.POINTER(C.c_double)]
+        lib.eeb_weight_layout.argtypes = [C.c_void_p, C.c_int, C.POINTER(_Layout)]
+        lib.eeb_host_stage_layer.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
+        lib.eeb_host_stage_base.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
+        lib.eeb_load_layers_from.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64]
+        lib.eeb_debug_stamps_cta.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         lib.eeb_debug_stamps.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_debug_stamps_read.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         lib.eeb_profile_enable.argtypes = [C.c_void_p, C.c_int]
@@ -223,6 +235,12 @@ def to_bf16_bits(a: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
     u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
     return u.astype(np.uint16)
+
+
+def _as_dtype_bytes(t, dtype: int) -> np.ndarray:
+    """f32 values -> raw bytes of the model dtype (bf16: round to nearest even)."""
+    a = np.ascontiguousarray(t, np.float32).ravel()
+    return (to_bf16_bits(a) if dtype == BF16 else a).view(np.uint8)
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:
@@ -429,6 +447,46 @@ class Context:
         _check(self.lib.eeb_debug_bench_gemm(self.h, tier, n, k, batch, iters, C.byref(ms)))
         return ms.value
 
+    # -- caller-supplied weights (eeb_weight_layout / eeb_host_stage_* / eeb_load_layers_from)
+    def weight_layout(self, model: int) -> dict:
+        lo = _Layout()
+        _check(self.lib.eeb_weight_layout(self.h, model, C.byref(lo)))
+        n = len(self.models[model].exit_layers)
+        return {"layer_bytes": lo.layer_bytes, "base_bytes": lo.base_bytes, "layer_off": list(lo.layer_off),
+                "base_off": list(lo.base_off)[:1 + 2 * n]}
+
+    def pack_layer(self, model: int, attn_norm, mlp_norm, wqkv, wo, wup, wdown) -> np.ndarray:
+        """One layer's tensors (f32 arrays of the documented shapes) packed into
+        the eeb.h host layout (norm gains f32, matrices in the model dtype)."""
+        desc, lo = self.models[model], self.weight_layout(model)
+        buf = np.zeros(lo["layer_bytes"], np.uint8)
+        for off, t, norm in zip(lo["layer_off"], (attn_norm, mlp_norm, wqkv, wo, wup, wdown),
+                                (True, True, False, False, False, False)):
+            b = _as_dtype_bytes(t, 0 if norm else desc.dtype)
+            buf[off:off + b.size] = b
+        return buf
+
+    def pack_base(self, model: int, embedding, heads, head_norms) -> np.ndarray:
+        desc, lo = self.models[model], self.weight_layout(model)
+        buf = np.zeros(lo["base_bytes"], np.uint8)
+        parts = [(embedding, desc.dtype)] + [(h, desc.dtype) for h in heads] + [(g, 0) for g in head_norms]
+        for off, (t, dt) in zip(lo["base_off"], parts):
+            b = _as_dtype_bytes(t, dt)
+            buf[off:off + b.size] = b
+        return buf
+
+    def host_stage_layer(self, model: int, layer: int, packed: np.ndarray) -> None:
+        packed = np.ascontiguousarray(packed, np.uint8)
+        _check(self.lib.eeb_host_stage_layer(self.h, model, layer, packed.ctypes.data, packed.size))
+
+    def host_stage_base(self, model: int, packed: np.ndarray) -> None:
+        packed = np.ascontiguousarray(packed, np.uint8)
+        _check(self.lib.eeb_host_stage_base(self.h, model, packed.ctypes.data, packed.size))
+
+    def load_layers_from(self, model: int, first: int, last: int, packed: np.ndarray) -> None:
+        packed = np.ascontiguousarray(packed, np.uint8)
+        _check(self.lib.eeb_load_layers_from(self.h, model, first, last, packed.ctypes.data, packed.size))
+
     def stamps(self, max_launches: int) -> None:
         """In-graph launch timeline of every later decode step (0 = off)."""
         _check(self.lib.eeb_debug_stamps(self.h, int(max_launches)))
@@ -441,6 +499,12 @@ class Context:
         buf = C.create_string_buffer(n)
         _check(self.lib.eeb_debug_stamps_read(self.h, buf, n))
         return json.loads(buf.value.decode())["launches"]
+
+    def stamps_cta(self, launch: int, n: int) -> np.ndarray:
+        """[n, 3] per-CTA (start, end, wait) ns of one launch of the last stamped step."""
+        a = np.zeros((3, n), np.int64)
+        _check(self.lib.eeb_debug_stamps_cta(self.h, launch, a[0].ctypes.data, a[1].ctypes.data, a[2].ctypes.data, n))
+        return a.T
 
     def profile_enable(self, on: bool) -> None:
         _check(self.lib.eeb_profile_enable(self.h, 1 if on else 0))

@@ -20,7 +20,7 @@ CATS = ("layer_gemm", "attention", "exit_head", "norm", "other")
 
 
 def kernel_kind(name: str) -> str:
-    for k in ("gemm_tc", "gemm_cc", "attention_mma", "attention_pipe", "attention_prefill", "attention_kernel",
+    for k in ("gemm_tc", "gemm_cc", "attention_dec", "attention_mma", "attention_pipe", "attention_prefill", "attention_kernel",
               "kv_append", "residual_norm", "plane_sum", "act_kernel", "decide", "gather_rows", "finalize",
               "head_reduce", "embed", "mark_depth"):
         if k in name:
@@ -38,8 +38,14 @@ def analyse(launches: list[dict]) -> dict:
             rows.append({**l, "crit_ns": 0, "busy_ns": 0})
             continue
         crit = max(0, l["end_ns"] - last)
+        w = l.get("wait_ns", -1)
+        # wait stamped (kernels that record it): launch/flush latency after the
+        # predecessor's end, and the work after the wait returned
+        lat = w - last if w >= 0 else -1
+        work = l["end_ns"] - w if w >= 0 else -1
         last = max(last, l["end_ns"])
-        rows.append({**l, "kind": kernel_kind(l["kernel"]), "crit_ns": crit, "busy_ns": l["end_ns"] - l["start_ns"]})
+        rows.append({**l, "kind": kernel_kind(l["kernel"]), "crit_ns": crit, "busy_ns": l["end_ns"] - l["start_ns"],
+                     "lat_ns": lat, "work_ns": work})
     span = last - t0
     cats = {}
     for r in rows:
@@ -67,10 +73,13 @@ def run(ctx, step, n_steps: int, max_launches: int = 1024) -> dict:
     assert all(len(p["launches"]) == n for p in per), "launch list changed between stamped steps"
     crit = np.mean([[r["crit_ns"] for r in p["launches"]] for p in per], axis=0)
     busy = np.mean([[r["busy_ns"] for r in p["launches"]] for p in per], axis=0)
+    lat = np.mean([[r["lat_ns"] for r in p["launches"]] for p in per], axis=0)
+    work = np.mean([[r["work_ns"] for r in p["launches"]] for p in per], axis=0)
     span = float(np.mean([p["span_ns"] for p in per]))
     launches = [{"kernel": r.get("kind", r["kernel"]), "cat": r["cat"], "ctas": r["ctas"],
-                 "crit_us": float(c) / 1e3, "busy_us": float(b) / 1e3}
-                for r, c, b in zip(per[0]["launches"], crit, busy)]
+                 "crit_us": float(c) / 1e3, "busy_us": float(b) / 1e3,
+                 **({"lat_us": float(la) / 1e3, "work_us": float(wo) / 1e3} if r["lat_ns"] >= 0 else {})}
+                for r, c, b, la, wo in zip(per[0]["launches"], crit, busy, lat, work)]
     cats = {}
     for l in launches:
         c = cats.setdefault(l["cat"], {"crit_ms": 0.0, "busy_ms": 0.0, "launches": 0})
@@ -89,6 +98,7 @@ def table(tl: dict, top: int = 0) -> str:
     if top:
         out.append("  launches (crit / busy us):")
         for i, l in enumerate(tl["launches"][:top]):
+            extra = (f"  (wait-after-prev {l['lat_us']:6.2f}, work {l['work_us']:6.2f})" if "lat_us" in l else "")
             out.append(f"    {i:4d} {l['kernel']:18s} {l['cat']:11s} ctas={l['ctas']:5d} "
-                       f"crit {l['crit_us']:7.2f}  busy {l['busy_us']:7.2f}")
+                       f"crit {l['crit_us']:7.2f}  busy {l['busy_us']:7.2f}{extra}")
     return "\n".join(out)

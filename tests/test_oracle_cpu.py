@@ -298,3 +298,50 @@ def test_biased_exit_heads_reproduce_stated_coverage():
     frac = first / d.vocab
     assert abs(frac - d.coverage()[0]) < 0.05, frac  # 73 % at the first head (FIXTURES.md:47-55)
     o.close()
+
+
+def test_kv_import_reproduces_the_oracles_own_state():
+    """orc_write_kv (the bench-config parity test seeds the oracle from the
+    GPU's prefilled KV): an oracle seeded with another oracle's KV takes the
+    same decode step bit for bit."""
+    for desc in (eeb.PRESETS["tiny"], eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, name="tiny-bf16")):
+        d = desc.replace(max_slots=3, max_seq_len=16)
+        a, b = OracleModel(d), OracleModel(d)
+        a.load(d.num_layers)
+        b.load(d.num_layers)
+        rng = np.random.default_rng(5)
+        slots = np.arange(3)
+        for p in range(4):
+            a.decode_step(0, eeb.FULL_DEPTH, 0.7, slots, rng.integers(0, d.vocab, 3), np.full(3, p))
+        hd = d.n_kv_heads * d.head_dim
+        for layer in range(1, d.num_layers + 1):
+            for s in range(3):
+                kv = [a.read_kv(layer, s, p) for p in range(4)]
+                b.write_kv(layer, s, 0, np.stack([x[0] for x in kv]), np.stack([x[1] for x in kv]))
+                assert np.array_equal(b.read_kv(layer, s, 2)[0], kv[2][0])
+        toks = rng.integers(0, d.vocab, 3)
+        for policy in (eeb.INTROSPECTIVE, eeb.PROFILE):
+            ra = a.decode_step(0, policy, 0.7, slots, toks, np.full(3, 4))
+            rb = b.decode_step(0, policy, 0.7, slots, toks, np.full(3, 4))
+            for k in ("exit_layer", "token_id", "confidence", "logprob", "hist", "head_confidence"):
+                assert np.array_equal(ra[k], rb[k]), k
+        assert hd == a.read_kv(1, 0, 0)[0].size
+        a.close()
+        b.close()
+
+
+def test_synthetic_kv_fill_is_deterministic_and_rounded():
+    d = eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, max_slots=2, max_seq_len=16)
+    a, b = OracleModel(d), OracleModel(d)
+    a.fill_kv_synthetic(1, 10, 3)
+    b.fill_kv_synthetic(1, 10, 3)
+    k1, v1 = a.read_kv(5, 1, 7)
+    k2, v2 = b.read_kv(5, 1, 7)
+    assert np.array_equal(k1, k2) and np.array_equal(v1, v2)
+    assert np.all(np.abs(k1) <= 1) and np.abs(k1).max() > 0
+    assert np.array_equal(eeb.bf16_round(k1), k1)  # bf16 model: values on the bf16 grid
+    assert not np.array_equal(k1, v1)
+    with pytest.raises(RuntimeError):
+        a.fill_kv_synthetic(2, 4)
+    a.close()
+    b.close()

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--depth", type=int, default=6)
     ap.add_argument("--top", type=int, default=0)
     ap.add_argument("--json", default="")
+    ap.add_argument("--cta", default="", help="launch indices whose per-CTA stamps to summarise, e.g. 2,3,4")
     args = ap.parse_args()
     import torch
 
@@ -64,6 +65,27 @@ def main():
     e1.synchronize()
     plain_ms = e0.elapsed_time(e1) / args.steps
     tl = timeline.run(ctx, step, args.steps)
+    if args.cta:
+        # one more stamped step, then per-CTA start / wait / end of the chosen launches
+        ctx.stamps(1024)
+        step(0)
+        ctx.synchronize()
+        step(1)
+        rows = ctx.stamps_read()
+        prev_end = 0
+        for i, l in enumerate(rows):
+            if str(i) in args.cta.split(","):
+                c = ctx.stamps_cta(i, min(l["ctas"], 2048)) / 1e3
+                c = c[c[:, 0] >= 0]
+                q = lambda v: " ".join(f"{x:7.2f}" for x in np.percentile(v, [0, 10, 50, 90, 100]))
+                print(f"launch {i} {timeline.kernel_kind(l['kernel'])} ctas={len(c)} (us after previous launch's end;"
+                      f" percentiles 0/10/50/90/100)")
+                print(f"   start {q(c[:, 0] - prev_end / 1e3)}")
+                if (c[:, 2] >= 0).any():
+                    print(f"   wait  {q(c[c[:, 2] >= 0][:, 2] - prev_end / 1e3)}")
+                print(f"   end   {q(c[:, 1] - prev_end / 1e3)}")
+            prev_end = max(prev_end, l["end_ns"])
+        ctx.stamps(0)
     print(f"unstamped graph steps: {plain_ms * 1e3:.1f} us/step (CUDA events, back to back)")
     print(timeline.table(tl, args.top))
     if args.json:
