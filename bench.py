@@ -174,6 +174,9 @@ def workload_name(args, desc):
     if desc.name.startswith("opt-1.3b") and args.policy == "introspective":
         return ("C2: OPT-1.3B-shape early-exit decode step, exits " + "/".join(map(str, desc.exit_layers)) +
                 ", introspective (earliest confident head, survivors compacted), teacher-forced synthetic tokens")
+    if desc.name.startswith("llama2-70b") and args.tp > 1:
+        return (f"C5: Llama2-70B-shape tensor-parallel over {args.tp} GPUs, greedy first-{args.depth}-layer "
+                f"loading, flat decode at depth {args.depth}, teacher-forced synthetic tokens")
     if desc.name.startswith("codellama-34b") and args.policy == "flat":
         return (f"C4: CodeLlama-34B-shape greedy first-{args.depth}-layer loading, flat decode at depth "
                 f"{args.depth} (observation_for_depth), teacher-forced synthetic tokens")
@@ -188,7 +191,9 @@ def workload_config(args, desc):
             "context": f"{args.prompt}..{args.prompt + args.warmup + args.steps - 1} (timed steps: "
                        f"{args.prompt + args.warmup}..{args.prompt + args.warmup + args.steps - 1})",
             "th": args.th, "policy": args.policy,
-            "parallelism": f"replicas x{args.gpus} (requests sharded, no data-path collective)",
+            "parallelism": (f"tp{args.tp} (Megatron shards; NCCL all-reduce of row-parallel partials and "
+                            f"all-gather of vocab-parallel head partials inside the step)" if args.tp > 1 else
+                            f"replicas x{args.gpus} (requests sharded, no data-path collective)"),
             "l2": "inputs larger than L2 (GBs of weights streamed per step > 126 MB L2)"}
 
 
@@ -197,36 +202,59 @@ def workload_config(args, desc):
 # ----------------------------------------------------------------------------
 def batch_sweep(ctx, eeb, desc, args, stream, batches=(1, 2, 4, 16, 32, 64, 128, 256), n_steps=10):
     """The metric is 'EE decode tokens/s vs batch': the same workload at each
-    batch (own model instance with a 256-slot KV pool, prompts prefilled)."""
+    batch (own model instance with a 256-slot KV pool, prompts prefilled),
+    with the layer-GEMM and exit-head fractions of the HBM roofline per batch
+    from the in-graph launch timeline of that batch's steps."""
     import torch
+
+    from paper_2504_10724_b200 import timeline
 
     P = args.prompt
     d = desc.replace(max_slots=max(batches), max_seq_len=P + 100, name=desc.name + "-sweep")
     m = ctx.register(d)
-    ctx.load_layers(m, d.num_layers)
     policy = {"introspective": eeb.INTROSPECTIVE, "flat": eeb.FLAT}.get(args.policy, eeb.INTROSPECTIVE)
     depth = args.depth if policy == eeb.FLAT else 0
+    run_layers = depth if policy == eeb.FLAT else d.num_layers
+    ctx.load_layers(m, run_layers)  # greedy first-k loading: only the layers the step runs
+    hbm = float(peaks()[0]["hbm_gbs"])
     rng = np.random.default_rng(77)
     dev = torch.device("cuda")
     out = []
     for B in batches:
         slots = np.arange(B, dtype=np.int32)
-        ctx.prefill(m, d.num_layers, slots, list(rng.integers(0, d.vocab, (B, P)).astype(np.int32)))
+        ctx.prefill(m, run_layers, slots, list(rng.integers(0, d.vocab, (B, P)).astype(np.int32)))
         toks = torch.from_numpy(rng.integers(0, d.vocab, (n_steps + 3, B)).astype(np.int32)).to(dev)
         pos = torch.from_numpy(np.stack([np.full(B, P + k, np.int32) for k in range(n_steps + 3)])).to(dev)
         sl = torch.from_numpy(slots).to(dev)
         torch.cuda.synchronize()
-        for k in range(3):
+
+        def one(k):
             ctx.decode_step_device(m, depth, policy, args.th, B, sl.data_ptr(), toks[k].data_ptr(), pos[k].data_ptr())
+
+        for k in range(3):
+            one(k)
         ctx.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for k in range(3, n_steps + 3):
-            ctx.decode_step_device(m, depth, policy, args.th, B, sl.data_ptr(), toks[k].data_ptr(), pos[k].data_ptr())
+            one(k)
         e1.record(stream)
         e1.synchronize()
         ms = e0.elapsed_time(e1) / n_steps
-        out.append({"batch": B, "ms_per_step": ms, "tokens_per_s": B / (ms / 1000.0)})
+        row = {"batch": B, "ms_per_step": ms, "tokens_per_s": B / (ms / 1000.0)}
+        try:
+            tl = timeline.run(ctx, lambda k: one(3 + k % n_steps), 2)
+            g_ms = sum(l["crit_us"] for l in tl["launches"] if l["cat"] == "layer_gemm") / 1e3
+            h_ms = sum(l["crit_us"] for l in tl["launches"]
+                       if l["cat"] == "exit_head" and l["kernel"] in ("gemm_tc", "gemm_cc")) / 1e3
+            heads = len(tl and [l for l in tl["launches"] if l["cat"] == "exit_head" and l["kernel"] == "gemm_tc"])
+            if g_ms > 0:
+                row["layer_gemm_frac"] = gemm_bytes_per_step(d, B, run_layers) / (g_ms / 1e3) / 1e9 / hbm
+            if h_ms > 0 and heads:
+                row["exit_head_frac"] = head_bytes(d, B) * heads / (h_ms / 1e3) / 1e9 / hbm
+        except Exception as e:  # per-batch roofline is extra information
+            row["roofline_error"] = repr(e)[:120]
+        out.append(row)
     ctx.evict(m)
     return out
 
@@ -334,6 +362,14 @@ def parity_sample(ctx, m, desc, eeb, args, policy, depth, toks_h, pos_h, e2e_out
                    "step from the GPU's prompt KV; bf16 bar: token agreement >= 0.99"}
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def run_eeb(args, desc):
     import torch
 
@@ -365,7 +401,21 @@ def run_eeb(args, desc):
               "full_depth": eeb.FULL_DEPTH}[args.policy]
     depth = args.depth if policy == eeb.FLAT else 0
     desc = desc.replace(max_slots=B, max_seq_len=P + 100)
+    tp = args.tp
+    if tp > 1:
+        # C5: one Megatron shard per rank (column-parallel QKV / up, row-parallel
+        # O / down + NCCL all-reduce, vocab-parallel heads + all-gather); every
+        # rank serves the same B rows
+        if tp != world:
+            raise SystemExit(f"--tp {tp} needs exactly {tp} ranks (got {world})")
+        desc = desc.replace(tp_size=tp, tp_rank=rank)
+    # rows served per step by the whole job: replicas add rows, a TP group does not
+    job_rows = B if tp > 1 else world * B
     ctx = eeb.Context(local)
+    if tp > 1:
+        uid = [eeb.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], world, rank)
     ctx.set_gemm_tier(args.tier)
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
@@ -384,7 +434,7 @@ def run_eeb(args, desc):
     ctx.prefill(m, desc.num_layers, slots, list(prompts))
     pf_s = max_over_ranks(time.perf_counter() - t_pf)
     prefill = {"tokens_per_gpu": B * P, "depth": desc.num_layers, "ms": 1000.0 * pf_s,
-               "tokens_per_s": world * B * P / pf_s, "ttft_ms": 1000.0 * pf_s,
+               "tokens_per_s": job_rows * P / pf_s, "ttft_ms": 1000.0 * pf_s,
                "how": "eeb_prefill of the batch's prompts (host tokens, H2D + chunked passes), wall clock "
                       "around the blocking call, max over ranks"}
 
@@ -442,7 +492,7 @@ def run_eeb(args, desc):
     hist_acc = hist_all[args.warmup:].sum(dim=0)
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms_local)
-    value = world * B / (ms / 1000.0)
+    value = job_rows / (ms / 1000.0)
 
     # ---- in-graph launch timeline of the same steps (eeb_debug_stamps) ---------
     # Every kernel of the captured PDL graph stamps its first-CTA start and
@@ -514,12 +564,12 @@ def run_eeb(args, desc):
         e2e_outs.append(ctx.decode_step(m, depth, policy, args.th, slots, toks_h[k], pos_h[k]))
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     parity = None
-    if rank == 0 and not args.no_parity:
+    if rank == 0 and not args.no_parity and tp == 1:
         try:
             parity = parity_sample(ctx, m, desc, eeb, args, policy, depth, toks_h, pos_h, e2e_outs)
         except Exception as e:  # reported, never fatal for the headline line
             parity = {"error": repr(e)[:200]}
-    e2e_value = world * B * args.steps / e2e_s
+    e2e_value = job_rows * args.steps / e2e_s
     h2d = 3 * B * 4
     d2h = B * (4 + 4 + 4 + 4 + 1 + 1) + ne * 8 + 8 + 8
 
@@ -528,7 +578,7 @@ def run_eeb(args, desc):
 
     prof_counters = replicas.ProfileCounters(desc.exit_layers, hist=hist_acc.cpu().numpy())
     prof_counters.tokens = int(prof_counters.hist.sum())
-    if world > 1:
+    if world > 1 and tp == 1:  # (a TP group serves the same rows on every rank: nothing to merge)
         uid = [eeb.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.nccl_init(uid[0], world, rank)
@@ -539,32 +589,75 @@ def run_eeb(args, desc):
     # ---- greedy loader: real pinned H2D of a second model's
     # first layers on the load stream, overlapped with this model's decode steps
     loader = sweep = None
-    if rank == 0 and world == 1 and not args.no_secondary:
+    if rank == 0 and world == 1 and (args.sweep or not args.no_secondary):
         try:
             sweep = batch_sweep(ctx, eeb, desc, args, stream)
         except Exception as e:  # reported, never fatal for the headline line
             sweep = {"error": repr(e)[:200]}
+    if rank == 0 and world == 1 and not args.no_secondary:
         try:
             loader = measure_loader(ctx, m, eeb, step, args, stream)
         except Exception as e:  # reported, never fatal for the headline line
             loader = {"error": repr(e)[:200]}
 
     ctx.close()
-    secondary = None
-    if rank == 0 and world == 1 and not args.no_secondary:
-        # C4 beside the headline: the 34B shape the north star's scaling target is
-        # quoted on (greedy first-12 layers, flat decode), measured in its own process.
-        cmd = [sys.executable, str(ROOT / "bench.py"), "--model", "codellama-34b", "--policy", "flat", "--depth", "12",
-               "--batch", str(args.batch), "--steps", "10", "--warmup", "3", "--no-cpu-baseline", "--no-secondary"]
+
+    def child_bench(extra: list, timeout: float):
+        """bench.py for another workload in a child process per rank (every
+        rank spawns one; under torchrun the children form their own process
+        group on a fresh port).  Rank 0 returns the child's JSON line."""
+        env = dict(os.environ)
+        if world > 1:
+            port = [_free_port() if rank == 0 else None]
+            dist.broadcast_object_list(port, src=0)
+            env["MASTER_PORT"] = str(port[0])
+            env.pop("TORCHELASTIC_USE_AGENT_STORE", None)  # the child's rank 0 hosts its own store
+        cmd = [sys.executable, str(ROOT / "bench.py"), "--gpus", str(world), *extra,
+               "--no-cpu-baseline", "--no-secondary", "--no-parity"]
         try:
-            out = subprocess.run(cmd, capture_output=True, text=True, timeout=900).stdout.strip().splitlines()
-            d = json.loads(out[-1])
-            secondary = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
-                         "ms_per_step": d["ms_per_step"], "batch": args.batch,
-                         "layer_gemm_roofline_frac": d["roofline"]["frac"], "step_roofline": d["step_roofline"],
-                         "exit_head_roofline_frac": (d.get("exit_head_roofline") or {}).get("frac")}
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+            lines = r.stdout.strip().splitlines()
+            if rank != 0:
+                return None
+            if r.returncode != 0 or not lines:
+                return {"error": f"rc={r.returncode}: " + (r.stderr.strip().splitlines() or [""])[-1][:200]}
+            return json.loads(lines[-1])
         except Exception as e:  # reported, never fatal for the headline line
-            secondary = {"error": repr(e)[:200]}
+            return {"error": repr(e)[:200]} if rank == 0 else None
+        finally:
+            barrier()
+
+    secondary = None
+    if not args.no_secondary and tp == 1:
+        # C4 beside the headline at every N: the 34B shape the north star's
+        # scaling target (>= 6x from 1 to 8 GPUs) is quoted on — greedy first-12
+        # layers (choose_depth, test_policy.cpp:322-327), flat decode, requests
+        # sharded over the ranks; with its batch sweep at N = 1.
+        d = child_bench(["--model", "codellama-34b", "--policy", "flat", "--depth", "12", "--batch", str(args.batch),
+                         "--steps", "10", "--warmup", "3"] + (["--sweep"] if world == 1 else []), 1200)
+        if d is not None and "error" not in d:
+            secondary = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
+                         "n_gpus": d["n_gpus"], "ms_per_step": d["ms_per_step"], "batch_per_gpu": args.batch,
+                         "e2e": d["e2e"], "layer_gemm_roofline_frac": d["roofline"]["frac"],
+                         "step_roofline": d["step_roofline"],
+                         "exit_head_roofline_frac": (d.get("exit_head_roofline") or {}).get("frac"),
+                         "clocks": d.get("clocks"), **({"batch_sweep": d["batch_sweep"]} if "batch_sweep" in d else {})}
+        else:
+            secondary = d
+    c5 = None
+    if not args.no_secondary and tp == 1 and world > 1:
+        # C5 (BASELINE configs[4]): Llama2-70B shape tensor-parallel over the
+        # launched ranks (NCCL inside the step), flat at the greedy depth 10
+        # (test_policy.cpp:328)
+        d = child_bench(["--model", "llama2-70b", "--tp", str(world), "--policy", "flat", "--depth", "10",
+                         "--batch", str(args.batch), "--steps", "10", "--warmup", "3"], 1500)
+        if d is not None and "error" not in d:
+            c5 = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"], "n_gpus": d["n_gpus"],
+                  "ms_per_step": d["ms_per_step"], "batch": args.batch, "e2e": d["e2e"],
+                  "layer_gemm_roofline_frac": d["roofline"]["frac"], "step_roofline": d["step_roofline"],
+                  "kernel_ms_per_step": d.get("kernel_ms_per_step")}
+        else:
+            c5 = d
 
     c3 = None
     serve_c3 = ROOT / "paper_2504_10724_b200" / "_build" / "serve_c3"
@@ -603,6 +696,8 @@ def run_eeb(args, desc):
                 "path": "per-op kernel chain (CUDA graph, PDL)"}
         if secondary is not None:
             line["secondary_c4"] = secondary
+        if c5 is not None:
+            line["secondary_c5"] = c5
         if c3 is not None:
             line["secondary_c3"] = c3
         if loader is not None:
@@ -632,6 +727,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of sampled e2e rows")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 (34B) line attached at N=1")
     ap.add_argument("--tier", type=int, default=0, help="0 auto, 1 CUDA-core GEMV, 2 tcgen05 GEMMs")
+    ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group = the launched ranks (C5)")
+    ap.add_argument("--sweep", action="store_true", help="batch sweep of this workload with per-batch roofline")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -89,7 +89,9 @@ public:
     /// Paged KV pool for models registered after this call (eeb_kv_configure_pages):
     /// n_pages pages of page_size positions instead of max_slots x max_seq_len
     /// (bf16 models with head_dim 64 or 128; other models keep the slot pool).
-    void set_kv_pages(int page_size, int n_pages) {
+    /// n_pages = 0: enough pages for every slot the engine sized from the
+    /// memory model (max_slots x ceil(max_seq_len / page_size)).
+    void set_kv_pages(int page_size, int n_pages = 0) {
         kv_page_ = page_size;
         kv_pages_ = n_pages;
     }
@@ -123,7 +125,10 @@ public:
         // attention kernels walk page tables); others keep the slot pool
         const int hd = a.n_heads > 0 ? a.d_model / a.n_heads : 0;
         if (kv_page_ > 0 && a.dtype == EEB_BF16 && (hd == 64 || hd == 128))
-            throw_if_error(eeb_kv_configure_pages(ctx_, h, kv_page_, kv_pages_), "eeb_kv_configure_pages");
+            throw_if_error(eeb_kv_configure_pages(ctx_, h, kv_page_,
+                                                  kv_pages_ > 0 ? kv_pages_
+                                                                : max_slots * ((max_seq_len + kv_page_ - 1) / kv_page_)),
+                           "eeb_kv_configure_pages");
         if (host_tier_) throw_if_error(eeb_host_stage(ctx_, h, spec.num_layers), "eeb_host_stage");
     }
 

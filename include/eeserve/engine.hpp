@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <optional>
 #include <string>
@@ -59,6 +60,10 @@ struct EngineConfig {
     // in-flight requests drain first, so actions still apply at request
     // boundaries (engine.hpp:143).  max_batch = 1 is the reference's loop.
     bool continuous = false;
+    // Teacher-forced input-token law (prompt and decode inputs); unset =
+    // synthetic_token(token_seed, ...).  serve_c3's drift workload picks
+    // tokens by their synthetic difficulty so breaches happen on the GPU.
+    std::function<int32_t(std::int64_t request_id, int position, int vocab)> token_fn;
 };
 
 struct RequestTiming {  // ↔ the request's TTFT (engine.hpp:333-337) and its tokens' TPOT
@@ -106,7 +111,12 @@ public:
     BatchedEngine(const ModelRepository& repo, DecodeBackend& backend, EngineConfig cfg)
         : repo_(repo), be_(backend), cfg_(std::move(cfg)) {}
 
-    EngineReport run(const std::vector<RequestSpec>& reqs) {
+    /// Validate the configuration, pick the candidates and register them with
+    /// the backend (device KV pool sized from the memory model; the host tier
+    /// stages their layers).  run() calls it when the caller did not, so a
+    /// caller may time setup and serving separately.
+    void prepare() {
+        if (prepared_) return;
         validate_memory_config(cfg_.mem);
         validate_policy_config(cfg_.policy);
         if (cfg_.max_batch < 1) throw ValidationError("engine: max_batch must be at least 1");
@@ -118,7 +128,34 @@ public:
                 throw ValidationError("mode model '" + cfg_.mode.model + "' is not in the repository");
             candidates_ = {cfg_.mode.model};
         }
-        for (const auto& id : candidates_) be_.register_model(repo_.at(id), cfg_.max_batch, cfg_.max_seq_len);
+        for (const auto& id : candidates_) {
+            const int slots = slots_for(repo_.at(id));
+            slots_[id] = slots;
+            be_.register_model(repo_.at(id), slots, cfg_.max_seq_len);
+        }
+        prepared_ = true;
+    }
+
+    /// Decode slots (the device KV pool's rows) for a model: the memory
+    /// model's batch capacity at full depth with only this model resident
+    /// (max_batch_size over kv_budget_bytes, memory_model.hpp:53-72), capped
+    /// by max_batch; at least 1 (load_for_eval raises CapacityError when not
+    /// even one sequence fits, engine.hpp:231-233).
+    int slots_for(const ModelSpec& spec) const {
+        MemoryState alone;
+        alone.loaded_depth[spec.id] = spec.num_layers;
+        const int cap =
+            max_batch_size(spec, spec.num_layers, kv_budget_bytes(cfg_.mem, alone, repo_), cfg_.mem.max_seq_len);
+        return std::max(1, std::min(cfg_.max_batch, cap));
+    }
+    int slots(const std::string& id) const {
+        auto it = slots_.find(id);
+        return it == slots_.end() ? cfg_.max_batch : it->second;
+    }
+
+    EngineReport run(const std::vector<RequestSpec>& reqs) {
+        prepare();
+        const PolicyConfig& pol = cfg_.policy;
         if (reqs.empty()) return finish();
         if (cfg_.mode.kind == Mode::helios) {
             since_eval_ = pol.ri;  // evaluate before serving anything (engine.hpp:130)
@@ -140,7 +177,7 @@ public:
                 serve_continuous(reqs, serving_, depth_, tp);
                 continue;
             }
-            const size_t n = std::min<size_t>(cfg_.max_batch, reqs.size() - cursor_);
+            const size_t n = std::min<size_t>(slots(serving_), reqs.size() - cursor_);
             std::vector<const RequestSpec*> batch;
             for (size_t i = 0; i < n; ++i) batch.push_back(&reqs[cursor_ + i]);
             cursor_ += n;
@@ -154,6 +191,8 @@ private:
     const ModelRepository& repo_;
     DecodeBackend& be_;
     EngineConfig cfg_;
+    bool prepared_ = false;
+    std::map<std::string, int> slots_;
     std::vector<std::string> candidates_;
     MemoryState mem_;
     std::string serving_;
@@ -168,6 +207,11 @@ private:
     std::int64_t unchanged_ = 0, unchanged_known_ = 0;
     double pending_stall_s_ = 0.0;  // loads charged to the next batch's TTFT (engine.hpp:205-207, :336)
     double clock_ = 0.0;            // serving clock of the event log (s)
+
+    int32_t token(std::int64_t request_id, int position, int vocab) const {
+        return cfg_.token_fn ? cfg_.token_fn(request_id, position, vocab)
+                             : synthetic_token(cfg_.token_seed, request_id, position, vocab);
+    }
 
     void emit(const char* kind, const JsonFields& f) {
         if (cfg_.record_events) rep_.events.push_back({clock_, kind, f.body()});
@@ -210,6 +254,8 @@ private:
             for (const auto& o : others) do_load(o, 0, "evict");
         }
         do_load(id, spec.num_layers, "eval");
+        if (max_batch_size(spec, spec.num_layers, kv_budget_bytes(cfg_.mem, mem_, repo_), cfg_.mem.max_seq_len) < 1)
+            throw CapacityError("cannot fit one sequence while profiling '" + id + "'");
     }
 
     void eval_cycle(const std::vector<RequestSpec>& reqs) {  // engine.hpp:243-278
@@ -226,7 +272,7 @@ private:
             const ModelSpec& spec = repo_.at(id);
             int served = 0;
             while (served < cfg_.policy.n_eval_requests && cursor_ < reqs.size()) {
-                const size_t n = std::min<size_t>({(size_t)cfg_.max_batch, reqs.size() - cursor_,
+                const size_t n = std::min<size_t>({(size_t)slots(id), reqs.size() - cursor_,
                                                    (size_t)(cfg_.policy.n_eval_requests - served)});
                 std::vector<const RequestSpec*> batch;
                 for (size_t i = 0; i < n; ++i) batch.push_back(&reqs[cursor_ + i]);
@@ -309,7 +355,7 @@ private:
                 pr.slots.push_back(i);
                 std::vector<int32_t> p(batch[i]->prompt_len);
                 for (int k = 0; k < batch[i]->prompt_len; ++k)
-                    p[k] = synthetic_token(cfg_.token_seed, batch[i]->request_id, k, vocab);
+                    p[k] = token(batch[i]->request_id, k, vocab);
                 pr.prompts.push_back(std::move(p));
             }
             prefill_s = be_.prefill(model, tp == TokenPolicy::flat ? depth : spec.num_layers, pr);
@@ -335,7 +381,7 @@ private:
                 if (t >= batch[i]->num_tokens) continue;
                 const int pos = batch[i]->prompt_len + t;
                 rows.slots.push_back(i);
-                rows.tokens.push_back(synthetic_token(cfg_.token_seed, batch[i]->request_id, pos, vocab));
+                rows.tokens.push_back(token(batch[i]->request_id, pos, vocab));
                 rows.positions.push_back(pos);
                 rows.request_ids.push_back(batch[i]->request_id);
                 rows.token_index.push_back(t);
@@ -390,7 +436,7 @@ private:
         };
         std::vector<Active> act;
         std::vector<int> free_slots;
-        for (int s = cfg_.max_batch - 1; s >= 0; --s) free_slots.push_back(s);  // lowest slot first
+        for (int s = slots(model) - 1; s >= 0; --s) free_slots.push_back(s);  // lowest slot first
         auto admissible = [&] {
             return cursor_ < reqs.size() && !pending_ &&
                    !(cfg_.mode.kind == Mode::helios && should_reassess(since_eval_, cfg_.policy));
@@ -426,7 +472,7 @@ private:
                     pr.slots.push_back(a.slot);
                     std::vector<int32_t> p(a.r->prompt_len);
                     for (int k = 0; k < a.r->prompt_len; ++k)
-                        p[k] = synthetic_token(cfg_.token_seed, a.r->request_id, k, vocab);
+                        p[k] = token(a.r->request_id, k, vocab);
                     pr.prompts.push_back(std::move(p));
                 }
                 prefill_s = be_.prefill(model, tp == TokenPolicy::flat ? depth : spec.num_layers, pr);
@@ -457,7 +503,7 @@ private:
             for (const auto& a : act) {
                 const int pos = a.r->prompt_len + a.t;
                 rows.slots.push_back(a.slot);
-                rows.tokens.push_back(synthetic_token(cfg_.token_seed, a.r->request_id, pos, vocab));
+                rows.tokens.push_back(token(a.r->request_id, pos, vocab));
                 rows.positions.push_back(pos);
                 rows.request_ids.push_back(a.r->request_id);
                 rows.token_index.push_back(a.t);

@@ -83,6 +83,25 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// L2 prefetch of this CTA's share of [p, p + bytes): the weights of the GEMM
+// that follows a latency-bound kernel (norm, attention), pulled into L2 while
+// that kernel runs so the GEMM streams them from L2.  One warp (the caller's
+// lanes) issues 16 KB bulk prefetches; no completion to wait for.
+__device__ __forceinline__ void l2_prefetch_share(const void* p, size_t bytes, int lane) {
+    if (!p || !bytes) return;
+    const size_t nct = (size_t)gridDim.x * gridDim.y;
+    const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    const size_t share = ((bytes + nct - 1) / nct + 255) & ~(size_t)255;
+    const size_t b0 = cta * share, b1 = b0 + share < bytes ? b0 + share : bytes;
+    constexpr size_t kPiece = 16384;
+    for (size_t o = b0 + (size_t)lane * kPiece; o < b1; o += 32 * kPiece) {
+        const uint32_t n = (uint32_t)((b1 - o < kPiece ? b1 - o : kPiece) & ~(size_t)15);
+        if (n)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const char*>(p) + o), "r"(n)
+                         : "memory");
+    }
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -135,6 +154,12 @@ struct StampScope {
 __device__ __forceinline__ void stamp_waited(const Stamp& s) {
     if (s.buf && threadIdx.x == 0)
         asm volatile("red.global.min.u64 [%0], %1;" ::"l"(stamp_cell(s) + 2 * s.end_off), "l"(gtimer()) : "memory");
+}
+// A kernel-specific midpoint (GEMM: accumulator complete), the latest over
+// CTAs: wait -> mark is the main loop, mark -> end the epilogue tail.
+__device__ __forceinline__ void stamp_mark(const Stamp& s) {
+    if (s.buf)
+        asm volatile("red.global.max.u64 [%0], %1;" ::"l"(stamp_cell(s) + 3 * s.end_off), "l"(gtimer()) : "memory");
 }
 // Host: the stamp for the next launch (defined in eeb_api.cu; buf null unless
 // the calling thread is recording a timeline).

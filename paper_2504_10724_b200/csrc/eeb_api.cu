@@ -135,7 +135,8 @@ struct Model {
     std::vector<int32_t> slot_npages;  // pages held per slot
     std::vector<int32_t> free_pages;   // LIFO free list
     bool table_dirty = false;
-    std::vector<std::array<uint8_t, 128>> k_maps, v_maps;  // bf16: per-layer TMA maps of the KV cache
+    std::vector<std::array<uint8_t, 128>> k_maps, v_maps;  // bf16: per-layer TMA maps of the KV cache (32-row boxes)
+    std::vector<std::array<uint8_t, 128>> k_maps8, v_maps8;  // the same with 8-row boxes (a pass's last chunk)
     // host tier + asynchronous loader state
     HostTier host;
     std::unique_ptr<PendingLoad> pending;
@@ -742,6 +743,7 @@ void stamp_reset(eeb_ctx* c) {
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.p, 0xFF, cells * 8, c->stream));
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + cells, 0, cells * 8, c->stream));
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + 2 * cells, 0xFF, cells * 8, c->stream));
+    EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + 3 * cells, 0, cells * 8, c->stream));
 }
 
 // Size the step workspace for `batch` rows of model m.  Buffers are shared by
@@ -959,6 +961,16 @@ const float* tp_allreduce(eeb_ctx* c, const Model& m, const float* planes_base, 
     return part;
 }
 
+// L2 prefetch of the next GEMM's weights from the latency-bound kernel before
+// it (attention -> O, mlp norm -> up, final norm -> next QKV); opt-in
+// EEB_L2PF_FUSED=1 — measured slower on C2 (1.473 vs 1.412 ms/step: issuing
+// the bulk prefetches delays the norm's own warps by ~3 us, more than the
+// GEMMs gain); the GEMMs' own pre-wait L2 prefetch (gemm_tc.cu) replaces it.
+bool l2pf_fused() {
+    static const bool on = std::getenv("EEB_L2PF_FUSED") && std::atoi(std::getenv("EEB_L2PF_FUSED")) != 0;
+    return on;
+}
+
 struct PlaneSet {
     const float* base;
     int planes;
@@ -1031,8 +1043,14 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         const size_t mk = (size_t)(l - 1) * m.shards + sh;
         a.k_map = m.k_maps.empty() ? nullptr : m.k_maps[mk].data();
         a.v_map = m.v_maps.empty() ? nullptr : m.v_maps[mk].data();
+        a.k_map8 = m.k_maps8.empty() ? nullptr : m.k_maps8[mk].data();
+        a.v_map8 = m.v_maps8.empty() ? nullptr : m.v_maps8[mk].data();
         a.num_sms = c->num_sms;
         a.kv_ready = kv_ready ? 1 : 0;
+        if (l2pf_fused() && pf_on) {
+            a.pf = static_cast<const char*>(W.wo.p) + (size_t)sh * D * m.dq_l * wb;
+            a.pf_bytes = (size_t)D * m.dq_l * wb;
+        }
         if (kv_ready) {
             launch_kv_append(a, s);
             count(c, kCatAttn, 1);
@@ -1056,7 +1074,8 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         Timer t(c, kCatNorm);
         if (!skip_cat("norm"))
             launch_residual_norm(d.dtype, o.base, o.planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
-                                 W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
+                                 W.mlp_norm.as<float>(), h, nullptr, nullptr, s, l2pf_fused() && pf_on ? W.wup.p : nullptr,
+                                 (size_t)m.up_l * D * wb);
         count(c, kCatNorm, 1);
     }
     static const bool act_unfused = std::getenv("EEB_ACT_UNFUSED") != nullptr;  // A/B
@@ -1227,9 +1246,13 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             void* o1 = g_next ? h_cur : c->hhead.p;
             const float* g2 = g_next ? g_head : nullptr;
             void* o2 = g_next && g_head ? c->hhead.p : nullptr;
+            // the next layer's QKV weights -> L2 during the norm (not before an
+            // exit head: its vocab-sized stream would evict them first)
+            const void* pf = l2pf_fused() && more && !exit_here && m.shards == 1 ? m.layers[l]->wqkv.p : nullptr;
             if (g1 && !skip_cat("norm"))
                 launch_residual_norm(d.dtype, planes_base, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
-                                     d.norm_eps, g1, o1, g2, o2, s);
+                                     d.norm_eps, g1, o1, g2, o2, s, pf,
+                                     (size_t)(m.dq_l + 2 * m.dkv_l) * D * m.wbytes);
             count(c, kCatNorm, 1);
         }
         while (head_at(hi, l)) {
@@ -1492,9 +1515,13 @@ void alloc_kv(eeb_ctx* c, Model& m, int page, int n_pages, bool paged) {
     EEB_CUDA(cudaMemsetAsync(m.v_cache.p, 0, m.v_cache.bytes, c->stream));
     m.k_maps.clear();
     m.v_maps.clear();
+    m.k_maps8.clear();
+    m.v_maps8.clear();
     if (d.dtype == EEB_BF16 && (m.head_dim == 64 || m.head_dim == 128) && gemm_tc_available()) {
         m.k_maps.resize((size_t)d.num_layers * m.shards);
         m.v_maps.resize((size_t)d.num_layers * m.shards);
+        m.k_maps8.resize((size_t)d.num_layers * m.shards);
+        m.v_maps8.resize((size_t)d.num_layers * m.shards);
         for (int l = 0; l < d.num_layers; ++l)
             for (int sh = 0; sh < m.shards; ++sh) {
                 const size_t off = ((size_t)l * m.kv_layer_elems + sh * m.kv_shard_elems) * 2;
@@ -1503,6 +1530,10 @@ void alloc_kv(eeb_ctx* c, Model& m, int page, int n_pages, bool paged) {
                                    n_pages * m.hkv_l, 32);
                 make_kv_tensor_map(m.v_maps[k].data(), static_cast<char*>(m.v_cache.p) + off, m.head_dim, page,
                                    n_pages * m.hkv_l, 32);
+                make_kv_tensor_map(m.k_maps8[k].data(), static_cast<char*>(m.k_cache.p) + off, m.head_dim, page,
+                                   n_pages * m.hkv_l, 8);
+                make_kv_tensor_map(m.v_maps8[k].data(), static_cast<char*>(m.v_cache.p) + off, m.head_dim, page,
+                                   n_pages * m.hkv_l, 8);
             }
     }
     m.h_table.assign((size_t)d.max_slots * m.pages_per_seq, paged ? -1 : 0);
@@ -2069,7 +2100,7 @@ eeb_status eeb_debug_stamps(eeb_ctx* c, int max_launches) {
         c->stamp_cap = max_launches;
         if (max_launches > 0) {
             c->stamp_buf.release();
-            c->stamp_buf.ensure((size_t)max_launches * kStampCtas * 3 * 8);
+            c->stamp_buf.ensure((size_t)max_launches * kStampCtas * 4 * 8);
         } else {
             c->stamp_buf.release();
         }
@@ -2082,18 +2113,19 @@ eeb_status eeb_debug_stamps_read(eeb_ctx* c, char* json_out, int64_t cap) {
         if (c->stamp_cap <= 0) throw Error(EEB_E_DOMAIN, "stamping is off (eeb_debug_stamps)");
         EEB_CUDA(cudaStreamSynchronize(c->stream));
         const size_t cells = (size_t)c->stamp_cap * kStampCtas;
-        std::vector<unsigned long long> h(3 * cells);
+        std::vector<unsigned long long> h(4 * cells);
         EEB_CUDA(cudaMemcpy(h.data(), c->stamp_buf.p, h.size() * 8, cudaMemcpyDeviceToHost));
         std::string j = "{\"launches\": [";
         unsigned long long t0 = ~0ull;
         for (size_t i = 0; i < c->stamp_last.first.size(); ++i)
             for (int k = 0; k < kStampCtas; ++k) t0 = std::min(t0, h[i * kStampCtas + k]);
         for (size_t i = 0; i < c->stamp_last.first.size(); ++i) {
-            unsigned long long st = ~0ull, en = 0, wt = ~0ull;
+            unsigned long long st = ~0ull, en = 0, wt = ~0ull, mk = 0;
             int ctas = 0;
             for (int k = 0; k < kStampCtas; ++k) {
                 const unsigned long long a = h[i * kStampCtas + k], b = h[cells + i * kStampCtas + k];
                 wt = std::min(wt, h[2 * cells + i * kStampCtas + k]);
+                mk = std::max(mk, h[3 * cells + i * kStampCtas + k]);
                 if (a != ~0ull) {
                     ++ctas;
                     st = std::min(st, a);
@@ -2106,9 +2138,10 @@ eeb_status eeb_debug_stamps_read(eeb_ctx* c, char* json_out, int64_t cap) {
             char buf[512];
             std::snprintf(buf, sizeof buf,
                           "%s{\"kernel\": \"%s\", \"cat\": \"%s\", \"start_ns\": %lld, \"end_ns\": %lld, "
-                          "\"wait_ns\": %lld, \"ctas\": %d}",
+                          "\"wait_ns\": %lld, \"mark_ns\": %lld, \"ctas\": %d}",
                           i ? ", " : "", name, cat >= 0 ? kCatNames[cat] : "?", ctas ? (long long)(st - t0) : -1LL,
-                          ctas ? (long long)(en - t0) : -1LL, wt != ~0ull ? (long long)(wt - t0) : -1LL, ctas);
+                          ctas ? (long long)(en - t0) : -1LL, wt != ~0ull ? (long long)(wt - t0) : -1LL,
+                          mk ? (long long)(mk - t0) : -1LL, ctas);
             j += buf;
         }
         j += "]}";

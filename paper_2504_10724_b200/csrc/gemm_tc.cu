@@ -165,6 +165,8 @@ struct TcParams {
     unsigned long long* trace;  // timing experiments: 8 globaltimer stamps per CTA (null = off)
     int dbg;                    // timing experiments: bit 0 = no plane stores (results wrong)
     int skip_dead;              // read n_active before the weight prefetch (skip it when 0)
+    int l2pf;                   // L2-prefetch the weight tiles beyond the smem stages before the PDL wait
+    int tma_out;                // split-K planes written by a TMA store of the smem-staged tile (tmap_o)
     Stamp st;                   // in-graph launch timeline (eeb_debug_stamps)
 };
 
@@ -188,7 +190,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
-                   TcParams p) {
+                   const __grid_constant__ CUtensorMap tmap_o, TcParams p) {
     StampScope stamp_scope(p.st);
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms.
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int hint = p.skip_dead ? *reinterpret_cast<const volatile int*>(p.n_active) : 1;
         prefetch_tmap(&tmap_w);
         prefetch_tmap(&tmap_x);
+        if (p.tma_out) prefetch_tmap(&tmap_o);
         for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
@@ -240,6 +243,15 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_expect_tx(full0 + 8 * i, stage_bytes);
             tma_load_2d(sa, &tmap_w, full0 + 8 * i, (kb0 + i) * kBK, m_tile * kBM, pol_w0);
         }
+        // the rest of this CTA's weight tiles -> L2, also before the wait: a
+        // CTA resident while a latency-bound predecessor (norm) runs streams
+        // its whole share then, and its later stages load from L2
+        if (p.l2pf && hint > 0)
+            for (int i = pre; i < nkb; ++i)
+                asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                                 reinterpret_cast<uint64_t>(&tmap_w)),
+                             "r"((kb0 + i) * kBK), "r"(m_tile * kBM)
+                             : "memory");
         pre_s = pre;
     }
     if (warp == 1) {
@@ -332,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (rows > 0) {
         mbar_wait(tfull, 0);
         tc_fence_after();
+        if (threadIdx.x == 64) stamp_mark(p.st);  // accumulator complete (timeline)
         EEB_STAMP(threadIdx.x == 64, 4);  // accumulator complete
         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
         if (p.head_tri && p.cs == 1) {
@@ -392,6 +405,39 @@ __global__ void __launch_bounds__(kThreads, 2)
                         if (n < p.N && c0 + j < lim)
                             p.act_out[(int64_t)(c0 + j) * p.N + n] = __float2bfloat16_rn(fmaxf(v[j], 0.f));
                 }
+            }
+        } else if (p.cs == 1 && p.tma_out) {
+            // Split-K plane through shared memory: the [rows][128] f32 tile is
+            // staged in the drained pipeline stages (thread = feature: each row
+            // is 32 consecutive floats per warp, conflict-free) and written by
+            // one TMA bulk tensor store — per-thread global stores of the
+            // same 32 KB cost ~2.4 us of the GEMM's tail (measured in the C2 step).
+            float* stg = reinterpret_cast<float*>(base_ptr);
+            const int f = quarter * 32 + lane;
+            const int lim = min(rows, p.bpad);
+            int c0 = 0;
+            for (; c0 + 32 <= p.bpad && c0 < lim; c0 += 32) {
+                float v[32];
+                tmem_ld32(taddr + (uint32_t)c0, v);  // warp-collective
+#pragma unroll
+                for (int j = 0; j < 32; ++j) stg[(c0 + j) * kBM + f] = v[j];
+            }
+            for (; c0 < lim; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) stg[(c0 + j) * kBM + f] = v[j];
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> TMA reads
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (threadIdx.x == 64) {
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmap_o)),
+                    "r"(m_tile * kBM), "r"(0), "r"(split), "r"(smem_u32(stg))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // written before the grid completes
             }
         } else if (p.cs == 1) {
             float* plane = p.part + (int64_t)split * p.split_stride;
@@ -721,8 +767,28 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.dbg = env_dbg;
     static const bool skip_dead = !std::getenv("EEB_SKIP_DEAD") || std::atoi(std::getenv("EEB_SKIP_DEAD")) != 0;
     p.skip_dead = skip_dead ? 1 : 0;
+    // measured slower on C2 (1.455 vs 1.412 ms/step: the prefetch stream slows the
+    // norm that runs beside it more than the GEMMs gain); opt-in EEB_TC_L2PF=1
+    static const int env_l2pf = std::getenv("EEB_TC_L2PF") ? std::atoi(std::getenv("EEB_TC_L2PF")) : 0;
+    p.l2pf = env_l2pf;
     const CUtensorMap mw = make_map(a.W, a.N, a.K, kBM);
     const CUtensorMap mx = make_map(a.X, a.max_rows, a.K, bpad);
+    // plane output map [planes][max_rows][N] f32, box 128 features x bpad rows
+    static const bool env_tma_out = !std::getenv("EEB_TC_TMA_OUT") || std::atoi(std::getenv("EEB_TC_TMA_OUT")) != 0;
+    CUtensorMap mo = mw;  // (unused unless tma_out)
+    p.tma_out = 0;
+    if (env_tma_out && !a.head_tri && !a.act_out && cs == 1 && a.out && (size_t)bpad * kBM * 4 <= (size_t)stages * stage_bytes &&
+        (a.plane_stride * 4) % 16 == 0 && ((size_t)a.N * 4) % 16 == 0) {
+        const cuuint64_t dims[3] = {(cuuint64_t)a.N, (cuuint64_t)a.max_rows, (cuuint64_t)(splits / cs)};
+        const cuuint64_t strides[2] = {(cuuint64_t)a.N * 4, (cuuint64_t)a.plane_stride * 4};
+        const cuuint32_t box[3] = {(cuuint32_t)kBM, (cuuint32_t)bpad, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode_fn()(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.out, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw Error(5, "cuTensorMapEncodeTiled (planes) failed: " + std::to_string((int)r));
+        p.tma_out = 1;
+    }
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
     p.cs = cs;
     EEB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -743,7 +809,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const bool force_cl = std::getenv("EEB_TC_CLUSTER_ATTR") != nullptr;
     cfg.numAttrs = cs > 1 || force_cl ? 2 : 1;  // no cluster attribute unless clustering (launch cost)
     p.st = stamp_next(reinterpret_cast<const void*>(gemm_tc_kernel));
-    EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p));
+    EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, mo, p));
     return splits / cs;
 }
 

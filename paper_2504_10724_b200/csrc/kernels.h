@@ -36,9 +36,10 @@ struct RowState {
 void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in,
                   int batch, int d, RowState st, cudaStream_t s);
 // x[i] += sum_s part[s][i] (part may be null); out1 = act(x*g1/rms), out2 = act(x*g2/rms) (optional).
+// pf / pf_bytes: the next GEMM's weights, prefetched into L2 by the CTAs (optional).
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
-                          void* out2, cudaStream_t s);
+                          void* out2, cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0);
 // out[i][:] = sum_s part[s][i][:] for the live rows (tensor-parallel partial before all-reduce).
 void launch_plane_sum(const float* part, int splits, int64_t split_stride, const int* n_active, int max_rows, int d,
                       float* out, int num_sms, cudaStream_t s);
@@ -111,6 +112,8 @@ struct AttnArgs {
     void* out;               // [maxB, dq] act dtype
     const void* k_map;       // bf16: TMA maps of this layer's K / V (128 B each), else null
     const void* v_map;
+    const void* k_map8 = nullptr;  // the same tensors with 8-row boxes (exact tails)
+    const void* v_map8 = nullptr;
     int num_sms;
     int kv_ready = 0;        // prefill: every row's K/V is already in the cache (launch_kv_append)
     // Paged KV pool: position p of slot s lives in page page_table[s * pages_per_seq + p / page_size]
@@ -132,6 +135,8 @@ struct AttnArgs {
     float* kv_part = nullptr;   // [max_rows][Hkv][kv_splits][8][hd + 2]
     int* kv_ticket = nullptr;   // [max_rows][Hkv]
     int dbg = 0;                // timing experiments (attention_dec, EEB_ATTN_DBG): 1 no compute, 2 no K/V loads
+    const void* pf = nullptr;   // the O GEMM's weights, prefetched into L2 during the attention (optional)
+    size_t pf_bytes = 0;
 };
 // Device address of (page-table row of slot, position, kv head, dim 0) in a layer's K or V cache.
 __host__ __device__ inline int64_t kv_elem_offset(const AttnArgs& a, int slot, int pos, int g) {

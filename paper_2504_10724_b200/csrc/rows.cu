@@ -66,11 +66,14 @@ __global__ void __launch_bounds__(kNormThreads)
     residual_norm_kernel(Stamp stamp, const float* part, int splits, int64_t split_stride,
                          const int* n_active, float* x, int d, float eps,
                          const float* g1, T* out1, const float* g2,
-                         T* out2) {
+                         T* out2, const void* pf, size_t pf_bytes) {
     StampScope stamp_scope(stamp);
     pdl_launch_dependents();
     pdl_wait();
     stamp_waited(stamp);
+    // the next GEMM's weights -> L2 while this latency-bound pass runs (after
+    // the wait: the predecessor GEMM's own weight stream has ended)
+    if (threadIdx.x < 32) l2_prefetch_share(pf, pf_bytes, threadIdx.x);
     const int i = blockIdx.x;
     if (i >= *n_active) return;
     __shared__ float red[32];
@@ -218,14 +221,15 @@ void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in
 
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
-                          void* out2, cudaStream_t s) {
+                          void* out2, cudaStream_t s, const void* pf, size_t pf_bytes) {
     const int q = d / 4;  // float4 groups per row
     if (d % 4 != 0 || q > 4 * kNormThreads)
         throw Error(1, "residual_norm: d_model must be a multiple of 4 and at most 8192");
     const int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
     const dim3 grid(max_rows), block(std::max(32, std::min(kNormThreads, (q / kv + 31) / 32 * 32)));
     auto go = [&](auto kern, auto* o1, auto* o2) {
-        launch_pdl(kern, grid, block, 0, s, part, splits, split_stride, n_active, x, d, eps, g1, o1, g2, o2);
+        launch_pdl(kern, grid, block, 0, s, part, splits, split_stride, n_active, x, d, eps, g1, o1, g2, o2, pf,
+                   pf_bytes);
     };
     if (dtype == 0) {
         float* o1 = static_cast<float*>(out1);

@@ -43,9 +43,11 @@ def analyse(launches: list[dict]) -> dict:
         # predecessor's end, and the work after the wait returned
         lat = w - last if w >= 0 else -1
         work = l["end_ns"] - w if w >= 0 else -1
+        mk = l.get("mark_ns", -1)
+        tail = l["end_ns"] - mk if mk >= 0 and w >= 0 else -1
         last = max(last, l["end_ns"])
         rows.append({**l, "kind": kernel_kind(l["kernel"]), "crit_ns": crit, "busy_ns": l["end_ns"] - l["start_ns"],
-                     "lat_ns": lat, "work_ns": work})
+                     "lat_ns": lat, "work_ns": work, "tail_ns": tail})
     span = last - t0
     cats = {}
     for r in rows:
@@ -75,11 +77,13 @@ def run(ctx, step, n_steps: int, max_launches: int = 1024) -> dict:
     busy = np.mean([[r["busy_ns"] for r in p["launches"]] for p in per], axis=0)
     lat = np.mean([[r["lat_ns"] for r in p["launches"]] for p in per], axis=0)
     work = np.mean([[r["work_ns"] for r in p["launches"]] for p in per], axis=0)
+    tail = np.mean([[r["tail_ns"] for r in p["launches"]] for p in per], axis=0)
     span = float(np.mean([p["span_ns"] for p in per]))
     launches = [{"kernel": r.get("kind", r["kernel"]), "cat": r["cat"], "ctas": r["ctas"],
                  "crit_us": float(c) / 1e3, "busy_us": float(b) / 1e3,
-                 **({"lat_us": float(la) / 1e3, "work_us": float(wo) / 1e3} if r["lat_ns"] >= 0 else {})}
-                for r, c, b, la, wo in zip(per[0]["launches"], crit, busy, lat, work)]
+                 **({"lat_us": float(la) / 1e3, "work_us": float(wo) / 1e3} if r["lat_ns"] >= 0 else {}),
+                 **({"tail_us": float(ta) / 1e3} if r["tail_ns"] >= 0 else {})}
+                for r, c, b, la, wo, ta in zip(per[0]["launches"], crit, busy, lat, work, tail)]
     cats = {}
     for l in launches:
         c = cats.setdefault(l["cat"], {"crit_ms": 0.0, "busy_ms": 0.0, "launches": 0})
@@ -98,7 +102,8 @@ def table(tl: dict, top: int = 0) -> str:
     if top:
         out.append("  launches (crit / busy us):")
         for i, l in enumerate(tl["launches"][:top]):
-            extra = (f"  (wait-after-prev {l['lat_us']:6.2f}, work {l['work_us']:6.2f})" if "lat_us" in l else "")
+            extra = (f"  (wait-after-prev {l['lat_us']:6.2f}, work {l['work_us']:6.2f}" +
+                     (f", tail {l['tail_us']:6.2f}" if "tail_us" in l else "") + ")" if "lat_us" in l else "")
             out.append(f"    {i:4d} {l['kernel']:18s} {l['cat']:11s} ctas={l['ctas']:5d} "
                        f"crit {l['crit_us']:7.2f}  busy {l['busy_us']:7.2f}{extra}")
     return "\n".join(out)

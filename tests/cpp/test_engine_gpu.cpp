@@ -11,6 +11,7 @@
 #include <string>
 
 #include "eeserve/engine.hpp"
+#include "../../paper_2504_10724_b200/csrc/synth.cuh"
 
 using namespace eeserve;
 
@@ -53,7 +54,9 @@ static ModelSpec make_model(const std::string& id, int layers, std::vector<int> 
 static ModelRepository make_repo() {
     ModelRepository r;
     r.models["small"] = make_model("small", 12, {6, 12}, 256, 4, 1024, 512, 7, 2.0);
-    r.models["large"] = make_model("large", 16, {8, 16}, 256, 4, 1024, 512, 8, 1.0);
+    // a wider second model: switching regrows the shared workspace and KV
+    // pools, which must invalidate the first model's captured graphs
+    r.models["large"] = make_model("large", 16, {8, 16}, 512, 4, 2048, 768, 8, 1.0);
     r.metric_directions["throughput"] = MetricDirection::higher_better;
     return r;
 }
@@ -128,6 +131,32 @@ int main(int argc, char** argv) {
                     (long long)rep.ld_count, (long long)rep.sw_count, rep.load_s * 1e3, (long long)rep.load_bytes,
                     rep.load_bytes / std::max(1e-12, rep.load_s) / 1e9, rep.prefill_s * 1e3);
     }
+    {  // drift: easy tokens while the candidates are profiled, then murky ones
+       // (difficulty z(t) above every head's coverage) at the greedy depth —
+       // the breach tracker must fire on real GPU verdicts and the engine apply
+       // a load-more or switch at a request boundary (engine.hpp:381-385,
+       // :301-323; the reference KAT is test_engine.cpp:186-204)
+        CudaBackend be(0, /*host_tier=*/true);
+        EngineConfig cfg = make_cfg(Mode::helios, "");
+        const std::uint64_t seed = repo.at("small").arch.seed;
+        cfg.token_fn = [seed](std::int64_t rid, int pos, int vocab) -> int32_t {
+            const bool murky = rid >= 32;  // the first eval phase profiles 2 x 16 easy requests
+            for (std::uint64_t k = 1;; ++k) {
+                const int32_t t = synthetic_token(k * 0x9e3779b97f4a7c15ULL, rid, pos, vocab);
+                const float z = eeb::synth::z_of(seed, t);
+                if (murky ? z > 0.85f : z < 0.6f) return t;
+            }
+        };
+        cfg.policy.ri = 1000;  // no reassessment after the first: only breaches move the plan
+        BatchedEngine eng(repo, be, cfg);
+        const EngineReport rep = eng.run(reqs);
+        check_report(rep, reqs);
+        CHECK(rep.ld_count + rep.sw_count >= 1);
+        CHECK(rep.serving_history.size() >= 2);
+        std::printf("drift: ld %lld, sw %lld, history", (long long)rep.ld_count, (long long)rep.sw_count);
+        for (const auto& [m, d] : rep.serving_history) std::printf(" %s@%d", m.c_str(), d);
+        std::printf("\n");
+    }
     {  // ee_single: introspective exits on the device; exit mixture near the calibrated 73/27
         CudaBackend be(0);
         BatchedEngine eng(repo, be, make_cfg(Mode::ee_single, "small"));
@@ -149,8 +178,10 @@ int main(int argc, char** argv) {
         const EngineReport rep = BatchedEngine(repo, be, cc).run(reqs);
         check_report(rep, reqs);
         CHECK(rep.steps < st.steps);
-        for (const auto& [l, p] : st.exit_table.at("small"))  // rows < 3 take the CUDA-core GEMV (other rounding)
-            CHECK(std::fabs((rep.exit_table.at("small").count(l) ? rep.exit_table.at("small").at(l) : 0.0) - p) < 1.0);
+        // batch invariance: a row's result does not depend on its slot or on
+        // the other rows of the step, so the exit tables agree exactly
+        for (const auto& [l, p] : st.exit_table.at("small"))
+            CHECK(std::fabs((rep.exit_table.at("small").count(l) ? rep.exit_table.at("small").at(l) : 0.0) - p) < 1e-9);
         std::printf("continuous+paged: %lld steps (static %lld), exit@6 %.1f%% (static %.1f%%)\n", (long long)rep.steps,
                     (long long)st.steps, rep.exit_table.at("small").count(6) ? rep.exit_table.at("small").at(6) : 0.0,
                     st.exit_table.at("small").count(6) ? st.exit_table.at("small").at(6) : 0.0);

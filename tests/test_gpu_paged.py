@@ -48,7 +48,11 @@ def _same(a, b, exact, stats):
     stats[1] += len(ca)
 
 
-@pytest.mark.parametrize("desc", [DESC, DESC128], ids=["hd64", "hd128"])
+DESC_MHA = eeb.ModelDesc("paged-mha", 4, 512, 8, 8, 1024, 1000, (2, 4), dtype=eeb.BF16, max_slots=8,
+                         max_seq_len=256)
+
+
+@pytest.mark.parametrize("desc", [DESC, DESC128, DESC_MHA], ids=["hd64", "hd128", "hd64-mha"])
 def test_paged_equals_unpaged(ctx, desc):
     mu = ctx.register(desc)
     mp = ctx.register(desc.replace(name=desc.name + "-p"))

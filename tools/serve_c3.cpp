@@ -6,13 +6,24 @@
 // switching, batch 256 with continuous batching over a paged KV pool.
 // Prints one JSON line (bench.py attaches it as "secondary_c3").
 //
-//   serve_c3 [n_requests] [prompt_len] [tokens]
+//   serve_c3 [n_requests] [prompt_len] [tokens] [calib|drift]
+//
+// drift (default): the reference's drift workload shape (fixtures/gen_drift.json:
+// alternating murky / easy segments with reference exit probabilities
+// [0.3, 0.1, 0.6] / [0.92, 0.05, 0.03]).  The synthetic model decides a
+// token's exit by its difficulty z(t) (synth.cuh: confident at head e iff
+// z(t) <= cumulative coverage_e), so the teacher-forced input tokens are drawn
+// per (request, position) from the z band of an exit sampled from the
+// segment's law: murky segments breach at the greedy depth on the GPU and
+// drive load-more / switch actions (test_engine.cpp:186-204).
+// calib: uniformly drawn tokens (the calibration mixture).
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <string>
 
 #include "eeserve/engine.hpp"
+#include "../paper_2504_10724_b200/csrc/synth.cuh"
 
 using namespace eeserve;
 
@@ -45,6 +56,7 @@ int main(int argc, char** argv) {
     const int n_req = argc > 1 ? std::atoi(argv[1]) : 1024;
     const int prompt = argc > 2 ? std::atoi(argv[2]) : 128;
     const int tokens = argc > 3 ? std::atoi(argv[3]) : 64;
+    const bool drift = argc > 4 ? std::string(argv[4]) != "calib" : true;
     ModelRepository repo;
     // public OPT dims: 1.3B L24 d2048 ffn 8192; 2.7B L32 d2560 ffn 10240; V 50272
     repo.models["opt-1.3b"] = opt_shape("opt-1.3b", 24, {6, 12, 24}, 2048, 32, 8192, 20260819, 2.0, 6e-5);
@@ -65,13 +77,31 @@ int main(int argc, char** argv) {
     cfg.max_batch = 256;
     cfg.max_seq_len = prompt + tokens;
     cfg.continuous = true;
+    const int seg_len = 256;  // requests per drift segment
+    if (drift) {
+        const std::uint64_t mseed = repo.models["opt-1.3b"].arch.seed;
+        const std::vector<double> cum = {0.73, 0.777, 1.0};  // default coverage 73.0 / 4.7 / 22.3 %
+        const double murky[3] = {0.3, 0.1, 0.6}, easy[3] = {0.92, 0.05, 0.03};
+        cfg.token_fn = [=](std::int64_t rid, int pos, int vocab) -> int32_t {
+            const double* law = (rid / seg_len) % 2 == 0 ? murky : easy;
+            const double u = (double)synthetic_token(0x5eedULL, rid, pos, 1 << 24) / (double)(1 << 24);
+            const int e = u < law[0] ? 0 : (u < law[0] + law[1] ? 1 : 2);
+            const double lo = (e == 0 ? 0.0 : cum[e - 1]) + 0.01, hi = cum[e] - 0.01;
+            for (std::uint64_t k = 1;; ++k) {
+                const int32_t t = synthetic_token(0x70c0ULL + k * 0x9e3779b97f4a7c15ULL, rid, pos, vocab);
+                const double z = eeb::synth::z_of(mseed, t);
+                if (z >= lo && z < hi) return t;
+            }
+        };
+    }
 
     const auto t0 = std::chrono::steady_clock::now();
     CudaBackend be(0, /*host_tier=*/true);
-    be.set_kv_pages(64, 256 * ((prompt + tokens + 63) / 64));
+    be.set_kv_pages(64);  // pages for every slot BatchedEngine::slots_for sizes (max_batch_size)
     std::vector<RequestSpec> reqs;
     for (int i = 0; i < n_req; ++i) reqs.push_back({i, prompt, tokens});
     BatchedEngine eng(repo, be, cfg);
+    eng.prepare();  // device pools sized from the memory model; both models staged in the pinned host tier
     const auto t1 = std::chrono::steady_clock::now();
     const EngineReport rep = eng.run(reqs);
     const auto t2 = std::chrono::steady_clock::now();
@@ -96,12 +126,14 @@ int main(int argc, char** argv) {
     std::printf(
         "{\"workload\": \"C3: OPT-1.3B + OPT-2.7B shapes, HELIOS mode (eval cycles, PHT, choose_depth, greedy "
         "loads from a pinned host tier, breach switching), batch 256, continuous batching over a paged KV pool\", "
+        "\"token_law\": \"%s\", \"slots\": {\"opt-1.3b\": %d, \"opt-2.7b\": %d}, "
         "\"requests\": %d, \"prompt_len\": %d, \"tokens_per_request\": %d, \"tokens\": %lld, \"steps\": %lld, "
-        "\"decode_tokens_per_s\": %.1f, \"serving_tokens_per_s\": %.1f, \"wall_s\": %.3f, \"host_stage_s\": %.3f, "
+        "\"decode_tokens_per_s\": %.1f, \"serving_tokens_per_s\": %.1f, \"wall_s\": %.3f, \"setup_s\": %.3f, "
         "\"mean_ttft_ms\": %.3f, \"mean_tpot_ms\": %.4f, \"achieved_batch\": %d, \"eval_cycles\": %lld, "
         "\"ld\": %lld, \"sw\": %lld, \"load_bytes\": %lld, \"load_s\": %.4f, \"load_gbs\": %.2f, \"prefill_s\": %.3f, "
         "\"perplexity\": %.6f, \"exit_table_pct\": %s, \"serving_history\": %s}\n",
-        n_req, prompt, tokens, (long long)rep.tokens, (long long)rep.steps, rep.throughput_tok_s,
+        drift ? "drift: alternating murky/easy segments of 256 requests (gen_drift.json exit laws), tokens drawn by synthetic difficulty" : "calibration: uniform tokens",
+        eng.slots("opt-1.3b"), eng.slots("opt-2.7b"), n_req, prompt, tokens, (long long)rep.tokens, (long long)rep.steps, rep.throughput_tok_s,
         rep.tokens / run_s, run_s, setup_s, rep.mean_ttft_s * 1e3, rep.mean_tpot_s * 1e3, rep.achieved_batch_size,
         (long long)rep.eval_cycles, (long long)rep.ld_count, (long long)rep.sw_count, (long long)rep.load_bytes,
         rep.load_s, rep.load_bytes / std::max(1e-9, rep.load_s) / 1e9, rep.prefill_s, rep.perplexity,
