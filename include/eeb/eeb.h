@@ -248,6 +248,7 @@ eeb_status eeb_debug_stamps_read(eeb_ctx* ctx, char* json_out, int64_t cap);
 /* Per-CTA stamps (ns from the step's first start; -1 = none) of launch
  * `launch` of the last stamped step, CTAs [0, n) in linear block order. */
 eeb_status eeb_debug_stamps_cta(eeb_ctx* ctx, int launch, int64_t* start_ns, int64_t* end_ns, int64_t* wait_ns,
+                                int64_t* mark_ns,
                                 int n);
 
 /* Test/diagnostic hooks (not used on the serving path). */

@@ -265,8 +265,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kThreads, 1)
     __syncthreads();
 
     // ---- this warp's items -----------------------------------------------------
-    const int h = lane >> 2, kq = (lane & 3) * 2;
-    int u = 0;  // chunks consumed by this warp
+    const int h = lane >> 2, kq = (lane & 3) * 2;    int u = 0;  // chunks consumed by this warp
     for (int k = warp; k < my; k += NW) {
         const int it = (int)blockIdx.x + k * grid, row = it / Hkv, g = it % Hkv;
         const int pos = rows_s[k].y;
@@ -420,259 +419,332 @@ bool launch_dec(const AttnArgs& a0, cudaStream_t s) {
 // MHA decode attention on the CUDA cores (one query head per kv head, head_dim
 // 64: the OPT shapes of C2 / C3).  With G = 1 an m16n8k16 score tile carries
 // one useful row in sixteen, and the per-chunk fragment / online-softmax
-// bookkeeping of the kernel above is what bounds it (measured: the kernel
-// with its K/V loads and MMAs switched off still takes ~11 us per C2 layer).
-// Here each warp owns whole (row, head) items and walks them in two passes
-// over its own TMA ring of 32-position chunks:
+// bookkeeping of the kernel above is what bounds it.  Here each warp owns
+// whole (row, head) items and walks each in two passes over its own ring:
 //
-//   K pass  lane = position: the lane's K row (128 B, 128B-swizzled by the
-//           TMA, so the 8 lanes of a quarter-warp hit 8 distinct bank groups)
-//           dotted with q held in 64 registers; masked scores -> per-warp smem;
+//   K pass  lane = position: the lane's K row (128 B) dotted with q held in
+//           64 registers, read in a lane-rotated 16-byte-chunk order (lane l
+//           reads chunk (j + l) mod 8 at step j, with q rotated the same way)
+//           so the 8 lanes of a quarter-warp hit 8 distinct bank groups;
+//           masked scores -> per-warp smem;
 //   softmax one warp max and one warp sum per item (no online rescaling);
 //   V pass  lane = 2 output dims: every position's V row is one conflict-free
 //           128-byte warp load, weighted by the broadcast probabilities.
 //
+// K / V move by 1-D bulk copies (cp.async.bulk) of exactly the rows an item
+// attends — (slot, head) rows are contiguous in the cache (a page's rows in
+// the paged pool) — in chunks of R rows: the CTA's stage pool is split over
+// its active warps, so with few live rows (after the exits) a warp's chunks
+// are large (up to 256 rows) and few, a whole item in flight in 2 copies per
+// pass.  Measured in the C2 step, each TMA tensor op of the 32-row-box
+// version cost ~60 cycles of issue per SM and the 10-20 ops per item made
+// the stream issue-bound at low batch.
+//
 // The item prologue (q / k / v summed over the QKV split-K planes, RoPE, the
-// new position's K / V rounded to bf16 and appended to the cache) is per warp
-// and overlaps the warp's first chunk loads; there is no CTA-wide barrier.
-// Arithmetic is f32 throughout (q is not rounded to bf16; exp via __expf),
-// and an item's result does not depend on which warp serves it or on the
-// batch.
+// new position's K / V rounded to bf16 and appended to the cache) is per warp;
+// the rows' slot / position are read in the same round trip as the live-row
+// count.  Arithmetic is f32 throughout (q is not rounded to bf16; exp via
+// __expf); an item's result does not depend on which warp serves it, on the
+// chunk size or on the batch.
 // ============================================================================
-constexpr int kMRows = 32;              // positions per chunk (one TMA box)
-constexpr uint32_t kMStage = kMRows * 128;  // one chunk of K or V: 32 rows x 64 bf16
-constexpr int kMItems = 8;              // items per warp (host sizes the grid)
+constexpr int kMItems = 8;       // items per warp at most (host sizes the grid)
+constexpr int kMMaxRing = 12;    // stages per warp at most
+constexpr uint32_t kMRow = 128;  // bytes per K / V row (head_dim 64, bf16)
+
+constexpr int kMRowsCta = 8;     // distinct rows of a CTA's (contiguous) item range at most
 
 struct MhaSmem {
-    int ring, s_pad;
-    size_t ring_off, sc_off, dep_off, q_off, total;
-    __host__ __device__ MhaSmem(int kMW, int nring, int max_seq) {
-        ring = nring;
+    int s_pad;
+    size_t sc_off, q_off, rope_off, dep_off, pt_off, total;
+    __host__ __device__ MhaSmem(int kMW, size_t pool, int max_seq) {
         s_pad = (max_seq + 31) & ~31;
-        ring_off = 0;                                                  // [warp][ring] 4 KB stages
-        sc_off = (size_t)kMW * nring * kMStage;                        // [warp][s_pad] f32 scores / probabilities
-        dep_off = sc_off + (size_t)kMW * s_pad * 4;                    // [warp][s_pad] KV-depth bytes
-        q_off = dep_off + (size_t)kMW * s_pad;                         // [warp][2][64] f32 q, new k
-        total = q_off + (size_t)kMW * 128 * 4;
+        sc_off = pool;                                      // [warp][s_pad] f32 scores / probabilities
+        q_off = sc_off + (size_t)kMW * s_pad * 4;           // [warp][2][64] f32 q, new k
+        rope_off = q_off + (size_t)kMW * 128 * 4;           // [row][2][32] f32 cos, sin at the row's position
+        dep_off = rope_off + (size_t)kMRowsCta * 64 * 4;    // [row][s_pad] KV-depth bytes
+        pt_off = dep_off + (size_t)kMRowsCta * s_pad;       // [row][32] pages (paged pool)
+        total = pt_off + (size_t)kMRowsCta * 32 * 4;
     }
 };
 
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 w;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "r"(a));
+    return w;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t w;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(a));
+    return w;
+}
 
 template <int kMW, bool PAGED>
 __global__ void __launch_bounds__(kMW * 32, 1)
-    attention_mha_kernel(Stamp stamp, const __grid_constant__ CUtensorMap kmap,
-                         const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap kmap8,
-                         const __grid_constant__ CUtensorMap vmap8, AttnArgs a, int nring) {
+    attention_mha_kernel(Stamp stamp, AttnArgs a, int pool_kb) {
     StampScope stamp_scope(stamp);
     constexpr int HD = 64;
+    constexpr int kP = 6;  // QKV planes loaded ahead (C2: all of them)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
     uint8_t* base = smem_raw + (sbase - raw);
-    __shared__ __align__(8) uint64_t full[kMW][4];
+    __shared__ __align__(8) uint64_t full[kMW][kMMaxRing];
+    __shared__ int s_rows, s_slot[kMRowsCta], s_pos[kMRowsCta];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane < nring) {
+    if (lane < kMMaxRing) {
         mbar_init(smem_u32(&full[warp][lane]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (threadIdx.x == 0) {
-        prefetch_tmap(&kmap);
-        prefetch_tmap(&vmap);
-        prefetch_tmap(&kmap8);
-        prefetch_tmap(&vmap8);
-    }
-    __syncwarp();
     pdl_launch_dependents();
     pdl_wait();
     stamp_waited(stamp);
-    if (warp == kMW - 1) l2_prefetch_share(a.pf, a.pf_bytes, lane);  // the O GEMM's weights -> L2
 
     const int H = a.n_heads, S = a.max_seq;
     const int dq = H * HD;
-    const int n_items = *a.n_active * H;
-    // items of this warp: it = gw, gw + nw, ... (warp-major over the grid so
-    // every CTA gets a share of a small batch)
-    const int gw = warp * gridDim.x + blockIdx.x, nw = gridDim.x * kMW;
-    const int my = gw < n_items ? (n_items - 1 - gw) / nw + 1 : 0;
-    if (my == 0) return;
-    const MhaSmem L(kMW, nring, S);
-    const uint32_t ring = sbase + (uint32_t)(L.ring_off + (size_t)warp * nring * kMStage);
-    float* sc_s = reinterpret_cast<float*>(base + L.sc_off) + (size_t)warp * L.s_pad;
-    uint8_t* dep_s = base + L.dep_off + (size_t)warp * L.s_pad;
-    float* q_s = reinterpret_cast<float*>(base + L.q_off) + warp * 128;
-    float* knew_s = q_s + 64;
-
-    // lane k < my holds item k's row, slot, position (shuffled out on demand)
-    int i_slot = 0, i_pos = 0;
-    if (lane < my) {
-        const int row = (gw + lane * nw) / H;
-        i_slot = a.slot[row];
-        i_pos = a.pos[row];
-    }
-    // paged: lane j holds page j of the item being issued (and of the next)
-    const int PS = PAGED ? a.page_size : S;
-    int pg_cur = 0, pg_nxt = 0;
-    auto load_pages = [&](int k) {
-        const int sl = __shfl_sync(0xffffffffu, i_slot, k & 31);
-        return (PAGED && k < my && lane < a.pages_per_seq) ? a.page_table[(int64_t)sl * a.pages_per_seq + lane] : 0;
-    };
-    if (PAGED) {
-        pg_cur = load_pages(0);
-        pg_nxt = load_pages(1);
-    }
-
-    // ---- the warp's chunk stream: item k, pass ph (0 K, 1 V), chunk ic -------
-    int ik = 0, iph = 0, ic = 0;
-    auto issue_next = [&](int st) {  // whole warp (shuffles); lane 0 issues
-        if (ik >= my) return;
-        const int pos = __shfl_sync(0xffffffffu, i_pos, ik);
-        const int slot = __shfl_sync(0xffffffffu, i_slot, ik);
-        const int g = (gw + ik * nw) % H;
-        const int p = ic * kMRows;
-        const int page = PAGED ? __shfl_sync(0xffffffffu, pg_cur, p / PS) : slot;
-        if (lane == 0) {
-            const uint32_t bar = smem_u32(&full[warp][st]), dst = ring + (uint32_t)st * kMStage;
-            const int r = PAGED ? p % PS : p, z = page * H + g;
-            const int rows = pos + 1 - p;  // positions of this chunk the item attends
-            if (rows >= kMRows) {
-                mbar_expect_tx(bar, kMStage);
-                tma_load_3d(dst, iph == 0 ? &kmap : &vmap, bar, 0, r, z);
-            } else {  // the pass's last chunk: 8-row boxes up to pos (one 1 KB swizzle atom each)
-                const int n8 = (rows + 7) >> 3;
-                mbar_expect_tx(bar, (uint32_t)n8 * 1024u);
-                for (int b = 0; b < n8; ++b) tma_load_3d(dst + 1024u * b, iph == 0 ? &kmap8 : &vmap8, bar, 0, r + 8 * b, z);
-            }
-        }
-        if (++ic > pos / kMRows) {
-            ic = 0;
-            if (++iph == 2) {
-                iph = 0;
-                ++ik;
-                if (PAGED) {
-                    pg_cur = pg_nxt;
-                    pg_nxt = load_pages(ik + 1);
-                }
-            }
-        }
-    };
-    for (int st = 0; st < nring; ++st) issue_next(st);
-
-    int u = 0;  // chunks consumed by this warp
-    const float qscale = 0.125f;  // 1 / sqrt(64), exact
-    for (int k = 0; k < my; ++k) {
-        const int it = gw + k * nw, row = it / H, g = it % H;
-        const int pos = __shfl_sync(0xffffffffu, i_pos, k);
-        const int slot = __shfl_sync(0xffffffffu, i_slot, k);
-        // ---- item prologue: lane = dims (2 lane, 2 lane + 1) -----------------
-        // every global load of the prologue in flight together: KV-depth words
-        // of the item's earlier positions (S % 4 == 0 checked on the host; the
-        // first 1024 positions here, the rest below), the RoPE row, the planes
-        const uint32_t* dep_g = reinterpret_cast<const uint32_t*>(a.kv_depth + (int64_t)slot * S);
-        uint32_t dw[8];
+    const MhaSmem L(kMW, (size_t)pool_kb << 10, S);
+    // The step's small shared arrays (live-row count, the rows' slot /
+    // position, RoPE rows, KV-depth rows, page rows) are read once per CTA
+    // into smem, not per warp (every warp of the grid would hit the same few
+    // L2 lines).
+    if (threadIdx.x == 0) s_rows = *a.n_active;
+    __syncthreads();
+    const int n_items = s_rows * H;
+    // contiguous item ranges per CTA: a CTA's items share one or two rows
+    const int per = (n_items + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int beg = (int)blockIdx.x * per, end = min(beg + per, n_items);
+    if (beg >= end) return;
+    const int r0 = beg / H, nr = (end - 1) / H - r0 + 1;  // <= kMRowsCta (host)
+    // this warp's items: beg + warp + kMW k.  The first item's QKV planes
+    // (they depend on the row only) are requested now and summed before the
+    // next barrier, overlapping the table loads.
+    const bool has = beg + warp < end;
+    const int my = has ? (end - beg - warp - 1) / kMW + 1 : 0;
+    float2 q2f = make_float2(0.f, 0.f), k2f = q2f, v2f = q2f;
+    {
+        const int it = beg + warp, row = it / H, g = it % H;
+        const float* src = a.qkv + (int64_t)row * (3 * dq) + g * HD + 2 * lane;
+        float2 xs[kP], ys[kP], zs[kP];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int w = lane + 32 * i;
-            dw[i] = 4 * w < pos ? __ldg(dep_g + w) : 0u;
+        for (int sp = 0; sp < kP; ++sp) {
+            const bool on = has && sp < a.splits;
+            const float* pl = src + (on ? sp : 0) * a.split_stride;
+            xs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl)) : make_float2(0.f, 0.f);
+            ys[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + dq)) : make_float2(0.f, 0.f);
+            zs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq)) : make_float2(0.f, 0.f);
         }
-        // RoPE over pairs (j, j + 32): lane l < 16 holds the first halves, l + 16 the partners
-        const int jj = (2 * lane) & 31;
-        const float2 cc = __ldg(reinterpret_cast<const float2*>(a.rope_cos + (int64_t)pos * 32 + jj));
-        const float2 ss = __ldg(reinterpret_cast<const float2*>(a.rope_sin + (int64_t)pos * 32 + jj));
-        const float* src = a.qkv + (int64_t)row * (dq + 2 * dq) + g * HD + 2 * lane;
-        float2 q2 = make_float2(0.f, 0.f), k2 = q2, v2 = q2;
+        if (threadIdx.x < nr) {
+            s_slot[threadIdx.x] = a.slot[r0 + threadIdx.x];
+            s_pos[threadIdx.x] = a.pos[r0 + threadIdx.x];
+        }
 #pragma unroll
-        for (int sp = 0; sp < 16; ++sp) {
-            if (sp >= a.splits) break;
+        for (int sp = 0; sp < kP; ++sp) {
+            q2f.x += xs[sp].x; q2f.y += xs[sp].y; k2f.x += ys[sp].x; k2f.y += ys[sp].y;
+            v2f.x += zs[sp].x; v2f.y += zs[sp].y;
+        }
+        for (int sp = kP; has && sp < a.splits; ++sp) {
             const float* pl = src + sp * a.split_stride;
             const float2 x = __ldcg(reinterpret_cast<const float2*>(pl));
             const float2 y = __ldcg(reinterpret_cast<const float2*>(pl + dq));
             const float2 z = __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq));
-            q2.x += x.x; q2.y += x.y; k2.x += y.x; k2.y += y.y; v2.x += z.x; v2.y += z.y;
+            q2f.x += x.x; q2f.y += x.y; k2f.x += y.x; k2f.y += y.y; v2f.x += z.x; v2f.y += z.y;
         }
+    }
+    __syncthreads();
+    float* rope_s = reinterpret_cast<float*>(base + L.rope_off);
+    uint8_t* depc_s = base + L.dep_off;
+    int* pt_s = reinterpret_cast<int*>(base + L.pt_off);
+    for (int e = threadIdx.x; e < nr * 64; e += kMW * 32) {
+        const int t = e >> 6, j = e & 63;
+        rope_s[e] = (j < 32 ? a.rope_cos : a.rope_sin)[(int64_t)s_pos[t] * 32 + (j & 31)];
+    }
+    {
+        const int wpr = L.s_pad / 4;  // depth words per row (S % 4 == 0: host)
+        for (int e = threadIdx.x; e < nr * wpr; e += kMW * 32) {
+            const int t = e / wpr, w = e - t * wpr;
+            if (4 * w < s_pos[t])
+                reinterpret_cast<uint32_t*>(depc_s)[e] =
+                    reinterpret_cast<const uint32_t*>(a.kv_depth + (int64_t)s_slot[t] * S)[w];
+        }
+    }
+    if (PAGED)
+        for (int e = threadIdx.x; e < nr * 32; e += kMW * 32)
+            if ((e & 31) < a.pages_per_seq) pt_s[e] = a.page_table[(int64_t)s_slot[e >> 5] * a.pages_per_seq + (e & 31)];
+    __syncthreads();
+    if (!has) return;
+    const int active = min(kMW, end - beg);
+    // the CTA's stage pool is shared by its active warps: chunk rows R (a
+    // multiple of 32, <= 256; <= the page size when paged) with >= 3 stages
+    const int per_warp = ((pool_kb << 10) / active) & ~1023;     // bytes (1 KB aligned)
+    int R = min(256, (per_warp / (3 * (int)kMRow)) & ~31);
+    if (PAGED) R = min(R, a.page_size);
+    R = max(R, 32);
+    const int nring = max(2, min(kMMaxRing, per_warp / (R * (int)kMRow)));
+    const uint32_t stage_bytes = (uint32_t)R * kMRow;
+    const uint32_t ring = sbase + (uint32_t)warp * (uint32_t)per_warp;
+    float* sc_s = reinterpret_cast<float*>(base + L.sc_off) + (size_t)warp * L.s_pad;
+    float* q_s = reinterpret_cast<float*>(base + L.q_off) + warp * 128;
+    float* knew_s = q_s + 64;
+    const int PS = PAGED ? a.page_size : S;
+    const __nv_bfloat16* kc = static_cast<const __nv_bfloat16*>(a.k_cache);
+    const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(a.v_cache);
+    // (slot, head) row p of the cache, in elements
+    auto row_off = [&](int lr, int g, int p) -> int64_t {
+        const int page = PAGED ? pt_s[lr * 32 + p / PS] : s_slot[lr];
+        return (((int64_t)page * H + g) * PS + (PAGED ? p % PS : p)) * HD;
+    };
+    const uint64_t pol = policy_evict_first();
+
+    // ---- the warp's chunk stream: item ik, pass iph (0 K, 1 V), chunk rows ip.
+    // The issue cursor's item (local row, head, rows attended) is set once per item.
+    int ik = 0, iph = 0, ip = 0;
+    int c_lr = (beg + warp) / H - r0, c_g = (beg + warp) % H, c_n = s_pos[c_lr] + 1;
+    auto issue_next = [&](int st) {  // lane 0
+        if (ik >= my) return;
+        const uint32_t bar = smem_u32(&full[warp][st]);
+        const int rows = min(R, c_n - ip);
+        mbar_expect_tx(bar, (uint32_t)rows * kMRow);
+        bulk_g2s(ring + (uint32_t)st * stage_bytes, (iph == 0 ? kc : vc) + row_off(c_lr, c_g, ip), (uint32_t)rows * kMRow,
+                 bar, pol);
+        ip += R;
+        if (ip >= c_n) {
+            ip = 0;
+            if (++iph == 2) {
+                iph = 0;
+                if (++ik < my) {
+                    const int it = beg + warp + kMW * ik;
+                    c_lr = it / H - r0;
+                    c_g = it % H;
+                    c_n = s_pos[c_lr] + 1;
+                }
+            }
+        }
+    };
+    if (lane == 0)
+        for (int st = 0; st < nring; ++st) issue_next(st);
+
+    int u = 0;  // chunks consumed by this warp
+    const float qscale = 0.125f;  // 1 / sqrt(64), exact
+    for (int k = 0; k < my; ++k) {
+        const int it = beg + warp + kMW * k, row = it / H, g = it % H, lr = row - r0;
+        const int pos = s_pos[lr];
+        const uint8_t* dep_s = depc_s + (size_t)lr * L.s_pad;
+        // ---- item prologue: lane = dims (2 lane, 2 lane + 1) -----------------
+        const float* src = a.qkv + (int64_t)row * (3 * dq) + g * HD + 2 * lane;
+        float2 q2 = q2f, k2 = k2f, v2 = v2f;  // the first item: summed above
+        if (k > 0) {
+            q2 = k2 = v2 = make_float2(0.f, 0.f);
+            float2 xs[kP], ys[kP], zs[kP];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (4 * (lane + 32 * i) < pos) reinterpret_cast<uint32_t*>(dep_s)[lane + 32 * i] = dw[i];
-        for (int w = lane + 256; 4 * w < pos; w += 32) reinterpret_cast<uint32_t*>(dep_s)[w] = dep_g[w];
-        const float c0 = cc.x, c1 = cc.y, s0 = ss.x, s1 = ss.y;
+            for (int sp = 0; sp < kP; ++sp) {
+                const bool on = sp < a.splits;
+                const float* pl = src + (on ? sp : 0) * a.split_stride;
+                xs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl)) : make_float2(0.f, 0.f);
+                ys[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + dq)) : make_float2(0.f, 0.f);
+                zs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq)) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int sp = 0; sp < kP; ++sp) {
+                q2.x += xs[sp].x; q2.y += xs[sp].y; k2.x += ys[sp].x; k2.y += ys[sp].y;
+                v2.x += zs[sp].x; v2.y += zs[sp].y;
+            }
+            for (int sp = kP; sp < a.splits; ++sp) {
+                const float* pl = src + sp * a.split_stride;
+                const float2 x = __ldcg(reinterpret_cast<const float2*>(pl));
+                const float2 y = __ldcg(reinterpret_cast<const float2*>(pl + dq));
+                const float2 z = __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq));
+                q2.x += x.x; q2.y += x.y; k2.x += y.x; k2.y += y.y; v2.x += z.x; v2.y += z.y;
+            }
+        }
+        const int jj = (2 * lane) & 31;  // RoPE pairs (j, j + 32): lanes l and l ^ 16
+        const float2 cc = *reinterpret_cast<const float2*>(rope_s + lr * 64 + jj);
+        const float2 ss = *reinterpret_cast<const float2*>(rope_s + lr * 64 + 32 + jj);
         const float qp0 = __shfl_xor_sync(0xffffffffu, q2.x, 16), qp1 = __shfl_xor_sync(0xffffffffu, q2.y, 16);
         const float kp0 = __shfl_xor_sync(0xffffffffu, k2.x, 16), kp1 = __shfl_xor_sync(0xffffffffu, k2.y, 16);
         float qr0, qr1, kr0, kr1;
         if (lane < 16) {  // x0 = mine, x1 = partner: x0 cos - x1 sin
-            qr0 = q2.x * c0 - qp0 * s0; qr1 = q2.y * c1 - qp1 * s1;
-            kr0 = k2.x * c0 - kp0 * s0; kr1 = k2.y * c1 - kp1 * s1;
+            qr0 = q2.x * cc.x - qp0 * ss.x; qr1 = q2.y * cc.y - qp1 * ss.y;
+            kr0 = k2.x * cc.x - kp0 * ss.x; kr1 = k2.y * cc.y - kp1 * ss.y;
         } else {          // x1 = mine, x0 = partner: x0 sin + x1 cos
-            qr0 = qp0 * s0 + q2.x * c0; qr1 = qp1 * s1 + q2.y * c1;
-            kr0 = kp0 * s0 + k2.x * c0; kr1 = kp1 * s1 + k2.y * c1;
+            qr0 = qp0 * ss.x + q2.x * cc.x; qr1 = qp1 * ss.y + q2.y * cc.y;
+            kr0 = kp0 * ss.x + k2.x * cc.x; kr1 = kp1 * ss.y + k2.y * cc.y;
         }
         const __nv_bfloat162 kb = __floats2bfloat162_rn(kr0, kr1), vb = __floats2bfloat162_rn(v2.x, v2.y);
         const float vn0 = __low2float(vb), vn1 = __high2float(vb);
         *reinterpret_cast<float2*>(q_s + 2 * lane) = make_float2(qr0 * qscale, qr1 * qscale);
         *reinterpret_cast<float2*>(knew_s + 2 * lane) = make_float2(__low2float(kb), __high2float(kb));
-        if (!a.kv_ready) {  // append the new position's K / V (the chunk holding it is patched from registers)
-            const int64_t off = (((int64_t)(PAGED ? a.page_table[(int64_t)slot * a.pages_per_seq + pos / PS] : slot) * H +
-                                  g) * PS + (PAGED ? pos % PS : pos)) * HD + 2 * lane;
+        if (!a.kv_ready) {  // append the new position's K / V (its row of the last chunk comes from registers)
+            const int64_t off = row_off(lr, g, pos) + 2 * lane;
             *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.k_cache) + off) = kb;
             *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.v_cache) + off) = vb;
         }
         __syncwarp();
-        float q[HD];
+        if (k == 0 && lane == 0 && warp == 0) stamp_mark(stamp);  // (timeline) first item's prologue done
+        // q rotated per lane: qr[8 j + t] = q[8 ((j + lane) mod 8) + t]
+        float qr[HD];
 #pragma unroll
-        for (int j = 0; j < HD; j += 4) {
-            const float4 t = *reinterpret_cast<const float4*>(q_s + j);
-            q[j] = t.x; q[j + 1] = t.y; q[j + 2] = t.z; q[j + 3] = t.w;
+        for (int j = 0; j < 8; ++j) {
+            const float4 t0 = *reinterpret_cast<const float4*>(q_s + 8 * ((j + lane) & 7));
+            const float4 t1 = *reinterpret_cast<const float4*>(q_s + 8 * ((j + lane) & 7) + 4);
+            qr[8 * j + 0] = t0.x; qr[8 * j + 1] = t0.y; qr[8 * j + 2] = t0.z; qr[8 * j + 3] = t0.w;
+            qr[8 * j + 4] = t1.x; qr[8 * j + 5] = t1.y; qr[8 * j + 6] = t1.z; qr[8 * j + 7] = t1.w;
         }
-        const int nch = pos / kMRows + 1;
+        const int nch = pos / R + 1;
         // ---- K pass: lane = position ------------------------------------------
         float mx = -INFINITY;
         for (int c = 0; c < nch; ++c, ++u) {
             const int st = u % nring;
-            const uint32_t stage = ring + (uint32_t)st * kMStage;
+            const uint32_t stage = ring + (uint32_t)st * stage_bytes;
             mbar_wait(smem_u32(&full[warp][st]), (uint32_t)((u / nring) & 1));
-            const int p = c * kMRows + lane;
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            if (p != pos) {
+            const int c0r = c * R, rows = min(R, pos + 1 - c0r);
+            for (int sb = 0; sb < rows; sb += 32) {
+                const int r = sb + lane, p = c0r + r;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                if (p < pos) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    uint4 w;
-                    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                                 : "r"(stage + swz128(lane, j)));
-                    acc[0] = fmaf(q[8 * j + 0], bf_lo(w.x), acc[0]);
-                    acc[1] = fmaf(q[8 * j + 1], bf_hi(w.x), acc[1]);
-                    acc[2] = fmaf(q[8 * j + 2], bf_lo(w.y), acc[2]);
-                    acc[3] = fmaf(q[8 * j + 3], bf_hi(w.y), acc[3]);
-                    acc[0] = fmaf(q[8 * j + 4], bf_lo(w.z), acc[0]);
-                    acc[1] = fmaf(q[8 * j + 5], bf_hi(w.z), acc[1]);
-                    acc[2] = fmaf(q[8 * j + 6], bf_lo(w.w), acc[2]);
-                    acc[3] = fmaf(q[8 * j + 7], bf_hi(w.w), acc[3]);
-                }
-            } else {  // the new position: K from the prologue
+                    for (int j = 0; j < 8; ++j) {
+                        const uint4 w = lds128(stage + (uint32_t)r * kMRow + (uint32_t)(((j + lane) & 7) << 4));
+                        acc[0] = fmaf(qr[8 * j + 0], bf_lo(w.x), acc[0]);
+                        acc[1] = fmaf(qr[8 * j + 1], bf_hi(w.x), acc[1]);
+                        acc[2] = fmaf(qr[8 * j + 2], bf_lo(w.y), acc[2]);
+                        acc[3] = fmaf(qr[8 * j + 3], bf_hi(w.y), acc[3]);
+                        acc[0] = fmaf(qr[8 * j + 4], bf_lo(w.z), acc[0]);
+                        acc[1] = fmaf(qr[8 * j + 5], bf_hi(w.z), acc[1]);
+                        acc[2] = fmaf(qr[8 * j + 6], bf_lo(w.w), acc[2]);
+                        acc[3] = fmaf(qr[8 * j + 7], bf_hi(w.w), acc[3]);
+                    }
+                } else if (p == pos) {  // the new position: K from the prologue
 #pragma unroll
-                for (int j = 0; j < HD; j += 4) {
-                    const float4 t = *reinterpret_cast<const float4*>(knew_s + j);
-                    acc[0] = fmaf(q[j], t.x, acc[0]);
-                    acc[1] = fmaf(q[j + 1], t.y, acc[1]);
-                    acc[2] = fmaf(q[j + 2], t.z, acc[2]);
-                    acc[3] = fmaf(q[j + 3], t.w, acc[3]);
+                    for (int j = 0; j < 8; ++j) {
+                        const float4 t0 = *reinterpret_cast<const float4*>(knew_s + 8 * ((j + lane) & 7));
+                        const float4 t1 = *reinterpret_cast<const float4*>(knew_s + 8 * ((j + lane) & 7) + 4);
+                        acc[0] = fmaf(qr[8 * j + 0], t0.x, acc[0]);
+                        acc[1] = fmaf(qr[8 * j + 1], t0.y, acc[1]);
+                        acc[2] = fmaf(qr[8 * j + 2], t0.z, acc[2]);
+                        acc[3] = fmaf(qr[8 * j + 3], t0.w, acc[3]);
+                        acc[0] = fmaf(qr[8 * j + 4], t1.x, acc[0]);
+                        acc[1] = fmaf(qr[8 * j + 5], t1.y, acc[1]);
+                        acc[2] = fmaf(qr[8 * j + 6], t1.z, acc[2]);
+                        acc[3] = fmaf(qr[8 * j + 7], t1.w, acc[3]);
+                    }
                 }
+                const float sc = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                const bool valid = p == pos || (p < pos && (int)dep_s[p] >= a.layer);
+                const float sv = valid ? sc : -INFINITY;
+                if (p <= pos) sc_s[p] = sv;
+                mx = fmaxf(mx, sv);
             }
-            const float sc = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-            const bool valid = p == pos || (p < pos && (int)dep_s[p] >= a.layer);
-            const float s = valid ? sc : -INFINITY;
-            if (p <= pos) sc_s[p] = s;
-            mx = fmaxf(mx, s);
             __syncwarp();  // every lane is done with the stage
-            issue_next(st);
+            if (lane == 0) issue_next(st);
         }
         // ---- softmax over the item's positions (one max, one sum) --------------
 #pragma unroll
         for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         float lsum = 0.f;
         for (int p = lane; p <= pos; p += 32) {
-            const float s = sc_s[p];
-            const float e = s == -INFINITY ? 0.f : __expf(s - mx);
+            const float sv = sc_s[p];
+            const float e = sv == -INFINITY ? 0.f : __expf(sv - mx);
             sc_s[p] = e;
             lsum += e;
         }
@@ -681,46 +753,41 @@ __global__ void __launch_bounds__(kMW * 32, 1)
         __syncwarp();
         // ---- V pass: lane = dims (2 lane, 2 lane + 1) -------------------------
         float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-        const uint32_t voff = ((uint32_t)(lane & 3) << 2);
+        const uint32_t voff = (uint32_t)lane << 2;
         for (int c = 0; c < nch; ++c, ++u) {
             const int st = u % nring;
-            const uint32_t stage = ring + (uint32_t)st * kMStage;
+            const uint32_t stage = ring + (uint32_t)st * stage_bytes;
             mbar_wait(smem_u32(&full[warp][st]), (uint32_t)((u / nring) & 1));
-            const int c0r = c * kMRows;
-            if (c0r + kMRows <= pos) {  // every row precedes the new position
-#pragma unroll
-                for (int r = 0; r < kMRows; r += 4) {
-                    const float4 e = *reinterpret_cast<const float4*>(sc_s + c0r + r);
-                    uint32_t w0, w1, w2, w3;
-                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w0) : "r"(stage + swz128(r, lane >> 2) + voff));
-                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w1) : "r"(stage + swz128(r + 1, lane >> 2) + voff));
-                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w2) : "r"(stage + swz128(r + 2, lane >> 2) + voff));
-                    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w3) : "r"(stage + swz128(r + 3, lane >> 2) + voff));
-                    o0 = fmaf(e.x, bf_lo(w0), o0); o1 = fmaf(e.x, bf_hi(w0), o1);
-                    o2 = fmaf(e.y, bf_lo(w1), o2); o3 = fmaf(e.y, bf_hi(w1), o3);
-                    o0 = fmaf(e.z, bf_lo(w2), o0); o1 = fmaf(e.z, bf_hi(w2), o1);
-                    o2 = fmaf(e.w, bf_lo(w3), o2); o3 = fmaf(e.w, bf_hi(w3), o3);
+            const int c0r = c * R;
+            const int nfull = min(R, pos - c0r) & ~3;  // rows before pos, in groups of 4
+            for (int r = 0; r < nfull; r += 4) {
+                const float4 e = *reinterpret_cast<const float4*>(sc_s + c0r + r);
+                const uint32_t w0 = lds32(stage + (uint32_t)r * kMRow + voff);
+                const uint32_t w1 = lds32(stage + (uint32_t)(r + 1) * kMRow + voff);
+                const uint32_t w2 = lds32(stage + (uint32_t)(r + 2) * kMRow + voff);
+                const uint32_t w3 = lds32(stage + (uint32_t)(r + 3) * kMRow + voff);
+                o0 = fmaf(e.x, bf_lo(w0), o0); o1 = fmaf(e.x, bf_hi(w0), o1);
+                o2 = fmaf(e.y, bf_lo(w1), o2); o3 = fmaf(e.y, bf_hi(w1), o3);
+                o0 = fmaf(e.z, bf_lo(w2), o0); o1 = fmaf(e.z, bf_hi(w2), o1);
+                o2 = fmaf(e.w, bf_lo(w3), o2); o3 = fmaf(e.w, bf_hi(w3), o3);
+            }
+            const int rows = min(R, pos + 1 - c0r);
+            for (int r = nfull; r < rows; ++r) {  // the rest, the new row from registers
+                const float e = sc_s[c0r + r];
+                float x0, x1;
+                if (c0r + r == pos) {
+                    x0 = vn0;
+                    x1 = vn1;
+                } else {
+                    const uint32_t w = lds32(stage + (uint32_t)r * kMRow + voff);
+                    x0 = bf_lo(w);
+                    x1 = bf_hi(w);
                 }
-            } else {  // the item's last chunk: rows up to pos, the new row from registers
-                const int nr = pos + 1 - c0r;
-                for (int r = 0; r < nr; ++r) {
-                    const float e = sc_s[c0r + r];
-                    float x0, x1;
-                    if (c0r + r == pos) {
-                        x0 = vn0;
-                        x1 = vn1;
-                    } else {
-                        uint32_t w;
-                        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(w) : "r"(stage + swz128(r, lane >> 2) + voff));
-                        x0 = bf_lo(w);
-                        x1 = bf_hi(w);
-                    }
-                    o0 = fmaf(e, x0, o0);
-                    o1 = fmaf(e, x1, o1);
-                }
+                o0 = fmaf(e, x0, o0);
+                o1 = fmaf(e, x1, o1);
             }
             __syncwarp();
-            issue_next(st);
+            if (lane == 0) issue_next(st);
         }
         const float inv = 1.f / lsum;
         *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.out) + (int64_t)row * dq + g * HD + 2 * lane) =
@@ -732,16 +799,20 @@ template <int kMW, bool PAGED>
 bool launch_mha_w(const AttnArgs& a, cudaStream_t s) {
     const int items_max = a.max_rows * a.n_kv_heads;
     const int grid = std::max(a.num_sms, (items_max + kMW * kMItems - 1) / (kMW * kMItems));
-    if ((items_max + grid * kMW - 1) / (grid * kMW) > std::min(kMItems, 32)) return false;
-    int nring = 3;
-    while (nring > 2 && 1024 + MhaSmem(kMW, nring, a.max_seq).total > 227 * 1024) --nring;
-    const size_t smem = 1024 + MhaSmem(kMW, nring, a.max_seq).total;
-    if (smem > 227 * 1024) return false;
+    if ((items_max + grid * kMW - 1) / (grid * kMW) > kMItems) return false;
+    // a CTA's contiguous item range spans at most kMRowsCta rows (any live count)
+    const int per_max = (items_max + grid - 1) / grid;
+    if ((per_max + a.n_kv_heads - 1) / a.n_kv_heads + 1 > kMRowsCta) return false;
+    // 227 KB less the static barriers; the stage pool takes what the per-warp
+    // buffers leave (at least 2 stages of 32 rows per warp)
+    constexpr size_t kBudget = 227 * 1024 - (size_t)kMW * kMMaxRing * 8 - 64;
+    const size_t fixed = 1024 + MhaSmem(kMW, 0, a.max_seq).total;
+    if (fixed + (size_t)kMW * 2 * 32 * kMRow > kBudget) return false;
+    const int pool_kb = (int)std::min<size_t>((kBudget - fixed) >> 10, 192);
+    const size_t smem = fixed + ((size_t)pool_kb << 10);
     auto kern = attention_mha_kernel<kMW, PAGED>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_pdl(kern, dim3(grid), dim3(kMW * 32), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
-               *static_cast<const CUtensorMap*>(a.v_map), *static_cast<const CUtensorMap*>(a.k_map8),
-               *static_cast<const CUtensorMap*>(a.v_map8), a, nring);
+    launch_pdl(kern, dim3(grid), dim3(kMW * 32), smem, s, a, pool_kb);
     EEB_CHECK_LAUNCH();
     return true;
 }
@@ -758,11 +829,10 @@ bool launch_attention_dec(const AttnArgs& a, cudaStream_t s) {
     static const char* env = std::getenv("EEB_ATTN");
     if (env && std::string(env) != "dec" && std::string(env) != "mha") return false;  // A/B against the one-item / pipelined kernels
     static const bool no_mha = env && std::string(env) == "dec";
-    if (!no_mha && a.dtype == 1 && !a.kv_ready && a.k_map && a.v_map && a.k_map8 && a.v_map8 && a.splits <= 16 &&
-        !a.kv_part &&
+    if (!no_mha && a.dtype == 1 && !a.kv_ready && a.splits <= 16 && !a.kv_part &&
         a.n_heads == a.n_kv_heads && a.head_dim == 64 && a.max_seq % 4 == 0) {
         const bool paged = a.page_size != a.max_seq;
-        if (!paged || (a.page_size % kMRows == 0 && a.pages_per_seq <= 32))
+        if (!paged || (a.page_size % 32 == 0 && a.pages_per_seq <= 32))
             if (paged ? launch_mha<true>(a, s) : launch_mha<false>(a, s)) return true;
     }
     if (a.dtype != 1 || a.kv_ready || !a.k_map || !a.v_map || a.splits > 16 || a.kv_part) return false;

@@ -2151,7 +2151,7 @@ eeb_status eeb_debug_stamps_read(eeb_ctx* c, char* json_out, int64_t cap) {
 }
 
 eeb_status eeb_debug_stamps_cta(eeb_ctx* c, int launch, int64_t* start_ns, int64_t* end_ns, int64_t* wait_ns,
-                                int n) {
+                                int64_t* mark_ns, int n) {
     return guarded([&] {
         if (!c || c->stamp_cap <= 0) throw Error(EEB_E_DOMAIN, "stamping is off (eeb_debug_stamps)");
         if (launch < 0 || launch >= (int)c->stamp_last.first.size() || n < 0 || n > kStampCtas)
@@ -2162,8 +2162,8 @@ eeb_status eeb_debug_stamps_cta(eeb_ctx* c, int launch, int64_t* start_ns, int64
         EEB_CUDA(cudaMemcpy(all.data(), c->stamp_buf.p, cells * 8, cudaMemcpyDeviceToHost));
         unsigned long long t0 = ~0ull;
         for (size_t i = 0; i < c->stamp_last.first.size() * kStampCtas; ++i) t0 = std::min(t0, all[i]);
-        std::vector<unsigned long long> h(3 * (size_t)n);
-        for (int w = 0; w < 3; ++w)
+        std::vector<unsigned long long> h(4 * (size_t)n);
+        for (int w = 0; w < 4; ++w)
             EEB_CUDA(cudaMemcpy(h.data() + (size_t)w * n, c->stamp_buf.as<unsigned long long>() + w * cells +
                                 (size_t)launch * kStampCtas, (size_t)n * 8, cudaMemcpyDeviceToHost));
         auto rel = [&](unsigned long long v, bool is_end) -> int64_t {
@@ -2174,6 +2174,7 @@ eeb_status eeb_debug_stamps_cta(eeb_ctx* c, int launch, int64_t* start_ns, int64
             if (start_ns) start_ns[k] = rel(h[k], false);
             if (end_ns) end_ns[k] = rel(h[(size_t)n + k], true);
             if (wait_ns) wait_ns[k] = rel(h[2 * (size_t)n + k], false);
+            if (mark_ns) mark_ns[k] = rel(h[3 * (size_t)n + k], true);
         }
     });
 }

@@ -127,7 +127,7 @@ def load_library() -> C.CDLL:
         lib.eeb_host_stage_layer.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64]
         lib.eeb_host_stage_base.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
         lib.eeb_load_layers_from.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64]
-        lib.eeb_debug_stamps_cta.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+        lib.eeb_debug_stamps_cta.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         lib.eeb_debug_stamps.argtypes = [C.c_void_p, C.c_int]
         lib.eeb_debug_stamps_read.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         lib.eeb_profile_enable.argtypes = [C.c_void_p, C.c_int]
@@ -501,9 +501,10 @@ class Context:
         return json.loads(buf.value.decode())["launches"]
 
     def stamps_cta(self, launch: int, n: int) -> np.ndarray:
-        """[n, 3] per-CTA (start, end, wait) ns of one launch of the last stamped step."""
-        a = np.zeros((3, n), np.int64)
-        _check(self.lib.eeb_debug_stamps_cta(self.h, launch, a[0].ctypes.data, a[1].ctypes.data, a[2].ctypes.data, n))
+        """[n, 4] per-CTA (start, end, wait, mark) ns of one launch of the last stamped step."""
+        a = np.zeros((4, n), np.int64)
+        _check(self.lib.eeb_debug_stamps_cta(self.h, launch, a[0].ctypes.data, a[1].ctypes.data, a[2].ctypes.data,
+                                             a[3].ctypes.data, n))
         return a.T
 
     def profile_enable(self, on: bool) -> None:

@@ -79,18 +79,23 @@ int main(int argc, char** argv) {
     cfg.continuous = true;
     const int seg_len = 256;  // requests per drift segment
     if (drift) {
-        const std::uint64_t mseed = repo.models["opt-1.3b"].arch.seed;
+        // a token's difficulty is per model (its own seeded z): draw tokens
+        // whose z lies in the sampled exit's band for BOTH candidates, so the
+        // segment's law holds whichever model serves
+        const std::uint64_t seed_a = repo.models["opt-1.3b"].arch.seed, seed_b = repo.models["opt-2.7b"].arch.seed;
         const std::vector<double> cum = {0.73, 0.777, 1.0};  // default coverage 73.0 / 4.7 / 22.3 %
         const double murky[3] = {0.3, 0.1, 0.6}, easy[3] = {0.92, 0.05, 0.03};
         cfg.token_fn = [=](std::int64_t rid, int pos, int vocab) -> int32_t {
-            const double* law = (rid / seg_len) % 2 == 0 ? murky : easy;
+            // easy, murky, easy, murky: the first evaluation sees an easy mix
+            // (greedy depth at the first exit), the murky segments then breach
+            const double* law = (rid / seg_len) % 2 == 0 ? easy : murky;
             const double u = (double)synthetic_token(0x5eedULL, rid, pos, 1 << 24) / (double)(1 << 24);
             const int e = u < law[0] ? 0 : (u < law[0] + law[1] ? 1 : 2);
-            const double lo = (e == 0 ? 0.0 : cum[e - 1]) + 0.01, hi = cum[e] - 0.01;
+            const double lo = (e == 0 ? 0.0 : cum[e - 1]) + 0.005, hi = cum[e] - 0.005;
             for (std::uint64_t k = 1;; ++k) {
                 const int32_t t = synthetic_token(0x70c0ULL + k * 0x9e3779b97f4a7c15ULL, rid, pos, vocab);
-                const double z = eeb::synth::z_of(mseed, t);
-                if (z >= lo && z < hi) return t;
+                const double za = eeb::synth::z_of(seed_a, t), zb = eeb::synth::z_of(seed_b, t);
+                if (za >= lo && za < hi && zb >= lo && zb < hi) return t;
             }
         };
     }
@@ -132,7 +137,7 @@ int main(int argc, char** argv) {
         "\"mean_ttft_ms\": %.3f, \"mean_tpot_ms\": %.4f, \"achieved_batch\": %d, \"eval_cycles\": %lld, "
         "\"ld\": %lld, \"sw\": %lld, \"load_bytes\": %lld, \"load_s\": %.4f, \"load_gbs\": %.2f, \"prefill_s\": %.3f, "
         "\"perplexity\": %.6f, \"exit_table_pct\": %s, \"serving_history\": %s}\n",
-        drift ? "drift: alternating murky/easy segments of 256 requests (gen_drift.json exit laws), tokens drawn by synthetic difficulty" : "calibration: uniform tokens",
+        drift ? "drift: easy/murky/easy/murky segments of 256 requests (gen_drift.json exit laws), tokens drawn by synthetic difficulty" : "calibration: uniform tokens",
         eng.slots("opt-1.3b"), eng.slots("opt-2.7b"), n_req, prompt, tokens, (long long)rep.tokens, (long long)rep.steps, rep.throughput_tok_s,
         rep.tokens / run_s, run_s, setup_s, rep.mean_ttft_s * 1e3, rep.mean_tpot_s * 1e3, rep.achieved_batch_size,
         (long long)rep.eval_cycles, (long long)rep.ld_count, (long long)rep.sw_count, (long long)rep.load_bytes,

@@ -83,6 +83,8 @@ def main():
                 print(f"   start {q(c[:, 0] - prev_end / 1e3)}")
                 if (c[:, 2] >= 0).any():
                     print(f"   wait  {q(c[c[:, 2] >= 0][:, 2] - prev_end / 1e3)}")
+                if (c[:, 3] >= 0).any():
+                    print(f"   mark  {q(c[c[:, 3] >= 0][:, 3] - prev_end / 1e3)}")
                 print(f"   end   {q(c[:, 1] - prev_end / 1e3)}")
             prev_end = max(prev_end, l["end_ns"])
         ctx.stamps(0)
