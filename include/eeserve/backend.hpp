@@ -11,6 +11,8 @@
 #pragma once
 
 #include <chrono>
+#include <functional>
+#include <set>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -248,6 +250,93 @@ private:
     std::map<std::string, Entry> handles_;
 };
 
+// The reference's per-token rule (engine.hpp:349-366) applied to one row's
+// record: the observation the policy uses, the exit layer, the breach and
+// unchanged flags, appended to `out`.
+inline void apply_token_policy(const ModelSpec& spec, const ModelTokenRecord& rec, int depth, TokenPolicy policy,
+                               double th, StepOutcome& out) {
+    const ExitObservation* obs = nullptr;
+    int exit_layer = 0;
+    bool breached = false;
+    switch (policy) {
+        case TokenPolicy::flat:
+            obs = &observation_for_depth(rec, depth);
+            exit_layer = depth;
+            breached = obs->confidence < th;
+            break;
+        case TokenPolicy::full_depth:
+            obs = &rec.observations.back();
+            exit_layer = spec.num_layers;
+            break;
+        default:
+            obs = &earliest_confident_obs(rec, th);
+            exit_layer = obs->layer;
+            breached = obs->confidence < th;
+            break;
+    }
+    if (out.hist.empty()) out.hist.assign(spec.exit_layers.size(), 0);
+    out.obs.push_back(*obs);
+    out.exit_layer.push_back(exit_layer);
+    out.breached.push_back(breached ? 1 : 0);
+    out.unchanged.push_back(obs->token_id == rec.final_token_id ? 1 : 0);
+    out.hist[exit_index(spec.exit_layers, obs->layer)] += 1;
+    out.n_breached += breached ? 1 : 0;
+    out.sum_logprob += obs->logprob;
+    if (policy == TokenPolicy::profile) out.records.push_back(rec);
+}
+
+// ---------------------------------------------------------------------------
+// Profile backend: the reference's serve_one semantics over live GPU decode.
+// Every step runs every exit head on the GPU at full depth (EEB_PROFILE: the
+// ModelTokenRecord the reference would look up in its trace,
+// engine.hpp:345) and applies the reference's token rule on the host, so a
+// BatchedEngine over it reproduces Simulator::run on the records the GPU
+// produces — the same decisions, exit tables and breach actions.  Times are
+// the reference's modelled ones (loads bytes / bandwidth, prefill and decode
+// per layer), so whole reports compare exactly.  Also a trace recorder: the
+// records of every step can be collected and written as a reference trace.
+// ---------------------------------------------------------------------------
+class ProfileBackend final : public DecodeBackend {
+public:
+    explicit ProfileBackend(CudaBackend& gpu) : gpu_(gpu) {}
+    void register_model(const ModelSpec& spec, int max_slots, int max_seq_len) override {
+        specs_[spec.id] = spec;
+        gpu_.register_model(spec, max_slots, max_seq_len);
+    }
+    LoadResult load(const std::string& model, int depth) override {
+        // every head needs every layer: resident at full depth on first use
+        if (depth > 0 && !full_.count(model)) {
+            gpu_.load(model, specs_.at(model).num_layers);
+            full_.insert(model);
+        }
+        return {};
+    }
+    double prefill(const std::string& model, int, const PrefillRows& rows) override {
+        gpu_.prefill(model, specs_.at(model).num_layers, rows);  // full-depth KV (profiled decode attends it)
+        return 0.0;
+    }
+    StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
+                     const StepRows& rows) override {
+        const ModelSpec& spec = specs_.at(model);
+        const StepOutcome gpu = gpu_.step(model, 0, TokenPolicy::profile, th, rows);
+        StepOutcome out;
+        for (int i = 0; i < rows.size(); ++i) {
+            apply_token_policy(spec, gpu.records[i], depth, policy, th, out);
+            if (recorder) recorder(model, rows.request_ids[i], rows.token_index[i], gpu.records[i]);
+        }
+        return out;
+    }
+    void release(const std::string& model, int slot) override { gpu_.release(model, slot); }
+
+    /// Called with every row's record (model, request id, token index, record).
+    std::function<void(const std::string&, std::int64_t, int, const ModelTokenRecord&)> recorder;
+
+private:
+    CudaBackend& gpu_;
+    std::map<std::string, ModelSpec> specs_;
+    std::set<std::string> full_;
+};
+
 // ---------------------------------------------------------------------------
 // Trace backend: the reference's token oracle, batched.
 // ---------------------------------------------------------------------------
@@ -263,39 +352,11 @@ public:
     StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
                      const StepRows& rows) override {
         const ModelSpec& spec = specs_.at(model);
-        const int b = rows.size();
         StepOutcome out;
         out.hist.assign(spec.exit_layers.size(), 0);
-        for (int i = 0; i < b; ++i) {
+        for (int i = 0; i < rows.size(); ++i) {
             const TraceRequest& req = *by_id_.at(rows.request_ids[i]);
-            const ModelTokenRecord& rec = req.tokens.at(rows.token_index[i]).for_model(model);
-            const ExitObservation* obs = nullptr;
-            int exit_layer = 0;
-            bool breached = false;
-            switch (policy) {
-                case TokenPolicy::flat:
-                    obs = &observation_for_depth(rec, depth);
-                    exit_layer = depth;
-                    breached = obs->confidence < th;
-                    break;
-                case TokenPolicy::full_depth:
-                    obs = &rec.observations.back();
-                    exit_layer = spec.num_layers;
-                    break;
-                default:
-                    obs = &earliest_confident_obs(rec, th);
-                    exit_layer = obs->layer;
-                    breached = obs->confidence < th;
-                    break;
-            }
-            out.obs.push_back(*obs);
-            out.exit_layer.push_back(exit_layer);
-            out.breached.push_back(breached ? 1 : 0);
-            out.unchanged.push_back(obs->token_id == rec.final_token_id ? 1 : 0);
-            out.hist[exit_index(spec.exit_layers, obs->layer)] += 1;
-            out.n_breached += breached ? 1 : 0;
-            out.sum_logprob += obs->logprob;
-            if (policy == TokenPolicy::profile) out.records.push_back(rec);
+            apply_token_policy(spec, req.tokens.at(rows.token_index[i]).for_model(model), depth, policy, th, out);
         }
         return out;
     }

@@ -278,6 +278,7 @@ private:
                 for (size_t i = 0; i < n; ++i) batch.push_back(&reqs[cursor_ + i]);
                 cursor_ += n;
                 served += (int)n;
+                since_eval_ += (std::int64_t)n;  // evaluation requests count toward ri (serve_one, engine.hpp:331)
                 serve_batch(batch, id, spec.num_layers, TokenPolicy::profile, true);
             }
             emit("eval_phase_end", JsonFields().str("model", id));

@@ -51,6 +51,29 @@ def build_serve_c3(verbose: bool = False) -> Path:
     return out
 
 
+def build_replay_gpu(verbose: bool = False) -> Path | None:
+    """tests/_bin/test_replay_gpu: GPU-recorded traces replayed by the compiled reference (needs a GPU to run)."""
+    ref = ROOT / "oracle" / "_ref" / "libeeref.so"
+    src = ROOT / "tests" / "cpp" / "test_replay_gpu.cpp"
+    out = ROOT / "tests" / "_bin" / "test_replay_gpu"
+    lib = ROOT / "paper_2504_10724_b200"
+    if not ref.exists() or not Path(JSON_INC).is_dir():
+        return None
+    deps = [src, ref, lib / "libeeb.so", ROOT / "include" / "eeb" / "eeb.h", *(ROOT / "include" / "eeserve").glob("*.hpp")]
+    if out.exists() and all(d.stat().st_mtime <= out.stat().st_mtime for d in deps):
+        return out
+    out.parent.mkdir(exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{JSON_INC}", "-I/usr/local/cuda/include",
+           str(src), "-o", str(out), f"-L{ref.parent}", "-leeref", f"-Wl,-rpath,{ref.parent}",
+           f"-L{lib}", "-leeb", f"-Wl,-rpath,{lib}", "-L/usr/local/cuda/lib64", "-lcudart"]
+    if verbose:
+        print(" ".join(cmd))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"replay GPU test build failed:\n{r.stderr}")
+    return out
+
+
 def build_host(verbose: bool = False) -> Path | None:
     ref = ROOT / "oracle" / "_ref" / "libeeref.so"
     src = ROOT / "tests" / "cpp" / "test_host.cpp"

@@ -34,8 +34,9 @@ def analyse(launches: list[dict]) -> dict:
     last = t0
     rows = []
     for l in launches:
-        if l["ctas"] <= 0:  # launched with zero CTAs recorded (should not happen)
-            rows.append({**l, "crit_ns": 0, "busy_ns": 0})
+        if l["ctas"] <= 0:  # not run (a conditional graph body switched off)
+            rows.append({**l, "kind": kernel_kind(l["kernel"]), "crit_ns": 0, "busy_ns": 0, "lat_ns": -1,
+                         "work_ns": -1, "tail_ns": -1})
             continue
         crit = max(0, l["end_ns"] - last)
         w = l.get("wait_ns", -1)

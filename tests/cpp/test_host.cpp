@@ -454,15 +454,19 @@ TEST_CASE(decide_action_matches_reference_randomized) {
 
 // ---- the batched engine replaying reference traces at batch 1 ---------------------------
 static void engine_matches_reference(const std::string& trace_path, const std::string& mode_str, Mode mode,
-                                     const std::string& model, int k, bool continuous = false) {
+                                     const std::string& model, int k, bool continuous = false, int ri = 150,
+                                     int window = 100, int cbc_max = 50) {
     const ModelRepository repo = load_repo(fx("repo_opt.json"));
     const Trace trace = load_trace(trace_path);
     const MemoryConfig mem{40'000'000'000, 1'000'000'000, 256, 8.4e9};
     PolicyConfig pol;
     pol.k = k;
     pol.n_eval_requests = 5;
-    pol.ri = 150;
-    const std::string pj = Json{{"k", k}, {"n_eval_requests", 5}, {"ri", 150}}.dump();
+    pol.ri = ri;
+    pol.window = window;
+    pol.cbc_max = cbc_max;
+    const std::string pj =
+        Json{{"k", k}, {"n_eval_requests", 5}, {"ri", ri}, {"window", window}, {"cbc_max", cbc_max}}.dump();
     const std::string mj = Json{{"capacity_bytes", mem.capacity_bytes}, {"reserve_bytes", mem.reserve_bytes},
                                 {"max_seq_len", 256}, {"bandwidth_bytes_per_s", 8.4e9}}.dump();
     std::vector<char> buf(1 << 24);
@@ -574,6 +578,16 @@ TEST_CASE(event_log_aggregates_to_engine_report_at_batch_4) {
         for (const auto& [l, pct] : per)
             CHECK(approx(agg.at("exit_table").at(m).at(std::to_string(l)).get<double>(), pct, 1e-12));
     CHECK(agg.at("per_request").size() == reqs.size());
+}
+
+// Breach actions: the drift workload (fixtures/gen_drift.json) at the
+// reference's drift policy (exp_drift.json: k 1, ri 300, window 100,
+// cbc_max 50) and at a tighter breach window that also switches models.
+TEST_CASE(engine_matches_reference_under_breaches) {
+    const std::string gen = "/tmp/eeserve_gen_drift.jsonl";
+    CHECK(ref_generate_trace(fx("gen_drift.json").c_str(), fx("repo_opt.json").c_str(), gen.c_str()) == 3000);
+    engine_matches_reference(gen, "helios", Mode::helios, "", 1, false, 300, 100, 50);
+    engine_matches_reference(gen, "helios", Mode::helios, "", 1, false, 40, 20, 5);
 }
 
 TEST_CASE(engine_replays_reference_traces_at_batch_1) {
