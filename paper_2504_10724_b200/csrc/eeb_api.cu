@@ -190,8 +190,7 @@ struct eeb_ctx {
     int pf_cur_items = 0;           // query blocks of the chunk being enqueued (graph key)
     void* pf_pin = nullptr;
     size_t pf_pin_bytes = 0;
-    eeb::DevBuf o_exit, o_tok, o_conf, o_logp, o_breach, o_unch, o_bin, o_hist, o_nbr, o_sum;
-    eeb::DevBuf o_htok, o_hconf, o_hlogp;
+    eeb::DevBuf o_all;  // the step's outputs, one block (OutLayout): one D2H copy per host-API step
     std::vector<std::unique_ptr<eeb::DevBuf>> logits_keep;
     int64_t ws_elems = 0;
     // pinned staging for the host-pointer API
@@ -746,6 +745,36 @@ void stamp_reset(eeb_ctx* c) {
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + 3 * cells, 0, cells * 8, c->stream));
 }
 
+// Byte offsets of the step outputs inside ctx->o_all for R rows and up to ne
+// exit heads: the per-row / per-step outputs first (common_end), the
+// per-head arrays of a profiling step after them.
+struct OutLayout {
+    size_t exit, tok, conf, logp, breach, unch, bin, hist, nbr, sum, common_end, htok, hconf, hlogp, total;
+    OutLayout(int R, int ne) {
+        size_t o = 0;
+        auto take = [&](size_t bytes) {
+            const size_t at = o;
+            o = (o + bytes + 255) & ~(size_t)255;
+            return at;
+        };
+        exit = take((size_t)R * 4);
+        tok = take((size_t)R * 4);
+        conf = take((size_t)R * 4);
+        logp = take((size_t)R * 4);
+        breach = take((size_t)R);
+        unch = take((size_t)R);
+        hist = take(64 * 8);
+        nbr = take(8);
+        sum = take(8);
+        common_end = o;
+        bin = take((size_t)R * 4);
+        htok = take((size_t)R * ne * 4);
+        hconf = take((size_t)R * ne * 4);
+        hlogp = take((size_t)R * ne * 4);
+        total = o;
+    }
+};
+
 // Size the step workspace for `batch` rows of model m.  Buffers are shared by
 // every model of the context and grow to the largest; whenever one moves, every
 // captured graph (of any model: a smaller model's graph holds the old pointer)
@@ -800,20 +829,8 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     if (m.tp > 1) moved |= c->tp_partial.ensure((size_t)R * D * 4);
     moved |= c->head_conf.ensure((size_t)R * 4);
     moved |= c->head_logp.ensure((size_t)R * 4);
-    moved |= c->o_exit.ensure((size_t)R * 4);
-    moved |= c->o_tok.ensure((size_t)R * 4);
-    moved |= c->o_conf.ensure((size_t)R * 4);
-    moved |= c->o_logp.ensure((size_t)R * 4);
-    moved |= c->o_breach.ensure((size_t)R);
-    moved |= c->o_unch.ensure((size_t)R);
-    moved |= c->o_bin.ensure((size_t)R * 4);
-    moved |= c->o_hist.ensure(64 * 8);
-    moved |= c->o_nbr.ensure(8);
-    moved |= c->o_sum.ensure(8);
-    moved |= c->o_htok.ensure((size_t)R * d.n_exits * 4);
-    moved |= c->o_hconf.ensure((size_t)R * d.n_exits * 4);
-    moved |= c->o_hlogp.ensure((size_t)R * d.n_exits * 4);
-    const size_t pin_need = (size_t)R * (3 * 4 + 6 * 4 + 2 + 3 * 64 * 4) + 1024;
+    moved |= c->o_all.ensure(OutLayout(R, 64).total);
+    const size_t pin_need = (size_t)R * 3 * 4 + 256 + OutLayout(R, 64).total;
     if (pin_need > c->pin_bytes) {
         if (c->pin) cudaFreeHost(c->pin);
         c->pin = nullptr;
@@ -825,19 +842,21 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
 
 StepOutDev out_dev(eeb_ctx* c) {
     StepOutDev o;
-    o.exit_layer = c->o_exit.as<int32_t>();
-    o.token_id = c->o_tok.as<int32_t>();
-    o.confidence = c->o_conf.as<float>();
-    o.logprob = c->o_logp.as<float>();
-    o.breached = c->o_breach.as<uint8_t>();
-    o.unchanged = c->o_unch.as<uint8_t>();
-    o.bin = c->o_bin.as<int32_t>();
-    o.hist = c->o_hist.as<int64_t>();
-    o.n_breached = c->o_nbr.as<int64_t>();
-    o.sum_logprob = c->o_sum.as<double>();
-    o.head_token = c->o_htok.as<int32_t>();
-    o.head_confidence = c->o_hconf.as<float>();
-    o.head_logprob = c->o_hlogp.as<float>();
+    const OutLayout L(c->cap_rows, 64);
+    char* b = static_cast<char*>(c->o_all.p);
+    o.exit_layer = reinterpret_cast<int32_t*>(b + L.exit);
+    o.token_id = reinterpret_cast<int32_t*>(b + L.tok);
+    o.confidence = reinterpret_cast<float*>(b + L.conf);
+    o.logprob = reinterpret_cast<float*>(b + L.logp);
+    o.breached = reinterpret_cast<uint8_t*>(b + L.breach);
+    o.unchanged = reinterpret_cast<uint8_t*>(b + L.unch);
+    o.bin = reinterpret_cast<int32_t*>(b + L.bin);
+    o.hist = reinterpret_cast<int64_t*>(b + L.hist);
+    o.n_breached = reinterpret_cast<int64_t*>(b + L.nbr);
+    o.sum_logprob = reinterpret_cast<double*>(b + L.sum);
+    o.head_token = reinterpret_cast<int32_t*>(b + L.htok);
+    o.head_confidence = reinterpret_cast<float*>(b + L.hconf);
+    o.head_logprob = reinterpret_cast<float*>(b + L.hlogp);
     return o;
 }
 
@@ -1882,48 +1901,45 @@ eeb_status eeb_decode_step(eeb_ctx* c, int model, int depth, int policy, float t
         Ints I = ints_of(c);
         cudaStream_t s = c->stream;
         // inputs: pinned staging → device
+        // inputs: the three row arrays are adjacent on the device (stride
+        // cap_rows): staged the same way in pinned memory, one H2D copy
+        const int R = c->cap_rows;
         char* pin = static_cast<char*>(c->pin);
         int32_t* pin_in = reinterpret_cast<int32_t*>(pin);
         std::memcpy(pin_in, input_tokens, (size_t)batch * 4);
-        std::memcpy(pin_in + batch, slot_ids, (size_t)batch * 4);
-        std::memcpy(pin_in + 2 * batch, positions, (size_t)batch * 4);
-        EEB_CUDA(cudaMemcpyAsync(I.tok, pin_in, (size_t)batch * 4, cudaMemcpyHostToDevice, s));
-        EEB_CUDA(cudaMemcpyAsync(I.slot, pin_in + batch, (size_t)batch * 4, cudaMemcpyHostToDevice, s));
-        EEB_CUDA(cudaMemcpyAsync(I.pos, pin_in + 2 * batch, (size_t)batch * 4, cudaMemcpyHostToDevice, s));
+        std::memcpy(pin_in + R, slot_ids, (size_t)batch * 4);
+        std::memcpy(pin_in + 2 * R, positions, (size_t)batch * 4);
+        EEB_CUDA(cudaMemcpyAsync(I.tok, pin_in, (size_t)(2 * R + batch) * 4, cudaMemcpyHostToDevice, s));
         run_step(c, model, depth, policy, th, batch);
-        // outputs: device → pinned staging → caller
-        char* po = pin + (size_t)batch * 12 + 256;
-        po = reinterpret_cast<char*>(((uintptr_t)po + 255) & ~(uintptr_t)255);
-        struct Item { void* dst; const void* src; size_t bytes; };
-        std::vector<Item> items;
+        // outputs: one D2H copy of the output block into pinned staging, then
+        // the requested arrays to the caller
+        const OutLayout L(R, 64);
+        char* po = reinterpret_cast<char*>(((uintptr_t)(pin + (size_t)R * 12) + 255) & ~(uintptr_t)255);
         const int ne = m.desc.n_exits;
         if (out) {
-            auto add = [&](void* dst, const DevBuf& src, size_t bytes) {
-                if (dst) items.push_back({dst, src.p, bytes});
-            };
-            add(out->exit_layer, c->o_exit, (size_t)batch * 4);
-            add(out->token_id, c->o_tok, (size_t)batch * 4);
-            add(out->confidence, c->o_conf, (size_t)batch * 4);
-            add(out->logprob, c->o_logp, (size_t)batch * 4);
-            add(out->breached, c->o_breach, (size_t)batch);
-            add(out->unchanged, c->o_unch, (size_t)batch);
-            add(out->hist, c->o_hist, (size_t)ne * 8);
-            add(out->n_breached, c->o_nbr, 8);
-            add(out->sum_logprob, c->o_sum, 8);
-            if (policy == EEB_PROFILE) {
-                add(out->head_token, c->o_htok, (size_t)batch * ne * 4);
-                add(out->head_confidence, c->o_hconf, (size_t)batch * ne * 4);
-                add(out->head_logprob, c->o_hlogp, (size_t)batch * ne * 4);
-            }
-        }
-        std::vector<char*> staged;
-        for (auto& it : items) {
-            staged.push_back(po);
-            EEB_CUDA(cudaMemcpyAsync(po, it.src, it.bytes, cudaMemcpyDeviceToHost, s));
-            po += (it.bytes + 255) & ~(size_t)255;
+            const size_t n = policy == EEB_PROFILE ? L.total : L.common_end;
+            EEB_CUDA(cudaMemcpyAsync(po, c->o_all.p, n, cudaMemcpyDeviceToHost, s));
         }
         EEB_CUDA(cudaStreamSynchronize(s));
-        for (size_t k = 0; k < items.size(); ++k) std::memcpy(items[k].dst, staged[k], items[k].bytes);
+        if (out) {
+            auto put = [&](void* dst, size_t off, size_t bytes) {
+                if (dst) std::memcpy(dst, po + off, bytes);
+            };
+            put(out->exit_layer, L.exit, (size_t)batch * 4);
+            put(out->token_id, L.tok, (size_t)batch * 4);
+            put(out->confidence, L.conf, (size_t)batch * 4);
+            put(out->logprob, L.logp, (size_t)batch * 4);
+            put(out->breached, L.breach, (size_t)batch);
+            put(out->unchanged, L.unch, (size_t)batch);
+            put(out->hist, L.hist, (size_t)ne * 8);
+            put(out->n_breached, L.nbr, 8);
+            put(out->sum_logprob, L.sum, 8);
+            if (policy == EEB_PROFILE) {
+                put(out->head_token, L.htok, (size_t)batch * ne * 4);
+                put(out->head_confidence, L.hconf, (size_t)batch * ne * 4);
+                put(out->head_logprob, L.hlogp, (size_t)batch * ne * 4);
+            }
+        }
         harvest_profile(c);
     });
 }
@@ -1947,22 +1963,23 @@ eeb_status eeb_decode_step_device(eeb_ctx* c, int model, int depth, int policy, 
         run_step(c, model, depth, policy, th, batch);
         if (d_out) {
             const int ne = m.desc.n_exits;
-            auto cp = [&](void* dst, const DevBuf& src, size_t bytes) {
-                if (dst) EEB_CUDA(cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDeviceToDevice, s));
+            const StepOutDev od = out_dev(c);
+            auto cp = [&](void* dst, const void* src, size_t bytes) {
+                if (dst) EEB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
             };
-            cp(d_out->exit_layer, c->o_exit, (size_t)batch * 4);
-            cp(d_out->token_id, c->o_tok, (size_t)batch * 4);
-            cp(d_out->confidence, c->o_conf, (size_t)batch * 4);
-            cp(d_out->logprob, c->o_logp, (size_t)batch * 4);
-            cp(d_out->breached, c->o_breach, (size_t)batch);
-            cp(d_out->unchanged, c->o_unch, (size_t)batch);
-            cp(d_out->hist, c->o_hist, (size_t)ne * 8);
-            cp(d_out->n_breached, c->o_nbr, 8);
-            cp(d_out->sum_logprob, c->o_sum, 8);
+            cp(d_out->exit_layer, od.exit_layer, (size_t)batch * 4);
+            cp(d_out->token_id, od.token_id, (size_t)batch * 4);
+            cp(d_out->confidence, od.confidence, (size_t)batch * 4);
+            cp(d_out->logprob, od.logprob, (size_t)batch * 4);
+            cp(d_out->breached, od.breached, (size_t)batch);
+            cp(d_out->unchanged, od.unchanged, (size_t)batch);
+            cp(d_out->hist, od.hist, (size_t)ne * 8);
+            cp(d_out->n_breached, od.n_breached, 8);
+            cp(d_out->sum_logprob, od.sum_logprob, 8);
             if (policy == EEB_PROFILE) {
-                cp(d_out->head_token, c->o_htok, (size_t)batch * ne * 4);
-                cp(d_out->head_confidence, c->o_hconf, (size_t)batch * ne * 4);
-                cp(d_out->head_logprob, c->o_hlogp, (size_t)batch * ne * 4);
+                cp(d_out->head_token, od.head_token, (size_t)batch * ne * 4);
+                cp(d_out->head_confidence, od.head_confidence, (size_t)batch * ne * 4);
+                cp(d_out->head_logprob, od.head_logprob, (size_t)batch * ne * 4);
             }
         }
         if (c->profiling) harvest_profile(c);
