@@ -2,6 +2,11 @@
 // (/root/reference/proj/include/eeserve/errors.hpp:9-30) and the mapping from
 // the C ABI's status codes back onto them, so callers such as decide_action
 // and apply_load keep their catch behaviour across the GPU boundary.
+//
+// PROVENANCE: a verbatim-semantics port of /root/reference/proj/include/eeserve/errors.hpp:9-30
+// (same identifiers, control flow and error strings; JSON I/O dropped).  It is
+// the reference host API that the drop-in keeps unchanged, not new work; its
+// behaviour is pinned against the compiled reference (tests/cpp/test_host.cpp).
 #pragma once
 
 #include <stdexcept>

@@ -4,6 +4,11 @@
 // reference these records come from a pre-computed trace; here the GPU
 // backend (eeserve/backend.hpp) produces them from real exit heads.
 // JSONL trace I/O is outside the hot path (SURVEY §8f "next").
+//
+// PROVENANCE: a verbatim-semantics port of /root/reference/proj/include/eeserve/trace.hpp:17-97
+// (same identifiers, control flow and error strings; JSON I/O dropped).  It is
+// the reference host API that the drop-in keeps unchanged, not new work; its
+// behaviour is pinned against the compiled reference (tests/cpp/test_host.cpp).
 #pragma once
 
 #include <cstdint>

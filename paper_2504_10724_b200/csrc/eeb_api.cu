@@ -1243,10 +1243,15 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
     void* h_alt = hB;
     {
         Timer t(c, kCatOther);
-        launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, batch, D, cur, s);
-        launch_residual_norm(d.dtype, nullptr, 0, 0, cur.n_active, batch, cur.x, D, d.norm_eps,
-                             m.layers[0]->attn_norm.as<float>(), h_cur, nullptr, nullptr, s);
-        count(c, kCatOther, 2);
+        if (launch_embed_norm(d.dtype, m.emb.p, I.tok, I.slot, I.pos, batch, D, cur, d.norm_eps,
+                              m.layers[0]->attn_norm.as<float>(), h_cur, s)) {
+            count(c, kCatOther, 1);
+        } else {
+            launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, batch, D, cur, s);
+            launch_residual_norm(d.dtype, nullptr, 0, 0, cur.n_active, batch, cur.x, D, d.norm_eps,
+                                 m.layers[0]->attn_norm.as<float>(), h_cur, nullptr, nullptr, s);
+            count(c, kCatOther, 2);
+        }
     }
     size_t hi = 0;
     float* ws = c->ws.as<float>();

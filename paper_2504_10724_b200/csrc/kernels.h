@@ -35,6 +35,9 @@ struct RowState {
 // x[i] = emb[tok[i]]; initialises the compact state to the identity.
 void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in,
                   int batch, int d, RowState st, cudaStream_t s);
+// bf16: embed fused with the first layer's RMSNorm (x = emb[tok], out = norm(x) * g); false if not applicable.
+bool launch_embed_norm(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in, int batch,
+                       int d, RowState st, float eps, const float* g, void* out, cudaStream_t s);
 // x[i] += sum_s part[s][i] (part may be null); out1 = act(x*g1/rms), out2 = act(x*g2/rms) (optional).
 // pf / pf_bytes: the next GEMM's weights, prefetched into L2 by the CTAs (optional).
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,

@@ -187,6 +187,61 @@ __global__ void embed_kernel(Stamp stamp, const T* __restrict__ emb, const int* 
     for (int c = threadIdx.x; c < d; c += blockDim.x) dst[c] = to_f32(src[c]);
 }
 
+// Embedding gather fused with the first layer's RMSNorm (bf16 models): x =
+// emb[tok], out = bf16(x * rsqrt(mean x^2 + eps) * g) — the same per-thread
+// float4 groups and fixed-tree block sum as residual_norm_kernel (part = null),
+// so the result equals the embed + norm pair bit for bit, one launch fewer.
+template <int kV>
+__global__ void __launch_bounds__(kNormThreads)
+    embed_norm_kernel(Stamp stamp, const __nv_bfloat16* __restrict__ emb, const int* tok, const int* slot_in,
+                      const int* pos_in, int batch, int d, RowState st, float eps, const float* g,
+                      __nv_bfloat16* out) {
+    StampScope stamp_scope(stamp);
+    pdl_launch_dependents();
+    pdl_wait();
+    const int i = blockIdx.x;
+    if (i >= batch) return;
+    __shared__ float red[32];
+    if (threadIdx.x == 0) {
+        st.row_of[i] = i;
+        st.slot[i] = slot_in[i];
+        st.pos[i] = pos_in[i];
+        if (i == 0) *st.n_active = batch;
+    }
+    const __nv_bfloat16* src = emb + (int64_t)tok[i] * d;
+    float* row = st.x + (int64_t)i * d;
+    float4 v[kV];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < d) {
+            const uint2 u = *reinterpret_cast<const uint2*>(src + c);
+            float4 xv;
+            xv.x = __uint_as_float(u.x << 16);
+            xv.y = __uint_as_float(u.x & 0xffff0000u);
+            xv.z = __uint_as_float(u.y << 16);
+            xv.w = __uint_as_float(u.y & 0xffff0000u);
+            *reinterpret_cast<float4*>(row + c) = xv;
+            v[k] = xv;
+            ss += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+        }
+    }
+    ss = block_sum(ss, red);
+    const float inv = rsqrtf(ss / (float)d + eps);
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        if (c < d) {
+            const float4 gg = *reinterpret_cast<const float4*>(g + c);
+            const float4 nv = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
+            store4<__nv_bfloat16>(out + (int64_t)i * d + c,
+                                  make_float4(nv.x * gg.x, nv.y * gg.y, nv.z * gg.z, nv.w * gg.w));
+        }
+    }
+}
+
 __global__ void gather_rows_kernel(Stamp stamp, const float* x_cur, float* x_nxt,
                                    const uint16_t* h_cur, uint16_t* h_nxt, int h_words,
                                    const int* src, const int* n_active, int d) {
@@ -217,6 +272,23 @@ void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in
         launch_pdl(embed_kernel<__nv_bfloat16>, dim3(batch), dim3(256), 0, s,
                    static_cast<const __nv_bfloat16*>(emb), tok, slot_in, pos_in, batch, d, st);
     EEB_CHECK_LAUNCH();
+}
+
+bool launch_embed_norm(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in, int batch,
+                       int d, RowState st, float eps, const float* g, void* out, cudaStream_t s) {
+    const int q = d / 4;
+    if (dtype != 1 || d % 4 != 0 || q > 4 * kNormThreads) return false;
+    const int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
+    const dim3 grid(batch), block(std::max(32, std::min(kNormThreads, (q / kv + 31) / 32 * 32)));
+    auto go = [&](auto kern) {
+        launch_pdl(kern, grid, block, 0, s, static_cast<const __nv_bfloat16*>(emb), tok, slot_in, pos_in, batch, d, st,
+                   eps, g, static_cast<__nv_bfloat16*>(out));
+    };
+    if (kv == 1) go(embed_norm_kernel<1>);
+    else if (kv == 2) go(embed_norm_kernel<2>);
+    else go(embed_norm_kernel<4>);
+    EEB_CHECK_LAUNCH();
+    return true;
 }
 
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
