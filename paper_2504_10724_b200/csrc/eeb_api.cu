@@ -1098,10 +1098,17 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         count(c, kCatNorm, 1);
     }
     static const bool act_unfused = std::getenv("EEB_ACT_UNFUSED") != nullptr;  // A/B
+    // The activation fused into the up GEMM (4-CTA clusters reducing K on chip)
+    // pays off at decode batches; above 128 rows the on-chip reduction of the
+    // wide accumulator tile dominates (C2 batch 256: 44 us fused vs 15 + 10 us
+    // planes + activation kernel), so larger batches take the split-K planes.
+    static const int act_fused_max = std::getenv("EEB_ACT_FUSED_MAX_ROWS")
+                                         ? std::atoi(std::getenv("EEB_ACT_FUSED_MAX_ROWS"))
+                                         : 128;
     for (int sh = 0; sh < m.shards; ++sh) {
         void* act_dst = static_cast<char*>(c->mlp_h.p) + (size_t)sh * batch * m.f_l * wb;
         const void* wup = static_cast<const char*>(W.wup.p) + (size_t)sh * m.up_l * D * wb;
-        if (!act_unfused && !skip_cat("gemm") && d.dtype == EEB_BF16 && c->gemm_tier != 1) {
+        if (!act_unfused && batch <= act_fused_max && !skip_cat("gemm") && d.dtype == EEB_BF16 && c->gemm_tier != 1) {
             // up projection with the activation in its epilogue (one split)
             Timer t(c, kCatGemm);
             GemmArgs ga;
@@ -2021,7 +2028,7 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
         wait_layers(c, m, depth);
         static const int env_chunk = std::getenv("EEB_PREFILL_CHUNK") ? std::atoi(std::getenv("EEB_PREFILL_CHUNK")) : 0;
         const int chunk = d.dtype == EEB_BF16 ? (env_chunk >= 16 && env_chunk <= 256 ? env_chunk : 256)
-                                              : 64;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
+                                              : 128;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
         ensure_workspace(c, m, (int)std::min<int64_t>(chunk, total));
         // (tok, slot, pos) of every prompt token: one pinned staging + one H2D,
         // then a device-to-device slice per chunk.

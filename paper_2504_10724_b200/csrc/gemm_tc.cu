@@ -167,6 +167,7 @@ struct TcParams {
     int skip_dead;              // read n_active before the weight prefetch (skip it when 0)
     int l2pf;                   // L2-prefetch the weight tiles beyond the smem stages before the PDL wait
     int tma_out;                // split-K planes written by a TMA store of the smem-staged tile (tmap_o)
+    int orows, obufs;           // rows per TMA store chunk, smem buffers (1 or 2)
     Stamp st;                   // in-graph launch timeline (eeb_debug_stamps)
 };
 
@@ -412,33 +413,47 @@ __global__ void __launch_bounds__(kThreads, 2)
             // is 32 consecutive floats per warp, conflict-free) and written by
             // one TMA bulk tensor store — per-thread global stores of the
             // same 32 KB cost ~2.4 us of the GEMM's tail (measured in the C2 step).
-            float* stg = reinterpret_cast<float*>(base_ptr);
+            // Large row counts (prefill chunks, batch >= 128) go in chunks of
+            // p.orows rows through two alternating smem buffers.
             const int f = quarter * 32 + lane;
             const int lim = min(rows, p.bpad);
-            int c0 = 0;
-            for (; c0 + 32 <= p.bpad && c0 < lim; c0 += 32) {
-                float v[32];
-                tmem_ld32(taddr + (uint32_t)c0, v);  // warp-collective
+            const int OR = p.orows;
+            const uint32_t buf_floats = (uint32_t)OR * kBM;
+            for (int r0 = 0, b = 0; r0 < lim; r0 += OR, b ^= 1) {
+                float* stg = reinterpret_cast<float*>(base_ptr) + (p.obufs > 1 ? b * buf_floats : 0);
+                if (r0 > 0 && (r0 >= 2 * OR || p.obufs == 1)) {  // this buffer's previous store has read its smem
+                    if (threadIdx.x == 64) {
+                        if (p.obufs > 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                }
+                const int rend = min(lim, r0 + OR);
+                int c0 = r0;
+                for (; c0 + 32 <= r0 + OR && c0 < rend; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + (uint32_t)c0, v);  // warp-collective
 #pragma unroll
-                for (int j = 0; j < 32; ++j) stg[(c0 + j) * kBM + f] = v[j];
-            }
-            for (; c0 < lim; c0 += 16) {
-                float v[16];
-                tmem_ld16(taddr + (uint32_t)c0, v);
+                    for (int j = 0; j < 32; ++j) stg[(c0 - r0 + j) * kBM + f] = v[j];
+                }
+                for (; c0 < rend; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(taddr + (uint32_t)c0, v);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) stg[(c0 + j) * kBM + f] = v[j];
+                    for (int j = 0; j < 16; ++j) stg[(c0 - r0 + j) * kBM + f] = v[j];
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> TMA reads
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (threadIdx.x == 64) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tmap_o)),
+                        "r"(m_tile * kBM), "r"(r0), "r"(split), "r"(smem_u32(stg))
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> TMA reads
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (threadIdx.x == 64) {
-                asm volatile(
-                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmap_o)),
-                    "r"(m_tile * kBM), "r"(0), "r"(split), "r"(smem_u32(stg))
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // written before the grid completes
-            }
+            if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // written before the grid completes
         } else if (p.cs == 1) {
             float* plane = p.part + (int64_t)split * p.split_stride;
             // only the live rows' columns (warp-uniform bound), 32 per wait
@@ -777,11 +792,25 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     static const bool env_tma_out = !std::getenv("EEB_TC_TMA_OUT") || std::atoi(std::getenv("EEB_TC_TMA_OUT")) != 0;
     CUtensorMap mo = mw;  // (unused unless tma_out)
     p.tma_out = 0;
-    if (env_tma_out && !a.head_tri && !a.act_out && cs == 1 && a.out && (size_t)bpad * kBM * 4 <= (size_t)stages * stage_bytes &&
+    // rows per store chunk: the whole tile when the drained stages hold it,
+    // else 32-row multiples, double-buffered when two chunks fit
+    const size_t stage_smem = (size_t)stages * stage_bytes;
+    int orows = (size_t)bpad * kBM * 4 <= stage_smem ? bpad : (int)(stage_smem / (kBM * 4)) / 32 * 32;
+    int obufs = 1;
+    if (orows < bpad) {
+        const int o2 = (int)(stage_smem / (2 * kBM * 4)) / 32 * 32;
+        if (o2 >= 32) {
+            orows = o2;
+            obufs = 2;
+        }
+    }
+    p.orows = orows;
+    p.obufs = obufs;
+    if (env_tma_out && !a.head_tri && !a.act_out && cs == 1 && a.out && orows >= 16 &&
         (a.plane_stride * 4) % 16 == 0 && ((size_t)a.N * 4) % 16 == 0) {
         const cuuint64_t dims[3] = {(cuuint64_t)a.N, (cuuint64_t)a.max_rows, (cuuint64_t)(splits / cs)};
         const cuuint64_t strides[2] = {(cuuint64_t)a.N * 4, (cuuint64_t)a.plane_stride * 4};
-        const cuuint32_t box[3] = {(cuuint32_t)kBM, (cuuint32_t)bpad, 1};
+        const cuuint32_t box[3] = {(cuuint32_t)kBM, (cuuint32_t)orows, 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode_fn()(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.out, dims, strides, box, estr,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
