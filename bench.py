@@ -243,13 +243,19 @@ def batch_sweep(ctx, eeb, desc, args, stream, batches=(1, 2, 4, 16, 32, 64, 128,
         ms = e0.elapsed_time(e1) / n_steps
         row = {"batch": B, "ms_per_step": ms, "tokens_per_s": B / (ms / 1000.0)}
         try:
-            tl = timeline.run(ctx, lambda k: one(3 + k % n_steps), 2)
+            tl = timeline.run(ctx, lambda k: one(3 + k % n_steps), 4)
             g_ms = sum(l["crit_us"] for l in tl["launches"] if l["cat"] == "layer_gemm") / 1e3
             h_ms = sum(l["crit_us"] for l in tl["launches"]
                        if l["cat"] == "exit_head" and l["kernel"] in ("gemm_tc", "gemm_cc")) / 1e3
-            heads = len(tl and [l for l in tl["launches"] if l["cat"] == "exit_head" and l["kernel"] == "gemm_tc"])
-            if g_ms > 0:
-                row["layer_gemm_frac"] = gemm_bytes_per_step(d, B, run_layers) / (g_ms / 1e3) / 1e9 / hbm
+            # bytes of the launches that ran (batch <= 2: conditional graph
+            # bodies skip the layers after a head when every row has exited;
+            # a skipped launch records no CTA; `ran` = share of stamped steps)
+            g_all = [l for l in tl["launches"] if l["cat"] == "layer_gemm"]
+            g_ran = sum(l["ran"] for l in g_all)
+            heads = sum(l["ran"] for l in tl["launches"] if l["cat"] == "exit_head" and l["kernel"] == "gemm_tc")
+            if g_ms > 0 and g_all:
+                row["layer_gemm_frac"] = (gemm_bytes_per_step(d, B, run_layers) * g_ran / len(g_all)
+                                          / (g_ms / 1e3) / 1e9 / hbm)
             if h_ms > 0 and heads:
                 row["exit_head_frac"] = head_bytes(d, B) * heads / (h_ms / 1e3) / 1e9 / hbm
         except Exception as e:  # per-batch roofline is extra information
@@ -296,15 +302,16 @@ def measure_loader(ctx, m, eeb, step, args, stream, depth=16, n_steps=20):
 
 def ncu_traffic(args, desc):
     """DRAM bytes per step of the layer GEMMs and the exit-head GEMMs from the
-    committed ncu launch list of this workload (profiles/r1, one serialised
+    committed ncu launch list of this workload (profiles/r2, one serialised
     --metrics dram__bytes_read.sum,dram__bytes_write.sum capture of a C2 step;
     cold cache).  None for other workloads."""
-    path = ROOT / "profiles" / "r1" / "launches_introspective_b64_s4.csv"
+    path = ROOT / "profiles" / "r2" / "launches_c2_b64.csv.gz"
     if not path.exists() or desc.name != "opt-1.3b-4x" or args.batch != 64 or args.policy != "introspective":
         return None
     import csv
+    import gzip
     launches = {}
-    with open(path) as f:
+    with gzip.open(path, "rt") as f:
         for r in csv.DictReader(line for line in f if not line.startswith("==")):
             d = launches.setdefault(r["ID"], {"name": r["Kernel Name"], "grid": r.get("Grid Size", "")})
             d[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))

@@ -79,12 +79,13 @@ def run(ctx, step, n_steps: int, max_launches: int = 1024) -> dict:
     lat = np.mean([[r["lat_ns"] for r in p["launches"]] for p in per], axis=0)
     work = np.mean([[r["work_ns"] for r in p["launches"]] for p in per], axis=0)
     tail = np.mean([[r["tail_ns"] for r in p["launches"]] for p in per], axis=0)
+    ran = np.mean([[1.0 if r["ctas"] > 0 else 0.0 for r in p["launches"]] for p in per], axis=0)
     span = float(np.mean([p["span_ns"] for p in per]))
-    launches = [{"kernel": r.get("kind", r["kernel"]), "cat": r["cat"], "ctas": r["ctas"],
+    launches = [{"kernel": r.get("kind", r["kernel"]), "cat": r["cat"], "ctas": r["ctas"], "ran": float(rn),
                  "crit_us": float(c) / 1e3, "busy_us": float(b) / 1e3,
                  **({"lat_us": float(la) / 1e3, "work_us": float(wo) / 1e3} if r["lat_ns"] >= 0 else {}),
                  **({"tail_us": float(ta) / 1e3} if r["tail_ns"] >= 0 else {})}
-                for r, c, b, la, wo, ta in zip(per[0]["launches"], crit, busy, lat, work, tail)]
+                for r, c, b, la, wo, ta, rn in zip(per[0]["launches"], crit, busy, lat, work, tail, ran)]
     cats = {}
     for l in launches:
         c = cats.setdefault(l["cat"], {"crit_ms": 0.0, "busy_ms": 0.0, "launches": 0})
