@@ -189,6 +189,10 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 
+// kCs4: the instantiation for 4-CTA clusters (the up projection's on-chip
+// K reduction, 16 rows x 4 peers of DSMEM loads in flight); its extra
+// registers stay out of the plane GEMMs' instantiation (occupancy).
+template <bool kCs4>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_o, TcParams p) {
@@ -519,41 +523,64 @@ __global__ void __launch_bounds__(kThreads, 2)
             const float* peer[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) peer[q] = cluster.map_shared_rank(red, q < p.cs ? q : 0);
+            auto finish = [&](int j, int row, float acc) {
+                if (p.head_tri) {
+                    fin[j * (kBM + 1) + t] = acc;
+                } else if (p.act_out) {
+                    if (p.act_kind == 2) {
+                        const float u = __shfl_xor_sync(0xffffffffu, acc, 1);  // odd lane: up, even: gate
+                        if ((t & 1) == 0 && n < p.N)
+                            p.act_out[(int64_t)row * (p.N / 2) + n / 2] = __float2bfloat16_rn(acc / (1.f + __expf(-acc)) * u);
+                    } else if (n < p.N) {
+                        p.act_out[(int64_t)row * p.N + n] = __float2bfloat16_rn(fmaxf(acc, 0.f));
+                    }
+                } else if (n < p.N) {
+                    plane[(int64_t)row * p.N + n] = acc;
+                }
+            };
             // kR rows x cs peers of DSMEM loads in flight at once (a
             // row-at-a-time loop pays one DSMEM round trip per load);
-            // warp-uniform trip counts (the SwiGLU pairing shuffles)
-            constexpr int kR = 4;
-            for (int j0 = 0; rank + j0 * p.cs < lim; j0 += kR) {
-                float v[kR][8];
+            // warp-uniform trip counts (the SwiGLU pairing shuffles).  The
+            // 4-CTA clusters of the decode up projection: 16 rows x 4 peers,
+            // a 64-row tile in one DSMEM round trip per rank.
+            if (kCs4) {
+                constexpr int kR4 = 16;
+                for (int j0 = 0; rank + j0 * 4 < lim; j0 += kR4) {
+                    float v[kR4][4];
 #pragma unroll
-                for (int r = 0; r < kR; ++r) {
-                    const int row = rank + (j0 + r) * p.cs;
+                    for (int r = 0; r < kR4; ++r) {
+                        const int row = rank + (j0 + r) * 4;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        v[r][q] = (q < p.cs && row < lim) ? peer[q][row * (kBM + 1) + t] : 0.f;
+                        for (int q = 0; q < 4; ++q) v[r][q] = row < lim ? peer[q][row * (kBM + 1) + t] : 0.f;
+                    }
+#pragma unroll
+                    for (int r = 0; r < kR4; ++r) {
+                        const int row = rank + (j0 + r) * 4;
+                        if (row >= lim) break;
+                        finish(j0 + r, row, ((v[r][0] + v[r][1]) + v[r][2]) + v[r][3]);
+                    }
                 }
+            } else {
+                constexpr int kR = 4;
+                for (int j0 = 0; rank + j0 * p.cs < lim; j0 += kR) {
+                    float v[kR][8];
 #pragma unroll
-                for (int r = 0; r < kR; ++r) {
-                    const int j = j0 + r;
-                    const int row = rank + j * p.cs;
-                    if (row >= lim) break;
-                    float acc = 0.f;
+                    for (int r = 0; r < kR; ++r) {
+                        const int row = rank + (j0 + r) * p.cs;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if (q < p.cs) acc += v[r][q];
-                    if (p.head_tri) {
-                        fin[j * (kBM + 1) + t] = acc;
-                    } else if (p.act_out) {
-                        if (p.act_kind == 2) {
-                            const float u = __shfl_xor_sync(0xffffffffu, acc, 1);  // odd lane: up, even: gate
-                            if ((t & 1) == 0 && n < p.N)
-                                p.act_out[(int64_t)row * (p.N / 2) + n / 2] =
-                                    __float2bfloat16_rn(acc / (1.f + __expf(-acc)) * u);
-                        } else if (n < p.N) {
-                            p.act_out[(int64_t)row * p.N + n] = __float2bfloat16_rn(fmaxf(acc, 0.f));
-                        }
-                    } else if (n < p.N) {
-                        plane[(int64_t)row * p.N + n] = acc;
+                        for (int q = 0; q < 8; ++q)
+                            v[r][q] = (q < p.cs && row < lim) ? peer[q][row * (kBM + 1) + t] : 0.f;
+                    }
+#pragma unroll
+                    for (int r = 0; r < kR; ++r) {
+                        const int j = j0 + r;
+                        const int row = rank + j * p.cs;
+                        if (row >= lim) break;
+                        float acc = 0.f;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (q < p.cs) acc += v[r][q];
+                        finish(j, row, acc);
                     }
                 }
             }
@@ -820,7 +847,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     }
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
     p.cs = cs;
-    EEB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = cs == 4 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
+    EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(tiles, splits);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -837,8 +865,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     cfg.attrs = attr;
     static const bool force_cl = std::getenv("EEB_TC_CLUSTER_ATTR") != nullptr;
     cfg.numAttrs = cs > 1 || force_cl ? 2 : 1;  // no cluster attribute unless clustering (launch cost)
-    p.st = stamp_next(reinterpret_cast<const void*>(gemm_tc_kernel));
-    EEB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, mo, p));
+    p.st = stamp_next(reinterpret_cast<const void*>(kern));
+    EEB_CUDA(cudaLaunchKernelEx(&cfg, kern, mw, mx, mo, p));
     return splits / cs;
 }
 
