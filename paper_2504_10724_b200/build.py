@@ -67,7 +67,8 @@ def build_eeb(verbose: bool = False, extra_flags: list[str] | None = None) -> Pa
             for f in [ex.submit(_run, j) for j in jobs]:
                 f.result()
     if jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl", "-lcublasLt",
+               "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         if verbose:
             print(" ".join(cmd))
         _run(cmd)

@@ -9,6 +9,7 @@
 #include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <cublasLt.h>
 
 #include <algorithm>
 #include <array>
@@ -169,6 +170,18 @@ struct eeb_ctx {
     cudaStream_t main_stream = nullptr;  // `stream` while a conditional body is being captured
     std::vector<cudaStream_t> cond_streams;  // capture streams of nested conditional bodies (step graphs)
     bool capturing = false;               // enqueue_step runs under stream capture
+    bool in_prefill = false;              // enqueue_prefill: the layer GEMMs may take cuBLASLt
+    // Prefill GEMMs (plain [rows x K] x [K x N] products of every prompt row,
+    // no early exit to skip): cuBLASLt, one plan per shape.
+    cublasLtHandle_t lt = nullptr;
+    eeb::DevBuf lt_ws;
+    struct LtPlan {
+        cublasLtMatmulDesc_t op = nullptr;
+        cublasLtMatrixLayout_t a = nullptr, b = nullptr, d = nullptr;
+        cublasLtMatmulAlgo_t algo{};
+        bool ok = false;
+    };
+    std::map<std::tuple<int, int, int>, LtPlan> lt_plans;
     size_t cond_open = 0;                 // conditional bodies open in the capture
     std::vector<std::unique_ptr<eeb::Model>> models;
     int graphs_enabled = 1;
@@ -745,6 +758,8 @@ void stamp_reset(eeb_ctx* c) {
     EEB_CUDA(cudaMemsetAsync(c->stamp_buf.as<unsigned long long>() + 3 * cells, 0, cells * 8, c->stream));
 }
 
+bool prefill_lt_ready(eeb_ctx* c);
+
 // Byte offsets of the step outputs inside ctx->o_all for R rows and up to ne
 // exit heads: the per-row / per-step outputs first (common_end), the
 // per-head arrays of a profiling step after them.
@@ -806,14 +821,19 @@ void ensure_workspace(eeb_ctx* c, const Model& m, int batch) {
     moved |= c->hn.ensure((size_t)R * D * act);
     moved |= c->hnB.ensure((size_t)R * D * act);
     moved |= c->hhead.ensure((size_t)R * D * act);
+    if (d.dtype == EEB_BF16) prefill_lt_ready(c);  // handle + workspace outside any capture
     moved |= c->attn.ensure((size_t)R * m.dq * act);
     moved |= c->mlp_h.ensure((size_t)R * F * act);
     // split-K partial bound: splits <= K / (32 * vec) for every GEMM of the step.
     const int64_t kmin = act == 4 ? 128 : 256;
     int64_t need = 0;  // split-K planes per GEMM: tier 1 <= K/(32 vec)+1, tier 2 <= SMs/tiles+1
+    // (the split GEMMs serve <= 256 rows; larger prefill chunks run cuBLASLt
+    // into one plane of R rows)
+    const int64_t Rs = std::min<int64_t>(R, 256);
     auto upd = [&](int64_t N, int64_t K) {
         const int64_t tiles = (N + 127) / 128;
-        need = std::max(need, std::max<int64_t>(K / kmin + 1, c->num_sms / tiles + 1) * R * N);
+        need = std::max(need, std::max<int64_t>(K / kmin + 1, c->num_sms / tiles + 1) * Rs * N);
+        need = std::max(need, (int64_t)R * N);
     };
     upd(m.dq_l + 2 * m.dkv_l, D);
     upd(D, m.dq_l);
@@ -899,6 +919,61 @@ void count(eeb_ctx* c, int cat, int n) {
     c->step_launches += n;
 }
 
+// The cuBLASLt handle and workspace of the prefill GEMMs (created outside any
+// stream capture); false when cuBLASLt is unavailable or switched off.
+bool prefill_lt_ready(eeb_ctx* c) {
+    static const bool on = !std::getenv("EEB_PREFILL_LT") || std::atoi(std::getenv("EEB_PREFILL_LT")) != 0;
+    if (!on) return false;
+    if (!c->lt) {
+        if (cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) {
+            c->lt = nullptr;
+            return false;
+        }
+        c->lt_ws.ensure(32u << 20);
+    }
+    return true;
+}
+
+// Prefill GEMM on cuBLASLt: out[rows][N] (f32) = X[rows][K] . W[N][K]^T in
+// one plane.  Column-major view: D (N x rows, ld N) = op(A) B with A = W (K x
+// N, ld K, transposed) and B = X (K x rows, ld K).  EEB_PREFILL_LT=0 keeps
+// the tcgen05 decode GEMM (split-K planes) for prefill too.
+bool gemm_lt(eeb_ctx* c, const void* W, const void* X, int N, int K, int rows, float* out) {
+    static const bool on = !std::getenv("EEB_PREFILL_LT") || std::atoi(std::getenv("EEB_PREFILL_LT")) != 0;
+    if (!on) return false;
+    constexpr size_t kWs = 32u << 20;
+    if (!c->lt || c->lt_ws.bytes < kWs) return false;  // (created by ensure_workspace, outside any capture)
+    auto& pl = c->lt_plans[{N, K, rows}];
+    if (!pl.op) {
+        const cublasComputeType_t ct = CUBLAS_COMPUTE_32F;
+        const cudaDataType_t st = CUDA_R_32F;
+        cublasLtMatmulDescCreate(&pl.op, ct, st);
+        const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+        cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta);
+        cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb);
+        cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_16BF, K, N, K);
+        cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_16BF, K, rows, K);
+        cublasLtMatrixLayoutCreate(&pl.d, CUDA_R_32F, N, rows, N);
+        cublasLtMatmulPreference_t pref;
+        cublasLtMatmulPreferenceCreate(&pref);
+        const size_t ws = kWs;
+        cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof ws);
+        cublasLtMatmulHeuristicResult_t res{};
+        int n = 0;
+        pl.ok = cublasLtMatmulAlgoGetHeuristic(c->lt, pl.op, pl.a, pl.b, pl.d, pl.d, pref, 1, &res, &n) ==
+                    CUBLAS_STATUS_SUCCESS &&
+                n > 0;
+        if (pl.ok) pl.algo = res.algo;
+        cublasLtMatmulPreferenceDestroy(pref);
+    }
+    if (!pl.ok) return false;
+    const float alpha = 1.f, beta = 0.f;
+    const cublasStatus_t r = cublasLtMatmul(c->lt, pl.op, &alpha, W, pl.a, X, pl.b, &beta, out, pl.d, out, pl.d,
+                                            &pl.algo, c->lt_ws.p, kWs, c->stream);
+    if (r != CUBLAS_STATUS_SUCCESS) throw Error(EEB_E_CUDA, "cublasLtMatmul failed: " + std::to_string((int)r));
+    return true;
+}
+
 // One decode GEMM into the split-K plane workspace; returns the planes written.
 int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int N, int K, const int* n_active,
          int batch, int plane0 = 0) {
@@ -919,6 +994,11 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     c->pf_ptr = nullptr;
     c->pf_bytes = 0;
     int planes = 0;
+    if (c->in_prefill && plane0 == 0 && batch >= 64 && m.desc.dtype == EEB_BF16 && c->gemm_tier != 1 &&
+        gemm_lt(c, W, X, N, K, batch, a.out)) {
+        count(c, cat, 1);
+        return 1;
+    }
     if (c->gemm_tier != 1 && m.desc.dtype == EEB_BF16) planes = gemm_tc(a, c->stream);
     if (planes == 0) {
         if (c->gemm_tier == 2 && m.desc.dtype == EEB_BF16 && batch >= tc_min_rows() && gemm_tc_available())
@@ -1396,6 +1476,11 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
 constexpr int kPolicyPrefill = 100;  // graph-cache key
 
 void enqueue_prefill(eeb_ctx* c, int mi, int depth, int rows) {
+    struct InPrefill {
+        eeb_ctx* c;
+        explicit InPrefill(eeb_ctx* cc) : c(cc) { c->in_prefill = true; }
+        ~InPrefill() { c->in_prefill = false; }
+    } in_prefill_scope(c);
     Model& m = model_of(c, mi);
     const eeb_model_desc& d = m.desc;
     const int D = d.d_model;
@@ -1675,6 +1760,13 @@ void eeb_destroy(eeb_ctx* c) {
     for (auto& [k, g] : c->graphs) cudaGraphExecDestroy(g);
     for (auto ev : c->ev_pool) cudaEventDestroy(ev);
     if (c->nccl) nccl().comm_destroy(c->nccl);
+    for (auto& [k, pl] : c->lt_plans) {
+        if (pl.a) cublasLtMatrixLayoutDestroy(pl.a);
+        if (pl.b) cublasLtMatrixLayoutDestroy(pl.b);
+        if (pl.d) cublasLtMatrixLayoutDestroy(pl.d);
+        if (pl.op) cublasLtMatmulDescDestroy(pl.op);
+    }
+    if (c->lt) cublasLtDestroy(c->lt);
     if (c->pin) cudaFreeHost(c->pin);
     if (c->pf_pin) cudaFreeHost(c->pf_pin);
     for (auto& m : c->models) {
@@ -2027,8 +2119,13 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
         EEB_CUDA(cudaSetDevice(c->device));
         wait_layers(c, m, depth);
         static const int env_chunk = std::getenv("EEB_PREFILL_CHUNK") ? std::atoi(std::getenv("EEB_PREFILL_CHUNK")) : 0;
-        const int chunk = d.dtype == EEB_BF16 ? (env_chunk >= 16 && env_chunk <= 256 ? env_chunk : 256)
-                                              : 128;  // tcgen05 N <= 256; CUDA-core tier <= 64 rows
+        // bf16: 1024-row chunks when the layer GEMMs run on cuBLASLt (fewer
+        // re-streams of the weights), else 256 (tcgen05 N <= 256); f32: the
+        // CUDA-core tier serves <= 64 rows per pass
+        const bool lt = d.dtype == EEB_BF16 && c->gemm_tier != 1 && prefill_lt_ready(c);
+        const int chunk = d.dtype == EEB_BF16 ? (env_chunk >= 16 && env_chunk <= (lt ? 1024 : 256) ? env_chunk
+                                                                                                   : (lt ? 1024 : 256))
+                                              : 128;
         ensure_workspace(c, m, (int)std::min<int64_t>(chunk, total));
         // (tok, slot, pos) of every prompt token: one pinned staging + one H2D,
         // then a device-to-device slice per chunk.
