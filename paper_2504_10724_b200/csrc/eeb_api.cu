@@ -1502,8 +1502,12 @@ void enqueue_prefill(eeb_ctx* c, int mi, int depth, int rows) {
     }
 }
 
-void run_prefill_chunk(eeb_ctx* c, int mi, int depth, int rows) {
-    const bool use_graph = c->graphs_enabled && !c->profiling;
+// full: a full-size chunk of its prefill.  Only those are captured into
+// graphs (a serving engine's prefills of a few admitted requests come in many
+// row counts and query-block layouts; each new one would pay a capture and
+// instantiation of a whole-depth graph, far more than launching it once).
+void run_prefill_chunk(eeb_ctx* c, int mi, int depth, int rows, bool full) {
+    const bool use_graph = c->graphs_enabled && !c->profiling && full;
     if (!use_graph) {
         enqueue_prefill(c, mi, depth, rows);
         return;
@@ -2194,7 +2198,7 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
             EEB_CUDA(cudaMemcpyAsync(c->pf_items.as<int4>() + n_items, di + ci * (max_items + 1) + n_items,
                                      sizeof(int4), cudaMemcpyDeviceToDevice, s));
             c->pf_cur_items = n_items;
-            run_prefill_chunk(c, model, depth, rows);
+            run_prefill_chunk(c, model, depth, rows, rows == chunk);
         }
         c->pf_cur_items = 0;
         EEB_CUDA(cudaStreamSynchronize(s));
