@@ -427,7 +427,7 @@ def run_eeb(args, desc):
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
-    rng = np.random.default_rng(1000 + rank)
+    rng = np.random.default_rng(1000 if tp > 1 else 1000 + rank)  # a TP group decodes the same rows
     slots = np.arange(B, dtype=np.int32)
 
     # prefill (eeb_prefill, chunked <= 256-token passes over all layers): the
@@ -641,7 +641,7 @@ def run_eeb(args, desc):
         # layers (choose_depth, test_policy.cpp:322-327), flat decode, requests
         # sharded over the ranks; with its batch sweep at N = 1.
         d = child_bench(["--model", "codellama-34b", "--policy", "flat", "--depth", "12", "--batch", str(args.batch),
-                         "--steps", "10", "--warmup", "3"] + (["--sweep"] if world == 1 else []), 1200)
+                         "--steps", "10", "--warmup", "3"] + (["--sweep"] if world == 1 else []), 600)
         if d is not None and "error" not in d:
             secondary = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"],
                          "n_gpus": d["n_gpus"], "ms_per_step": d["ms_per_step"], "batch_per_gpu": args.batch,
@@ -657,7 +657,7 @@ def run_eeb(args, desc):
         # launched ranks (NCCL inside the step), flat at the greedy depth 10
         # (test_policy.cpp:328)
         d = child_bench(["--model", "llama2-70b", "--tp", str(world), "--policy", "flat", "--depth", "10",
-                         "--batch", str(args.batch), "--steps", "10", "--warmup", "3"], 1500)
+                         "--batch", str(args.batch), "--steps", "10", "--warmup", "3"], 420)
         if d is not None and "error" not in d:
             c5 = {"workload": d["config"]["workload"], "value": d["value"], "unit": d["unit"], "n_gpus": d["n_gpus"],
                   "ms_per_step": d["ms_per_step"], "batch": args.batch, "e2e": d["e2e"],
