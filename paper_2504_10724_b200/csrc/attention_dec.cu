@@ -449,19 +449,17 @@ bool launch_dec(const AttnArgs& a0, cudaStream_t s) {
 // ============================================================================
 constexpr int kMItems = 8;       // items per warp at most (host sizes the grid)
 constexpr int kMMaxRing = 12;    // stages per warp at most
-constexpr uint32_t kMRow = 128;  // bytes per K / V row (head_dim 64, bf16)
-
 constexpr int kMRowsCta = 8;     // distinct rows of a CTA's (contiguous) item range at most
 
 struct MhaSmem {
     int s_pad;
     size_t sc_off, q_off, rope_off, dep_off, pt_off, total;
-    __host__ __device__ MhaSmem(int kMW, size_t pool, int max_seq) {
+    __host__ __device__ MhaSmem(int HD, int kMW, size_t pool, int max_seq) {
         s_pad = (max_seq + 31) & ~31;
         sc_off = pool;                                      // [warp][s_pad] f32 scores / probabilities
-        q_off = sc_off + (size_t)kMW * s_pad * 4;           // [warp][2][64] f32 q, new k
-        rope_off = q_off + (size_t)kMW * 128 * 4;           // [row][2][32] f32 cos, sin at the row's position
-        dep_off = rope_off + (size_t)kMRowsCta * 64 * 4;    // [row][s_pad] KV-depth bytes
+        q_off = sc_off + (size_t)kMW * s_pad * 4;           // [warp][2][HD] f32 q, new k
+        rope_off = q_off + (size_t)kMW * 2 * HD * 4;        // [row][HD] f32 cos | sin at the row's position
+        dep_off = rope_off + (size_t)kMRowsCta * HD * 4;    // [row][s_pad] KV-depth bytes
         pt_off = dep_off + (size_t)kMRowsCta * s_pad;       // [row][32] pages (paged pool)
         total = pt_off + (size_t)kMRowsCta * 32 * 4;
     }
@@ -480,12 +478,16 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     return w;
 }
 
-template <int kMW, bool PAGED>
+// HD: head_dim (64, 80, 128); rows of HD bf16 = NC 16-byte chunks; lane l
+// owns the dim pairs p = l + 32 t < HD / 2 (t < PPL) in the prologue and the
+// V pass.
+template <int HD, int kMW, bool PAGED>
 __global__ void __launch_bounds__(kMW * 32, 1)
     attention_mha_kernel(Stamp stamp, AttnArgs a, int pool_kb) {
     StampScope stamp_scope(stamp);
-    constexpr int HD = 64;
-    constexpr int kP = 6;  // QKV planes loaded ahead (C2: all of them)
+    constexpr int NC = HD / 8, NP = HD / 2, HALF = HD / 2, PPL = (NP + 31) / 32;
+    constexpr uint32_t kRow = HD * 2;  // bytes per K / V row
+    constexpr int kP = 6;              // QKV planes loaded ahead (C2: all of them)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -503,7 +505,7 @@ __global__ void __launch_bounds__(kMW * 32, 1)
 
     const int H = a.n_heads, S = a.max_seq;
     const int dq = H * HD;
-    const MhaSmem L(kMW, (size_t)pool_kb << 10, S);
+    const MhaSmem L(HD, kMW, (size_t)pool_kb << 10, S);
     // The step's small shared arrays (live-row count, the rows' slot /
     // position, RoPE rows, KV-depth rows, page rows) are read once per CTA
     // into smem, not per warp (every warp of the grid would hit the same few
@@ -521,43 +523,51 @@ __global__ void __launch_bounds__(kMW * 32, 1)
     // next barrier, overlapping the table loads.
     const bool has = beg + warp < end;
     const int my = has ? (end - beg - warp - 1) / kMW + 1 : 0;
-    float2 q2f = make_float2(0.f, 0.f), k2f = q2f, v2f = q2f;
-    {
-        const int it = beg + warp, row = it / H, g = it % H;
+    // the QKV sums of one item: lane's pairs, q / k / v
+    auto sum_planes = [&](int it, bool on_item, float2 (&q2)[PPL], float2 (&k2)[PPL], float2 (&v2)[PPL], bool first) {
+        const int row = it / H, g = it % H;
         const float* src = a.qkv + (int64_t)row * (3 * dq) + g * HD + 2 * lane;
-        float2 xs[kP], ys[kP], zs[kP];
+        float2 xs[PPL][kP], ys[PPL][kP], zs[PPL][kP];
 #pragma unroll
-        for (int sp = 0; sp < kP; ++sp) {
-            const bool on = has && sp < a.splits;
-            const float* pl = src + (on ? sp : 0) * a.split_stride;
-            xs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl)) : make_float2(0.f, 0.f);
-            ys[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + dq)) : make_float2(0.f, 0.f);
-            zs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq)) : make_float2(0.f, 0.f);
-        }
-        if (threadIdx.x < nr) {
+        for (int t = 0; t < PPL; ++t)
+#pragma unroll
+            for (int sp = 0; sp < kP; ++sp) {
+                const bool on = on_item && sp < a.splits && lane + 32 * t < NP;
+                const float* pl = src + 64 * t + (on ? sp : 0) * a.split_stride;
+                xs[t][sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl)) : make_float2(0.f, 0.f);
+                ys[t][sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + dq)) : make_float2(0.f, 0.f);
+                zs[t][sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq)) : make_float2(0.f, 0.f);
+            }
+        if (first && threadIdx.x < nr) {  // (the rows' tables ride the same round trip)
             s_slot[threadIdx.x] = a.slot[r0 + threadIdx.x];
             s_pos[threadIdx.x] = a.pos[r0 + threadIdx.x];
         }
 #pragma unroll
-        for (int sp = 0; sp < kP; ++sp) {
-            q2f.x += xs[sp].x; q2f.y += xs[sp].y; k2f.x += ys[sp].x; k2f.y += ys[sp].y;
-            v2f.x += zs[sp].x; v2f.y += zs[sp].y;
+        for (int t = 0; t < PPL; ++t) {
+            q2[t] = k2[t] = v2[t] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int sp = 0; sp < kP; ++sp) {
+                q2[t].x += xs[t][sp].x; q2[t].y += xs[t][sp].y; k2[t].x += ys[t][sp].x; k2[t].y += ys[t][sp].y;
+                v2[t].x += zs[t][sp].x; v2[t].y += zs[t][sp].y;
+            }
+            for (int sp = kP; on_item && sp < a.splits && lane + 32 * t < NP; ++sp) {
+                const float* pl = src + 64 * t + sp * a.split_stride;
+                const float2 x = __ldcg(reinterpret_cast<const float2*>(pl));
+                const float2 y = __ldcg(reinterpret_cast<const float2*>(pl + dq));
+                const float2 z = __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq));
+                q2[t].x += x.x; q2[t].y += x.y; k2[t].x += y.x; k2[t].y += y.y; v2[t].x += z.x; v2[t].y += z.y;
+            }
         }
-        for (int sp = kP; has && sp < a.splits; ++sp) {
-            const float* pl = src + sp * a.split_stride;
-            const float2 x = __ldcg(reinterpret_cast<const float2*>(pl));
-            const float2 y = __ldcg(reinterpret_cast<const float2*>(pl + dq));
-            const float2 z = __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq));
-            q2f.x += x.x; q2f.y += x.y; k2f.x += y.x; k2f.y += y.y; v2f.x += z.x; v2f.y += z.y;
-        }
-    }
+    };
+    float2 q2f[PPL], k2f[PPL], v2f[PPL];
+    sum_planes(beg + warp, has, q2f, k2f, v2f, true);
     __syncthreads();
     float* rope_s = reinterpret_cast<float*>(base + L.rope_off);
     uint8_t* depc_s = base + L.dep_off;
     int* pt_s = reinterpret_cast<int*>(base + L.pt_off);
-    for (int e = threadIdx.x; e < nr * 64; e += kMW * 32) {
-        const int t = e >> 6, j = e & 63;
-        rope_s[e] = (j < 32 ? a.rope_cos : a.rope_sin)[(int64_t)s_pos[t] * 32 + (j & 31)];
+    for (int e = threadIdx.x; e < nr * HD; e += kMW * 32) {
+        const int t = e / HD, j = e - t * HD;
+        rope_s[e] = (j < HALF ? a.rope_cos : a.rope_sin)[(int64_t)s_pos[t] * HALF + (j < HALF ? j : j - HALF)];
     }
     {
         const int wpr = L.s_pad / 4;  // depth words per row (S % 4 == 0: host)
@@ -577,15 +587,15 @@ __global__ void __launch_bounds__(kMW * 32, 1)
     // the CTA's stage pool is shared by its active warps: chunk rows R (a
     // multiple of 32, <= 256; <= the page size when paged) with >= 3 stages
     const int per_warp = ((pool_kb << 10) / active) & ~1023;     // bytes (1 KB aligned)
-    int R = min(256, (per_warp / (3 * (int)kMRow)) & ~31);
+    int R = min(256, (per_warp / (3 * (int)kRow)) & ~31);
     if (PAGED) R = min(R, a.page_size);
     R = max(R, 32);
-    const int nring = max(2, min(kMMaxRing, per_warp / (R * (int)kMRow)));
-    const uint32_t stage_bytes = (uint32_t)R * kMRow;
+    const int nring = max(2, min(kMMaxRing, per_warp / (R * (int)kRow)));
+    const uint32_t stage_bytes = (uint32_t)R * kRow;
     const uint32_t ring = sbase + (uint32_t)warp * (uint32_t)per_warp;
     float* sc_s = reinterpret_cast<float*>(base + L.sc_off) + (size_t)warp * L.s_pad;
-    float* q_s = reinterpret_cast<float*>(base + L.q_off) + warp * 128;
-    float* knew_s = q_s + 64;
+    float* q_s = reinterpret_cast<float*>(base + L.q_off) + warp * 2 * HD;
+    float* knew_s = q_s + HD;
     const int PS = PAGED ? a.page_size : S;
     const __nv_bfloat16* kc = static_cast<const __nv_bfloat16*>(a.k_cache);
     const __nv_bfloat16* vc = static_cast<const __nv_bfloat16*>(a.v_cache);
@@ -604,8 +614,8 @@ __global__ void __launch_bounds__(kMW * 32, 1)
         if (ik >= my) return;
         const uint32_t bar = smem_u32(&full[warp][st]);
         const int rows = min(R, c_n - ip);
-        mbar_expect_tx(bar, (uint32_t)rows * kMRow);
-        bulk_g2s(ring + (uint32_t)st * stage_bytes, (iph == 0 ? kc : vc) + row_off(c_lr, c_g, ip), (uint32_t)rows * kMRow,
+        mbar_expect_tx(bar, (uint32_t)rows * kRow);
+        bulk_g2s(ring + (uint32_t)st * stage_bytes, (iph == 0 ? kc : vc) + row_off(c_lr, c_g, ip), (uint32_t)rows * kRow,
                  bar, pol);
         ip += R;
         if (ip >= c_n) {
@@ -625,68 +635,72 @@ __global__ void __launch_bounds__(kMW * 32, 1)
         for (int st = 0; st < nring; ++st) issue_next(st);
 
     int u = 0;  // chunks consumed by this warp
-    const float qscale = 0.125f;  // 1 / sqrt(64), exact
+    const float qscale = rsqrtf((float)HD);
     for (int k = 0; k < my; ++k) {
         const int it = beg + warp + kMW * k, row = it / H, g = it % H, lr = row - r0;
         const int pos = s_pos[lr];
         const uint8_t* dep_s = depc_s + (size_t)lr * L.s_pad;
-        // ---- item prologue: lane = dims (2 lane, 2 lane + 1) -----------------
-        const float* src = a.qkv + (int64_t)row * (3 * dq) + g * HD + 2 * lane;
-        float2 q2 = q2f, k2 = k2f, v2 = v2f;  // the first item: summed above
-        if (k > 0) {
-            q2 = k2 = v2 = make_float2(0.f, 0.f);
-            float2 xs[kP], ys[kP], zs[kP];
+        // ---- item prologue ------------------------------------------------------
+        float2 q2[PPL], k2[PPL], v2[PPL];
+        if (k == 0) {
 #pragma unroll
-            for (int sp = 0; sp < kP; ++sp) {
-                const bool on = sp < a.splits;
-                const float* pl = src + (on ? sp : 0) * a.split_stride;
-                xs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl)) : make_float2(0.f, 0.f);
-                ys[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + dq)) : make_float2(0.f, 0.f);
-                zs[sp] = on ? __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq)) : make_float2(0.f, 0.f);
-            }
+            for (int t = 0; t < PPL; ++t) { q2[t] = q2f[t]; k2[t] = k2f[t]; v2[t] = v2f[t]; }
+        } else {
+            sum_planes(it, true, q2, k2, v2, false);
+        }
+        // RoPE over pairs (j, j + HD/2) through smem: raw q / k, then rotated
 #pragma unroll
-            for (int sp = 0; sp < kP; ++sp) {
-                q2.x += xs[sp].x; q2.y += xs[sp].y; k2.x += ys[sp].x; k2.y += ys[sp].y;
-                v2.x += zs[sp].x; v2.y += zs[sp].y;
+        for (int t = 0; t < PPL; ++t)
+            if (lane + 32 * t < NP) {
+                *reinterpret_cast<float2*>(q_s + 2 * (lane + 32 * t)) = q2[t];
+                *reinterpret_cast<float2*>(knew_s + 2 * (lane + 32 * t)) = k2[t];
             }
-            for (int sp = kP; sp < a.splits; ++sp) {
-                const float* pl = src + sp * a.split_stride;
-                const float2 x = __ldcg(reinterpret_cast<const float2*>(pl));
-                const float2 y = __ldcg(reinterpret_cast<const float2*>(pl + dq));
-                const float2 z = __ldcg(reinterpret_cast<const float2*>(pl + 2 * dq));
-                q2.x += x.x; q2.y += x.y; k2.x += y.x; k2.y += y.y; v2.x += z.x; v2.y += z.y;
+        __syncwarp();
+        float qr0[PPL], qr1[PPL], kr0[PPL], kr1[PPL];
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int d0 = 2 * (lane + 32 * t);
+            if (d0 >= HD) continue;
+            const bool lo = d0 < HALF;
+            const int jj = lo ? d0 : d0 - HALF, pd = lo ? d0 + HALF : d0 - HALF;
+            const float2 cc = *reinterpret_cast<const float2*>(rope_s + lr * HD + jj);
+            const float2 ss = *reinterpret_cast<const float2*>(rope_s + lr * HD + HALF + jj);
+            const float2 qp = *reinterpret_cast<const float2*>(q_s + pd);
+            const float2 kp = *reinterpret_cast<const float2*>(knew_s + pd);
+            if (lo) {  // x0 = mine, x1 = partner: x0 cos - x1 sin
+                qr0[t] = q2[t].x * cc.x - qp.x * ss.x; qr1[t] = q2[t].y * cc.y - qp.y * ss.y;
+                kr0[t] = k2[t].x * cc.x - kp.x * ss.x; kr1[t] = k2[t].y * cc.y - kp.y * ss.y;
+            } else {   // x1 = mine, x0 = partner: x0 sin + x1 cos
+                qr0[t] = qp.x * ss.x + q2[t].x * cc.x; qr1[t] = qp.y * ss.y + q2[t].y * cc.y;
+                kr0[t] = kp.x * ss.x + k2[t].x * cc.x; kr1[t] = kp.y * ss.y + k2[t].y * cc.y;
             }
         }
-        const int jj = (2 * lane) & 31;  // RoPE pairs (j, j + 32): lanes l and l ^ 16
-        const float2 cc = *reinterpret_cast<const float2*>(rope_s + lr * 64 + jj);
-        const float2 ss = *reinterpret_cast<const float2*>(rope_s + lr * 64 + 32 + jj);
-        const float qp0 = __shfl_xor_sync(0xffffffffu, q2.x, 16), qp1 = __shfl_xor_sync(0xffffffffu, q2.y, 16);
-        const float kp0 = __shfl_xor_sync(0xffffffffu, k2.x, 16), kp1 = __shfl_xor_sync(0xffffffffu, k2.y, 16);
-        float qr0, qr1, kr0, kr1;
-        if (lane < 16) {  // x0 = mine, x1 = partner: x0 cos - x1 sin
-            qr0 = q2.x * cc.x - qp0 * ss.x; qr1 = q2.y * cc.y - qp1 * ss.y;
-            kr0 = k2.x * cc.x - kp0 * ss.x; kr1 = k2.y * cc.y - kp1 * ss.y;
-        } else {          // x1 = mine, x0 = partner: x0 sin + x1 cos
-            qr0 = qp0 * ss.x + q2.x * cc.x; qr1 = qp1 * ss.y + q2.y * cc.y;
-            kr0 = kp0 * ss.x + k2.x * cc.x; kr1 = kp1 * ss.y + k2.y * cc.y;
-        }
-        const __nv_bfloat162 kb = __floats2bfloat162_rn(kr0, kr1), vb = __floats2bfloat162_rn(v2.x, v2.y);
-        const float vn0 = __low2float(vb), vn1 = __high2float(vb);
-        *reinterpret_cast<float2*>(q_s + 2 * lane) = make_float2(qr0 * qscale, qr1 * qscale);
-        *reinterpret_cast<float2*>(knew_s + 2 * lane) = make_float2(__low2float(kb), __high2float(kb));
-        if (!a.kv_ready) {  // append the new position's K / V (its row of the last chunk comes from registers)
-            const int64_t off = row_off(lr, g, pos) + 2 * lane;
-            *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.k_cache) + off) = kb;
-            *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.v_cache) + off) = vb;
+        __syncwarp();
+        float vn0[PPL], vn1[PPL];
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) {
+            const int d0 = 2 * (lane + 32 * t);
+            if (d0 >= HD) continue;
+            const __nv_bfloat162 kb = __floats2bfloat162_rn(kr0[t], kr1[t]), vb = __floats2bfloat162_rn(v2[t].x, v2[t].y);
+            vn0[t] = __low2float(vb);
+            vn1[t] = __high2float(vb);
+            *reinterpret_cast<float2*>(q_s + d0) = make_float2(qr0[t] * qscale, qr1[t] * qscale);
+            *reinterpret_cast<float2*>(knew_s + d0) = make_float2(__low2float(kb), __high2float(kb));
+            if (!a.kv_ready) {  // append the new position's K / V (its row of the last chunk comes from registers)
+                const int64_t off = row_off(lr, g, pos) + d0;
+                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.k_cache) + off) = kb;
+                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.v_cache) + off) = vb;
+            }
         }
         __syncwarp();
         if (k == 0 && lane == 0 && warp == 0) stamp_mark(stamp);  // (timeline) first item's prologue done
-        // q rotated per lane: qr[8 j + t] = q[8 ((j + lane) mod 8) + t]
+        // q rotated per lane: qr[8 j + t] = q[8 ((j + lane) mod NC) + t]
         float qr[HD];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float4 t0 = *reinterpret_cast<const float4*>(q_s + 8 * ((j + lane) & 7));
-            const float4 t1 = *reinterpret_cast<const float4*>(q_s + 8 * ((j + lane) & 7) + 4);
+        for (int j = 0; j < NC; ++j) {
+            const int cj = (j + lane) % NC;
+            const float4 t0 = *reinterpret_cast<const float4*>(q_s + 8 * cj);
+            const float4 t1 = *reinterpret_cast<const float4*>(q_s + 8 * cj + 4);
             qr[8 * j + 0] = t0.x; qr[8 * j + 1] = t0.y; qr[8 * j + 2] = t0.z; qr[8 * j + 3] = t0.w;
             qr[8 * j + 4] = t1.x; qr[8 * j + 5] = t1.y; qr[8 * j + 6] = t1.z; qr[8 * j + 7] = t1.w;
         }
@@ -703,8 +717,8 @@ __global__ void __launch_bounds__(kMW * 32, 1)
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
                 if (p < pos) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const uint4 w = lds128(stage + (uint32_t)r * kMRow + (uint32_t)(((j + lane) & 7) << 4));
+                    for (int j = 0; j < NC; ++j) {
+                        const uint4 w = lds128(stage + (uint32_t)r * kRow + (uint32_t)(((j + lane) % NC) << 4));
                         acc[0] = fmaf(qr[8 * j + 0], bf_lo(w.x), acc[0]);
                         acc[1] = fmaf(qr[8 * j + 1], bf_hi(w.x), acc[1]);
                         acc[2] = fmaf(qr[8 * j + 2], bf_lo(w.y), acc[2]);
@@ -716,9 +730,10 @@ __global__ void __launch_bounds__(kMW * 32, 1)
                     }
                 } else if (p == pos) {  // the new position: K from the prologue
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 t0 = *reinterpret_cast<const float4*>(knew_s + 8 * ((j + lane) & 7));
-                        const float4 t1 = *reinterpret_cast<const float4*>(knew_s + 8 * ((j + lane) & 7) + 4);
+                    for (int j = 0; j < NC; ++j) {
+                        const int cj = (j + lane) % NC;
+                        const float4 t0 = *reinterpret_cast<const float4*>(knew_s + 8 * cj);
+                        const float4 t1 = *reinterpret_cast<const float4*>(knew_s + 8 * cj + 4);
                         acc[0] = fmaf(qr[8 * j + 0], t0.x, acc[0]);
                         acc[1] = fmaf(qr[8 * j + 1], t0.y, acc[1]);
                         acc[2] = fmaf(qr[8 * j + 2], t0.z, acc[2]);
@@ -751,9 +766,10 @@ __global__ void __launch_bounds__(kMW * 32, 1)
 #pragma unroll
         for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
         __syncwarp();
-        // ---- V pass: lane = dims (2 lane, 2 lane + 1) -------------------------
-        float o0 = 0.f, o1 = 0.f, o2 = 0.f, o3 = 0.f;
-        const uint32_t voff = (uint32_t)lane << 2;
+        // ---- V pass: lane = its dim pairs ---------------------------------------
+        float o[PPL][4];
+#pragma unroll
+        for (int t = 0; t < PPL; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
         for (int c = 0; c < nch; ++c, ++u) {
             const int st = u % nring;
             const uint32_t stage = ring + (uint32_t)st * stage_bytes;
@@ -762,40 +778,53 @@ __global__ void __launch_bounds__(kMW * 32, 1)
             const int nfull = min(R, pos - c0r) & ~3;  // rows before pos, in groups of 4
             for (int r = 0; r < nfull; r += 4) {
                 const float4 e = *reinterpret_cast<const float4*>(sc_s + c0r + r);
-                const uint32_t w0 = lds32(stage + (uint32_t)r * kMRow + voff);
-                const uint32_t w1 = lds32(stage + (uint32_t)(r + 1) * kMRow + voff);
-                const uint32_t w2 = lds32(stage + (uint32_t)(r + 2) * kMRow + voff);
-                const uint32_t w3 = lds32(stage + (uint32_t)(r + 3) * kMRow + voff);
-                o0 = fmaf(e.x, bf_lo(w0), o0); o1 = fmaf(e.x, bf_hi(w0), o1);
-                o2 = fmaf(e.y, bf_lo(w1), o2); o3 = fmaf(e.y, bf_hi(w1), o3);
-                o0 = fmaf(e.z, bf_lo(w2), o0); o1 = fmaf(e.z, bf_hi(w2), o1);
-                o2 = fmaf(e.w, bf_lo(w3), o2); o3 = fmaf(e.w, bf_hi(w3), o3);
+#pragma unroll
+                for (int t = 0; t < PPL; ++t) {
+                    if (lane + 32 * t >= NP) continue;
+                    const uint32_t vo = (uint32_t)(lane + 32 * t) << 2;
+                    const uint32_t w0 = lds32(stage + (uint32_t)r * kRow + vo);
+                    const uint32_t w1 = lds32(stage + (uint32_t)(r + 1) * kRow + vo);
+                    const uint32_t w2 = lds32(stage + (uint32_t)(r + 2) * kRow + vo);
+                    const uint32_t w3 = lds32(stage + (uint32_t)(r + 3) * kRow + vo);
+                    o[t][0] = fmaf(e.x, bf_lo(w0), o[t][0]); o[t][1] = fmaf(e.x, bf_hi(w0), o[t][1]);
+                    o[t][2] = fmaf(e.y, bf_lo(w1), o[t][2]); o[t][3] = fmaf(e.y, bf_hi(w1), o[t][3]);
+                    o[t][0] = fmaf(e.z, bf_lo(w2), o[t][0]); o[t][1] = fmaf(e.z, bf_hi(w2), o[t][1]);
+                    o[t][2] = fmaf(e.w, bf_lo(w3), o[t][2]); o[t][3] = fmaf(e.w, bf_hi(w3), o[t][3]);
+                }
             }
             const int rows = min(R, pos + 1 - c0r);
             for (int r = nfull; r < rows; ++r) {  // the rest, the new row from registers
                 const float e = sc_s[c0r + r];
-                float x0, x1;
-                if (c0r + r == pos) {
-                    x0 = vn0;
-                    x1 = vn1;
-                } else {
-                    const uint32_t w = lds32(stage + (uint32_t)r * kMRow + voff);
-                    x0 = bf_lo(w);
-                    x1 = bf_hi(w);
+#pragma unroll
+                for (int t = 0; t < PPL; ++t) {
+                    if (lane + 32 * t >= NP) continue;
+                    float x0, x1;
+                    if (c0r + r == pos) {
+                        x0 = vn0[t];
+                        x1 = vn1[t];
+                    } else {
+                        const uint32_t w = lds32(stage + (uint32_t)r * kRow + ((uint32_t)(lane + 32 * t) << 2));
+                        x0 = bf_lo(w);
+                        x1 = bf_hi(w);
+                    }
+                    o[t][0] = fmaf(e, x0, o[t][0]);
+                    o[t][1] = fmaf(e, x1, o[t][1]);
                 }
-                o0 = fmaf(e, x0, o0);
-                o1 = fmaf(e, x1, o1);
             }
             __syncwarp();
             if (lane == 0) issue_next(st);
         }
         const float inv = 1.f / lsum;
-        *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.out) + (int64_t)row * dq + g * HD + 2 * lane) =
-            __floats2bfloat162_rn((o0 + o2) * inv, (o1 + o3) * inv);
+#pragma unroll
+        for (int t = 0; t < PPL; ++t)
+            if (lane + 32 * t < NP)
+                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.out) + (int64_t)row * dq + g * HD +
+                                                    2 * (lane + 32 * t)) =
+                    __floats2bfloat162_rn((o[t][0] + o[t][2]) * inv, (o[t][1] + o[t][3]) * inv);
     }
 }
 
-template <int kMW, bool PAGED>
+template <int HD, int kMW, bool PAGED>
 bool launch_mha_w(const AttnArgs& a, cudaStream_t s) {
     const int items_max = a.max_rows * a.n_kv_heads;
     const int grid = std::max(a.num_sms, (items_max + kMW * kMItems - 1) / (kMW * kMItems));
@@ -806,21 +835,27 @@ bool launch_mha_w(const AttnArgs& a, cudaStream_t s) {
     // 227 KB less the static barriers; the stage pool takes what the per-warp
     // buffers leave (at least 2 stages of 32 rows per warp)
     constexpr size_t kBudget = 227 * 1024 - (size_t)kMW * kMMaxRing * 8 - 64;
-    const size_t fixed = 1024 + MhaSmem(kMW, 0, a.max_seq).total;
-    if (fixed + (size_t)kMW * 2 * 32 * kMRow > kBudget) return false;
+    const size_t fixed = 1024 + MhaSmem(HD, kMW, 0, a.max_seq).total;
+    if (fixed + (size_t)kMW * 2 * 32 * HD * 2 > kBudget) return false;
     const int pool_kb = (int)std::min<size_t>((kBudget - fixed) >> 10, 192);
     const size_t smem = fixed + ((size_t)pool_kb << 10);
-    auto kern = attention_mha_kernel<kMW, PAGED>;
+    auto kern = attention_mha_kernel<HD, kMW, PAGED>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(kern, dim3(grid), dim3(kMW * 32), smem, s, a, pool_kb);
     EEB_CHECK_LAUNCH();
     return true;
 }
 
+// head_dim 64: 16 warps (q in 64 registers); 80 / 128: 8 warps (more
+// registers per thread for the wider q and dim pairs)
 template <bool PAGED>
 bool launch_mha(const AttnArgs& a, cudaStream_t s) {
-    static const int warps = std::getenv("EEB_MHA_WARPS") ? std::atoi(std::getenv("EEB_MHA_WARPS")) : 16;
-    return warps == 8 ? launch_mha_w<8, PAGED>(a, s) : launch_mha_w<16, PAGED>(a, s);
+    switch (a.head_dim) {
+        case 64: return launch_mha_w<64, 16, PAGED>(a, s);
+        case 80: return launch_mha_w<80, 8, PAGED>(a, s);
+        case 128: return launch_mha_w<128, 8, PAGED>(a, s);
+        default: return false;
+    }
 }
 
 }  // namespace
@@ -830,7 +865,8 @@ bool launch_attention_dec(const AttnArgs& a, cudaStream_t s) {
     if (env && std::string(env) != "dec" && std::string(env) != "mha") return false;  // A/B against the one-item / pipelined kernels
     static const bool no_mha = env && std::string(env) == "dec";
     if (!no_mha && a.dtype == 1 && !a.kv_ready && a.splits <= 16 && !a.kv_part &&
-        a.n_heads == a.n_kv_heads && a.head_dim == 64 && a.max_seq % 4 == 0) {
+        a.n_heads == a.n_kv_heads && (a.head_dim == 64 || a.head_dim == 80 || a.head_dim == 128) &&
+        a.max_seq % 4 == 0) {
         const bool paged = a.page_size != a.max_seq;
         if (!paged || (a.page_size % 32 == 0 && a.pages_per_seq <= 32))
             if (paged ? launch_mha<true>(a, s) : launch_mha<false>(a, s)) return true;

@@ -149,11 +149,15 @@ MINI128 = eeb.ModelDesc("mini-hd128", 4, 1024, 8, 2, 1024, 1000, (2, 4), dtype=e
 # decode attention (attention_mha_kernel); 300 positions = ten 32-position chunks
 MINI_MHA = eeb.ModelDesc("mini-mha", 4, 512, 8, 8, 1024, 1000, (2, 4), dtype=eeb.BF16,
                          max_slots=16, max_seq_len=320, seed=13)
+MINI_MHA128 = eeb.ModelDesc("mini-mha128", 4, 1024, 8, 8, 1024, 1000, (2, 4), dtype=eeb.BF16,
+                            max_slots=16, max_seq_len=320, seed=17)
+MINI_MHA80 = eeb.ModelDesc("mini-mha80", 4, 1280, 16, 16, 1024, 1000, (2, 4), dtype=eeb.BF16,
+                           max_slots=16, max_seq_len=320, seed=19)
 
 
 @pytest.mark.parametrize("desc,npos", [(MINI.replace(dtype=eeb.BF16, name="mini-bf16"), 8), (MINI128, 300),
-                                       (MINI_MHA, 300)],
-                         ids=["hd64-gqa4", "hd128-gqa4-2chunks", "hd64-mha-10chunks"])
+                                       (MINI_MHA, 300), (MINI_MHA128, 300), (MINI_MHA80, 300)],
+                         ids=["hd64-gqa4", "hd128-gqa4-2chunks", "hd64-mha-10chunks", "hd128-mha", "hd80-mha"])
 def test_bf16_token_agreement(ctx, desc, npos):
     """bf16 tensor-core path (mma.sync flash-decode attention, tcgen05 GEMMs at
     B=16) against the oracle; npos=300 crosses the 128-position attention chunk."""
