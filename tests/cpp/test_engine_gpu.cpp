@@ -157,6 +157,29 @@ int main(int argc, char** argv) {
         for (const auto& [m, d] : rep.serving_history) std::printf(" %s@%d", m.c_str(), d);
         std::printf("\n");
     }
+    {  // drift with one candidate: no model to switch to, so the breach actions
+       // deepen the serving model (load-more from the pinned host tier)
+        CudaBackend be(0, /*host_tier=*/true);
+        EngineConfig cfg = make_cfg(Mode::helios, "");
+        cfg.policy.k = 1;
+        const std::uint64_t seed = repo.at("small").arch.seed;
+        cfg.token_fn = [seed](std::int64_t rid, int pos, int vocab) -> int32_t {
+            const bool murky = rid >= 16;  // the first eval phase profiles 16 easy requests
+            for (std::uint64_t k = 1;; ++k) {
+                const int32_t t = synthetic_token(k * 0x9e3779b97f4a7c15ULL, rid, pos, vocab);
+                const float z = eeb::synth::z_of(seed, t);
+                if (murky ? z > 0.85f : z < 0.6f) return t;
+            }
+        };
+        cfg.policy.ri = 1000;
+        BatchedEngine eng(repo, be, cfg);
+        const EngineReport rep = eng.run(reqs);
+        check_report(rep, reqs);
+        CHECK(rep.ld_count >= 1 && rep.sw_count == 0);
+        std::printf("drift (k=1): ld %lld, sw %lld, history", (long long)rep.ld_count, (long long)rep.sw_count);
+        for (const auto& [m, d] : rep.serving_history) std::printf(" %s@%d", m.c_str(), d);
+        std::printf("\n");
+    }
     {  // ee_single: introspective exits on the device; exit mixture near the calibrated 73/27
         CudaBackend be(0);
         BatchedEngine eng(repo, be, make_cfg(Mode::ee_single, "small"));
