@@ -701,6 +701,21 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // (at most 16 planes: the attention kernels sum up to 16 QKV planes in registers;
     //  only narrow GEMMs such as a 70B tensor-parallel QKV shard would want more)
     int splits = std::max(1, std::min(std::min(kblocks / 2, wave / tiles), 16));
+    static const int env_widesplit = std::getenv("EEB_TC_WIDESPLIT") ? std::atoi(std::getenv("EEB_TC_WIDESPLIT")) : 2;
+    if (tiles > wave / 2 && !a.head_tri && !a.act_out) {
+        // wide GEMMs (more tiles than half a wave, e.g. the 34B up projection:
+        // 344 tiles): the split count with the best wave efficiency, planes
+        // capped at the weight bytes (s * rows * 4 <= K * 2)
+        double best = 0.0;
+        for (int sp = 1; sp <= env_widesplit && sp <= kblocks / 2 && (size_t)sp * bpad * 4 <= (size_t)a.K * 2; ++sp) {
+            const int units = tiles * sp;
+            const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
+            if (eff > best + 0.02) {
+                best = eff;
+                splits = sp;
+            }
+        }
+    }
     // many rows (prefill chunks): cap the f32 partial planes at about the
     // weight bytes (splits * rows * N * 4 <= N * K * 2); decode shapes are
     // unaffected (C2: K / (2 * 64) = 16 >= the splits chosen above)
