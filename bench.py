@@ -191,8 +191,11 @@ def workload_config(args, desc):
             "context": f"{args.prompt}..{args.prompt + args.warmup + args.steps - 1} (timed steps: "
                        f"{args.prompt + args.warmup}..{args.prompt + args.warmup + args.steps - 1})",
             "th": args.th, "policy": args.policy,
-            "parallelism": (f"tp{args.tp} (Megatron shards; NCCL all-reduce of row-parallel partials and "
-                            f"all-gather of vocab-parallel head partials inside the step)" if args.tp > 1 else
+            "parallelism": ((f"tp{args.tp} (Megatron shards; row-parallel partials reduce-scattered, "
+                             f"all-gathered and folded into the residual + RMSNorm by one peer-memory kernel; "
+                             f"vocab-parallel head partials all-gathered by peer copies)" if args.tp_comm == "px" else
+                             f"tp{args.tp} (Megatron shards; NCCL all-reduce of row-parallel partials and "
+                             f"all-gather of vocab-parallel head partials inside the step)") if args.tp > 1 else
                             f"replicas x{args.gpus} (requests sharded, no data-path collective)"),
             "l2": "inputs larger than L2 (GBs of weights streamed per step > 126 MB L2)"}
 
@@ -419,12 +422,19 @@ def run_eeb(args, desc):
     # rows served per step by the whole job: replicas add rows, a TP group does not
     job_rows = B if tp > 1 else world * B
     ctx = eeb.Context(local)
-    if tp > 1:
+    if tp > 1 and args.tp_comm == "nccl":
         uid = [eeb.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.nccl_init(uid[0], world, rank)
     ctx.set_gemm_tier(args.tier)
     m = ctx.register(desc)
+    if tp > 1 and args.tp_comm == "px":
+        # peer-memory exchange (tp_norm / px_gather kernels over NVLink P2P):
+        # every rank's exchange buffer through CUDA IPC handles
+        _, h = ctx.tp_px_alloc(m)
+        handles = [None] * world
+        dist.all_gather_object(handles, h)
+        ctx.tp_px_attach(m, world, handles=handles)
     ctx.load_layers(m, desc.num_layers)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
     rng = np.random.default_rng(1000 if tp > 1 else 1000 + rank)  # a TP group decodes the same rows
@@ -735,6 +745,9 @@ def main():
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 (34B) line attached at N=1")
     ap.add_argument("--tier", type=int, default=0, help="0 auto, 1 CUDA-core GEMV, 2 tcgen05 GEMMs")
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel group = the launched ranks (C5)")
+    ap.add_argument("--tp-comm", choices=["px", "nccl"], default="px",
+                    help="C5 exchange: px = fused peer-memory reduce + residual + RMSNorm kernels (default), "
+                         "nccl = NCCL all-reduce / all-gather between the step's kernels")
     ap.add_argument("--sweep", action="store_true", help="batch sweep of this workload with per-batch roofline")
     args = ap.parse_args()
     if args.warmup < 3:

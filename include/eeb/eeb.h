@@ -292,6 +292,24 @@ eeb_status eeb_nccl_unique_id(uint8_t* id128);
 eeb_status eeb_nccl_init(eeb_ctx* ctx, const uint8_t* id128, int nranks, int rank);
 eeb_status eeb_profile_allreduce(eeb_ctx* ctx, int64_t* counters, int n, double* sum_neg_logprob);
 
+/* Peer-memory tensor parallelism (C5 over NVLink / NVSwitch, no NCCL on the
+ * step's data path).  Each rank context of a tp_size > 1 model allocates one
+ * exchange buffer (eeb_tp_px_alloc: returns its device pointer and a CUDA IPC
+ * handle, 64 bytes), the caller distributes them (one process per GPU: the
+ * IPC handles; ranks of one process: the pointers), and every rank attaches
+ * the full set in rank order (eeb_tp_px_attach; peer_ptrs[p] may be null
+ * where ipc_handles64 + 64 p is given; the own entry is ignored).  From then
+ * on each row-parallel O / down GEMM is followed by ONE kernel that
+ * reduce-scatters the partial planes across the ranks through peer memory,
+ * all-gathers the reduced rows, and applies the residual add + RMSNorm
+ * (tp_norm), and the vocab-parallel exit-head partials are all-gathered by a
+ * peer-memory copy kernel.  Every rank must issue the same sequence of steps
+ * and prefills (as with NCCL).  Replaces the reference's per-token model call
+ * for a model served over several GPUs (engine.hpp:325-398). */
+eeb_status eeb_tp_px_alloc(eeb_ctx* ctx, int model, void** dev_ptr, uint8_t* ipc_handle64);
+eeb_status eeb_tp_px_attach(eeb_ctx* ctx, int model, int nranks, void* const* peer_ptrs,
+                            const uint8_t* ipc_handles64);
+
 #ifdef __cplusplus
 }
 #endif

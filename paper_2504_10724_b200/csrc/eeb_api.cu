@@ -143,6 +143,18 @@ struct Model {
     std::unique_ptr<PendingLoad> pending;
     double last_load_s = 0.0;
     int64_t last_load_bytes = 0;
+    // peer-memory tensor parallelism (eeb_tp_px_alloc / eeb_tp_px_attach):
+    // this rank's exchange buffer and every rank's, as mapped here
+    DevBuf px;
+    PxPeers pxp;
+    std::vector<void*> px_opened;  // CUDA IPC mappings of peer buffers
+    bool px_on() const { return pxp.nranks > 1; }
+    Model() = default;
+    Model(const Model&) = delete;
+    Model& operator=(const Model&) = delete;
+    ~Model() {
+        for (void* q : px_opened) cudaIpcCloseMemHandle(q);
+    }
 };
 
 struct GraphKey {
@@ -190,6 +202,9 @@ struct eeb_ctx {
     // the next tensor-core GEMM's weights, prefetched into L2 by the current one
     const void* pf_ptr = nullptr;
     size_t pf_bytes = 0;
+    // plane output redirected into a TP exchange buffer (PxPlanesScope)
+    float* gemm_out = nullptr;
+    int64_t gemm_out_elems = 0;
     // step workspace (grow-only)
     int cap_rows = 0;
     eeb::DevBuf xA, xB, hn, hnB, hhead, attn, mlp_h, ws;
@@ -986,8 +1001,9 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     a.N = N;
     a.K = K;
     a.plane_stride = (int64_t)batch * N;
-    a.out = c->ws.as<float>() + (int64_t)plane0 * a.plane_stride;
-    a.max_planes = (int)std::min<int64_t>(64, c->ws_elems / a.plane_stride - plane0);
+    a.out = (c->gemm_out ? c->gemm_out : c->ws.as<float>()) + (int64_t)plane0 * a.plane_stride;
+    a.max_planes = (int)std::min<int64_t>(64, (c->gemm_out ? c->gemm_out_elems : c->ws_elems) / a.plane_stride - plane0);
+    if (a.max_planes < 1) throw Error(EEB_E_CAPACITY, "GEMM output planes do not fit the workspace");
     a.num_sms = c->num_sms;
     a.pf = c->pf_ptr;
     a.pf_bytes = c->pf_bytes;
@@ -1073,6 +1089,23 @@ bool l2pf_fused() {
 struct PlaneSet {
     const float* base;
     int planes;
+    bool px = false;  // the planes sit in the TP exchange buffer: reduce with launch_tp_norm
+};
+
+// The row-parallel GEMMs of a peer-memory TP rank write their planes into the
+// rank's exchange buffer, where the row owners read them.
+struct PxPlanesScope {
+    eeb_ctx* c;
+    PxPlanesScope(eeb_ctx* cc, const Model& m, bool on) : c(cc) {
+        if (on) {
+            c->gemm_out = reinterpret_cast<float*>(m.pxp.base[m.pxp.rank] + m.pxp.lay.planes);
+            c->gemm_out_elems = m.pxp.lay.planes_elems;
+        }
+    }
+    ~PxPlanesScope() {
+        c->gemm_out = nullptr;
+        c->gemm_out_elems = 0;
+    }
 };
 
 // One decoder layer up to (not including) the final residual + RMSNorm:
@@ -1159,8 +1192,10 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
     }
     int planes = 0;
     next_pf(W.wup.p, (size_t)m.up_l * D * wb);
+    const bool px = m.tp > 1 && m.shards == 1 && m.px_on();
     {
         Timer t(c, kCatGemm);
+        PxPlanesScope px_scope(c, m, px);
         for (int sh = 0; sh < m.shards; ++sh)
             planes += skip_cat("gemm") ? 1
                                        : gemm(c, kCatGemm, m, static_cast<const char*>(W.wo.p) + (size_t)sh * D * m.dq_l * wb,
@@ -1168,8 +1203,15 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
                                               m.dq_l, cur.n_active, batch, planes);
     }
     PlaneSet o{ws, planes};
-    if (m.tp > 1 && m.shards == 1) o = {tp_allreduce(c, m, ws, planes, cur.n_active, batch), 1};
-    {
+    if (px) {
+        Timer t(c, kCatNorm);
+        launch_tp_norm(d.dtype, m.pxp, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
+                       W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
+        count(c, kCatNorm, 1);
+    } else if (m.tp > 1 && m.shards == 1) {
+        o = {tp_allreduce(c, m, ws, planes, cur.n_active, batch), 1};
+    }
+    if (!px) {
         Timer t(c, kCatNorm);
         if (!skip_cat("norm"))
             launch_residual_norm(d.dtype, o.base, o.planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
@@ -1231,12 +1273,14 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         next_pf(m.layers[l]->wqkv.p, (size_t)qkv_l * D * wb);
     {
         Timer t(c, kCatGemm);
+        PxPlanesScope px_scope(c, m, px);
         for (int sh = 0; sh < m.shards; ++sh)
             planes += skip_cat("gemm") ? 1
                                        : gemm(c, kCatGemm, m, static_cast<const char*>(W.wdown.p) + (size_t)sh * D * m.f_l * wb,
                                               static_cast<const char*>(c->mlp_h.p) + (size_t)sh * batch * m.f_l * wb, D,
                                               m.f_l, cur.n_active, batch, planes);
     }
+    if (px) return {reinterpret_cast<const float*>(m.pxp.base[m.pxp.rank] + m.pxp.lay.planes), planes, true};
     PlaneSet dn{ws, planes};
     if (m.tp > 1 && m.shards == 1) dn = {tp_allreduce(c, m, ws, planes, cur.n_active, batch), 1};
     return dn;
@@ -1360,7 +1404,10 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             // the next layer's QKV weights -> L2 during the norm (not before an
             // exit head: its vocab-sized stream would evict them first)
             const void* pf = l2pf_fused() && more && !exit_here && m.shards == 1 ? m.layers[l]->wqkv.p : nullptr;
-            if (g1 && !skip_cat("norm"))
+            if (g1 && dn.px)
+                launch_tp_norm(d.dtype, m.pxp, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
+                               g1, o1, g2, o2, s);
+            else if (g1 && !skip_cat("norm"))
                 launch_residual_norm(d.dtype, planes_base, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D,
                                      d.norm_eps, g1, o1, g2, o2, s, pf,
                                      (size_t)(m.dq_l + 2 * m.dkv_l) * D * m.wbytes);
@@ -1381,14 +1428,19 @@ void enqueue_step(eeb_ctx* c, int mi, int depth, int policy, float th, int batch
             const int64_t region = (int64_t)batch * tiles_l * 4;  // floats per rank region
             if (!c->retain_logits && !skip_cat("head") && c->gemm_tier != 1 && d.dtype == EEB_BF16 &&
                 !std::getenv("EEB_HEAD_UNFUSED")) {
+                const bool px = m.tp > 1 && m.shards == 1 && m.px_on();
                 for (int sh = 0; sh < m.shards; ++sh) {
                     const int g = m.shard_rank(sh);
+                    float* tri = px ? reinterpret_cast<float*>(m.pxp.base[m.pxp.rank] + m.pxp.lay.head)
+                                    : c->head_tri.as<float>() + g * region;
                     head_tiles = gemm_head_fused(c, m, static_cast<const char*>(m.head[e]->p) + (size_t)sh * m.v_l * D * m.wbytes,
-                                                 c->hhead.p, m.v_l, D, cur.n_active, batch,
-                                                 c->head_tri.as<float>() + g * region, g * m.v_l);
+                                                 c->hhead.p, m.v_l, D, cur.n_active, batch, tri, g * m.v_l);
                     if (head_tiles == 0) break;
                 }
-                if (head_tiles && m.tp > 1 && m.shards == 1) {
+                if (head_tiles && px) {
+                    launch_px_gather(m.pxp, region, c->head_tri.as<float>(), s);
+                    count(c, kCatHead, 1);
+                } else if (head_tiles && m.tp > 1 && m.shards == 1) {
                     if (!c->nccl) throw Error(EEB_E_DOMAIN, "tensor-parallel rank without a communicator (eeb_nccl_init)");
                     float* all = c->head_tri.as<float>();
                     const ncclResult_t r = nccl().all_gather(all + m.rank * region, all, (size_t)region, ncclFloat32,
@@ -1495,7 +1547,10 @@ void enqueue_prefill(eeb_ctx* c, int mi, int depth, int rows) {
     count(c, kCatOther, 3);
     for (int l = 1; l <= depth; ++l) {
         const PlaneSet dn = layer_core(c, m, l, cur, h, rows, true);
-        if (l < depth)  // the next layer's attention norm (the last layer's residual is not needed)
+        if (l < depth && dn.px)  // the next layer's attention norm (the last layer's residual is not needed)
+            launch_tp_norm(d.dtype, m.pxp, dn.planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D, d.norm_eps,
+                           m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+        else if (l < depth)
             launch_residual_norm(d.dtype, dn.base, dn.planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D,
                                  d.norm_eps, m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
         count(c, kCatNorm, l < depth ? 1 : 0);
@@ -1704,6 +1759,28 @@ void kv_sync_table(eeb_ctx* c, Model& m) {
     EEB_CUDA(cudaMemcpyAsync(m.page_table.p, m.h_table.data(), m.h_table.size() * 4, cudaMemcpyHostToDevice,
                              c->stream));
     m.table_dirty = false;
+}
+
+// Peer-memory tensor parallelism: the exchange-buffer layout is a function of
+// the model descriptor only, so every rank computes the same offsets.
+PxLayout px_layout(const Model& m) {
+    const eeb_model_desc& d = m.desc;
+    PxLayout L;
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    int64_t off = 0;
+    L.arrive = off; off += al((int64_t)kPxMaxRanks * kPxMaxCtas * 4);
+    L.pushed = off; off += al((int64_t)kPxMaxCtas * 4);
+    L.epoch = off; off += al((int64_t)kPxMaxCtas * 4);
+    L.g_arrive = off; off += al((int64_t)kPxMaxRanks * kPxGatherCtas * 4);
+    L.g_epoch = off; off += al((int64_t)kPxGatherCtas * 4);
+    L.rows = std::max(d.max_slots, kPxMaxCtas);
+    L.planes_elems = (int64_t)16 * L.rows * d.d_model;
+    L.planes = off; off += al(L.planes_elems * 4);
+    L.red = off; off += al((int64_t)L.rows * d.d_model * 4);
+    L.head_elems = (int64_t)d.max_slots * ((m.v_l + 127) / 128) * 4;
+    L.head = off; off += al(L.head_elems * 4);
+    L.bytes = off;
+    return L;
 }
 
 }  // namespace
@@ -2681,6 +2758,72 @@ eeb_status eeb_profile_read(eeb_ctx* c, char* json_out, int64_t cap) {
 }
 
 void* eeb_stream(eeb_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+eeb_status eeb_tp_px_alloc(eeb_ctx* c, int model, void** dev_ptr, uint8_t* ipc_handle64) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        Model& m = model_of(c, model);
+        if (m.tp < 2 || m.rank < 0)
+            throw Error(EEB_E_DOMAIN, "peer exchange needs a tensor-parallel rank model (tp_size >= 2, tp_rank >= 0)");
+        if (m.tp > kPxMaxRanks) throw Error(EEB_E_DOMAIN, "peer exchange supports at most 8 ranks");
+        EEB_CUDA(cudaSetDevice(c->device));
+        const PxLayout L = px_layout(m);
+        if (m.px.bytes < (size_t)L.bytes) {
+            m.px.release();
+            m.px.ensure((size_t)L.bytes);
+        }
+        EEB_CUDA(cudaMemset(m.px.p, 0, m.px.bytes));
+        if (dev_ptr) *dev_ptr = m.px.p;
+        if (ipc_handle64) {
+            cudaIpcMemHandle_t h;
+            EEB_CUDA(cudaIpcGetMemHandle(&h, m.px.p));
+            static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+            std::memcpy(ipc_handle64, &h, 64);
+        }
+    });
+}
+
+eeb_status eeb_tp_px_attach(eeb_ctx* c, int model, int nranks, void* const* peer_ptrs, const uint8_t* ipc_handles64) {
+    return guarded([&] {
+        if (!c) throw Error(EEB_E_DOMAIN, "null context");
+        Model& m = model_of(c, model);
+        if (!m.px.p) throw Error(EEB_E_STALE, "eeb_tp_px_alloc first");
+        if (nranks != m.tp) throw Error(EEB_E_DOMAIN, "nranks must equal the model's tp_size");
+        if (!peer_ptrs && !ipc_handles64) throw Error(EEB_E_DOMAIN, "peer pointers or IPC handles required");
+        EEB_CUDA(cudaSetDevice(c->device));
+        cudaDeviceSynchronize();
+        for (void* q : m.px_opened) cudaIpcCloseMemHandle(q);
+        m.px_opened.clear();
+        PxPeers P;
+        P.nranks = nranks;
+        P.rank = m.rank;
+        P.lay = px_layout(m);
+        for (int p = 0; p < nranks; ++p) {
+            if (p == m.rank) {
+                P.base[p] = static_cast<char*>(m.px.p);
+            } else if (peer_ptrs && peer_ptrs[p]) {
+                // a buffer of this process: same device, or a peer GPU over NVLink
+                cudaPointerAttributes at{};
+                EEB_CUDA(cudaPointerGetAttributes(&at, peer_ptrs[p]));
+                if (at.device != c->device) {
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                    else EEB_CUDA(e);
+                }
+                P.base[p] = static_cast<char*>(peer_ptrs[p]);
+            } else {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, ipc_handles64 + (size_t)p * 64, 64);
+                void* q = nullptr;
+                EEB_CUDA(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+                m.px_opened.push_back(q);
+                P.base[p] = static_cast<char*>(q);
+            }
+        }
+        m.pxp = P;
+        drop_graphs(c, model);  // captured steps hold the exchange pointers by value
+    });
+}
 
 eeb_status eeb_nccl_unique_id(uint8_t* id128) {
     return guarded([&] {

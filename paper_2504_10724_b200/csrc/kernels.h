@@ -43,6 +43,45 @@ bool launch_embed_norm(int dtype, const void* emb, const int* tok, const int* sl
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
                           void* out2, cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0);
+// ---- tensor-parallel exchange over peer memory (rows.cu) ---------------------
+// Every rank of a TP group owns one exchange buffer ("px") with the same
+// layout; `base[p]` is rank p's buffer as mapped in this process (NVLink P2P
+// or CUDA IPC; on one device, plain pointers).  Flags are u32 cells written by
+// peers with st.release.sys and polled with ld.acquire.sys; each CTA index
+// keeps its own epoch counter, and every rank launches the same sequence of
+// exchanges with the same grids, so epochs advance in lockstep.
+constexpr int kPxMaxRanks = 8;
+constexpr int kPxMaxCtas = 1024;    // tp_norm: one CTA per row (prefill chunks <= 1024 rows)
+constexpr int kPxGatherCtas = 64;   // head-partial all-gather
+struct PxLayout {
+    int64_t arrive = 0;   // u32 [kPxMaxRanks][kPxMaxCtas]: rank p's CTA i reached the exchange
+    int64_t pushed = 0;   // u32 [kPxMaxCtas]: the row owner's reduced row i has landed here
+    int64_t epoch = 0;    // u32 [kPxMaxCtas]: this rank's per-CTA epoch counters (local only)
+    int64_t g_arrive = 0; // u32 [kPxMaxRanks][kPxGatherCtas]
+    int64_t g_epoch = 0;  // u32 [kPxGatherCtas]
+    int64_t planes = 0;   // f32 row-parallel GEMM partial planes (this rank's)
+    int64_t red = 0;      // f32 [rows][d]: reduced rows pushed by their owners
+    int64_t head = 0;     // f32 this rank's exit-head tile partials (vocab shard)
+    int64_t planes_elems = 0, rows = 0, head_elems = 0, bytes = 0;
+};
+struct PxPeers {
+    char* base[kPxMaxRanks];
+    int nranks = 0, rank = 0;
+    PxLayout lay;
+};
+// Two-shot all-reduce of the row-parallel partials fused with the residual add
+// and RMSNorm: CTA i's row is owned by rank i % nranks, which sums every rank's
+// `planes` planes of row i (rank-major, plane-minor: the order of the
+// all-shards context's split-K reduction) and pushes the sum to every rank;
+// every rank then applies x += sum, out1 = T(rmsnorm(x) g1), out2 likewise —
+// so all ranks hold bit-identical residual streams.
+void launch_tp_norm(int dtype, const PxPeers& px, int planes, int64_t plane_stride, const int* n_active, int max_rows,
+                    float* x, int d, float eps, const float* g1, void* out1, const float* g2, void* out2,
+                    cudaStream_t s);
+// All-gather of the vocab-parallel exit-head partials: rank p's `region`
+// floats (its px head area) land at dst + p * region on every rank.
+void launch_px_gather(const PxPeers& px, int64_t region, float* dst, cudaStream_t s);
+
 // out[i][:] = sum_s part[s][i][:] for the live rows (tensor-parallel partial before all-reduce).
 void launch_plane_sum(const float* part, int splits, int64_t split_stride, const int* n_active, int max_rows, int d,
                       float* out, int num_sms, cudaStream_t s);

@@ -261,6 +261,176 @@ __global__ void gather_rows_kernel(Stamp stamp, const float* x_cur, float* x_nxt
     }
 }
 
+
+// ---- tensor-parallel exchange over peer memory (see kernels.h) ---------------
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Spin until *flag >= want.  A peer that never arrives (a rank that died or
+// launched a different exchange sequence) traps after ~10 s instead of
+// hanging the device.
+__device__ __forceinline__ void px_wait(const uint32_t* flag, uint32_t want) {
+    if ((int32_t)(ld_acquire_sys(flag) - want) >= 0) return;
+    const unsigned long long t0 = gtimer();
+    while ((int32_t)(ld_acquire_sys(flag) - want) < 0) {
+        __nanosleep(64);
+        if (gtimer() - t0 > 10000000000ull) {
+            printf("eeb: tensor-parallel exchange timed out (flag %p want %u have %u)\n", flag, want,
+                   ld_acquire_sys(flag));
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ uint32_t* px_u32(const PxPeers& px, int rank, int64_t off) {
+    return reinterpret_cast<uint32_t*>(px.base[rank] + off);
+}
+
+// One CTA per row (grid = the step's max rows, identical on every rank).
+template <typename T, int kV>
+__global__ void __launch_bounds__(kNormThreads)
+    tp_norm_kernel(Stamp stamp, PxPeers px, int planes, int64_t plane_stride, const int* n_active, float* x, int d,
+                   float eps, const float* g1, T* out1, const float* g2, T* out2) {
+    StampScope stamp_scope(stamp);
+    pdl_wait();  // this rank's partial planes are complete
+    stamp_waited(stamp);
+    const int i = blockIdx.x, me = px.rank;
+    const int owner = i % px.nranks;
+    __shared__ float red[32];
+    __shared__ uint32_t epoch_s;
+    uint32_t* epoch_cell = px_u32(px, me, px.lay.epoch) + i;
+    if (threadIdx.x == 0) {
+        const uint32_t e = *epoch_cell + 1;
+        epoch_s = e;
+        if (owner != me) {
+            __threadfence_system();
+            st_release_sys(px_u32(px, owner, px.lay.arrive) + me * kPxMaxCtas + i, e);
+        } else {
+            for (int p = 0; p < px.nranks; ++p)
+                if (p != me) px_wait(px_u32(px, me, px.lay.arrive) + p * kPxMaxCtas + i, e);
+        }
+    }
+    __syncthreads();
+    const uint32_t e = epoch_s;
+    const int n = *n_active;
+    const bool live = i < n;
+    float4 y[kV];
+    if (owner == me) {
+        // reduce row i over every rank's planes, rank-major then plane order
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const int c = 4 * (threadIdx.x + k * blockDim.x);
+            y[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (live && c < d) {
+                for (int p = 0; p < px.nranks; ++p) {
+                    const float* src = reinterpret_cast<const float*>(px.base[p] + px.lay.planes) + (int64_t)i * d + c;
+                    for (int s0 = 0; s0 < planes; s0 += kBatch) {
+                        float4 t[kBatch];
+#pragma unroll
+                        for (int j = 0; j < kBatch; ++j)
+                            if (s0 + j < planes) t[j] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + j) * plane_stride));
+#pragma unroll
+                        for (int j = 0; j < kBatch; ++j)
+                            if (s0 + j < planes) add4(y[k], t[j]);
+                    }
+                }
+                for (int p = 0; p < px.nranks; ++p)
+                    if (p != me)
+                        __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(px.base[p] + px.lay.red) +
+                                                         (int64_t)i * d + c),
+                               y[k]);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (int p = 0; p < px.nranks; ++p)
+                if (p != me) st_release_sys(px_u32(px, p, px.lay.pushed) + i, e);
+        }
+    } else {
+        if (threadIdx.x == 0) px_wait(px_u32(px, me, px.lay.pushed) + i, e);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const int c = 4 * (threadIdx.x + k * blockDim.x);
+            y[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (live && c < d)
+                y[k] = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(px.base[me] + px.lay.red) +
+                                                              (int64_t)i * d + c));
+        }
+    }
+    if (threadIdx.x == 0) *epoch_cell = e;
+    pdl_launch_dependents();
+    if (!live) return;
+    // x += sum; RMSNorm — as residual_norm_kernel
+    float* row = x + (int64_t)i * d;
+    float4 v[kV];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < d) {
+            float4 xv = *reinterpret_cast<const float4*>(row + c);
+            add4(xv, y[k]);
+            *reinterpret_cast<float4*>(row + c) = xv;
+            v[k] = xv;
+            ss += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+        }
+    }
+    ss = block_sum(ss, red);
+    const float inv = rsqrtf(ss / (float)d + eps);
+    if (!out1) return;
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        if (c < d) {
+            const float4 gg = *reinterpret_cast<const float4*>(g1 + c);
+            const float4 nv = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
+            store4<T>(out1 + (int64_t)i * d + c, make_float4(nv.x * gg.x, nv.y * gg.y, nv.z * gg.z, nv.w * gg.w));
+            if (out2) {
+                const float4 g = *reinterpret_cast<const float4*>(g2 + c);
+                store4<T>(out2 + (int64_t)i * d + c, make_float4(nv.x * g.x, nv.y * g.y, nv.z * g.z, nv.w * g.w));
+            }
+        }
+    }
+}
+
+// Pull-style all-gather: after every rank's CTA b arrived (its head partials
+// are complete), CTA b copies its slice of every rank's head area into dst.
+// A rank overwrites its head area only at its next exit head, i.e. after at
+// least one tp_norm exchange, which every rank enters only once its previous
+// kernels (this gather included) have finished.
+__global__ void __launch_bounds__(256) px_gather_kernel(Stamp stamp, PxPeers px, int64_t region4, float4* dst) {
+    StampScope stamp_scope(stamp);
+    pdl_wait();
+    stamp_waited(stamp);
+    const int b = blockIdx.x, me = px.rank;
+    __shared__ uint32_t epoch_s;
+    uint32_t* epoch_cell = px_u32(px, me, px.lay.g_epoch) + b;
+    if (threadIdx.x == 0) {
+        const uint32_t e = *epoch_cell + 1;
+        epoch_s = e;
+        __threadfence_system();
+        for (int p = 0; p < px.nranks; ++p)
+            if (p != me) st_release_sys(px_u32(px, p, px.lay.g_arrive) + me * kPxGatherCtas + b, e);
+        for (int p = 0; p < px.nranks; ++p)
+            if (p != me) px_wait(px_u32(px, me, px.lay.g_arrive) + p * kPxGatherCtas + b, e);
+    }
+    __syncthreads();
+    for (int p = 0; p < px.nranks; ++p) {
+        const float4* src = reinterpret_cast<const float4*>(px.base[p] + px.lay.head);
+        for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < region4; k += (int64_t)gridDim.x * blockDim.x)
+            dst[p * region4 + k] = __ldcg(src + k);
+    }
+    if (threadIdx.x == 0) *epoch_cell = epoch_s;
+    pdl_launch_dependents();
+}
+
 }  // namespace
 
 void launch_embed(int dtype, const void* emb, const int* tok, const int* slot_in, const int* pos_in,
@@ -316,6 +486,42 @@ void launch_residual_norm(int dtype, const float* part, int splits, int64_t spli
         else if (kv == 2) go(residual_norm_kernel<__nv_bfloat16, 2>, o1, o2);
         else go(residual_norm_kernel<__nv_bfloat16, 4>, o1, o2);
     }
+    EEB_CHECK_LAUNCH();
+}
+
+void launch_tp_norm(int dtype, const PxPeers& px, int planes, int64_t plane_stride, const int* n_active, int max_rows,
+                    float* x, int d, float eps, const float* g1, void* out1, const float* g2, void* out2,
+                    cudaStream_t s) {
+    const int q = d / 4;
+    if (d % 4 != 0 || q > 4 * kNormThreads) throw Error(1, "tp_norm: d_model must be a multiple of 4 and at most 8192");
+    if (max_rows > kPxMaxCtas || max_rows > px.lay.rows) throw Error(1, "tp_norm: more rows than the exchange buffer holds");
+    if (px.nranks < 2 || px.nranks > kPxMaxRanks) throw Error(1, "tp_norm: bad rank count");
+    const int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
+    const dim3 grid(max_rows), block(std::max(32, std::min(kNormThreads, (q / kv + 31) / 32 * 32)));
+    auto go = [&](auto kern, auto* o1, auto* o2) {
+        launch_pdl(kern, grid, block, 0, s, px, planes, plane_stride, n_active, x, d, eps, g1, o1, g2, o2);
+    };
+    if (dtype == 0) {
+        float* o1 = static_cast<float*>(out1);
+        float* o2 = static_cast<float*>(out2);
+        if (kv == 1) go(tp_norm_kernel<float, 1>, o1, o2);
+        else if (kv == 2) go(tp_norm_kernel<float, 2>, o1, o2);
+        else go(tp_norm_kernel<float, 4>, o1, o2);
+    } else {
+        __nv_bfloat16* o1 = static_cast<__nv_bfloat16*>(out1);
+        __nv_bfloat16* o2 = static_cast<__nv_bfloat16*>(out2);
+        if (kv == 1) go(tp_norm_kernel<__nv_bfloat16, 1>, o1, o2);
+        else if (kv == 2) go(tp_norm_kernel<__nv_bfloat16, 2>, o1, o2);
+        else go(tp_norm_kernel<__nv_bfloat16, 4>, o1, o2);
+    }
+    EEB_CHECK_LAUNCH();
+}
+
+void launch_px_gather(const PxPeers& px, int64_t region, float* dst, cudaStream_t s) {
+    if (region % 4 != 0 || region > px.lay.head_elems) throw Error(1, "px_gather: region does not fit the exchange buffer");
+    const int64_t r4 = region / 4;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(kPxGatherCtas, (r4 + 255) / 256));
+    launch_pdl(px_gather_kernel, dim3(grid), dim3(256), 0, s, px, r4, reinterpret_cast<float4*>(dst));
     EEB_CHECK_LAUNCH();
 }
 

@@ -70,6 +70,7 @@ EXPORTED = [
     "eeb_kv_configure_pages", "eeb_kv_reserve", "eeb_kv_release", "eeb_kv_pages",
     "eeb_debug_stamps", "eeb_debug_stamps_read", "eeb_debug_read_kv_span",
     "eeb_weight_layout", "eeb_host_stage_layer", "eeb_host_stage_base", "eeb_load_layers_from",
+    "eeb_tp_px_alloc", "eeb_tp_px_attach",
     "eeb_debug_stamps_cta",
 ]
 
@@ -532,6 +533,23 @@ class Context:
 
         b = (C.c_uint8 * 128)(*uid)
         _check(self.lib.eeb_nccl_init(self.h, b, nranks, rank))
+
+    # -- peer-memory tensor parallelism ---------------------------------------------
+    def tp_px_alloc(self, model: int) -> tuple[int, bytes]:
+        """This rank's TP exchange buffer: (device pointer, CUDA IPC handle)."""
+        ptr = C.c_void_p()
+        h = (C.c_uint8 * 64)()
+        _check(self.lib.eeb_tp_px_alloc(self.h, model, C.byref(ptr), h))
+        return int(ptr.value), bytes(h)
+
+    def tp_px_attach(self, model: int, nranks: int, ptrs=None, handles=None) -> None:
+        """Attach every rank's exchange buffer (rank order): device pointers of
+        this process (`ptrs`) or CUDA IPC handles from other processes."""
+        p = (C.c_void_p * nranks)(*([int(x) if x else None for x in ptrs] if ptrs else [None] * nranks))
+        hb = None
+        if handles is not None:
+            hb = (C.c_uint8 * (64 * nranks))(*b"".join(handles))
+        _check(self.lib.eeb_tp_px_attach(self.h, model, nranks, p if ptrs else None, hb))
 
     def profile_allreduce(self, counters: np.ndarray, sum_neg_logprob: float) -> tuple[np.ndarray, float]:
         c = np.ascontiguousarray(counters, dtype=np.int64).copy()
