@@ -2679,6 +2679,18 @@ eeb_status eeb_debug_bench_gemm(eeb_ctx* c, int tier, int n, int k, int batch, i
         GemmArgs a;
         a.dtype = EEB_BF16; a.W = wv[0]->p; a.X = x.p; a.n_active = na.as<int>(); a.max_rows = batch; a.N = n; a.K = k;
         a.out = ws.as<float>(); a.plane_stride = plane; a.max_planes = max_planes; a.num_sms = c->num_sms;
+        // EEB_BENCH_ACT=1 (ReLU) / 2 (SwiGLU): the fused up projection (4-CTA
+        // cluster K reduction + activation epilogue) as layer_core launches it
+        static const int bench_act = std::getenv("EEB_BENCH_ACT") ? std::atoi(std::getenv("EEB_BENCH_ACT")) : 0;
+        DevBuf act;
+        if (bench_act) {
+            act.ensure((size_t)batch * n * 2);
+            a.out = nullptr;
+            a.plane_stride = 0;
+            a.max_planes = 1;
+            a.act_out = act.p;
+            a.act_kind = bench_act;
+        }
         int it = 0;
         static const bool bench_pf = std::getenv("EEB_BENCH_PF") != nullptr;  // + L2 prefetch of the next copy
         auto run = [&] {

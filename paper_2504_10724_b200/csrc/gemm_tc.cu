@@ -31,6 +31,7 @@ namespace eeb {
 namespace {
 
 constexpr int kBM = 128;           // output features per tile (UMMA M)
+constexpr int kRS = kBM + 4;         // row stride (floats) of a staged cs > 1 partial: 16-B aligned rows
 constexpr int kBK = 64;            // K per stage: one 128-byte swizzle atom of bf16
 constexpr int kThreads = 192;
 constexpr int kSmemBudget = 227 * 1024;
@@ -489,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 float v[16];
                 tmem_ld16(taddr + (uint32_t)c0, v);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) red[(c0 + j) * (kBM + 1) + f] = v[j];
+                for (int j = 0; j < 16; ++j) red[(c0 + j) * kRS + f] = v[j];
             }
         }
         }  // rows > 0
@@ -510,12 +511,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         // barrier (no cg::sync, whose GPU-scope fence would also drain this
         // CTA's global stores)
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        EEB_STAMP(threadIdx.x == 64, 7);  // cluster partials visible
         const int rank = (int)cluster.block_rank();
-        const int rows = *p.n_active;
-        const int lim = min(rows, p.bpad);
+        const int lim = min(rows_all, p.bpad);  // (not re-read: an L2 round trip after the barrier's L1 flush)
         const float* red = reinterpret_cast<const float*>(base_ptr);
         // this rank's finished rows (head mode), after the staged partials
-        float* fin = reinterpret_cast<float*>(base_ptr) + (size_t)p.bpad * (kBM + 1);
+        float* fin = reinterpret_cast<float*>(base_ptr) + (size_t)p.bpad * kRS;
         if (warp >= 2) {
             const int t = threadIdx.x - 64;  // 0..127: feature of the tile
             const int n = m_tile * kBM + t;
@@ -525,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int q = 0; q < 8; ++q) peer[q] = cluster.map_shared_rank(red, q < p.cs ? q : 0);
             auto finish = [&](int j, int row, float acc) {
                 if (p.head_tri) {
-                    fin[j * (kBM + 1) + t] = acc;
+                    fin[j * kRS + t] = acc;
                 } else if (p.act_out) {
                     if (p.act_kind == 2) {
                         const float u = __shfl_xor_sync(0xffffffffu, acc, 1);  // odd lane: up, even: gate
@@ -544,20 +545,49 @@ __global__ void __launch_bounds__(kThreads, 2)
             // 4-CTA clusters of the decode up projection: 16 rows x 4 peers,
             // a 64-row tile in one DSMEM round trip per rank.
             if (kCs4) {
-                constexpr int kR4 = 16;
-                for (int j0 = 0; rank + j0 * 4 < lim; j0 += kR4) {
-                    float v[kR4][4];
+                // 16-byte DSMEM loads (DSMEM moves ~20 B/clk per SM; per-thread
+                // 4-byte loads took 2.7 us for the 64-row tile): lane = 4
+                // consecutive features, epilogue warp ew takes this rank's
+                // rows j = ew, ew + 4, ...; kJ rows x 4 peers in flight.
+                const int ew = warp - 2, n4 = m_tile * kBM + 4 * lane;
+                constexpr int kJ = 4;
+                for (int j0 = ew; rank + j0 * 4 < lim; j0 += 4 * kJ) {
+                    float4 v[kJ][4];
 #pragma unroll
-                    for (int r = 0; r < kR4; ++r) {
-                        const int row = rank + (j0 + r) * 4;
+                    for (int r = 0; r < kJ; ++r) {
+                        const int row = rank + (j0 + 4 * r) * 4;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) v[r][q] = row < lim ? peer[q][row * (kBM + 1) + t] : 0.f;
+                        for (int q = 0; q < 4; ++q)
+                            v[r][q] = row < lim ? *reinterpret_cast<const float4*>(peer[q] + row * kRS + 4 * lane)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
-                    for (int r = 0; r < kR4; ++r) {
-                        const int row = rank + (j0 + r) * 4;
+                    for (int r = 0; r < kJ; ++r) {
+                        const int j = j0 + 4 * r, row = rank + j * 4;
                         if (row >= lim) break;
-                        finish(j0 + r, row, ((v[r][0] + v[r][1]) + v[r][2]) + v[r][3]);
+                        float4 a;  // rank (= k) order, as the scalar path
+                        a.x = ((v[r][0].x + v[r][1].x) + v[r][2].x) + v[r][3].x;
+                        a.y = ((v[r][0].y + v[r][1].y) + v[r][2].y) + v[r][3].y;
+                        a.z = ((v[r][0].z + v[r][1].z) + v[r][2].z) + v[r][3].z;
+                        a.w = ((v[r][0].w + v[r][1].w) + v[r][2].w) + v[r][3].w;
+                        if (p.head_tri) {
+                            *reinterpret_cast<float4*>(fin + j * kRS + 4 * lane) = a;
+                        } else if (n4 < p.N) {
+                            if (p.act_out && p.act_kind == 2) {  // (gate, up) pairs -> 2 outputs
+                                const __nv_bfloat162 o = __floats2bfloat162_rn(a.x / (1.f + __expf(-a.x)) * a.y,
+                                                                               a.z / (1.f + __expf(-a.z)) * a.w);
+                                *reinterpret_cast<__nv_bfloat162*>(p.act_out + (int64_t)row * (p.N / 2) + n4 / 2) = o;
+                            } else if (p.act_out) {
+                                const __nv_bfloat162 lo = __floats2bfloat162_rn(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
+                                const __nv_bfloat162 hi = __floats2bfloat162_rn(fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
+                                uint2 u;
+                                u.x = *reinterpret_cast<const uint32_t*>(&lo);
+                                u.y = *reinterpret_cast<const uint32_t*>(&hi);
+                                *reinterpret_cast<uint2*>(p.act_out + (int64_t)row * p.N + n4) = u;
+                            } else {
+                                *reinterpret_cast<float4*>(plane + (int64_t)row * p.N + n4) = a;
+                            }
+                        }
                     }
                 }
             } else {
@@ -569,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int row = rank + (j0 + r) * p.cs;
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
-                            v[r][q] = (q < p.cs && row < lim) ? peer[q][row * (kBM + 1) + t] : 0.f;
+                            v[r][q] = (q < p.cs && row < lim) ? peer[q][row * kRS + t] : 0.f;
                     }
 #pragma unroll
                     for (int r = 0; r < kR; ++r) {
@@ -598,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int j0 = 0; j0 < nmine; j0 += 64) {
                 const int j = j0 + (t >> 1);
                 const int nvr = j < nmine ? nv : 0;
-                const float* src = fin + min(j, max(nmine - 1, 0)) * (kBM + 1) + hf * 64;
+                const float* src = fin + min(j, max(nmine - 1, 0)) * kRS + hf * 64;
                 float m = -INFINITY;
                 int am = 0x7fffffff;
                 for (int q = 0; q < nvr; ++q)
@@ -744,17 +774,21 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
         static const int env_act_cs = std::getenv("EEB_ACT_CS") ? std::atoi(std::getenv("EEB_ACT_CS")) : -1;
         static const int env_head_cs = std::getenv("EEB_HEAD_CS") ? std::atoi(std::getenv("EEB_HEAD_CS")) : 1;
         const int env_fcs = a.head_tri ? env_head_cs : env_act_cs;
-        // cs: the best wave efficiency tiles*cs / (waves * wave), ties to the
-        // smaller cluster (e.g. C2 up-proj 64 tiles -> 4, C2 head 393 -> 2).
+        // cs: the best wave efficiency tiles*cs / (waves * wave).  Heads: ties
+        // to the smaller cluster.  Activations: cs in {1, 2, 4}, near-ties to
+        // the larger (the 4-CTA clusters have the vectorised DSMEM reduction;
+        // measured B=64: 80 tiles x K 2560 cs 8 / 2 / 4 = 25.5 / 19.6 / 18.4 us,
+        // 86 x 4096: 38.0 / 33.1 / 30.9, 344 x 8192: 167 / 149 / 125).
         cs = 1;
         double best = 0.0;
         for (int c = 1; c <= 8; ++c) {
             if (kblocks % c != 0 || (c > 1 && kblocks / c < 2)) continue;
             if (env_fcs >= 1 && c != env_fcs) continue;
+            if (a.act_out && env_fcs < 1 && c != 1 && c != 2 && c != 4) continue;
             const int units = tiles * c;
             const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
-            if (eff > best + 0.02) {
-                best = eff;
+            if (a.act_out ? eff >= best - 0.02 : eff > best + 0.02) {
+                best = std::max(best, eff);
                 cs = c;
             }
         }
@@ -787,7 +821,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // smem the epilogue reuses from the drained pipeline stages: the staged
     // [bpad][129] f32 partial (cs > 1) or logits tile (head), plus the head's
     // finished rows when the head is split
-    const size_t red_bytes = (size_t)bpad * (kBM + 1) * 4;
+    const size_t red_bytes = (size_t)bpad * kRS * 4;
     const size_t need = (cs > 1 || a.head_tri) ? red_bytes * (a.head_tri && cs > 1 ? 2 : 1) : 0;
     while (need > (size_t)stages * stage_bytes && stages < 8) ++stages;
     if (need > (size_t)stages * stage_bytes || 1024 + (size_t)stages * stage_bytes + 256 > (size_t)kSmemBudget) {
