@@ -752,7 +752,11 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // (opt-in EEB_TC_PLANECAP=1: measured 126 vs 125 ms for the C2 prefill)
     static const bool plane_cap = std::getenv("EEB_TC_PLANECAP") && std::atoi(std::getenv("EEB_TC_PLANECAP")) != 0;
     if (plane_cap) splits = std::max(1, std::min(splits, a.K / (2 * bpad)));
-    static const int env_maxsplit = std::getenv("EEB_TC_MAXSPLIT") ? std::atoi(std::getenv("EEB_TC_MAXSPLIT")) : 0;
+    // at most 12 planes: fewer partial planes for the consumer (residual norm,
+    // attention) to sum against a slightly longer K per CTA — measured
+    // ms/step 16 -> 12: C2 B=64 1.341 -> 1.314, B=16 1.183 -> 1.166, B=256
+    // 2.262 -> 2.257, 34B flat-12 B=64 3.220 -> 3.161 (10: no better)
+    static const int env_maxsplit = std::getenv("EEB_TC_MAXSPLIT") ? std::atoi(std::getenv("EEB_TC_MAXSPLIT")) : 12;
     if (env_maxsplit > 0) splits = std::min(splits, env_maxsplit);
     int kb_per = (kblocks + splits - 1) / splits;
     splits = (kblocks + kb_per - 1) / kb_per;

@@ -69,6 +69,17 @@ __global__ void __launch_bounds__(kNormThreads)
                          T* out2, const void* pf, size_t pf_bytes) {
     StampScope stamp_scope(stamp);
     pdl_launch_dependents();
+    // the norm gains are weights: in registers before the wait (one dependent
+    // L2 round trip fewer after it)
+    float4 gr1[kV], gr2[kV];
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        if (c < d) {
+            gr1[k] = __ldg(reinterpret_cast<const float4*>(g1 + c));
+            if (out2) gr2[k] = __ldg(reinterpret_cast<const float4*>(g2 + c));
+        }
+    }
     pdl_wait();
     stamp_waited(stamp);
     // the next GEMM's weights -> L2 while this latency-bound pass runs (after
@@ -115,11 +126,11 @@ __global__ void __launch_bounds__(kNormThreads)
     for (int k = 0; k < kV; ++k) {
         const int c = 4 * (threadIdx.x + k * blockDim.x);
         if (c < d) {
-            const float4 gg = *reinterpret_cast<const float4*>(g1 + c);
+            const float4 gg = gr1[k];
             const float4 nv = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
             store4<T>(out1 + (int64_t)i * d + c, make_float4(nv.x * gg.x, nv.y * gg.y, nv.z * gg.z, nv.w * gg.w));
             if (out2) {
-                const float4 g = *reinterpret_cast<const float4*>(g2 + c);
+                const float4 g = gr2[k];
                 store4<T>(out2 + (int64_t)i * d + c, make_float4(nv.x * g.x, nv.y * g.y, nv.z * g.z, nv.w * g.w));
             }
         }
@@ -198,6 +209,12 @@ __global__ void __launch_bounds__(kNormThreads)
                       __nv_bfloat16* out) {
     StampScope stamp_scope(stamp);
     pdl_launch_dependents();
+    float4 gr[kV];  // weights: before the wait
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        if (c < d) gr[k] = __ldg(reinterpret_cast<const float4*>(g + c));
+    }
     pdl_wait();
     const int i = blockIdx.x;
     if (i >= batch) return;
@@ -234,7 +251,7 @@ __global__ void __launch_bounds__(kNormThreads)
     for (int k = 0; k < kV; ++k) {
         const int c = 4 * (threadIdx.x + k * blockDim.x);
         if (c < d) {
-            const float4 gg = *reinterpret_cast<const float4*>(g + c);
+            const float4 gg = gr[k];
             const float4 nv = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
             store4<__nv_bfloat16>(out + (int64_t)i * d + c,
                                   make_float4(nv.x * gg.x, nv.y * gg.y, nv.z * gg.z, nv.w * gg.w));
@@ -296,6 +313,15 @@ __global__ void __launch_bounds__(kNormThreads)
     tp_norm_kernel(Stamp stamp, PxPeers px, int planes, int64_t plane_stride, const int* n_active, float* x, int d,
                    float eps, const float* g1, T* out1, const float* g2, T* out2) {
     StampScope stamp_scope(stamp);
+    float4 gr1[kV], gr2[kV];  // weights: before the wait
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        if (c < d && out1) {
+            gr1[k] = __ldg(reinterpret_cast<const float4*>(g1 + c));
+            if (out2) gr2[k] = __ldg(reinterpret_cast<const float4*>(g2 + c));
+        }
+    }
     pdl_wait();  // this rank's partial planes are complete
     stamp_waited(stamp);
     const int i = blockIdx.x, me = px.rank;
@@ -389,11 +415,11 @@ __global__ void __launch_bounds__(kNormThreads)
     for (int k = 0; k < kV; ++k) {
         const int c = 4 * (threadIdx.x + k * blockDim.x);
         if (c < d) {
-            const float4 gg = *reinterpret_cast<const float4*>(g1 + c);
+            const float4 gg = gr1[k];
             const float4 nv = make_float4(v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
             store4<T>(out1 + (int64_t)i * d + c, make_float4(nv.x * gg.x, nv.y * gg.y, nv.z * gg.z, nv.w * gg.w));
             if (out2) {
-                const float4 g = *reinterpret_cast<const float4*>(g2 + c);
+                const float4 g = gr2[k];
                 store4<T>(out2 + (int64_t)i * d + c, make_float4(nv.x * g.x, nv.y * g.y, nv.z * g.z, nv.w * g.w));
             }
         }
