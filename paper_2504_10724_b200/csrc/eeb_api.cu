@@ -1221,12 +1221,13 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
     }
     static const bool act_unfused = std::getenv("EEB_ACT_UNFUSED") != nullptr;  // A/B
     // The activation fused into the up GEMM (4-CTA clusters reducing K on chip)
-    // pays off at decode batches; above 128 rows the on-chip reduction of the
-    // wide accumulator tile dominates (C2 batch 256: 44 us fused vs 15 + 10 us
-    // planes + activation kernel), so larger batches take the split-K planes.
+    // at every decode batch: above 128 rows the GEMM runs two 128-row CTAs per
+    // weight tile (gemm_tc), so the on-chip reduction stays a 128-column tile
+    // (C2 batch 256: 2.148 -> 2.108 ms/step against split-K planes + the
+    // activation kernel; with one 256-column tile it was 44 us vs 15 + 10 us).
     static const int act_fused_max = std::getenv("EEB_ACT_FUSED_MAX_ROWS")
                                          ? std::atoi(std::getenv("EEB_ACT_FUSED_MAX_ROWS"))
-                                         : 128;
+                                         : 256;
     for (int sh = 0; sh < m.shards; ++sh) {
         void* act_dst = static_cast<char*>(c->mlp_h.p) + (size_t)sh * batch * m.f_l * wb;
         const void* wup = static_cast<const char*>(W.wup.p) + (size_t)sh * m.up_l * D * wb;

@@ -150,7 +150,8 @@ struct TcParams {
     int N, K;
     int kb_per;        // k-blocks per split
     int kblocks;       // total k-blocks
-    int bpad;          // UMMA N (batch rows, multiple of 16)
+    int bpad;          // UMMA N (batch rows per CTA, multiple of 16)
+    int rh;            // row blocks: CTA x = m_tile * rh + block; block b covers rows [b bpad, (b + 1) bpad)
     int stages;
     int tmem_cols;
     const int* n_active;
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m_tile = blockIdx.x, split = blockIdx.y;
+    const int m_tile = blockIdx.x / p.rh, split = blockIdx.y;
+    const int r_off = (blockIdx.x % p.rh) * p.bpad;  // this CTA's first batch row
     const int kb0 = split * p.kb_per;
     const int kb1 = min(kb0 + p.kb_per, p.kblocks);
     const int nkb = kb1 - kb0;
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // inits).  No weight prefetch when no row is live (all exited): read
         // before the PDL wait it may be stale, which costs only a useless or a
         // missed prefetch — the count after the wait decides what is computed.
-        const int hint = p.skip_dead ? *reinterpret_cast<const volatile int*>(p.n_active) : 1;
+        const int hint = p.skip_dead ? *reinterpret_cast<const volatile int*>(p.n_active) - r_off : 1;
         prefetch_tmap(&tmap_w);
         prefetch_tmap(&tmap_x);
         if (p.tma_out) prefetch_tmap(&tmap_o);
@@ -296,12 +298,12 @@ __global__ void __launch_bounds__(kThreads, 2)
             stamp_waited(p.st);
             EEB_STAMP(true, 2);  // predecessor complete
             for (int i = 0; i < pre; ++i)
-                tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, 0,
+                tma_load_2d(base + (uint32_t)i * stage_bytes + a_bytes, &tmap_x, full0 + 8 * i, (kb0 + i) * kBK, r_off,
                             pol_x);
             // every row exited before this layer: complete the stages already
             // in flight (their barriers expect the X bytes too) and stream no
             // more (read after the X loads are issued: off the critical path)
-            const int last = *p.n_active > 0 ? nkb : pre;
+            const int last = *p.n_active - r_off > 0 ? nkb : pre;
             if (last == pre)
                 for (int i = 0; i < pre; ++i) mbar_wait(full0 + 8 * i, 0);
             for (int i = pre; i < last; ++i) {
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mbar_expect_tx(full0 + 8 * s, stage_bytes);
                 const int kc = (kb0 + i) * kBK;
                 tma_load_2d(sa, &tmap_w, full0 + 8 * s, kc, m_tile * kBM, pol_w);
-                tma_load_2d(sa + a_bytes, &tmap_x, full0 + 8 * s, kc, 0, pol_x);
+                tma_load_2d(sa + a_bytes, &tmap_x, full0 + 8 * s, kc, r_off, pol_x);
             }
         }
         __syncwarp();  // reconverge before the CTA barrier (bar.sync is warp-aligned)
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // single-lane loop issues tcgen05.mma several times slower.
         const uint32_t idesc = instr_desc(kBM, p.bpad);
         pdl_wait();
-        const int live = *p.n_active;  // 0: every row exited, nothing to multiply
+        const int live = *p.n_active - r_off;  // <= 0: every row of this block exited, nothing to multiply
         for (int i = 0; i < (live > 0 ? nkb : 0); ++i) {
             const int s = i % S;
             const uint32_t ph = (uint32_t)(i / S) & 1u;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int quarter = warp & 3;
         const int n = m_tile * kBM + quarter * 32 + lane;
         pdl_wait();  // n_active and the plane workspace belong to the previous kernels
-        const int rows = *p.n_active;
+        const int rows = *p.n_active - r_off;  // this CTA's live rows (<= 0: none)
         if (rows > 0) {
         mbar_wait(tfull, 0);
         tc_fence_after();
@@ -402,14 +404,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const float u = __shfl_xor_sync(0xffffffffu, v[j], 1);  // odd lane: up, even: gate
                         if ((lane & 1) == 0 && n < p.N && c0 + j < lim) {
                             const float g = v[j];
-                            p.act_out[(int64_t)(c0 + j) * half_n + n / 2] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+                            p.act_out[(int64_t)(c0 + j + r_off) * half_n + n / 2] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
                         }
                     }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (n < p.N && c0 + j < lim)
-                            p.act_out[(int64_t)(c0 + j) * p.N + n] = __float2bfloat16_rn(fmaxf(v[j], 0.f));
+                            p.act_out[(int64_t)(c0 + j + r_off) * p.N + n] = __float2bfloat16_rn(fmaxf(v[j], 0.f));
                 }
             }
         } else if (p.cs == 1 && p.tma_out) {
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     asm volatile(
                         "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                             reinterpret_cast<uint64_t>(&tmap_o)),
-                        "r"(m_tile * kBM), "r"(r0), "r"(split), "r"(smem_u32(stg))
+                        "r"(m_tile * kBM), "r"(r0 + r_off), "r"(split), "r"(smem_u32(stg))
                         : "memory");
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (n < p.N && !(p.dbg & 1)) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (c0 + j < lim) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
+                        if (c0 + j < lim) plane[(int64_t)(c0 + j + r_off) * p.N + n] = v[j];
                 }
             }
             for (; c0 < lim; c0 += 16) {
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (n < p.N && !(p.dbg & 1)) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (c0 + j < lim) plane[(int64_t)(c0 + j) * p.N + n] = v[j];
+                        if (c0 + j < lim) plane[(int64_t)(c0 + j + r_off) * p.N + n] = v[j];
                 }
             }
         } else {
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     // every thread: the live-row count (uniform over a cluster) gates the on-chip reduction
     pdl_wait();
-    const int rows_all = *p.n_active;
+    const int rows_all = *p.n_active - r_off;  // (r_off is uniform over a cluster: clusters run along K)
     if (p.cs > 1 && rows_all > 0) {
         // Split-K reduction on chip: the cs CTAs of a cluster hold consecutive
         // k-ranges of one tile; CTA rank r sums rows r, r+cs, ... of the tile
@@ -531,12 +533,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (p.act_kind == 2) {
                         const float u = __shfl_xor_sync(0xffffffffu, acc, 1);  // odd lane: up, even: gate
                         if ((t & 1) == 0 && n < p.N)
-                            p.act_out[(int64_t)row * (p.N / 2) + n / 2] = __float2bfloat16_rn(acc / (1.f + __expf(-acc)) * u);
+                            p.act_out[(int64_t)(row + r_off) * (p.N / 2) + n / 2] = __float2bfloat16_rn(acc / (1.f + __expf(-acc)) * u);
                     } else if (n < p.N) {
-                        p.act_out[(int64_t)row * p.N + n] = __float2bfloat16_rn(fmaxf(acc, 0.f));
+                        p.act_out[(int64_t)(row + r_off) * p.N + n] = __float2bfloat16_rn(fmaxf(acc, 0.f));
                     }
                 } else if (n < p.N) {
-                    plane[(int64_t)row * p.N + n] = acc;
+                    plane[(int64_t)(row + r_off) * p.N + n] = acc;
                 }
             };
             // kR rows x cs peers of DSMEM loads in flight at once (a
@@ -576,16 +578,16 @@ __global__ void __launch_bounds__(kThreads, 2)
                             if (p.act_out && p.act_kind == 2) {  // (gate, up) pairs -> 2 outputs
                                 const __nv_bfloat162 o = __floats2bfloat162_rn(a.x / (1.f + __expf(-a.x)) * a.y,
                                                                                a.z / (1.f + __expf(-a.z)) * a.w);
-                                *reinterpret_cast<__nv_bfloat162*>(p.act_out + (int64_t)row * (p.N / 2) + n4 / 2) = o;
+                                *reinterpret_cast<__nv_bfloat162*>(p.act_out + (int64_t)(row + r_off) * (p.N / 2) + n4 / 2) = o;
                             } else if (p.act_out) {
                                 const __nv_bfloat162 lo = __floats2bfloat162_rn(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f));
                                 const __nv_bfloat162 hi = __floats2bfloat162_rn(fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
                                 uint2 u;
                                 u.x = *reinterpret_cast<const uint32_t*>(&lo);
                                 u.y = *reinterpret_cast<const uint32_t*>(&hi);
-                                *reinterpret_cast<uint2*>(p.act_out + (int64_t)row * p.N + n4) = u;
+                                *reinterpret_cast<uint2*>(p.act_out + (int64_t)(row + r_off) * p.N + n4) = u;
                             } else {
-                                *reinterpret_cast<float4*>(plane + (int64_t)row * p.N + n4) = a;
+                                *reinterpret_cast<float4*>(plane + (int64_t)(row + r_off) * p.N + n4) = a;
                             }
                         }
                     }
@@ -721,8 +723,16 @@ void make_kv_tensor_map(void* out_map, const void* base, int head_dim, int max_s
 int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     if (a.dtype != 1 || a.max_rows < tc_min_rows() || a.max_rows > 256 || a.K % kBK != 0) return 0;
     if (!gemm_tc_available()) return 0;
-    const int bpad = (a.max_rows + 15) / 16 * 16;
+    int bpad = (a.max_rows + 15) / 16 * 16;
     const int tiles = (a.N + kBM - 1) / kBM;
+    // more than 128 rows (large decode batches) on plain split-K GEMMs: two
+    // CTAs per weight tile, 128 rows each (adjacent CTAs: the second read of
+    // the tile hits L2), so each CTA keeps 3 pipeline stages and a 128-column
+    // accumulator and the split count halves (longer K per CTA)
+    static const bool env_rhalf = !std::getenv("EEB_TC_RHALF") || std::atoi(std::getenv("EEB_TC_RHALF")) != 0;
+    const int rh = env_rhalf && bpad > 128 && !a.head_tri ? (bpad + 127) / 128 : 1;
+    if (rh > 1) bpad = 128;
+    const int mt = tiles * rh;  // CTAs per split
     const int kblocks = a.K / kBK;
     // split K so the grid covers the SMs once, keeping >= 2 k-blocks per CTA
     static const int env_wave = std::getenv("EEB_TC_WAVE") ? std::atoi(std::getenv("EEB_TC_WAVE")) : 0;
@@ -730,15 +740,15 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
     // (at most 16 planes: the attention kernels sum up to 16 QKV planes in registers;
     //  only narrow GEMMs such as a 70B tensor-parallel QKV shard would want more)
-    int splits = std::max(1, std::min(std::min(kblocks / 2, wave / tiles), 16));
+    int splits = std::max(1, std::min(std::min(kblocks / 2, wave / mt), 16));
     static const int env_widesplit = std::getenv("EEB_TC_WIDESPLIT") ? std::atoi(std::getenv("EEB_TC_WIDESPLIT")) : 2;
-    if (tiles > wave / 2 && !a.head_tri && !a.act_out) {
+    if (mt > wave / 2 && !a.head_tri && !a.act_out) {
         // wide GEMMs (more tiles than half a wave, e.g. the 34B up projection:
         // 344 tiles): the split count with the best wave efficiency, planes
         // capped at the weight bytes (s * rows * 4 <= K * 2)
         double best = 0.0;
         for (int sp = 1; sp <= env_widesplit && sp <= kblocks / 2 && (size_t)sp * bpad * 4 <= (size_t)a.K * 2; ++sp) {
-            const int units = tiles * sp;
+            const int units = mt * sp;
             const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
             if (eff > best + 0.02) {
                 best = eff;
@@ -789,7 +799,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
             if (kblocks % c != 0 || (c > 1 && kblocks / c < 2)) continue;
             if (env_fcs >= 1 && c != env_fcs) continue;
             if (a.act_out && env_fcs < 1 && c != 1 && c != 2 && c != 4) continue;
-            const int units = tiles * c;
+            const int units = mt * c;
             const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
             if (a.act_out ? eff >= best - 0.02 : eff > best + 0.02) {
                 best = std::max(best, eff);
@@ -842,6 +852,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.kb_per = kb_per;
     p.kblocks = kblocks;
     p.bpad = bpad;
+    p.rh = rh;
     p.stages = stages;
     p.tmem_cols = tmem_cols;
     p.n_active = a.n_active;
@@ -902,7 +913,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     p.cs = cs;
     auto kern = cs == 4 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid(tiles, splits);
+    dim3 grid(mt, splits);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);
