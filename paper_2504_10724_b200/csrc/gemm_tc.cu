@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float M = fmaxf(m, m2);
                 const int A = (m2 > m || (m2 == m && a2 < am)) ? a2 : am;
                 const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
-                if (hf == 0 && r < lim) p.head_tri[(int64_t)r * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
+                if (hf == 0 && r < lim)
+                    p.head_tri[(int64_t)(r + r_off) * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
             }
         } else if (p.act_out && p.cs == 1) {
             // Fused MLP activation: the up projection's tile goes straight to the
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const float S = (m == -INFINITY ? 0.f : sum * __expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - M));
                 const int row = rank + j * p.cs;
                 if (hf == 0 && j < nmine)
-                    p.head_tri[(int64_t)row * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
+                    p.head_tri[(int64_t)(row + r_off) * p.tiles + m_tile] = make_float4(M, S, __int_as_float(A + p.vocab_off), 0.f);
             }
         }
     }
@@ -730,7 +731,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // the tile hits L2), so each CTA keeps 3 pipeline stages and a 128-column
     // accumulator and the split count halves (longer K per CTA)
     static const bool env_rhalf = !std::getenv("EEB_TC_RHALF") || std::atoi(std::getenv("EEB_TC_RHALF")) != 0;
-    const int rh = env_rhalf && bpad > 128 && !a.head_tri ? (bpad + 127) / 128 : 1;
+    const int rh = env_rhalf && bpad > 128 ? (bpad + 127) / 128 : 1;
     if (rh > 1) bpad = 128;
     const int mt = tiles * rh;  // CTAs per split
     const int kblocks = a.K / kBK;

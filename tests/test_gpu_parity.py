@@ -184,6 +184,33 @@ def test_bf16_token_agreement(ctx, desc, npos):
     assert conf_err < 0.05, conf_err
 
 
+def test_bf16_large_batch_two_row_blocks(ctx):
+    """200 rows: every GEMM (layer, fused up + activation, exit head) runs two
+    128-row CTAs per weight tile (the second block ragged, 72 rows) — against
+    the oracle for PROFILE (every head) and INTROSPECTIVE (compaction) steps."""
+    desc = MINI_MHA.replace(name="mini-mha-b200", max_slots=200, max_seq_len=64)
+    m, ref = _pair(ctx, desc)
+    rng = np.random.default_rng(23)
+    B = 200
+    slots = np.arange(B)
+    agree = total = 0
+    for pos in range(6):
+        toks = rng.integers(0, desc.vocab, B)
+        policy = eeb.PROFILE if pos % 2 == 0 else eeb.INTROSPECTIVE
+        g = ctx.decode_step(m, 0, policy, TH, slots, toks, np.full(B, pos))
+        r = ref.decode_step(0, policy, TH, slots, toks, np.full(B, pos))
+        if policy == eeb.PROFILE:
+            agree += int((g["head_token"] == r["head_token"]).sum())
+            total += g["head_token"].size
+            assert np.abs(g["head_confidence"] - r["head_confidence"]).max() < 0.05
+        else:
+            same = g["exit_layer"] == r["exit_layer"]
+            assert same.mean() >= 0.97, same.mean()
+            agree += int((g["token_id"][same] == r["token_id"][same]).sum())
+            total += int(same.sum())
+    assert agree / total >= BF16_AGREE, agree / total
+
+
 def test_graph_replay_matches_eager(ctx):
     desc = eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, name="tiny-bf16")
     m = ctx.register(desc)
