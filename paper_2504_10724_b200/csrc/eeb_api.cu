@@ -1770,7 +1770,7 @@ PxLayout px_layout(const Model& m) {
     auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
     int64_t off = 0;
     L.arrive = off; off += al((int64_t)kPxMaxRanks * kPxMaxCtas * 4);
-    L.pushed = off; off += al((int64_t)kPxMaxCtas * 4);
+    L.pushed = off; off += al((int64_t)kPxMaxRanks * kPxMaxCtas * 4);
     L.epoch = off; off += al((int64_t)kPxMaxCtas * 4);
     L.g_arrive = off; off += al((int64_t)kPxMaxRanks * kPxGatherCtas * 4);
     L.g_epoch = off; off += al((int64_t)kPxGatherCtas * 4);

@@ -55,12 +55,12 @@ constexpr int kPxMaxCtas = 1024;    // tp_norm: one CTA per row (prefill chunks 
 constexpr int kPxGatherCtas = 64;   // head-partial all-gather
 struct PxLayout {
     int64_t arrive = 0;   // u32 [kPxMaxRanks][kPxMaxCtas]: rank p's CTA i reached the exchange
-    int64_t pushed = 0;   // u32 [kPxMaxCtas]: the row owner's reduced row i has landed here
+    int64_t pushed = 0;   // u32 [kPxMaxRanks][kPxMaxCtas]: rank p's reduced slice of row i has landed here
     int64_t epoch = 0;    // u32 [kPxMaxCtas]: this rank's per-CTA epoch counters (local only)
     int64_t g_arrive = 0; // u32 [kPxMaxRanks][kPxGatherCtas]
     int64_t g_epoch = 0;  // u32 [kPxGatherCtas]
     int64_t planes = 0;   // f32 row-parallel GEMM partial planes (this rank's)
-    int64_t red = 0;      // f32 [rows][d]: reduced rows pushed by their owners
+    int64_t red = 0;      // f32 [rows][d]: reduced rows (each rank pushes its 1/N slice)
     int64_t head = 0;     // f32 this rank's exit-head tile partials (vocab shard)
     int64_t planes_elems = 0, rows = 0, head_elems = 0, bytes = 0;
 };
@@ -70,11 +70,11 @@ struct PxPeers {
     PxLayout lay;
 };
 // Two-shot all-reduce of the row-parallel partials fused with the residual add
-// and RMSNorm: CTA i's row is owned by rank i % nranks, which sums every rank's
-// `planes` planes of row i (rank-major, plane-minor: the order of the
-// all-shards context's split-K reduction) and pushes the sum to every rank;
-// every rank then applies x += sum, out1 = T(rmsnorm(x) g1), out2 likewise —
-// so all ranks hold bit-identical residual streams.
+// and RMSNorm: CTA i of rank r sums the r-th 1/N slice of row i over every
+// rank's `planes` planes (rank-major, plane-minor: the order of the all-shards
+// context's split-K reduction) and pushes it to every rank (reduce-scatter +
+// all-gather); every rank then applies x += sum, out1 = T(rmsnorm(x) g1),
+// out2 likewise — so all ranks hold bit-identical residual streams.
 void launch_tp_norm(int dtype, const PxPeers& px, int planes, int64_t plane_stride, const int* n_active, int max_rows,
                     float* x, int d, float eps, const float* g1, void* out1, const float* g2, void* out2,
                     cudaStream_t s);

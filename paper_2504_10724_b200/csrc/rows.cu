@@ -324,70 +324,66 @@ __global__ void __launch_bounds__(kNormThreads)
     }
     pdl_wait();  // this rank's partial planes are complete
     stamp_waited(stamp);
-    const int i = blockIdx.x, me = px.rank;
-    const int owner = i % px.nranks;
+    const int i = blockIdx.x, me = px.rank, N = px.nranks;
     __shared__ float red[32];
     __shared__ uint32_t epoch_s;
     uint32_t* epoch_cell = px_u32(px, me, px.lay.epoch) + i;
+    // 1. every rank's CTA i has arrived: its partial planes are complete
     if (threadIdx.x == 0) {
         const uint32_t e = *epoch_cell + 1;
         epoch_s = e;
-        if (owner != me) {
-            __threadfence_system();
-            st_release_sys(px_u32(px, owner, px.lay.arrive) + me * kPxMaxCtas + i, e);
-        } else {
-            for (int p = 0; p < px.nranks; ++p)
-                if (p != me) px_wait(px_u32(px, me, px.lay.arrive) + p * kPxMaxCtas + i, e);
-        }
+        __threadfence_system();
+        for (int p = 0; p < N; ++p)
+            if (p != me) st_release_sys(px_u32(px, p, px.lay.arrive) + me * kPxMaxCtas + i, e);
+        for (int p = 0; p < N; ++p)
+            if (p != me) px_wait(px_u32(px, me, px.lay.arrive) + p * kPxMaxCtas + i, e);
     }
     __syncthreads();
     const uint32_t e = epoch_s;
     const int n = *n_active;
     const bool live = i < n;
-    float4 y[kV];
-    if (owner == me) {
-        // reduce row i over every rank's planes, rank-major then plane order
+    // 2. reduce-scatter: this rank sums its 1/N slice of row i over every
+    // rank's planes (rank-major, then plane order) and stores the slice into
+    // every rank's reduced row (all-gather by push)
+    if (live) {
+        const int q = d / 4, g0 = me * q / N, g1e = (me + 1) * q / N;
+        for (int gi = g0 + (int)threadIdx.x; gi < g1e; gi += blockDim.x) {
+            const int c = 4 * gi;
+            float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int p = 0; p < N; ++p) {
+                const float* src = reinterpret_cast<const float*>(px.base[p] + px.lay.planes) + (int64_t)i * d + c;
+                for (int s0 = 0; s0 < planes; s0 += kBatch) {
+                    float4 t[kBatch];
 #pragma unroll
-        for (int k = 0; k < kV; ++k) {
-            const int c = 4 * (threadIdx.x + k * blockDim.x);
-            y[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (live && c < d) {
-                for (int p = 0; p < px.nranks; ++p) {
-                    const float* src = reinterpret_cast<const float*>(px.base[p] + px.lay.planes) + (int64_t)i * d + c;
-                    for (int s0 = 0; s0 < planes; s0 += kBatch) {
-                        float4 t[kBatch];
+                    for (int j = 0; j < kBatch; ++j)
+                        if (s0 + j < planes) t[j] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + j) * plane_stride));
 #pragma unroll
-                        for (int j = 0; j < kBatch; ++j)
-                            if (s0 + j < planes) t[j] = __ldcg(reinterpret_cast<const float4*>(src + (s0 + j) * plane_stride));
-#pragma unroll
-                        for (int j = 0; j < kBatch; ++j)
-                            if (s0 + j < planes) add4(y[k], t[j]);
-                    }
+                    for (int j = 0; j < kBatch; ++j)
+                        if (s0 + j < planes) add4(y, t[j]);
                 }
-                for (int p = 0; p < px.nranks; ++p)
-                    if (p != me)
-                        __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(px.base[p] + px.lay.red) +
-                                                         (int64_t)i * d + c),
-                               y[k]);
             }
+            for (int p = 0; p < N; ++p)
+                __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(px.base[p] + px.lay.red) + (int64_t)i * d + c), y);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence_system();
-            for (int p = 0; p < px.nranks; ++p)
-                if (p != me) st_release_sys(px_u32(px, p, px.lay.pushed) + i, e);
-        }
-    } else {
-        if (threadIdx.x == 0) px_wait(px_u32(px, me, px.lay.pushed) + i, e);
-        __syncthreads();
+    }
+    // 3. every rank's slice of row i has landed here
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < N; ++p)
+            if (p != me) st_release_sys(px_u32(px, p, px.lay.pushed) + me * kPxMaxCtas + i, e);
+        for (int p = 0; p < N; ++p)
+            if (p != me) px_wait(px_u32(px, me, px.lay.pushed) + p * kPxMaxCtas + i, e);
+    }
+    __syncthreads();
+    float4 y[kV];
 #pragma unroll
-        for (int k = 0; k < kV; ++k) {
-            const int c = 4 * (threadIdx.x + k * blockDim.x);
-            y[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (live && c < d)
-                y[k] = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(px.base[me] + px.lay.red) +
-                                                              (int64_t)i * d + c));
-        }
+    for (int k = 0; k < kV; ++k) {
+        const int c = 4 * (threadIdx.x + k * blockDim.x);
+        y[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live && c < d)
+            y[k] = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(px.base[me] + px.lay.red) +
+                                                          (int64_t)i * d + c));
     }
     if (threadIdx.x == 0) *epoch_cell = e;
     pdl_launch_dependents();
