@@ -191,10 +191,11 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 
-// kCs4: the instantiation for 4-CTA clusters (the up projection's on-chip
-// K reduction, 16 rows x 4 peers of DSMEM loads in flight); its extra
-// registers stay out of the plane GEMMs' instantiation (occupancy).
-template <bool kCs4>
+// kCsF: the instantiations for 2- and 4-CTA clusters (the on-chip K
+// reduction of the fused up projection with 16-byte DSMEM loads); their
+// extra registers stay out of the plane GEMMs' instantiation (kCsF = 0:
+// no cluster, or any other cluster size through the scalar path).
+template <int kCsF>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
                    const __grid_constant__ CUtensorMap tmap_o, TcParams p) {
@@ -547,32 +548,36 @@ __global__ void __launch_bounds__(kThreads, 2)
             // warp-uniform trip counts (the SwiGLU pairing shuffles).  The
             // 4-CTA clusters of the decode up projection: 16 rows x 4 peers,
             // a 64-row tile in one DSMEM round trip per rank.
-            if (kCs4) {
+            if (kCsF == 2 || kCsF == 4) {
                 // 16-byte DSMEM loads (DSMEM moves ~20 B/clk per SM; per-thread
                 // 4-byte loads took 2.7 us for the 64-row tile): lane = 4
                 // consecutive features, epilogue warp ew takes this rank's
-                // rows j = ew, ew + 4, ...; kJ rows x 4 peers in flight.
+                // rows j = ew, ew + 4, ...; kJ rows x kCsF peers in flight.
+                constexpr int C = kCsF == 4 ? 4 : 2;
                 const int ew = warp - 2, n4 = m_tile * kBM + 4 * lane;
                 constexpr int kJ = 4;
-                for (int j0 = ew; rank + j0 * 4 < lim; j0 += 4 * kJ) {
-                    float4 v[kJ][4];
+                for (int j0 = ew; rank + j0 * C < lim; j0 += 4 * kJ) {
+                    float4 v[kJ][C];
 #pragma unroll
                     for (int r = 0; r < kJ; ++r) {
-                        const int row = rank + (j0 + 4 * r) * 4;
+                        const int row = rank + (j0 + 4 * r) * C;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < C; ++q)
                             v[r][q] = row < lim ? *reinterpret_cast<const float4*>(peer[q] + row * kRS + 4 * lane)
                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
 #pragma unroll
                     for (int r = 0; r < kJ; ++r) {
-                        const int j = j0 + 4 * r, row = rank + j * 4;
+                        const int j = j0 + 4 * r, row = rank + j * C;
                         if (row >= lim) break;
-                        float4 a;  // rank (= k) order, as the scalar path
-                        a.x = ((v[r][0].x + v[r][1].x) + v[r][2].x) + v[r][3].x;
-                        a.y = ((v[r][0].y + v[r][1].y) + v[r][2].y) + v[r][3].y;
-                        a.z = ((v[r][0].z + v[r][1].z) + v[r][2].z) + v[r][3].z;
-                        a.w = ((v[r][0].w + v[r][1].w) + v[r][2].w) + v[r][3].w;
+                        float4 a = v[r][0];  // rank (= k) order, as the scalar path
+#pragma unroll
+                        for (int q = 1; q < C; ++q) {
+                            a.x += v[r][q].x;
+                            a.y += v[r][q].y;
+                            a.z += v[r][q].z;
+                            a.w += v[r][q].w;
+                        }
                         if (p.head_tri) {
                             *reinterpret_cast<float4*>(fin + j * kRS + 4 * lane) = a;
                         } else if (n4 < p.N) {
@@ -789,11 +794,11 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
         static const int env_act_cs = std::getenv("EEB_ACT_CS") ? std::atoi(std::getenv("EEB_ACT_CS")) : -1;
         static const int env_head_cs = std::getenv("EEB_HEAD_CS") ? std::atoi(std::getenv("EEB_HEAD_CS")) : 1;
         const int env_fcs = a.head_tri ? env_head_cs : env_act_cs;
-        // cs: the best wave efficiency tiles*cs / (waves * wave).  Heads: ties
-        // to the smaller cluster.  Activations: cs in {1, 2, 4}, near-ties to
-        // the larger (the 4-CTA clusters have the vectorised DSMEM reduction;
-        // measured B=64: 80 tiles x K 2560 cs 8 / 2 / 4 = 25.5 / 19.6 / 18.4 us,
-        // 86 x 4096: 38.0 / 33.1 / 30.9, 344 x 8192: 167 / 149 / 125).
+        // cs: the best wave efficiency tiles*cs / (waves * wave), near-ties to
+        // the smaller cluster (fewer CTAs, longer K each).  Activations: cs in
+        // {1, 2, 4} (the 2- and 4-CTA clusters have the vectorised DSMEM
+        // reduction; with the scalar one, B=64: 80 tiles x K 2560 cs 8 / 2 / 4
+        // = 25.5 / 19.6 / 18.4 us).
         cs = 1;
         double best = 0.0;
         for (int c = 1; c <= 8; ++c) {
@@ -802,8 +807,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
             if (a.act_out && env_fcs < 1 && c != 1 && c != 2 && c != 4) continue;
             const int units = mt * c;
             const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
-            if (a.act_out ? eff >= best - 0.02 : eff > best + 0.02) {
-                best = std::max(best, eff);
+            if (eff > best + 0.02) {
+                best = eff;
                 cs = c;
             }
         }
@@ -912,7 +917,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     }
     const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 1) * 8 + 16;
     p.cs = cs;
-    auto kern = cs == 4 ? gemm_tc_kernel<true> : gemm_tc_kernel<false>;
+    auto kern = cs == 4 ? gemm_tc_kernel<4> : cs == 2 ? gemm_tc_kernel<2> : gemm_tc_kernel<0>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 grid(mt, splits);
     cudaLaunchConfig_t cfg = {};
