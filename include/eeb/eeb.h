@@ -151,6 +151,14 @@ eeb_status eeb_host_stage_base(eeb_ctx* ctx, int model, const void* host, int64_
  * the host tier and made resident (from <= loaded_depth + 1); returns when done. */
 eeb_status eeb_load_layers_from(eeb_ctx* ctx, int model, int from, int to, const void* host, int64_t bytes);
 
+/* Reserve device memory for a later load of layers up to `depth` (and the
+ * base weights): the buffers are allocated and parked in the context's weight
+ * block pool, so loads and reloads while serving (model switches, depth
+ * changes) reuse them instead of calling cudaMalloc / cudaFree (host time,
+ * device synchronisation).  Pooled blocks go back to the driver when any
+ * allocation of the library fails. */
+eeb_status eeb_weight_reserve(eeb_ctx* ctx, int model, int depth);
+
 /* Host tier ↔ the model held in CPU memory that HELIOS's greedy loader pulls
  * layers from (engine.hpp:197-216; memory_model.hpp:76-105): layers [1, depth]
  * plus the base weights (embedding, exit heads) packed into pinned host

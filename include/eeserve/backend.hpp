@@ -131,7 +131,11 @@ public:
                                                   kv_pages_ > 0 ? kv_pages_
                                                                 : max_slots * ((max_seq_len + kv_page_ - 1) / kv_page_)),
                            "eeb_kv_configure_pages");
-        if (host_tier_) throw_if_error(eeb_host_stage(ctx_, h, spec.num_layers), "eeb_host_stage");
+        if (host_tier_) {
+            throw_if_error(eeb_host_stage(ctx_, h, spec.num_layers), "eeb_host_stage");
+            // device blocks for every depth the engine may load, allocated now (setup)
+            throw_if_error(eeb_weight_reserve(ctx_, h, spec.num_layers), "eeb_weight_reserve");
+        }
     }
 
     void release(const std::string& model, int slot) override {

@@ -395,7 +395,7 @@ private:
                 dur = deepest * spec.t_decode_per_layer_s;
             }
             clock_ += dur;  // every row of the step is emitted at the step's end (one t_s)
-            for (int i = 0; i < rows.size(); ++i)
+            for (int i = 0; cfg_.record_events && i < rows.size(); ++i)  // (no JSON built unless recorded)
                 emit("token_emitted", JsonFields()
                                           .i64("request_id", rows.request_ids[i])
                                           .str("model", model)
@@ -517,7 +517,7 @@ private:
                 dur = deepest * spec.t_decode_per_layer_s;
             }
             clock_ += dur;
-            for (int i = 0; i < rows.size(); ++i)
+            for (int i = 0; cfg_.record_events && i < rows.size(); ++i)  // (no JSON built unless recorded)
                 emit("token_emitted", JsonFields()
                                           .i64("request_id", rows.request_ids[i])
                                           .str("model", model)

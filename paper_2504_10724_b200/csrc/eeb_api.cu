@@ -33,15 +33,76 @@ namespace {
 
 thread_local std::string g_last_error;
 
+// Device block cache for model weights.  The greedy loader evicts and reloads
+// layers as the served model and depth change; cudaMalloc / cudaFree of those
+// GBs cost ~1 s of host time per C3 serving run (and every cudaFree
+// synchronises the device).  Evicted weight buffers are kept here and handed
+// to the next allocation of the same size; an allocation that fails anywhere
+// in the library first returns every pool's blocks to the driver.
+struct BlockPool;
+std::mutex g_pools_mu;
+std::vector<BlockPool*> g_pools;
+struct BlockPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> blocks;
+    BlockPool() {
+        std::lock_guard<std::mutex> g(g_pools_mu);
+        g_pools.push_back(this);
+    }
+    ~BlockPool() {
+        {
+            std::lock_guard<std::mutex> g(g_pools_mu);
+            g_pools.erase(std::find(g_pools.begin(), g_pools.end(), this));
+        }
+        trim();
+    }
+    BlockPool(const BlockPool&) = delete;
+    BlockPool& operator=(const BlockPool&) = delete;
+    void trim() {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& kv : blocks) cudaFree(kv.second);
+        blocks.clear();
+    }
+    void* take(size_t n) {
+        std::lock_guard<std::mutex> g(mu);
+        const auto it = blocks.find(n);
+        if (it == blocks.end()) return nullptr;
+        void* q = it->second;
+        blocks.erase(it);
+        return q;
+    }
+    void put(void* q, size_t n) {
+        std::lock_guard<std::mutex> g(mu);
+        blocks.emplace(n, q);
+    }
+};
+void dev_malloc(void** q, size_t n) {
+    cudaError_t e = cudaMalloc(q, n);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        {
+            std::lock_guard<std::mutex> g(g_pools_mu);
+            for (BlockPool* bp : g_pools) bp->trim();
+        }
+        e = cudaMalloc(q, n);
+    }
+    EEB_CUDA(e);
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    BlockPool* pool = nullptr;  // weights: blocks recycled through the context's pool
     DevBuf() = default;
+    explicit DevBuf(BlockPool* bp) : pool(bp) {}
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (pool) pool->put(p, bytes);
+            else cudaFree(p);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -49,7 +110,8 @@ struct DevBuf {
     bool ensure(size_t n) {
         if (n <= bytes) return false;
         release();
-        EEB_CUDA(cudaMalloc(&p, n));
+        p = pool ? pool->take(n) : nullptr;
+        if (!p) dev_malloc(&p, n);
         bytes = n;
         // debugging aid: fill fresh allocations with NaN-ish bytes so reads of
         // never-written memory show up deterministically
@@ -63,6 +125,9 @@ struct DevBuf {
 struct LayerWeights {
     DevBuf attn_norm, mlp_norm, wqkv, wo, wup, wdown;
     DevBuf* parts[6] = {&attn_norm, &mlp_norm, &wqkv, &wo, &wup, &wdown};
+    explicit LayerWeights(BlockPool* bp) {
+        for (DevBuf* b : parts) b->pool = bp;
+    }
 };
 
 // Pinned host memory (the host tier the greedy loader copies from).
@@ -117,6 +182,7 @@ struct Model {
     int hq_l = 0, hkv_l = 0, dq_l = 0, dkv_l = 0, f_l = 0, up_l = 0, v_l = 0;  // per-shard dims
     int shard_rank(int s) const { return rank >= 0 ? rank : s; }
     size_t kv_shard_elems = 0;  // one (layer, shard) block of the KV cache
+    BlockPool* pool = nullptr;  // the context's weight block cache (set at registration)
     // base weights
     DevBuf emb;
     std::vector<std::unique_ptr<DevBuf>> head, head_norm;
@@ -175,6 +241,7 @@ const char* kCatNames[kNumCat] = {"layer_gemm", "attention", "exit_head", "norm"
 }  // namespace eeb
 
 struct eeb_ctx {
+    eeb::BlockPool wpool;  // first member: outlives every model's weight buffers
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
@@ -367,12 +434,12 @@ void synth_base(Model& m, cudaStream_t s) {
     m.head.clear();
     m.head_norm.clear();
     for (int e = 0; e < d.n_exits; ++e) {
-        auto h = std::make_unique<DevBuf>();
+        auto h = std::make_unique<DevBuf>(m.pool);
         h->ensure((size_t)m.shards * m.v_l * D * m.wbytes);  // vocab shards, shard-major
         for (int sh = 0; sh < m.shards; ++sh)
             synth_head(d.dtype, static_cast<char*>(h->p) + (size_t)sh * m.v_l * D * m.wbytes, d.seed, e, m.alphas[e],
                        d.vocab, D, s, m.shard_rank(sh) * m.v_l, m.v_l);
-        auto g = std::make_unique<DevBuf>();
+        auto g = std::make_unique<DevBuf>(m.pool);
         g->ensure((size_t)D * sizeof(float));
         synth_norm(g->p, d.seed, synth::base_tid(synth::kHeadNorm, e), D, s);
         m.head.push_back(std::move(h));
@@ -383,7 +450,7 @@ void synth_base(Model& m, cudaStream_t s) {
 // Device buffers of layer l, sized but not filled.
 std::unique_ptr<LayerWeights> alloc_layer(const Model& m) {
     const int D = m.desc.d_model, F = m.desc.d_ffn;
-    auto L = std::make_unique<LayerWeights>();
+    auto L = std::make_unique<LayerWeights>(m.pool);
     L->attn_norm.ensure((size_t)D * 4);
     L->mlp_norm.ensure((size_t)D * 4);
     const size_t S = (size_t)m.shards;
@@ -453,6 +520,9 @@ void load_to(eeb_ctx* c, Model& m, int to) {
                                       std::to_string(d.num_layers) + "]");
     settle_pending(m);
     cudaStream_t s = c->stream;
+    // evicted weight blocks go back to the pool (reusable at once): nothing
+    // queued on the decode stream may still read them
+    EEB_CUDA(cudaStreamSynchronize(s));
     if (to == 0) {
         m.layers.clear();
         m.head.clear();
@@ -556,11 +626,11 @@ void base_from_host(Model& m, cudaStream_t s) {
     m.head.clear();
     m.head_norm.clear();
     for (int e = 0; e < d.n_exits; ++e) {
-        auto h = std::make_unique<DevBuf>();
+        auto h = std::make_unique<DevBuf>(m.pool);
         h->ensure(b.sz[1 + e]);
         EEB_CUDA(cudaMemcpyAsync(h->p, static_cast<const char*>(b.buf.p) + b.off[1 + e], b.sz[1 + e],
                                  cudaMemcpyHostToDevice, s));
-        auto g = std::make_unique<DevBuf>();
+        auto g = std::make_unique<DevBuf>(m.pool);
         g->ensure(b.sz[1 + d.n_exits + e]);
         EEB_CUDA(cudaMemcpyAsync(g->p, static_cast<const char*>(b.buf.p) + b.off[1 + d.n_exits + e],
                                  b.sz[1 + d.n_exits + e], cudaMemcpyHostToDevice, s));
@@ -632,9 +702,9 @@ void load_async(eeb_ctx* c, Model& m, int to) {
         m.head.clear();
         m.head_norm.clear();
         for (int e = 0; e < d.n_exits; ++e) {
-            m.head.push_back(std::make_unique<DevBuf>());
+            m.head.push_back(std::make_unique<DevBuf>(m.pool));
             m.head.back()->ensure(b.sz[1 + e]);
-            m.head_norm.push_back(std::make_unique<DevBuf>());
+            m.head_norm.push_back(std::make_unique<DevBuf>(m.pool));
             m.head_norm.back()->ensure(b.sz[1 + d.n_exits + e]);
         }
     }
@@ -1897,6 +1967,8 @@ eeb_status eeb_model_register(eeb_ctx* c, const eeb_model_desc* desc, int* model
         m->v_l = d.vocab / m->tp;
         if (m->head_dim % 16 != 0 || m->head_dim > 128) throw Error(EEB_E_VALIDATION, "head_dim must be a multiple of 16, <= 128");
         alloc_kv(c, *m, d.max_seq_len, d.max_slots, false);
+        m->pool = &c->wpool;
+        m->emb.pool = &c->wpool;
         m->kv_depth.ensure((size_t)d.max_slots * d.max_seq_len);
         EEB_CUDA(cudaMemsetAsync(m->kv_depth.p, 0, m->kv_depth.bytes, c->stream));
         EEB_CUDA(cudaStreamSynchronize(c->stream));
@@ -1929,6 +2001,31 @@ eeb_status eeb_load_layers(eeb_ctx* c, int model, int to_depth) {
 }
 
 eeb_status eeb_evict(eeb_ctx* c, int model) { return eeb_load_layers(c, model, 0); }
+
+eeb_status eeb_weight_reserve(eeb_ctx* c, int model, int depth) {
+    return guarded([&] {
+        Model& m = model_of(c, model);
+        const eeb_model_desc& d = m.desc;
+        if (depth < 0 || depth > d.num_layers) throw Error(EEB_E_DOMAIN, "depth outside [0, num_layers]");
+        EEB_CUDA(cudaSetDevice(c->device));
+        // allocate what a load to `depth` would (beyond what is resident) and
+        // hand it straight to the context's block pool
+        std::vector<std::unique_ptr<LayerWeights>> tmp;
+        for (int l = (int)m.layers.size() + 1; l <= depth; ++l) tmp.push_back(alloc_layer(m));
+        if (m.loaded == 0 && depth > 0) {
+            const int D = d.d_model;
+            DevBuf e(m.pool);
+            e.ensure((size_t)d.vocab * D * m.wbytes);
+            std::vector<std::unique_ptr<DevBuf>> hs;
+            for (int x = 0; x < d.n_exits; ++x) {
+                hs.push_back(std::make_unique<DevBuf>(m.pool));
+                hs.back()->ensure((size_t)m.v_l * D * m.wbytes * m.shards);
+                hs.push_back(std::make_unique<DevBuf>(m.pool));
+                hs.back()->ensure((size_t)D * 4);
+            }
+        }
+    });
+}
 
 eeb_status eeb_host_stage(eeb_ctx* c, int model, int depth) {
     return guarded([&] {
@@ -2062,12 +2159,13 @@ eeb_status eeb_reset_slots(eeb_ctx* c, int model, int32_t n, const int32_t* slot
 
 static void validate_rows_host(const Model& m, int batch, const int32_t* slot, const int32_t* tok,
                                const int32_t* pos) {
+    thread_local std::vector<uint8_t> seen;
+    seen.assign((size_t)m.desc.max_slots, 0);
     for (int i = 0; i < batch; ++i) {
         if (slot[i] < 0 || slot[i] >= m.desc.max_slots) throw Error(EEB_E_DOMAIN, "slot id out of range");
         if (tok[i] < 0 || tok[i] >= m.desc.vocab) throw Error(EEB_E_DOMAIN, "token id out of range");
         if (pos[i] < 0 || pos[i] >= m.desc.max_seq_len) throw Error(EEB_E_DOMAIN, "position out of range");
-        for (int j = 0; j < i; ++j)
-            if (slot[j] == slot[i]) throw Error(EEB_E_VALIDATION, "duplicate slot id in one step");
+        if (seen[slot[i]]++) throw Error(EEB_E_VALIDATION, "duplicate slot id in one step");
     }
 }
 

@@ -70,7 +70,7 @@ EXPORTED = [
     "eeb_kv_configure_pages", "eeb_kv_reserve", "eeb_kv_release", "eeb_kv_pages",
     "eeb_debug_stamps", "eeb_debug_stamps_read", "eeb_debug_read_kv_span",
     "eeb_weight_layout", "eeb_host_stage_layer", "eeb_host_stage_base", "eeb_load_layers_from",
-    "eeb_tp_px_alloc", "eeb_tp_px_attach",
+    "eeb_tp_px_alloc", "eeb_tp_px_attach", "eeb_weight_reserve",
     "eeb_debug_stamps_cta",
 ]
 

@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <stdexcept>
 #include <string>
 
 #include "eeserve/engine.hpp"
@@ -51,6 +52,50 @@ static ModelSpec opt_shape(const std::string& id, int layers, std::vector<int> e
     validate_model_spec(s);
     return s;
 }
+
+// Wall time spent in each backend call, so the serving wall splits into GPU
+// calls and the engine's own host work.
+class TimedBackend final : public DecodeBackend {
+public:
+    explicit TimedBackend(DecodeBackend& inner) : in_(inner) {}
+    double step_s = 0.0, prefill_s = 0.0, load_s = 0.0, other_s = 0.0;
+    void register_model(const ModelSpec& spec, int max_slots, int max_seq_len) override {
+        const auto t = now();
+        in_.register_model(spec, max_slots, max_seq_len);
+        other_s += since(t);
+    }
+    LoadResult load(const std::string& model, int depth) override {
+        const auto t = now();
+        const LoadResult r = in_.load(model, depth);
+        load_s += since(t);
+        return r;
+    }
+    double prefill(const std::string& model, int depth, const PrefillRows& rows) override {
+        const auto t = now();
+        const double r = in_.prefill(model, depth, rows);
+        prefill_s += since(t);
+        return r;
+    }
+    StepOutcome step(const std::string& model, int depth, TokenPolicy policy, double th,
+                     const StepRows& rows) override {
+        const auto t = now();
+        StepOutcome r = in_.step(model, depth, policy, th, rows);
+        step_s += since(t);
+        return r;
+    }
+    void release(const std::string& model, int slot) override {
+        const auto t = now();
+        in_.release(model, slot);
+        other_s += since(t);
+    }
+
+private:
+    static std::chrono::steady_clock::time_point now() { return std::chrono::steady_clock::now(); }
+    static double since(std::chrono::steady_clock::time_point t) {
+        return std::chrono::duration<double>(now() - t).count();
+    }
+    DecodeBackend& in_;
+};
 
 int main(int argc, char** argv) {
     const int n_req = argc > 1 ? std::atoi(argv[1]) : 1024;
@@ -85,29 +130,42 @@ int main(int argc, char** argv) {
         const std::uint64_t seed_a = repo.models["opt-1.3b"].arch.seed, seed_b = repo.models["opt-2.7b"].arch.seed;
         const std::vector<double> cum = {0.73, 0.777, 1.0};  // default coverage 73.0 / 4.7 / 22.3 %
         const double murky[3] = {0.3, 0.1, 0.6}, easy[3] = {0.92, 0.05, 0.03};
-        cfg.token_fn = [=](std::int64_t rid, int pos, int vocab) -> int32_t {
+        // the vocabulary bucketed once by exit band (both models' z in the
+        // band), so drawing a token is O(1) — rejection sampling for the
+        // narrow middle band took ~100 us a token, host time that landed in
+        // the serving wall
+        const int vocab_all = repo.models["opt-1.3b"].arch.vocab;
+        std::vector<std::vector<int32_t>> bands(3);
+        for (int32_t t = 0; t < vocab_all; ++t) {
+            const double za = eeb::synth::z_of(seed_a, t), zb = eeb::synth::z_of(seed_b, t);
+            for (int e = 0; e < 3; ++e) {
+                const double lo = (e == 0 ? 0.0 : cum[e - 1]) + 0.005, hi = cum[e] - 0.005;
+                if (za >= lo && za < hi && zb >= lo && zb < hi) bands[e].push_back(t);
+            }
+        }
+        for (const auto& b : bands)
+            if (b.empty()) throw std::runtime_error("drift workload: an exit band holds no token of the vocabulary");
+        cfg.token_fn = [=](std::int64_t rid, int pos, int /*vocab*/) -> int32_t {
             // easy, murky, easy, murky: the first evaluation sees an easy mix
             // (greedy depth at the first exit), the murky segments then breach
             const double* law = (rid / seg_len) % 2 == 0 ? easy : murky;
             const double u = (double)synthetic_token(0x5eedULL, rid, pos, 1 << 24) / (double)(1 << 24);
             const int e = u < law[0] ? 0 : (u < law[0] + law[1] ? 1 : 2);
-            const double lo = (e == 0 ? 0.0 : cum[e - 1]) + 0.005, hi = cum[e] - 0.005;
-            for (std::uint64_t k = 1;; ++k) {
-                const int32_t t = synthetic_token(0x70c0ULL + k * 0x9e3779b97f4a7c15ULL, rid, pos, vocab);
-                const double za = eeb::synth::z_of(seed_a, t), zb = eeb::synth::z_of(seed_b, t);
-                if (za >= lo && za < hi && zb >= lo && zb < hi) return t;
-            }
+            const auto& b = bands[e];
+            return b[(size_t)synthetic_token(0x70c0ULL, rid, pos, (int)b.size())];
         };
     }
 
     const auto t0 = std::chrono::steady_clock::now();
-    CudaBackend be(0, /*host_tier=*/true);
-    be.set_kv_pages(64);  // pages for every slot BatchedEngine::slots_for sizes (max_batch_size)
+    CudaBackend cuda_be(0, /*host_tier=*/true);
+    cuda_be.set_kv_pages(64);  // pages for every slot BatchedEngine::slots_for sizes (max_batch_size)
+    TimedBackend be(cuda_be);
     std::vector<RequestSpec> reqs;
     for (int i = 0; i < n_req; ++i) reqs.push_back({i, prompt, tokens});
     BatchedEngine eng(repo, be, cfg);
     eng.prepare();  // device pools sized from the memory model; both models staged in the pinned host tier
     const auto t1 = std::chrono::steady_clock::now();
+    be.step_s = be.prefill_s = be.load_s = be.other_s = 0.0;  // (setup's calls are in setup_s)
     const EngineReport rep = eng.run(reqs);
     const auto t2 = std::chrono::steady_clock::now();
     const double setup_s = std::chrono::duration<double>(t1 - t0).count();
@@ -136,12 +194,14 @@ int main(int argc, char** argv) {
         "\"decode_tokens_per_s\": %.1f, \"serving_tokens_per_s\": %.1f, \"wall_s\": %.3f, \"setup_s\": %.3f, "
         "\"mean_ttft_ms\": %.3f, \"mean_tpot_ms\": %.4f, \"achieved_batch\": %d, \"eval_cycles\": %lld, "
         "\"ld\": %lld, \"sw\": %lld, \"load_bytes\": %lld, \"load_s\": %.4f, \"load_gbs\": %.2f, \"prefill_s\": %.3f, "
-        "\"perplexity\": %.6f, \"exit_table_pct\": %s, \"serving_history\": %s}\n",
+        "\"perplexity\": %.6f, \"wall_split_s\": {\"step_calls\": %.3f, \"prefill_calls\": %.3f, \"load_calls\": %.3f, "
+        "\"other_calls\": %.3f, \"engine_host\": %.3f}, \"exit_table_pct\": %s, \"serving_history\": %s}\n",
         drift ? "drift: easy/murky/easy/murky segments of 256 requests (gen_drift.json exit laws), tokens drawn by synthetic difficulty" : "calibration: uniform tokens",
         eng.slots("opt-1.3b"), eng.slots("opt-2.7b"), n_req, prompt, tokens, (long long)rep.tokens, (long long)rep.steps, rep.throughput_tok_s,
         rep.tokens / run_s, run_s, setup_s, rep.mean_ttft_s * 1e3, rep.mean_tpot_s * 1e3, rep.achieved_batch_size,
         (long long)rep.eval_cycles, (long long)rep.ld_count, (long long)rep.sw_count, (long long)rep.load_bytes,
         rep.load_s, rep.load_bytes / std::max(1e-9, rep.load_s) / 1e9, rep.prefill_s, rep.perplexity,
+        be.step_s, be.prefill_s, be.load_s, be.other_s, run_s - be.step_s - be.prefill_s - be.load_s - be.other_s,
         exits.c_str(), hist.c_str());
     return 0;
 }
