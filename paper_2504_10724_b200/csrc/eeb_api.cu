@@ -2303,8 +2303,9 @@ eeb_status eeb_prefill(eeb_ctx* c, int model, int depth, int32_t n_seq, const in
         // re-streams of the weights), else 256 (tcgen05 N <= 256); f32: the
         // CUDA-core tier serves <= 64 rows per pass
         const bool lt = d.dtype == EEB_BF16 && c->gemm_tier != 1 && prefill_lt_ready(c);
-        const int chunk = d.dtype == EEB_BF16 ? (env_chunk >= 16 && env_chunk <= (lt ? 1024 : 256) ? env_chunk
-                                                                                                   : (lt ? 1024 : 256))
+        const int lt_max = m.tp > 1 ? 1024 : 4096;  // (TP exchange: one CTA per row, <= 1024)
+        const int chunk = d.dtype == EEB_BF16 ? (env_chunk >= 16 && env_chunk <= (lt ? lt_max : 256) ? env_chunk
+                                                                                                     : (lt ? 1024 : 256))
                                               : 128;
         ensure_workspace(c, m, (int)std::min<int64_t>(chunk, total));
         // (tok, slot, pos) of every prompt token: one pinned staging + one H2D,
