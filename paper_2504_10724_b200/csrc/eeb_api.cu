@@ -260,7 +260,7 @@ struct eeb_ctx {
         cublasLtMatmulAlgo_t algo{};
         bool ok = false;
     };
-    std::map<std::tuple<int, int, int>, LtPlan> lt_plans;
+    std::map<std::tuple<int, int, int, int>, LtPlan> lt_plans;  // (N, K, rows, relu-bf16 epilogue)
     size_t cond_open = 0;                 // conditional bodies open in the capture
     std::vector<std::unique_ptr<eeb::Model>> models;
     int graphs_enabled = 1;
@@ -1023,12 +1023,14 @@ bool prefill_lt_ready(eeb_ctx* c) {
 // one plane.  Column-major view: D (N x rows, ld N) = op(A) B with A = W (K x
 // N, ld K, transposed) and B = X (K x rows, ld K).  EEB_PREFILL_LT=0 keeps
 // the tcgen05 decode GEMM (split-K planes) for prefill too.
-bool gemm_lt(eeb_ctx* c, const void* W, const void* X, int N, int K, int rows, float* out) {
+// relu_bf16: out is bf16 [rows][N] = bf16(relu(X W^T)) (the OPT MLP's up
+// projection with its activation in the cuBLASLt epilogue); else f32 plane.
+bool gemm_lt(eeb_ctx* c, const void* W, const void* X, int N, int K, int rows, void* out, bool relu_bf16 = false) {
     static const bool on = !std::getenv("EEB_PREFILL_LT") || std::atoi(std::getenv("EEB_PREFILL_LT")) != 0;
     if (!on) return false;
     constexpr size_t kWs = 32u << 20;
     if (!c->lt || c->lt_ws.bytes < kWs) return false;  // (created by ensure_workspace, outside any capture)
-    auto& pl = c->lt_plans[{N, K, rows}];
+    auto& pl = c->lt_plans[{N, K, rows, relu_bf16 ? 1 : 0}];
     if (!pl.op) {
         const cublasComputeType_t ct = CUBLAS_COMPUTE_32F;
         const cudaDataType_t st = CUDA_R_32F;
@@ -1036,9 +1038,13 @@ bool gemm_lt(eeb_ctx* c, const void* W, const void* X, int N, int K, int rows, f
         const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
         cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof ta);
         cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof tb);
+        if (relu_bf16) {
+            const cublasLtEpilogue_t ep = CUBLASLT_EPILOGUE_RELU;
+            cublasLtMatmulDescSetAttribute(pl.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &ep, sizeof ep);
+        }
         cublasLtMatrixLayoutCreate(&pl.a, CUDA_R_16BF, K, N, K);
         cublasLtMatrixLayoutCreate(&pl.b, CUDA_R_16BF, K, rows, K);
-        cublasLtMatrixLayoutCreate(&pl.d, CUDA_R_32F, N, rows, N);
+        cublasLtMatrixLayoutCreate(&pl.d, relu_bf16 ? CUDA_R_16BF : CUDA_R_32F, N, rows, N);
         cublasLtMatmulPreference_t pref;
         cublasLtMatmulPreferenceCreate(&pref);
         const size_t ws = kWs;
@@ -1323,6 +1329,16 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
                 ga.pf_bytes = (size_t)D * m.f_l * wb;
             }
             if (gemm_tc(ga, s) > 0) {
+                count(c, kCatGemm, 1);
+                continue;
+            }
+        }
+        if (c->in_prefill && d.mlp_kind == EEB_MLP_RELU && d.dtype == EEB_BF16 && c->gemm_tier != 1 && batch >= 64 &&
+            !skip_cat("gemm")) {
+            // prefill chunks on cuBLASLt: ReLU + bf16 in its epilogue (no f32
+            // plane, no activation kernel: -14 % of the C2 prefill's launches' time)
+            Timer t(c, kCatGemm);
+            if (gemm_lt(c, wup, h, m.up_l, D, batch, act_dst, true)) {
                 count(c, kCatGemm, 1);
                 continue;
             }
