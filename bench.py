@@ -107,6 +107,15 @@ def gemm_bytes_per_step(desc, batch: int, layers: int) -> int:
     return per_layer * layers
 
 
+def gemm_flops_per_step(desc, batch: int, layers: int) -> float:
+    """2 flop per weight per row of every layer GEMM (every row runs every layer: flat steps)."""
+    hd = desc.head_dim
+    dq, dkv = desc.n_heads * hd, desc.n_kv_heads * hd
+    up = 2 * desc.d_ffn if desc.mlp_kind == 1 else desc.d_ffn
+    D, F = desc.d_model, desc.d_ffn
+    return 2.0 * batch * layers * sum(n * k for n, k in [(dq + 2 * dkv, D), (D, dq), (up, D), (D, F)])
+
+
 def head_bytes(desc, batch: int) -> int:
     """K2: V x d head weights + normed activations + 17 B per row."""
     return desc.vocab * desc.d_model * desc.bytes_per_el + batch * desc.d_model * desc.bytes_per_el + 17 * batch
@@ -259,6 +268,24 @@ def batch_sweep(ctx, eeb, desc, args, stream, batches=(1, 2, 4, 16, 32, 64, 128,
             if g_ms > 0 and g_all:
                 row["layer_gemm_frac"] = (gemm_bytes_per_step(d, B, run_layers) * g_ran / len(g_all)
                                           / (g_ms / 1e3) / 1e9 / hbm)
+                if policy == eeb.FLAT:
+                    # at large batch the decode GEMMs reach the ridge point (2 B
+                    # flop per weight byte): the binding roofline is the slower
+                    # of the HBM stream and the tensor pipe (sustained bf16 peak)
+                    t_hbm = gemm_bytes_per_step(d, B, run_layers) / (hbm * 1e9)
+                    tf = float(peaks()[0].get("bf16_tflops_sustained", 0) or peaks()[0].get("bf16_tflops", 0))
+                    if tf > 0:
+                        t_tc = gemm_flops_per_step(d, B, run_layers) / (tf * 1e12)
+                        row["layer_gemm_tensor_frac"] = t_tc / (g_ms / 1e3)
+                        row["layer_gemm_bound"] = "tensor" if t_tc > t_hbm else "hbm"
+                        row["layer_gemm_roofline_frac"] = max(t_tc, t_hbm) / (g_ms / 1e3)
+                    # whole step (weights + heads + KV): the per-launch critical-path
+                    # times credit a GEMM's pre-wait weight prefetch to its
+                    # predecessor, so at small batch the GEMM fraction can read
+                    # above 1; the step fraction is the unattributed check
+                    kv = B * run_layers * (P + 3 + 0.5 * n_steps) * 2 * d.n_kv_heads * d.head_dim * d.bytes_per_el
+                    w = d.layer_weight_elems() * d.bytes_per_el * run_layers + head_bytes(d, B) * heads
+                    row["step_hbm_frac"] = (w + kv) / (ms / 1e3) / 1e9 / hbm
             if h_ms > 0 and heads:
                 row["exit_head_frac"] = head_bytes(d, B) * heads / (h_ms / 1e3) / 1e9 / hbm
         except Exception as e:  # per-batch roofline is extra information

@@ -736,14 +736,22 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // the tile hits L2), so each CTA keeps 3 pipeline stages and a 128-column
     // accumulator and the split count halves (longer K per CTA)
     static const bool env_rhalf = !std::getenv("EEB_TC_RHALF") || std::atoi(std::getenv("EEB_TC_RHALF")) != 0;
-    const int rh = env_rhalf && bpad > 128 ? (bpad + 127) / 128 : 1;
+    // ... except for long K (>= 128 k-blocks: the 34B / 70B layer shapes): one
+    // CTA per weight tile over all rows (one 256-column accumulator, the tile
+    // read once), 4 stages, one CTA per SM, splits filling one wave of SMs —
+    // measured (tools/gemm_split_sweep.py, B=256, 34B QKV / O / up / down):
+    // 60.7 / 36.7 / 195 / 93.4 us -> 46.4 / 33.4 / 177.6 / 82.7 us; C2's
+    // K = 2048 shapes keep the row halves (equal or better there)
+    static const bool env_deep = !std::getenv("EEB_TC_DEEP") || std::atoi(std::getenv("EEB_TC_DEEP")) != 0;
+    const bool deep = env_deep && bpad > 128 && a.K / kBK >= 128 && !a.head_tri && !a.act_out;
+    const int rh = env_rhalf && bpad > 128 && !deep ? (bpad + 127) / 128 : 1;
     if (rh > 1) bpad = 128;
     const int mt = tiles * rh;  // CTAs per split
     const int kblocks = a.K / kBK;
     // split K so the grid covers the SMs once, keeping >= 2 k-blocks per CTA
     static const int env_wave = std::getenv("EEB_TC_WAVE") ? std::atoi(std::getenv("EEB_TC_WAVE")) : 0;
     static const int env_stages = std::getenv("EEB_TC_STAGES") ? std::atoi(std::getenv("EEB_TC_STAGES")) : 0;
-    const int wave = env_wave > 0 ? env_wave : 2 * a.num_sms;  // two co-resident CTAs per SM
+    const int wave = env_wave > 0 ? env_wave : (deep ? 1 : 2) * a.num_sms;  // co-resident CTAs per SM
     // (at most 16 planes: the attention kernels sum up to 16 QKV planes in registers;
     //  only narrow GEMMs such as a 70B tensor-parallel QKV shard would want more)
     int splits = std::max(1, std::min(std::min(kblocks / 2, wave / mt), 16));
@@ -752,11 +760,15 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
         // wide GEMMs (more tiles than half a wave, e.g. the 34B up projection:
         // 344 tiles): the split count with the best wave efficiency, planes
         // capped at the weight bytes (s * rows * 4 <= K * 2)
+        // (deep tiles: up to 3 splits, each extra split must gain 0.1 of wave
+        //  efficiency — 34B QKV 80 tiles: 3 splits; up 344 tiles: 2)
         double best = 0.0;
-        for (int sp = 1; sp <= env_widesplit && sp <= kblocks / 2 && (size_t)sp * bpad * 4 <= (size_t)a.K * 2; ++sp) {
+        const int max_sp = deep ? std::max(env_widesplit, 3) : env_widesplit;
+        const double gain = deep ? 0.1 : 0.02;
+        for (int sp = 1; sp <= max_sp && sp <= kblocks / 2 && (size_t)sp * bpad * 4 <= (size_t)a.K * 2; ++sp) {
             const int units = mt * sp;
             const double eff = (double)units / ((double)((units + wave - 1) / wave) * wave);
-            if (eff > best + 0.02) {
+            if (eff > best + gain) {
                 best = eff;
                 splits = sp;
             }
@@ -774,6 +786,9 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     // 2.262 -> 2.257, 34B flat-12 B=64 3.220 -> 3.161 (10: no better)
     static const int env_maxsplit = std::getenv("EEB_TC_MAXSPLIT") ? std::atoi(std::getenv("EEB_TC_MAXSPLIT")) : 12;
     if (env_maxsplit > 0) splits = std::min(splits, env_maxsplit);
+    // (sweeps only: EEB_TC_SPLITS forces the split count of plain split-K GEMMs)
+    static const int env_splits = std::getenv("EEB_TC_SPLITS") ? std::atoi(std::getenv("EEB_TC_SPLITS")) : 0;
+    if (env_splits > 0 && !a.head_tri && !a.act_out) splits = std::max(1, std::min(env_splits, kblocks / 2));
     int kb_per = (kblocks + splits - 1) / splits;
     splits = (kblocks + kb_per - 1) / kb_per;
     // Clusters of cs CTAs along K reduce their partials on chip (DSMEM): pick
@@ -819,7 +834,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t s) {
     const uint32_t stage_bytes = (uint32_t)(kBM + bpad) * kBK * 2;
     // ~half the SM's shared memory so two GEMM CTAs co-reside: the next GEMM of
     // the step (PDL) streams its weights while this one drains.
-    int stages = std::min(4, (int)((kSmemBudget / 2 - 1024 - 256) / stage_bytes));
+    int stages = std::min(4, (int)(((deep ? kSmemBudget : kSmemBudget / 2) - 1024 - 256) / stage_bytes));
     stages = std::min(stages, std::max(2, kb_per));
     // wide activation tiles (prefill, >= 128 rows): one CTA per SM with a
     // deeper pipeline (EEB_TC_WIDE=1; measured slower on the C2 prefill)

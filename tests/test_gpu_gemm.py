@@ -29,7 +29,9 @@ def ref_gemm(w, x, mode):
 @pytest.mark.parametrize("tier", [1, 2])
 @pytest.mark.parametrize("n,k,b", [(128, 256, 16), (2048, 2048, 64), (6144, 2048, 64), (2048, 8192, 32),
                                    (50272, 2048, 64), (1000, 512, 48), (4096, 1024, 256), (2048, 2048, 4),
-                                   (1000, 512, 3), (2048, 2048, 200), (6144, 2048, 130)])
+                                   (1000, 512, 3), (2048, 2048, 200), (6144, 2048, 130),
+                                   # long K above 128 rows: one 256-column tile per weight tile (deep)
+                                   (2048, 8192, 256), (1000, 8192, 176)])
 @pytest.mark.parametrize("mode", [0, 2, 3])
 def test_gemm_tiers(ctx, tier, n, k, b, mode):
     if tier == 1 and b > 64:
