@@ -74,13 +74,15 @@ struct DecSmem {
     }
 };
 
-template <int HD, bool PAGED>
+// NRW: ring stages per warp (DecCfg's 3; 2 when a large batch's per-CTA
+// prologue staging would not fit beside three)
+template <int HD, bool PAGED, int NRW>
 __global__ void __launch_bounds__(DecCfg<HD>::kThreads, 1)
     attention_dec_kernel(Stamp stamp, const __grid_constant__ CUtensorMap kmap,
                          const __grid_constant__ CUtensorMap vmap, AttnArgs a, int items_cap) {
     StampScope stamp_scope(stamp);
     using C = DecCfg<HD>;
-    constexpr int CB = C::CB, NW = C::NW, NRW = C::NRW, NT = HD / 8, KS = HD / 16;
+    constexpr int CB = C::CB, NW = C::NW, NT = HD / 8, KS = HD / 16;
     constexpr uint32_t kBlk = C::kBlk, kStage = C::kStage;
     constexpr int kNT = NW * 32;
     extern __shared__ uint8_t smem_raw[];
@@ -402,12 +404,27 @@ bool launch_dec(const AttnArgs& a0, cudaStream_t s) {
     a.dbg = dbg;
     const int G = a.n_heads / a.n_kv_heads;
     const int items_max = a.max_rows * a.n_kv_heads;
-    const int grid = std::max(std::min(items_max, a.num_sms), (items_max + kMaxItems - 1) / kMaxItems);
+    const int grid0 = std::max(std::min(items_max, a.num_sms), (items_max + kMaxItems - 1) / kMaxItems);
+    // The CTA stages its items' prologue data (q, new k / v, KV depth, RoPE)
+    // beside the warps' rings: at large batch (34B at 256 rows: 2048 items, 14
+    // per CTA, 57 KB of q) that does not fit next to 3-deep rings; take 2-deep
+    // rings, then more CTAs (fewer items each), before giving up.
+    int grid = grid0, nrw = C::NRW;
+    size_t smem = 0;
+    for (;;) {
+        const int cap = (items_max + grid - 1) / grid;
+        smem = 1024 + DecSmem(HD, G, cap, a.max_seq, PAGED, (size_t)C::NW * nrw * C::kStage).total;
+        if (smem <= 227 * 1024) break;
+        if (nrw == C::NRW) {
+            nrw = 2;
+        } else if (cap > 1) {
+            grid += a.num_sms;
+        } else {
+            return false;
+        }
+    }
     const int cap = (items_max + grid - 1) / grid;
-    const DecSmem L(HD, G, cap, a.max_seq, PAGED, (size_t)C::NW * C::NRW * C::kStage);
-    const size_t smem = 1024 + L.total;
-    if (smem > 227 * 1024) return false;
-    auto kern = attention_dec_kernel<HD, PAGED>;
+    auto kern = nrw == 2 ? attention_dec_kernel<HD, PAGED, 2> : attention_dec_kernel<HD, PAGED, C::NRW>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(kern, dim3(grid), dim3(C::kThreads), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a, cap);

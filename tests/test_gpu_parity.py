@@ -358,3 +358,29 @@ def test_head_dim_80(ctx, dtype):
         agree += int((g["token_id"] == r["token_id"]).sum())
         total += 4
     assert agree / total >= BF16_AGREE, agree / total
+
+
+def test_bf16_gqa_large_batch_staging():
+    """34B-style GQA (8 query heads per kv head, head_dim 128) at 256 rows:
+    1024 (row, kv head) items, 7 per CTA — the streaming decode attention's
+    per-CTA prologue staging no longer fits beside 3-deep rings, so it runs
+    2-deep rings (the C4 batch-256 configuration) — against the oracle."""
+    desc = eeb.ModelDesc("mini-gqa8-b256", 2, 4096, 32, 4, 1024, 1000, (1, 2), dtype=eeb.BF16,
+                         mlp_kind=eeb.MLP_SWIGLU, max_slots=256, max_seq_len=64, seed=29)
+    c = eeb.Context(0)
+    try:
+        m, ref = _pair(c, desc)
+        rng = np.random.default_rng(31)
+        B = 256
+        slots = np.arange(B)
+        agree = total = 0
+        for pos in range(3):
+            toks = rng.integers(0, desc.vocab, B)
+            g = c.decode_step(m, 0, eeb.PROFILE, TH, slots, toks, np.full(B, pos))
+            r = ref.decode_step(0, eeb.PROFILE, TH, slots, toks, np.full(B, pos))
+            agree += int((g["head_token"] == r["head_token"]).sum())
+            total += g["head_token"].size
+            assert np.abs(g["head_confidence"] - r["head_confidence"]).max() < 0.05
+        assert agree / total >= BF16_AGREE, agree / total
+    finally:
+        c.close()
