@@ -56,7 +56,11 @@ struct DecCfg {
     static constexpr uint32_t kStage = 2 * CB * kBlk;  // K + V of one chunk
     static constexpr int NW = HD == 64 ? 8 : 4;        // compute warps (each owns whole items)
     static constexpr int NRW = 3;                      // ring stages per warp
-    static constexpr int kThreads = NW * 32;
+    // + NW helper warps for the prologue (q / k / v plane sums, KV-depth and
+    // RoPE staging, RoPE + K/V append) only: twice the loads in flight per
+    // round trip (34B B=64: the prologue took 11 of the 20 us per layer)
+    static constexpr int NH = NW;
+    static constexpr int kThreads = (NW + NH) * 32;
 };
 
 // Shared-memory plan after the rings (host and device agree).
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kThreads, 1)
     using C = DecCfg<HD>;
     constexpr int CB = C::CB, NW = C::NW, NT = HD / 8, KS = HD / 16;
     constexpr uint32_t kBlk = C::kBlk, kStage = C::kStage;
-    constexpr int kNT = NW * 32;
+    constexpr int kNT = C::kThreads;  // prologue loops: every warp, helpers included
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -159,8 +163,10 @@ __global__ void __launch_bounds__(DecCfg<HD>::kThreads, 1)
             ik += NW;
         }
     };
-    if (lane == 0)
-        for (int s = 0; s < NRW; ++s) issue_next(s);
+    // ring stages issued before the prologue (a.pre_stages; the rest after it)
+    const int pre = min(NRW, a.pre_stages);
+    if (lane == 0 && warp < NW)
+        for (int s = 0; s < pre; ++s) issue_next(s);
 
     // ---- prologue (all warps, every item of the CTA) --------------------------
     // Phase A: every global load in flight together — the q/k/v float4s of up
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kThreads, 1)
     float* sn_s = cs_s + (size_t)items_cap * half;
     if (!(a.dbg & 4)) {  // (timing experiment 4: no prologue)
         const int n4 = (G + 2) * HD / 4, nq4 = G * HD / 4, total = my * n4;
-        constexpr int kR = 4;
+        constexpr int kR = 8;
         for (int e0 = t; e0 < total; e0 += kR * kNT) {
             float4 acc[kR];
             const float* src[kR];
@@ -265,6 +271,10 @@ __global__ void __launch_bounds__(DecCfg<HD>::kThreads, 1)
         }
     }
     __syncthreads();
+    if (t == 0) stamp_mark(stamp);  // (timeline) prologue done
+    if (warp >= NW) return;  // helper warps: prologue only
+    if (lane == 0)
+        for (int s = pre; s < NRW; ++s) issue_next(s);
 
     // ---- this warp's items -----------------------------------------------------
     const int h = lane >> 2, kq = (lane & 3) * 2;    int u = 0;  // chunks consumed by this warp
@@ -402,6 +412,8 @@ bool launch_dec(const AttnArgs& a0, cudaStream_t s) {
     AttnArgs a = a0;
     static const int dbg = std::getenv("EEB_ATTN_DBG") ? std::atoi(std::getenv("EEB_ATTN_DBG")) : 0;
     a.dbg = dbg;
+    static const int env_pre = std::getenv("EEB_ATTN_PRE") ? std::atoi(std::getenv("EEB_ATTN_PRE")) : 1;
+    a.pre_stages = env_pre;
     const int G = a.n_heads / a.n_kv_heads;
     const int items_max = a.max_rows * a.n_kv_heads;
     const int grid0 = std::max(std::min(items_max, a.num_sms), (items_max + kMaxItems - 1) / kMaxItems);

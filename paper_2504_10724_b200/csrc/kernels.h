@@ -177,6 +177,7 @@ struct AttnArgs {
     float* kv_part = nullptr;   // [max_rows][Hkv][kv_splits][8][hd + 2]
     int* kv_ticket = nullptr;   // [max_rows][Hkv]
     int dbg = 0;                // timing experiments (attention_dec, EEB_ATTN_DBG): 1 no compute, 2 no K/V loads
+    int pre_stages = 1;         // attention_dec: ring stages issued before the prologue (EEB_ATTN_PRE)
     const void* pf = nullptr;   // the O GEMM's weights, prefetched into L2 during the attention (optional)
     size_t pf_bytes = 0;
 };

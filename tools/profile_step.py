@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--policy", default="introspective")
+    ap.add_argument("--depth", type=int, default=6, help="flat policy: serving depth")
     ap.add_argument("--graphs", type=int, default=-1)  # -1: library default (stream launches under ncu)
     args = ap.parse_args()
     import torch
@@ -39,7 +40,7 @@ def main():
     slots = np.arange(B)
     for p in range(args.prompt):
         ctx.decode_step(m, 0, eeb.FULL_DEPTH, 0.7, slots, rng.integers(0, desc.vocab, B), np.full(B, p))
-    depth = 6 if pol == eeb.FLAT else 0
+    depth = args.depth if pol == eeb.FLAT else 0
     for k in range(3):  # warm (graph capture happens here)
         ctx.decode_step(m, depth, pol, 0.7, slots, rng.integers(0, desc.vocab, B), np.full(B, args.prompt + k))
     torch.cuda.synchronize()
