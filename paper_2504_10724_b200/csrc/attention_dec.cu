@@ -643,9 +643,13 @@ __global__ void __launch_bounds__(kMW * 32, 1)
         if (ik >= my) return;
         const uint32_t bar = smem_u32(&full[warp][st]);
         const int rows = min(R, c_n - ip);
-        mbar_expect_tx(bar, (uint32_t)rows * kRow);
-        bulk_g2s(ring + (uint32_t)st * stage_bytes, (iph == 0 ? kc : vc) + row_off(c_lr, c_g, ip), (uint32_t)rows * kRow,
-                 bar, pol);
+        if (a.dbg & 2) {  // timing experiment: no loads (the stage completes empty)
+            mbar_arrive(bar);
+        } else {
+            mbar_expect_tx(bar, (uint32_t)rows * kRow);
+            bulk_g2s(ring + (uint32_t)st * stage_bytes, (iph == 0 ? kc : vc) + row_off(c_lr, c_g, ip),
+                     (uint32_t)rows * kRow, bar, pol);
+        }
         ip += R;
         if (ip >= c_n) {
             ip = 0;
@@ -740,7 +744,7 @@ __global__ void __launch_bounds__(kMW * 32, 1)
             const int st = u % nring;
             const uint32_t stage = ring + (uint32_t)st * stage_bytes;
             mbar_wait(smem_u32(&full[warp][st]), (uint32_t)((u / nring) & 1));
-            const int c0r = c * R, rows = min(R, pos + 1 - c0r);
+            const int c0r = c * R, rows = (a.dbg & 1) ? 0 : min(R, pos + 1 - c0r);  // (dbg 1: no compute)
             for (int sb = 0; sb < rows; sb += 32) {
                 const int r = sb + lane, p = c0r + r;
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -804,7 +808,7 @@ __global__ void __launch_bounds__(kMW * 32, 1)
             const uint32_t stage = ring + (uint32_t)st * stage_bytes;
             mbar_wait(smem_u32(&full[warp][st]), (uint32_t)((u / nring) & 1));
             const int c0r = c * R;
-            const int nfull = min(R, pos - c0r) & ~3;  // rows before pos, in groups of 4
+            const int nfull = (a.dbg & 1) ? 0 : min(R, pos - c0r) & ~3;  // rows before pos, in groups of 4
             for (int r = 0; r < nfull; r += 4) {
                 const float4 e = *reinterpret_cast<const float4*>(sc_s + c0r + r);
 #pragma unroll
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(kMW * 32, 1)
                     o[t][2] = fmaf(e.w, bf_lo(w3), o[t][2]); o[t][3] = fmaf(e.w, bf_hi(w3), o[t][3]);
                 }
             }
-            const int rows = min(R, pos + 1 - c0r);
+            const int rows = (a.dbg & 1) ? 0 : min(R, pos + 1 - c0r);
             for (int r = nfull; r < rows; ++r) {  // the rest, the new row from registers
                 const float e = sc_s[c0r + r];
 #pragma unroll
@@ -870,7 +874,10 @@ bool launch_mha_w(const AttnArgs& a, cudaStream_t s) {
     const size_t smem = fixed + ((size_t)pool_kb << 10);
     auto kern = attention_mha_kernel<HD, kMW, PAGED>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_pdl(kern, dim3(grid), dim3(kMW * 32), smem, s, a, pool_kb);
+    static const int dbg = std::getenv("EEB_ATTN_DBG") ? std::atoi(std::getenv("EEB_ATTN_DBG")) : 0;
+    AttnArgs ad = a;
+    ad.dbg = dbg;  // timing experiments: 1 no compute, 2 no K/V loads
+    launch_pdl(kern, dim3(grid), dim3(kMW * 32), smem, s, ad, pool_kb);
     EEB_CHECK_LAUNCH();
     return true;
 }
