@@ -364,8 +364,10 @@ def test_bf16_gqa_large_batch_staging():
     """34B-style GQA (8 query heads per kv head, head_dim 128) at 256 rows:
     1024 (row, kv head) items, 7 per CTA — the streaming decode attention's
     per-CTA prologue staging no longer fits beside 3-deep rings, so it runs
-    2-deep rings (the C4 batch-256 configuration) — against the oracle."""
-    desc = eeb.ModelDesc("mini-gqa8-b256", 2, 4096, 32, 4, 1024, 1000, (1, 2), dtype=eeb.BF16,
+    2-deep rings (the C4 batch-256 configuration); d_ffn 8192 puts the down
+    projection (K = 8192) on the long-K one-tile-per-weight-tile GEMM path —
+    against the oracle."""
+    desc = eeb.ModelDesc("mini-gqa8-b256", 2, 4096, 32, 4, 8192, 1000, (1, 2), dtype=eeb.BF16,
                          mlp_kind=eeb.MLP_SWIGLU, max_slots=256, max_seq_len=64, seed=29)
     c = eeb.Context(0)
     try:
