@@ -248,6 +248,41 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
     return (to_bf16_bits(a).astype(np.uint32) << 16).view(np.float32)
 
 
+def _i32(a) -> np.ndarray:
+    if isinstance(a, np.ndarray) and a.dtype == np.int32 and a.flags.c_contiguous:
+        return a
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _addr(a: np.ndarray) -> int:
+    return a.__array_interface__["data"][0]
+
+
+_OUT_CACHE: dict = {}
+
+
+def _out_layout(b: int, ne: int, profile: bool):
+    """(field, dtype, shape, byte offset) of eeb_step_out's arrays packed into
+    one buffer (8-byte aligned), in _Out field order, and the total bytes."""
+    key = (b, ne, profile)
+    hit = _OUT_CACHE.get(key)
+    if hit is not None:
+        return hit
+    fields = [("exit_layer", np.int32, (b,)), ("token_id", np.int32, (b,)), ("confidence", np.float32, (b,)),
+              ("logprob", np.float32, (b,)), ("breached", np.uint8, (b,)), ("unchanged", np.uint8, (b,)),
+              ("hist", np.int64, (ne,)), ("n_breached", np.int64, (1,)), ("sum_logprob", np.float64, (1,))]
+    if profile:
+        fields += [("head_token", np.int32, (b, ne)), ("head_confidence", np.float32, (b, ne)),
+                   ("head_logprob", np.float32, (b, ne))]
+    spec, off = [], 0
+    for name, dt, shape in fields:
+        off = (off + 7) & ~7
+        spec.append((name, dt, shape, off))
+        off += int(np.prod(shape)) * np.dtype(dt).itemsize
+    _OUT_CACHE[key] = (spec, max(off, 8))
+    return _OUT_CACHE[key]
+
+
 class StepResult(dict):
     """Per-row outputs of one decode step (numpy arrays)."""
 
@@ -365,25 +400,17 @@ class Context:
                     ) -> StepResult:
         """eeb_decode_step with host buffers (H2D/D2H inside the call)."""
         desc = self.models[model]
-        slots = np.ascontiguousarray(slots, dtype=np.int32)
-        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
-        positions = np.ascontiguousarray(positions, dtype=np.int32)
+        slots, tokens, positions = _i32(slots), _i32(tokens), _i32(positions)
         b = len(tokens)
-        ne = len(desc.exit_layers)
-        r = StepResult(
-            exit_layer=np.zeros(b, np.int32), token_id=np.zeros(b, np.int32),
-            confidence=np.zeros(b, np.float32), logprob=np.zeros(b, np.float32),
-            breached=np.zeros(b, np.uint8), unchanged=np.zeros(b, np.uint8),
-            hist=np.zeros(ne, np.int64), n_breached=np.zeros(1, np.int64),
-            sum_logprob=np.zeros(1, np.float64))
-        if policy == PROFILE:
-            r["head_token"] = np.zeros((b, ne), np.int32)
-            r["head_confidence"] = np.zeros((b, ne), np.float32)
-            r["head_logprob"] = np.zeros((b, ne), np.float32)
-        out = _Out(*[r[k].ctypes.data if k in r else None for k, _ in _Out._fields_])
-        _check(self.lib.eeb_decode_step(self.h, model, depth, policy, float(th), b, slots.ctypes.data,
-                                        tokens.ctypes.data, positions.ctypes.data, C.byref(out)))
-        return r
+        # every output array is a view of one fresh buffer (the library writes
+        # each field it is given a pointer for): one allocation per step
+        spec, total = _out_layout(b, len(desc.exit_layers), policy == PROFILE)
+        buf = np.empty(total, np.uint8)
+        base = buf.__array_interface__["data"][0]
+        out = _Out(*[base + o for _, _, _, o in spec])
+        _check(self.lib.eeb_decode_step(self.h, model, depth, policy, float(th), b, _addr(slots),
+                                        _addr(tokens), _addr(positions), C.byref(out)))
+        return StepResult({k: np.ndarray(shape, dt, buf, o) for k, dt, shape, o in spec})
 
     def decode_step_device(self, model: int, depth: int, policy: int, th: float, batch: int,
                              d_slots: int, d_tokens: int, d_positions: int, out_ptrs: dict | None = None):
