@@ -1086,7 +1086,10 @@ int gemm(eeb_ctx* c, int cat, const Model& m, const void* W, const void* X, int 
     c->pf_ptr = nullptr;
     c->pf_bytes = 0;
     int planes = 0;
-    if (c->in_prefill && plane0 == 0 && batch >= 64 && m.desc.dtype == EEB_BF16 && c->gemm_tier != 1 &&
+    // (prefill chunks: one cuBLASLt plane, after the planes earlier row-parallel
+    //  shards of an all-shards context wrote — chunks above 256 rows have no
+    //  split-K tcgen05 path)
+    if (c->in_prefill && batch >= 64 && m.desc.dtype == EEB_BF16 && c->gemm_tier != 1 &&
         gemm_lt(c, W, X, N, K, batch, a.out)) {
         count(c, cat, 1);
         return 1;

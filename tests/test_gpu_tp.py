@@ -68,23 +68,27 @@ def test_tp_shards_decode_like_unsharded(ctx, tp):
     ctx.evict(sh)
 
 
-def test_tp_matches_oracle_and_prefill(ctx):
-    desc = BASE.replace(name="tp2-oracle", tp_size=2, tp_rank=-1)
+@pytest.mark.parametrize("plen", [12, 40], ids=["chunk192", "chunk640"])
+def test_tp_matches_oracle_and_prefill(ctx, plen):
+    """Sharded model prefilled then decoded against the oracle; 16 x 40 = 640
+    prompt rows put the row-parallel shards' prefill GEMMs on cuBLASLt planes
+    side by side (chunks above 256 rows have no split-K tcgen05 path)."""
+    desc = BASE.replace(name=f"tp2-oracle-{plen}", tp_size=2, tp_rank=-1)
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
     ref = OracleModel(BASE)
     ref.load(BASE.num_layers)
     rng = np.random.default_rng(9)
     B = 16
-    prompts = [rng.integers(0, BASE.vocab, 12) for _ in range(B)]
+    prompts = [rng.integers(0, BASE.vocab, plen) for _ in range(B)]
     ctx.prefill(m, desc.num_layers, np.arange(B), prompts)
-    for k in range(12):
+    for k in range(plen):
         ref.decode_step(0, eeb.FULL_DEPTH, TH, np.arange(B), np.array([p[k] for p in prompts]), np.full(B, k))
     agree = []
     for k in range(4):
         toks = rng.integers(0, BASE.vocab, B)
-        g = ctx.decode_step(m, 0, eeb.INTROSPECTIVE, TH, np.arange(B), toks, np.full(B, 12 + k))
-        r = ref.decode_step(0, eeb.INTROSPECTIVE, TH, np.arange(B), toks, np.full(B, 12 + k))
+        g = ctx.decode_step(m, 0, eeb.INTROSPECTIVE, TH, np.arange(B), toks, np.full(B, plen + k))
+        r = ref.decode_step(0, eeb.INTROSPECTIVE, TH, np.arange(B), toks, np.full(B, plen + k))
         agree.extend(g["token_id"] == r["token_id"])
     assert np.mean(agree) >= 0.99, np.mean(agree)
     ctx.evict(m)
