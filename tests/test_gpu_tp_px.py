@@ -33,27 +33,27 @@ BASE = eeb.ModelDesc("tp-px", 6, 512, 8, 4, 1024, 1024, (2, 4, 6), dtype=eeb.BF1
 B, STEPS = 16, 6
 
 
-def _schedule():
+def _schedule(plen):
     rng = np.random.default_rng(11)
-    prompts = [rng.integers(0, BASE.vocab, 8).astype(np.int32) for _ in range(B)]
+    prompts = [rng.integers(0, BASE.vocab, plen).astype(np.int32) for _ in range(B)]
     toks = [rng.integers(0, BASE.vocab, B).astype(np.int32) for _ in range(STEPS)]
     return prompts, toks
 
 
-def _decode(ctx, m):
-    prompts, toks = _schedule()
+def _decode(ctx, m, plen):
+    prompts, toks = _schedule(plen)
     ctx.load_layers(m, BASE.num_layers)
     ctx.prefill(m, BASE.num_layers, np.arange(B), prompts)
     out = []
     for k, t in enumerate(toks):
         pol = eeb.PROFILE if k % 2 == 0 else eeb.INTROSPECTIVE
-        r = ctx.decode_step(m, 0, pol, TH, np.arange(B), t, np.full(B, 8 + k))
+        r = ctx.decode_step(m, 0, pol, TH, np.arange(B), t, np.full(B, plen + k))
         out.append(np.stack([r["token_id"], r["exit_layer"]]).astype(np.int64))
         out.append(np.asarray(r["confidence"], np.float32)[None])
     return out
 
 
-def _rank(rank, d, graphs, devices):
+def _rank(rank, d, graphs, devices, plen):
     ctx = eeb.Context(devices[rank])
     if not graphs:
         ctx.set_graphs(False)
@@ -66,27 +66,30 @@ def _rank(rank, d, graphs, devices):
         time.sleep(0.02)
     handles = [open(os.path.join(d, f"h{p}"), "rb").read() for p in range(2)]
     ctx.tp_px_attach(m, 2, handles=handles)
-    res = _decode(ctx, m)
+    res = _decode(ctx, m, plen)
     np.savez(os.path.join(d, f"rank{rank}.npz"), *res)
     ctx.close()
 
 
-@pytest.mark.parametrize("graphs,devices", [(True, (0, 0)), (False, (0, 0)), (True, (0, 1))],
-                         ids=["graph-1gpu", "eager-1gpu", "graph-2gpu"])
-def test_tp2_peer_memory_ranks_match_all_shards_bit_for_bit(graphs, devices):
+# plen 40: 16 x 40 = 640 prompt rows in one prefill chunk (cuBLASLt planes
+# written into the exchange buffer, tp_norm over 640 rows)
+@pytest.mark.parametrize("graphs,devices,plen", [(True, (0, 0), 8), (False, (0, 0), 8), (True, (0, 1), 8),
+                                                 (True, (0, 0), 40)],
+                         ids=["graph-1gpu", "eager-1gpu", "graph-2gpu", "graph-1gpu-prefill640"])
+def test_tp2_peer_memory_ranks_match_all_shards_bit_for_bit(graphs, devices, plen):
     import torch
     import torch.multiprocessing as mp
 
     if max(devices) >= torch.cuda.device_count():
         pytest.skip("needs 2 GPUs (one shard per GPU over NVLink P2P)")
     with tempfile.TemporaryDirectory() as d:
-        mp.start_processes(_rank, args=(d, graphs, devices), nprocs=2, join=True, start_method="spawn")
+        mp.start_processes(_rank, args=(d, graphs, devices, plen), nprocs=2, join=True, start_method="spawn")
         got = []
         for r in range(2):
             z = np.load(os.path.join(d, f"rank{r}.npz"))
             got.append([z[f"arr_{i}"] for i in range(len(z.files))])
     ctx = eeb.Context(0)
-    ref = _decode(ctx, ctx.register(BASE.replace(name="px-all", tp_size=2, tp_rank=-1)))
+    ref = _decode(ctx, ctx.register(BASE.replace(name="px-all", tp_size=2, tp_rank=-1)), plen)
     ctx.close()
     for r in range(2):
         for k in range(len(ref)):
