@@ -123,10 +123,11 @@ public:
         int h = -1;
         throw_if_error(eeb_model_register(ctx_, &d, &h), "eeb_model_register");
         handles_[spec.id] = {h, spec};
-        // the paged pool serves bf16 models with head_dim 64 / 128 (the tensor-core
-        // attention kernels walk page tables); others keep the slot pool
+        // the paged pool serves bf16 models with head_dim 64 / 80 / 128 (the
+        // decode and prefill attention kernels walk page tables); others keep
+        // the slot pool
         const int hd = a.n_heads > 0 ? a.d_model / a.n_heads : 0;
-        if (kv_page_ > 0 && a.dtype == EEB_BF16 && (hd == 64 || hd == 128))
+        if (kv_page_ > 0 && a.dtype == EEB_BF16 && (hd == 64 || hd == 80 || hd == 128))
             throw_if_error(eeb_kv_configure_pages(ctx_, h, kv_page_,
                                                   kv_pages_ > 0 ? kv_pages_
                                                                 : max_slots * ((max_seq_len + kv_page_ - 1) / kv_page_)),

@@ -1076,11 +1076,16 @@ __global__ void kv_append_kernel(Stamp stamp, AttnArgs a) {
     const float* sn = a.rope_sin + (int64_t)pos * half;
     T* kc = static_cast<T*>(a.k_cache);
     T* vc = static_cast<T*>(a.v_cache);
+    // index idx = (kv head g, 4 dims jj of the first half): the key pair
+    // (jj, jj + half) rotated, and the value's same two 4-dim groups — every
+    // load of an index in flight before the first use (one round trip)
     const int q4 = half / 4;
     for (int idx = threadIdx.x; idx < Hkv * q4; idx += blockDim.x) {
         const int g = idx / q4, jj = 4 * (idx % q4);
         const float4 x0 = plane_sum4(row + dq + g * hd + jj, a.splits, a.split_stride);
         const float4 x1 = plane_sum4(row + dq + g * hd + jj + half, a.splits, a.split_stride);
+        const float4 v0 = plane_sum4(row + dq + dkv + g * hd + jj, a.splits, a.split_stride);
+        const float4 v1 = plane_sum4(row + dq + dkv + g * hd + jj + half, a.splits, a.split_stride);
         const float4 c = *reinterpret_cast<const float4*>(cs + jj);
         const float4 sv = *reinterpret_cast<const float4*>(sn + jj);
         T* dst = kc + kv_elem_offset(a, slot, pos, g);
@@ -1088,12 +1093,9 @@ __global__ void kv_append_kernel(Stamp stamp, AttnArgs a) {
                      x0.w * c.w - x1.w * sv.w);
         store4_kv<T>(dst + jj + half, x0.x * sv.x + x1.x * c.x, x0.y * sv.y + x1.y * c.y, x0.z * sv.z + x1.z * c.z,
                      x0.w * sv.w + x1.w * c.w);
-    }
-    const int h4 = hd / 4;
-    for (int idx = threadIdx.x; idx < Hkv * h4; idx += blockDim.x) {
-        const int g = idx / h4, j = 4 * (idx % h4);
-        const float4 v = plane_sum4(row + dq + dkv + g * hd + j, a.splits, a.split_stride);
-        store4_kv<T>(vc + kv_elem_offset(a, slot, pos, g) + j, v.x, v.y, v.z, v.w);
+        T* vdst = vc + kv_elem_offset(a, slot, pos, g);
+        store4_kv<T>(vdst + jj, v0.x, v0.y, v0.z, v0.w);
+        store4_kv<T>(vdst + jj + half, v1.x, v1.y, v1.z, v1.w);
     }
 }
 
@@ -1108,12 +1110,18 @@ __global__ void kv_append_kernel(Stamp stamp, AttnArgs a) {
 // Masking is the decode rule per row: position p is visible to the row at
 // position r iff p <= r and (p == r or kv_depth[p] >= layer).
 // ---------------------------------------------------------------------------
-template <int HD, bool PAGED>
+// HD: the padded head dim (a multiple of 64: the TMA column blocks and the
+// shared-memory rows); HR: the model's head dim (80 for OPT-2.7B: the KV maps'
+// rows are 80 wide, so the second column block's dims 80..127 arrive as TMA
+// out-of-bounds zeros, and q is zero-padded to match).
+template <int HD, bool PAGED, int HR = HD>
 __global__ void __launch_bounds__(128)
     attention_prefill_kernel(Stamp stamp, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                              AttnArgs a) {
     StampScope stamp_scope(stamp);
-    constexpr int CB = HD / 64, CP = 64, NT = HD / 8, KS = HD / 16, NB = 2;
+    static_assert(HR <= HD && HR % 16 == 0, "real head dim within the padded one");
+    constexpr int CB = HD / 64, CP = 64, NB = 2;
+    constexpr int NT = (HR + 15) / 16 * 2, KS = (HR + 31) / 32 * 2;  // n-tiles / k-steps over the real dims
     constexpr uint32_t kBlockBytes = CP * 128, kBufBytes = 2 * CB * kBlockBytes;
     constexpr int kDep = 1024, kMaxPt = PAGED ? 64 : 1;
     pdl_launch_dependents();
@@ -1123,7 +1131,7 @@ __global__ void __launch_bounds__(128)
     const int4 it = a.pf_items[item];  // {first row, rows, slot, first position}
     const int hq = blockIdx.x;
     const int H = a.n_heads, Hkv = a.n_kv_heads, G = H / Hkv, g = hq / G;
-    const int dq = H * HD, dkv = Hkv * HD, half = HD / 2;
+    const int dq = H * HR, dkv = Hkv * HR, half = HR / 2;
     const int r0 = it.x, nrows = it.y, slot = it.z, p0 = it.w;
     const int last = p0 + nrows - 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1172,12 +1180,17 @@ __global__ void __launch_bounds__(128)
         for (int c = 0; c < NB && c < n_chunks; ++c) issue(c);
     }
     // queries: fixed-order plane sums, RoPE at each row's position, 1/sqrt(hd), bf16
-    const float qscale = rsqrtf((float)HD);
+    const float qscale = rsqrtf((float)HR);
+    if constexpr (HR < HD)  // the padding dims of q: zeros (K's arrive as zeros too)
+        for (int idx = threadIdx.x; idx < 64 * ((HD - HR) / 4); idx += blockDim.x) {
+            const int r = idx / ((HD - HR) / 4), jj = HR + 4 * (idx % ((HD - HR) / 4));
+            store4_kv<__nv_bfloat16>(q_s + r * HD + jj, 0.f, 0.f, 0.f, 0.f);
+        }
     for (int idx = threadIdx.x; idx < 64 * (half / 4); idx += blockDim.x) {
         const int r = idx / (half / 4), jj = 4 * (idx % (half / 4));
         float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
         if (r < nrows) {
-            const float* src = a.qkv + (int64_t)(r0 + r) * (dq + 2 * dkv) + hq * HD + jj;
+            const float* src = a.qkv + (int64_t)(r0 + r) * (dq + 2 * dkv) + hq * HR + jj;
             lo = plane_sum4(src, a.splits, a.split_stride);
             hi = plane_sum4(src + half, a.splits, a.split_stride);
             const int pos = p0 + r;
@@ -1320,18 +1333,19 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
         const int d = 8 * n + kq;
+        if (d >= HR) continue;
         if (live_a)
-            *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + ra) * dq + hq * HD + d) = pack_bf16(o[n][0] * ia, o[n][1] * ia);
+            *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + ra) * dq + hq * HR + d) = pack_bf16(o[n][0] * ia, o[n][1] * ia);
         if (live_b)
-            *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + rb) * dq + hq * HD + d) = pack_bf16(o[n][2] * ib, o[n][3] * ib);
+            *reinterpret_cast<uint32_t*>(out + (int64_t)(r0 + rb) * dq + hq * HR + d) = pack_bf16(o[n][2] * ib, o[n][3] * ib);
     }
 }
 
-template <int HD>
+template <int HD, int HR = HD>
 void launch_prefill_attn(const AttnArgs& a, cudaStream_t s) {
     const size_t smem = 1024 + 2 * 2 * (size_t)(HD / 64) * 64 * 128 + 64 * HD * 2;
     const bool paged = a.page_size != a.max_seq;
-    auto kern = paged ? attention_prefill_kernel<HD, true> : attention_prefill_kernel<HD, false>;
+    auto kern = paged ? attention_prefill_kernel<HD, true, HR> : attention_prefill_kernel<HD, false, HR>;
     EEB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch_pdl(kern, dim3(a.n_heads, a.pf_max_items), dim3(128), smem, s, *static_cast<const CUtensorMap*>(a.k_map),
                *static_cast<const CUtensorMap*>(a.v_map), a);
@@ -1426,8 +1440,10 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     const bool paged = a.page_size != a.max_seq;
     static const bool no_pf_attn = std::getenv("EEB_PREFILL_ATTN") && std::atoi(std::getenv("EEB_PREFILL_ATTN")) == 0;
     if (a.kv_ready && a.pf_items && !no_pf_attn && a.dtype == 1 && a.k_map && a.v_map &&
-        (a.head_dim == 64 || a.head_dim == 128) && a.max_seq <= 1024) {
+        (a.head_dim == 64 || a.head_dim == 80 || a.head_dim == 128)) {
+        // (KV depth of positions >= 1024 is read from global memory, not staged)
         if (a.head_dim == 64) launch_prefill_attn<64>(a, s);
+        else if (a.head_dim == 80) launch_prefill_attn<128, 80>(a, s);  // OPT-2.7B
         else launch_prefill_attn<128>(a, s);
         return;
     }

@@ -1285,7 +1285,7 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
     if (px) {
         Timer t(c, kCatNorm);
         launch_tp_norm(d.dtype, m.pxp, planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
-                       W.mlp_norm.as<float>(), h, nullptr, nullptr, s);
+                       W.mlp_norm.as<float>(), h, nullptr, nullptr, s, c->in_prefill ? 4 : 1);
         count(c, kCatNorm, 1);
     } else if (m.tp > 1 && m.shards == 1) {
         o = {tp_allreduce(c, m, ws, planes, cur.n_active, batch), 1};
@@ -1295,7 +1295,7 @@ PlaneSet layer_core(eeb_ctx* c, Model& m, int l, const RowState& cur, void* h, i
         if (!skip_cat("norm"))
             launch_residual_norm(d.dtype, o.base, o.planes, (int64_t)batch * D, cur.n_active, batch, cur.x, D, d.norm_eps,
                                  W.mlp_norm.as<float>(), h, nullptr, nullptr, s, l2pf_fused() && pf_on ? W.wup.p : nullptr,
-                                 (size_t)m.up_l * D * wb);
+                                 (size_t)m.up_l * D * wb, c->in_prefill ? 4 : 1);
         count(c, kCatNorm, 1);
     }
     static const bool act_unfused = std::getenv("EEB_ACT_UNFUSED") != nullptr;  // A/B
@@ -1632,17 +1632,18 @@ void enqueue_prefill(eeb_ctx* c, int mi, int depth, int rows) {
     void* h = c->hn.p;
     launch_embed(d.dtype, m.emb.p, I.tok, I.slot, I.pos, rows, D, cur, s);
     launch_mark_depth(rows, I.slot, I.pos, m.kv_depth.as<uint8_t>(), d.max_seq_len, depth, s);
+    // (prefill row kernels: 4 float4 groups per thread, see norm_vec)
     launch_residual_norm(d.dtype, nullptr, 0, 0, cur.n_active, rows, cur.x, D, d.norm_eps,
-                         m.layers[0]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+                         m.layers[0]->attn_norm.as<float>(), h, nullptr, nullptr, s, nullptr, 0, 4);
     count(c, kCatOther, 3);
     for (int l = 1; l <= depth; ++l) {
         const PlaneSet dn = layer_core(c, m, l, cur, h, rows, true);
         if (l < depth && dn.px)  // the next layer's attention norm (the last layer's residual is not needed)
             launch_tp_norm(d.dtype, m.pxp, dn.planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D, d.norm_eps,
-                           m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+                           m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s, 4);
         else if (l < depth)
             launch_residual_norm(d.dtype, dn.base, dn.planes, (int64_t)rows * D, cur.n_active, rows, cur.x, D,
-                                 d.norm_eps, m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s);
+                                 d.norm_eps, m.layers[l]->attn_norm.as<float>(), h, nullptr, nullptr, s, nullptr, 0, 4);
         count(c, kCatNorm, l < depth ? 1 : 0);
     }
 }
@@ -1782,7 +1783,9 @@ void alloc_kv(eeb_ctx* c, Model& m, int page, int n_pages, bool paged) {
     m.v_maps.clear();
     m.k_maps8.clear();
     m.v_maps8.clear();
-    if (d.dtype == EEB_BF16 && (m.head_dim == 64 || m.head_dim == 128) && gemm_tc_available()) {
+    // (head_dim 80: rows of 160 B; the maps' second 64-dim box reads dims
+    //  80..127 as out-of-bounds zeros — the prefill attention's padded tiles)
+    if (d.dtype == EEB_BF16 && (m.head_dim == 64 || m.head_dim == 80 || m.head_dim == 128) && gemm_tc_available()) {
         m.k_maps.resize((size_t)d.num_layers * m.shards);
         m.v_maps.resize((size_t)d.num_layers * m.shards);
         m.k_maps8.resize((size_t)d.num_layers * m.shards);
@@ -2587,8 +2590,9 @@ eeb_status eeb_kv_configure_pages(eeb_ctx* c, int model, int32_t page_size, int3
         if (n_pages <= 0) throw Error(EEB_E_VALIDATION, "n_pages must be positive");
         if ((d.max_seq_len + page_size - 1) / page_size > 64)
             throw Error(EEB_E_VALIDATION, "at most 64 pages per sequence (max_seq_len / page_size)");
-        if (d.dtype != EEB_BF16 || (m.head_dim != 64 && m.head_dim != 128) || !gemm_tc_available())
-            throw Error(EEB_E_DOMAIN, "the paged KV pool needs a bf16 model with head_dim 64 or 128");
+        if (d.dtype != EEB_BF16 || (m.head_dim != 64 && m.head_dim != 80 && m.head_dim != 128) ||
+            !gemm_tc_available())
+            throw Error(EEB_E_DOMAIN, "the paged KV pool needs a bf16 model with head_dim 64, 80 or 128");
         EEB_CUDA(cudaSetDevice(c->device));
         EEB_CUDA(cudaStreamSynchronize(c->stream));
         drop_graphs(c, model);  // captured steps hold the old KV maps and the unpaged kernel

@@ -42,7 +42,8 @@ bool launch_embed_norm(int dtype, const void* emb, const int* tok, const int* sl
 // pf / pf_bytes: the next GEMM's weights, prefetched into L2 by the CTAs (optional).
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
-                          void* out2, cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0);
+                          void* out2, cudaStream_t s, const void* pf = nullptr, size_t pf_bytes = 0,
+                          int min_vec = 1);
 // ---- tensor-parallel exchange over peer memory (rows.cu) ---------------------
 // Every rank of a TP group owns one exchange buffer ("px") with the same
 // layout; `base[p]` is rank p's buffer as mapped in this process (NVLink P2P
@@ -77,7 +78,7 @@ struct PxPeers {
 // out2 likewise — so all ranks hold bit-identical residual streams.
 void launch_tp_norm(int dtype, const PxPeers& px, int planes, int64_t plane_stride, const int* n_active, int max_rows,
                     float* x, int d, float eps, const float* g1, void* out1, const float* g2, void* out2,
-                    cudaStream_t s);
+                    cudaStream_t s, int min_vec = 1);
 // All-gather of the vocab-parallel exit-head partials: rank p's `region`
 // floats (its px head area) land at dst + p * region on every rank.
 void launch_px_gather(const PxPeers& px, int64_t region, float* dst, cudaStream_t s);

@@ -483,13 +483,23 @@ bool launch_embed_norm(int dtype, const void* emb, const int* tok, const int* sl
     return true;
 }
 
+// float4 groups per thread of the row kernels: the fewest that fit 512
+// threads, or min_vec (prefill chunks of up to 1024 rows: 4 -> 128-thread CTAs,
+// 16 resident per SM instead of 4, the whole chunk in one wave; the row sum's
+// order follows the choice, so decode and prefill each keep one)
+int norm_vec(int q, int min_vec) {
+    int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
+    while (kv < min_vec && kv < 4 && q / (2 * kv) >= 32) kv *= 2;
+    return kv;
+}
+
 void launch_residual_norm(int dtype, const float* part, int splits, int64_t split_stride, const int* n_active,
                           int max_rows, float* x, int d, float eps, const float* g1, void* out1, const float* g2,
-                          void* out2, cudaStream_t s, const void* pf, size_t pf_bytes) {
+                          void* out2, cudaStream_t s, const void* pf, size_t pf_bytes, int min_vec) {
     const int q = d / 4;  // float4 groups per row
     if (d % 4 != 0 || q > 4 * kNormThreads)
         throw Error(1, "residual_norm: d_model must be a multiple of 4 and at most 8192");
-    const int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
+    const int kv = norm_vec(q, min_vec);
     const dim3 grid(max_rows), block(std::max(32, std::min(kNormThreads, (q / kv + 31) / 32 * 32)));
     auto go = [&](auto kern, auto* o1, auto* o2) {
         launch_pdl(kern, grid, block, 0, s, part, splits, split_stride, n_active, x, d, eps, g1, o1, g2, o2, pf,
@@ -513,12 +523,12 @@ void launch_residual_norm(int dtype, const float* part, int splits, int64_t spli
 
 void launch_tp_norm(int dtype, const PxPeers& px, int planes, int64_t plane_stride, const int* n_active, int max_rows,
                     float* x, int d, float eps, const float* g1, void* out1, const float* g2, void* out2,
-                    cudaStream_t s) {
+                    cudaStream_t s, int min_vec) {
     const int q = d / 4;
     if (d % 4 != 0 || q > 4 * kNormThreads) throw Error(1, "tp_norm: d_model must be a multiple of 4 and at most 8192");
     if (max_rows > kPxMaxCtas || max_rows > px.lay.rows) throw Error(1, "tp_norm: more rows than the exchange buffer holds");
     if (px.nranks < 2 || px.nranks > kPxMaxRanks) throw Error(1, "tp_norm: bad rank count");
-    const int kv = q <= kNormThreads ? 1 : (q <= 2 * kNormThreads ? 2 : 4);
+    const int kv = norm_vec(q, min_vec);
     const dim3 grid(max_rows), block(std::max(32, std::min(kNormThreads, (q / kv + 31) / 32 * 32)));
     auto go = [&](auto kern, auto* o1, auto* o2) {
         launch_pdl(kern, grid, block, 0, s, px, planes, plane_stride, n_active, x, d, eps, g1, o1, g2, o2);

@@ -78,7 +78,13 @@ HD128 = eeb.ModelDesc("pf-gqa-hd128", 4, 1024, 8, 2, 1024, 1000, (2, 4), dtype=e
                       max_seq_len=160)
 
 
-@pytest.mark.parametrize("which", ["tiny", "gqa-hd128", "paged", "history"])
+# OPT-2.7B's head_dim 80 (C3): padded 128-wide attention tiles, the KV maps'
+# dims 80..127 read as TMA out-of-bounds zeros
+HD80 = eeb.ModelDesc("pf-mha-hd80", 4, 1280, 16, 16, 1024, 1000, (2, 4), dtype=eeb.BF16, max_slots=8,
+                     max_seq_len=160)
+
+
+@pytest.mark.parametrize("which", ["tiny", "gqa-hd128", "mha-hd80", "paged-hd80", "paged", "history"])
 def test_prefill_bf16_chunk_boundary(ctx, which):
     """bf16, > 256 prompt tokens: two chunks, one sequence split across them;
     the tensor-core prefill attention (64-row query blocks, causal within the
@@ -86,12 +92,14 @@ def test_prefill_bf16_chunk_boundary(ctx, which):
     that continue a sequence with decoded history (start position > 0)."""
     if which == "gqa-hd128":
         desc = HD128
+    elif which.endswith("hd80"):
+        desc = HD80.replace(name="pf-" + which)
     else:
         desc = eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, name="tiny-bf16-pf-" + which, max_slots=8,
                                            max_seq_len=192)
     m = ctx.register(desc)
     ctx.load_layers(m, desc.num_layers)
-    if which == "paged":
+    if which.startswith("paged"):
         ctx.kv_configure_pages(m, 64, 20)
         ctx.kv_reserve(m, 7, 64)  # page 0 taken: the sequences' pages differ from their slots
     ref = OracleModel(desc)
@@ -141,3 +149,32 @@ def test_prefill_validation(ctx):
     with pytest.raises(eeb.EebError) as e:
         ctx.prefill(m, 4, [0, 0], [[1], [2]])
     assert e.value.kind == "ValidationError"
+
+
+def test_prefill_bf16_long_context(ctx):
+    """A 1100-token prompt (max_seq_len 2048): the tensor-core prefill
+    attention past the 1024 positions whose KV depth it stages in shared
+    memory (the rest read from global), against the oracle."""
+    desc = eeb.PRESETS["tiny"].replace(dtype=eeb.BF16, name="tiny-bf16-long", max_slots=2, max_seq_len=2048)
+    m = ctx.register(desc)
+    ctx.load_layers(m, desc.num_layers)
+    ref = OracleModel(desc)
+    ref.load(desc.num_layers)
+    rng = np.random.default_rng(17)
+    slots = np.array([0, 1])
+    lens = [1100, 30]
+    start = np.zeros(2, np.int32)
+    prompts = [rng.integers(0, desc.vocab, n) for n in lens]
+    ctx.prefill(m, desc.num_layers, slots, prompts, start)
+    for k in range(max(lens)):  # the oracle decodes the prompts token by token
+        live = np.array([i for i in range(2) if k < lens[i]])
+        ref.decode_step(0, eeb.FULL_DEPTH, TH, slots[live], np.array([prompts[i][k] for i in live]), np.full(len(live), k))
+    agree = []
+    for step in range(3):
+        nxt = rng.integers(0, desc.vocab, 2)
+        pos = np.array(lens) + step
+        g = ctx.decode_step(m, 0, eeb.INTROSPECTIVE, TH, slots, nxt, pos)
+        r = ref.decode_step(0, eeb.INTROSPECTIVE, TH, slots, nxt, pos)
+        agree.extend(g["token_id"] == r["token_id"])
+    assert np.mean(agree) >= 0.99, np.mean(agree)
+
