@@ -91,6 +91,38 @@ __global__ void __launch_bounds__(kNormThreads)
     float* row = x + (int64_t)i * d;
     float4 v[kV];
     float ss = 0.f;
+    // wide rows with few planes (34B: 4 float4 groups x 4 planes per thread):
+    // every load of the thread in flight at once, then the same in-order sums
+    // (the general loop below issues one column group's loads at a time)
+    constexpr int kP = 24 / kV;
+    if (kV > 1 && part && splits <= kP) {
+        float4 xs[kV], t[kV][kP];
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const int c = 4 * (threadIdx.x + k * blockDim.x);
+            if (c < d) {
+                xs[k] = *reinterpret_cast<const float4*>(row + c);
+#pragma unroll
+                for (int j = 0; j < kP; ++j)
+                    if (j < splits) t[k][j] = __ldcg(reinterpret_cast<const float4*>(part + (int64_t)i * d + c + j * split_stride));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kV; ++k) {
+            const int c = 4 * (threadIdx.x + k * blockDim.x);
+            v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < d) {
+                float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < kP; ++j)
+                    if (j < splits) add4(y, t[k][j]);
+                add4(xs[k], y);
+                *reinterpret_cast<float4*>(row + c) = xs[k];
+                v[k] = xs[k];
+                ss += xs[k].x * xs[k].x + xs[k].y * xs[k].y + xs[k].z * xs[k].z + xs[k].w * xs[k].w;
+            }
+        }
+    } else
 #pragma unroll
     for (int k = 0; k < kV; ++k) {
         const int c = 4 * (threadIdx.x + k * blockDim.x);
