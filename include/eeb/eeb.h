@@ -192,7 +192,7 @@ eeb_status eeb_reset_slots(eeb_ctx* ctx, int model, int32_t n, const int32_t* sl
  * themselves, eeb_decode_step_device needs eeb_kv_reserve first (its positions
  * are device-side).  Out of pages -> EEB_E_CAPACITY (CapacityError).
  * eeb_kv_release returns a finished request's pages (continuous batching:
- * the slot is free for the next request).  bf16 models with head_dim 64/128. */
+ * the slot is free for the next request).  bf16 models with head_dim 64/80/128. */
 eeb_status eeb_kv_configure_pages(eeb_ctx* ctx, int model, int32_t page_size, int32_t n_pages);
 eeb_status eeb_kv_reserve(eeb_ctx* ctx, int model, int32_t slot, int32_t n_positions);
 eeb_status eeb_kv_release(eeb_ctx* ctx, int model, int32_t slot);
