@@ -467,7 +467,7 @@ def run_eeb(args, desc):
     rng = np.random.default_rng(1000 if tp > 1 else 1000 + rank)  # a TP group decodes the same rows
     slots = np.arange(B, dtype=np.int32)
 
-    # prefill (eeb_prefill, chunked <= 256-token passes over all layers): the
+    # prefill (eeb_prefill, 1024-row chunked passes over all layers): the
     # prompts' KV at every layer.  One untimed pass (graph capture), then a
     # timed one over the same prompts (TTFT of the batch: every request's first
     # token waits for it; host->device copy of the prompts included).
