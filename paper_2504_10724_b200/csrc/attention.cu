@@ -1061,7 +1061,7 @@ __device__ __forceinline__ void store4_kv(T* dst, float x, float y, float z, flo
 
 // Prefill: RoPE the keys and append K/V of every live row (one CTA per row;
 // a thread owns 4 dims of each half of a key head, or 4 dims of a value head).
-template <typename T>
+template <typename T, bool ONE>
 __global__ void kv_append_kernel(Stamp stamp, AttnArgs a) {
     StampScope stamp_scope(stamp);
     pdl_launch_dependents();
@@ -1082,10 +1082,17 @@ __global__ void kv_append_kernel(Stamp stamp, AttnArgs a) {
     const int q4 = half / 4;
     for (int idx = threadIdx.x; idx < Hkv * q4; idx += blockDim.x) {
         const int g = idx / q4, jj = 4 * (idx % q4);
-        const float4 x0 = plane_sum4(row + dq + g * hd + jj, a.splits, a.split_stride);
-        const float4 x1 = plane_sum4(row + dq + g * hd + jj + half, a.splits, a.split_stride);
-        const float4 v0 = plane_sum4(row + dq + dkv + g * hd + jj, a.splits, a.split_stride);
-        const float4 v1 = plane_sum4(row + dq + dkv + g * hd + jj + half, a.splits, a.split_stride);
+        // (one plane — the cuBLASLt prefill GEMMs — is a plain load: the
+        //  8-plane batches of plane_sum4 would hold 32 float4 registers)
+        const float* kr = row + dq + g * hd + jj;
+        const float* vr = row + dq + dkv + g * hd + jj;
+        constexpr bool one = ONE;
+        const float4 x0 = one ? __ldcg(reinterpret_cast<const float4*>(kr)) : plane_sum4(kr, a.splits, a.split_stride);
+        const float4 x1 = one ? __ldcg(reinterpret_cast<const float4*>(kr + half))
+                              : plane_sum4(kr + half, a.splits, a.split_stride);
+        const float4 v0 = one ? __ldcg(reinterpret_cast<const float4*>(vr)) : plane_sum4(vr, a.splits, a.split_stride);
+        const float4 v1 = one ? __ldcg(reinterpret_cast<const float4*>(vr + half))
+                              : plane_sum4(vr + half, a.splits, a.split_stride);
         const float4 c = *reinterpret_cast<const float4*>(cs + jj);
         const float4 sv = *reinterpret_cast<const float4*>(sn + jj);
         T* dst = kc + kv_elem_offset(a, slot, pos, g);
@@ -1423,10 +1430,13 @@ void launch_mma(const AttnArgs& a, cudaStream_t s) {
 }  // namespace
 
 void launch_kv_append(const AttnArgs& a, cudaStream_t s) {
+    // (one plane: the cuBLASLt prefill GEMMs' output; plain loads, few registers)
     if (a.dtype == 0)
-        launch_pdl(kv_append_kernel<float>, dim3(a.max_rows), dim3(256), 0, s, a);
+        launch_pdl(a.splits == 1 ? kv_append_kernel<float, true> : kv_append_kernel<float, false>, dim3(a.max_rows),
+                   dim3(256), 0, s, a);
     else
-        launch_pdl(kv_append_kernel<__nv_bfloat16>, dim3(a.max_rows), dim3(256), 0, s, a);
+        launch_pdl(a.splits == 1 ? kv_append_kernel<__nv_bfloat16, true> : kv_append_kernel<__nv_bfloat16, false>,
+                   dim3(a.max_rows), dim3(256), 0, s, a);
     EEB_CHECK_LAUNCH();
 }
 

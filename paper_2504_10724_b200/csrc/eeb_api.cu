@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -292,6 +293,7 @@ struct eeb_ctx {
     void* pin = nullptr;
     size_t pin_bytes = 0;
     std::map<eeb::GraphKey, cudaGraphExec_t> graphs;
+    std::set<eeb::GraphKey> pf_seen;  // prefill chunk layouts run once eagerly (captured on a repeat)
     // profiling
     int profiling = 0;
     std::vector<cudaEvent_t> ev_pool;
@@ -1660,6 +1662,13 @@ void run_prefill_chunk(eeb_ctx* c, int mi, int depth, int rows, bool full) {
     }
     GraphKey key{mi, depth, kPolicyPrefill, rows, c->gemm_tier, (uint32_t)c->pf_cur_items};
     auto it = c->graphs.find(key);
+    if (it == c->graphs.end() && c->pf_seen.insert(key).second) {
+        // first sighting of this chunk layout: eager (a serving engine's
+        // admissions produce many one-off query-block layouts; capturing and
+        // instantiating a whole-depth graph for each cost ~0.7 s of a C3 run)
+        enqueue_prefill(c, mi, depth, rows);
+        return;
+    }
     if (it == c->graphs.end()) {
         cudaGraph_t g;
         EEB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
